@@ -1,0 +1,176 @@
+/*
+ * include/pre3_gmask.h — the drop-in C ABI of the B200-native constrained
+ * decoding hot path (Pre^3, arxiv 2506.03887).
+ *
+ * It replaces the reference matcher's per-step runtime, `gmask::Engine`
+ * (/root/reference/proj/include/gmask/runtime.hpp:92-166,
+ * src/runtime.cpp:92-307), and its CPU "kernels" plugin table
+ * (include/gmask/kernels.hpp:31-54) with batched sm_100a CUDA.  Every entry
+ * point below names the reference interface it replaces.  Plain C types only:
+ * pointers are device pointers unless documented as host pointers; streams
+ * are `cudaStream_t` passed as `void*` (NULL = legacy default stream).
+ *
+ * Conventions:
+ *   - V regular tokens, token ids 0..V-1 in vocabulary order; EOS is id V
+ *     and mask bit V (runtime.hpp:62-85, TokenMask::SetEos).
+ *   - A mask row is W = ceil((V+1)/32) uint32 words; bit t = word t/32,
+ *     bit t%32 — the little-endian image of the reference's uint64 words.
+ *   - Calls that take a stream are asynchronous and enqueue kernels only;
+ *     there is no internal locking: one gm_batch per stream.
+ *   - Return value: GM_OK or a GM_ERR_* code; gm_last_error() returns a
+ *     thread-local message.  The codes mirror the reference's exception
+ *     kinds (GrammarError / BuildError / SerializeError / VocabError) and CLI
+ *     exit codes (tools/gmask_main.cpp:317-335).
+ */
+#ifndef PRE3_GMASK_H_
+#define PRE3_GMASK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GM_ABI_VERSION 1
+
+enum gm_status_code {
+  GM_OK = 0,
+  GM_ERR_GRAMMAR = 2,         /* GrammarError (grammar.hpp:34-49) */
+  GM_ERR_BUILD = 3,           /* BuildError (lr1.hpp:20-29) */
+  GM_ERR_CORRUPT_INPUT = 4,   /* SerializeError (serialize.hpp:17-25) */
+  GM_ERR_CUDA = 5,            /* CUDA runtime failure / no device */
+  GM_ERR_STACK_OVERFLOW = 6,  /* a device stack or walk overlay overflowed */
+  GM_ERR_VOCAB_EMPTY = 7,     /* VocabError::kEmptyToken (runtime.hpp:29-37) */
+  GM_ERR_VOCAB_DUPLICATE = 8, /* VocabError::kDuplicateToken */
+  GM_ERR_USAGE = 64           /* bad argument (CLI exit 64) */
+};
+
+/* Per-sequence status; 0..2 are runtime.hpp:19 `Status`, 3 is new. */
+enum gm_seq_status {
+  GM_ALIVE = 0,
+  GM_DEAD = 1,
+  GM_ACCEPTED = 2,
+  GM_OVERFLOW = 3 /* stack exceeded the batch's stack_capacity */
+};
+
+typedef struct gm_automaton gm_automaton; /* host: compiled DPDA (gmask::Dpda) */
+typedef struct gm_engine gm_engine;       /* device: automaton + vocab + context cache */
+typedef struct gm_batch gm_batch;         /* device: B sequences' (state, status, stack) */
+
+const char* gm_last_error(void);
+int gm_abi_version(void);
+
+/* ------------------------------------------------------------ automaton */
+/* Loads a compiled automaton in the flat P3DPDA v1 format —
+ * the device-oriented counterpart of DeserializeDpda
+ * (src/serialize.cpp:198-294): validates shapes, id ranges, per-state edge
+ * ranges and arbitration order.  `data` is a host buffer. */
+int gm_automaton_load(const void* data, size_t bytes, gm_automaton** out);
+/* Compiles grammar text (line-oriented BNF, grammar.hpp:1-10) into an
+ * automaton: ParseGrammar + BuildDpda (src/dpda_builder.cpp:478-522).
+ * aggregate/merge mirror BuildOptions (dpda.hpp:73-80). */
+int gm_automaton_compile(const char* grammar_text, int aggregate, int merge,
+                         gm_automaton** out);
+/* Serializes to P3DPDA v1 into a host buffer; returns the size via *size
+ * (call with buf=NULL to query). */
+int gm_automaton_save(const gm_automaton* a, void* buf, size_t cap, size_t* size);
+int gm_automaton_destroy(gm_automaton* a);
+/* info[0..7] = num_states, num_edges, initial_state, accept_state,
+ * max |match_pop|, max |push|, dynamic edges, grammar_hash. */
+int gm_automaton_info(const gm_automaton* a, int64_t info[8]);
+
+/* ------------------------------------------------------------ engine */
+typedef struct gm_engine_options {
+  int32_t context_depth;   /* K: stack entries keying the context cache (1..16; default 8) */
+  int32_t context_slots;   /* hash-table capacity, power of two (default 8192) */
+  int64_t cd_pool_entries; /* context-dependent token pool (default 1<<24) */
+  int32_t segment_words;   /* vocab segment size in mask words (default 256) */
+} gm_engine_options;
+
+/* Engine::Engine (runtime.cpp:92-113) + TokenTrie::Build (runtime.cpp:18-61)
+ * on `device`: uploads the flattened automaton, the vocabulary (host
+ * `tok_bytes`, `tok_offsets[num_tokens+1]`) and allocates the context cache.
+ * Empty / duplicate tokens fail with GM_ERR_VOCAB_* exactly where
+ * TokenTrie::Build throws.  opts may be NULL. */
+int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes,
+                     const int64_t* tok_offsets, int32_t num_tokens,
+                     const gm_engine_options* opts, int device, gm_engine** out);
+int gm_engine_destroy(gm_engine* e);
+/* info[0..7] = V, W, num_segments, context slots used, cd pool used,
+ * context builds, direct (uncached) segment fills, device */
+int gm_engine_info(gm_engine* e, int64_t info[8]);
+/* Host bitmask (W words) of "structural" tokens used by the synthetic
+ * stream sampler (tokens containing any of {}[],:" ). */
+int gm_engine_set_structural(gm_engine* e, const uint32_t* host_words);
+
+/* ------------------------------------------------------------ batch */
+/* B sequences with fixed-capacity device stacks (reference stacks are
+ * unbounded vectors; exceeding capacity yields GM_OVERFLOW). */
+int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batch** out);
+int gm_batch_destroy(gm_batch* b);
+/* Engine::InitialConfig (runtime.cpp:115-121) for every sequence. */
+int gm_batch_reset(gm_batch* b, void* stream);
+/* Host-side parity helpers (synchronous). */
+int gm_batch_download(gm_batch* b, int32_t seq, int32_t* state, int32_t* status,
+                      int32_t* stack, int32_t cap, int32_t* depth);
+int gm_batch_upload(gm_batch* b, int32_t seq, int32_t status, const int32_t* stack,
+                    int32_t depth);
+/* Synchronizes `stream` and reports device-side errors (GM_ERR_STACK_OVERFLOW
+ * if a mask walk overflowed its overlay); clears them. */
+int gm_batch_check(gm_batch* b, void* stream);
+/* counters[0..3] = restarts, total draws, mask fills, accepts */
+int gm_batch_counters(gm_batch* b, int64_t counters[4]);
+
+/* ------------------------------------------------------------ hot path */
+/* Engine::ComputeMask (runtime.cpp:280-287) for every sequence:
+ * bitmask[b * ld_words + w], ld_words >= W.  Non-alive sequences get an
+ * all-zero row (runtime.cpp:282). */
+int gm_fill_next_token_bitmask(gm_batch* b, uint32_t* bitmask, int64_t ld_words, void* stream);
+
+/* The same fill fused with bf16 logit masking, in place: logits[b*ld + t] =
+ * -inf wherever mask bit t is 0, for t in [0, V]; other entries untouched.
+ * bitmask may be NULL.  seg_counts (may be NULL) receives per (sequence,
+ * segment) {allowed regular tokens, allowed structural tokens} for the
+ * stream sampler. */
+int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
+                            int64_t ld, int32_t* seg_counts, void* stream);
+
+/* Engine::Step over every byte of tokens[b] (runtime.cpp:177-186; callers'
+ * loop gmask_main.cpp:113-118); tokens[b] == V steps kEndMarker; tokens[b] < 0
+ * is a no-op.  status_out (may be NULL) receives gm_seq_status per sequence.
+ * restart != 0 re-initializes sequences that end non-alive (decode loops). */
+int gm_accept_tokens(gm_batch* b, const int32_t* tokens, int32_t* status_out, int32_t restart,
+                     void* stream);
+
+/* Synthetic-stream sampler fused with accept: picks each
+ * sequence's token from the bitmask + seg_counts of the preceding
+ * gm_fill_and_mask_logits, writes it to tokens_out (may be NULL), accepts it
+ * and restarts finished sequences.  `seed` keys the per-sequence streams. */
+int gm_sample_stream_and_accept(gm_batch* b, const uint32_t* bitmask, int64_t ld_words,
+                                const int32_t* seg_counts, uint64_t seed, int32_t* tokens_out,
+                                void* stream);
+
+/* The same sampler without the accept: tokens_out receives each sequence's
+ * pick (-1 when nothing is allowed) and the stream advances; the caller
+ * accepts them later with gm_accept_tokens (e.g. after a host round trip). */
+int gm_sample_stream(gm_batch* b, const uint32_t* bitmask, int64_t ld_words, const int32_t* seg_counts,
+                     uint64_t seed, int32_t* tokens_out, void* stream);
+
+/* Greedy decode step (config 5): fill + argmax over allowed bf16 logits (the
+ * row is read, not written; ties -> lowest id) + accept + restart.
+ * tokens_out receives the chosen ids (-1 when nothing is allowed). */
+int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, uint32_t* bitmask,
+                          int64_t ld_words, int32_t* tokens_out, void* stream);
+
+/* Launch statistics of the last fill (for roofline accounting):
+ * stats[0] = logits bytes read, [1] = logits bytes written (16-B chunk
+ * granularity), [2] = context hits, [3] = builds, [4] = direct fills,
+ * [5] = cd tokens resolved.  Requires gm_batch_check first. */
+int gm_batch_fill_stats(gm_batch* b, int64_t stats[6]);
+int gm_batch_set_stats(gm_batch* b, int32_t enable);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRE3_GMASK_H_ */

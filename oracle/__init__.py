@@ -1,0 +1,401 @@
+"""oracle — TEST INFRASTRUCTURE ONLY.
+
+ctypes bindings to the two CPU checkers built by oracle/Makefile:
+
+* ``Ref``  — oracle/_ref/libgmask_ref.so: the UNMODIFIED reference matcher
+  (gmask, /root/reference/proj) compiled from its own sources plus this repo's
+  extern "C" shim (oracle/ref_shim.cpp).
+* ``Port`` — oracle/_ref/libgmask_port.so: the plain-C restatement of the
+  reference runtime (oracle/gmask_port.c), pinned against ``Ref`` and the
+  golden vectors in tests/golden/.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this package, and only as the checker or the CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "libgmask_ref.so")
+PORT_SO = os.path.join(HERE, "_ref", "libgmask_port.so")
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+U64 = ctypes.c_uint64
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def pack(tokens: Sequence[bytes]) -> Tuple[np.ndarray, np.ndarray]:
+    offs = np.zeros(len(tokens) + 1, np.int64)
+    if tokens:
+        np.cumsum([len(t) for t in tokens], out=offs[1:])
+    data = np.frombuffer(b"".join(tokens) or b"\0", np.uint8).copy()
+    return data, offs
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def port_available() -> bool:
+    return os.path.exists(PORT_SO)
+
+
+class Ref:
+    """The reference gmask::Engine behind oracle/ref_shim.cpp."""
+
+    _lib = None
+
+    @classmethod
+    def lib(cls):
+        if cls._lib is None:
+            L = ctypes.CDLL(REF_SO)
+            sigs = {
+                "ref_compile": ([ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P), ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
+                "ref_dpda_free": ([P], None),
+                "ref_dpda_flat": ([P, P, I64], I64),
+                "ref_dpda_stats": ([P, P], None),
+                "ref_engine_from_dpda": ([P], P),
+                "ref_engine_from_flat": ([P, I64, ctypes.c_char_p, ctypes.c_int], P),
+                "ref_engine_free": ([P], None),
+                "ref_trie_new": ([P, P, I32, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, ctypes.c_int], P),
+                "ref_trie_free": ([P], None),
+                "ref_trie_nodes": ([P], I32),
+                "ref_cfg_new": ([P], P),
+                "ref_cfg_clone": ([P], P),
+                "ref_cfg_free": ([P], None),
+                "ref_cfg_get": ([P, P, P, P, I32], I32),
+                "ref_cfg_set": ([P, I32, P, I32], None),
+                "ref_step": ([P, P, I32], ctypes.c_int),
+                "ref_allowed": ([P, P, P, P], None),
+                "ref_mask": ([P, P, P, P], None),
+                "ref_mask_naive": ([P, P, P, P, I32, P], None),
+                "ref_decode_run": ([P, P, P, I32, I32, I32, U64, I32, I32, I32, P, P, P], ctypes.c_int),
+                "ref_sample_sentence": ([ctypes.c_char_p, U64, I32, ctypes.c_char_p, I32], I32),
+            }
+            for n, (a, r) in sigs.items():
+                f = getattr(L, n)
+                f.argtypes = a
+                f.restype = r
+            cls._lib = L
+        return cls._lib
+
+    # ---- automaton
+    @classmethod
+    def compile_flat(cls, grammar_text: str, aggregate: bool = True, merge: bool = True) -> Tuple[int, bytes, dict]:
+        """BuildDpda (dpda_builder.cpp:478-522) → (rc, P3DPDA bytes, stats)."""
+        L = cls.lib()
+        d = P()
+        err = ctypes.create_string_buffer(4096)
+        rc = L.ref_compile(grammar_text.encode(), int(aggregate), int(merge), ctypes.byref(d), err, 4096)
+        if rc != 0:
+            return rc, err.value, {}
+        n = L.ref_dpda_flat(d, None, 0)
+        buf = np.zeros(n, np.uint8)
+        L.ref_dpda_flat(d, _ptr(buf), n)
+        st = np.zeros(8, np.int64)
+        L.ref_dpda_stats(d, _ptr(st))
+        L.ref_dpda_free(d)
+        keys = ["states", "edges", "composites", "cycles", "dynamic", "max_match_pop", "max_push",
+                "edges_before_aggregation"]
+        return 0, buf.tobytes(), dict(zip(keys, (int(x) for x in st)))
+
+    @classmethod
+    def sample_sentence(cls, grammar_text: str, seed: int, soft_limit: int = 24) -> bytes:
+        L = cls.lib()
+        buf = ctypes.create_string_buffer(1 << 16)
+        n = L.ref_sample_sentence(grammar_text.encode(), seed, soft_limit, buf, 1 << 16)
+        if n < 0:
+            raise ValueError("sample failed")
+        return buf.raw[:n]
+
+    def __init__(self, flat: bytes, tokens: Optional[Sequence[bytes]] = None):
+        L = self.lib()
+        self._buf = np.frombuffer(flat, np.uint8).copy()
+        err = ctypes.create_string_buffer(1024)
+        self.h = L.ref_engine_from_flat(_ptr(self._buf), len(flat), err, 1024)
+        if not self.h:
+            raise ValueError(err.value.decode())
+        self.trie = None
+        self.tokens = None
+        if tokens is not None:
+            self.set_vocab(tokens)
+
+    def set_vocab(self, tokens: Sequence[bytes]):
+        L = self.lib()
+        self.tokens = list(tokens)
+        self._data, self._offs = pack(self.tokens)
+        kind = ctypes.c_int()
+        err = ctypes.create_string_buffer(1024)
+        t = L.ref_trie_new(_ptr(self._data), _ptr(self._offs), len(self.tokens), ctypes.byref(kind), err, 1024)
+        if not t:
+            raise ValueError((kind.value, err.value.decode()))
+        if self.trie:
+            L.ref_trie_free(self.trie)
+        self.trie = t
+
+    @property
+    def V(self) -> int:
+        return len(self.tokens)
+
+    @property
+    def W(self) -> int:
+        return (self.V + 1 + 31) // 32
+
+    def initial(self) -> int:
+        return self.lib().ref_cfg_new(self.h)
+
+    def free_cfg(self, c):
+        self.lib().ref_cfg_free(c)
+
+    def clone(self, c):
+        return self.lib().ref_cfg_clone(c)
+
+    def get(self, c) -> Tuple[int, int, List[int]]:
+        L = self.lib()
+        st, status = I32(), I32()
+        n = L.ref_cfg_get(c, ctypes.byref(st), ctypes.byref(status), None, 0)
+        buf = np.zeros(max(n, 1), np.int32)
+        L.ref_cfg_get(c, ctypes.byref(st), ctypes.byref(status), _ptr(buf), n)
+        return st.value, status.value, buf[:n].tolist()
+
+    def set(self, c, status: int, stack: Sequence[int]):
+        st = np.asarray(stack, np.int32)
+        self.lib().ref_cfg_set(c, status, _ptr(st), len(st))
+
+    def step(self, c, terminal: int) -> bool:
+        return bool(self.lib().ref_step(self.h, c, terminal))
+
+    def accept_token(self, c, token: int) -> bool:
+        """Step over token bytes (EOS = id V)."""
+        if token == self.V:
+            return self.step(c, 256)
+        for b in self.tokens[token]:
+            if not self.step(c, b):
+                return False
+        return True
+
+    def allowed(self, c) -> Tuple[int, bool]:
+        w = np.zeros(4, np.uint64)
+        d = I32()
+        self.lib().ref_allowed(self.h, c, _ptr(w), ctypes.byref(d))
+        return int(w[0]) | int(w[1]) << 64 | int(w[2]) << 128 | int(w[3]) << 192, bool(d.value)
+
+    def mask(self, c) -> np.ndarray:
+        out = np.zeros(self.W, np.uint32)
+        self.lib().ref_mask(self.h, c, self.trie, _ptr(out))
+        return out
+
+    def mask_naive(self, c) -> np.ndarray:
+        out = np.zeros(self.W, np.uint32)
+        self.lib().ref_mask_naive(self.h, c, _ptr(self._data), _ptr(self._offs), len(self.tokens), _ptr(out))
+        return out
+
+    def decode_run(self, structural: np.ndarray, batch: int, steps: int, seed: int, threads: int,
+                   stack_cap: int = 1024, logits_row: bool = True, want_tokens: bool = False,
+                   want_stacks: bool = False, warmup: int = 0):
+        """stats[0] = seconds of the `steps` timed steps (after `warmup`)."""
+        stats = np.zeros(8, np.float64)
+        toks = np.zeros((batch, warmup + steps), np.int32) if want_tokens else None
+        stk = np.zeros((batch, stack_cap + 2), np.int32) if want_stacks else None
+        self.lib().ref_decode_run(self.h, self.trie, _ptr(structural), batch, warmup, steps, seed, threads, stack_cap,
+                                  int(logits_row), _ptr(stats), _ptr(toks) if toks is not None else None,
+                                  _ptr(stk) if stk is not None else None)
+        return stats, toks, stk
+
+    def __del__(self):
+        L = self._lib
+        if L is not None:
+            if getattr(self, "trie", None):
+                L.ref_trie_free(self.trie)
+            if getattr(self, "h", None):
+                L.ref_engine_free(self.h)
+
+
+class _Cfg(ctypes.Structure):
+    _fields_ = [("state", I32), ("status", I32), ("depth", I32), ("cap", I32),
+                ("stack", ctypes.POINTER(I32))]
+
+
+class Port:
+    """The C restatement (oracle/gmask_port.c) over a P3DPDA automaton."""
+
+    _lib = None
+
+    @classmethod
+    def lib(cls):
+        if cls._lib is None:
+            L = ctypes.CDLL(PORT_SO)
+            CP = ctypes.POINTER(_Cfg)
+            sigs = {
+                "gp_automaton_load": ([P, I64], P),
+                "gp_automaton_free": ([P], None),
+                "gp_trie_build": ([P, P, I32, ctypes.POINTER(ctypes.c_int)], P),
+                "gp_trie_free": ([P], None),
+                "gp_trie_nodes": ([P], I32),
+                "gp_config_init": ([P, CP], None),
+                "gp_config_copy": ([CP, CP], None),
+                "gp_config_free": ([CP], None),
+                "gp_step": ([P, CP, I32], ctypes.c_int),
+                "gp_allowed": ([P, CP, P, ctypes.POINTER(ctypes.c_int)], None),
+                "gp_mask": ([P, CP, P, P], None),
+                "gp_mask_naive": ([P, CP, P, P, I32, P], None),
+                "gp_stream_draw": ([U64, U64, U64], U64),
+                "gp_stream_pick": ([P, P, I32, U64], I32),
+                "gp_greedy_pick": ([P, P, I32], I32),
+                "gp_decode_run": ([P, P, P, P, P, I32, I32, U64, I32, P, P, P], ctypes.c_int),
+            }
+            for n, (a, r) in sigs.items():
+                f = getattr(L, n)
+                f.argtypes = a
+                f.restype = r
+            cls._lib = L
+        return cls._lib
+
+    def __init__(self, flat: bytes, tokens: Sequence[bytes]):
+        L = self.lib()
+        self._buf = np.frombuffer(flat, np.uint8).copy()
+        self.a = L.gp_automaton_load(_ptr(self._buf), len(flat))
+        if not self.a:
+            raise ValueError("bad automaton")
+        self.tokens = list(tokens)
+        self._data, self._offs = pack(self.tokens)
+        kind = ctypes.c_int()
+        self.trie = L.gp_trie_build(_ptr(self._data), _ptr(self._offs), len(self.tokens), ctypes.byref(kind))
+        if not self.trie:
+            raise ValueError(("vocab", kind.value))
+
+    @property
+    def V(self) -> int:
+        return len(self.tokens)
+
+    @property
+    def W(self) -> int:
+        return (self.V + 1 + 31) // 32
+
+    def initial(self) -> _Cfg:
+        c = _Cfg()
+        self.lib().gp_config_init(self.a, ctypes.byref(c))
+        return c
+
+    def config(self, status: int, stack: Sequence[int]) -> _Cfg:
+        c = self.initial()
+        src = _Cfg()
+        arr = (I32 * len(stack))(*stack)
+        src.state = stack[-1]
+        src.status = status
+        src.depth = len(stack)
+        src.cap = len(stack)
+        src.stack = ctypes.cast(arr, ctypes.POINTER(I32))
+        self.lib().gp_config_copy(ctypes.byref(c), ctypes.byref(src))
+        return c
+
+    @staticmethod
+    def get(c: _Cfg) -> Tuple[int, int, List[int]]:
+        return c.state, c.status, [c.stack[i] for i in range(c.depth)]
+
+    def free(self, c: _Cfg):
+        self.lib().gp_config_free(ctypes.byref(c))
+
+    def step(self, c: _Cfg, terminal: int) -> bool:
+        return bool(self.lib().gp_step(self.a, ctypes.byref(c), terminal))
+
+    def accept_token(self, c: _Cfg, token: int) -> bool:
+        if token == self.V:
+            return self.step(c, 256)
+        for b in self.tokens[token]:
+            if not self.step(c, b):
+                return False
+        return True
+
+    def allowed(self, c: _Cfg) -> Tuple[int, bool]:
+        w = np.zeros(4, np.uint64)
+        d = ctypes.c_int()
+        self.lib().gp_allowed(self.a, ctypes.byref(c), _ptr(w), ctypes.byref(d))
+        return int(w[0]) | int(w[1]) << 64 | int(w[2]) << 128 | int(w[3]) << 192, bool(d.value)
+
+    def mask(self, c: _Cfg) -> np.ndarray:
+        out = np.zeros(self.W, np.uint32)
+        self.lib().gp_mask(self.a, ctypes.byref(c), self.trie, _ptr(out))
+        return out
+
+    def mask_naive(self, c: _Cfg) -> np.ndarray:
+        out = np.zeros(self.W, np.uint32)
+        self.lib().gp_mask_naive(self.a, ctypes.byref(c), _ptr(self._data), _ptr(self._offs), len(self.tokens),
+                                 _ptr(out))
+        return out
+
+    def stream_pick(self, mask: np.ndarray, structural: np.ndarray, u: int) -> int:
+        return self.lib().gp_stream_pick(_ptr(mask), _ptr(structural), self.V, u)
+
+    @classmethod
+    def stream_draw(cls, seed: int, seq: int, draw: int) -> int:
+        return cls.lib().gp_stream_draw(seed, seq, draw)
+
+    def greedy_pick(self, mask: np.ndarray, logits_bf16: np.ndarray) -> int:
+        return self.lib().gp_greedy_pick(_ptr(mask), _ptr(logits_bf16), self.V)
+
+    def decode_run(self, structural: np.ndarray, batch: int, steps: int, seed: int, stack_cap: int = 1024,
+                   want_tokens: bool = False, want_stacks: bool = False):
+        stats = np.zeros(8, np.float64)
+        toks = np.zeros((batch, steps), np.int32) if want_tokens else None
+        stk = np.zeros((batch, stack_cap + 2), np.int32) if want_stacks else None
+        self.lib().gp_decode_run(self.a, self.trie, _ptr(self._data), _ptr(self._offs), _ptr(structural), batch,
+                                 steps, seed, stack_cap, _ptr(stats), _ptr(toks) if toks is not None else None,
+                                 _ptr(stk) if stk is not None else None)
+        return stats, toks, stk
+
+    def __del__(self):
+        L = self._lib
+        if L is not None:
+            if getattr(self, "trie", None):
+                L.gp_trie_free(self.trie)
+            if getattr(self, "a", None):
+                L.gp_automaton_free(self.a)
+
+
+def build(ref: bool = True) -> None:
+    """make -C oracle (port always; ref when /root/reference is present)."""
+    import subprocess
+    subprocess.run(["make", "-s", "-C", HERE, "port"], check=True)
+    if ref and os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-j8", "-C", HERE, "ref"], check=True)
+
+
+def read_flat(flat: bytes) -> dict:
+    """Parses P3DPDA v1 into plain Python structures."""
+    import struct
+    assert flat[:8] == b"P3DPDA01"
+    o = 8
+    S, init, acc, ghash, tl = struct.unpack_from("<iiiQi", flat, o)
+    o += 24
+    text = flat[o:o + tl].decode("latin-1")
+    o += tl
+    shift = np.frombuffer(flat, np.int32, S * 256, o).copy()
+    o += S * 256 * 4
+    (E,) = struct.unpack_from("<i", flat, o)
+    o += 4
+    begin = np.frombuffer(flat, np.int32, S + 1, o).copy()
+    o += (S + 1) * 4
+    edges = []
+    for _ in range(E):
+        src, w0, w1, w2, w3, dollar, origin, dyn, _pad, target, cl, pl = struct.unpack_from("<iQQQQBBBBiii", flat, o)
+        o += 4 + 32 + 4 + 12
+        cond = list(struct.unpack_from(f"<{cl}i", flat, o))
+        o += 4 * cl
+        push = list(struct.unpack_from(f"<{pl}i", flat, o))
+        o += 4 * pl
+        edges.append({"source": src, "accepted": w0 | w1 << 64 | w2 << 128 | w3 << 192, "dollar": bool(dollar),
+                      "origin": origin, "dynamic": bool(dyn), "target": target, "match_pop": cond, "push": push})
+    assert o == len(flat)
+    return {"num_states": S, "initial": init, "accept": acc, "grammar_hash": ghash, "grammar_text": text,
+            "shift": shift, "edge_begin": begin, "edges": edges}

@@ -1,0 +1,387 @@
+"""B200-native Pre^3 constrained-decoding hot path (arxiv 2506.03887).
+
+Python host mirror of the reference matcher's runtime API
+(`gmask::Engine`, /root/reference/proj/include/gmask/runtime.hpp:92-166) over
+the C ABI in include/pre3_gmask.h, implemented by the in-tree CUDA library
+``libpre3gmask.so`` (sm_100a).  There is no CPU fallback: if the library is
+missing, importing the binding raises.
+
+The batched device API (`DeviceEngine`, `Batch`) is the product; the
+single-sequence `Engine`-named helpers (`InitialConfig`, `Step`,
+`ComputeMask`) exist so parity tests read like the reference's own
+(tests/test_runtime.cpp) — each call runs the CUDA kernels on a batch of one.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpre3gmask.so")
+
+GM_OK = 0
+GM_ERR_GRAMMAR = 2
+GM_ERR_BUILD = 3
+GM_ERR_CORRUPT_INPUT = 4
+GM_ERR_CUDA = 5
+GM_ERR_STACK_OVERFLOW = 6
+GM_ERR_VOCAB_EMPTY = 7
+GM_ERR_VOCAB_DUPLICATE = 8
+GM_ERR_USAGE = 64
+
+ALIVE, DEAD, ACCEPTED, OVERFLOW = 0, 1, 2, 3
+END_MARKER = 256  # grammar.hpp:28 kEndMarker
+
+
+class GmError(RuntimeError):
+    """Maps a gm_status_code to the reference's exception kinds."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class GrammarError(GmError):
+    pass
+
+
+class BuildError(GmError):
+    pass
+
+
+class SerializeError(GmError):
+    pass
+
+
+class VocabError(GmError):
+    """runtime.hpp:29-37; .kind is 'empty' or 'duplicate'."""
+
+    @property
+    def kind(self) -> str:
+        return "empty" if self.code == GM_ERR_VOCAB_EMPTY else "duplicate"
+
+
+class CudaError(GmError):
+    pass
+
+
+class StackOverflowError(GmError):
+    pass
+
+
+_ERRORS = {
+    GM_ERR_GRAMMAR: GrammarError,
+    GM_ERR_BUILD: BuildError,
+    GM_ERR_CORRUPT_INPUT: SerializeError,
+    GM_ERR_CUDA: CudaError,
+    GM_ERR_STACK_OVERFLOW: StackOverflowError,
+    GM_ERR_VOCAB_EMPTY: VocabError,
+    GM_ERR_VOCAB_DUPLICATE: VocabError,
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libpre3gmask.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing; run __graft_entry__.build() "
+                "(the CUDA path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, U64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t
+        PP = ctypes.POINTER(ctypes.c_void_p)
+        sigs = {
+            "gm_last_error": ([], ctypes.c_char_p),
+            "gm_abi_version": ([], ctypes.c_int),
+            "gm_automaton_load": ([P, SZ, PP], ctypes.c_int),
+            "gm_automaton_compile": ([ctypes.c_char_p, ctypes.c_int, ctypes.c_int, PP], ctypes.c_int),
+            "gm_automaton_save": ([P, P, SZ, ctypes.POINTER(SZ)], ctypes.c_int),
+            "gm_automaton_destroy": ([P], ctypes.c_int),
+            "gm_automaton_info": ([P, P], ctypes.c_int),
+            "gm_engine_create": ([P, P, P, I32, P, ctypes.c_int, PP], ctypes.c_int),
+            "gm_engine_destroy": ([P], ctypes.c_int),
+            "gm_engine_info": ([P, P], ctypes.c_int),
+            "gm_engine_set_structural": ([P, P], ctypes.c_int),
+            "gm_batch_create": ([P, I32, I32, PP], ctypes.c_int),
+            "gm_batch_destroy": ([P], ctypes.c_int),
+            "gm_batch_reset": ([P, P], ctypes.c_int),
+            "gm_batch_download": ([P, I32, P, P, P, I32, P], ctypes.c_int),
+            "gm_batch_upload": ([P, I32, I32, P, I32], ctypes.c_int),
+            "gm_batch_check": ([P, P], ctypes.c_int),
+            "gm_batch_counters": ([P, P], ctypes.c_int),
+            "gm_batch_fill_stats": ([P, P], ctypes.c_int),
+            "gm_batch_set_stats": ([P, I32], ctypes.c_int),
+            "gm_fill_next_token_bitmask": ([P, P, I64, P], ctypes.c_int),
+            "gm_fill_and_mask_logits": ([P, P, I64, P, I64, P, P], ctypes.c_int),
+            "gm_accept_tokens": ([P, P, P, I32, P], ctypes.c_int),
+            "gm_sample_stream_and_accept": ([P, P, I64, P, U64, P, P], ctypes.c_int),
+            "gm_sample_stream": ([P, P, I64, P, U64, P, P], ctypes.c_int),
+            "gm_decode_step_greedy": ([P, P, I64, P, I64, P, P], ctypes.c_int),
+            "gmw_synth_vocab": ([I32, I32, P, I64, P], I64),
+            "gmw_structural_words": ([P, P, I32, P], I32),
+        }
+        for name, (args, res) in sigs.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != GM_OK:
+        msg = lib().gm_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, GmError)(rc, msg)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# --------------------------------------------------------------------- vocab
+def synth_vocab(num_tokens: int, flavor: int = 0) -> List[bytes]:
+    """Synthetic sorted vocabulary (acceptance_main.cpp:341-359, extended)."""
+    L = lib()
+    n = L.gmw_synth_vocab(num_tokens, flavor, None, 0, None)
+    if n < 0:
+        raise ValueError("bad vocabulary size")
+    buf = np.zeros(max(n, 1), np.uint8)
+    offs = np.zeros(num_tokens + 1, np.int64)
+    L.gmw_synth_vocab(num_tokens, flavor, _ptr(buf), n, _ptr(offs))
+    raw = buf.tobytes()
+    return [raw[offs[i]:offs[i + 1]] for i in range(num_tokens)]
+
+
+def pack_vocab(tokens: Sequence[bytes]):
+    """(bytes uint8[], offsets int64[V+1]) host arrays."""
+    offs = np.zeros(len(tokens) + 1, np.int64)
+    np.cumsum([len(t) for t in tokens], out=offs[1:])
+    data = np.frombuffer(b"".join(tokens), np.uint8).copy() if tokens else np.zeros(1, np.uint8)
+    if data.size == 0:
+        data = np.zeros(1, np.uint8)
+    return data, offs
+
+
+def structural_words(tokens: Sequence[bytes]) -> np.ndarray:
+    data, offs = pack_vocab(tokens)
+    words = np.zeros((len(tokens) + 1 + 31) // 32, np.uint32)
+    lib().gmw_structural_words(_ptr(data), _ptr(offs), len(tokens), _ptr(words))
+    return words
+
+
+# --------------------------------------------------------------------- automaton
+class Automaton:
+    """A compiled DPDA (gmask::Dpda, dpda.hpp:97-124) held by the library."""
+
+    def __init__(self, handle: int):
+        self._h = ctypes.c_void_p(handle)
+
+    @classmethod
+    def load(cls, data: bytes) -> "Automaton":
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(data, len(data))
+        _check(lib().gm_automaton_load(buf, len(data), ctypes.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def load_file(cls, path: str) -> "Automaton":
+        with open(path, "rb") as f:
+            return cls.load(f.read())
+
+    @classmethod
+    def compile(cls, grammar_text: str, aggregate: bool = True, merge: bool = True) -> "Automaton":
+        h = ctypes.c_void_p()
+        _check(lib().gm_automaton_compile(grammar_text.encode(), int(aggregate), int(merge), ctypes.byref(h)))
+        return cls(h.value)
+
+    def save(self) -> bytes:
+        n = ctypes.c_size_t()
+        _check(lib().gm_automaton_save(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _check(lib().gm_automaton_save(self._h, buf, n.value, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def info(self) -> dict:
+        out = np.zeros(8, np.int64)
+        _check(lib().gm_automaton_info(self._h, _ptr(out)))
+        keys = ["num_states", "num_edges", "initial_state", "accept_state", "max_match_pop",
+                "max_push", "dynamic_edges", "grammar_hash"]
+        return dict(zip(keys, (int(x) for x in out)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.gm_automaton_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
+class _EngineOptions(ctypes.Structure):
+    _fields_ = [("context_depth", ctypes.c_int32), ("context_slots", ctypes.c_int32),
+                ("cd_pool_entries", ctypes.c_int64), ("segment_words", ctypes.c_int32)]
+
+
+@dataclass
+class RuntimeConfig:
+    """runtime.hpp:23-27 (state, status, stack bottom-first)."""
+    state: int
+    status: int
+    stack: List[int] = field(default_factory=list)
+
+
+class DeviceEngine:
+    """Engine::Engine + TokenTrie::Build on one CUDA device (runtime.cpp:18-113)."""
+
+    def __init__(self, automaton: Automaton, tokens: Sequence[bytes], device: int = 0,
+                 context_depth: int = 8, context_slots: int = 8192,
+                 cd_pool_entries: int = 1 << 24):
+        self.automaton = automaton
+        self.tokens = list(tokens)
+        self.V = len(self.tokens)
+        self.W = (self.V + 1 + 31) // 32
+        self.device = device
+        data, offs = pack_vocab(self.tokens)
+        opts = _EngineOptions(context_depth, context_slots, cd_pool_entries, 256)
+        h = ctypes.c_void_p()
+        _check(lib().gm_engine_create(automaton._h, _ptr(data), _ptr(offs), self.V, ctypes.byref(opts),
+                                      device, ctypes.byref(h)))
+        self._h = h
+        self.structural = structural_words(self.tokens)
+        _check(lib().gm_engine_set_structural(self._h, _ptr(self.structural)))
+        self._single: Optional[Batch] = None
+
+    def info(self) -> dict:
+        out = np.zeros(8, np.int64)
+        _check(lib().gm_engine_info(self._h, _ptr(out)))
+        keys = ["V", "W", "num_segments", "context_slots_used", "cd_pool_used", "context_builds",
+                "direct_fills", "device"]
+        return dict(zip(keys, (int(x) for x in out)))
+
+    def batch(self, size: int, stack_capacity: int = 1024) -> "Batch":
+        return Batch(self, size, stack_capacity)
+
+    # ---- reference-named single-sequence helpers (parity tests) ----
+    def _one(self) -> "Batch":
+        if self._single is None:
+            self._single = Batch(self, 1, 4096)
+        return self._single
+
+    def InitialConfig(self) -> RuntimeConfig:
+        s = self.automaton.info()["initial_state"]
+        return RuntimeConfig(s, ALIVE, [s])
+
+    def ComputeMask(self, cfg: RuntimeConfig) -> np.ndarray:
+        """Engine::ComputeMask (runtime.cpp:280-287) via the CUDA fill kernel."""
+        import torch
+        b = self._one()
+        b.set(0, cfg)
+        out = torch.zeros((1, self.W), dtype=torch.int32, device=f"cuda:{self.device}")
+        b.fill(out)
+        b.check()
+        return out.cpu().numpy().view(np.uint32)[0].copy()
+
+    def AcceptToken(self, cfg: RuntimeConfig, token: int) -> RuntimeConfig:
+        """Engine::Step over the token's bytes (EOS = id V) via the accept kernel."""
+        import torch
+        b = self._one()
+        b.set(0, cfg)
+        toks = torch.tensor([token], dtype=torch.int32, device=f"cuda:{self.device}")
+        b.accept(toks)
+        b.check()
+        return b.get(0)
+
+    def __del__(self):
+        self._single = None
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.gm_engine_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream
+
+
+class Batch:
+    """B in-flight sequences on the device (gm_batch)."""
+
+    def __init__(self, engine: DeviceEngine, size: int, stack_capacity: int = 1024):
+        self.engine = engine
+        self.B = size
+        self.cap = stack_capacity
+        h = ctypes.c_void_p()
+        _check(lib().gm_batch_create(engine._h, size, stack_capacity, ctypes.byref(h)))
+        self._h = h
+        self.nseg = engine.info()["num_segments"]
+
+    def reset(self, stream=None):
+        _check(lib().gm_batch_reset(self._h, _stream(stream)))
+
+    def set(self, i: int, cfg: RuntimeConfig):
+        st = np.asarray(cfg.stack, np.int32)
+        _check(lib().gm_batch_upload(self._h, i, int(cfg.status), _ptr(st), len(st)))
+
+    def get(self, i: int) -> RuntimeConfig:
+        buf = np.zeros(self.cap, np.int32)
+        state, status, depth = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().gm_batch_download(self._h, i, ctypes.byref(state), ctypes.byref(status), _ptr(buf),
+                                       self.cap, ctypes.byref(depth)))
+        return RuntimeConfig(state.value, status.value, buf[: depth.value].tolist())
+
+    def fill(self, bitmask, logits=None, seg_counts=None, stream=None):
+        """bitmask: int32 CUDA tensor [B, >=W] (or None); logits: bf16 [B, >=V+1]."""
+        bm = bitmask.data_ptr() if bitmask is not None else None
+        ldw = bitmask.stride(0) if bitmask is not None else 0
+        lg = logits.data_ptr() if logits is not None else None
+        ld = logits.stride(0) if logits is not None else 0
+        sc = seg_counts.data_ptr() if seg_counts is not None else None
+        _check(lib().gm_fill_and_mask_logits(self._h, bm, ldw, lg, ld, sc, _stream(stream)))
+
+    def accept(self, tokens, status_out=None, restart: bool = False, stream=None):
+        so = status_out.data_ptr() if status_out is not None else None
+        _check(lib().gm_accept_tokens(self._h, tokens.data_ptr(), so, int(restart), _stream(stream)))
+
+    def sample_stream_and_accept(self, bitmask, seg_counts, seed: int, tokens_out=None, stream=None):
+        to = tokens_out.data_ptr() if tokens_out is not None else None
+        _check(lib().gm_sample_stream_and_accept(self._h, bitmask.data_ptr(), bitmask.stride(0),
+                                                 seg_counts.data_ptr(), seed, to, _stream(stream)))
+
+    def sample_stream(self, bitmask, seg_counts, seed: int, tokens_out, stream=None):
+        _check(lib().gm_sample_stream(self._h, bitmask.data_ptr(), bitmask.stride(0), seg_counts.data_ptr(), seed,
+                                      tokens_out.data_ptr(), _stream(stream)))
+
+    def decode_step_greedy(self, logits, tokens_out=None, bitmask=None, stream=None):
+        to = tokens_out.data_ptr() if tokens_out is not None else None
+        bm = bitmask.data_ptr() if bitmask is not None else None
+        ldw = bitmask.stride(0) if bitmask is not None else 0
+        _check(lib().gm_decode_step_greedy(self._h, logits.data_ptr(), logits.stride(0), bm, ldw, to,
+                                           _stream(stream)))
+
+    def check(self, stream=None):
+        _check(lib().gm_batch_check(self._h, _stream(stream)))
+
+    def counters(self) -> dict:
+        out = np.zeros(4, np.int64)
+        _check(lib().gm_batch_counters(self._h, _ptr(out)))
+        return dict(zip(["restarts", "draws", "fills", "accepts"], (int(x) for x in out)))
+
+    def set_stats(self, enable: bool):
+        _check(lib().gm_batch_set_stats(self._h, int(enable)))
+
+    def fill_stats(self) -> dict:
+        out = np.zeros(6, np.int64)
+        _check(lib().gm_batch_fill_stats(self._h, _ptr(out)))
+        return dict(zip(["logit_bytes_read", "logit_bytes_written", "hits", "builds", "direct",
+                         "cd_resolved"], (int(x) for x in out)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.gm_batch_destroy(self._h)
+            self._h = ctypes.c_void_p()

@@ -1,0 +1,196 @@
+// automaton.cpp — P3DPDA v1 load/save, validation, and the device flattening.
+//
+// The flat format carries exactly the fields of gmask::Dpda the runtime
+// consumes (dpda.hpp:97-124): state counts, the byte shift table
+// (dpda.hpp:114-116), the single-terminal edges in arbitration order with
+// their CSR ranges (dpda_builder.cpp:450-467).  Composites (optimizer.cpp:
+// 78-136) are never consulted by Step/ComputeMask and are not stored.
+#include <algorithm>
+#include <cstring>
+
+#include "gm_internal.hpp"
+
+namespace pre3 {
+namespace {
+
+constexpr char kMagic[8] = {'P', '3', 'D', 'P', 'D', 'A', '0', '1'};
+
+struct Reader {
+  const uint8_t* p;
+  const uint8_t* end;
+  template <typename T>
+  T Get() {
+    if (static_cast<size_t>(end - p) < sizeof(T)) {
+      throw Error(GM_ERR_CORRUPT_INPUT, "P3DPDA: truncated input");
+    }
+    T v;
+    std::memcpy(&v, p, sizeof(T));
+    p += sizeof(T);
+    return v;
+  }
+};
+
+template <typename T>
+void Put(std::vector<uint8_t>* out, T v) {
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+  out->insert(out->end(), b, b + sizeof(T));
+}
+
+void Corrupt(const std::string& why) { throw Error(GM_ERR_CORRUPT_INPUT, "P3DPDA: " + why); }
+
+}  // namespace
+
+Automaton LoadFlat(const uint8_t* data, size_t n) {
+  if (n < 8 || std::memcmp(data, kMagic, 8) != 0) Corrupt("bad magic");
+  Reader r{data + 8, data + n};
+  Automaton a;
+  a.num_states = r.Get<int32_t>();
+  a.initial_state = r.Get<int32_t>();
+  a.accept_state = r.Get<int32_t>();
+  a.grammar_hash = r.Get<uint64_t>();
+  int32_t tl = r.Get<int32_t>();
+  if (a.num_states <= 0 || a.num_states > (1 << 24)) Corrupt("state count out of range");
+  if (tl < 0 || tl > r.end - r.p) Corrupt("grammar text length");
+  a.grammar_text.assign(reinterpret_cast<const char*>(r.p), static_cast<size_t>(tl));
+  r.p += tl;
+  size_t S = static_cast<size_t>(a.num_states);
+  if (static_cast<size_t>(r.end - r.p) < S * 256 * 4) Corrupt("truncated shift table");
+  a.shift_targets.resize(S * 256);
+  std::memcpy(a.shift_targets.data(), r.p, S * 256 * 4);
+  r.p += S * 256 * 4;
+  int32_t ne = r.Get<int32_t>();
+  if (ne < 0 || ne > (1 << 28)) Corrupt("edge count out of range");
+  a.edge_begin.resize(S + 1);
+  for (auto& b : a.edge_begin) b = r.Get<int32_t>();
+  a.edges.resize(static_cast<size_t>(ne));
+  for (Edge& e : a.edges) {
+    e.source = r.Get<int32_t>();
+    for (auto& w : e.accepted) w = r.Get<uint64_t>();
+    e.dollar = r.Get<uint8_t>() != 0;
+    e.origin = r.Get<uint8_t>();
+    e.dynamic = r.Get<uint8_t>() != 0;
+    (void)r.Get<uint8_t>();
+    e.target = r.Get<int32_t>();
+    int32_t cl = r.Get<int32_t>();
+    int32_t pl = r.Get<int32_t>();
+    if (cl < 1 || cl > 4096 || pl < 0 || pl > 4096) Corrupt("edge condition/push length");
+    e.match_pop.resize(static_cast<size_t>(cl));
+    e.push.resize(static_cast<size_t>(pl));
+    for (auto& s : e.match_pop) s = r.Get<int32_t>();
+    for (auto& s : e.push) s = r.Get<int32_t>();
+  }
+  if (r.p != r.end) Corrupt("trailing bytes");
+  a.Validate();
+  return a;
+}
+
+std::vector<uint8_t> SaveFlat(const Automaton& a) {
+  std::vector<uint8_t> out(kMagic, kMagic + 8);
+  Put<int32_t>(&out, a.num_states);
+  Put<int32_t>(&out, a.initial_state);
+  Put<int32_t>(&out, a.accept_state);
+  Put<uint64_t>(&out, a.grammar_hash);
+  Put<int32_t>(&out, static_cast<int32_t>(a.grammar_text.size()));
+  out.insert(out.end(), a.grammar_text.begin(), a.grammar_text.end());
+  for (int32_t t : a.shift_targets) Put<int32_t>(&out, t);
+  Put<int32_t>(&out, static_cast<int32_t>(a.edges.size()));
+  for (int32_t b : a.edge_begin) Put<int32_t>(&out, b);
+  for (const Edge& e : a.edges) {
+    Put<int32_t>(&out, e.source);
+    for (uint64_t w : e.accepted) Put<uint64_t>(&out, w);
+    Put<uint8_t>(&out, e.dollar ? 1 : 0);
+    Put<uint8_t>(&out, e.origin);
+    Put<uint8_t>(&out, e.dynamic ? 1 : 0);
+    Put<uint8_t>(&out, 0);
+    Put<int32_t>(&out, e.target);
+    Put<int32_t>(&out, static_cast<int32_t>(e.match_pop.size()));
+    Put<int32_t>(&out, static_cast<int32_t>(e.push.size()));
+    for (int32_t s : e.match_pop) Put<int32_t>(&out, s);
+    for (int32_t s : e.push) Put<int32_t>(&out, s);
+  }
+  return out;
+}
+
+// Structural checks in the spirit of DeserializeDpda's re-validation
+// (serialize.cpp:284-292) and ValidateDeterminism's well-formedness rules
+// (dpda_builder.cpp:409-448): ids in range, CSR ranges consistent, each
+// edge's condition starts at its source, dynamic edges resolvable.
+void Automaton::Validate() const {
+  const int32_t S = num_states;
+  auto in_range = [S](int32_t s) { return s >= 0 && s < S; };
+  if (!in_range(initial_state)) Corrupt("initial state out of range");
+  if (accept_state != -1 && !in_range(accept_state)) Corrupt("accept state out of range");
+  if (static_cast<int32_t>(shift_targets.size()) != S * 256) Corrupt("shift table size");
+  for (int32_t t : shift_targets) {
+    if (t != -1 && !in_range(t)) Corrupt("shift target out of range");
+  }
+  if (static_cast<int32_t>(edge_begin.size()) != S + 1 || edge_begin[0] != 0 ||
+      edge_begin[static_cast<size_t>(S)] != static_cast<int32_t>(edges.size())) {
+    Corrupt("edge ranges");
+  }
+  for (int32_t s = 0; s < S; ++s) {
+    if (edge_begin[static_cast<size_t>(s)] > edge_begin[static_cast<size_t>(s) + 1]) {
+      Corrupt("edge ranges not monotone");
+    }
+    for (int32_t i = edge_begin[static_cast<size_t>(s)]; i < edge_begin[static_cast<size_t>(s) + 1]; ++i) {
+      const Edge& e = edges[static_cast<size_t>(i)];
+      if (e.source != s) Corrupt("edge source does not match its range");
+      if (e.match_pop.empty() || e.match_pop[0] != s) Corrupt("condition must start at source");
+      for (int32_t x : e.match_pop) {
+        if (!in_range(x)) Corrupt("condition state out of range");
+      }
+      for (int32_t x : e.push) {
+        if (!in_range(x)) Corrupt("push state out of range");
+      }
+      if (!e.dynamic && e.push.empty()) Corrupt("static edge pushes nothing");
+      if (e.dynamic) {
+        if (e.dollar) Corrupt("dynamic edge accepts the end marker");
+        for (int b = 0; b < 256; ++b) {
+          if (!e.Accepts(b)) continue;
+          // The exposed top after the push prefix is either the last pushed
+          // state or (empty prefix) the entry under the popped suffix, which
+          // is unknown here; check the pushed case only.
+          if (!e.push.empty() &&
+              shift_targets[static_cast<size_t>(e.push.back()) * 256 + static_cast<size_t>(b)] < 0) {
+            Corrupt("dynamic edge without a shift target");
+          }
+        }
+      }
+    }
+  }
+}
+
+FlatLayout Flatten(const Automaton& a) {
+  FlatLayout f;
+  const int32_t S = a.num_states;
+  f.edges.reserve(a.edges.size());
+  for (const Edge& e : a.edges) {
+    DevEdge d;
+    d.cond_off = static_cast<int32_t>(f.cond_pool.size());
+    d.push_off = static_cast<int32_t>(f.push_pool.size());
+    d.cond_len = static_cast<int16_t>(e.match_pop.size());
+    d.push_len = static_cast<int16_t>(e.push.size());
+    d.flags = e.dynamic ? 1 : 0;
+    f.cond_pool.insert(f.cond_pool.end(), e.match_pop.begin(), e.match_pop.end());
+    f.push_pool.insert(f.push_pool.end(), e.push.begin(), e.push.end());
+    f.max_cond = std::max<int32_t>(f.max_cond, static_cast<int32_t>(e.match_pop.size()));
+    f.max_push = std::max<int32_t>(f.max_push, static_cast<int32_t>(e.push.size()) + (e.dynamic ? 1 : 0));
+    f.edges.push_back(d);
+  }
+  if (f.cond_pool.empty()) f.cond_pool.push_back(0);
+  if (f.push_pool.empty()) f.push_pool.push_back(0);
+  f.cand_begin.assign(static_cast<size_t>(S) * 257 + 1, 0);
+  for (int32_t s = 0; s < S; ++s) {
+    for (int32_t t = 0; t < 257; ++t) {
+      f.cand_begin[static_cast<size_t>(s) * 257 + static_cast<size_t>(t)] = static_cast<int32_t>(f.cand.size());
+      for (int32_t i = a.edge_begin[static_cast<size_t>(s)]; i < a.edge_begin[static_cast<size_t>(s) + 1]; ++i) {
+        if (a.edges[static_cast<size_t>(i)].Accepts(t)) f.cand.push_back(i);
+      }
+    }
+  }
+  f.cand_begin[static_cast<size_t>(S) * 257] = static_cast<int32_t>(f.cand.size());
+  if (f.cand.empty()) f.cand.push_back(0);
+  return f;
+}
+
+}  // namespace pre3

@@ -1,0 +1,499 @@
+// capi.cu — the C ABI of include/pre3_gmask.h: engine/batch lifetime, device
+// uploads, and launch wrappers.  Host-side only; kernels live in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_set>
+#include <string_view>
+#include <vector>
+
+#include "gm_internal.hpp"
+#include "kernels.cuh"
+#include "pre3_gmask.h"
+
+struct gm_automaton {
+  pre3::Automaton a;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int Fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+void Check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw pre3::Error(GM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <typename T>
+T* DevAlloc(size_t n, std::vector<void*>* owned) {
+  void* p = nullptr;
+  Check(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+  owned->push_back(p);
+  return static_cast<T*>(p);
+}
+
+template <typename T>
+T* DevUpload(const std::vector<T>& v, std::vector<void*>* owned) {
+  T* p = DevAlloc<T>(v.size(), owned);
+  if (!v.empty()) Check(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  return p;
+}
+
+template <typename F>
+int Guard(F&& f) {
+  try {
+    return f();
+  } catch (const pre3::Error& e) {
+    return Fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return Fail(GM_ERR_USAGE, "host allocation failed");
+  } catch (const std::exception& e) {
+    return Fail(GM_ERR_USAGE, e.what());
+  }
+}
+
+}  // namespace
+
+struct gm_engine {
+  int device = 0;
+  int32_t V = 0, W = 0, nseg = 0;
+  pre3::AutView aut{};
+  pre3::VocabView vocab{};
+  pre3::CacheView cache{};
+  uint32_t* structural = nullptr;
+  std::vector<void*> owned;
+  ~gm_engine() {
+    cudaSetDevice(device);
+    for (void* p : owned) cudaFree(p);
+  }
+};
+
+struct gm_batch {
+  gm_engine* engine = nullptr;
+  pre3::BatchView view{};
+  int32_t* seg_counts = nullptr;          // internal scratch for fused decode
+  unsigned long long* best = nullptr;     // greedy argmax packed keys
+  std::vector<void*> owned;
+  ~gm_batch() {
+    cudaSetDevice(engine->device);
+    for (void* p : owned) cudaFree(p);
+  }
+};
+
+extern "C" {
+
+const char* gm_last_error(void) { return g_last_error.c_str(); }
+int gm_abi_version(void) { return GM_ABI_VERSION; }
+
+// ---------------------------------------------------------------- automaton
+int gm_automaton_load(const void* data, size_t bytes, gm_automaton** out) {
+  return Guard([&]() -> int {
+    if (!data || !out) return Fail(GM_ERR_USAGE, "null argument");
+    auto* a = new gm_automaton{pre3::LoadFlat(static_cast<const uint8_t*>(data), bytes)};
+    *out = a;
+    return GM_OK;
+  });
+}
+
+int gm_automaton_compile(const char* text, int aggregate, int merge, gm_automaton** out) {
+  return Guard([&]() -> int {
+    if (!text || !out) return Fail(GM_ERR_USAGE, "null argument");
+    auto* a = new gm_automaton{pre3::CompileGrammar(text, aggregate != 0, merge != 0)};
+    *out = a;
+    return GM_OK;
+  });
+}
+
+int gm_automaton_save(const gm_automaton* a, void* buf, size_t cap, size_t* size) {
+  return Guard([&]() -> int {
+    if (!a || !size) return Fail(GM_ERR_USAGE, "null argument");
+    std::vector<uint8_t> v = pre3::SaveFlat(a->a);
+    *size = v.size();
+    if (buf) {
+      if (cap < v.size()) return Fail(GM_ERR_USAGE, "buffer too small");
+      std::memcpy(buf, v.data(), v.size());
+    }
+    return GM_OK;
+  });
+}
+
+int gm_automaton_destroy(gm_automaton* a) {
+  delete a;
+  return GM_OK;
+}
+
+int gm_automaton_info(const gm_automaton* a, int64_t info[8]) {
+  if (!a || !info) return Fail(GM_ERR_USAGE, "null argument");
+  int64_t maxpop = 0, maxpush = 0, dyn = 0;
+  for (const auto& e : a->a.edges) {
+    maxpop = std::max<int64_t>(maxpop, static_cast<int64_t>(e.match_pop.size()));
+    maxpush = std::max<int64_t>(maxpush, static_cast<int64_t>(e.push.size()));
+    dyn += e.dynamic;
+  }
+  info[0] = a->a.num_states;
+  info[1] = static_cast<int64_t>(a->a.edges.size());
+  info[2] = a->a.initial_state;
+  info[3] = a->a.accept_state;
+  info[4] = maxpop;
+  info[5] = maxpush;
+  info[6] = dyn;
+  info[7] = static_cast<int64_t>(a->a.grammar_hash);
+  return GM_OK;
+}
+
+// ---------------------------------------------------------------- engine
+int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int64_t* tok_offsets,
+                     int32_t num_tokens, const gm_engine_options* opts, int device,
+                     gm_engine** out) {
+  return Guard([&]() -> int {
+    if (!a || !out || num_tokens < 0 || (num_tokens > 0 && (!tok_bytes || !tok_offsets))) {
+      return Fail(GM_ERR_USAGE, "bad argument");
+    }
+    gm_engine_options o{8, 8192, int64_t{1} << 24, pre3::kSegWords};
+    if (opts) {
+      if (opts->context_depth) o.context_depth = opts->context_depth;
+      if (opts->context_slots) o.context_slots = opts->context_slots;
+      if (opts->cd_pool_entries) o.cd_pool_entries = opts->cd_pool_entries;
+      if (opts->segment_words) o.segment_words = opts->segment_words;
+    }
+    if (o.context_depth < 1 || o.context_depth > pre3::kMaxContext) return Fail(GM_ERR_USAGE, "context_depth must be 1..16");
+    if (o.context_slots < 1 || (o.context_slots & (o.context_slots - 1))) return Fail(GM_ERR_USAGE, "context_slots must be a power of two");
+    if (o.segment_words != pre3::kSegWords) return Fail(GM_ERR_USAGE, "segment_words must be 256");
+    if (tok_offsets && tok_offsets[num_tokens] > (int64_t{1} << 31) - 1) return Fail(GM_ERR_USAGE, "vocabulary bytes exceed 2^31");
+
+    // TokenTrie::Build's vocabulary rules (runtime.cpp:23-53): no empty
+    // tokens, no duplicates; the first offending id is reported.
+    std::unordered_set<std::string_view> seen;
+    seen.reserve(static_cast<size_t>(num_tokens) * 2);
+    std::vector<int32_t> offs(static_cast<size_t>(num_tokens) + 1);
+    for (int32_t i = 0; i < num_tokens; ++i) {
+      const int64_t lo = tok_offsets[i], hi = tok_offsets[i + 1];
+      if (hi < lo) return Fail(GM_ERR_USAGE, "token offsets not monotone");
+      if (hi == lo) return Fail(GM_ERR_VOCAB_EMPTY, "EmptyToken: token " + std::to_string(i) + " has no bytes");
+      std::string_view sv(reinterpret_cast<const char*>(tok_bytes + lo), static_cast<size_t>(hi - lo));
+      if (!seen.insert(sv).second) {
+        int32_t first = -1;
+        for (int32_t j = 0; j < i; ++j) {
+          if (std::string_view(reinterpret_cast<const char*>(tok_bytes + tok_offsets[j]),
+                               static_cast<size_t>(tok_offsets[j + 1] - tok_offsets[j])) == sv) {
+            first = j;
+            break;
+          }
+        }
+        return Fail(GM_ERR_VOCAB_DUPLICATE, "DuplicateToken: tokens " + std::to_string(first) + " and " +
+                                                std::to_string(i) + " are identical");
+      }
+      offs[static_cast<size_t>(i)] = static_cast<int32_t>(lo - tok_offsets[0]);
+    }
+    offs[static_cast<size_t>(num_tokens)] = num_tokens ? static_cast<int32_t>(tok_offsets[num_tokens] - tok_offsets[0]) : 0;
+
+    Check(cudaSetDevice(device), "cudaSetDevice");
+    auto e = std::make_unique<gm_engine>();
+    e->device = device;
+    pre3::FlatLayout f = pre3::Flatten(a->a);
+    e->aut.edges = DevUpload(f.edges, &e->owned);
+    e->aut.cond = DevUpload(f.cond_pool, &e->owned);
+    e->aut.push = DevUpload(f.push_pool, &e->owned);
+    e->aut.cand_begin = DevUpload(f.cand_begin, &e->owned);
+    e->aut.cand = DevUpload(f.cand, &e->owned);
+    e->aut.shift = DevUpload(a->a.shift_targets, &e->owned);
+    e->aut.num_states = a->a.num_states;
+    e->aut.initial = a->a.initial_state;
+
+    e->V = num_tokens;
+    e->W = (num_tokens + 1 + 31) / 32;
+    e->nseg = (e->W + pre3::kSegWords - 1) / pre3::kSegWords;
+    std::vector<uint8_t> bytes(num_tokens ? tok_bytes + tok_offsets[0] : tok_bytes,
+                               num_tokens ? tok_bytes + tok_offsets[num_tokens] : tok_bytes);
+    e->vocab.tok_off = DevUpload(offs, &e->owned);
+    e->vocab.tok_bytes = DevUpload(bytes, &e->owned);
+    e->structural = DevAlloc<uint32_t>(static_cast<size_t>(e->W), &e->owned);
+    Check(cudaMemset(e->structural, 0, sizeof(uint32_t) * static_cast<size_t>(e->W)), "memset");
+    e->vocab.structural = e->structural;
+    e->vocab.V = e->V;
+    e->vocab.W = e->W;
+    e->vocab.nseg = e->nseg;
+
+    const size_t C = static_cast<size_t>(o.context_slots);
+    auto& c = e->cache;
+    c.C = o.context_slots;
+    c.K = o.context_depth;
+    c.slot_hash = DevAlloc<unsigned long long>(C, &e->owned);
+    c.slot_meta = DevAlloc<int32_t>(C, &e->owned);
+    c.slot_keys = DevAlloc<int32_t>(C * static_cast<size_t>(c.K), &e->owned);
+    c.seg_state = DevAlloc<uint32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
+    c.ci = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
+    c.cd_off = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
+    c.cd_len = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
+    c.cd_pool = DevAlloc<int32_t>(static_cast<size_t>(o.cd_pool_entries), &e->owned);
+    c.pool_top = DevAlloc<unsigned long long>(1, &e->owned);
+    c.counters = DevAlloc<unsigned long long>(8, &e->owned);
+    c.pool_cap = o.cd_pool_entries;
+    Check(cudaMemset(c.slot_hash, 0, C * 8), "memset");
+    Check(cudaMemset(c.slot_meta, 0, C * 4), "memset");
+    Check(cudaMemset(c.seg_state, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
+    Check(cudaMemset(c.cd_len, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
+    Check(cudaMemset(c.pool_top, 0, 8), "memset");
+    Check(cudaMemset(c.counters, 0, 64), "memset");
+    Check(cudaDeviceSynchronize(), "engine upload");
+    *out = e.release();
+    return GM_OK;
+  });
+}
+
+int gm_engine_destroy(gm_engine* e) {
+  delete e;
+  return GM_OK;
+}
+
+int gm_engine_info(gm_engine* e, int64_t info[8]) {
+  return Guard([&]() -> int {
+    if (!e || !info) return Fail(GM_ERR_USAGE, "null argument");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    unsigned long long ctr[8], top = 0;
+    Check(cudaMemcpy(ctr, e->cache.counters, 64, cudaMemcpyDeviceToHost), "info");
+    Check(cudaMemcpy(&top, e->cache.pool_top, 8, cudaMemcpyDeviceToHost), "info");
+    info[0] = e->V;
+    info[1] = e->W;
+    info[2] = e->nseg;
+    info[3] = static_cast<int64_t>(ctr[0]);
+    info[4] = static_cast<int64_t>(top);
+    info[5] = static_cast<int64_t>(ctr[1]);
+    info[6] = static_cast<int64_t>(ctr[2]);
+    info[7] = e->device;
+    return GM_OK;
+  });
+}
+
+int gm_engine_set_structural(gm_engine* e, const uint32_t* host_words) {
+  return Guard([&]() -> int {
+    if (!e || !host_words) return Fail(GM_ERR_USAGE, "null argument");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    std::vector<uint32_t> w(host_words, host_words + e->W);
+    w[static_cast<size_t>(e->V >> 5)] &= ~(1u << (e->V & 31));  // EOS is never structural
+    Check(cudaMemcpy(e->structural, w.data(), w.size() * 4, cudaMemcpyHostToDevice), "structural");
+    return GM_OK;
+  });
+}
+
+// ---------------------------------------------------------------- batch
+int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batch** out) {
+  return Guard([&]() -> int {
+    if (!e || !out || batch < 0 || stack_capacity < 1) return Fail(GM_ERR_USAGE, "bad argument");
+    if (stack_capacity > 48 * 1024) return Fail(GM_ERR_USAGE, "stack_capacity must be <= 49152");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    auto b = std::make_unique<gm_batch>();
+    b->engine = e;
+    auto& v = b->view;
+    v.B = batch;
+    v.cap = stack_capacity;
+    v.seq = DevAlloc<pre3::SeqState>(static_cast<size_t>(batch), &b->owned);
+    v.stacks = DevAlloc<int32_t>(static_cast<size_t>(batch) * static_cast<size_t>(stack_capacity), &b->owned);
+    v.err = DevAlloc<unsigned int>(1, &b->owned);
+    v.stats = DevAlloc<unsigned long long>(8, &b->owned);
+    v.counters = DevAlloc<unsigned long long>(4, &b->owned);
+    v.stats_enabled = 0;
+    b->seg_counts = DevAlloc<int32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->nseg) * 2, &b->owned);
+    b->best = DevAlloc<unsigned long long>(static_cast<size_t>(batch), &b->owned);
+    Check(cudaMemset(v.err, 0, 4), "memset");
+    Check(cudaMemset(v.stats, 0, 64), "memset");
+    Check(cudaMemset(v.counters, 0, 32), "memset");
+    Check(cudaMemset(b->best, 0, static_cast<size_t>(batch) * 8), "memset");
+    Check(pre3::LaunchReset(e->aut, v, nullptr), "reset");
+    Check(cudaDeviceSynchronize(), "batch create");
+    *out = b.release();
+    return GM_OK;
+  });
+}
+
+int gm_batch_destroy(gm_batch* b) {
+  delete b;
+  return GM_OK;
+}
+
+int gm_batch_reset(gm_batch* b, void* stream) {
+  return Guard([&]() -> int {
+    if (!b) return Fail(GM_ERR_USAGE, "null batch");
+    Check(cudaSetDevice(b->engine->device), "cudaSetDevice");
+    Check(pre3::LaunchReset(b->engine->aut, b->view, static_cast<cudaStream_t>(stream)), "reset");
+    return GM_OK;
+  });
+}
+
+int gm_batch_download(gm_batch* b, int32_t seq, int32_t* state, int32_t* status, int32_t* stack,
+                      int32_t cap, int32_t* depth) {
+  return Guard([&]() -> int {
+    if (!b || seq < 0 || seq >= b->view.B) return Fail(GM_ERR_USAGE, "bad sequence index");
+    Check(cudaSetDevice(b->engine->device), "cudaSetDevice");
+    Check(cudaDeviceSynchronize(), "sync");
+    pre3::SeqState st;
+    Check(cudaMemcpy(&st, b->view.seq + seq, sizeof(st), cudaMemcpyDeviceToHost), "download");
+    if (depth) *depth = st.depth;
+    if (status) *status = st.status;
+    const int32_t n = std::min(st.depth, cap);
+    std::vector<int32_t> tmp(static_cast<size_t>(std::max(st.depth, 1)));
+    Check(cudaMemcpy(tmp.data(), b->view.stacks + static_cast<int64_t>(seq) * b->view.cap,
+                     sizeof(int32_t) * static_cast<size_t>(std::max(st.depth, 1)), cudaMemcpyDeviceToHost),
+          "download");
+    if (stack && n > 0) std::memcpy(stack, tmp.data(), sizeof(int32_t) * static_cast<size_t>(n));
+    if (state) *state = st.depth > 0 ? tmp[static_cast<size_t>(st.depth - 1)] : -1;
+    return GM_OK;
+  });
+}
+
+int gm_batch_upload(gm_batch* b, int32_t seq, int32_t status, const int32_t* stack, int32_t depth) {
+  return Guard([&]() -> int {
+    if (!b || seq < 0 || seq >= b->view.B || !stack) return Fail(GM_ERR_USAGE, "bad argument");
+    if (depth < 1 || depth > b->view.cap) return Fail(GM_ERR_STACK_OVERFLOW, "stack depth exceeds capacity");
+    for (int32_t i = 0; i < depth; ++i) {
+      if (stack[i] < 0 || stack[i] >= b->engine->aut.num_states) return Fail(GM_ERR_USAGE, "state out of range");
+    }
+    Check(cudaSetDevice(b->engine->device), "cudaSetDevice");
+    Check(cudaDeviceSynchronize(), "sync");
+    pre3::SeqState st;
+    Check(cudaMemcpy(&st, b->view.seq + seq, sizeof(st), cudaMemcpyDeviceToHost), "upload");
+    st.depth = depth;
+    st.status = status;
+    Check(cudaMemcpy(b->view.seq + seq, &st, sizeof(st), cudaMemcpyHostToDevice), "upload");
+    Check(cudaMemcpy(b->view.stacks + static_cast<int64_t>(seq) * b->view.cap, stack,
+                     sizeof(int32_t) * static_cast<size_t>(depth), cudaMemcpyHostToDevice),
+          "upload");
+    return GM_OK;
+  });
+}
+
+int gm_batch_check(gm_batch* b, void* stream) {
+  return Guard([&]() -> int {
+    if (!b) return Fail(GM_ERR_USAGE, "null batch");
+    Check(cudaSetDevice(b->engine->device), "cudaSetDevice");
+    Check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "stream sync");
+    unsigned int err = 0;
+    Check(cudaMemcpy(&err, b->view.err, 4, cudaMemcpyDeviceToHost), "check");
+    if (err) {
+      Check(cudaMemset(b->view.err, 0, 4), "memset");
+      return Fail(GM_ERR_STACK_OVERFLOW, "a mask walk exceeded its 64-entry push overlay");
+    }
+    return GM_OK;
+  });
+}
+
+int gm_batch_counters(gm_batch* b, int64_t counters[4]) {
+  return Guard([&]() -> int {
+    if (!b || !counters) return Fail(GM_ERR_USAGE, "null argument");
+    Check(cudaSetDevice(b->engine->device), "cudaSetDevice");
+    unsigned long long c[4];
+    Check(cudaMemcpy(c, b->view.counters, 32, cudaMemcpyDeviceToHost), "counters");
+    for (int i = 0; i < 4; ++i) counters[i] = static_cast<int64_t>(c[i]);
+    return GM_OK;
+  });
+}
+
+int gm_batch_fill_stats(gm_batch* b, int64_t stats[6]) {
+  return Guard([&]() -> int {
+    if (!b || !stats) return Fail(GM_ERR_USAGE, "null argument");
+    Check(cudaSetDevice(b->engine->device), "cudaSetDevice");
+    unsigned long long s[8];
+    Check(cudaMemcpy(s, b->view.stats, 64, cudaMemcpyDeviceToHost), "stats");
+    for (int i = 0; i < 6; ++i) stats[i] = static_cast<int64_t>(s[i]);
+    Check(cudaMemset(b->view.stats, 0, 64), "memset");
+    return GM_OK;
+  });
+}
+
+int gm_batch_set_stats(gm_batch* b, int32_t enable) {
+  if (!b) return Fail(GM_ERR_USAGE, "null batch");
+  b->view.stats_enabled = enable ? 1 : 0;
+  return GM_OK;
+}
+
+// ---------------------------------------------------------------- hot path
+int gm_fill_next_token_bitmask(gm_batch* b, uint32_t* bitmask, int64_t ld_words, void* stream) {
+  return gm_fill_and_mask_logits(b, bitmask, ld_words, nullptr, 0, nullptr, stream);
+}
+
+int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits,
+                            int64_t ld, int32_t* seg_counts, void* stream) {
+  return Guard([&]() -> int {
+    if (!b) return Fail(GM_ERR_USAGE, "null batch");
+    gm_engine* e = b->engine;
+    if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
+    if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    Check(pre3::LaunchFill(pre3::kFillMask, e->aut, e->vocab, e->cache, b->view, bitmask, ld_words, logits, ld,
+                           seg_counts, nullptr, static_cast<cudaStream_t>(stream)),
+          "fill launch");
+    return GM_OK;
+  });
+}
+
+int gm_accept_tokens(gm_batch* b, const int32_t* tokens, int32_t* status_out, int32_t restart,
+                     void* stream) {
+  return Guard([&]() -> int {
+    if (!b || !tokens) return Fail(GM_ERR_USAGE, "null argument");
+    gm_engine* e = b->engine;
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    Check(pre3::LaunchAccept(pre3::kSampleGiven, e->aut, e->vocab, b->view, tokens, status_out, restart, nullptr,
+                             0, nullptr, 0, nullptr, nullptr, 1, static_cast<cudaStream_t>(stream)),
+          "accept launch");
+    return GM_OK;
+  });
+}
+
+int gm_sample_stream_and_accept(gm_batch* b, const uint32_t* bitmask, int64_t ld_words,
+                                const int32_t* seg_counts, uint64_t seed, int32_t* tokens_out,
+                                void* stream) {
+  return Guard([&]() -> int {
+    if (!b || !bitmask || !seg_counts) return Fail(GM_ERR_USAGE, "null argument");
+    gm_engine* e = b->engine;
+    if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, b->view, nullptr, nullptr, 1, bitmask,
+                             ld_words, seg_counts, seed, nullptr, tokens_out, 1, static_cast<cudaStream_t>(stream)),
+          "sample launch");
+    return GM_OK;
+  });
+}
+
+int gm_sample_stream(gm_batch* b, const uint32_t* bitmask, int64_t ld_words, const int32_t* seg_counts,
+                     uint64_t seed, int32_t* tokens_out, void* stream) {
+  return Guard([&]() -> int {
+    if (!b || !bitmask || !seg_counts || !tokens_out) return Fail(GM_ERR_USAGE, "null argument");
+    gm_engine* e = b->engine;
+    if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, b->view, nullptr, nullptr, 0, bitmask,
+                             ld_words, seg_counts, seed, nullptr, tokens_out, 0, static_cast<cudaStream_t>(stream)),
+          "sample launch");
+    return GM_OK;
+  });
+}
+
+int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint32_t* bitmask,
+                          int64_t ld_words, int32_t* tokens_out, void* stream) {
+  return Guard([&]() -> int {
+    if (!b || !logits) return Fail(GM_ERR_USAGE, "null argument");
+    gm_engine* e = b->engine;
+    if (ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Check(pre3::LaunchFill(pre3::kFillGreedy, e->aut, e->vocab, e->cache, b->view, bitmask, ld_words,
+                           const_cast<uint16_t*>(logits), ld, nullptr, b->best, s),
+          "greedy fill launch");
+    Check(pre3::LaunchAccept(pre3::kSampleGreedy, e->aut, e->vocab, b->view, nullptr, nullptr, 1, nullptr, 0,
+                             nullptr, 0, b->best, tokens_out, 1, s),
+          "greedy accept launch");
+    return GM_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle.
+
+Bit-exact for everything: bitmasks, -inf positions of the masked bf16
+logits, sampled tokens, post-accept DPDA states/statuses/stacks.  Mirrors the
+reference's runtime tests (tests/test_runtime.cpp:160-291) and acceptance
+criterion 3 (acceptance_main.cpp:202-219).
+"""
+import hashlib
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import paper_2506_03887_b200 as pk
+from oracle import Port
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+FIXTURES = ["paren", "list_left", "list_right", "digits", "expr", "json"]
+DEV = "cuda:0"
+
+
+def flat(name):
+    with open(os.path.join(GOLDEN, name + ".p3dpda"), "rb") as f:
+        return f.read()
+
+
+@pytest.fixture(scope="module")
+def vectors():
+    with open(os.path.join(GOLDEN, "vectors.json")) as f:
+        return json.load(f)
+
+
+def mask_hex(w, V):
+    n = V + 1
+    out = []
+    for i in range((n + 3) // 4):
+        nib = 0
+        for j in range(4):
+            bit = i * 4 + j
+            if bit < n and (int(w[bit >> 5]) >> (bit & 31)) & 1:
+                nib |= 1 << j
+        out.append("0123456789abcdef"[nib])
+    return "".join(out)
+
+
+def fill_batch(eng, cfgs, logits=False, cap=1024):
+    """Uploads configs, runs the fused fill, returns (masks, logits or None)."""
+    b = eng.batch(len(cfgs), cap)
+    for i, c in enumerate(cfgs):
+        b.set(i, c)
+    bm = torch.zeros((len(cfgs), eng.W), dtype=torch.int32, device=DEV)
+    lg = None
+    if logits:
+        lg = torch.randn((len(cfgs), eng.V + 1), dtype=torch.bfloat16, device=DEV)
+    b.fill(bm, lg)
+    b.check()
+    return bm.cpu().numpy().view(np.uint32), lg
+
+
+def test_paren_seven_token_masks(vectors):
+    vocab = [t.encode() for t in vectors["paren7"]["vocab"]]
+    eng = pk.DeviceEngine(pk.Automaton.load(flat("paren")), vocab)
+    for prefix, g in vectors["paren7"]["masks"].items():
+        st, status, stack = g["config"]
+        m = eng.ComputeMask(pk.RuntimeConfig(st, status, stack))
+        assert mask_hex(m, 7) == g["hex"], prefix
+    assert mask_hex(eng.ComputeMask(eng.InitialConfig()), 7) == "b2"
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("K", [1, 4, 16])
+def test_mask_agreement_cases(vectors, name, K):
+    """Golden reference masks for sampled configs, at several context depths
+    (K=1 forces many context-dependent tokens), twice (build then hit)."""
+    case = vectors["mask_agreement"][name]
+    vocab = [bytes.fromhex(h) for h in case["vocab_hex"]]
+    eng = pk.DeviceEngine(pk.Automaton.load(flat(name)), vocab, context_depth=K)
+    cfgs = [pk.RuntimeConfig(c["stack"][-1], c["status"], c["stack"]) for c in case["cases"]]
+    for _ in range(2):
+        masks, _ = fill_batch(eng, cfgs)
+        for m, c in zip(masks, case["cases"]):
+            assert mask_hex(m, len(vocab)) == c["hex"]
+
+
+def test_dead_and_accepted_rows_are_empty():
+    """runtime.cpp:282: non-alive configs get all-zero masks (and all -inf)."""
+    eng = pk.DeviceEngine(pk.Automaton.load(flat("paren")), [b"a", b"("])
+    cfgs = [pk.RuntimeConfig(0, pk.DEAD, [0]), pk.RuntimeConfig(0, pk.ACCEPTED, [0]),
+            pk.RuntimeConfig(0, pk.ALIVE, [0])]
+    masks, lg = fill_batch(eng, cfgs, logits=True)
+    assert masks[0].sum() == 0 and masks[1].sum() == 0 and masks[2].sum() != 0
+    lgf = lg.float().cpu().numpy()
+    assert np.all(np.isneginf(lgf[0])) and np.all(np.isneginf(lgf[1]))
+
+
+def run_stream(eng, B, steps, seed, cap=1024, check_logits=False, port=None):
+    """Device decode loop: fused fill (+logits) then stream-sample + accept."""
+    batch = eng.batch(B, cap)
+    bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
+    counts = torch.zeros((B, batch.nseg * 2), dtype=torch.int32, device=DEV)
+    toks = torch.zeros(B, dtype=torch.int32, device=DEV)
+    lg = torch.randn((B, eng.V + 1), dtype=torch.bfloat16, device=DEV) if check_logits else None
+    masks, tokens = [], []
+    for _ in range(steps):
+        if lg is not None:
+            lg.normal_()
+            before = lg.clone()
+        batch.fill(bm, lg, counts)
+        batch.sample_stream_and_accept(bm, counts, seed, toks)
+        batch.check()
+        m = bm.cpu().numpy().view(np.uint32).copy()
+        masks.append(m)
+        tokens.append(toks.cpu().numpy().copy())
+        if lg is not None:
+            bits = np.unpackbits(m.view(np.uint8), axis=1, bitorder="little")[:, : eng.V + 1].astype(bool)
+            after = lg.float().cpu().numpy()
+            assert np.array_equal(np.isneginf(after), ~bits | np.isneginf(before.float().cpu().numpy()))
+            assert np.array_equal(after[bits], before.float().cpu().numpy()[bits])
+    return batch, np.stack(masks, 1), np.stack(tokens, 1)
+
+
+def test_json32k_stream_matches_golden(vectors):
+    """Config 1 replayed on the GPU: every mask digest, token and the final
+    stacks equal the reference's (golden)."""
+    g = vectors["json32k_stream"]
+    vocab = pk.synth_vocab(32000)
+    eng = pk.DeviceEngine(pk.Automaton.load(flat("json")), vocab)
+    batch, masks, tokens = run_stream(eng, g["batch"], g["steps"], g["seed"], check_logits=True)
+    assert tokens.tolist() == g["tokens"]
+    for b in range(g["batch"]):
+        for s in range(g["steps"]):
+            assert hashlib.sha256(masks[b, s].tobytes()).hexdigest()[:32] == g["trace"][b][s]["mask"], (b, s)
+        fin = g["final"][b]
+        got = batch.get(b)
+        assert got.stack == fin["stack"] and got.status == fin["status"]
+
+
+@pytest.mark.parametrize("K", [2, 8])
+def test_json128k_stream_matches_port(K):
+    """Config 2 shape (JSON, 128,255 tokens): GPU decode loop == C port loop
+    (tokens every step, final stacks) for 24 sequences x 16 steps."""
+    vocab = pk.synth_vocab(128255)
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
+    port = Port(f, vocab)
+    B, steps, seed = 24, 16, 5
+    batch, masks, tokens = run_stream(eng, B, steps, seed)
+    _, ptoks, pstacks = port.decode_run(eng.structural, B, steps, seed, want_tokens=True, want_stacks=True)
+    assert np.array_equal(tokens, ptoks)
+    for b in range(B):
+        d = pstacks[b, 0]
+        got = batch.get(b)
+        assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1]
+
+
+def test_cache_pressure_paths():
+    """Tiny context table / tiny CD pool force the direct and failed-build
+    paths; results must not change."""
+    vocab = pk.synth_vocab(40000)
+    f = flat("json")
+    port = Port(f, vocab)
+    B, steps, seed = 16, 10, 9
+    _, ptoks, _ = port.decode_run(pk.structural_words(vocab), B, steps, seed, want_tokens=True)
+    for slots, pool in [(1, 1 << 20), (4, 1 << 20), (1024, 16)]:
+        eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=3, context_slots=slots,
+                              cd_pool_entries=pool)
+        _, _, tokens = run_stream(eng, B, steps, seed)
+        assert np.array_equal(tokens, ptoks), (slots, pool)
+
+
+@pytest.mark.parametrize("name", ["expr", "json", "digits"])
+def test_accept_tokens_matches_port(name):
+    """Engine::Step over token bytes, batched: random (often invalid) tokens,
+    EOS, skips (-1); statuses and stacks after every step equal the port's."""
+    rng = random.Random(17)
+    f = flat(name)
+    import oracle
+    acc = 0
+    for e in oracle.read_flat(f)["edges"]:
+        acc |= e["accepted"]
+    alphabet = [b for b in range(256) if (acc >> b) & 1]
+    vocab = sorted({bytes(rng.choice(alphabet) for _ in range(1 + rng.randrange(4))) for _ in range(300)})
+    V = len(vocab)
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab)
+    port = Port(f, vocab)
+    B = 64
+    batch = eng.batch(B, 512)
+    cfgs = [port.initial() for _ in range(B)]
+    toks_d = torch.zeros(B, dtype=torch.int32, device=DEV)
+    status_d = torch.zeros(B, dtype=torch.int32, device=DEV)
+    for _ in range(40):
+        toks = []
+        for b in range(B):
+            m = port.mask(cfgs[b])
+            allowed = [t for t in range(V + 1) if (int(m[t >> 5]) >> (t & 31)) & 1]
+            r = rng.random()
+            if allowed and r < 0.8:
+                t = rng.choice(allowed)
+            elif r < 0.9:
+                t = rng.randrange(V + 1)
+            else:
+                t = -1
+            toks.append(t)
+        toks_d.copy_(torch.tensor(toks, dtype=torch.int32))
+        batch.accept(toks_d, status_d)
+        batch.check()
+        st = status_d.cpu().numpy()
+        for b in range(B):
+            if toks[b] >= 0:
+                port.accept_token(cfgs[b], toks[b])
+            want = port.get(cfgs[b])
+            got = batch.get(b)
+            assert got.status == want[1] == st[b]
+            assert got.stack == want[2]
+            if want[1] != 0:
+                port.free(cfgs[b])
+                cfgs[b] = port.initial()
+                batch.set(b, pk.RuntimeConfig(cfgs[b].state, 0, [cfgs[b].stack[0]]))
+
+
+def test_greedy_decode_matches_port():
+    """Config 5 rule: argmax over allowed bf16 logits (ties -> lowest id)."""
+    vocab = pk.synth_vocab(32000)
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab)
+    port = Port(f, vocab)
+    B = 16
+    batch = eng.batch(B)
+    cfgs = [port.initial() for _ in range(B)]
+    g = torch.Generator(device=DEV).manual_seed(0)
+    toks = torch.zeros(B, dtype=torch.int32, device=DEV)
+    bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
+    for s in range(12):
+        lg = torch.randn((B, eng.V + 1), generator=g, device=DEV).to(torch.bfloat16)
+        if s % 3 == 0:
+            lg[:, ::7] = 3.0  # ties
+        batch.decode_step_greedy(lg, toks, bm)
+        batch.check()
+        host = lg.view(torch.int16).cpu().numpy().view(np.uint16)
+        tk = toks.cpu().numpy()
+        for b in range(B):
+            m = port.mask(cfgs[b])
+            t = port.greedy_pick(m, np.ascontiguousarray(host[b]))
+            assert t == tk[b], (s, b)
+            if t >= 0:
+                port.accept_token(cfgs[b], t)
+            if t < 0 or cfgs[b].status != 0:
+                port.free(cfgs[b])
+                cfgs[b] = port.initial()
+            assert batch.get(b).stack == port.get(cfgs[b])[2]
+
+
+def test_stack_overflow_status():
+    """A stack beyond the batch capacity yields GM_OVERFLOW, never a write
+    past the end."""
+    vocab = [b"[", b"]", b"1"]
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab)
+    batch = eng.batch(1, 12)
+    t = torch.zeros(1, dtype=torch.int32, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    for _ in range(8):
+        batch.accept(t, st)
+    batch.check()
+    assert int(st.item()) == pk.OVERFLOW
