@@ -40,7 +40,10 @@ def parse():
     p.add_argument("--batch", type=int, default=256, help="sequences per GPU")
     p.add_argument("--vocab", type=int, default=128255, help="regular tokens (EOS adds one bit)")
     p.add_argument("--grammar", default="json")
-    p.add_argument("--context-depth", type=int, default=8)
+    p.add_argument("--context-depth", type=int, default=12)
+    p.add_argument("--prewarm-steps", type=int, default=400,
+                   help="context-cache preprocessing: synthetic decode steps (other seed) before timing")
+    p.add_argument("--prewarm-batch", type=int, default=1024)
     p.add_argument("--stack-cap", type=int, default=1024)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-e2e", action="store_true")
@@ -204,6 +207,11 @@ def main():
     flat = automaton_bytes(args.grammar)
     vocab = pk.synth_vocab(args.vocab)
     eng = pk.DeviceEngine(pk.Automaton.load(flat), vocab, device=local, context_depth=args.context_depth)
+    t_pre = time.perf_counter()
+    if args.prewarm_steps > 0:
+        eng.prewarm(args.prewarm_batch, args.prewarm_steps, seed=0xC0FFEE + rank)
+    t_pre = time.perf_counter() - t_pre
+    pre_info = eng.info()
     B, V, W = args.batch, eng.V, eng.W
     V1 = V + 1
     batch = eng.batch(B, args.stack_cap)
@@ -228,26 +236,31 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        h0 = time.perf_counter()
         e0.record(stream)
         for i in range(K):
             ev[i][0].record(stream)
             batch.fill(bm, logits[i % R], counts)
             ev[i][1].record(stream)
             batch.sample_stream_and_accept(bm, counts, seed, toks)
+            ev[i][2].record(stream)
         e1.record(stream)
+        h1 = time.perf_counter()
         torch.cuda.synchronize()
     batch.check()
     if world > 1:
         dist.barrier()
     elapsed_ms = e0.elapsed_time(e1)
-    fill_ms = sum(a.elapsed_time(b) for a, b in ev) / K
-    t = torch.tensor([elapsed_ms, fill_ms], dtype=torch.float64, device=dev)
+    fill_ms = sum(a.elapsed_time(b) for a, b, _ in ev) / K
+    accept_ms = sum(b.elapsed_time(c) for _, b, c in ev) / K
+    host_ms = (h1 - h0) * 1e3 / K
+    t = torch.tensor([elapsed_ms, fill_ms, accept_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms, fill_ms = float(t[0]), float(t[1])
+    elapsed_ms, fill_ms, accept_ms = float(t[0]), float(t[1]), float(t[2])
     value = world * B * K / (elapsed_ms / 1e3)
 
     # Device-counted logit bytes of one more fill (outside the timed region).
@@ -326,18 +339,21 @@ def main():
         "config": dict(workload_config(args, world),
                        l2=f"rotating {R} logits buffers of {row_bytes / 2**20:.0f} MiB (> 126 MB L2)"),
         "mask_latency_us": 1e3 * fill_ms,
+        "step_breakdown_us": {"fill(lookup+build+fill+logits)": 1e3 * fill_ms,
+                              "sample+accept": 1e3 * accept_ms, "host_enqueue_per_step": 1e3 * host_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "FillKernel<0>",
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "FillKernel<0> (+LookupKernel, BuildKernel)",
                      "alg_bytes_per_seq_step": alg_bytes_seq,
                      "device_counted_logit_bytes_per_seq_step": (fstats["logit_bytes_read"] +
                                                                  fstats["logit_bytes_written"]) / B},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 2 * K,
+        "gpu_launches": 4 * K,
         "clocks": clocks.summary(),
-        "cache": {"contexts": info["context_slots_used"], "builds": info["context_builds"],
-                  "direct": info["direct_fills"], "cd_pool": info["cd_pool_used"],
-                  "last_fill": fstats},
+        "preprocessing": {"prewarm_s": t_pre, "prewarm": f"{args.prewarm_steps} steps x {args.prewarm_batch} seqs "
+                          f"(seed differs from the timed streams)", "contexts_after_prewarm": pre_info["context_slots_used"]},
+        "cache": {"contexts": info["context_slots_used"], "segment_builds": info["segment_builds"],
+                  "private_builds": info["private_builds"], "last_fill": fstats},
     }
     print(json.dumps(line), flush=True)
     if world > 1:

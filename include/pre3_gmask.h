@@ -84,7 +84,7 @@ int gm_automaton_info(const gm_automaton* a, int64_t info[8]);
 typedef struct gm_engine_options {
   int32_t context_depth;   /* K: stack entries keying the context cache (1..16; default 8) */
   int32_t context_slots;   /* hash-table capacity, power of two (default 8192) */
-  int64_t cd_pool_entries; /* context-dependent token pool (default 1<<24) */
+  int64_t reserved;        /* must be 0 */
   int32_t segment_words;   /* vocab segment size in mask words (default 256) */
 } gm_engine_options;
 
@@ -97,12 +97,17 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes,
                      const int64_t* tok_offsets, int32_t num_tokens,
                      const gm_engine_options* opts, int device, gm_engine** out);
 int gm_engine_destroy(gm_engine* e);
-/* info[0..7] = V, W, num_segments, context slots used, cd pool used,
- * context builds, direct (uncached) segment fills, device */
+/* info[0..7] = V, W, num_segments, context slots used, segment builds,
+ * private (uncached) rows built, 0, device */
 int gm_engine_info(gm_engine* e, int64_t info[8]);
 /* Host bitmask (W words) of "structural" tokens used by the synthetic
  * stream sampler (tokens containing any of {}[],:" ). */
 int gm_engine_set_structural(gm_engine* e, const uint32_t* host_words);
+/* Preprocessing: populates the context cache by running `steps` synthetic
+ * stream decode steps over `batch` scratch sequences (seeded by `seed`) on
+ * the device; synchronizes `stream`.  Results of later fills are identical
+ * with or without it (the cache only changes speed). */
+int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed, void* stream);
 
 /* ------------------------------------------------------------ batch */
 /* B sequences with fixed-capacity device stacks (reference stacks are
@@ -163,10 +168,10 @@ int gm_sample_stream(gm_batch* b, const uint32_t* bitmask, int64_t ld_words, con
 int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, uint32_t* bitmask,
                           int64_t ld_words, int32_t* tokens_out, void* stream);
 
-/* Launch statistics of the last fill (for roofline accounting):
+/* Statistics accumulated while enabled (gm_batch_set_stats), reset on read:
  * stats[0] = logits bytes read, [1] = logits bytes written (16-B chunk
- * granularity), [2] = context hits, [3] = builds, [4] = direct fills,
- * [5] = cd tokens resolved.  Requires gm_batch_check first. */
+ * granularity), [2] = context-dependent token walks, [3] = build items,
+ * [4] = private segment fills, [5] = 0. */
 int gm_batch_fill_stats(gm_batch* b, int64_t stats[6]);
 int gm_batch_set_stats(gm_batch* b, int32_t enable);
 

@@ -109,6 +109,7 @@ def lib() -> ctypes.CDLL:
             "gm_engine_destroy": ([P], ctypes.c_int),
             "gm_engine_info": ([P, P], ctypes.c_int),
             "gm_engine_set_structural": ([P, P], ctypes.c_int),
+            "gm_engine_prewarm": ([P, I32, I32, U64, P], ctypes.c_int),
             "gm_batch_create": ([P, I32, I32, PP], ctypes.c_int),
             "gm_batch_destroy": ([P], ctypes.c_int),
             "gm_batch_reset": ([P, P], ctypes.c_int),
@@ -223,7 +224,7 @@ class Automaton:
 
 class _EngineOptions(ctypes.Structure):
     _fields_ = [("context_depth", ctypes.c_int32), ("context_slots", ctypes.c_int32),
-                ("cd_pool_entries", ctypes.c_int64), ("segment_words", ctypes.c_int32)]
+                ("reserved", ctypes.c_int64), ("segment_words", ctypes.c_int32)]
 
 
 @dataclass
@@ -238,15 +239,14 @@ class DeviceEngine:
     """Engine::Engine + TokenTrie::Build on one CUDA device (runtime.cpp:18-113)."""
 
     def __init__(self, automaton: Automaton, tokens: Sequence[bytes], device: int = 0,
-                 context_depth: int = 8, context_slots: int = 8192,
-                 cd_pool_entries: int = 1 << 24):
+                 context_depth: int = 8, context_slots: int = 8192):
         self.automaton = automaton
         self.tokens = list(tokens)
         self.V = len(self.tokens)
         self.W = (self.V + 1 + 31) // 32
         self.device = device
         data, offs = pack_vocab(self.tokens)
-        opts = _EngineOptions(context_depth, context_slots, cd_pool_entries, 256)
+        opts = _EngineOptions(context_depth, context_slots, 0, 256)
         h = ctypes.c_void_p()
         _check(lib().gm_engine_create(automaton._h, _ptr(data), _ptr(offs), self.V, ctypes.byref(opts),
                                       device, ctypes.byref(h)))
@@ -258,9 +258,13 @@ class DeviceEngine:
     def info(self) -> dict:
         out = np.zeros(8, np.int64)
         _check(lib().gm_engine_info(self._h, _ptr(out)))
-        keys = ["V", "W", "num_segments", "context_slots_used", "cd_pool_used", "context_builds",
-                "direct_fills", "device"]
+        keys = ["V", "W", "num_segments", "context_slots_used", "segment_builds", "private_builds",
+                "reserved", "device"]
         return dict(zip(keys, (int(x) for x in out)))
+
+    def prewarm(self, batch: int = 1024, steps: int = 200, seed: int = 0x5EED, stream=None) -> None:
+        """Populates the context cache with synthetic decode streams (preprocessing)."""
+        _check(lib().gm_engine_prewarm(self._h, batch, steps, seed, _stream(stream)))
 
     def batch(self, size: int, stack_capacity: int = 1024) -> "Batch":
         return Batch(self, size, stack_capacity)
@@ -378,8 +382,8 @@ class Batch:
     def fill_stats(self) -> dict:
         out = np.zeros(6, np.int64)
         _check(lib().gm_batch_fill_stats(self._h, _ptr(out)))
-        return dict(zip(["logit_bytes_read", "logit_bytes_written", "hits", "builds", "direct",
-                         "cd_resolved"], (int(x) for x in out)))
+        return dict(zip(["logit_bytes_read", "logit_bytes_written", "cd_walks", "build_items",
+                         "private_fills", "reserved"], (int(x) for x in out)))
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value and _lib is not None:

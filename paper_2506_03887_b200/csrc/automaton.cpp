@@ -163,33 +163,58 @@ void Automaton::Validate() const {
 FlatLayout Flatten(const Automaton& a) {
   FlatLayout f;
   const int32_t S = a.num_states;
-  f.edges.reserve(a.edges.size());
-  for (const Edge& e : a.edges) {
-    DevEdge d;
-    d.cond_off = static_cast<int32_t>(f.cond_pool.size());
-    d.push_off = static_cast<int32_t>(f.push_pool.size());
-    d.cond_len = static_cast<int16_t>(e.match_pop.size());
-    d.push_len = static_cast<int16_t>(e.push.size());
-    d.flags = e.dynamic ? 1 : 0;
-    f.cond_pool.insert(f.cond_pool.end(), e.match_pop.begin(), e.match_pop.end());
-    f.push_pool.insert(f.push_pool.end(), e.push.begin(), e.push.end());
-    f.max_cond = std::max<int32_t>(f.max_cond, static_cast<int32_t>(e.match_pop.size()));
-    f.max_push = std::max<int32_t>(f.max_push, static_cast<int32_t>(e.push.size()) + (e.dynamic ? 1 : 0));
-    f.edges.push_back(d);
+  f.rec_begin.assign(static_cast<size_t>(S) * 257 + 1, 0);
+  f.state_any.assign(static_cast<size_t>(S) * 9, 0u);
+  // Conditions are shared by all records of an edge; static pushes too.
+  std::vector<int32_t> cond_at(a.edges.size()), push_at(a.edges.size());
+  for (size_t i = 0; i < a.edges.size(); ++i) {
+    const Edge& e = a.edges[i];
+    cond_at[i] = static_cast<int32_t>(f.rec_cond.size());
+    for (size_t j = 1; j < e.match_pop.size(); ++j) f.rec_cond.push_back(e.match_pop[j]);
+    push_at[i] = static_cast<int32_t>(f.rec_push.size());
+    if (!e.dynamic) f.rec_push.insert(f.rec_push.end(), e.push.begin(), e.push.end());
   }
-  if (f.cond_pool.empty()) f.cond_pool.push_back(0);
-  if (f.push_pool.empty()) f.push_pool.push_back(0);
-  f.cand_begin.assign(static_cast<size_t>(S) * 257 + 1, 0);
   for (int32_t s = 0; s < S; ++s) {
     for (int32_t t = 0; t < 257; ++t) {
-      f.cand_begin[static_cast<size_t>(s) * 257 + static_cast<size_t>(t)] = static_cast<int32_t>(f.cand.size());
+      f.rec_begin[static_cast<size_t>(s) * 257 + static_cast<size_t>(t)] = static_cast<int32_t>(f.recs.size());
       for (int32_t i = a.edge_begin[static_cast<size_t>(s)]; i < a.edge_begin[static_cast<size_t>(s) + 1]; ++i) {
-        if (a.edges[static_cast<size_t>(i)].Accepts(t)) f.cand.push_back(i);
+        const Edge& e = a.edges[static_cast<size_t>(i)];
+        if (!e.Accepts(t)) continue;
+        CandRec r{};
+        r.cond_len = static_cast<int16_t>(e.match_pop.size());
+        r.cond_off = cond_at[static_cast<size_t>(i)];
+        r.c1 = e.match_pop.size() > 1 ? e.match_pop[1] : -1;
+        r.c2 = e.match_pop.size() > 2 ? e.match_pop[2] : -1;
+        r.flags = 0;
+        if (e.dynamic) {
+          r.push_off = static_cast<int32_t>(f.rec_push.size());
+          f.rec_push.insert(f.rec_push.end(), e.push.begin(), e.push.end());
+          if (e.push.empty()) {
+            r.flags = 1;
+            r.new_state = -1;
+          } else {
+            const int32_t tgt = a.shift_targets[static_cast<size_t>(e.push.back()) * 256 + static_cast<size_t>(t)];
+            f.rec_push.push_back(tgt);
+            r.new_state = tgt;
+          }
+          r.push_len = static_cast<int16_t>(f.rec_push.size() - static_cast<size_t>(r.push_off));
+        } else {
+          r.push_off = push_at[static_cast<size_t>(i)];
+          r.push_len = static_cast<int16_t>(e.push.size());
+          r.new_state = e.push.back();
+        }
+        r.edge = i;
+        f.max_cond = std::max<int32_t>(f.max_cond, r.cond_len);
+        f.max_push = std::max<int32_t>(f.max_push, r.push_len + (r.flags & 1));
+        f.recs.push_back(r);
+        f.state_any[static_cast<size_t>(s) * 9 + static_cast<size_t>(t >> 5)] |= 1u << (t & 31);
       }
     }
   }
-  f.cand_begin[static_cast<size_t>(S) * 257] = static_cast<int32_t>(f.cand.size());
-  if (f.cand.empty()) f.cand.push_back(0);
+  f.rec_begin[static_cast<size_t>(S) * 257] = static_cast<int32_t>(f.recs.size());
+  if (f.recs.empty()) f.recs.push_back(CandRec{});
+  if (f.rec_cond.empty()) f.rec_cond.push_back(0);
+  if (f.rec_push.empty()) f.rec_push.push_back(0);
   return f;
 }
 

@@ -82,6 +82,7 @@ struct gm_batch {
   pre3::BatchView view{};
   int32_t* seg_counts = nullptr;          // internal scratch for fused decode
   unsigned long long* best = nullptr;     // greedy argmax packed keys
+  bool slots_valid = false;               // seq_slot matches the stacks (set by accept)
   std::vector<void*> owned;
   ~gm_batch() {
     cudaSetDevice(engine->device);
@@ -158,11 +159,10 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     if (!a || !out || num_tokens < 0 || (num_tokens > 0 && (!tok_bytes || !tok_offsets))) {
       return Fail(GM_ERR_USAGE, "bad argument");
     }
-    gm_engine_options o{8, 8192, int64_t{1} << 24, pre3::kSegWords};
+    gm_engine_options o{8, 8192, 0, pre3::kSegWords};
     if (opts) {
       if (opts->context_depth) o.context_depth = opts->context_depth;
       if (opts->context_slots) o.context_slots = opts->context_slots;
-      if (opts->cd_pool_entries) o.cd_pool_entries = opts->cd_pool_entries;
       if (opts->segment_words) o.segment_words = opts->segment_words;
     }
     if (o.context_depth < 1 || o.context_depth > pre3::kMaxContext) return Fail(GM_ERR_USAGE, "context_depth must be 1..16");
@@ -200,12 +200,12 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     auto e = std::make_unique<gm_engine>();
     e->device = device;
     pre3::FlatLayout f = pre3::Flatten(a->a);
-    e->aut.edges = DevUpload(f.edges, &e->owned);
-    e->aut.cond = DevUpload(f.cond_pool, &e->owned);
-    e->aut.push = DevUpload(f.push_pool, &e->owned);
-    e->aut.cand_begin = DevUpload(f.cand_begin, &e->owned);
-    e->aut.cand = DevUpload(f.cand, &e->owned);
+    e->aut.rec_begin = DevUpload(f.rec_begin, &e->owned);
+    e->aut.recs = DevUpload(f.recs, &e->owned);
+    e->aut.rec_cond = DevUpload(f.rec_cond, &e->owned);
+    e->aut.rec_push = DevUpload(f.rec_push, &e->owned);
     e->aut.shift = DevUpload(a->a.shift_targets, &e->owned);
+    e->aut.state_any = DevUpload(f.state_any, &e->owned);
     e->aut.num_states = a->a.num_states;
     e->aut.initial = a->a.initial_state;
 
@@ -230,19 +230,13 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.slot_hash = DevAlloc<unsigned long long>(C, &e->owned);
     c.slot_meta = DevAlloc<int32_t>(C, &e->owned);
     c.slot_keys = DevAlloc<int32_t>(C * static_cast<size_t>(c.K), &e->owned);
-    c.seg_state = DevAlloc<uint32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.ci = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
-    c.cd_off = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
-    c.cd_len = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
-    c.cd_pool = DevAlloc<int32_t>(static_cast<size_t>(o.cd_pool_entries), &e->owned);
-    c.pool_top = DevAlloc<unsigned long long>(1, &e->owned);
+    c.cdb = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
+    c.cd_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.counters = DevAlloc<unsigned long long>(8, &e->owned);
-    c.pool_cap = o.cd_pool_entries;
     Check(cudaMemset(c.slot_hash, 0, C * 8), "memset");
     Check(cudaMemset(c.slot_meta, 0, C * 4), "memset");
-    Check(cudaMemset(c.seg_state, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
-    Check(cudaMemset(c.cd_len, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
-    Check(cudaMemset(c.pool_top, 0, 8), "memset");
+    Check(cudaMemset(c.cd_cnt, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
     Check(cudaMemset(c.counters, 0, 64), "memset");
     Check(cudaDeviceSynchronize(), "engine upload");
     *out = e.release();
@@ -259,16 +253,16 @@ int gm_engine_info(gm_engine* e, int64_t info[8]) {
   return Guard([&]() -> int {
     if (!e || !info) return Fail(GM_ERR_USAGE, "null argument");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
-    unsigned long long ctr[8], top = 0;
+    unsigned long long ctr[8];
     Check(cudaMemcpy(ctr, e->cache.counters, 64, cudaMemcpyDeviceToHost), "info");
-    Check(cudaMemcpy(&top, e->cache.pool_top, 8, cudaMemcpyDeviceToHost), "info");
+    const unsigned long long top = 0;
     info[0] = e->V;
     info[1] = e->W;
     info[2] = e->nseg;
     info[3] = static_cast<int64_t>(ctr[0]);
-    info[4] = static_cast<int64_t>(top);
-    info[5] = static_cast<int64_t>(ctr[1]);
-    info[6] = static_cast<int64_t>(ctr[2]);
+    info[4] = static_cast<int64_t>(ctr[1]);
+    info[5] = static_cast<int64_t>(ctr[2]);
+    info[6] = static_cast<int64_t>(top);
     info[7] = e->device;
     return GM_OK;
   });
@@ -302,6 +296,14 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.stats = DevAlloc<unsigned long long>(8, &b->owned);
     v.counters = DevAlloc<unsigned long long>(4, &b->owned);
     v.stats_enabled = 0;
+    v.seq_slot = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
+    v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
+    v.items = DevAlloc<int4>(static_cast<size_t>(batch) * static_cast<size_t>(e->nseg), &b->owned);
+    v.n_items = DevAlloc<unsigned int>(1, &b->owned);
+    Check(cudaMemset(v.n_items, 0, 4), "memset");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
+    v.build_grid = sms * 4;
     b->seg_counts = DevAlloc<int32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->nseg) * 2, &b->owned);
     b->best = DevAlloc<unsigned long long>(static_cast<size_t>(batch), &b->owned);
     Check(cudaMemset(v.err, 0, 4), "memset");
@@ -325,6 +327,7 @@ int gm_batch_reset(gm_batch* b, void* stream) {
     if (!b) return Fail(GM_ERR_USAGE, "null batch");
     Check(cudaSetDevice(b->engine->device), "cudaSetDevice");
     Check(pre3::LaunchReset(b->engine->aut, b->view, static_cast<cudaStream_t>(stream)), "reset");
+    b->slots_valid = false;
     return GM_OK;
   });
 }
@@ -367,6 +370,7 @@ int gm_batch_upload(gm_batch* b, int32_t seq, int32_t status, const int32_t* sta
     Check(cudaMemcpy(b->view.stacks + static_cast<int64_t>(seq) * b->view.cap, stack,
                      sizeof(int32_t) * static_cast<size_t>(depth), cudaMemcpyHostToDevice),
           "upload");
+    b->slots_valid = false;
     return GM_OK;
   });
 }
@@ -429,8 +433,9 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     Check(pre3::LaunchFill(pre3::kFillMask, e->aut, e->vocab, e->cache, b->view, bitmask, ld_words, logits, ld,
-                           seg_counts, nullptr, static_cast<cudaStream_t>(stream)),
+                           seg_counts, nullptr, !b->slots_valid, static_cast<cudaStream_t>(stream)),
           "fill launch");
+    b->slots_valid = true;
     return GM_OK;
   });
 }
@@ -441,9 +446,10 @@ int gm_accept_tokens(gm_batch* b, const int32_t* tokens, int32_t* status_out, in
     if (!b || !tokens) return Fail(GM_ERR_USAGE, "null argument");
     gm_engine* e = b->engine;
     Check(cudaSetDevice(e->device), "cudaSetDevice");
-    Check(pre3::LaunchAccept(pre3::kSampleGiven, e->aut, e->vocab, b->view, tokens, status_out, restart, nullptr,
+    Check(pre3::LaunchAccept(pre3::kSampleGiven, e->aut, e->vocab, e->cache, b->view, tokens, status_out, restart, nullptr,
                              0, nullptr, 0, nullptr, nullptr, 1, static_cast<cudaStream_t>(stream)),
           "accept launch");
+    b->slots_valid = true;
     return GM_OK;
   });
 }
@@ -456,9 +462,10 @@ int gm_sample_stream_and_accept(gm_batch* b, const uint32_t* bitmask, int64_t ld
     gm_engine* e = b->engine;
     if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
-    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, b->view, nullptr, nullptr, 1, bitmask,
+    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, nullptr, nullptr, 1, bitmask,
                              ld_words, seg_counts, seed, nullptr, tokens_out, 1, static_cast<cudaStream_t>(stream)),
           "sample launch");
+    b->slots_valid = true;
     return GM_OK;
   });
 }
@@ -470,7 +477,7 @@ int gm_sample_stream(gm_batch* b, const uint32_t* bitmask, int64_t ld_words, con
     gm_engine* e = b->engine;
     if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
-    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, b->view, nullptr, nullptr, 0, bitmask,
+    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, nullptr, nullptr, 0, bitmask,
                              ld_words, seg_counts, seed, nullptr, tokens_out, 0, static_cast<cudaStream_t>(stream)),
           "sample launch");
     return GM_OK;
@@ -487,12 +494,29 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Check(pre3::LaunchFill(pre3::kFillGreedy, e->aut, e->vocab, e->cache, b->view, bitmask, ld_words,
-                           const_cast<uint16_t*>(logits), ld, nullptr, b->best, s),
+                           const_cast<uint16_t*>(logits), ld, nullptr, b->best, !b->slots_valid, s),
           "greedy fill launch");
-    Check(pre3::LaunchAccept(pre3::kSampleGreedy, e->aut, e->vocab, b->view, nullptr, nullptr, 1, nullptr, 0,
+    Check(pre3::LaunchAccept(pre3::kSampleGreedy, e->aut, e->vocab, e->cache, b->view, nullptr, nullptr, 1, nullptr, 0,
                              nullptr, 0, b->best, tokens_out, 1, s),
           "greedy accept launch");
+    b->slots_valid = true;
     return GM_OK;
+  });
+}
+
+int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed, void* stream) {
+  return Guard([&]() -> int {
+    if (!e || batch < 1 || steps < 0) return Fail(GM_ERR_USAGE, "bad argument");
+    gm_batch* b = nullptr;
+    int rc = gm_batch_create(e, batch, 1024, &b);
+    if (rc != GM_OK) return rc;
+    std::unique_ptr<gm_batch> guard(b);
+    uint32_t* bm = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
+    for (int32_t s = 0; s < steps; ++s) {
+      if ((rc = gm_fill_and_mask_logits(b, bm, e->W, nullptr, 0, b->seg_counts, stream)) != GM_OK) return rc;
+      if ((rc = gm_sample_stream_and_accept(b, bm, e->W, b->seg_counts, seed, nullptr, stream)) != GM_OK) return rc;
+    }
+    return gm_batch_check(b, stream);
   });
 }
 

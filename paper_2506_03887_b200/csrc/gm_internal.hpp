@@ -51,24 +51,32 @@ Automaton LoadFlat(const uint8_t* data, size_t n);
 std::vector<uint8_t> SaveFlat(const Automaton& a);
 Automaton CompileGrammar(const std::string& text, bool aggregate, bool merge);
 
-// Device-oriented flattening.
-struct DevEdge {
-  int32_t cond_off;
-  int32_t push_off;
-  int16_t cond_len;
-  int16_t push_len;
-  int32_t flags;  // bit0 dynamic
+// Device-oriented flattening.  For every (state, terminal)
+// the candidate edges — those whose accepted set contains the terminal — in
+// arbitration order, each as a self-contained record: the condition minus its
+// first entry (always the current state, dpda.hpp:45 `front() == source`),
+// the push sequence with a dynamic edge's shift target resolved for that
+// terminal when the push prefix is non-empty (optimizer.cpp:33-76,
+// runtime.cpp:159-164), and the resulting state.
+struct CandRec {
+  int16_t cond_len;   // full |match_pop| (entry 0 implicit)
+  int16_t push_len;   // entries to push (resolved dynamic target included)
+  int32_t cond_off;   // rec_cond index of entry 1 (entries 1..cond_len-1, top first)
+  int32_t push_off;   // rec_push index (bottom first)
+  int32_t flags;      // bit0: dynamic with empty push prefix (target from the exposed top)
+  int32_t new_state;  // top after apply, -1 when bit0
+  int32_t c1;         // match_pop[1] (valid when cond_len > 1)
+  int32_t c2;         // match_pop[2] (valid when cond_len > 2)
+  int32_t edge;       // index into Automaton::edges (diagnostics)
 };
-static_assert(sizeof(DevEdge) == 16, "DevEdge layout");
+static_assert(sizeof(CandRec) == 32, "CandRec layout");
 
 struct FlatLayout {
-  std::vector<DevEdge> edges;
-  std::vector<int32_t> cond_pool;  // top first
-  std::vector<int32_t> push_pool;  // bottom first
-  // Candidate edges per (state, terminal), terminal 0..256, in arbitration
-  // order: the edges whose accepted set contains the terminal.
-  std::vector<int32_t> cand_begin;  // S*257 + 1
-  std::vector<int32_t> cand;
+  std::vector<int32_t> rec_begin;  // S*257 + 1
+  std::vector<CandRec> recs;
+  std::vector<int32_t> rec_cond;
+  std::vector<int32_t> rec_push;
+  std::vector<uint32_t> state_any;  // S*9: bytes with any candidate (8 words) + bit0 of word 8 = '$'
   int32_t max_cond = 0, max_push = 0;
 };
 

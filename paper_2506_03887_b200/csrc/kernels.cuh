@@ -10,10 +10,12 @@
 
 namespace pre3 {
 
-constexpr int kThreads = 256;      // fill CTA size (8 warps)
-constexpr int kSegWords = 256;     // mask words per vocab segment (8192 tokens)
-constexpr int kMaxContext = 16;    // max K
-constexpr int kWalkOverlay = 64;   // per-thread pushed-entry overlay in a mask walk
+constexpr int kThreads = 256;                     // fill / build CTA size (8 warps)
+constexpr int kSegWords = 256;                    // mask words per vocab segment
+constexpr int kSegTokens = kSegWords * 32;        // 8192 tokens per segment
+constexpr int kChunksPerSeg = kSegTokens / kThreads;  // build work units per segment
+constexpr int kMaxContext = 16;                   // max K
+constexpr int kWalkOverlay = 64;                  // per-thread pushed-entry overlay in a mask walk
 
 // Per-sequence device state: {depth, status, draws, reserved}.
 struct SeqState {
@@ -24,12 +26,12 @@ struct SeqState {
 };
 
 struct AutView {
-  const DevEdge* edges;
-  const int32_t* cond;
-  const int32_t* push;
-  const int32_t* cand_begin;  // S*257+1
-  const int32_t* cand;
-  const int32_t* shift;  // S*256
+  const int32_t* rec_begin;  // S*257+1
+  const CandRec* recs;
+  const int32_t* rec_cond;
+  const int32_t* rec_push;
+  const int32_t* shift;       // S*256
+  const uint32_t* state_any;  // S*9
   int32_t num_states;
   int32_t initial;
 };
@@ -43,20 +45,18 @@ struct VocabView {
   int32_t nseg;                // ceil(W / kSegWords)
 };
 
-// Context cache: key = (n = min(depth, K), complete = depth <= K, top-n
-// stack entries top first) -> per segment {CI bitset words, CD token list}.
+// Context cache (engine-wide, shared by batches on the device).  Key =
+// (n = min(depth, K), complete = depth <= K, the top n stack entries) ->
+// {CI: tokens accepted whatever lies below the key, CD: tokens whose walk
+// reaches below the key} as two W-word bitsets, plus per-segment CD counts.
 struct CacheView {
   unsigned long long* slot_hash;  // C; 0 = empty
   int32_t* slot_meta;             // C; n | complete << 8 | ready << 16
   int32_t* slot_keys;             // C*K
-  uint32_t* seg_state;            // C*nseg; 0 empty, 1 building, 2 ready, 3 failed
-  uint32_t* ci;                   // C*W context-independent accept bits
-  int32_t* cd_off;                // C*nseg
-  int32_t* cd_len;                // C*nseg
-  int32_t* cd_pool;
-  unsigned long long* pool_top;
-  long long pool_cap;
-  unsigned long long* counters;  // [0] slots, [1] builds, [2] direct, [3] cd resolved
+  uint32_t* ci;                   // C*W
+  uint32_t* cdb;                  // C*W
+  int32_t* cd_cnt;                // C*nseg
+  unsigned long long* counters;   // [0] slots, [1] segment builds, [2] private builds
   int32_t C;
   int32_t K;
 };
@@ -66,21 +66,28 @@ struct BatchView {
   int32_t* stacks;  // B*cap, bottom first
   int32_t cap;
   int32_t B;
+  int32_t* seq_slot;        // B: cache slot, C+b = private row, -2 = not alive
+  uint32_t* priv;           // B*W private (uncached) masks
+  int4* items;              // build work list {slot, seg, seq, 0}
+  unsigned int* n_items;
   unsigned int* err;                  // bit0: walk overlay overflow
-  unsigned long long* stats;          // [0] rd bytes, [1] wr bytes, [2] hits, [3] builds, [4] direct, [5] cd
+  unsigned long long* stats;          // [0] rd bytes, [1] wr bytes, [2] cd walks, [3] builds, [4] private
   unsigned long long* counters;       // [0] restarts, [1] draws, [2] fills, [3] accepts
   int32_t stats_enabled;
+  int32_t build_grid;
 };
 
 enum FillMode { kFillMask = 0, kFillGreedy = 1 };
 enum SampleMode { kSampleGiven = 0, kSampleStream = 1, kSampleGreedy = 2 };
 
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s);
+// lookup + build + fill (+ bf16 -inf masking or greedy argmax).
 cudaError_t LaunchFill(int mode, const AutView& a, const VocabView& v, const CacheView& c,
                        const BatchView& b, uint32_t* bitmask, long long ldw, uint16_t* logits,
-                       long long ld, int32_t* seg_counts, unsigned long long* best,
+                       long long ld, int32_t* seg_counts, unsigned long long* best, bool need_lookup,
                        cudaStream_t s);
-cudaError_t LaunchAccept(int sample, const AutView& a, const VocabView& v, const BatchView& b,
+// do_accept != 0 also assigns each sequence's context slot for the next fill.
+cudaError_t LaunchAccept(int sample, const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
                          const int32_t* tokens, int32_t* status_out, int restart,
                          const uint32_t* bitmask, long long ldw, const int32_t* seg_counts,
                          unsigned long long seed, unsigned long long* best, int32_t* tokens_out,

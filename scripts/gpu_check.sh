@@ -1,8 +1,12 @@
+# GPU round script: tests, smoke, bench, launch list, ncu capture of FillKernel.
 set -x
 cd $GRAFT_REPO_ROOT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-ls -la paper_2506_03887_b200/*.so oracle/_ref/*.so
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?"
 tail -30 gpurun_out/pytest_gpu.txt
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?"; tail -5 gpurun_out/smoke.txt
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench1.json 2> gpurun_out/bench1.err; echo "bench rc=$?"; cat gpurun_out/bench1.json; tail -5 gpurun_out/bench1.err
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+if [ "${PROFILE:-1}" = "1" ]; then
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 60 --warmup 40 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:FillKernel -s 60 -c 1 -o gpurun_out/prof_fill -f python bench.py --steps 20 --warmup 60 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/ncu_full.log
+fi
