@@ -83,6 +83,20 @@ struct gm_batch {
   int32_t* seg_counts = nullptr;          // internal scratch for fused decode
   unsigned long long* best = nullptr;     // greedy argmax packed keys
   bool slots_valid = false;               // seq_slot matches the stacks (set by accept)
+  bool lookup_pending = false;            // builds queued by an accept, not yet consumed by a fill
+
+  // Accept flags: bit0 accept; bit1 assign context slots, at most once per
+  // fill so the build queue (2*B*nseg items) cannot overflow.
+  int AcceptFlags() {
+    const int flags = lookup_pending ? 1 : 3;
+    slots_valid = !lookup_pending;
+    lookup_pending = true;
+    return flags;
+  }
+  void FillDone() {
+    slots_valid = true;
+    lookup_pending = false;
+  }
   std::vector<void*> owned;
   ~gm_batch() {
     cudaSetDevice(engine->device);
@@ -298,7 +312,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.stats_enabled = 0;
     v.seq_slot = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
     v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
-    v.items = DevAlloc<int4>(static_cast<size_t>(batch) * static_cast<size_t>(e->nseg), &b->owned);
+    v.items = DevAlloc<int4>(2 * static_cast<size_t>(batch) * static_cast<size_t>(e->nseg), &b->owned);
     v.n_items = DevAlloc<unsigned int>(1, &b->owned);
     Check(cudaMemset(v.n_items, 0, 4), "memset");
     int sms = 148;
@@ -435,7 +449,7 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     Check(pre3::LaunchFill(pre3::kFillMask, e->aut, e->vocab, e->cache, b->view, bitmask, ld_words, logits, ld,
                            seg_counts, nullptr, !b->slots_valid, static_cast<cudaStream_t>(stream)),
           "fill launch");
-    b->slots_valid = true;
+    b->FillDone();
     return GM_OK;
   });
 }
@@ -447,9 +461,8 @@ int gm_accept_tokens(gm_batch* b, const int32_t* tokens, int32_t* status_out, in
     gm_engine* e = b->engine;
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     Check(pre3::LaunchAccept(pre3::kSampleGiven, e->aut, e->vocab, e->cache, b->view, tokens, status_out, restart, nullptr,
-                             0, nullptr, 0, nullptr, nullptr, 1, static_cast<cudaStream_t>(stream)),
+                             0, nullptr, 0, nullptr, nullptr, b->AcceptFlags(), static_cast<cudaStream_t>(stream)),
           "accept launch");
-    b->slots_valid = true;
     return GM_OK;
   });
 }
@@ -463,9 +476,9 @@ int gm_sample_stream_and_accept(gm_batch* b, const uint32_t* bitmask, int64_t ld
     if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, nullptr, nullptr, 1, bitmask,
-                             ld_words, seg_counts, seed, nullptr, tokens_out, 1, static_cast<cudaStream_t>(stream)),
+                             ld_words, seg_counts, seed, nullptr, tokens_out, b->AcceptFlags(),
+                             static_cast<cudaStream_t>(stream)),
           "sample launch");
-    b->slots_valid = true;
     return GM_OK;
   });
 }
@@ -496,10 +509,10 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     Check(pre3::LaunchFill(pre3::kFillGreedy, e->aut, e->vocab, e->cache, b->view, bitmask, ld_words,
                            const_cast<uint16_t*>(logits), ld, nullptr, b->best, !b->slots_valid, s),
           "greedy fill launch");
+    b->FillDone();
     Check(pre3::LaunchAccept(pre3::kSampleGreedy, e->aut, e->vocab, e->cache, b->view, nullptr, nullptr, 1, nullptr, 0,
-                             nullptr, 0, b->best, tokens_out, 1, s),
+                             nullptr, 0, b->best, tokens_out, b->AcceptFlags(), s),
           "greedy accept launch");
-    b->slots_valid = true;
     return GM_OK;
   });
 }

@@ -213,16 +213,15 @@ __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int com
 // ---------------------------------------------------------------------------
 // Context slot of sequence b for the next fill (seq_slot[b]); queues the
 // build of a new slot.  Used by LookupKernel and, fused, by AcceptKernel.
-__device__ void AssignSlot(const CacheView& Cc, const BatchView& Bt, int b, const SeqState& st, int nseg) {
+// `key` = the top min(depth, K) stack entries, top first.
+__device__ void AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int b, const SeqState& st, int nseg,
+                              const int32_t* key) {
   if (st.status != kAlive) {
     Bt.seq_slot[b] = -2;
     return;
   }
-  const int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
   const int n = min(st.depth, Cc.K);
   const int complete = st.depth <= Cc.K ? 1 : 0;
-  int32_t key[kMaxContext];
-  for (int i = 0; i < n; ++i) key[i] = stack[st.depth - 1 - i];
   bool created = false;
   int slot = LookupSlot(Cc, key, n, complete, &created);
   if (slot < 0 || created) {
@@ -242,7 +241,12 @@ __device__ void AssignSlot(const CacheView& Cc, const BatchView& Bt, int b, cons
 __global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, int nseg) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= Bt.B) return;
-  AssignSlot(Cc, Bt, b, Bt.seq[b], nseg);
+  const SeqState st = Bt.seq[b];
+  const int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+  int32_t key[kMaxContext];
+  const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
+  for (int i = 0; i < n; ++i) key[i] = stack[st.depth - 1 - i];
+  AssignSlotKey(Cc, Bt, b, st, nseg, key);
 }
 
 // ---------------------------------------------------------------------------
@@ -256,11 +260,21 @@ __global__ void __launch_bounds__(kThreads) BuildKernel(AutView A, VocabView Vv,
     const int chunk = static_cast<int>(u % kChunksPerSeg);
     const int slot = it.x, seg = it.y, b = it.z;
     const bool priv = slot >= Cc.C;
-    const int depth = Bt.seq[b].depth;
-    const int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
-    const int nb = priv ? depth : min(depth, Cc.K);
-    const bool complete = priv || depth <= Cc.K;
-    for (int i = tid; i < nb; i += kThreads) base_s[i] = stack[depth - nb + i];
+    int nb;
+    bool complete;
+    if (priv) {
+      // Private row: the sequence's whole current stack (always complete).
+      nb = Bt.seq[b].depth;
+      complete = true;
+      const int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+      for (int i = tid; i < nb; i += kThreads) base_s[i] = stack[i];
+    } else {
+      // Shared slot: its stored key (top first), independent of any stack.
+      const int meta = __ldcg(Cc.slot_meta + slot);
+      nb = meta & 0xff;
+      complete = (meta >> 8) & 1;
+      for (int i = tid; i < nb; i += kThreads) base_s[i] = __ldcg(Cc.slot_keys + slot * Cc.K + (nb - 1 - i));
+    }
     __syncthreads();
     const int t = seg * kSegTokens + chunk * kThreads + tid;
     int r = kReject;
@@ -522,23 +536,48 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
       const bool use_s = ((u >> 34) & 1ull) && ns > 0;
       const uint32_t nsel = static_cast<uint32_t>(use_s ? ns : na);
       uint32_t r = static_cast<uint32_t>((static_cast<unsigned long long>(static_cast<uint32_t>(u)) * nsel) >> 32);
-      int seg = 0;
-      for (; seg < Vv.nseg; ++seg) {
-        const int c = seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + (use_s ? 1 : 0)];
-        if (r < static_cast<uint32_t>(c)) break;
-        r -= static_cast<uint32_t>(c);
+      // Segment holding the r-th selected token: warp prefix sum over the
+      // per-segment counts, 32 segments per round.
+      int seg = -1;
+      for (int s0 = 0; s0 < Vv.nseg && seg < 0; s0 += 32) {
+        const int s = s0 + lane;
+        const int c = s < Vv.nseg ? seg_counts[(static_cast<long long>(b) * Vv.nseg + s) * 2 + (use_s ? 1 : 0)] : 0;
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, inc, 31);
+        if (r < static_cast<uint32_t>(total)) {
+          const int src = __ffs(__ballot_sync(0xffffffffu, static_cast<uint32_t>(inc) > r)) - 1;
+          seg = s0 + src;
+          r -= static_cast<uint32_t>(__shfl_sync(0xffffffffu, inc - c, src));
+        } else {
+          r -= static_cast<uint32_t>(total);
+        }
       }
-      const int w0 = seg * kSegWords;
-      const int w1 = min(Vv.W, w0 + kSegWords);
-      tok = -1;
-      for (int wb = w0; wb < w1 && tok < 0; wb += 32) {
-        const int w = wb + lane;
+      const int w0 = max(seg, 0) * kSegWords;
+      const int w1 = seg < 0 ? w0 : min(Vv.W, w0 + kSegWords);
+      // All of the segment's words are loaded up front (independent loads).
+      uint32_t xs[kSegWords / 32];
+#pragma unroll
+      for (int j = 0; j < kSegWords / 32; ++j) {
+        const int w = w0 + j * 32 + lane;
         uint32_t x = 0;
         if (w < w1) {
           x = row[w];
           if (w == (Vv.V >> 5)) x &= ~(1u << (Vv.V & 31));
           if (use_s) x &= __ldg(Vv.structural + w);
         }
+        xs[j] = x;
+      }
+      tok = -1;
+#pragma unroll
+      for (int j = 0; j < kSegWords / 32; ++j) {
+        if (tok >= 0) break;
+        const int w = w0 + j * 32 + lane;
+        uint32_t x = xs[j];
         const int c = __popc(x);
         int inc = c;
 #pragma unroll
@@ -563,7 +602,7 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
     }
   }
   if (tokens_out != nullptr && lane == 0) tokens_out[b] = tok;
-  if (!do_accept) {
+  if (!(do_accept & 1)) {
     if (lane == 0) {
       Bt.seq[b].draws = st.draws;
       if (SAMPLE == kSampleStream) atomicAdd(Bt.counters + 1, 1ull);
@@ -636,11 +675,19 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
     st.status = kAlive;
   }
   __syncwarp();
+  // Key of the next fill's context: lane i loads entry i, lane 0 gathers.
+  int32_t key[kMaxContext];
+  if (do_accept & 2) {
+    const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
+    const int32_t kv = lane < n ? stack[st.depth - 1 - lane] : 0;
+#pragma unroll
+    for (int i = 0; i < kMaxContext; ++i) key[i] = __shfl_sync(0xffffffffu, kv, i);
+  }
   if (lane == 0) {
     Bt.seq[b] = st;
     atomicAdd(Bt.counters + 3, 1ull);
     if (SAMPLE == kSampleStream) atomicAdd(Bt.counters + 1, 1ull);
-    AssignSlot(Cc, Bt, b, st, Vv.nseg);  // context of the next fill
+    if (do_accept & 2) AssignSlotKey(Cc, Bt, b, st, Vv.nseg, key);
   }
 }
 

@@ -86,7 +86,8 @@ cudaError_t LaunchFill(int mode, const AutView& a, const VocabView& v, const Cac
                        const BatchView& b, uint32_t* bitmask, long long ldw, uint16_t* logits,
                        long long ld, int32_t* seg_counts, unsigned long long* best, bool need_lookup,
                        cudaStream_t s);
-// do_accept != 0 also assigns each sequence's context slot for the next fill.
+// do_accept: bit0 = accept the token (else sample only), bit1 = also assign
+// each sequence's context slot for the next fill (queues builds).
 cudaError_t LaunchAccept(int sample, const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
                          const int32_t* tokens, int32_t* status_out, int restart,
                          const uint32_t* bitmask, long long ldw, const int32_t* seg_counts,
