@@ -310,7 +310,7 @@ struct FillShared {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+__global__ void __launch_bounds__(kThreads, 8) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                        uint32_t* __restrict__ bitmask, long long ldw,
                                                        uint16_t* __restrict__ logits, long long ld,
                                                        int32_t* __restrict__ seg_counts,
@@ -408,22 +408,24 @@ __global__ void __launch_bounds__(kThreads) FillKernel(AutView A, VocabView Vv, 
       const int valid = min(8, t1 - tb);
       if (valid == 8 && vec_ok) {
         if (byte == 0xffu) continue;
-        uint4* p = reinterpret_cast<uint4*>(row + tb);
         if (byte == 0u) {
-          __stcs(p, make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u));
+          __stcs(reinterpret_cast<uint4*>(row + tb), make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u));
           wr += 16;
         } else {
-          uint4 v = __ldcs(p);
-          uint32_t* vv = reinterpret_cast<uint32_t*>(&v);
+          // Mixed chunk: store only the masked halves/pairs (no read of the
+          // row; L2 merges the partial sector).
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const uint32_t keep = (((byte >> (2 * j)) & 1u) ? 0x0000FFFFu : 0u) |
-                                  (((byte >> (2 * j + 1)) & 1u) ? 0xFFFF0000u : 0u);
-            vv[j] = (vv[j] & keep) | (0xFF80FF80u & ~keep);
+            const uint32_t pair = (byte >> (2 * j)) & 3u;
+            if (pair == 0u) {
+              __stcs(reinterpret_cast<uint32_t*>(row + tb) + j, 0xFF80FF80u);
+              wr += 4;
+            } else if (pair != 3u) {
+              __stcs(reinterpret_cast<unsigned short*>(row + tb + 2 * j + (pair == 2u ? 0 : 1)),
+                     static_cast<unsigned short>(0xFF80u));
+              wr += 2;
+            }
           }
-          __stcs(p, v);
-          rd += 16;
-          wr += 16;
         }
       } else {
         for (int j = 0; j < valid; ++j) {

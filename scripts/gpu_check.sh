@@ -15,3 +15,6 @@ python scripts/launches.py gpurun_out/launches.csv
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:FillKernel -s 450 -c 1 -o gpurun_out/prof_fill -f python bench.py --steps 20 --warmup 60 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu fill rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:BuildKernel -s 3 -c 1 -o gpurun_out/prof_build -f python bench.py --steps 5 --warmup 5 --prewarm-steps 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_build.log 2>&1; echo "ncu build rc=$?"
 fi
+if [ "${PROFILE:-1}" = "1" ]; then
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:AcceptKernel -s 450 -c 1 -o gpurun_out/prof_accept -f python bench.py --steps 20 --warmup 60 --no-e2e --no-cpu-baseline > gpurun_out/ncu_accept.log 2>&1; echo "ncu accept rc=$?"
+fi
