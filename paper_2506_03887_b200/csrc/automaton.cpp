@@ -166,9 +166,16 @@ FlatLayout Flatten(const Automaton& a) {
   f.rec_begin.assign(static_cast<size_t>(S) * 257 + 1, 0);
   f.state_any.assign(static_cast<size_t>(S) * 9, 0u);
   // Conditions are shared by all records of an edge; static pushes too.
+  // Every list starts on a 16-byte boundary so the device reads it with
+  // independent int4 loads (one memory latency per list, not per entry).
+  auto align4 = [](std::vector<int32_t>* v) {
+    while (v->size() % 4) v->push_back(-1);
+  };
   std::vector<int32_t> cond_at(a.edges.size()), push_at(a.edges.size());
   for (size_t i = 0; i < a.edges.size(); ++i) {
     const Edge& e = a.edges[i];
+    align4(&f.rec_cond);
+    align4(&f.rec_push);
     cond_at[i] = static_cast<int32_t>(f.rec_cond.size());
     for (size_t j = 1; j < e.match_pop.size(); ++j) f.rec_cond.push_back(e.match_pop[j]);
     push_at[i] = static_cast<int32_t>(f.rec_push.size());
@@ -187,6 +194,7 @@ FlatLayout Flatten(const Automaton& a) {
         r.c2 = e.match_pop.size() > 2 ? e.match_pop[2] : -1;
         r.flags = 0;
         if (e.dynamic) {
+          align4(&f.rec_push);
           r.push_off = static_cast<int32_t>(f.rec_push.size());
           f.rec_push.insert(f.rec_push.end(), e.push.begin(), e.push.end());
           if (e.push.empty()) {
@@ -213,8 +221,11 @@ FlatLayout Flatten(const Automaton& a) {
   }
   f.rec_begin[static_cast<size_t>(S) * 257] = static_cast<int32_t>(f.recs.size());
   if (f.recs.empty()) f.recs.push_back(CandRec{});
-  if (f.rec_cond.empty()) f.rec_cond.push_back(0);
-  if (f.rec_push.empty()) f.rec_push.push_back(0);
+  // Tail padding: vector reads of the last list stay in bounds.
+  f.rec_cond.insert(f.rec_cond.end(), 16, -1);
+  f.rec_push.insert(f.rec_push.end(), 16, -1);
+  align4(&f.rec_cond);
+  align4(&f.rec_push);
   return f;
 }
 

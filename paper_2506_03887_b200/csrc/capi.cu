@@ -243,7 +243,7 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.K = o.context_depth;
     c.slot_hash = DevAlloc<unsigned long long>(C, &e->owned);
     c.slot_meta = DevAlloc<int32_t>(C, &e->owned);
-    c.slot_keys = DevAlloc<int32_t>(C * static_cast<size_t>(c.K), &e->owned);
+    c.slot_keys = DevAlloc<int32_t>(C * static_cast<size_t>(pre3::kMaxContext), &e->owned);
     c.ci = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
     c.cdb = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
     c.cd_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);

@@ -83,25 +83,36 @@ __device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const
     CandRec fr;
     for (int c = cb; c < ce; ++c) {
       const CandRec r = LoadRec(A.recs + c);
-      bool match = true;
-      for (int j = 1; j < r.cond_len; ++j) {
-        const int want = j == 1 ? r.c1 : (j == 2 ? r.c2 : __ldg(A.rec_cond + r.cond_off + j - 1));
-        int v;
-        if (j < nl) {
-          v = loc[nl - 1 - j];
-        } else if (j - nl < nb) {
-          v = base[nb - 1 - (j - nl)];
-        } else {
-          if (!complete) return kUnknown;  // every known entry matched so far
-          match = false;
-          break;
-        }
-        if (v != want) {
-          match = false;
-          break;
+      // ConditionMatches (runtime.cpp:123-131) for entries 1..k-1 (entry 0 is
+      // the current state); the list is read 16 entries per round with
+      // independent int4 loads.
+      int verdict = 1;  // 1 match, 0 no match, 2 unknown
+      const int4* cp = reinterpret_cast<const int4*>(A.rec_cond + r.cond_off);
+      for (int j0 = 1; j0 < r.cond_len && verdict == 1; j0 += 16) {
+        int4 q[4];
+        const int nvec = min(4, (r.cond_len - j0 + 3) >> 2);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) q[v] = v < nvec ? __ldg(cp + ((j0 - 1) >> 2) + v) : make_int4(-1, -1, -1, -1);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int j = j0 + u;
+          if (j >= r.cond_len || verdict != 1) break;
+          const int4 qq = q[u >> 2];
+          const int want = (u & 3) == 0 ? qq.x : (u & 3) == 1 ? qq.y : (u & 3) == 2 ? qq.z : qq.w;
+          int have;
+          if (j < nl) {
+            have = loc[nl - 1 - j];
+          } else if (j - nl < nb) {
+            have = base[nb - 1 - (j - nl)];
+          } else {
+            verdict = complete ? 0 : 2;  // reaches below the known stack
+            break;
+          }
+          if (have != want) verdict = 0;
         }
       }
-      if (match) {
+      if (verdict == 2) return kUnknown;  // every known entry matched so far
+      if (verdict == 1) {
         found = c;
         fr = r;
         break;
@@ -118,7 +129,16 @@ __device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const
       nl = 0;
     }
     if (nl + fr.push_len + 1 > kWalkOverlay) return kOverflow;
-    for (int j = 0; j < fr.push_len; ++j) loc[nl++] = __ldg(A.rec_push + fr.push_off + j);
+    {
+      const int4* pp = reinterpret_cast<const int4*>(A.rec_push + fr.push_off);
+      for (int j0 = 0; j0 < fr.push_len; j0 += 4) {
+        const int4 q = __ldg(pp + (j0 >> 2));
+        loc[nl++] = q.x;
+        if (j0 + 1 < fr.push_len) loc[nl++] = q.y;
+        if (j0 + 2 < fr.push_len) loc[nl++] = q.z;
+        if (j0 + 3 < fr.push_len) loc[nl++] = q.w;
+      }
+    }
     if (fr.flags & 1) {
       const int top = nl > 0 ? loc[nl - 1] : (nb > 0 ? base[nb - 1] : -1);
       if (top < 0) return complete ? kReject : kUnknown;
@@ -187,7 +207,7 @@ __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int com
     if (cur == 0) {
       unsigned long long expect = 0;
       if (slot.compare_exchange_strong(expect, h, cuda::memory_order_relaxed)) {
-        for (int j = 0; j < n; ++j) C.slot_keys[i * C.K + j] = key[j];
+        for (int j = 0; j < kMaxContext; ++j) C.slot_keys[i * kMaxContext + j] = j < n ? key[j] : -1;
         atomic_i32 meta(C.slot_meta[i]);
         meta.store(meta_want | (1 << 16), cuda::memory_order_release);
         atomicAdd(C.counters + 0, 1ull);
@@ -202,7 +222,17 @@ __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int com
     if (!(m & (1 << 16))) return -1;
     if ((m & 0xffff) != meta_want) continue;
     bool same = true;
-    for (int j = 0; j < n && same; ++j) same = __ldcg(C.slot_keys + i * C.K + j) == key[j];
+    // Whole 16-entry row in four independent loads.
+    const int4* row = reinterpret_cast<const int4*>(C.slot_keys + i * kMaxContext);
+    int4 q[kMaxContext / 4];
+#pragma unroll
+    for (int v = 0; v < kMaxContext / 4; ++v) q[v] = 4 * v < n ? __ldcg(row + v) : make_int4(-1, -1, -1, -1);
+#pragma unroll
+    for (int j = 0; j < kMaxContext; ++j) {
+      const int4 qq = q[j >> 2];
+      const int have = (j & 3) == 0 ? qq.x : (j & 3) == 1 ? qq.y : (j & 3) == 2 ? qq.z : qq.w;
+      if (j < n && have != key[j]) same = false;
+    }
     if (same) return i;
   }
   return -1;
@@ -273,7 +303,7 @@ __global__ void __launch_bounds__(kThreads) BuildKernel(AutView A, VocabView Vv,
       const int meta = __ldcg(Cc.slot_meta + slot);
       nb = meta & 0xff;
       complete = (meta >> 8) & 1;
-      for (int i = tid; i < nb; i += kThreads) base_s[i] = __ldcg(Cc.slot_keys + slot * Cc.K + (nb - 1 - i));
+      for (int i = tid; i < nb; i += kThreads) base_s[i] = __ldcg(Cc.slot_keys + slot * kMaxContext + (nb - 1 - i));
     }
     __syncthreads();
     const int t = seg * kSegTokens + chunk * kThreads + tid;
@@ -310,7 +340,7 @@ struct FillShared {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 8) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+__global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                        uint32_t* __restrict__ bitmask, long long ldw,
                                                        uint16_t* __restrict__ logits, long long ld,
                                                        int32_t* __restrict__ seg_counts,
@@ -324,22 +354,21 @@ __global__ void __launch_bounds__(kThreads, 8) FillKernel(AutView A, VocabView V
   const int t0 = w0 * 32;
   const int t1 = min(Vv.V + 1, t0 + nwords * 32);
 
-  if (tid == 0) {
-    if (seg == 0 && b == 0) *Bt.n_items = 0u;  // this step's builds are complete
-    const int slot = Bt.seq_slot[b];
-    sh.slot = slot;
-    sh.cd_cnt = (slot >= 0 && slot < Cc.C) ? Cc.cd_cnt[static_cast<long long>(slot) * Vv.nseg + seg] : 0;
-  }
-  __syncthreads();
-  const int slot = sh.slot;
-  const int cd_cnt = sh.cd_cnt;
-  unsigned long long n_walks = 0;
-  if (slot == -2) {
-    for (int w = tid; w < nwords; w += kThreads) sh.mask[w] = 0u;
-  } else {
+  static_assert(kSegWords == kThreads, "one mask word per thread");
+  if (tid == 0 && seg == 0 && b == 0) *Bt.n_items = 0u;  // this step's builds are complete
+  // Independent loads first: the structural word, then slot -> {CI word, CD count}.
+  const uint32_t sw = (seg_counts != nullptr && tid < nwords) ? __ldg(Vv.structural + w0 + tid) : 0u;
+  const int slot = Bt.seq_slot[b];  // same address in every thread: one broadcast load
+  const int cd_cnt = (slot >= 0 && slot < Cc.C) ? Cc.cd_cnt[static_cast<long long>(slot) * Vv.nseg + seg] : 0;
+  uint32_t mword = 0u;
+  if (slot != -2 && tid < nwords) {
     const uint32_t* src = slot < Cc.C ? Cc.ci + static_cast<long long>(slot) * Vv.W
                                       : Bt.priv + static_cast<long long>(slot - Cc.C) * Vv.W;
-    for (int w = tid; w < nwords; w += kThreads) sh.mask[w] = __ldcg(src + w0 + w);
+    mword = __ldcg(src + w0 + tid);
+  }
+  sh.mask[tid] = mword;
+  unsigned long long n_walks = 0;
+  {
     if (cd_cnt > 0) {
       // Context-dependent tokens: walk them against the sequence's real stack.
       const uint32_t* cdsrc = Cc.cdb + static_cast<long long>(slot) * Vv.W + w0;
@@ -378,11 +407,11 @@ __global__ void __launch_bounds__(kThreads, 8) FillKernel(AutView A, VocabView V
   if (seg_counts != nullptr) {
     const int eos_w = Vv.V >> 5;
     int ca = 0, cs = 0;
-    for (int w = tid; w < nwords; w += kThreads) {
-      uint32_t m = sh.mask[w];
-      if (w0 + w == eos_w) m &= ~(1u << (Vv.V & 31));
-      ca += __popc(m);
-      cs += __popc(m & __ldg(Vv.structural + w0 + w));
+    if (tid < nwords) {
+      uint32_t m = sh.mask[tid];
+      if (w0 + tid == eos_w) m &= ~(1u << (Vv.V & 31));
+      ca = __popc(m);
+      cs = __popc(m & sw);
     }
     ca = WarpSum(ca);
     cs = WarpSum(cs);
@@ -620,19 +649,34 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
     int depth = st.depth;
     for (int i = 0; i < nterm; ++i) {
       const int x = eos ? 256 : static_cast<int>(bytes[i]);
-      const int state = stack[depth - 1];
+      // Top 32 stack entries, lane j holding entry j (0 = top): one coalesced load.
+      const int topv = lane < depth ? stack[depth - 1 - lane] : -1;
+      const int state = __shfl_sync(0xffffffffu, topv, 0);
       const int cb = A.rec_begin[state * 257 + x];
       const int ce = A.rec_begin[state * 257 + x + 1];
       int found = -1;
       for (int c0 = cb; c0 < ce && found < 0; c0 += 32) {
         const int c = c0 + lane;
-        bool match = false;
+        CandRec r;
+        r.cond_len = 0;
+        int4 q[4];
         if (c < ce) {
-          const CandRec r = LoadRec(A.recs + c);
-          match = r.cond_len <= depth;
-          for (int j = 1; j < r.cond_len && match; ++j) {
-            match = stack[depth - 1 - j] == A.rec_cond[r.cond_off + j - 1];
-          }
+          r = LoadRec(A.recs + c);
+          const int4* cp = reinterpret_cast<const int4*>(A.rec_cond + r.cond_off);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) q[v] = 4 * v + 1 < r.cond_len ? __ldg(cp + v) : make_int4(-1, -1, -1, -1);
+        }
+        bool match = c < ce && r.cond_len <= depth;
+        // Entries 1..16 from the register window (lane-indexed shuffles).
+#pragma unroll
+        for (int j = 1; j <= 16; ++j) {
+          const int have = __shfl_sync(0xffffffffu, topv, j);
+          const int4 qq = q[(j - 1) >> 2];
+          const int want = ((j - 1) & 3) == 0 ? qq.x : ((j - 1) & 3) == 1 ? qq.y : ((j - 1) & 3) == 2 ? qq.z : qq.w;
+          if (j < r.cond_len && have != want) match = false;
+        }
+        for (int j = 17; j < r.cond_len && match; ++j) {  // long conditions: rare
+          match = stack[depth - 1 - j] == A.rec_cond[r.cond_off + j - 1];
         }
         const unsigned m = __ballot_sync(0xffffffffu, match);
         if (m) found = c0 + __ffs(m) - 1;

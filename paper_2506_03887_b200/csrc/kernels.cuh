@@ -52,7 +52,7 @@ struct VocabView {
 struct CacheView {
   unsigned long long* slot_hash;  // C; 0 = empty
   int32_t* slot_meta;             // C; n | complete << 8 | ready << 16
-  int32_t* slot_keys;             // C*K
+  int32_t* slot_keys;             // C*kMaxContext (rows padded with -1)
   uint32_t* ci;                   // C*W
   uint32_t* cdb;                  // C*W
   int32_t* cd_cnt;                // C*nseg
