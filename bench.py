@@ -225,8 +225,7 @@ def main():
     logits = [torch.randn((B, V1), dtype=torch.bfloat16, device=dev) for _ in range(R)]
 
     def step(i):
-        batch.fill(bm, logits[i % R], counts)
-        batch.sample_stream_and_accept(bm, counts, seed, toks)
+        batch.decode_step_stream(seed, bitmask=bm, logits=logits[i % R], tokens_out=toks)
 
     for i in range(args.warmup):
         step(i)
@@ -236,17 +235,15 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     K = args.steps
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(K)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         h0 = time.perf_counter()
         e0.record(stream)
         for i in range(K):
             ev[i][0].record(stream)
-            batch.fill(bm, logits[i % R], counts)
+            batch.decode_step_stream(seed, bitmask=bm, logits=logits[i % R], tokens_out=toks)
             ev[i][1].record(stream)
-            batch.sample_stream_and_accept(bm, counts, seed, toks)
-            ev[i][2].record(stream)
         e1.record(stream)
         h1 = time.perf_counter()
         torch.cuda.synchronize()
@@ -254,22 +251,20 @@ def main():
     if world > 1:
         dist.barrier()
     elapsed_ms = e0.elapsed_time(e1)
-    fill_ms = sum(a.elapsed_time(b) for a, b, _ in ev) / K
-    accept_ms = sum(b.elapsed_time(c) for _, b, c in ev) / K
+    fill_ms = sum(a.elapsed_time(b) for a, b in ev) / K
     host_ms = (h1 - h0) * 1e3 / K
-    t = torch.tensor([elapsed_ms, fill_ms, accept_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([elapsed_ms, fill_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms, fill_ms, accept_ms = float(t[0]), float(t[1]), float(t[2])
+    elapsed_ms, fill_ms = float(t[0]), float(t[1])
     value = world * B * K / (elapsed_ms / 1e3)
 
     # Device-counted logit bytes of one more fill (outside the timed region).
     batch.set_stats(True)
-    batch.fill(bm, logits[K % R], counts)
+    batch.decode_step_stream(seed, bitmask=bm, logits=logits[K % R], tokens_out=toks)
     batch.check()
     fstats = batch.fill_stats()
     batch.set_stats(False)
-    batch.sample_stream_and_accept(bm, counts, seed, toks)
 
     # ---- e2e through the public API with host buffers.
     e2e = None
@@ -339,16 +334,15 @@ def main():
         "config": dict(workload_config(args, world),
                        l2=f"rotating {R} logits buffers of {row_bytes / 2**20:.0f} MiB (> 126 MB L2)"),
         "mask_latency_us": 1e3 * fill_ms,
-        "step_breakdown_us": {"fill(lookup+build+fill+logits)": 1e3 * fill_ms,
-                              "sample+accept": 1e3 * accept_ms, "host_enqueue_per_step": 1e3 * host_ms},
+        "step_breakdown_us": {"decode_step_kernel": 1e3 * fill_ms, "host_enqueue_per_step": 1e3 * host_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "FillKernel<0> (+LookupKernel, BuildKernel)",
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "FillKernel<mask,stream-tail> (whole fused step)",
                      "alg_bytes_per_seq_step": alg_bytes_seq,
                      "device_counted_logit_bytes_per_seq_step": (fstats["logit_bytes_read"] +
                                                                  fstats["logit_bytes_written"]) / B},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 4 * K,
+        "gpu_launches": K,
         "clocks": clocks.summary(),
         "preprocessing": {"prewarm_s": t_pre, "prewarm": f"{args.prewarm_steps} steps x {args.prewarm_batch} seqs "
                           f"(seed differs from the timed streams)", "contexts_after_prewarm": pre_info["context_slots_used"]},

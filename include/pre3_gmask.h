@@ -141,6 +141,14 @@ int gm_fill_next_token_bitmask(gm_batch* b, uint32_t* bitmask, int64_t ld_words,
 int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
                             int64_t ld, int32_t* seg_counts, void* stream);
 
+/* One fused decode step in a single launch: the fill above (bitmask and
+ * logits may be NULL), then per sequence the synthetic-stream sample
+ * (DESIGN.md §5), accept (with restart of finished sequences) and the context
+ * lookup of the next step.  Equivalent to gm_fill_and_mask_logits followed by
+ * gm_sample_stream_and_accept. */
+int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
+                          int64_t ld, uint64_t seed, int32_t* tokens_out, void* stream);
+
 /* Engine::Step over every byte of tokens[b] (runtime.cpp:177-186; callers'
  * loop gmask_main.cpp:113-118); tokens[b] == V steps kEndMarker; tokens[b] < 0
  * is a no-op.  status_out (may be NULL) receives gm_seq_status per sequence.

@@ -124,6 +124,7 @@ def lib() -> ctypes.CDLL:
             "gm_accept_tokens": ([P, P, P, I32, P], ctypes.c_int),
             "gm_sample_stream_and_accept": ([P, P, I64, P, U64, P, P], ctypes.c_int),
             "gm_sample_stream": ([P, P, I64, P, U64, P, P], ctypes.c_int),
+            "gm_decode_step_stream": ([P, P, I64, P, I64, U64, P, P], ctypes.c_int),
             "gm_decode_step_greedy": ([P, P, I64, P, I64, P, P], ctypes.c_int),
             "gmw_synth_vocab": ([I32, I32, P, I64, P], I64),
             "gmw_structural_words": ([P, P, I32, P], I32),
@@ -360,6 +361,15 @@ class Batch:
     def sample_stream(self, bitmask, seg_counts, seed: int, tokens_out, stream=None):
         _check(lib().gm_sample_stream(self._h, bitmask.data_ptr(), bitmask.stride(0), seg_counts.data_ptr(), seed,
                                       tokens_out.data_ptr(), _stream(stream)))
+
+    def decode_step_stream(self, seed: int, bitmask=None, logits=None, tokens_out=None, stream=None):
+        """Fused fill + -inf logits + stream sample + accept (one launch)."""
+        bm = bitmask.data_ptr() if bitmask is not None else None
+        ldw = bitmask.stride(0) if bitmask is not None else 0
+        lg = logits.data_ptr() if logits is not None else None
+        ld = logits.stride(0) if logits is not None else 0
+        to = tokens_out.data_ptr() if tokens_out is not None else None
+        _check(lib().gm_decode_step_stream(self._h, bm, ldw, lg, ld, seed, to, _stream(stream)))
 
     def decode_step_greedy(self, logits, tokens_out=None, bitmask=None, stream=None):
         to = tokens_out.data_ptr() if tokens_out is not None else None

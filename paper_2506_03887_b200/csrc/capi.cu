@@ -77,29 +77,36 @@ struct gm_engine {
   }
 };
 
+// Host bookkeeping of the two build queues.  Lookups (fused into accepts or
+// the fill's tail, or LookupKernel) feed queue[prod]; the next fill drains
+// queue[prod].  At most two lookup passes reach a queue before it is drained
+// (capacity 2*B*nseg items).
 struct gm_batch {
   gm_engine* engine = nullptr;
   pre3::BatchView view{};
   int32_t* seg_counts = nullptr;          // internal scratch for fused decode
+  uint32_t* scratch_mask = nullptr;       // internal bitmask when the caller passes none
   unsigned long long* best = nullptr;     // greedy argmax packed keys
-  bool slots_valid = false;               // seq_slot matches the stacks (set by accept)
-  bool lookup_pending = false;            // builds queued by an accept, not yet consumed by a fill
+  int prod = 0;                           // queue the next fill drains
+  bool slots_valid = false;               // seq_slot matches the stacks
+  bool lookup_pending = false;            // queue[prod] got a lookup pass since the last fill
 
-  // Accept flags: bit0 accept; bit1 assign context slots, at most once per
-  // fill so the build queue (2*B*nseg items) cannot overflow.
-  int AcceptFlags() {
-    const int flags = lookup_pending ? 1 : 3;
-    slots_valid = !lookup_pending;
+  // Queue for an accept's fused lookup, or -1 (then the next fill looks up).
+  int AcceptLookupQueue() {
+    if (lookup_pending) {
+      slots_valid = false;
+      return -1;
+    }
     lookup_pending = true;
-    return flags;
-  }
-  void FillDone() {
     slots_valid = true;
-    lookup_pending = false;
+    return prod;
   }
   std::vector<void*> owned;
   ~gm_batch() {
     cudaSetDevice(engine->device);
+    // Builds still queued belong to contexts other batches may already use.
+    for (int q = 0; q < 2; ++q) pre3::LaunchDrain(engine->aut, engine->vocab, engine->cache, view, q, nullptr);
+    cudaDeviceSynchronize();
     for (void* p : owned) cudaFree(p);
   }
 };
@@ -247,10 +254,12 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.ci = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
     c.cdb = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
     c.cd_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
+    c.seg_done = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.counters = DevAlloc<unsigned long long>(8, &e->owned);
     Check(cudaMemset(c.slot_hash, 0, C * 8), "memset");
     Check(cudaMemset(c.slot_meta, 0, C * 4), "memset");
     Check(cudaMemset(c.cd_cnt, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
+    Check(cudaMemset(c.seg_done, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
     Check(cudaMemset(c.counters, 0, 64), "memset");
     Check(cudaDeviceSynchronize(), "engine upload");
     *out = e.release();
@@ -310,15 +319,28 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.stats = DevAlloc<unsigned long long>(8, &b->owned);
     v.counters = DevAlloc<unsigned long long>(4, &b->owned);
     v.stats_enabled = 0;
+    const size_t bn = static_cast<size_t>(std::max(batch, 1)) * static_cast<size_t>(e->nseg);
+    v.nseg = e->nseg;
     v.seq_slot = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
     v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
-    v.items = DevAlloc<int4>(2 * static_cast<size_t>(batch) * static_cast<size_t>(e->nseg), &b->owned);
-    v.n_items = DevAlloc<unsigned int>(1, &b->owned);
-    Check(cudaMemset(v.n_items, 0, 4), "memset");
+    v.priv_done = DevAlloc<int32_t>(bn, &b->owned);
+    Check(cudaMemset(v.priv_done, 0, bn * 4), "memset");
+    for (int q = 0; q < 2; ++q) {
+      v.queue[q].items = DevAlloc<int4>(2 * bn, &b->owned);
+      v.queue[q].n_items = DevAlloc<unsigned int>(1, &b->owned);
+      v.queue[q].next_unit = DevAlloc<unsigned int>(1, &b->owned);
+      Check(cudaMemset(v.queue[q].n_items, 0, 4), "memset");
+      Check(cudaMemset(v.queue[q].next_unit, 0, 4), "memset");
+    }
+    v.seq_arrive = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
+    Check(cudaMemset(v.seq_arrive, 0, static_cast<size_t>(batch) * 4), "memset");
+    v.kernel_done = DevAlloc<unsigned int>(1, &b->owned);
+    Check(cudaMemset(v.kernel_done, 0, 4), "memset");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
     v.build_grid = sms * 4;
-    b->seg_counts = DevAlloc<int32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->nseg) * 2, &b->owned);
+    b->seg_counts = DevAlloc<int32_t>(bn * 2, &b->owned);
+    b->scratch_mask = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     b->best = DevAlloc<unsigned long long>(static_cast<size_t>(batch), &b->owned);
     Check(cudaMemset(v.err, 0, 4), "memset");
     Check(cudaMemset(v.stats, 0, 64), "memset");
@@ -446,10 +468,52 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
-    Check(pre3::LaunchFill(pre3::kFillMask, e->aut, e->vocab, e->cache, b->view, bitmask, ld_words, logits, ld,
-                           seg_counts, nullptr, !b->slots_valid, static_cast<cudaStream_t>(stream)),
-          "fill launch");
-    b->FillDone();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, s), "lookup launch");
+    pre3::FillArgs f{};
+    f.bitmask = bitmask;
+    f.ldw = ld_words;
+    f.logits = logits;
+    f.ld = ld;
+    f.seg_counts = seg_counts;
+    f.best = b->best;
+    f.consume = b->prod;
+    f.produce = 1 - b->prod;
+    Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s), "fill launch");
+    b->slots_valid = true;
+    b->lookup_pending = false;
+    return GM_OK;
+  });
+}
+
+// One fused decode step: fill + in-place bf16 -inf logits + stream sample +
+// accept + next-step context lookup, in a single launch.
+int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits, int64_t ld,
+                          uint64_t seed, int32_t* tokens_out, void* stream) {
+  return Guard([&]() -> int {
+    if (!b) return Fail(GM_ERR_USAGE, "null batch");
+    gm_engine* e = b->engine;
+    if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
+    if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, s), "lookup launch");
+    pre3::FillArgs f{};
+    f.bitmask = bitmask ? bitmask : b->scratch_mask;
+    f.ldw = bitmask ? ld_words : e->W;
+    f.logits = logits;
+    f.ld = ld;
+    f.seg_counts = b->seg_counts;
+    f.best = b->best;
+    f.tokens_out = tokens_out;
+    f.seed = seed;
+    f.consume = b->prod;
+    f.produce = 1 - b->prod;
+    Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailStream, e->aut, e->vocab, e->cache, b->view, f, s),
+          "decode launch");
+    b->prod = 1 - b->prod;
+    b->slots_valid = true;
+    b->lookup_pending = true;
     return GM_OK;
   });
 }
@@ -460,8 +524,14 @@ int gm_accept_tokens(gm_batch* b, const int32_t* tokens, int32_t* status_out, in
     if (!b || !tokens) return Fail(GM_ERR_USAGE, "null argument");
     gm_engine* e = b->engine;
     Check(cudaSetDevice(e->device), "cudaSetDevice");
-    Check(pre3::LaunchAccept(pre3::kSampleGiven, e->aut, e->vocab, e->cache, b->view, tokens, status_out, restart, nullptr,
-                             0, nullptr, 0, nullptr, nullptr, b->AcceptFlags(), static_cast<cudaStream_t>(stream)),
+    pre3::AcceptArgs g{};
+    g.tokens = tokens;
+    g.status_out = status_out;
+    g.restart = restart;
+    g.do_accept = 1;
+    g.lookup_queue = b->AcceptLookupQueue();
+    Check(pre3::LaunchAccept(pre3::kSampleGiven, e->aut, e->vocab, e->cache, b->view, g,
+                             static_cast<cudaStream_t>(stream)),
           "accept launch");
     return GM_OK;
   });
@@ -475,8 +545,16 @@ int gm_sample_stream_and_accept(gm_batch* b, const uint32_t* bitmask, int64_t ld
     gm_engine* e = b->engine;
     if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
-    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, nullptr, nullptr, 1, bitmask,
-                             ld_words, seg_counts, seed, nullptr, tokens_out, b->AcceptFlags(),
+    pre3::AcceptArgs g{};
+    g.restart = 1;
+    g.bitmask = bitmask;
+    g.ldw = ld_words;
+    g.seg_counts = seg_counts;
+    g.seed = seed;
+    g.tokens_out = tokens_out;
+    g.do_accept = 1;
+    g.lookup_queue = b->AcceptLookupQueue();
+    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, g,
                              static_cast<cudaStream_t>(stream)),
           "sample launch");
     return GM_OK;
@@ -490,8 +568,16 @@ int gm_sample_stream(gm_batch* b, const uint32_t* bitmask, int64_t ld_words, con
     gm_engine* e = b->engine;
     if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
-    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, nullptr, nullptr, 0, bitmask,
-                             ld_words, seg_counts, seed, nullptr, tokens_out, 0, static_cast<cudaStream_t>(stream)),
+    pre3::AcceptArgs g{};
+    g.bitmask = bitmask;
+    g.ldw = ld_words;
+    g.seg_counts = seg_counts;
+    g.seed = seed;
+    g.tokens_out = tokens_out;
+    g.do_accept = 0;
+    g.lookup_queue = -1;
+    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, g,
+                             static_cast<cudaStream_t>(stream)),
           "sample launch");
     return GM_OK;
   });
@@ -506,13 +592,21 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Check(pre3::LaunchFill(pre3::kFillGreedy, e->aut, e->vocab, e->cache, b->view, bitmask, ld_words,
-                           const_cast<uint16_t*>(logits), ld, nullptr, b->best, !b->slots_valid, s),
-          "greedy fill launch");
-    b->FillDone();
-    Check(pre3::LaunchAccept(pre3::kSampleGreedy, e->aut, e->vocab, e->cache, b->view, nullptr, nullptr, 1, nullptr, 0,
-                             nullptr, 0, b->best, tokens_out, b->AcceptFlags(), s),
-          "greedy accept launch");
+    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, s), "lookup launch");
+    pre3::FillArgs f{};
+    f.bitmask = bitmask ? bitmask : b->scratch_mask;
+    f.ldw = bitmask ? ld_words : e->W;
+    f.logits = const_cast<uint16_t*>(logits);
+    f.ld = ld;
+    f.best = b->best;
+    f.tokens_out = tokens_out;
+    f.consume = b->prod;
+    f.produce = 1 - b->prod;
+    Check(pre3::LaunchFill(pre3::kFillGreedy, pre3::kTailGreedy, e->aut, e->vocab, e->cache, b->view, f, s),
+          "greedy decode launch");
+    b->prod = 1 - b->prod;
+    b->slots_valid = true;
+    b->lookup_pending = true;
     return GM_OK;
   });
 }
@@ -524,10 +618,8 @@ int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed,
     int rc = gm_batch_create(e, batch, 1024, &b);
     if (rc != GM_OK) return rc;
     std::unique_ptr<gm_batch> guard(b);
-    uint32_t* bm = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     for (int32_t s = 0; s < steps; ++s) {
-      if ((rc = gm_fill_and_mask_logits(b, bm, e->W, nullptr, 0, b->seg_counts, stream)) != GM_OK) return rc;
-      if ((rc = gm_sample_stream_and_accept(b, bm, e->W, b->seg_counts, seed, nullptr, stream)) != GM_OK) return rc;
+      if ((rc = gm_decode_step_stream(b, nullptr, 0, nullptr, 0, seed, nullptr, stream)) != GM_OK) return rc;
     }
     return gm_batch_check(b, stream);
   });

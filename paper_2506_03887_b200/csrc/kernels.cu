@@ -1,22 +1,21 @@
 // kernels.cu — sm_100a kernels of the constrained-decoding hot path.
 //
-// One mask fill (Engine::ComputeMask, runtime.cpp:261-287, for a batch) is
-// three launches on one stream:
-//   LookupKernel  thread per sequence: key = top-K stack entries; find or
-//                 insert its context slot; a new slot queues one build item
-//                 per vocab segment (table full -> a private, uncached row).
-//   BuildKernel   fixed grid, CTA per (item, 256-token chunk): classifies
-//                 tokens against the key — accept / reject / context-
-//                 dependent (the walk reached below the key) — into the
-//                 slot's CI and CD bitsets.  Exits at once when nothing is
-//                 queued (the steady state).
-//   FillKernel    CTA per (segment, sequence): streams the CI bits, walks
-//                 only the CD tokens against the real stack, writes the
-//                 32-bit mask words and, fused, the bf16 -inf logits (or the
-//                 greedy argmax).
-// AcceptKernel: Engine::Step over a token's bytes (runtime.cpp:177-186), one
-// warp per sequence, lanes testing candidate edges in arbitration order
-// (FindEdge, runtime.cpp:138-146) with __ballot_sync; optional fused sampler.
+// A decode step is ONE launch of FillKernel (grid: vocab segment x sequence):
+//   1. help build: CTAs first drain the build queue produced by the previous
+//      step's lookups — each unit classifies 256 tokens against a new context
+//      key (accept / reject / context-dependent) into the slot's CI and CD
+//      bitsets.  Empty in the steady state.
+//   2. fill: CTA (seg, b) streams its 256 CI words, walks only the CD tokens
+//      against the sequence's real stack (Engine::ComputeMask,
+//      runtime.cpp:261-287), writes the 32-bit mask words and, fused, the
+//      bf16 -inf logits (or a greedy argmax partial).
+//   3. tail: the last CTA to finish a sequence samples its token (synthetic
+//      stream or greedy), accepts it — Engine::Step per byte
+//      (runtime.cpp:177-186), one warp, lanes over candidate edges in
+//      arbitration order (FindEdge, runtime.cpp:138-146) — and looks up the
+//      context slot of the next step, queueing builds for new contexts.
+// The same pieces run standalone for the reference-shaped API
+// (LookupKernel, AcceptKernel, FillKernel without a tail).
 //
 // Integer/bit work only: no tensor cores (nothing here is a contraction).
 #include <cuda/atomic>
@@ -55,6 +54,10 @@ __device__ __forceinline__ CandRec LoadRec(const CandRec* p) {
   return r;
 }
 
+__device__ __forceinline__ int Lane4(const int4& q, int i) {
+  return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w;
+}
+
 // ---------------------------------------------------------------------------
 // One token walk: the body of ComputeMaskNaive's per-token replay
 // (runtime.cpp:289-307) — Step per byte with FindEdge's first match in
@@ -65,8 +68,8 @@ __device__ __forceinline__ CandRec LoadRec(const CandRec* p) {
 // dynamic target read from below it, makes the outcome kUnknown.  Because
 // arbitration is first-match, an unknown earlier candidate is also unknown.
 // ---------------------------------------------------------------------------
-__device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
-                         bool complete, const uint32_t* any) {
+__device__ __noinline__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
+                         bool complete) {
   int32_t loc[kWalkOverlay];
   int nl = 0;
   const bool eos = t == Vv.V;
@@ -76,7 +79,7 @@ __device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const
   int state = base[nb - 1];
   for (int i = 0; i < nterm; ++i) {
     const int x = eos ? 256 : static_cast<int>(__ldg(bytes + i));
-    if (!((any[state * 9 + (x >> 5)] >> (x & 31)) & 1u)) return kReject;
+    if (!((__ldg(A.state_any + state * 9 + (x >> 5)) >> (x & 31)) & 1u)) return kReject;
     const int cb = __ldg(A.rec_begin + state * 257 + x);
     const int ce = __ldg(A.rec_begin + state * 257 + x + 1);
     int found = -1;
@@ -97,8 +100,7 @@ __device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const
         for (int u = 0; u < 16; ++u) {
           const int j = j0 + u;
           if (j >= r.cond_len || verdict != 1) break;
-          const int4 qq = q[u >> 2];
-          const int want = (u & 3) == 0 ? qq.x : (u & 3) == 1 ? qq.y : (u & 3) == 2 ? qq.z : qq.w;
+          const int want = Lane4(q[u >> 2], u & 3);
           int have;
           if (j < nl) {
             have = loc[nl - 1 - j];
@@ -129,15 +131,13 @@ __device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const
       nl = 0;
     }
     if (nl + fr.push_len + 1 > kWalkOverlay) return kOverflow;
-    {
-      const int4* pp = reinterpret_cast<const int4*>(A.rec_push + fr.push_off);
-      for (int j0 = 0; j0 < fr.push_len; j0 += 4) {
-        const int4 q = __ldg(pp + (j0 >> 2));
-        loc[nl++] = q.x;
-        if (j0 + 1 < fr.push_len) loc[nl++] = q.y;
-        if (j0 + 2 < fr.push_len) loc[nl++] = q.z;
-        if (j0 + 3 < fr.push_len) loc[nl++] = q.w;
-      }
+    const int4* pp = reinterpret_cast<const int4*>(A.rec_push + fr.push_off);
+    for (int j0 = 0; j0 < fr.push_len; j0 += 4) {
+      const int4 q = __ldg(pp + (j0 >> 2));
+      loc[nl++] = q.x;
+      if (j0 + 1 < fr.push_len) loc[nl++] = q.y;
+      if (j0 + 2 < fr.push_len) loc[nl++] = q.z;
+      if (j0 + 3 < fr.push_len) loc[nl++] = q.w;
     }
     if (fr.flags & 1) {
       const int top = nl > 0 ? loc[nl - 1] : (nb > 0 ? base[nb - 1] : -1);
@@ -158,25 +158,24 @@ __device__ __forceinline__ int WarpSum(int v) {
   return v;
 }
 
+__device__ __forceinline__ int WarpInclusiveScan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
 // Block-wide exclusive scan of one int per thread (blockDim == kThreads).
 __device__ int BlockExclusiveScan(int v, int* scratch, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
+  const int inc = WarpInclusiveScan(v, lane);
   if (lane == 31) scratch[warp] = inc;
   __syncthreads();
   if (warp == 0) {
     const int w = lane < kThreads / 32 ? scratch[lane] : 0;
-    int winc = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, winc, o);
-      if (lane >= o) winc += y;
-    }
+    const int winc = WarpInclusiveScan(w, lane);
     if (lane < kThreads / 32) scratch[lane] = winc - w;
     if (lane == kThreads / 32 - 1) scratch[kThreads / 32] = winc;
   }
@@ -195,7 +194,7 @@ __device__ unsigned long long KeyHash(const int32_t* key, int n, int complete) {
 
 // Finds or inserts the slot of a key.  Returns the slot (created = true when
 // this thread inserted it) or -1 (table full, or the key is being published
-// by another thread of this same launch).
+// by another thread right now).
 __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int complete, bool* created) {
   const unsigned long long h = KeyHash(key, n, complete);
   const int meta_want = n | (complete << 8);
@@ -221,31 +220,26 @@ __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int com
     const int m = meta.load(cuda::memory_order_acquire);
     if (!(m & (1 << 16))) return -1;
     if ((m & 0xffff) != meta_want) continue;
-    bool same = true;
     // Whole 16-entry row in four independent loads.
     const int4* row = reinterpret_cast<const int4*>(C.slot_keys + i * kMaxContext);
     int4 q[kMaxContext / 4];
 #pragma unroll
     for (int v = 0; v < kMaxContext / 4; ++v) q[v] = 4 * v < n ? __ldcg(row + v) : make_int4(-1, -1, -1, -1);
+    bool same = true;
 #pragma unroll
     for (int j = 0; j < kMaxContext; ++j) {
-      const int4 qq = q[j >> 2];
-      const int have = (j & 3) == 0 ? qq.x : (j & 3) == 1 ? qq.y : (j & 3) == 2 ? qq.z : qq.w;
-      if (j < n && have != key[j]) same = false;
+      if (j < n && Lane4(q[j >> 2], j & 3) != key[j]) same = false;
     }
     if (same) return i;
   }
   return -1;
 }
 
-}  // namespace
-
-// ---------------------------------------------------------------------------
-// Context slot of sequence b for the next fill (seq_slot[b]); queues the
-// build of a new slot.  Used by LookupKernel and, fused, by AcceptKernel.
+// Context slot of sequence b for the next fill (seq_slot[b]); a new shared
+// slot or a private row queues one build item per segment into `q`.
 // `key` = the top min(depth, K) stack entries, top first.
-__device__ void AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int b, const SeqState& st, int nseg,
-                              const int32_t* key) {
+__device__ void AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, int b, const SeqState& st,
+                              int nseg, const int32_t* key) {
   if (st.status != kAlive) {
     Bt.seq_slot[b] = -2;
     return;
@@ -257,18 +251,268 @@ __device__ void AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int b, c
   if (slot < 0 || created) {
     if (slot < 0) {
       slot = Cc.C + b;
+      for (int s = 0; s < nseg; ++s) Bt.priv_done[static_cast<long long>(b) * nseg + s] = 0;
       atomicAdd(Cc.counters + 2, 1ull);
     } else {
-      for (int s = 0; s < nseg; ++s) Cc.cd_cnt[static_cast<long long>(slot) * nseg + s] = 0;
+      for (int s = 0; s < nseg; ++s) {
+        Cc.cd_cnt[static_cast<long long>(slot) * nseg + s] = 0;
+        Cc.seg_done[static_cast<long long>(slot) * nseg + s] = 0;
+      }
       atomicAdd(Cc.counters + 1, static_cast<unsigned long long>(nseg));
     }
-    const unsigned int at = atomicAdd(Bt.n_items, static_cast<unsigned int>(nseg));
-    for (int s = 0; s < nseg; ++s) Bt.items[at + s] = make_int4(slot, s, b, 0);
+    __threadfence();  // zeroed counters visible before the items
+    const unsigned int at = atomicAdd(Bt.queue[q].n_items, static_cast<unsigned int>(nseg));
+    for (int s = 0; s < nseg; ++s) Bt.queue[q].items[at + s] = make_int4(slot, s, b, 0);
   }
   Bt.seq_slot[b] = slot;
 }
 
-__global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, int nseg) {
+// ---------------------------------------------------------------------------
+// Build unit: 256 tokens of one (slot, segment) item, one per thread.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt,
+                          const int4 it, int chunk, int32_t* base_s) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot = it.x, seg = it.y, b = it.z;
+  const bool priv = slot >= Cc.C;
+  int nb;
+  bool complete;
+  __syncthreads();  // base_s reuse
+  if (priv) {
+    // Private row: the sequence's whole current stack (always complete).
+    nb = Bt.seq[b].depth;
+    complete = true;
+    const int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+    for (int i = tid; i < nb; i += kThreads) base_s[i] = stack[i];
+  } else {
+    // Shared slot: its stored key (top first), independent of any stack.
+    const int meta = __ldcg(Cc.slot_meta + slot);
+    nb = meta & 0xff;
+    complete = (meta >> 8) & 1;
+    for (int i = tid; i < nb; i += kThreads) base_s[i] = __ldcg(Cc.slot_keys + slot * kMaxContext + (nb - 1 - i));
+  }
+  __syncthreads();
+  const int t = seg * kSegTokens + chunk * kThreads + tid;
+  int r = kReject;
+  if (t <= Vv.V) r = WalkToken(A, Vv, t, base_s, nb, complete);
+  const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
+  const unsigned cd = __ballot_sync(0xffffffffu, r == kUnknown);
+  if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(Bt.err, 1u);
+  const int w = seg * kSegWords + chunk * (kThreads / 32) + warp;
+  if (lane == 0 && w < Vv.W) {
+    if (priv) {
+      Bt.priv[static_cast<long long>(slot - Cc.C) * Vv.W + w] = acc;
+    } else {
+      Cc.ci[static_cast<long long>(slot) * Vv.W + w] = acc;
+      Cc.cdb[static_cast<long long>(slot) * Vv.W + w] = cd;
+      if (cd) atomicAdd(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg, __popc(cd));
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    int* done = priv ? Bt.priv_done + static_cast<long long>(b) * Vv.nseg + seg
+                     : Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg;
+    atomicAdd(done, 1);
+  }
+}
+
+// Drains build queue q (CTA-cooperative).  Items were appended by earlier
+// launches, so the count is final here.
+__device__ void HelpBuild(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int q,
+                          int32_t* base_s, int* sh_unit) {
+  const unsigned int n_items = *reinterpret_cast<volatile unsigned int*>(Bt.queue[q].n_items);
+  if (n_items == 0) return;
+  const unsigned int units = n_items * kChunksPerSeg;
+  for (;;) {
+    if (threadIdx.x == 0) *sh_unit = static_cast<int>(atomicAdd(Bt.queue[q].next_unit, 1u));
+    __syncthreads();
+    const unsigned int u = static_cast<unsigned int>(*sh_unit);
+    __syncthreads();
+    if (u >= units) break;
+    BuildUnit(A, Vv, Cc, Bt, Bt.queue[q].items[u / kChunksPerSeg], static_cast<int>(u % kChunksPerSeg), base_s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-level sampler + accept (+ lookup) of one sequence.
+// ---------------------------------------------------------------------------
+// Synthetic stream; identical rule in oracle/gmask_port.c.
+__device__ __noinline__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row, const int32_t* counts,
+                                unsigned long long seed, uint32_t draw, int lane) {
+  int na = 0, ns = 0;
+  for (int s = lane; s < Vv.nseg; s += 32) {
+    na += __ldcg(counts + 2 * s);
+    ns += __ldcg(counts + 2 * s + 1);
+  }
+  na = WarpSum(na);
+  ns = WarpSum(ns);
+  const bool eos = (__ldcg(row + (Vv.V >> 5)) >> (Vv.V & 31)) & 1u;
+  const unsigned long long u =
+      Mix64(Mix64(seed ^ (static_cast<unsigned long long>(b) * 0xD1B54A32D192ED03ull)) ^
+            static_cast<unsigned long long>(draw));
+  if (na == 0) return eos ? Vv.V : -1;
+  if (eos && ((u >> 32) & 3ull) != 0) return Vv.V;
+  const bool use_s = ((u >> 34) & 1ull) && ns > 0;
+  const uint32_t nsel = static_cast<uint32_t>(use_s ? ns : na);
+  uint32_t r = static_cast<uint32_t>((static_cast<unsigned long long>(static_cast<uint32_t>(u)) * nsel) >> 32);
+  // Segment holding the r-th selected token: warp prefix sum over the
+  // per-segment counts, 32 segments per round.
+  int seg = -1;
+  for (int s0 = 0; s0 < Vv.nseg && seg < 0; s0 += 32) {
+    const int s = s0 + lane;
+    const int c = s < Vv.nseg ? __ldcg(counts + 2 * s + (use_s ? 1 : 0)) : 0;
+    const int inc = WarpInclusiveScan(c, lane);
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    if (r < static_cast<uint32_t>(total)) {
+      const int src = __ffs(__ballot_sync(0xffffffffu, static_cast<uint32_t>(inc) > r)) - 1;
+      seg = s0 + src;
+      r -= static_cast<uint32_t>(__shfl_sync(0xffffffffu, inc - c, src));
+    } else {
+      r -= static_cast<uint32_t>(total);
+    }
+  }
+  if (seg < 0) return -1;
+  const int w0 = seg * kSegWords;
+  const int w1 = min(Vv.W, w0 + kSegWords);
+  // All of the segment's words are loaded up front (independent loads).
+  uint32_t xs[kSegWords / 32];
+#pragma unroll
+  for (int j = 0; j < kSegWords / 32; ++j) {
+    const int w = w0 + j * 32 + lane;
+    uint32_t x = 0;
+    if (w < w1) {
+      x = __ldcg(row + w);
+      if (w == (Vv.V >> 5)) x &= ~(1u << (Vv.V & 31));
+      if (use_s) x &= __ldg(Vv.structural + w);
+    }
+    xs[j] = x;
+  }
+#pragma unroll
+  for (int j = 0; j < kSegWords / 32; ++j) {
+    const int c = __popc(xs[j]);
+    const int inc = WarpInclusiveScan(c, lane);
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    if (r < static_cast<uint32_t>(total)) {
+      const int src = __ffs(__ballot_sync(0xffffffffu, static_cast<uint32_t>(inc) > r)) - 1;
+      int tok = -1;
+      if (lane == src) {
+        uint32_t x = xs[j];
+        for (uint32_t rr = r - static_cast<uint32_t>(inc - c); rr > 0; --rr) x &= x - 1;
+        tok = (w0 + j * 32 + lane) * 32 + __ffs(x) - 1;
+      }
+      return __shfl_sync(0xffffffffu, tok, src);
+    }
+    r -= static_cast<uint32_t>(total);
+  }
+  return -1;
+}
+
+// Engine::Step over the bytes of `tok` (EOS = V) on the device stack; then
+// optional restart and (do_lookup) the context slot of the next fill.
+__device__ __noinline__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int b,
+                           SeqState st, int tok, int32_t* status_out, int restart, int lookup_queue, int lane) {
+  int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+  if (tok >= 0 && st.status == kAlive) {
+    const bool eos = tok == Vv.V;
+    const int off = eos ? 0 : __ldg(Vv.tok_off + tok);
+    const int nterm = eos ? 1 : __ldg(Vv.tok_off + tok + 1) - off;
+    const uint8_t* bytes = Vv.tok_bytes + off;
+    int depth = st.depth;
+    // Top 32 stack entries, lane j holding entry j (0 = top): one coalesced load.
+    int topv = lane < depth ? stack[depth - 1 - lane] : -1;
+    for (int i = 0; i < nterm; ++i) {
+      const int x = eos ? 256 : static_cast<int>(__ldg(bytes + i));
+      const int state = __shfl_sync(0xffffffffu, topv, 0);
+      const int cb = __ldg(A.rec_begin + state * 257 + x);
+      const int ce = __ldg(A.rec_begin + state * 257 + x + 1);
+      int found = -1;
+      CandRec fr;
+      for (int c0 = cb; c0 < ce && found < 0; c0 += 32) {
+        const int c = c0 + lane;
+        CandRec r;
+        r.cond_len = 0;
+        int4 q[4];
+        if (c < ce) {
+          r = LoadRec(A.recs + c);
+          const int4* cp = reinterpret_cast<const int4*>(A.rec_cond + r.cond_off);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) q[v] = 4 * v + 1 < r.cond_len ? __ldg(cp + v) : make_int4(-1, -1, -1, -1);
+        }
+        bool match = c < ce && r.cond_len <= depth;
+        // Entries 1..16 from the register window (lane-indexed shuffles).
+#pragma unroll
+        for (int j = 1; j <= 16; ++j) {
+          const int have = __shfl_sync(0xffffffffu, topv, j);
+          if (j < r.cond_len && have != Lane4(q[(j - 1) >> 2], (j - 1) & 3)) match = false;
+        }
+        for (int j = 17; j < r.cond_len && match; ++j) {  // long conditions: rare
+          match = stack[depth - 1 - j] == __ldg(A.rec_cond + r.cond_off + j - 1);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, match);
+        if (m) {
+          const int src = __ffs(m) - 1;
+          found = c0 + src;
+        }
+      }
+      if (found < 0) {
+        st.status = kDead;  // earlier bytes stay applied (runtime.cpp:179-183)
+        break;
+      }
+      fr = LoadRec(A.recs + found);
+      const int dyn = fr.flags & 1;
+      const int nd = depth - fr.cond_len + fr.push_len + dyn;
+      const int base = depth - fr.cond_len;
+      if (nd > Bt.cap) {
+        st.status = kStackOverflow;
+        break;
+      }
+      if (dyn && base + fr.push_len == 0) {
+        st.status = kDead;  // no exposed top: unreachable for validated automata
+        break;
+      }
+      for (int j = lane; j < fr.push_len; j += 32) stack[base + j] = __ldg(A.rec_push + fr.push_off + j);
+      __syncwarp();
+      if (dyn && lane == 0) {
+        const int top = stack[base + fr.push_len - 1];
+        stack[base + fr.push_len] = __ldg(A.shift + top * 256 + x);
+      }
+      __syncwarp();
+      depth = nd;
+      if (eos) st.status = kAccepted;
+      if (i + 1 < nterm) topv = lane < depth ? stack[depth - 1 - lane] : -1;
+    }
+    st.depth = depth;
+  }
+  if (status_out != nullptr && lane == 0) status_out[b] = st.status;
+  if (restart && st.status != kAlive) {
+    if (lane == 0) {
+      stack[0] = A.initial;
+      atomicAdd(Bt.counters + 0, 1ull);
+    }
+    st.depth = 1;
+    st.status = kAlive;
+  }
+  __syncwarp();
+  // Key of the next fill's context: lane i loads entry i, lane 0 gathers.
+  int32_t key[kMaxContext];
+  if (lookup_queue >= 0) {
+    const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
+    const int32_t kv = lane < n ? stack[st.depth - 1 - lane] : 0;
+#pragma unroll
+    for (int i = 0; i < kMaxContext; ++i) key[i] = __shfl_sync(0xffffffffu, kv, i);
+  }
+  if (lane == 0) {
+    Bt.seq[b] = st;
+    atomicAdd(Bt.counters + 3, 1ull);
+    if (lookup_queue >= 0) AssignSlotKey(Cc, Bt, lookup_queue, b, st, Vv.nseg, key);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, int q) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= Bt.B) return;
   const SeqState st = Bt.seq[b];
@@ -276,56 +520,20 @@ __global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, 
   int32_t key[kMaxContext];
   const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
   for (int i = 0; i < n; ++i) key[i] = stack[st.depth - 1 - i];
-  AssignSlotKey(Cc, Bt, b, st, nseg, key);
+  AssignSlotKey(Cc, Bt, q, b, st, Bt.nseg, key);
 }
 
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) BuildKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt) {
+// Builds everything queued in q, then empties q (used when a batch goes away
+// or before a standalone fill should not pay for builds).
+__global__ void __launch_bounds__(kThreads) DrainKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt, int q) {
   extern __shared__ int32_t base_s[];
-  const unsigned int n_items = *reinterpret_cast<volatile unsigned int*>(Bt.n_items);
-  const long long units = static_cast<long long>(n_items) * kChunksPerSeg;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-    const int4 it = Bt.items[u / kChunksPerSeg];
-    const int chunk = static_cast<int>(u % kChunksPerSeg);
-    const int slot = it.x, seg = it.y, b = it.z;
-    const bool priv = slot >= Cc.C;
-    int nb;
-    bool complete;
-    if (priv) {
-      // Private row: the sequence's whole current stack (always complete).
-      nb = Bt.seq[b].depth;
-      complete = true;
-      const int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
-      for (int i = tid; i < nb; i += kThreads) base_s[i] = stack[i];
-    } else {
-      // Shared slot: its stored key (top first), independent of any stack.
-      const int meta = __ldcg(Cc.slot_meta + slot);
-      nb = meta & 0xff;
-      complete = (meta >> 8) & 1;
-      for (int i = tid; i < nb; i += kThreads) base_s[i] = __ldcg(Cc.slot_keys + slot * kMaxContext + (nb - 1 - i));
-    }
-    __syncthreads();
-    const int t = seg * kSegTokens + chunk * kThreads + tid;
-    int r = kReject;
-    if (t <= Vv.V) r = WalkToken(A, Vv, t, base_s, nb, complete, A.state_any);
-    const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
-    const unsigned cd = __ballot_sync(0xffffffffu, r == kUnknown);
-    if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(Bt.err, 1u);
-    const int w = seg * kSegWords + chunk * (kThreads / 32) + warp;
-    if (lane == 0 && w < Vv.W) {
-      if (priv) {
-        Bt.priv[static_cast<long long>(slot - Cc.C) * Vv.W + w] = acc;
-      } else {
-        Cc.ci[static_cast<long long>(slot) * Vv.W + w] = acc;
-        Cc.cdb[static_cast<long long>(slot) * Vv.W + w] = cd;
-        if (cd) atomicAdd(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg, __popc(cd));
-      }
-    }
-    __syncthreads();
-  }
-  if (Bt.stats_enabled && blockIdx.x == 0 && tid == 0) {
-    atomicAdd(Bt.stats + 3, static_cast<unsigned long long>(n_items));
+  __shared__ int unit;
+  HelpBuild(A, Vv, Cc, Bt, q, base_s, &unit);
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(Bt.kernel_done, 1u) == gridDim.x - 1) {
+    *Bt.queue[q].n_items = 0u;
+    *Bt.queue[q].next_unit = 0u;
+    *Bt.kernel_done = 0u;
   }
 }
 
@@ -336,15 +544,12 @@ struct FillShared {
   int pre[kSegWords];
   int scratch[kThreads / 32 + 1];
   unsigned long long best[kThreads / 32];
-  int slot, cd_cnt;
+  int unit, last;
 };
 
-template <int MODE>
+template <int MODE, int TAIL>
 __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
-                                                       uint32_t* __restrict__ bitmask, long long ldw,
-                                                       uint16_t* __restrict__ logits, long long ld,
-                                                       int32_t* __restrict__ seg_counts,
-                                                       unsigned long long* __restrict__ best, int vec_ok) {
+                                                          FillArgs F) {
   __shared__ FillShared sh;
   extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -353,63 +558,97 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
   const int nwords = min(Vv.W - w0, kSegWords);
   const int t0 = w0 * 32;
   const int t1 = min(Vv.V + 1, t0 + nwords * 32);
-
   static_assert(kSegWords == kThreads, "one mask word per thread");
-  if (tid == 0 && seg == 0 && b == 0) *Bt.n_items = 0u;  // this step's builds are complete
-  // Independent loads first: the structural word, then slot -> {CI word, CD count}.
-  const uint32_t sw = (seg_counts != nullptr && tid < nwords) ? __ldg(Vv.structural + w0 + tid) : 0u;
-  const int slot = Bt.seq_slot[b];  // same address in every thread: one broadcast load
-  const int cd_cnt = (slot >= 0 && slot < Cc.C) ? Cc.cd_cnt[static_cast<long long>(slot) * Vv.nseg + seg] : 0;
+
+  // ---- 1. help build (new contexts queued by the previous step).
+  HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);
+
+  // ---- 2. fill.  Independent loads first: structural word, slot -> {CI, CD count}.
+  const uint32_t sw = (F.seg_counts != nullptr && tid < nwords) ? __ldg(Vv.structural + w0 + tid) : 0u;
+  int slot = Bt.seq_slot[b];  // same address in every thread: one broadcast load
+  if (slot != -2) {
+    if (tid == 0) {
+      // Wait for the build of the slot's segment.  Units of this batch's
+      // queue were all dequeued by running CTAs before any CTA got here, so
+      // they finish; a slot whose build sits in another batch's queue may
+      // not, so the wait is bounded and the segment is then filled directly.
+      const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg
+                                    : Bt.priv_done + static_cast<long long>(slot - Cc.C) * Vv.nseg + seg;
+      int ok = *reinterpret_cast<const volatile int*>(done) >= kChunksPerSeg;
+      if (!ok) {
+        unsigned long long t_start, t_now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        do {
+          __nanosleep(256);
+          ok = *reinterpret_cast<const volatile int*>(done) >= kChunksPerSeg;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+        } while (!ok && t_now - t_start < 2000000ull);
+      }
+      __threadfence();
+      sh.unit = ok;
+    }
+    __syncthreads();
+    if (!sh.unit) slot = -3;  // direct fill
+  }
+  const int cd_cnt = (slot >= 0 && slot < Cc.C) ? __ldcg(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg) : 0;
   uint32_t mword = 0u;
-  if (slot != -2 && tid < nwords) {
+  if (slot >= 0 && tid < nwords) {
     const uint32_t* src = slot < Cc.C ? Cc.ci + static_cast<long long>(slot) * Vv.W
                                       : Bt.priv + static_cast<long long>(slot - Cc.C) * Vv.W;
     mword = __ldcg(src + w0 + tid);
   }
   sh.mask[tid] = mword;
   unsigned long long n_walks = 0;
-  {
-    if (cd_cnt > 0) {
-      // Context-dependent tokens: walk them against the sequence's real stack.
-      const uint32_t* cdsrc = Cc.cdb + static_cast<long long>(slot) * Vv.W + w0;
-      const int depth = Bt.seq[b].depth;
-      const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
-      for (int i = tid; i < depth; i += kThreads) stack_s[i] = gstack[i];
-      const uint32_t x = tid < nwords ? __ldcg(cdsrc + tid) : 0u;
-      sh.cd[tid] = x;
-      int total = 0;
-      const int excl = BlockExclusiveScan(__popc(x), sh.scratch, &total);  // has barriers
-      sh.pre[tid] = excl;
-      __syncthreads();
-      for (int q = tid; q < total; q += kThreads) {
-        int lo = 0, hi = kThreads - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (sh.pre[mid] <= q) lo = mid; else hi = mid - 1;
-        }
-        uint32_t bits = sh.cd[lo];
-        for (int r = q - sh.pre[lo]; r > 0; --r) bits &= bits - 1;
-        const int t = t0 + lo * 32 + (__ffs(bits) - 1);
-        const int r = WalkToken(A, Vv, t, stack_s, depth, true, A.state_any);
-        if (r == kAccept) atomicOr(&sh.mask[lo], 1u << ((t - t0) & 31));
-        if (r == kOverflow) atomicOr(Bt.err, 1u);
-      }
-      n_walks = total;
+  if (slot == -3) {
+    // Uncached: walk every token of the segment against the real stack.
+    const int depth = Bt.seq[b].depth;
+    const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+    for (int i = tid; i < depth; i += kThreads) stack_s[i] = gstack[i];
+    __syncthreads();
+    for (int base_t = 0; base_t < nwords * 32; base_t += kThreads) {
+      const int t = t0 + base_t + tid;
+      const int r = t < t1 ? WalkToken(A, Vv, t, stack_s, depth, true) : kReject;
+      const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
+      if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(Bt.err, 1u);
+      if (lane == 0) sh.mask[(base_t >> 5) + warp] = acc;
     }
+    n_walks = t1 - t0;
+  } else if (cd_cnt > 0) {
+    // Context-dependent tokens: walk them against the sequence's real stack.
+    const uint32_t* cdsrc = Cc.cdb + static_cast<long long>(slot) * Vv.W + w0;
+    const int depth = Bt.seq[b].depth;
+    const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+    for (int i = tid; i < depth; i += kThreads) stack_s[i] = gstack[i];
+    const uint32_t x = tid < nwords ? __ldcg(cdsrc + tid) : 0u;
+    sh.cd[tid] = x;
+    int total = 0;
+    const int excl = BlockExclusiveScan(__popc(x), sh.scratch, &total);  // has barriers
+    sh.pre[tid] = excl;
+    __syncthreads();
+    for (int q = tid; q < total; q += kThreads) {
+      int lo = 0, hi = kThreads - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sh.pre[mid] <= q) lo = mid; else hi = mid - 1;
+      }
+      uint32_t bits = sh.cd[lo];
+      for (int r = q - sh.pre[lo]; r > 0; --r) bits &= bits - 1;
+      const int t = t0 + lo * 32 + (__ffs(bits) - 1);
+      const int r = WalkToken(A, Vv, t, stack_s, depth, true);
+      if (r == kAccept) atomicOr(&sh.mask[lo], 1u << ((t - t0) & 31));
+      if (r == kOverflow) atomicOr(Bt.err, 1u);
+    }
+    n_walks = total;
   }
   __syncthreads();
 
   // ---- outputs: bitmask words, sampler counts, logits.
-  if (bitmask != nullptr) {
-    uint32_t* out = bitmask + static_cast<long long>(b) * ldw + w0;
-    for (int w = tid; w < nwords; w += kThreads) out[w] = sh.mask[w];
-  }
-  if (seg_counts != nullptr) {
-    const int eos_w = Vv.V >> 5;
+  if (F.bitmask != nullptr && tid < nwords) F.bitmask[static_cast<long long>(b) * F.ldw + w0 + tid] = sh.mask[tid];
+  if (F.seg_counts != nullptr) {
     int ca = 0, cs = 0;
     if (tid < nwords) {
       uint32_t m = sh.mask[tid];
-      if (w0 + tid == eos_w) m &= ~(1u << (Vv.V & 31));
+      if (w0 + tid == (Vv.V >> 5)) m &= ~(1u << (Vv.V & 31));
       ca = __popc(m);
       cs = __popc(m & sw);
     }
@@ -423,19 +662,19 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
     if (tid == 0) {
       int ta = 0, ts = 0;
       for (int i = 0; i < kThreads / 32; ++i) ta += sh.scratch[i], ts += sh.pre[i];
-      seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 0] = ta;
-      seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = ts;
+      F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 0] = ta;
+      F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = ts;
     }
   }
   unsigned long long rd = 0, wr = 0;
-  if (MODE == kFillMask && logits != nullptr) {
-    uint16_t* row = logits + static_cast<long long>(b) * ld;
+  if (MODE == kFillMask && F.logits != nullptr) {
+    uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
     const int nchunks = (t1 - t0 + 7) >> 3;
     for (int c = tid; c < nchunks; c += kThreads) {
       const int tb = t0 + c * 8;
       const uint32_t byte = (sh.mask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
       const int valid = min(8, t1 - tb);
-      if (valid == 8 && vec_ok) {
+      if (valid == 8 && F.vec_ok) {
         if (byte == 0xffu) continue;
         if (byte == 0u) {
           __stcs(reinterpret_cast<uint4*>(row + tb), make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u));
@@ -464,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
       }
     }
   } else if (MODE == kFillGreedy) {
-    const uint16_t* row = logits + static_cast<long long>(b) * ld;
+    const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
     const int nchunks = (t1 - t0 + 7) >> 3;
     unsigned long long mine = 0;
     for (int c = tid; c < nchunks; c += kThreads) {
@@ -473,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
       if (byte == 0u) continue;
       const int valid = min(8, t1 - tb);
       uint16_t vals[8];
-      if (valid == 8 && vec_ok) {
+      if (valid == 8 && F.vec_ok) {
         const uint4 v = __ldcs(reinterpret_cast<const uint4*>(row + tb));
         const uint16_t* pv = reinterpret_cast<const uint16_t*>(&v);
 #pragma unroll
@@ -503,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
     if (tid == 0) {
       unsigned long long m = 0;
       for (int i = 0; i < kThreads / 32; ++i) m = sh.best[i] > m ? sh.best[i] : m;
-      if (m) atomicMax(best + b, m);
+      if (m) atomicMax(F.best + b, m);
     }
   }
   if (Bt.stats_enabled) {
@@ -517,224 +756,75 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
     if (tid == 0 && slot >= Cc.C) atomicAdd(Bt.stats + 4, 1ull);
   }
   if (tid == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
+
+  // ---- 3. tail: the sequence's last CTA samples, accepts and looks up.
+  if (TAIL != kTailNone) {
+    __threadfence();  // this CTA's words / counts / argmax visible device-wide
+    __syncthreads();
+    if (tid == 0) sh.last = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
+    __syncthreads();
+    if (sh.last && warp == 0) {
+      __threadfence();
+      if (lane == 0) Bt.seq_arrive[b] = 0;
+      SeqState st = Bt.seq[b];
+      int tok;
+      if (TAIL == kTailGreedy) {
+        const unsigned long long p = __ldcg(F.best + b);
+        tok = p ? static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(p)) : -1;
+        if (lane == 0) F.best[b] = 0ull;
+      } else {
+        tok = SampleStreamWarp(Vv, b, F.bitmask + static_cast<long long>(b) * F.ldw,
+                               F.seg_counts + static_cast<long long>(b) * Vv.nseg * 2, F.seed, st.draws, lane);
+        st.draws += 1;
+        if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
+      }
+      if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
+      AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, lane);
+    }
+  }
+
+  // ---- kernel-wide last CTA: the consumed build queue is empty again.
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned int total = gridDim.x * gridDim.y;
+    if (atomicAdd(Bt.kernel_done, 1u) == total - 1) {
+      *Bt.queue[F.consume].n_items = 0u;
+      *Bt.queue[F.consume].next_unit = 0u;
+      *Bt.kernel_done = 0u;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
-// AcceptKernel: one warp per sequence.
+// AcceptKernel: one warp per sequence (standalone accept / sample).
 // ---------------------------------------------------------------------------
 template <int SAMPLE>
 __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
-                                                    const int32_t* __restrict__ tokens,
-                                                    int32_t* __restrict__ status_out, int restart,
-                                                    const uint32_t* __restrict__ bitmask, long long ldw,
-                                                    const int32_t* __restrict__ seg_counts,
-                                                    unsigned long long seed,
-                                                    unsigned long long* __restrict__ best,
-                                                    int32_t* __restrict__ tokens_out, int do_accept) {
+                                                    AcceptArgs G) {
   const int lane = threadIdx.x & 31;
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= Bt.B) return;
   SeqState st = Bt.seq[b];
-  int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
   int tok = -1;
   if (SAMPLE == kSampleGiven) {
-    tok = tokens[b];
+    tok = G.tokens[b];
   } else if (SAMPLE == kSampleGreedy) {
-    const unsigned long long p = best[b];
+    const unsigned long long p = G.best[b];
     tok = p ? static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(p)) : -1;
     __syncwarp();
-    if (lane == 0) best[b] = 0ull;
+    if (lane == 0) G.best[b] = 0ull;
   } else {
-    // Synthetic stream; identical rule in oracle/gmask_port.c.
-    int na = 0, ns = 0;
-    for (int s = lane; s < Vv.nseg; s += 32) {
-      na += seg_counts[(static_cast<long long>(b) * Vv.nseg + s) * 2];
-      ns += seg_counts[(static_cast<long long>(b) * Vv.nseg + s) * 2 + 1];
-    }
-    na = WarpSum(na);
-    ns = WarpSum(ns);
-    const uint32_t* row = bitmask + static_cast<long long>(b) * ldw;
-    const bool eos = (row[Vv.V >> 5] >> (Vv.V & 31)) & 1u;
-    const unsigned long long u =
-        Mix64(Mix64(seed ^ (static_cast<unsigned long long>(b) * 0xD1B54A32D192ED03ull)) ^
-              static_cast<unsigned long long>(st.draws));
+    tok = SampleStreamWarp(Vv, b, G.bitmask + static_cast<long long>(b) * G.ldw,
+                           G.seg_counts + static_cast<long long>(b) * Vv.nseg * 2, G.seed, st.draws, lane);
     st.draws += 1;
-    if (na == 0) {
-      tok = eos ? Vv.V : -1;
-    } else if (eos && ((u >> 32) & 3ull) != 0) {
-      tok = Vv.V;
-    } else {
-      const bool use_s = ((u >> 34) & 1ull) && ns > 0;
-      const uint32_t nsel = static_cast<uint32_t>(use_s ? ns : na);
-      uint32_t r = static_cast<uint32_t>((static_cast<unsigned long long>(static_cast<uint32_t>(u)) * nsel) >> 32);
-      // Segment holding the r-th selected token: warp prefix sum over the
-      // per-segment counts, 32 segments per round.
-      int seg = -1;
-      for (int s0 = 0; s0 < Vv.nseg && seg < 0; s0 += 32) {
-        const int s = s0 + lane;
-        const int c = s < Vv.nseg ? seg_counts[(static_cast<long long>(b) * Vv.nseg + s) * 2 + (use_s ? 1 : 0)] : 0;
-        int inc = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, inc, 31);
-        if (r < static_cast<uint32_t>(total)) {
-          const int src = __ffs(__ballot_sync(0xffffffffu, static_cast<uint32_t>(inc) > r)) - 1;
-          seg = s0 + src;
-          r -= static_cast<uint32_t>(__shfl_sync(0xffffffffu, inc - c, src));
-        } else {
-          r -= static_cast<uint32_t>(total);
-        }
-      }
-      const int w0 = max(seg, 0) * kSegWords;
-      const int w1 = seg < 0 ? w0 : min(Vv.W, w0 + kSegWords);
-      // All of the segment's words are loaded up front (independent loads).
-      uint32_t xs[kSegWords / 32];
-#pragma unroll
-      for (int j = 0; j < kSegWords / 32; ++j) {
-        const int w = w0 + j * 32 + lane;
-        uint32_t x = 0;
-        if (w < w1) {
-          x = row[w];
-          if (w == (Vv.V >> 5)) x &= ~(1u << (Vv.V & 31));
-          if (use_s) x &= __ldg(Vv.structural + w);
-        }
-        xs[j] = x;
-      }
-      tok = -1;
-#pragma unroll
-      for (int j = 0; j < kSegWords / 32; ++j) {
-        if (tok >= 0) break;
-        const int w = w0 + j * 32 + lane;
-        uint32_t x = xs[j];
-        const int c = __popc(x);
-        int inc = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, inc, 31);
-        if (r < static_cast<uint32_t>(total)) {
-          const unsigned hit = __ballot_sync(0xffffffffu, static_cast<uint32_t>(inc) > r);
-          const int src = __ffs(hit) - 1;
-          if (lane == src) {
-            uint32_t rr = r - static_cast<uint32_t>(inc - c);
-            while (rr--) x &= x - 1;
-            tok = w * 32 + __ffs(x) - 1;
-          }
-          tok = __shfl_sync(0xffffffffu, tok, src);
-        } else {
-          r -= static_cast<uint32_t>(total);
-        }
-      }
-    }
+    if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
   }
-  if (tokens_out != nullptr && lane == 0) tokens_out[b] = tok;
-  if (!(do_accept & 1)) {
-    if (lane == 0) {
-      Bt.seq[b].draws = st.draws;
-      if (SAMPLE == kSampleStream) atomicAdd(Bt.counters + 1, 1ull);
-    }
+  if (G.tokens_out != nullptr && lane == 0) G.tokens_out[b] = tok;
+  if (!G.do_accept) {
+    if (lane == 0) Bt.seq[b].draws = st.draws;
     return;
   }
-
-  if (tok >= 0 && st.status == kAlive) {
-    const bool eos = tok == Vv.V;
-    const int off = eos ? 0 : Vv.tok_off[tok];
-    const int nterm = eos ? 1 : Vv.tok_off[tok + 1] - off;
-    const uint8_t* bytes = Vv.tok_bytes + off;
-    int depth = st.depth;
-    for (int i = 0; i < nterm; ++i) {
-      const int x = eos ? 256 : static_cast<int>(bytes[i]);
-      // Top 32 stack entries, lane j holding entry j (0 = top): one coalesced load.
-      const int topv = lane < depth ? stack[depth - 1 - lane] : -1;
-      const int state = __shfl_sync(0xffffffffu, topv, 0);
-      const int cb = A.rec_begin[state * 257 + x];
-      const int ce = A.rec_begin[state * 257 + x + 1];
-      int found = -1;
-      for (int c0 = cb; c0 < ce && found < 0; c0 += 32) {
-        const int c = c0 + lane;
-        CandRec r;
-        r.cond_len = 0;
-        int4 q[4];
-        if (c < ce) {
-          r = LoadRec(A.recs + c);
-          const int4* cp = reinterpret_cast<const int4*>(A.rec_cond + r.cond_off);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) q[v] = 4 * v + 1 < r.cond_len ? __ldg(cp + v) : make_int4(-1, -1, -1, -1);
-        }
-        bool match = c < ce && r.cond_len <= depth;
-        // Entries 1..16 from the register window (lane-indexed shuffles).
-#pragma unroll
-        for (int j = 1; j <= 16; ++j) {
-          const int have = __shfl_sync(0xffffffffu, topv, j);
-          const int4 qq = q[(j - 1) >> 2];
-          const int want = ((j - 1) & 3) == 0 ? qq.x : ((j - 1) & 3) == 1 ? qq.y : ((j - 1) & 3) == 2 ? qq.z : qq.w;
-          if (j < r.cond_len && have != want) match = false;
-        }
-        for (int j = 17; j < r.cond_len && match; ++j) {  // long conditions: rare
-          match = stack[depth - 1 - j] == A.rec_cond[r.cond_off + j - 1];
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, match);
-        if (m) found = c0 + __ffs(m) - 1;
-      }
-      if (found < 0) {
-        st.status = kDead;  // earlier bytes stay applied (runtime.cpp:179-183)
-        break;
-      }
-      const CandRec r = LoadRec(A.recs + found);
-      const int dyn = r.flags & 1;
-      const int nd = depth - r.cond_len + r.push_len + dyn;
-      const int base = depth - r.cond_len;
-      if (nd > Bt.cap) {
-        st.status = kStackOverflow;
-        break;
-      }
-      if (dyn && base + r.push_len == 0) {
-        st.status = kDead;  // no exposed top: unreachable for validated automata
-        break;
-      }
-      for (int j = lane; j < r.push_len; j += 32) stack[base + j] = A.rec_push[r.push_off + j];
-      __syncwarp();
-      if (dyn) {
-        if (lane == 0) {
-          const int top = stack[base + r.push_len - 1];
-          stack[base + r.push_len] = A.shift[top * 256 + x];
-        }
-        __syncwarp();
-      }
-      depth = nd;
-      if (eos) st.status = kAccepted;
-    }
-    st.depth = depth;
-  }
-  if (status_out != nullptr && lane == 0) status_out[b] = st.status;
-  if (restart && st.status != kAlive) {
-    if (lane == 0) {
-      stack[0] = A.initial;
-      atomicAdd(Bt.counters + 0, 1ull);
-    }
-    st.depth = 1;
-    st.status = kAlive;
-  }
-  __syncwarp();
-  // Key of the next fill's context: lane i loads entry i, lane 0 gathers.
-  int32_t key[kMaxContext];
-  if (do_accept & 2) {
-    const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
-    const int32_t kv = lane < n ? stack[st.depth - 1 - lane] : 0;
-#pragma unroll
-    for (int i = 0; i < kMaxContext; ++i) key[i] = __shfl_sync(0xffffffffu, kv, i);
-  }
-  if (lane == 0) {
-    Bt.seq[b] = st;
-    atomicAdd(Bt.counters + 3, 1ull);
-    if (SAMPLE == kSampleStream) atomicAdd(Bt.counters + 1, 1ull);
-    if (do_accept & 2) AssignSlotKey(Cc, Bt, b, st, Vv.nseg, key);
-  }
+  AcceptWarp(A, Vv, Cc, Bt, b, st, tok, G.status_out, G.restart, G.lookup_queue, lane);
 }
 
 __global__ void ResetKernel(AutView A, BatchView Bt) {
@@ -756,56 +846,61 @@ cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <typename K>
-static void AllowSmem(K kernel, size_t dyn) {
-  if (dyn > 48 * 1024) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
-  }
+cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, cudaStream_t s) {
+  if (b.B == 0) return cudaSuccess;
+  LookupKernel<<<(b.B + 127) / 128, 128, 0, s>>>(c, b, queue);
+  return cudaGetLastError();
 }
 
-cudaError_t LaunchFill(int mode, const AutView& a, const VocabView& v, const CacheView& c,
-                       const BatchView& b, uint32_t* bitmask, long long ldw, uint16_t* logits,
-                       long long ld, int32_t* seg_counts, unsigned long long* best, bool need_lookup,
-                       cudaStream_t s) {
-  if (b.B == 0) return cudaSuccess;
-  const int vec_ok = logits != nullptr && (ld % 8) == 0 && (reinterpret_cast<uintptr_t>(logits) % 16) == 0;
+cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,
+                        cudaStream_t s) {
   const size_t dyn = static_cast<size_t>(b.cap) * sizeof(int32_t);
-  if (need_lookup) LookupKernel<<<(b.B + 127) / 128, 128, 0, s>>>(c, b, v.nseg);
-  AllowSmem(BuildKernel, dyn);
-  BuildKernel<<<b.build_grid, kThreads, dyn, s>>>(a, v, c, b);
+  if (dyn > 48 * 1024) {
+    cudaFuncSetAttribute(DrainKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+  }
+  DrainKernel<<<b.build_grid, kThreads, dyn, s>>>(a, v, c, b, queue);
+  return cudaGetLastError();
+}
+
+template <int MODE, int TAIL>
+static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
+                        const FillArgs& f, size_t dyn, cudaStream_t s) {
+  if (dyn > 48 * 1024) {
+    cudaFuncSetAttribute(FillKernel<MODE, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+  }
   dim3 grid(static_cast<unsigned>(v.nseg), static_cast<unsigned>(b.B));
+  FillKernel<MODE, TAIL><<<grid, kThreads, dyn, s>>>(a, v, c, b, f);
+}
+
+cudaError_t LaunchFill(int mode, int tail, const AutView& a, const VocabView& v, const CacheView& c,
+                       const BatchView& b, FillArgs f, cudaStream_t s) {
+  if (b.B == 0) return cudaSuccess;
+  f.vec_ok = f.logits != nullptr && (f.ld % 8) == 0 && (reinterpret_cast<uintptr_t>(f.logits) % 16) == 0;
+  const size_t dyn = static_cast<size_t>(b.cap) * sizeof(int32_t);
   if (mode == kFillGreedy) {
-    AllowSmem(FillKernel<kFillGreedy>, dyn);
-    FillKernel<kFillGreedy><<<grid, kThreads, dyn, s>>>(a, v, c, b, bitmask, ldw, logits, ld, seg_counts, best,
-                                                        vec_ok);
+    LaunchFillT<kFillGreedy, kTailGreedy>(a, v, c, b, f, dyn, s);
+  } else if (tail == kTailStream) {
+    LaunchFillT<kFillMask, kTailStream>(a, v, c, b, f, dyn, s);
   } else {
-    AllowSmem(FillKernel<kFillMask>, dyn);
-    FillKernel<kFillMask><<<grid, kThreads, dyn, s>>>(a, v, c, b, bitmask, ldw, logits, ld, seg_counts, best,
-                                                      vec_ok);
+    LaunchFillT<kFillMask, kTailNone>(a, v, c, b, f, dyn, s);
   }
   return cudaGetLastError();
 }
 
 cudaError_t LaunchAccept(int sample, const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
-                         const int32_t* tokens, int32_t* status_out, int restart,
-                         const uint32_t* bitmask, long long ldw, const int32_t* seg_counts,
-                         unsigned long long seed, unsigned long long* best, int32_t* tokens_out,
-                         int do_accept, cudaStream_t s) {
+                         const AcceptArgs& g, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
   const int threads = 128;
   const int blocks = (b.B * 32 + threads - 1) / threads;
   switch (sample) {
     case kSampleGiven:
-      AcceptKernel<kSampleGiven><<<blocks, threads, 0, s>>>(a, v, c, b, tokens, status_out, restart, bitmask, ldw,
-                                                           seg_counts, seed, best, tokens_out, do_accept);
+      AcceptKernel<kSampleGiven><<<blocks, threads, 0, s>>>(a, v, c, b, g);
       break;
     case kSampleStream:
-      AcceptKernel<kSampleStream><<<blocks, threads, 0, s>>>(a, v, c, b, tokens, status_out, restart, bitmask, ldw,
-                                                            seg_counts, seed, best, tokens_out, do_accept);
+      AcceptKernel<kSampleStream><<<blocks, threads, 0, s>>>(a, v, c, b, g);
       break;
     default:
-      AcceptKernel<kSampleGreedy><<<blocks, threads, 0, s>>>(a, v, c, b, tokens, status_out, restart, bitmask, ldw,
-                                                            seg_counts, seed, best, tokens_out, do_accept);
+      AcceptKernel<kSampleGreedy><<<blocks, threads, 0, s>>>(a, v, c, b, g);
       break;
   }
   return cudaGetLastError();

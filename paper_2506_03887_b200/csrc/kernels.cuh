@@ -10,12 +10,12 @@
 
 namespace pre3 {
 
-constexpr int kThreads = 256;                     // fill / build CTA size (8 warps)
-constexpr int kSegWords = 256;                    // mask words per vocab segment
-constexpr int kSegTokens = kSegWords * 32;        // 8192 tokens per segment
+constexpr int kThreads = 256;                         // fill / build CTA size (8 warps)
+constexpr int kSegWords = 256;                        // mask words per vocab segment
+constexpr int kSegTokens = kSegWords * 32;            // 8192 tokens per segment
 constexpr int kChunksPerSeg = kSegTokens / kThreads;  // build work units per segment
-constexpr int kMaxContext = 16;                   // max K
-constexpr int kWalkOverlay = 64;                  // per-thread pushed-entry overlay in a mask walk
+constexpr int kMaxContext = 16;                       // max K
+constexpr int kWalkOverlay = 64;                      // per-thread pushed-entry overlay in a mask walk
 
 // Per-sequence device state: {depth, status, draws, reserved}.
 struct SeqState {
@@ -28,8 +28,8 @@ struct SeqState {
 struct AutView {
   const int32_t* rec_begin;  // S*257+1
   const CandRec* recs;
-  const int32_t* rec_cond;
-  const int32_t* rec_push;
+  const int32_t* rec_cond;   // 16-B aligned lists
+  const int32_t* rec_push;   // 16-B aligned lists
   const int32_t* shift;       // S*256
   const uint32_t* state_any;  // S*9
   int32_t num_states;
@@ -48,7 +48,8 @@ struct VocabView {
 // Context cache (engine-wide, shared by batches on the device).  Key =
 // (n = min(depth, K), complete = depth <= K, the top n stack entries) ->
 // {CI: tokens accepted whatever lies below the key, CD: tokens whose walk
-// reaches below the key} as two W-word bitsets, plus per-segment CD counts.
+// reaches below the key} as two W-word bitsets, plus per-segment CD counts
+// and build-completion counters.
 struct CacheView {
   unsigned long long* slot_hash;  // C; 0 = empty
   int32_t* slot_meta;             // C; n | complete << 8 | ready << 16
@@ -56,9 +57,17 @@ struct CacheView {
   uint32_t* ci;                   // C*W
   uint32_t* cdb;                  // C*W
   int32_t* cd_cnt;                // C*nseg
+  int32_t* seg_done;              // C*nseg completed build units (kChunksPerSeg = built)
   unsigned long long* counters;   // [0] slots, [1] segment builds, [2] private builds
   int32_t C;
   int32_t K;
+};
+
+// Build work queue: items {slot, seg, seq, 0}; units = items * kChunksPerSeg.
+struct BuildQueue {
+  int4* items;
+  unsigned int* n_items;
+  unsigned int* next_unit;
 };
 
 struct BatchView {
@@ -66,32 +75,60 @@ struct BatchView {
   int32_t* stacks;  // B*cap, bottom first
   int32_t cap;
   int32_t B;
+  int32_t nseg;
   int32_t* seq_slot;        // B: cache slot, C+b = private row, -2 = not alive
   uint32_t* priv;           // B*W private (uncached) masks
-  int4* items;              // build work list {slot, seg, seq, 0}
-  unsigned int* n_items;
+  int32_t* priv_done;       // B*nseg build-completion counters of private rows
+  BuildQueue queue[2];      // produced by lookups, consumed by the next fill
+  int32_t* seq_arrive;      // B: fill CTAs finished per sequence (fused tail)
+  unsigned int* kernel_done;  // CTAs finished per launch (queue reset)
   unsigned int* err;                  // bit0: walk overlay overflow
-  unsigned long long* stats;          // [0] rd bytes, [1] wr bytes, [2] cd walks, [3] builds, [4] private
+  unsigned long long* stats;          // [0] rd bytes, [1] wr bytes, [2] walks, [3] -, [4] private
   unsigned long long* counters;       // [0] restarts, [1] draws, [2] fills, [3] accepts
   int32_t stats_enabled;
   int32_t build_grid;
 };
 
 enum FillMode { kFillMask = 0, kFillGreedy = 1 };
+enum FillTail { kTailNone = 0, kTailStream = 1, kTailGreedy = 2 };
 enum SampleMode { kSampleGiven = 0, kSampleStream = 1, kSampleGreedy = 2 };
 
+struct FillArgs {
+  uint32_t* bitmask;        // [B][ldw] (never null with a tail)
+  long long ldw;
+  uint16_t* logits;         // bf16 [B][ld] or null
+  long long ld;
+  int32_t* seg_counts;      // [B][nseg][2] or null (required by the stream tail)
+  unsigned long long* best; // [B] greedy partials
+  int32_t* tokens_out;      // tail: sampled ids or null
+  unsigned long long seed;  // stream tail
+  int consume;              // build queue drained by this launch
+  int produce;              // build queue fed by the tail's lookups
+  int vec_ok;               // set by LaunchFill
+};
+
+struct AcceptArgs {
+  const int32_t* tokens;
+  int32_t* status_out;
+  int restart;
+  const uint32_t* bitmask;
+  long long ldw;
+  const int32_t* seg_counts;
+  unsigned long long seed;
+  unsigned long long* best;
+  int32_t* tokens_out;
+  int do_accept;     // 0: sample only
+  int lookup_queue;  // >= 0: assign next-fill context slots into this queue
+};
+
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s);
-// lookup + build + fill (+ bf16 -inf masking or greedy argmax).
-cudaError_t LaunchFill(int mode, const AutView& a, const VocabView& v, const CacheView& c,
-                       const BatchView& b, uint32_t* bitmask, long long ldw, uint16_t* logits,
-                       long long ld, int32_t* seg_counts, unsigned long long* best, bool need_lookup,
-                       cudaStream_t s);
-// do_accept: bit0 = accept the token (else sample only), bit1 = also assign
-// each sequence's context slot for the next fill (queues builds).
+cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, cudaStream_t s);
+cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,
+                        cudaStream_t s);
+// Help-build + fill (+ bf16 -inf masking or greedy argmax) (+ fused tail).
+cudaError_t LaunchFill(int mode, int tail, const AutView& a, const VocabView& v, const CacheView& c,
+                       const BatchView& b, FillArgs f, cudaStream_t s);
 cudaError_t LaunchAccept(int sample, const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
-                         const int32_t* tokens, int32_t* status_out, int restart,
-                         const uint32_t* bitmask, long long ldw, const int32_t* seg_counts,
-                         unsigned long long seed, unsigned long long* best, int32_t* tokens_out,
-                         int do_accept, cudaStream_t s);
+                         const AcceptArgs& g, cudaStream_t s);
 
 }  // namespace pre3

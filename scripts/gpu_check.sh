@@ -1,4 +1,4 @@
-# GPU round script: tests, smoke, bench, launch list, ncu captures.
+# GPU round script: tests, smoke, bench, launch list, ncu capture of the fused step kernel.
 set -x
 cd $GRAFT_REPO_ROOT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
@@ -7,14 +7,10 @@ timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out
 tail -30 gpurun_out/pytest_gpu.txt
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?"; tail -5 gpurun_out/smoke.txt
 fi
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+timeout 600 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
 if [ "${PROFILE:-1}" = "1" ]; then
-# prewarm 400 steps = 1200 launches (accept, build, fill), bench warm-up 40 steps = 120 more
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 1320 -c 150 --csv --log-file gpurun_out/launches.csv python bench.py --steps 60 --warmup 40 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
+# prewarm: 400 launches (+2 drains); bench: 1 lookup + 40 warm-up steps
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 450 -c 100 --csv --log-file gpurun_out/launches.csv python bench.py --steps 60 --warmup 40 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu list rc=$?"
 python scripts/launches.py gpurun_out/launches.csv
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:FillKernel -s 450 -c 1 -o gpurun_out/prof_fill -f python bench.py --steps 20 --warmup 60 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu fill rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:BuildKernel -s 3 -c 1 -o gpurun_out/prof_build -f python bench.py --steps 5 --warmup 5 --prewarm-steps 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_build.log 2>&1; echo "ncu build rc=$?"
-fi
-if [ "${PROFILE:-1}" = "1" ]; then
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:AcceptKernel -s 450 -c 1 -o gpurun_out/prof_accept -f python bench.py --steps 20 --warmup 60 --no-e2e --no-cpu-baseline > gpurun_out/ncu_accept.log 2>&1; echo "ncu accept rc=$?"
 fi

@@ -98,8 +98,9 @@ def test_dead_and_accepted_rows_are_empty():
     assert np.all(np.isneginf(lgf[0])) and np.all(np.isneginf(lgf[1]))
 
 
-def run_stream(eng, B, steps, seed, cap=1024, check_logits=False, port=None):
-    """Device decode loop: fused fill (+logits) then stream-sample + accept."""
+def run_stream(eng, B, steps, seed, cap=1024, check_logits=False, fused=False):
+    """Device decode loop: fill (+logits) then stream-sample + accept, as two
+    API calls or (fused=True) one gm_decode_step_stream launch."""
     batch = eng.batch(B, cap)
     bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
     counts = torch.zeros((B, batch.nseg * 2), dtype=torch.int32, device=DEV)
@@ -110,8 +111,11 @@ def run_stream(eng, B, steps, seed, cap=1024, check_logits=False, port=None):
         if lg is not None:
             lg.normal_()
             before = lg.clone()
-        batch.fill(bm, lg, counts)
-        batch.sample_stream_and_accept(bm, counts, seed, toks)
+        if fused:
+            batch.decode_step_stream(seed, bitmask=bm, logits=lg, tokens_out=toks)
+        else:
+            batch.fill(bm, lg, counts)
+            batch.sample_stream_and_accept(bm, counts, seed, toks)
         batch.check()
         m = bm.cpu().numpy().view(np.uint32).copy()
         masks.append(m)
@@ -124,13 +128,14 @@ def run_stream(eng, B, steps, seed, cap=1024, check_logits=False, port=None):
     return batch, np.stack(masks, 1), np.stack(tokens, 1)
 
 
-def test_json32k_stream_matches_golden(vectors):
+@pytest.mark.parametrize("fused", [False, True])
+def test_json32k_stream_matches_golden(vectors, fused):
     """Config 1 replayed on the GPU: every mask digest, token and the final
     stacks equal the reference's (golden)."""
     g = vectors["json32k_stream"]
     vocab = pk.synth_vocab(32000)
     eng = pk.DeviceEngine(pk.Automaton.load(flat("json")), vocab)
-    batch, masks, tokens = run_stream(eng, g["batch"], g["steps"], g["seed"], check_logits=True)
+    batch, masks, tokens = run_stream(eng, g["batch"], g["steps"], g["seed"], check_logits=True, fused=fused)
     assert tokens.tolist() == g["tokens"]
     for b in range(g["batch"]):
         for s in range(g["steps"]):
@@ -140,8 +145,8 @@ def test_json32k_stream_matches_golden(vectors):
         assert got.stack == fin["stack"] and got.status == fin["status"]
 
 
-@pytest.mark.parametrize("K", [2, 8])
-def test_json128k_stream_matches_port(K):
+@pytest.mark.parametrize("K,fused", [(2, False), (8, False), (12, True)])
+def test_json128k_stream_matches_port(K, fused):
     """Config 2 shape (JSON, 128,255 tokens): GPU decode loop == C port loop
     (tokens every step, final stacks) for 24 sequences x 16 steps."""
     vocab = pk.synth_vocab(128255)
@@ -149,7 +154,7 @@ def test_json128k_stream_matches_port(K):
     eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
     port = Port(f, vocab)
     B, steps, seed = 24, 16, 5
-    batch, masks, tokens = run_stream(eng, B, steps, seed)
+    batch, masks, tokens = run_stream(eng, B, steps, seed, fused=fused)
     _, ptoks, pstacks = port.decode_run(eng.structural, B, steps, seed, want_tokens=True, want_stacks=True)
     assert np.array_equal(tokens, ptoks)
     for b in range(B):
@@ -169,6 +174,8 @@ def test_cache_pressure_paths():
     for slots in [1, 4, 1024]:
         eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=3, context_slots=slots)
         _, _, tokens = run_stream(eng, B, steps, seed)
+        assert np.array_equal(tokens, ptoks), slots
+        _, _, tokens = run_stream(eng, B, steps, seed, fused=True)  # warm cache, second batch
         assert np.array_equal(tokens, ptoks), slots
         if slots <= 4:
             assert eng.info()["private_builds"] > 0
