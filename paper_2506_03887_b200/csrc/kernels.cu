@@ -54,6 +54,13 @@ __device__ __forceinline__ CandRec LoadRec(const CandRec* p) {
   return r;
 }
 
+// Device-scope relaxed load (L2; neither a stale L1 hit nor a system-scope
+// volatile access).
+template <typename T>
+__device__ __forceinline__ T LoadRelaxed(const T* p) {
+  return cuda::atomic_ref<T, cuda::thread_scope_device>(*const_cast<T*>(p)).load(cuda::memory_order_relaxed);
+}
+
 __device__ __forceinline__ int Lane4(const int4& q, int i) {
   return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w;
 }
@@ -321,7 +328,7 @@ __device__ __noinline__ void BuildUnit(const AutView& A, const VocabView& Vv, co
 // launches, so the count is final here.
 __device__ void HelpBuild(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int q,
                           int32_t* base_s, int* sh_unit) {
-  const unsigned int n_items = *reinterpret_cast<volatile unsigned int*>(Bt.queue[q].n_items);
+  const unsigned int n_items = LoadRelaxed(Bt.queue[q].n_items);
   if (n_items == 0) return;
   const unsigned int units = n_items * kChunksPerSeg;
   for (;;) {
@@ -574,13 +581,13 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
       // not, so the wait is bounded and the segment is then filled directly.
       const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg
                                     : Bt.priv_done + static_cast<long long>(slot - Cc.C) * Vv.nseg + seg;
-      int ok = *reinterpret_cast<const volatile int*>(done) >= kChunksPerSeg;
+      int ok = LoadRelaxed(done) >= kChunksPerSeg;
       if (!ok) {
         unsigned long long t_start, t_now;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         do {
           __nanosleep(256);
-          ok = *reinterpret_cast<const volatile int*>(done) >= kChunksPerSeg;
+          ok = LoadRelaxed(done) >= kChunksPerSeg;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
         } while (!ok && t_now - t_start < 2000000ull);
       }
@@ -667,42 +674,7 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
     }
   }
   unsigned long long rd = 0, wr = 0;
-  if (MODE == kFillMask && F.logits != nullptr) {
-    uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
-    const int nchunks = (t1 - t0 + 7) >> 3;
-    for (int c = tid; c < nchunks; c += kThreads) {
-      const int tb = t0 + c * 8;
-      const uint32_t byte = (sh.mask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
-      const int valid = min(8, t1 - tb);
-      if (valid == 8 && F.vec_ok) {
-        if (byte == 0xffu) continue;
-        if (byte == 0u) {
-          __stcs(reinterpret_cast<uint4*>(row + tb), make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u));
-          wr += 16;
-        } else {
-          // Mixed chunk: store only the masked halves/pairs (no read of the
-          // row; L2 merges the partial sector).
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t pair = (byte >> (2 * j)) & 3u;
-            if (pair == 0u) {
-              __stcs(reinterpret_cast<uint32_t*>(row + tb) + j, 0xFF80FF80u);
-              wr += 4;
-            } else if (pair != 3u) {
-              __stcs(reinterpret_cast<unsigned short*>(row + tb + 2 * j + (pair == 2u ? 0 : 1)),
-                     static_cast<unsigned short>(0xFF80u));
-              wr += 2;
-            }
-          }
-        }
-      } else {
-        for (int j = 0; j < valid; ++j) {
-          if (!((byte >> j) & 1u)) row[tb + j] = 0xFF80u;
-        }
-        wr += 2 * valid;
-      }
-    }
-  } else if (MODE == kFillGreedy) {
+  if (MODE == kFillGreedy) {
     const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
     const int nchunks = (t1 - t0 + 7) >> 3;
     unsigned long long mine = 0;
@@ -745,6 +717,52 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
       if (m) atomicMax(F.best + b, m);
     }
   }
+
+  // ---- arrival: the sequence's last CTA runs the tail.  Only the mask
+  // words, counts and argmax partials must be visible to it, so the fence
+  // precedes the (bulk) logits stores below.
+  if (TAIL != kTailNone) __threadfence();
+  __syncthreads();
+  if (tid == 0) sh.last = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
+  __syncthreads();
+  const bool last = sh.last;
+
+  if (MODE == kFillMask && F.logits != nullptr) {
+    uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
+    const int nchunks = (t1 - t0 + 7) >> 3;
+    for (int c = tid; c < nchunks; c += kThreads) {
+      const int tb = t0 + c * 8;
+      const uint32_t byte = (sh.mask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
+      const int valid = min(8, t1 - tb);
+      if (valid == 8 && F.vec_ok) {
+        if (byte == 0xffu) continue;
+        if (byte == 0u) {
+          __stcs(reinterpret_cast<uint4*>(row + tb), make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u));
+          wr += 16;
+        } else {
+          // Mixed chunk: store only the masked halves/pairs (no read of the
+          // row; L2 merges the partial sector).
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t pair = (byte >> (2 * j)) & 3u;
+            if (pair == 0u) {
+              __stcs(reinterpret_cast<uint32_t*>(row + tb) + j, 0xFF80FF80u);
+              wr += 4;
+            } else if (pair != 3u) {
+              __stcs(reinterpret_cast<unsigned short*>(row + tb + 2 * j + (pair == 2u ? 0 : 1)),
+                     static_cast<unsigned short>(0xFF80u));
+              wr += 2;
+            }
+          }
+        }
+      } else {
+        for (int j = 0; j < valid; ++j) {
+          if (!((byte >> j) & 1u)) row[tb + j] = 0xFF80u;
+        }
+        wr += 2 * valid;
+      }
+    }
+  }
   if (Bt.stats_enabled) {
     rd = static_cast<unsigned long long>(WarpSum(static_cast<int>(rd)));
     wr = static_cast<unsigned long long>(WarpSum(static_cast<int>(wr)));
@@ -758,14 +776,10 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
   if (tid == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
 
   // ---- 3. tail: the sequence's last CTA samples, accepts and looks up.
+  if (!last) return;
   if (TAIL != kTailNone) {
-    __threadfence();  // this CTA's words / counts / argmax visible device-wide
-    __syncthreads();
-    if (tid == 0) sh.last = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
-    __syncthreads();
-    if (sh.last && warp == 0) {
+    if (warp == 0) {
       __threadfence();
-      if (lane == 0) Bt.seq_arrive[b] = 0;
       SeqState st = Bt.seq[b];
       int tok;
       if (TAIL == kTailGreedy) {
@@ -783,11 +797,11 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
     }
   }
 
-  // ---- kernel-wide last CTA: the consumed build queue is empty again.
-  __syncthreads();
+  // ---- last sequence to complete: every CTA is past HelpBuild, so the
+  // consumed build queue can be emptied.
   if (tid == 0) {
-    const unsigned int total = gridDim.x * gridDim.y;
-    if (atomicAdd(Bt.kernel_done, 1u) == total - 1) {
+    Bt.seq_arrive[b] = 0;
+    if (atomicAdd(Bt.kernel_done, 1u) == gridDim.y - 1) {
       *Bt.queue[F.consume].n_items = 0u;
       *Bt.queue[F.consume].next_unit = 0u;
       *Bt.kernel_done = 0u;
