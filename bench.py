@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--prewarm-batch", type=int, default=1024)
     p.add_argument("--stack-cap", type=int, default=1024)
     p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--fused", action="store_true", help="one-launch decode step (gm_decode_step_stream)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
@@ -225,7 +226,11 @@ def main():
     logits = [torch.randn((B, V1), dtype=torch.bfloat16, device=dev) for _ in range(R)]
 
     def step(i):
-        batch.decode_step_stream(seed, bitmask=bm, logits=logits[i % R], tokens_out=toks)
+        if args.fused:
+            batch.decode_step_stream(seed, bitmask=bm, logits=logits[i % R], tokens_out=toks)
+        else:
+            batch.fill(bm, logits[i % R], counts)
+            batch.sample_stream_and_accept(bm, counts, seed, toks)
 
     for i in range(args.warmup):
         step(i)
@@ -242,8 +247,13 @@ def main():
         e0.record(stream)
         for i in range(K):
             ev[i][0].record(stream)
-            batch.decode_step_stream(seed, bitmask=bm, logits=logits[i % R], tokens_out=toks)
-            ev[i][1].record(stream)
+            if args.fused:
+                step(i)
+                ev[i][1].record(stream)
+            else:  # events bracket the fill kernel alone (the roofline kernel)
+                batch.fill(bm, logits[i % R], counts)
+                ev[i][1].record(stream)
+                batch.sample_stream_and_accept(bm, counts, seed, toks)
         e1.record(stream)
         h1 = time.perf_counter()
         torch.cuda.synchronize()
@@ -261,7 +271,7 @@ def main():
 
     # Device-counted logit bytes of one more fill (outside the timed region).
     batch.set_stats(True)
-    batch.decode_step_stream(seed, bitmask=bm, logits=logits[K % R], tokens_out=toks)
+    step(K)
     batch.check()
     fstats = batch.fill_stats()
     batch.set_stats(False)
@@ -334,15 +344,15 @@ def main():
         "config": dict(workload_config(args, world),
                        l2=f"rotating {R} logits buffers of {row_bytes / 2**20:.0f} MiB (> 126 MB L2)"),
         "mask_latency_us": 1e3 * fill_ms,
-        "step_breakdown_us": {"decode_step_kernel": 1e3 * fill_ms, "host_enqueue_per_step": 1e3 * host_ms},
+        "step_breakdown_us": {("decode_step_kernel" if args.fused else "fill_kernel"): 1e3 * fill_ms, "host_enqueue_per_step": 1e3 * host_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": "FillKernel<mask,stream-tail> (whole fused step)",
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "FillKernel (whole fused step)" if args.fused else "FillKernel + AcceptKernel (one step)",
                      "alg_bytes_per_seq_step": alg_bytes_seq,
                      "device_counted_logit_bytes_per_seq_step": (fstats["logit_bytes_read"] +
                                                                  fstats["logit_bytes_written"]) / B},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": K,
+        "gpu_launches": K * (1 if args.fused else 2),
         "clocks": clocks.summary(),
         "preprocessing": {"prewarm_s": t_pre, "prewarm": f"{args.prewarm_steps} steps x {args.prewarm_batch} seqs "
                           f"(seed differs from the timed streams)", "contexts_after_prewarm": pre_info["context_slots_used"]},
