@@ -88,8 +88,22 @@ struct gm_batch {
   uint32_t* scratch_mask = nullptr;       // internal bitmask when the caller passes none
   unsigned long long* best = nullptr;     // greedy argmax packed keys
   int prod = 0;                           // queue the next fill drains
+  int last_consumed = -1;                 // queue the previous fill drained (reset by the next)
   bool slots_valid = false;               // seq_slot matches the stacks
   bool lookup_pending = false;            // queue[prod] got a lookup pass since the last fill
+
+  // Queue roles of a fill launch (3-queue ring, see kernels.cuh BatchView).
+  void BeginFill(pre3::FillArgs* f) const {
+    f->consume = prod;
+    f->produce = (prod + 1) % 3;
+    f->reset = last_consumed;
+  }
+  void EndFill(bool tail) {
+    last_consumed = prod;
+    prod = (prod + 1) % 3;
+    slots_valid = true;
+    lookup_pending = tail;  // the tail fed the new queue[prod]
+  }
 
   // Queue for an accept's fused lookup, or -1 (then the next fill looks up).
   int AcceptLookupQueue() {
@@ -105,7 +119,7 @@ struct gm_batch {
   ~gm_batch() {
     cudaSetDevice(engine->device);
     // Builds still queued belong to contexts other batches may already use.
-    for (int q = 0; q < 2; ++q) pre3::LaunchDrain(engine->aut, engine->vocab, engine->cache, view, q, nullptr);
+    for (int q = 0; q < 3; ++q) pre3::LaunchDrain(engine->aut, engine->vocab, engine->cache, view, q, nullptr);
     cudaDeviceSynchronize();
     for (void* p : owned) cudaFree(p);
   }
@@ -325,7 +339,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     v.priv_done = DevAlloc<int32_t>(bn, &b->owned);
     Check(cudaMemset(v.priv_done, 0, bn * 4), "memset");
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < 3; ++q) {
       v.queue[q].items = DevAlloc<int4>(2 * bn, &b->owned);
       v.queue[q].n_items = DevAlloc<unsigned int>(1, &b->owned);
       v.queue[q].next_unit = DevAlloc<unsigned int>(1, &b->owned);
@@ -477,11 +491,9 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     f.ld = ld;
     f.seg_counts = seg_counts;
     f.best = b->best;
-    f.consume = b->prod;
-    f.produce = 1 - b->prod;
+    b->BeginFill(&f);
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s), "fill launch");
-    b->slots_valid = true;
-    b->lookup_pending = false;
+    b->EndFill(false);
     return GM_OK;
   });
 }
@@ -507,13 +519,10 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
     f.best = b->best;
     f.tokens_out = tokens_out;
     f.seed = seed;
-    f.consume = b->prod;
-    f.produce = 1 - b->prod;
+    b->BeginFill(&f);
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailStream, e->aut, e->vocab, e->cache, b->view, f, s),
           "decode launch");
-    b->prod = 1 - b->prod;
-    b->slots_valid = true;
-    b->lookup_pending = true;
+    b->EndFill(true);
     return GM_OK;
   });
 }
@@ -600,13 +609,10 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     f.ld = ld;
     f.best = b->best;
     f.tokens_out = tokens_out;
-    f.consume = b->prod;
-    f.produce = 1 - b->prod;
+    b->BeginFill(&f);
     Check(pre3::LaunchFill(pre3::kFillGreedy, pre3::kTailGreedy, e->aut, e->vocab, e->cache, b->view, f, s),
           "greedy decode launch");
-    b->prod = 1 - b->prod;
-    b->slots_valid = true;
-    b->lookup_pending = true;
+    b->EndFill(true);
     return GM_OK;
   });
 }

@@ -61,6 +61,11 @@ __device__ __forceinline__ T LoadRelaxed(const T* p) {
   return cuda::atomic_ref<T, cuda::thread_scope_device>(*const_cast<T*>(p)).load(cuda::memory_order_relaxed);
 }
 
+template <typename T>
+__device__ __forceinline__ T LoadAcquire(const T* p) {
+  return cuda::atomic_ref<T, cuda::thread_scope_device>(*const_cast<T*>(p)).load(cuda::memory_order_acquire);
+}
+
 __device__ __forceinline__ int Lane4(const int4& q, int i) {
   return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w;
 }
@@ -555,7 +560,7 @@ struct FillShared {
 };
 
 template <int MODE, int TAIL>
-__global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+__global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                           FillArgs F) {
   __shared__ FillShared sh;
   extern __shared__ int32_t stack_s[];
@@ -566,6 +571,13 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
   const int t0 = w0 * 32;
   const int t1 = min(Vv.V + 1, t0 + nwords * 32);
   static_assert(kSegWords == kThreads, "one mask word per thread");
+
+  // ---- 0. the queue drained by the previous fill is free again (nobody
+  // produces into it until the fill after next consumes it: 3-queue ring).
+  if (F.reset >= 0 && seg == 0 && b == 0 && tid == 0) {
+    *Bt.queue[F.reset].n_items = 0u;
+    *Bt.queue[F.reset].next_unit = 0u;
+  }
 
   // ---- 1. help build (new contexts queued by the previous step).
   HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);
@@ -581,17 +593,16 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
       // not, so the wait is bounded and the segment is then filled directly.
       const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg
                                     : Bt.priv_done + static_cast<long long>(slot - Cc.C) * Vv.nseg + seg;
-      int ok = LoadRelaxed(done) >= kChunksPerSeg;
+      int ok = LoadAcquire(done) >= kChunksPerSeg;
       if (!ok) {
         unsigned long long t_start, t_now;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         do {
           __nanosleep(256);
-          ok = LoadRelaxed(done) >= kChunksPerSeg;
+          ok = LoadAcquire(done) >= kChunksPerSeg;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
         } while (!ok && t_now - t_start < 2000000ull);
       }
-      __threadfence();
       sh.unit = ok;
     }
     __syncthreads();
@@ -721,11 +732,14 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
   // ---- arrival: the sequence's last CTA runs the tail.  Only the mask
   // words, counts and argmax partials must be visible to it, so the fence
   // precedes the (bulk) logits stores below.
-  if (TAIL != kTailNone) __threadfence();
-  __syncthreads();
-  if (tid == 0) sh.last = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
-  __syncthreads();
-  const bool last = sh.last;
+  bool last = false;
+  if (TAIL != kTailNone) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sh.last = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
+    __syncthreads();
+    last = sh.last;
+  }
 
   if (MODE == kFillMask && F.logits != nullptr) {
     uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
@@ -793,18 +807,8 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
         if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
       }
       if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
+      if (lane == 0) Bt.seq_arrive[b] = 0;
       AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, lane);
-    }
-  }
-
-  // ---- last sequence to complete: every CTA is past HelpBuild, so the
-  // consumed build queue can be emptied.
-  if (tid == 0) {
-    Bt.seq_arrive[b] = 0;
-    if (atomicAdd(Bt.kernel_done, 1u) == gridDim.y - 1) {
-      *Bt.queue[F.consume].n_items = 0u;
-      *Bt.queue[F.consume].next_unit = 0u;
-      *Bt.kernel_done = 0u;
     }
   }
 }

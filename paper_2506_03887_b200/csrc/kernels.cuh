@@ -79,7 +79,7 @@ struct BatchView {
   int32_t* seq_slot;        // B: cache slot, C+b = private row, -2 = not alive
   uint32_t* priv;           // B*W private (uncached) masks
   int32_t* priv_done;       // B*nseg build-completion counters of private rows
-  BuildQueue queue[2];      // produced by lookups, consumed by the next fill
+  BuildQueue queue[3];      // ring: lookups feed queue[p], fill drains it, the next fill resets it
   int32_t* seq_arrive;      // B: fill CTAs finished per sequence (fused tail)
   unsigned int* kernel_done;  // CTAs finished per launch (queue reset)
   unsigned int* err;                  // bit0: walk overlay overflow
@@ -104,6 +104,7 @@ struct FillArgs {
   unsigned long long seed;  // stream tail
   int consume;              // build queue drained by this launch
   int produce;              // build queue fed by the tail's lookups
+  int reset;                // queue drained by the previous fill, emptied here (-1: none)
   int vec_ok;               // set by LaunchFill
 };
 
