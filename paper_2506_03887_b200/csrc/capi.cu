@@ -269,6 +269,8 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.cdb = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
     c.cd_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.seg_done = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
+    c.slot_built = DevAlloc<int32_t>(C, &e->owned);
+    Check(cudaMemset(c.slot_built, 0, C * 4), "memset");
     c.counters = DevAlloc<unsigned long long>(8, &e->owned);
     Check(cudaMemset(c.slot_hash, 0, C * 8), "memset");
     Check(cudaMemset(c.slot_meta, 0, C * 4), "memset");

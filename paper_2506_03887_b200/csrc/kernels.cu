@@ -66,6 +66,12 @@ __device__ __forceinline__ T LoadAcquire(const T* p) {
   return cuda::atomic_ref<T, cuda::thread_scope_device>(*const_cast<T*>(p)).load(cuda::memory_order_acquire);
 }
 
+// Queue q of the batch, selected without indexing the by-value parameter
+// struct (a dynamic index would copy the whole BatchView to local memory).
+__device__ __forceinline__ BuildQueue QueueOf(const BatchView& Bt, int q) {
+  return q == 0 ? Bt.queue[0] : (q == 1 ? Bt.queue[1] : Bt.queue[2]);
+}
+
 __device__ __forceinline__ int Lane4(const int4& q, int i) {
   return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w;
 }
@@ -260,23 +266,25 @@ __device__ void AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, i
   const int complete = st.depth <= Cc.K ? 1 : 0;
   bool created = false;
   int slot = LookupSlot(Cc, key, n, complete, &created);
+  bool wait = true;
   if (slot < 0 || created) {
+    // Slots are never reused, so a new slot's counters are still zero.
     if (slot < 0) {
       slot = Cc.C + b;
       for (int s = 0; s < nseg; ++s) Bt.priv_done[static_cast<long long>(b) * nseg + s] = 0;
       atomicAdd(Cc.counters + 2, 1ull);
+      __threadfence();  // zeroed counters visible before the items
     } else {
-      for (int s = 0; s < nseg; ++s) {
-        Cc.cd_cnt[static_cast<long long>(slot) * nseg + s] = 0;
-        Cc.seg_done[static_cast<long long>(slot) * nseg + s] = 0;
-      }
       atomicAdd(Cc.counters + 1, static_cast<unsigned long long>(nseg));
     }
-    __threadfence();  // zeroed counters visible before the items
-    const unsigned int at = atomicAdd(Bt.queue[q].n_items, static_cast<unsigned int>(nseg));
-    for (int s = 0; s < nseg; ++s) Bt.queue[q].items[at + s] = make_int4(slot, s, b, 0);
+    const BuildQueue Q = QueueOf(Bt, q);
+    const unsigned int at = atomicAdd(Q.n_items, static_cast<unsigned int>(nseg));
+    for (int s = 0; s < nseg; ++s) Q.items[at + s] = make_int4(slot, s, b, 0);
+  } else {
+    // Existing slot: only one whose build is still queued needs a wait.
+    wait = LoadAcquire(Cc.slot_built + slot) < nseg * kChunksPerSeg;
   }
-  Bt.seq_slot[b] = slot;
+  Bt.seq_slot[b] = slot | (wait ? kSlotWait : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -326,6 +334,7 @@ __device__ __noinline__ void BuildUnit(const AutView& A, const VocabView& Vv, co
     int* done = priv ? Bt.priv_done + static_cast<long long>(b) * Vv.nseg + seg
                      : Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg;
     atomicAdd(done, 1);
+    if (!priv) atomicAdd(Cc.slot_built + slot, 1);
   }
 }
 
@@ -333,16 +342,17 @@ __device__ __noinline__ void BuildUnit(const AutView& A, const VocabView& Vv, co
 // launches, so the count is final here.
 __device__ void HelpBuild(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int q,
                           int32_t* base_s, int* sh_unit) {
-  const unsigned int n_items = LoadRelaxed(Bt.queue[q].n_items);
+  const BuildQueue Q = QueueOf(Bt, q);
+  const unsigned int n_items = LoadRelaxed(Q.n_items);
   if (n_items == 0) return;
   const unsigned int units = n_items * kChunksPerSeg;
   for (;;) {
-    if (threadIdx.x == 0) *sh_unit = static_cast<int>(atomicAdd(Bt.queue[q].next_unit, 1u));
+    if (threadIdx.x == 0) *sh_unit = static_cast<int>(atomicAdd(Q.next_unit, 1u));
     __syncthreads();
     const unsigned int u = static_cast<unsigned int>(*sh_unit);
     __syncthreads();
     if (u >= units) break;
-    BuildUnit(A, Vv, Cc, Bt, Bt.queue[q].items[u / kChunksPerSeg], static_cast<int>(u % kChunksPerSeg), base_s);
+    BuildUnit(A, Vv, Cc, Bt, Q.items[u / kChunksPerSeg], static_cast<int>(u % kChunksPerSeg), base_s);
   }
 }
 
@@ -543,8 +553,8 @@ __global__ void __launch_bounds__(kThreads) DrainKernel(AutView A, VocabView Vv,
   HelpBuild(A, Vv, Cc, Bt, q, base_s, &unit);
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(Bt.kernel_done, 1u) == gridDim.x - 1) {
-    *Bt.queue[q].n_items = 0u;
-    *Bt.queue[q].next_unit = 0u;
+    *QueueOf(Bt, q).n_items = 0u;
+    *QueueOf(Bt, q).next_unit = 0u;
     *Bt.kernel_done = 0u;
   }
 }
@@ -575,8 +585,8 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
   // ---- 0. the queue drained by the previous fill is free again (nobody
   // produces into it until the fill after next consumes it: 3-queue ring).
   if (F.reset >= 0 && seg == 0 && b == 0 && tid == 0) {
-    *Bt.queue[F.reset].n_items = 0u;
-    *Bt.queue[F.reset].next_unit = 0u;
+    *QueueOf(Bt, F.reset).n_items = 0u;
+    *QueueOf(Bt, F.reset).next_unit = 0u;
   }
 
   // ---- 1. help build (new contexts queued by the previous step).
@@ -585,7 +595,9 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
   // ---- 2. fill.  Independent loads first: structural word, slot -> {CI, CD count}.
   const uint32_t sw = (F.seg_counts != nullptr && tid < nwords) ? __ldg(Vv.structural + w0 + tid) : 0u;
   int slot = Bt.seq_slot[b];  // same address in every thread: one broadcast load
-  if (slot != -2) {
+  const bool wait = slot >= 0 && (slot & kSlotWait);
+  if (slot >= 0) slot &= ~kSlotWait;
+  if (wait) {
     if (tid == 0) {
       // Wait for the build of the slot's segment.  Units of this batch's
       // queue were all dequeued by running CTAs before any CTA got here, so

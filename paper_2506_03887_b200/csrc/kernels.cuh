@@ -16,6 +16,7 @@ constexpr int kSegTokens = kSegWords * 32;            // 8192 tokens per segment
 constexpr int kChunksPerSeg = kSegTokens / kThreads;  // build work units per segment
 constexpr int kMaxContext = 16;                       // max K
 constexpr int kWalkOverlay = 64;                      // per-thread pushed-entry overlay in a mask walk
+constexpr int kSlotWait = 1 << 30;                    // seq_slot flag: wait for the slot's build
 
 // Per-sequence device state: {depth, status, draws, reserved}.
 struct SeqState {
@@ -58,6 +59,7 @@ struct CacheView {
   uint32_t* cdb;                  // C*W
   int32_t* cd_cnt;                // C*nseg
   int32_t* seg_done;              // C*nseg completed build units (kChunksPerSeg = built)
+  int32_t* slot_built;            // C completed build units over all segments
   unsigned long long* counters;   // [0] slots, [1] segment builds, [2] private builds
   int32_t C;
   int32_t K;
@@ -76,7 +78,8 @@ struct BatchView {
   int32_t cap;
   int32_t B;
   int32_t nseg;
-  int32_t* seq_slot;        // B: cache slot, C+b = private row, -2 = not alive
+  int32_t* seq_slot;        // B: cache slot, C+b = private row, -2 = not alive; | kSlotWait
+                            //    when the slot's build may still be pending
   uint32_t* priv;           // B*W private (uncached) masks
   int32_t* priv_done;       // B*nseg build-completion counters of private rows
   BuildQueue queue[3];      // ring: lookups feed queue[p], fill drains it, the next fill resets it
