@@ -86,7 +86,7 @@ __device__ __forceinline__ int Lane4(const int4& q, int i) {
 // dynamic target read from below it, makes the outcome kUnknown.  Because
 // arbitration is first-match, an unknown earlier candidate is also unknown.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
+__device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
                          bool complete) {
   int32_t loc[kWalkOverlay];
   int nl = 0;
@@ -290,7 +290,7 @@ __device__ void AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, i
 // ---------------------------------------------------------------------------
 // Build unit: 256 tokens of one (slot, segment) item, one per thread.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt,
+__device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt,
                           const int4 it, int chunk, int32_t* base_s) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot = it.x, seg = it.y, b = it.z;
@@ -360,7 +360,7 @@ __device__ void HelpBuild(const AutView& A, const VocabView& Vv, const CacheView
 // Warp-level sampler + accept (+ lookup) of one sequence.
 // ---------------------------------------------------------------------------
 // Synthetic stream; identical rule in oracle/gmask_port.c.
-__device__ __noinline__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row, const int32_t* counts,
+__device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row, const int32_t* counts,
                                 unsigned long long seed, uint32_t draw, int lane) {
   int na = 0, ns = 0;
   for (int s = lane; s < Vv.nseg; s += 32) {
@@ -432,7 +432,7 @@ __device__ __noinline__ int SampleStreamWarp(const VocabView& Vv, int b, const u
 
 // Engine::Step over the bytes of `tok` (EOS = V) on the device stack; then
 // optional restart and (do_lookup) the context slot of the next fill.
-__device__ __noinline__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int b,
+__device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int b,
                            SeqState st, int tok, int32_t* status_out, int restart, int lookup_queue, int lane) {
   int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
   if (tok >= 0 && st.status == kAlive) {
