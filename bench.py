@@ -324,7 +324,8 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{args.grammar}:{args.vocab}:{B}")
+            entry = json.load(open(tpath)).get(f"{args.grammar}:{args.vocab}:{B}")
+            traffic = entry["dram_bytes_per_launch"] if entry else None
         except Exception:
             traffic = None
 

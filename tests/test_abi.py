@@ -128,3 +128,17 @@ def test_synth_vocab_shape():
     assert s.shape == ((32001 + 31) // 32,)
     n = sum(bin(int(x)).count("1") for x in s)
     assert n == sum(1 for t in v if any(c in b'{}[],:"' for c in t))
+
+
+def test_cpp_wrapper_compiles_against_the_abi(tmp_path):
+    """include/pre3/device_engine.hpp (the reference-side C++ binding) builds
+    and links against libpre3gmask.so."""
+    import subprocess
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "pre3/device_engine.hpp"\n'
+                   'int main(){ return gm_abi_version() == GM_ABI_VERSION ? 0 : 1; }\n')
+    lib_dir = os.path.join(ROOT, "paper_2506_03887_b200")
+    exe = tmp_path / "t"
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                    "-L", lib_dir, "-lpre3gmask", f"-Wl,-rpath,{lib_dir}"], check=True)
+    assert subprocess.run([str(exe)]).returncode == 0
