@@ -89,6 +89,7 @@ struct gm_batch {
   unsigned long long* best = nullptr;     // greedy argmax packed keys
   int prod = 0;                           // queue the next fill drains
   int last_consumed = -1;                 // queue the previous fill drained (reset by the next)
+  int fill_seq = 0;                       // number of the next fill (heavy-list tags)
   bool slots_valid = false;               // seq_slot matches the stacks
   bool lookup_pending = false;            // queue[prod] got a lookup pass since the last fill
 
@@ -97,8 +98,10 @@ struct gm_batch {
     f->consume = prod;
     f->produce = (prod + 1) % 3;
     f->reset = last_consumed;
+    f->fill_no = fill_seq;
   }
   void EndFill(bool tail) {
+    ++fill_seq;
     last_consumed = prod;
     prod = (prod + 1) % 3;
     slots_valid = true;
@@ -270,6 +273,8 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.cd_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.seg_done = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.slot_built = DevAlloc<int32_t>(C, &e->owned);
+    c.cd_segmask = DevAlloc<uint32_t>(C, &e->owned);
+    Check(cudaMemset(c.cd_segmask, 0, C * 4), "memset");
     Check(cudaMemset(c.slot_built, 0, C * 4), "memset");
     c.counters = DevAlloc<unsigned long long>(8, &e->owned);
     Check(cudaMemset(c.slot_hash, 0, C * 8), "memset");
@@ -340,11 +345,17 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.seq_slot = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
     v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     v.priv_done = DevAlloc<int32_t>(bn, &b->owned);
+    v.heavy_index = DevAlloc<int32_t>(bn, &b->owned);
+    Check(cudaMemset(v.heavy_index, 0xff, bn * 4), "memset");
+    v.h_cap = static_cast<int32_t>(std::min<size_t>(bn, std::max<size_t>(64, 2 * static_cast<size_t>(batch))));
     Check(cudaMemset(v.priv_done, 0, bn * 4), "memset");
     for (int q = 0; q < 3; ++q) {
       v.queue[q].items = DevAlloc<int4>(2 * bn, &b->owned);
       v.queue[q].n_items = DevAlloc<unsigned int>(1, &b->owned);
       v.queue[q].next_unit = DevAlloc<unsigned int>(1, &b->owned);
+      v.queue[q].heavy = DevAlloc<int2>(static_cast<size_t>(v.h_cap), &b->owned);
+      v.queue[q].n_heavy = DevAlloc<unsigned int>(1, &b->owned);
+      Check(cudaMemset(v.queue[q].n_heavy, 0, 4), "memset");
       Check(cudaMemset(v.queue[q].n_items, 0, 4), "memset");
       Check(cudaMemset(v.queue[q].next_unit, 0, 4), "memset");
     }
@@ -485,7 +496,7 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, s), "lookup launch");
+    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
     pre3::FillArgs f{};
     f.bitmask = bitmask;
     f.ldw = ld_words;
@@ -511,7 +522,7 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
     if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, s), "lookup launch");
+    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
     pre3::FillArgs f{};
     f.bitmask = bitmask ? bitmask : b->scratch_mask;
     f.ldw = bitmask ? ld_words : e->W;
@@ -541,6 +552,7 @@ int gm_accept_tokens(gm_batch* b, const int32_t* tokens, int32_t* status_out, in
     g.restart = restart;
     g.do_accept = 1;
     g.lookup_queue = b->AcceptLookupQueue();
+    g.lookup_tag = b->fill_seq;
     Check(pre3::LaunchAccept(pre3::kSampleGiven, e->aut, e->vocab, e->cache, b->view, g,
                              static_cast<cudaStream_t>(stream)),
           "accept launch");
@@ -565,6 +577,7 @@ int gm_sample_stream_and_accept(gm_batch* b, const uint32_t* bitmask, int64_t ld
     g.tokens_out = tokens_out;
     g.do_accept = 1;
     g.lookup_queue = b->AcceptLookupQueue();
+    g.lookup_tag = b->fill_seq;
     Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, g,
                              static_cast<cudaStream_t>(stream)),
           "sample launch");
@@ -603,7 +616,7 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, s), "lookup launch");
+    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
     pre3::FillArgs f{};
     f.bitmask = bitmask ? bitmask : b->scratch_mask;
     f.ldw = bitmask ? ld_words : e->W;

@@ -255,12 +255,12 @@ __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int com
 
 // Context slot of sequence b for the next fill (seq_slot[b]); a new shared
 // slot or a private row queues one build item per segment into `q`.
-// `key` = the top min(depth, K) stack entries, top first.
-__device__ void AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, int b, const SeqState& st,
-                              int nseg, const int32_t* key) {
+// `key` = the top min(depth, K) stack entries, top first.  Returns seq_slot[b].
+__device__ int AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, int b, const SeqState& st,
+                             int nseg, const int32_t* key) {
   if (st.status != kAlive) {
     Bt.seq_slot[b] = -2;
-    return;
+    return -2;
   }
   const int n = min(st.depth, Cc.K);
   const int complete = st.depth <= Cc.K ? 1 : 0;
@@ -284,7 +284,45 @@ __device__ void AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, i
     // Existing slot: only one whose build is still queued needs a wait.
     wait = LoadAcquire(Cc.slot_built + slot) < nseg * kChunksPerSeg;
   }
-  Bt.seq_slot[b] = slot | (wait ? kSlotWait : 0);
+  const int flagged = slot | (wait ? kSlotWait : 0);
+  Bt.seq_slot[b] = flagged;
+  return flagged;
+}
+
+// heavy_index entry: (fill number mod 2^15) << 16 | heavy-list index.  Every
+// lookup pass rewrites all entries, so an entry is at most one fill stale and
+// the tag tells the fill whether it was written for it.
+__device__ __forceinline__ int HeavyTag(int fill_no, int idx) { return ((fill_no & 0x7fff) << 16) | idx; }
+
+// Segments of sequence b the next fill should schedule first: those with
+// context-dependent tokens (walks) or a pending build (waits).
+__device__ uint32_t HeavyMask(const CacheView& Cc, int flagged, int nseg) {
+  if (flagged < 0) return 0u;
+  const uint32_t all = nseg >= 32 ? 0xffffffffu : ((1u << nseg) - 1u);
+  if ((flagged & kSlotWait) || (flagged & ~kSlotWait) >= Cc.C) return all;
+  return LoadRelaxed(Cc.cd_segmask + (flagged & ~kSlotWait)) & all;
+}
+
+// Appends b's heavy segments to queue q's heavy list and records, for every
+// segment of b, its heavy-list index or -1 (exactly-once scheduling even when
+// two lookup passes feed one queue).  `lane`/`nl` split the stores over a warp.
+__device__ void PublishHeavy(const BatchView& Bt, int q, int tag, int b, uint32_t mask, int nseg, int lane,
+                             int nl) {
+  unsigned int base = 0;
+  if (lane == 0 && mask) base = atomicAdd(QueueOf(Bt, q).n_heavy, static_cast<unsigned int>(__popc(mask)));
+  if (nl > 1) base = __shfl_sync(0xffffffffu, base, 0);
+  const BuildQueue Q = QueueOf(Bt, q);
+  for (int s = lane; s < nseg; s += nl) {
+    int idx = -1;
+    if (s < 32 && ((mask >> s) & 1u)) {
+      const unsigned int k = base + static_cast<unsigned int>(__popc(mask & ((1u << s) - 1u)));
+      if (k < static_cast<unsigned int>(Bt.h_cap)) {
+        Q.heavy[k] = make_int2(b, s);
+        idx = HeavyTag(tag, static_cast<int>(k));
+      }
+    }
+    Bt.heavy_index[static_cast<long long>(b) * nseg + s] = idx;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -325,7 +363,10 @@ __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView
     } else {
       Cc.ci[static_cast<long long>(slot) * Vv.W + w] = acc;
       Cc.cdb[static_cast<long long>(slot) * Vv.W + w] = cd;
-      if (cd) atomicAdd(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg, __popc(cd));
+      if (cd) {
+        atomicAdd(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg, __popc(cd));
+        if (seg < 32) atomicOr(Cc.cd_segmask + slot, 1u << seg);
+      }
     }
   }
   __threadfence();
@@ -433,7 +474,8 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
 // Engine::Step over the bytes of `tok` (EOS = V) on the device stack; then
 // optional restart and (do_lookup) the context slot of the next fill.
 __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int b,
-                           SeqState st, int tok, int32_t* status_out, int restart, int lookup_queue, int lane) {
+                           SeqState st, int tok, int32_t* status_out, int restart, int lookup_queue, int lookup_tag,
+                           int lane) {
   int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
   if (tok >= 0 && st.status == kAlive) {
     const bool eos = tok == Vv.V;
@@ -524,17 +566,22 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
 #pragma unroll
     for (int i = 0; i < kMaxContext; ++i) key[i] = __shfl_sync(0xffffffffu, kv, i);
   }
+  int flagged = -2;
   if (lane == 0) {
     Bt.seq[b] = st;
     atomicAdd(Bt.counters + 3, 1ull);
-    if (lookup_queue >= 0) AssignSlotKey(Cc, Bt, lookup_queue, b, st, Vv.nseg, key);
+    if (lookup_queue >= 0) flagged = AssignSlotKey(Cc, Bt, lookup_queue, b, st, Vv.nseg, key);
+  }
+  if (lookup_queue >= 0) {
+    const uint32_t mask = __shfl_sync(0xffffffffu, lane == 0 ? HeavyMask(Cc, flagged, Vv.nseg) : 0u, 0);
+    PublishHeavy(Bt, lookup_queue, lookup_tag, b, mask, Vv.nseg, lane, 32);
   }
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, int q) {
+__global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, int q, int tag) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= Bt.B) return;
   const SeqState st = Bt.seq[b];
@@ -542,7 +589,8 @@ __global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, 
   int32_t key[kMaxContext];
   const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
   for (int i = 0; i < n; ++i) key[i] = stack[st.depth - 1 - i];
-  AssignSlotKey(Cc, Bt, q, b, st, Bt.nseg, key);
+  const int flagged = AssignSlotKey(Cc, Bt, q, b, st, Bt.nseg, key);
+  PublishHeavy(Bt, q, tag, b, HeavyMask(Cc, flagged, Bt.nseg), Bt.nseg, 0, 1);
 }
 
 // Builds everything queued in q, then empties q (used when a batch goes away
@@ -555,6 +603,7 @@ __global__ void __launch_bounds__(kThreads) DrainKernel(AutView A, VocabView Vv,
   if (threadIdx.x == 0 && atomicAdd(Bt.kernel_done, 1u) == gridDim.x - 1) {
     *QueueOf(Bt, q).n_items = 0u;
     *QueueOf(Bt, q).next_unit = 0u;
+    *QueueOf(Bt, q).n_heavy = 0u;
     *Bt.kernel_done = 0u;
   }
 }
@@ -575,19 +624,44 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
   __shared__ FillShared sh;
   extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int seg = blockIdx.x, b = blockIdx.y;
+
+  // ---- 0. the queue drained by the previous fill is free again (nobody
+  // produces into it until the fill after next consumes it: 3-queue ring).
+  if (F.reset >= 0 && blockIdx.x == 0 && tid == 0) {
+    const BuildQueue R = QueueOf(Bt, F.reset);
+    *R.n_items = 0u;
+    *R.next_unit = 0u;
+    *R.n_heavy = 0u;
+  }
+
+  // 1-D grid: h_cap "heavy pass" CTAs (segments with CD walks or pending
+  // builds, listed by the lookups) are scheduled first, then one CTA per
+  // (sequence, segment) that skips pairs the heavy pass owns.
+  int seg, b;
+  {
+    const int bid = static_cast<int>(blockIdx.x);
+    const int tag = HeavyTag(F.fill_no, 0);
+    if (bid < Bt.h_cap) {
+      const BuildQueue Qc = QueueOf(Bt, F.consume);
+      if (static_cast<unsigned int>(bid) >= LoadRelaxed(Qc.n_heavy)) return;
+      const int2 hv = Qc.heavy[bid];
+      b = hv.x;
+      seg = hv.y;
+      if (Bt.heavy_index[static_cast<long long>(b) * Vv.nseg + seg] != (tag | bid)) return;  // stale
+    } else {
+      const int j = bid - Bt.h_cap;
+      b = j / Vv.nseg;
+      seg = j - b * Vv.nseg;
+      const int hi = Bt.heavy_index[static_cast<long long>(b) * Vv.nseg + seg];
+      if (hi >= 0 && (hi & ~0xffff) == tag) return;  // owned by the heavy pass
+    }
+  }
   const int w0 = seg * kSegWords;
   const int nwords = min(Vv.W - w0, kSegWords);
   const int t0 = w0 * 32;
   const int t1 = min(Vv.V + 1, t0 + nwords * 32);
   static_assert(kSegWords == kThreads, "one mask word per thread");
 
-  // ---- 0. the queue drained by the previous fill is free again (nobody
-  // produces into it until the fill after next consumes it: 3-queue ring).
-  if (F.reset >= 0 && seg == 0 && b == 0 && tid == 0) {
-    *QueueOf(Bt, F.reset).n_items = 0u;
-    *QueueOf(Bt, F.reset).next_unit = 0u;
-  }
 
   // ---- 1. help build (new contexts queued by the previous step).
   HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);
@@ -820,7 +894,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
       }
       if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
       if (lane == 0) Bt.seq_arrive[b] = 0;
-      AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, lane);
+      AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, F.fill_no + 1, lane);
     }
   }
 }
@@ -854,7 +928,7 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
     if (lane == 0) Bt.seq[b].draws = st.draws;
     return;
   }
-  AcceptWarp(A, Vv, Cc, Bt, b, st, tok, G.status_out, G.restart, G.lookup_queue, lane);
+  AcceptWarp(A, Vv, Cc, Bt, b, st, tok, G.status_out, G.restart, G.lookup_queue, G.lookup_tag, lane);
 }
 
 __global__ void ResetKernel(AutView A, BatchView Bt) {
@@ -876,9 +950,9 @@ cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, cudaStream_t s) {
+cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
-  LookupKernel<<<(b.B + 127) / 128, 128, 0, s>>>(c, b, queue);
+  LookupKernel<<<(b.B + 127) / 128, 128, 0, s>>>(c, b, queue, tag);
   return cudaGetLastError();
 }
 
@@ -898,7 +972,7 @@ static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c
   if (dyn > 48 * 1024) {
     cudaFuncSetAttribute(FillKernel<MODE, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
   }
-  dim3 grid(static_cast<unsigned>(v.nseg), static_cast<unsigned>(b.B));
+  const unsigned grid = static_cast<unsigned>(b.h_cap) + static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
   FillKernel<MODE, TAIL><<<grid, kThreads, dyn, s>>>(a, v, c, b, f);
 }
 

@@ -60,16 +60,23 @@ struct CacheView {
   int32_t* cd_cnt;                // C*nseg
   int32_t* seg_done;              // C*nseg completed build units (kChunksPerSeg = built)
   int32_t* slot_built;            // C completed build units over all segments
+  uint32_t* cd_segmask;           // C: bit s set when segment s has context-dependent tokens
   unsigned long long* counters;   // [0] slots, [1] segment builds, [2] private builds
   int32_t C;
   int32_t K;
 };
 
 // Build work queue: items {slot, seg, seq, 0}; units = items * kChunksPerSeg.
+// Per-step work descriptor produced by the lookups for the next fill: build
+// items {slot, seg, seq, 0} (units = items * kChunksPerSeg) and the "heavy"
+// (sequence, segment) pairs — those with context-dependent tokens or a
+// pending build — that the fill schedules first.
 struct BuildQueue {
   int4* items;
   unsigned int* n_items;
   unsigned int* next_unit;
+  int2* heavy;
+  unsigned int* n_heavy;
 };
 
 struct BatchView {
@@ -82,6 +89,8 @@ struct BatchView {
                             //    when the slot's build may still be pending
   uint32_t* priv;           // B*W private (uncached) masks
   int32_t* priv_done;       // B*nseg build-completion counters of private rows
+  int32_t* heavy_index;     // B*nseg: index in the consumed heavy list, or -1
+  int32_t h_cap;            // heavy list capacity (= heavy-pass CTAs of a fill grid)
   BuildQueue queue[3];      // ring: lookups feed queue[p], fill drains it, the next fill resets it
   int32_t* seq_arrive;      // B: fill CTAs finished per sequence (fused tail)
   unsigned int* kernel_done;  // CTAs finished per launch (queue reset)
@@ -108,6 +117,7 @@ struct FillArgs {
   int consume;              // build queue drained by this launch
   int produce;              // build queue fed by the tail's lookups
   int reset;                // queue drained by the previous fill, emptied here (-1: none)
+  int fill_no;              // this fill's number (heavy_index tags; the tail tags fill_no + 1)
   int vec_ok;               // set by LaunchFill
 };
 
@@ -123,10 +133,11 @@ struct AcceptArgs {
   int32_t* tokens_out;
   int do_accept;     // 0: sample only
   int lookup_queue;  // >= 0: assign next-fill context slots into this queue
+  int lookup_tag;    // number of the fill that consumes it
 };
 
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s);
-cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, cudaStream_t s);
+cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s);
 cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,
                         cudaStream_t s);
 // Help-build + fill (+ bf16 -inf masking or greedy argmax) (+ fused tail).
