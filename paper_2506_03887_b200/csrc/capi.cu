@@ -345,8 +345,8 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.seq_slot = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
     v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     v.priv_done = DevAlloc<int32_t>(bn, &b->owned);
-    v.heavy_index = DevAlloc<int32_t>(bn, &b->owned);
-    Check(cudaMemset(v.heavy_index, 0xff, bn * 4), "memset");
+    v.heavy_index = DevAlloc<int32_t>(2 * bn, &b->owned);  // double-buffered by fill parity
+    Check(cudaMemset(v.heavy_index, 0xff, 2 * bn * 4), "memset");
     v.h_cap = static_cast<int32_t>(std::min<size_t>(bn, std::max<size_t>(64, 2 * static_cast<size_t>(batch))));
     Check(cudaMemset(v.priv_done, 0, bn * 4), "memset");
     for (int q = 0; q < 3; ++q) {

@@ -294,6 +294,12 @@ __device__ int AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, in
 // the tag tells the fill whether it was written for it.
 __device__ __forceinline__ int HeavyTag(int fill_no, int idx) { return ((fill_no & 0x7fff) << 16) | idx; }
 
+// heavy_index is double-buffered by fill parity: the fused tail of fill N
+// writes fill N+1's entries while fill N's CTAs may still read their own.
+__device__ __forceinline__ int32_t* HeavyIndex(const BatchView& Bt, int fill_no, int nseg) {
+  return Bt.heavy_index + static_cast<long long>(fill_no & 1) * Bt.B * nseg;
+}
+
 // Segments of sequence b the next fill should schedule first: those with
 // context-dependent tokens (walks) or a pending build (waits).
 __device__ uint32_t HeavyMask(const CacheView& Cc, int flagged, int nseg) {
@@ -321,7 +327,7 @@ __device__ void PublishHeavy(const BatchView& Bt, int q, int tag, int b, uint32_
         idx = HeavyTag(tag, static_cast<int>(k));
       }
     }
-    Bt.heavy_index[static_cast<long long>(b) * nseg + s] = idx;
+    HeavyIndex(Bt, tag, nseg)[static_cast<long long>(b) * nseg + s] = idx;
   }
 }
 
@@ -647,12 +653,12 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
       const int2 hv = Qc.heavy[bid];
       b = hv.x;
       seg = hv.y;
-      if (Bt.heavy_index[static_cast<long long>(b) * Vv.nseg + seg] != (tag | bid)) return;  // stale
+      if (HeavyIndex(Bt, F.fill_no, Vv.nseg)[static_cast<long long>(b) * Vv.nseg + seg] != (tag | bid)) return;
     } else {
       const int j = bid - Bt.h_cap;
       b = j / Vv.nseg;
       seg = j - b * Vv.nseg;
-      const int hi = Bt.heavy_index[static_cast<long long>(b) * Vv.nseg + seg];
+      const int hi = HeavyIndex(Bt, F.fill_no, Vv.nseg)[static_cast<long long>(b) * Vv.nseg + seg];
       if (hi >= 0 && (hi & ~0xffff) == tag) return;  // owned by the heavy pass
     }
   }

@@ -145,7 +145,7 @@ def test_json32k_stream_matches_golden(vectors, fused):
         assert got.stack == fin["stack"] and got.status == fin["status"]
 
 
-@pytest.mark.parametrize("K,fused", [(2, False), (8, False), (12, True)])
+@pytest.mark.parametrize("K,fused", [(2, False), (8, False), (12, True), (16, True), (16, False)])
 def test_json128k_stream_matches_port(K, fused):
     """Config 2 shape (JSON, 128,255 tokens): GPU decode loop == C port loop
     (tokens every step, final stacks) for 24 sequences x 16 steps."""
