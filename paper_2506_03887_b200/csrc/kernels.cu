@@ -625,7 +625,8 @@ struct FillShared {
 };
 
 template <int MODE, int TAIL>
-__global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+__global__ void __launch_bounds__(kThreads, TAIL == kTailNone ? 8 : 4) FillKernel(AutView A, VocabView Vv, CacheView Cc,
+                                                                                 BatchView Bt,
                                                           FillArgs F) {
   __shared__ FillShared sh;
   extern __shared__ int32_t stack_s[];
