@@ -259,7 +259,6 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     e->vocab.structural = e->structural;
     e->vocab.V = e->V;
     e->vocab.W = e->W;
-    e->vocab.Wp = (e->W + 7) / 8 * 8;
     e->vocab.nseg = e->nseg;
 
     const size_t C = static_cast<size_t>(o.context_slots);
@@ -269,11 +268,8 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.slot_hash = DevAlloc<unsigned long long>(C, &e->owned);
     c.slot_meta = DevAlloc<int32_t>(C, &e->owned);
     c.slot_keys = DevAlloc<int32_t>(C * static_cast<size_t>(pre3::kMaxContext), &e->owned);
-    const size_t Wp = static_cast<size_t>(e->vocab.Wp);
-    c.ci = DevAlloc<uint32_t>(C * Wp, &e->owned);
-    c.cdb = DevAlloc<uint32_t>(C * Wp, &e->owned);
-    Check(cudaMemset(c.ci, 0, C * Wp * 4), "memset");
-    Check(cudaMemset(c.cdb, 0, C * Wp * 4), "memset");
+    c.ci = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
+    c.cdb = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
     c.cd_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.seg_done = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.slot_built = DevAlloc<int32_t>(C, &e->owned);
@@ -347,8 +343,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     const size_t bn = static_cast<size_t>(std::max(batch, 1)) * static_cast<size_t>(e->nseg);
     v.nseg = e->nseg;
     v.seq_slot = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
-    v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->vocab.Wp), &b->owned);
-    Check(cudaMemset(v.priv, 0, static_cast<size_t>(batch) * static_cast<size_t>(e->vocab.Wp) * 4), "memset");
+    v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     v.priv_done = DevAlloc<int32_t>(bn, &b->owned);
     v.heavy_index = DevAlloc<int32_t>(2 * bn, &b->owned);  // double-buffered by fill parity
     Check(cudaMemset(v.heavy_index, 0xff, 2 * bn * 4), "memset");

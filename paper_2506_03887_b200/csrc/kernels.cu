@@ -20,8 +20,6 @@
 // Integer/bit work only: no tensor cores (nothing here is a contraction).
 #include <cuda/atomic>
 
-#include <algorithm>
-
 #include "kernels.cuh"
 
 namespace pre3 {
@@ -367,10 +365,10 @@ __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView
   const int w = seg * kSegWords + chunk * (kThreads / 32) + warp;
   if (lane == 0 && w < Vv.W) {
     if (priv) {
-      Bt.priv[static_cast<long long>(slot - Cc.C) * Vv.Wp + w] = acc;
+      Bt.priv[static_cast<long long>(slot - Cc.C) * Vv.W + w] = acc;
     } else {
-      Cc.ci[static_cast<long long>(slot) * Vv.Wp + w] = acc;
-      Cc.cdb[static_cast<long long>(slot) * Vv.Wp + w] = cd;
+      Cc.ci[static_cast<long long>(slot) * Vv.W + w] = acc;
+      Cc.cdb[static_cast<long long>(slot) * Vv.W + w] = cd;
       if (cd) {
         atomicAdd(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg, __popc(cd));
         if (seg < 32) atomicOr(Cc.cd_segmask + slot, 1u << seg);
@@ -617,76 +615,21 @@ __global__ void __launch_bounds__(kThreads) DrainKernel(AutView A, VocabView Vv,
 }
 
 // ---------------------------------------------------------------------------
-// FillKernel: one WARP per (sequence, segment) item, eight warps per CTA,
-// items assigned statically in the order [heavy list | all pairs], so every
-// item of a step is in flight at once (no CTA barriers between items) and
-// the CD walks / pending builds start first.
-// ---------------------------------------------------------------------------
-constexpr int kFillWarps = kThreads / 32;
-
 struct FillShared {
-  uint32_t mask[kFillWarps][kSegWords];  // per-warp item mask (8 KB)
-  uint32_t cd[kFillWarps][kSegWords];    // per-warp CD words (8 KB)
-  int pre[kFillWarps][32];               // per-warp lane prefix of CD counts
-  int unit;
+  uint32_t mask[kSegWords];
+  uint32_t cd[kSegWords];
+  int pre[kSegWords];
+  int scratch[kThreads / 32 + 1];
+  unsigned long long best[kThreads / 32];
+  int unit, last;
 };
 
-// Walks the item's context-dependent tokens (CD bits in sh_cd) against the
-// sequence's real stack and ORs the accepted ones into sh_mask (warp).
-__device__ __noinline__ int ResolveCd(const AutView A, const VocabView Vv, const int32_t* stack, int depth, int t0,
-                                      uint32_t* sh_mask, const uint32_t* sh_cd, int* sh_pre, unsigned int* err,
-                                      int lane) {
-  int c = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) c += __popc(sh_cd[lane * 8 + j]);
-  const int inc = WarpInclusiveScan(c, lane);
-  sh_pre[lane] = inc - c;
-  const int total = __shfl_sync(0xffffffffu, inc, 31);
-  __syncwarp();
-  for (int q = lane; q < total; q += 32) {
-    int lo = 0, hi = 31;  // owner lane: last with pre <= q
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (sh_pre[mid] <= q) lo = mid; else hi = mid - 1;
-    }
-    int r = q - sh_pre[lo];
-    int w = lo * 8;
-    for (;; ++w) {
-      const int pc = __popc(sh_cd[w]);
-      if (r < pc) break;
-      r -= pc;
-    }
-    uint32_t bits = sh_cd[w];
-    for (; r > 0; --r) bits &= bits - 1;
-    const int bit = __ffs(bits) - 1;
-    const int t = t0 + w * 32 + bit;
-    const int res = WalkToken(A, Vv, t, stack, depth, true);
-    if (res == kAccept) atomicOr(sh_mask + w, 1u << bit);
-    if (res == kOverflow) atomicOr(err, 1u);
-  }
-  __syncwarp();
-  return total;
-}
-
-// Uncached segment: every token walked against the real stack (warp).
-__device__ __noinline__ int DirectSegment(const AutView A, const VocabView Vv, const int32_t* stack, int depth,
-                                          int t0, int t1, uint32_t* sh_mask, unsigned int* err, int lane) {
-  for (int w = 0; w < kSegWords; ++w) {
-    const int t = t0 + w * 32 + lane;
-    const int r = t < t1 ? WalkToken(A, Vv, t, stack, depth, true) : kReject;
-    const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
-    if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(err, 1u);
-    if (lane == 0) sh_mask[w] = acc;
-  }
-  __syncwarp();
-  return t1 - t0;
-}
-
 template <int MODE, int TAIL>
-__global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+__global__ void __launch_bounds__(kThreads, TAIL == kTailNone ? 8 : 4) FillKernel(AutView A, VocabView Vv, CacheView Cc,
+                                                                                 BatchView Bt,
                                                           FillArgs F) {
   __shared__ FillShared sh;
-  extern __shared__ int32_t stack_s[];  // private-row builds only
+  extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // ---- 0. the queue drained by the previous fill is free again (nobody
@@ -697,237 +640,252 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
     *R.next_unit = 0u;
     *R.n_heavy = 0u;
   }
+
+  // 1-D grid: h_cap "heavy pass" CTAs (segments with CD walks or pending
+  // builds, listed by the lookups) are scheduled first, then one CTA per
+  // (sequence, segment) that skips pairs the heavy pass owns.
+  int seg, b;
+  {
+    const int bid = static_cast<int>(blockIdx.x);
+    const int tag = HeavyTag(F.fill_no, 0);
+    if (bid < Bt.h_cap) {
+      const BuildQueue Qc = QueueOf(Bt, F.consume);
+      if (static_cast<unsigned int>(bid) >= LoadRelaxed(Qc.n_heavy)) return;
+      const int2 hv = Qc.heavy[bid];
+      b = hv.x;
+      seg = hv.y;
+      if (HeavyIndex(Bt, F.fill_no, Vv.nseg)[static_cast<long long>(b) * Vv.nseg + seg] != (tag | bid)) return;
+    } else {
+      const int j = bid - Bt.h_cap;
+      b = j / Vv.nseg;
+      seg = j - b * Vv.nseg;
+      const int hi = HeavyIndex(Bt, F.fill_no, Vv.nseg)[static_cast<long long>(b) * Vv.nseg + seg];
+      if (hi >= 0 && (hi & ~0xffff) == tag) return;  // owned by the heavy pass
+    }
+  }
+  const int w0 = seg * kSegWords;
+  const int nwords = min(Vv.W - w0, kSegWords);
+  const int t0 = w0 * 32;
+  const int t1 = min(Vv.V + 1, t0 + nwords * 32);
+  static_assert(kSegWords == kThreads, "one mask word per thread");
+
+
   // ---- 1. help build (new contexts queued by the previous step).
   HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);
 
-  const BuildQueue Qc = QueueOf(Bt, F.consume);
-  const int n_heavy = min(static_cast<int>(LoadRelaxed(Qc.n_heavy)), Bt.h_cap);
-  const int total = n_heavy + Bt.B * Vv.nseg;
-  const int tag = HeavyTag(F.fill_no, 0);
-  const int32_t* hidx = HeavyIndex(Bt, F.fill_no, Vv.nseg);
-  uint32_t* smask = sh.mask[warp];
-  const int nwarps = gridDim.x * kFillWarps;
+  // ---- 2. fill.  Independent loads first: structural word, slot -> {CI, CD count}.
+  const uint32_t sw = (F.seg_counts != nullptr && tid < nwords) ? __ldg(Vv.structural + w0 + tid) : 0u;
+  int slot = Bt.seq_slot[b];  // same address in every thread: one broadcast load
+  const bool wait = slot >= 0 && (slot & kSlotWait);
+  if (slot >= 0) slot &= ~kSlotWait;
+  if (wait) {
+    if (tid == 0) {
+      // Wait for the build of the slot's segment.  Units of this batch's
+      // queue were all dequeued by running CTAs before any CTA got here, so
+      // they finish; a slot whose build sits in another batch's queue may
+      // not, so the wait is bounded and the segment is then filled directly.
+      const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg
+                                    : Bt.priv_done + static_cast<long long>(slot - Cc.C) * Vv.nseg + seg;
+      int ok = LoadAcquire(done) >= kChunksPerSeg;
+      if (!ok) {
+        unsigned long long t_start, t_now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        do {
+          __nanosleep(256);
+          ok = LoadAcquire(done) >= kChunksPerSeg;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+        } while (!ok && t_now - t_start < 2000000ull);
+      }
+      sh.unit = ok;
+    }
+    __syncthreads();
+    if (!sh.unit) slot = -3;  // direct fill
+  }
+  const int cd_cnt = (slot >= 0 && slot < Cc.C) ? __ldcg(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg) : 0;
+  uint32_t mword = 0u;
+  if (slot >= 0 && tid < nwords) {
+    const uint32_t* src = slot < Cc.C ? Cc.ci + static_cast<long long>(slot) * Vv.W
+                                      : Bt.priv + static_cast<long long>(slot - Cc.C) * Vv.W;
+    mword = __ldcg(src + w0 + tid);
+  }
+  sh.mask[tid] = mword;
+  unsigned long long n_walks = 0;
+  if (slot == -3) {
+    // Uncached: walk every token of the segment against the real stack.
+    const int depth = Bt.seq[b].depth;
+    const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+    for (int i = tid; i < depth; i += kThreads) stack_s[i] = gstack[i];
+    __syncthreads();
+    for (int base_t = 0; base_t < nwords * 32; base_t += kThreads) {
+      const int t = t0 + base_t + tid;
+      const int r = t < t1 ? WalkToken(A, Vv, t, stack_s, depth, true) : kReject;
+      const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
+      if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(Bt.err, 1u);
+      if (lane == 0) sh.mask[(base_t >> 5) + warp] = acc;
+    }
+    n_walks = t1 - t0;
+  } else if (cd_cnt > 0) {
+    // Context-dependent tokens: walk them against the sequence's real stack.
+    const uint32_t* cdsrc = Cc.cdb + static_cast<long long>(slot) * Vv.W + w0;
+    const int depth = Bt.seq[b].depth;
+    const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+    for (int i = tid; i < depth; i += kThreads) stack_s[i] = gstack[i];
+    const uint32_t x = tid < nwords ? __ldcg(cdsrc + tid) : 0u;
+    sh.cd[tid] = x;
+    int total = 0;
+    const int excl = BlockExclusiveScan(__popc(x), sh.scratch, &total);  // has barriers
+    sh.pre[tid] = excl;
+    __syncthreads();
+    for (int q = tid; q < total; q += kThreads) {
+      int lo = 0, hi = kThreads - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sh.pre[mid] <= q) lo = mid; else hi = mid - 1;
+      }
+      uint32_t bits = sh.cd[lo];
+      for (int r = q - sh.pre[lo]; r > 0; --r) bits &= bits - 1;
+      const int t = t0 + lo * 32 + (__ffs(bits) - 1);
+      const int r = WalkToken(A, Vv, t, stack_s, depth, true);
+      if (r == kAccept) atomicOr(&sh.mask[lo], 1u << ((t - t0) & 31));
+      if (r == kOverflow) atomicOr(Bt.err, 1u);
+    }
+    n_walks = total;
+  }
+  __syncthreads();
 
-  for (int it = blockIdx.x * kFillWarps + warp; it < total; it += nwarps) {
-    // ---- map the item (warp-uniform).
-    int b, seg;
-    if (it < n_heavy) {
-      const int2 hv = Qc.heavy[it];
-      b = hv.x;
-      seg = hv.y;
-      if (hidx[static_cast<long long>(b) * Vv.nseg + seg] != (tag | it)) continue;  // stale duplicate
-    } else {
-      const int j = it - n_heavy;
-      b = j / Vv.nseg;
-      seg = j - b * Vv.nseg;
-      const int hi = hidx[static_cast<long long>(b) * Vv.nseg + seg];
-      if (hi >= 0 && (hi & ~0xffff) == tag) continue;  // owned by the heavy list
+  // ---- outputs: bitmask words, sampler counts, logits.
+  if (F.bitmask != nullptr && tid < nwords) F.bitmask[static_cast<long long>(b) * F.ldw + w0 + tid] = sh.mask[tid];
+  if (F.seg_counts != nullptr) {
+    int ca = 0, cs = 0;
+    if (tid < nwords) {
+      uint32_t m = sh.mask[tid];
+      if (w0 + tid == (Vv.V >> 5)) m &= ~(1u << (Vv.V & 31));
+      ca = __popc(m);
+      cs = __popc(m & sw);
     }
-    const int w0 = seg * kSegWords;
-    const int nwords = min(Vv.W - w0, kSegWords);
-    const int t0 = w0 * 32;
-    const int t1 = min(Vv.V + 1, t0 + nwords * 32);
-
-    // ---- slot -> CI words (8 per lane), CD count; structural words.
-    int slot = Bt.seq_slot[b];
-    if (slot >= 0 && (slot & kSlotWait)) {
-      slot &= ~kSlotWait;
-      int ok = 1;
-      if (lane == 0) {
-        // Build of this slot's segment: units of this batch's queue were all
-        // dequeued by running CTAs before any warp got here, so they finish;
-        // a build sitting in another batch's queue may not, so the wait is
-        // bounded and the segment is then filled directly.
-        const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg
-                                      : Bt.priv_done + static_cast<long long>(slot - Cc.C) * Vv.nseg + seg;
-        ok = LoadAcquire(done) >= kChunksPerSeg;
-        if (!ok) {
-          unsigned long long t_start, t_now;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-          do {
-            __nanosleep(256);
-            ok = LoadAcquire(done) >= kChunksPerSeg;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
-          } while (!ok && t_now - t_start < 2000000ull);
-        }
-      }
-      if (!__shfl_sync(0xffffffffu, ok, 0)) slot = -3;  // direct fill
-    } else if (slot >= 0) {
-      slot &= ~kSlotWait;
+    ca = WarpSum(ca);
+    cs = WarpSum(cs);
+    if (lane == 0) {
+      sh.scratch[warp] = ca;
+      sh.pre[warp] = cs;
     }
-    const int wl = lane * 8;  // this lane's 8 words
-    uint4 m0 = make_uint4(0, 0, 0, 0), m1 = m0;
-    int cd_cnt = 0;
-    if (slot >= 0) {
-      const uint32_t* src = slot < Cc.C ? Cc.ci + static_cast<long long>(slot) * Vv.Wp
-                                        : Bt.priv + static_cast<long long>(slot - Cc.C) * Vv.Wp;
-      if (wl < nwords) {
-        const uint4* p = reinterpret_cast<const uint4*>(src + w0 + wl);
-        m0 = __ldcg(p);
-        m1 = __ldcg(p + 1);
-      }
-      if (slot < Cc.C) cd_cnt = __ldcg(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg);
+    __syncthreads();
+    if (tid == 0) {
+      int ta = 0, ts = 0;
+      for (int i = 0; i < kThreads / 32; ++i) ta += sh.scratch[i], ts += sh.pre[i];
+      F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 0] = ta;
+      F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = ts;
     }
-    reinterpret_cast<uint4*>(smask + wl)[0] = m0;
-    reinterpret_cast<uint4*>(smask + wl)[1] = m1;
-    __syncwarp();
-    int n_walks = 0;
-    if (slot == -3 || cd_cnt > 0) {
-      const int depth = Bt.seq[b].depth;
-      const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
-      if (slot == -3) {
-        n_walks = DirectSegment(A, Vv, gstack, depth, t0, t1, smask, Bt.err, lane);
-      } else {
-        uint32_t* scd = sh.cd[warp];
-        uint4 c0 = make_uint4(0, 0, 0, 0), c1 = c0;
-        if (wl < nwords) {
-          const uint4* p = reinterpret_cast<const uint4*>(Cc.cdb + static_cast<long long>(slot) * Vv.Wp + w0 + wl);
-          c0 = __ldcg(p);
-          c1 = __ldcg(p + 1);
-        }
-        reinterpret_cast<uint4*>(scd + wl)[0] = c0;
-        reinterpret_cast<uint4*>(scd + wl)[1] = c1;
-        __syncwarp();
-        n_walks = ResolveCd(A, Vv, gstack, depth, t0, smask, scd, sh.pre[warp], Bt.err, lane);
-      }
-    }
-
-    // ---- outputs: bitmask words (2 x 16 B per lane), sampler counts.
-    if (wl < nwords) {
-      m0 = reinterpret_cast<const uint4*>(smask + wl)[0];
-      m1 = reinterpret_cast<const uint4*>(smask + wl)[1];
-    }
-    if (F.bitmask != nullptr && wl < nwords) {
-      uint32_t* out = F.bitmask + static_cast<long long>(b) * F.ldw + w0 + wl;
-      if (F.bm_vec_ok && wl + 8 <= nwords) {
-        reinterpret_cast<uint4*>(out)[0] = m0;
-        reinterpret_cast<uint4*>(out)[1] = m1;
-      } else {
-        for (int j = 0; j < 8 && wl + j < nwords; ++j) out[j] = smask[wl + j];
-      }
-    }
-    if (F.seg_counts != nullptr) {
-      int ca = 0, cs = 0;
+  }
+  unsigned long long rd = 0, wr = 0;
+  if (MODE == kFillGreedy) {
+    const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
+    const int nchunks = (t1 - t0 + 7) >> 3;
+    unsigned long long mine = 0;
+    for (int c = tid; c < nchunks; c += kThreads) {
+      const int tb = t0 + c * 8;
+      const uint32_t byte = (sh.mask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
+      if (byte == 0u) continue;
+      const int valid = min(8, t1 - tb);
+      uint16_t vals[8];
+      if (valid == 8 && F.vec_ok) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(row + tb));
+        const uint16_t* pv = reinterpret_cast<const uint16_t*>(&v);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int w = wl + j;
-        if (w < nwords) {
-          uint32_t m = smask[w];
-          if (w0 + w == (Vv.V >> 5)) m &= ~(1u << (Vv.V & 31));
-          ca += __popc(m);
-          cs += __popc(m & __ldg(Vv.structural + w0 + w));
-        }
+        for (int j = 0; j < 8; ++j) vals[j] = pv[j];
+        rd += 16;
+      } else {
+        for (int j = 0; j < valid; ++j) vals[j] = row[tb + j];
+        rd += 2 * valid;
       }
-      ca = WarpSum(ca);
-      cs = WarpSum(cs);
-      if (lane == 0) {
-        F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 0] = ca;
-        F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = cs;
+      for (int j = 0; j < valid; ++j) {
+        if (!((byte >> j) & 1u)) continue;
+        const uint32_t bits = static_cast<uint32_t>(vals[j]) << 16;
+        const uint32_t key = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
+        const unsigned long long packed =
+            (static_cast<unsigned long long>(key) << 32) |
+            static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(tb + j));
+        mine = packed > mine ? packed : mine;
       }
     }
-    unsigned long long rd = 0, wr = 0;
-    if (MODE == kFillGreedy) {
-      const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
-      const int nchunks = (t1 - t0 + 7) >> 3;
-      unsigned long long mine = 0;
-      for (int c = lane; c < nchunks; c += 32) {
-        const int tb = t0 + c * 8;
-        const uint32_t byte = (smask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
-        if (byte == 0u) continue;
-        const int valid = min(8, t1 - tb);
-        uint16_t vals[8];
-        if (valid == 8 && F.vec_ok) {
-          const uint4 v = __ldcs(reinterpret_cast<const uint4*>(row + tb));
-          const uint16_t* pv = reinterpret_cast<const uint16_t*>(&v);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) vals[j] = pv[j];
-          rd += 16;
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, mine, o);
+      mine = y > mine ? y : mine;
+    }
+    if (lane == 0) sh.best[warp] = mine;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long m = 0;
+      for (int i = 0; i < kThreads / 32; ++i) m = sh.best[i] > m ? sh.best[i] : m;
+      if (m) atomicMax(F.best + b, m);
+    }
+  }
+
+  // ---- arrival: the sequence's last CTA runs the tail.  Only the mask
+  // words, counts and argmax partials must be visible to it, so the fence
+  // precedes the (bulk) logits stores below.
+  bool last = false;
+  if (TAIL != kTailNone) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sh.last = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
+    __syncthreads();
+    last = sh.last;
+  }
+
+  if (MODE == kFillMask && F.logits != nullptr) {
+    uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
+    const int nchunks = (t1 - t0 + 7) >> 3;
+    for (int c = tid; c < nchunks; c += kThreads) {
+      const int tb = t0 + c * 8;
+      const uint32_t byte = (sh.mask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
+      const int valid = min(8, t1 - tb);
+      if (valid == 8 && F.vec_ok) {
+        if (byte == 0xffu) continue;
+        if (byte == 0u) {
+          __stcs(reinterpret_cast<uint4*>(row + tb), make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u));
+          wr += 16;
         } else {
-          for (int j = 0; j < valid; ++j) vals[j] = row[tb + j];
-          rd += 2 * valid;
-        }
-        for (int j = 0; j < valid; ++j) {
-          if (!((byte >> j) & 1u)) continue;
-          const uint32_t bits = static_cast<uint32_t>(vals[j]) << 16;
-          const uint32_t key = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
-          const unsigned long long packed =
-              (static_cast<unsigned long long>(key) << 32) |
-              static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(tb + j));
-          mine = packed > mine ? packed : mine;
-        }
-      }
+          // Mixed chunk: store only the masked halves/pairs (no read of the
+          // row; L2 merges the partial sector).
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(0xffffffffu, mine, o);
-        mine = y > mine ? y : mine;
-      }
-      if (lane == 0 && mine) atomicMax(F.best + b, mine);
-    }
-
-    // ---- arrival (fused tail): only the mask words, counts and argmax
-    // partials must be visible to the sequence's last warp, so the fence
-    // precedes the bulk logits stores.
-    bool last = false;
-    if (TAIL != kTailNone) {
-      __threadfence();
-      __syncwarp();
-      int l = 0;
-      if (lane == 0) l = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
-      last = __shfl_sync(0xffffffffu, l, 0);
-    }
-
-    if (MODE == kFillMask && F.logits != nullptr) {
-      uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
-      const int nchunks = (t1 - t0 + 7) >> 3;
-      for (int c = lane; c < nchunks; c += 32) {
-        const int tb = t0 + c * 8;
-        const uint32_t byte = (smask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
-        const int valid = min(8, t1 - tb);
-        if (valid == 8 && F.vec_ok) {
-          if (byte == 0xffu) continue;
-          if (byte == 0u) {
-            __stcs(reinterpret_cast<uint4*>(row + tb), make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u));
-            wr += 16;
-          } else {
-            // Mixed chunk: store only the masked halves/pairs (no read of the
-            // row; L2 merges the partial sector).
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t pair = (byte >> (2 * j)) & 3u;
-              if (pair == 0u) {
-                __stcs(reinterpret_cast<uint32_t*>(row + tb) + j, 0xFF80FF80u);
-                wr += 4;
-              } else if (pair != 3u) {
-                __stcs(reinterpret_cast<unsigned short*>(row + tb + 2 * j + (pair == 2u ? 0 : 1)),
-                       static_cast<unsigned short>(0xFF80u));
-                wr += 2;
-              }
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t pair = (byte >> (2 * j)) & 3u;
+            if (pair == 0u) {
+              __stcs(reinterpret_cast<uint32_t*>(row + tb) + j, 0xFF80FF80u);
+              wr += 4;
+            } else if (pair != 3u) {
+              __stcs(reinterpret_cast<unsigned short*>(row + tb + 2 * j + (pair == 2u ? 0 : 1)),
+                     static_cast<unsigned short>(0xFF80u));
+              wr += 2;
             }
           }
-        } else {
-          for (int j = 0; j < valid; ++j) {
-            if (!((byte >> j) & 1u)) row[tb + j] = 0xFF80u;
-          }
-          wr += 2 * valid;
         }
+      } else {
+        for (int j = 0; j < valid; ++j) {
+          if (!((byte >> j) & 1u)) row[tb + j] = 0xFF80u;
+        }
+        wr += 2 * valid;
       }
     }
-    if (Bt.stats_enabled) {
-      rd = static_cast<unsigned long long>(WarpSum(static_cast<int>(rd)));
-      wr = static_cast<unsigned long long>(WarpSum(static_cast<int>(wr)));
-      if (lane == 0) {
-        if (rd | wr) {
-          atomicAdd(Bt.stats + 0, rd);
-          atomicAdd(Bt.stats + 1, wr);
-        }
-        if (n_walks) atomicAdd(Bt.stats + 2, static_cast<unsigned long long>(n_walks));
-        if (slot >= Cc.C) atomicAdd(Bt.stats + 4, 1ull);
-      }
+  }
+  if (Bt.stats_enabled) {
+    rd = static_cast<unsigned long long>(WarpSum(static_cast<int>(rd)));
+    wr = static_cast<unsigned long long>(WarpSum(static_cast<int>(wr)));
+    if (lane == 0 && (rd | wr)) {
+      atomicAdd(Bt.stats + 0, rd);
+      atomicAdd(Bt.stats + 1, wr);
     }
-    if (lane == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
+    if (tid == 0 && n_walks) atomicAdd(Bt.stats + 2, n_walks);
+    if (tid == 0 && slot >= Cc.C) atomicAdd(Bt.stats + 4, 1ull);
+  }
+  if (tid == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
 
-    // ---- tail: the sequence's last warp samples, accepts and looks up.
-    if (TAIL != kTailNone && last) {
+  // ---- 3. tail: the sequence's last CTA samples, accepts and looks up.
+  if (!last) return;
+  if (TAIL != kTailNone) {
+    if (warp == 0) {
       __threadfence();
       SeqState st = Bt.seq[b];
       int tok;
@@ -945,7 +903,6 @@ __global__ void __launch_bounds__(kThreads, 6) FillKernel(AutView A, VocabView V
       if (lane == 0) Bt.seq_arrive[b] = 0;
       AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, F.fill_no + 1, lane);
     }
-    __syncwarp();
   }
 }
 
@@ -1022,9 +979,7 @@ static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c
   if (dyn > 48 * 1024) {
     cudaFuncSetAttribute(FillKernel<MODE, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
   }
-  // One warp per item, all items of a step resident at once when they fit.
-  const unsigned items = static_cast<unsigned>(b.h_cap) + static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
-  const unsigned grid = std::min((items + kFillWarps - 1) / kFillWarps, static_cast<unsigned>(b.build_grid) * 2u);
+  const unsigned grid = static_cast<unsigned>(b.h_cap) + static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
   FillKernel<MODE, TAIL><<<grid, kThreads, dyn, s>>>(a, v, c, b, f);
 }
 
@@ -1032,7 +987,6 @@ cudaError_t LaunchFill(int mode, int tail, const AutView& a, const VocabView& v,
                        const BatchView& b, FillArgs f, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
   f.vec_ok = f.logits != nullptr && (f.ld % 8) == 0 && (reinterpret_cast<uintptr_t>(f.logits) % 16) == 0;
-  f.bm_vec_ok = f.bitmask != nullptr && (f.ldw % 4) == 0 && (reinterpret_cast<uintptr_t>(f.bitmask) % 16) == 0;
   const size_t dyn = static_cast<size_t>(b.cap) * sizeof(int32_t);
   if (mode == kFillGreedy) {
     LaunchFillT<kFillGreedy, kTailGreedy>(a, v, c, b, f, dyn, s);

@@ -43,7 +43,6 @@ struct VocabView {
   const uint32_t* structural;  // W words
   int32_t V;                   // regular tokens; EOS = V
   int32_t W;                   // ceil((V+1)/32)
-  int32_t Wp;                  // W rounded up to 8: row stride of CI / CD / private rows
   int32_t nseg;                // ceil(W / kSegWords)
 };
 
@@ -119,8 +118,7 @@ struct FillArgs {
   int produce;              // build queue fed by the tail's lookups
   int reset;                // queue drained by the previous fill, emptied here (-1: none)
   int fill_no;              // this fill's number (heavy_index tags; the tail tags fill_no + 1)
-  int vec_ok;               // set by LaunchFill (16-B logits stores)
-  int bm_vec_ok;            // set by LaunchFill (16-B bitmask stores)
+  int vec_ok;               // set by LaunchFill
 };
 
 struct AcceptArgs {
