@@ -625,7 +625,7 @@ struct FillShared {
 };
 
 template <int MODE, int TAIL>
-__global__ void __launch_bounds__(kThreads, TAIL == kTailNone ? 8 : 4) FillKernel(AutView A, VocabView Vv, CacheView Cc,
+__global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView Vv, CacheView Cc,
                                                                                  BatchView Bt,
                                                           FillArgs F) {
   __shared__ FillShared sh;
