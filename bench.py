@@ -58,6 +58,23 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
+def max_over_ranks(values, device, world):
+    """Max of each timing over all ranks (NCCL on the GPUs, gloo in tests)."""
+    if world <= 1:
+        return [float(v) for v in values]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t]
+
+
+def aggregate_rate(world, units_per_rank, seconds):
+    """Whole-job throughput: every rank's units over the slowest rank's time
+    (weak scaling: each rank owns its own sequences)."""
+    return world * units_per_rank / seconds
+
+
 def automaton_bytes(grammar: str) -> bytes:
     with open(os.path.join(ROOT, "tests", "golden", grammar + ".p3dpda"), "rb") as f:
         return f.read()
@@ -263,11 +280,8 @@ def main():
     elapsed_ms = e0.elapsed_time(e1)
     fill_ms = sum(a.elapsed_time(b) for a, b in ev) / K
     host_ms = (h1 - h0) * 1e3 / K
-    t = torch.tensor([elapsed_ms, fill_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms, fill_ms = float(t[0]), float(t[1])
-    value = world * B * K / (elapsed_ms / 1e3)
+    elapsed_ms, fill_ms = max_over_ranks([elapsed_ms, fill_ms], dev, world)
+    value = aggregate_rate(world, B * K, elapsed_ms / 1e3)
 
     # Device-counted logit bytes of one more fill (outside the timed region).
     batch.set_stats(True)
@@ -305,10 +319,8 @@ def main():
             e2e_step(i)
         t_e2e = time.perf_counter() - t0
         batch.check()
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * B * Ke / float(tt[0]), "unit": UNIT, "h2d_bytes_per_step": B * 4,
+        (t_e2e,) = max_over_ranks([t_e2e], dev, world)
+        e2e = {"value": aggregate_rate(world, B * Ke, t_e2e), "unit": UNIT, "h2d_bytes_per_step": B * 4,
                "d2h_bytes_per_step": B * W * 4 + B * 4, "steps": Ke,
                "path": "gm_accept_tokens(H2D ids) → gm_fill_and_mask_logits → gm_sample_stream → D2H bitmask+ids"}
 
