@@ -79,6 +79,12 @@ int gm_automaton_destroy(gm_automaton* a);
 /* info[0..7] = num_states, num_edges, initial_state, accept_state,
  * max |match_pop|, max |push|, dynamic edges, grammar_hash. */
 int gm_automaton_info(const gm_automaton* a, int64_t info[8]);
+/* Compile statistics of an automaton made by gm_automaton_compile (zero for
+ * loaded ones): stats[0] = two-terminal composites MergeEdges would build
+ * (optimizer.cpp:78-136; sequence-runner only, not part of the device
+ * automaton), stats[1] = rewritten pumping circuits (DetectCycles,
+ * dpda_builder.cpp:340-364), stats[2..3] = 0. */
+int gm_automaton_compile_stats(const gm_automaton* a, int64_t stats[4]);
 
 /* ------------------------------------------------------------ engine */
 typedef struct gm_engine_options {

@@ -105,6 +105,7 @@ def lib() -> ctypes.CDLL:
             "gm_automaton_save": ([P, P, SZ, ctypes.POINTER(SZ)], ctypes.c_int),
             "gm_automaton_destroy": ([P], ctypes.c_int),
             "gm_automaton_info": ([P, P], ctypes.c_int),
+            "gm_automaton_compile_stats": ([P, P], ctypes.c_int),
             "gm_engine_create": ([P, P, P, I32, P, ctypes.c_int, PP], ctypes.c_int),
             "gm_engine_destroy": ([P], ctypes.c_int),
             "gm_engine_info": ([P, P], ctypes.c_int),
@@ -216,6 +217,11 @@ class Automaton:
         keys = ["num_states", "num_edges", "initial_state", "accept_state", "max_match_pop",
                 "max_push", "dynamic_edges", "grammar_hash"]
         return dict(zip(keys, (int(x) for x in out)))
+
+    def compile_stats(self) -> dict:
+        out = np.zeros(4, np.int64)
+        _check(lib().gm_automaton_compile_stats(self._h, _ptr(out)))
+        return {"composites": int(out[0]), "cycles": int(out[1])}
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value and _lib is not None:

@@ -170,6 +170,15 @@ int gm_automaton_destroy(gm_automaton* a) {
   return GM_OK;
 }
 
+int gm_automaton_compile_stats(const gm_automaton* a, int64_t stats[4]) {
+  if (!a || !stats) return Fail(GM_ERR_USAGE, "null argument");
+  stats[0] = a->a.composites;
+  stats[1] = a->a.cycles;
+  stats[2] = 0;
+  stats[3] = 0;
+  return GM_OK;
+}
+
 int gm_automaton_info(const gm_automaton* a, int64_t info[8]) {
   if (!a || !info) return Fail(GM_ERR_USAGE, "null argument");
   int64_t maxpop = 0, maxpush = 0, dyn = 0;

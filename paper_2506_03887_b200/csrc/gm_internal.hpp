@@ -43,6 +43,10 @@ struct Automaton {
   std::vector<int32_t> shift_targets;  // S*256
   std::vector<Edge> edges;
   std::vector<int32_t> edge_begin;  // S+1
+  // Compile statistics (not serialized): two-terminal composites MergeEdges
+  // would build (sequence-runner only) and rewritten pumping circuits.
+  int64_t composites = 0;
+  int64_t cycles = 0;
 
   void Validate() const;  // throws Error(GM_ERR_CORRUPT_INPUT)
 };
