@@ -615,6 +615,333 @@ __global__ void __launch_bounds__(kThreads) DrainKernel(AutView A, VocabView Vv,
 }
 
 // ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kWarps = kThreads / 32;     // light items per fill CTA
+constexpr int kSpans = kSegWords / 32;    // 1024-token spans per segment
+
+// Greedy key of bf16 bits at token t: order-preserving float key in the high
+// word, 0xFFFFFFFF - t in the low word (ties -> lowest id).
+__device__ __forceinline__ unsigned long long GreedyKey(uint16_t v, int t) {
+  const uint32_t bits = static_cast<uint32_t>(v) << 16;
+  const uint32_t key = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
+  return (static_cast<unsigned long long>(key) << 32) | static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(t));
+}
+
+// Mask byte of chunk c = 32k + lane of a 1024-token span whose 32 mask words
+// are spread one per lane (`mword`): word c/4, byte c%4.
+__device__ __forceinline__ void SpanBytes(uint32_t mword, int lane, uint32_t byte[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = 32 * k + lane;
+    byte[k] = (__shfl_sync(0xffffffffu, mword, c >> 2) >> ((c & 3) * 8)) & 0xffu;
+  }
+}
+
+// In-place bf16 -inf over the span [tw, tw + 1024) ∩ [.., t1): 4 rounds of
+// 32 lanes x 16 B, each round one coalesced 512-B stretch of the row.  A fully
+// masked chunk is one -inf store (no read); a mixed chunk is read, blended
+// and written back whole (partial 2/4-B stores measured 1.5x slower: L2
+// merges them sector by sector and still fetches the rest of each sector
+// from HBM); an all-allowed chunk is skipped.
+__device__ __forceinline__ void MaskSpan(uint16_t* row, int tw, int t1, bool vec_ok, uint32_t mword, int lane,
+                                         unsigned long long* rd, unsigned long long* wr) {
+  uint32_t byte[4];
+  SpanBytes(mword, lane, byte);
+  if (vec_ok && tw + 1024 <= t1) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (byte[k] != 0u && byte[k] != 0xffu) {
+        v[k] = __ldcs(reinterpret_cast<const uint4*>(row + tw + (32 * k + lane) * 8));
+        *rd += 16;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (byte[k] == 0xffu) continue;
+      uint4 o = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+      if (byte[k] != 0u) {
+        // keep-mask per 32-bit pair: low half <- bit 2j, high half <- bit 2j+1
+        const uint32_t x = byte[k];
+        uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+        const uint32_t* pv = reinterpret_cast<const uint32_t*>(&v[k]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t keep = ((x >> (2 * j)) & 1u ? 0x0000FFFFu : 0u) | ((x >> (2 * j + 1)) & 1u ? 0xFFFF0000u : 0u);
+          po[j] = (pv[j] & keep) | (0xFF80FF80u & ~keep);
+        }
+      }
+      __stcs(reinterpret_cast<uint4*>(row + tw + (32 * k + lane) * 8), o);
+      *wr += 16;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int tb = tw + (32 * k + lane) * 8;
+      if (byte[k] == 0xffu || tb >= t1) continue;
+      const int valid = min(8, t1 - tb);
+      for (int j = 0; j < valid; ++j) {
+        if (!((byte[k] >> j) & 1u)) {
+          row[tb + j] = 0xFF80u;
+          *wr += 2;
+        }
+      }
+    }
+  }
+}
+
+// This lane's best allowed (key, token) of the span (0 when none).
+__device__ __forceinline__ unsigned long long ArgmaxSpan(const uint16_t* row, int tw, int t1, bool vec_ok,
+                                                         uint32_t mword, int lane, unsigned long long* rd) {
+  uint32_t byte[4];
+  SpanBytes(mword, lane, byte);
+  unsigned long long mine = 0;
+  if (vec_ok && tw + 1024 <= t1) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (byte[k]) {
+        v[k] = __ldcs(reinterpret_cast<const uint4*>(row + tw + (32 * k + lane) * 8));
+        *rd += 16;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!byte[k]) continue;
+      const uint16_t* pv = reinterpret_cast<const uint16_t*>(&v[k]);
+      const int tb = tw + (32 * k + lane) * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if ((byte[k] >> j) & 1u) {
+          const unsigned long long p = GreedyKey(pv[j], tb + j);
+          mine = p > mine ? p : mine;
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int tb = tw + (32 * k + lane) * 8;
+      if (!byte[k] || tb >= t1) continue;
+      const int valid = min(8, t1 - tb);
+      for (int j = 0; j < valid; ++j) {
+        if ((byte[k] >> j) & 1u) {
+          const unsigned long long p = GreedyKey(row[tb + j], tb + j);
+          *rd += 2;
+          mine = p > mine ? p : mine;
+        }
+      }
+    }
+  }
+  return mine;
+}
+
+__device__ __forceinline__ unsigned long long WarpMax64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+    v = y > v ? y : v;
+  }
+  return v;
+}
+
+// Bounded wait (one thread) for the build of (slot, seg).  Units of this
+// batch's queue were all dequeued by running CTAs before any fill item got
+// here, so they finish; a slot whose build sits in another batch's queue may
+// not, so the wait gives up after 2 ms and the caller fills directly.
+__device__ bool WaitBuilt(const CacheView& Cc, const BatchView& Bt, int slot, int seg, int nseg) {
+  const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * nseg + seg
+                                : Bt.priv_done + static_cast<long long>(slot - Cc.C) * nseg + seg;
+  bool ok = LoadAcquire(done) >= kChunksPerSeg;
+  if (!ok) {
+    unsigned long long t_start, t_now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    do {
+      __nanosleep(256);
+      ok = LoadAcquire(done) >= kChunksPerSeg;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+    } while (!ok && t_now - t_start < 2000000ull);
+  }
+  return ok;
+}
+
+// The sequence's last finished fill item: sample (stream or greedy), accept,
+// restart, and look up the next step's context slot.  One warp.
+template <int TAIL>
+__device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& Vv, const CacheView& Cc,
+                                             const BatchView& Bt, const FillArgs& F, int b, int lane) {
+  __threadfence();
+  SeqState st = Bt.seq[b];
+  int tok;
+  if (TAIL == kTailGreedy) {
+    const unsigned long long p = __ldcg(F.best + b);
+    tok = p ? static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(p)) : -1;
+    if (lane == 0) F.best[b] = 0ull;
+  } else {
+    tok = SampleStreamWarp(Vv, b, F.bitmask + static_cast<long long>(b) * F.ldw,
+                           F.seg_counts + static_cast<long long>(b) * Vv.nseg * 2, F.seed, st.draws, lane);
+    st.draws += 1;
+    if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
+  }
+  if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
+  if (lane == 0) Bt.seq_arrive[b] = 0;
+  AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, F.fill_no + 1, lane);
+}
+
+// Light item: one warp fills one (sequence, segment) — the steady state (a
+// ready context slot, few or no context-dependent tokens).  Lane j owns mask
+// words j, 32+j, ..., 224+j of the segment (registers m[]); span i = words
+// [32i, 32i+32) = tokens t0 + [1024i, 1024i+1024).  No CTA barriers.
+template <int MODE, int TAIL>
+__device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv, const CacheView& Cc,
+                                          const BatchView& Bt, const FillArgs& F, int b, int seg, int slot,
+                                          int lane) {
+  const int w0 = seg * kSegWords;
+  const int nwords = min(Vv.W - w0, kSegWords);
+  const int t0 = w0 * 32;
+  const int t1 = min(Vv.V + 1, t0 + nwords * 32);
+  const bool wait = slot >= 0 && (slot & kSlotWait);
+  if (slot >= 0) slot &= ~kSlotWait;
+  if (wait) {
+    int ok = 0;
+    if (lane == 0) ok = WaitBuilt(Cc, Bt, slot, seg, Vv.nseg) ? 1 : 0;
+    if (!__shfl_sync(0xffffffffu, ok, 0)) slot = -3;  // direct fill
+  }
+  uint32_t m[kSpans];
+  int cd_cnt = 0;
+  if (slot >= 0) {
+    const uint32_t* src = slot < Cc.C ? Cc.ci + static_cast<long long>(slot) * Vv.W
+                                      : Bt.priv + static_cast<long long>(slot - Cc.C) * Vv.W;
+#pragma unroll
+    for (int i = 0; i < kSpans; ++i) {
+      const int w = 32 * i + lane;
+      m[i] = w < nwords ? __ldcg(src + w0 + w) : 0u;
+    }
+    if (slot < Cc.C) cd_cnt = __ldcg(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kSpans; ++i) m[i] = 0u;
+  }
+  int n_walks = 0;
+  if (slot == -3 || cd_cnt > 0) {
+    // Rare in the light pass (the lookups list such segments for the heavy
+    // pass; only a full heavy list lands them here): walk against the
+    // sequence's stack in HBM.
+    const int depth = Bt.seq[b].depth;
+    const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+    const uint32_t* cdsrc = Cc.cdb + static_cast<long long>(slot) * Vv.W + w0;
+#pragma unroll 1
+    for (int i = 0; i < kSpans; ++i) {
+      const int w = 32 * i + lane;
+      uint32_t add = 0u;
+      if (slot == -3) {
+#pragma unroll 1
+        for (int j = 0; j < 32; ++j) {  // word 32i+j: lane = bit
+          const int t = t0 + (32 * i + j) * 32 + lane;
+          const int r = t < t1 ? WalkToken(A, Vv, t, gstack, depth, true) : kReject;
+          const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
+          if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(Bt.err, 1u);
+          if (lane == j) add = acc;
+        }
+        n_walks += 32;
+      } else {
+        uint32_t x = w < nwords ? __ldcg(cdsrc + w) : 0u;
+        n_walks += __popc(x);
+        while (x) {
+          const int bit = __ffs(x) - 1;
+          x &= x - 1;
+          const int r = WalkToken(A, Vv, t0 + w * 32 + bit, gstack, depth, true);
+          if (r == kAccept) add |= 1u << bit;
+          if (r == kOverflow) atomicOr(Bt.err, 1u);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kSpans; ++k) {
+        if (k == i) m[k] |= add;
+      }
+    }
+  }
+
+  // ---- bitmask words and sampler counts.
+  const int eos_word = Vv.V >> 5;
+  int ca = 0, cs = 0;
+#pragma unroll
+  for (int i = 0; i < kSpans; ++i) {
+    const int w = 32 * i + lane;
+    if (w < nwords) {
+      if (F.bitmask != nullptr) F.bitmask[static_cast<long long>(b) * F.ldw + w0 + w] = m[i];
+      if (F.seg_counts != nullptr) {
+        uint32_t mm = m[i];
+        if (w0 + w == eos_word) mm &= ~(1u << (Vv.V & 31));
+        ca += __popc(mm);
+        cs += __popc(mm & __ldg(Vv.structural + w0 + w));
+      }
+    }
+  }
+  if (F.seg_counts != nullptr) {
+    ca = WarpSum(ca);
+    cs = WarpSum(cs);
+    if (lane == 0) {
+      F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 0] = ca;
+      F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = cs;
+    }
+  }
+  unsigned long long rd = 0, wr = 0;
+  if (MODE == kFillGreedy) {
+    const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
+    unsigned long long mine = 0;
+#pragma unroll 1
+    for (int i = 0; i < kSpans; ++i) {
+      const int tw = t0 + 1024 * i;
+      if (tw >= t1) break;
+      uint32_t mi = 0u;
+#pragma unroll
+      for (int k = 0; k < kSpans; ++k) mi = k == i ? m[k] : mi;
+      const unsigned long long p = ArgmaxSpan(row, tw, t1, F.vec_ok, mi, lane, &rd);
+      mine = p > mine ? p : mine;
+    }
+    mine = WarpMax64(mine);
+    if (lane == 0 && mine) atomicMax(F.best + b, mine);
+  }
+
+  // ---- arrival (fused tail): mask words, counts and argmax partials are
+  // made visible first; the bulk logits stores follow.
+  bool last = false;
+  if (TAIL != kTailNone) {
+    __threadfence();
+    __syncwarp();
+    int l = 0;
+    if (lane == 0) l = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
+    last = __shfl_sync(0xffffffffu, l, 0) != 0;
+  }
+  if (MODE == kFillMask && F.logits != nullptr) {
+    uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
+#pragma unroll
+    for (int i = 0; i < kSpans; ++i) {
+      const int tw = t0 + 1024 * i;
+      if (tw < t1) MaskSpan(row, tw, t1, F.vec_ok, m[i], lane, &rd, &wr);
+    }
+  }
+  if (Bt.stats_enabled) {
+    rd = static_cast<unsigned long long>(WarpSum(static_cast<int>(rd)));
+    wr = static_cast<unsigned long long>(WarpSum(static_cast<int>(wr)));
+    n_walks = WarpSum(n_walks);
+    if (lane == 0) {
+      if (rd | wr) {
+        atomicAdd(Bt.stats + 0, rd);
+        atomicAdd(Bt.stats + 1, wr);
+      }
+      if (n_walks) atomicAdd(Bt.stats + 2, static_cast<unsigned long long>(n_walks));
+      if (slot >= Cc.C) atomicAdd(Bt.stats + 4, 1ull);
+    }
+  }
+  if (lane == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
+  if (TAIL != kTailNone && last) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
+}
+
+}  // namespace
+
 struct FillShared {
   uint32_t mask[kSegWords];
   uint32_t cd[kSegWords];
@@ -624,15 +951,22 @@ struct FillShared {
   int unit, last;
 };
 
+// Grid: h_cap heavy CTAs, then ceil(B * nseg / kWarps) light CTAs.
+//  * Heavy CTA: one (sequence, segment) listed by the lookups — a segment
+//    with context-dependent tokens or a pending build — 256 threads: CD
+//    tokens are walked one per thread, a direct fill walks 256 tokens a round.
+//  * Light CTA: kWarps consecutive (sequence, segment) items, one per warp,
+//    skipping items the heavy pass owns (LightItem).
+// Every CTA first helps drain the build queue of new contexts (empty in the
+// steady state).
 template <int MODE, int TAIL>
-__global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView Vv, CacheView Cc,
-                                                                                 BatchView Bt,
+__global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                           FillArgs F) {
   __shared__ FillShared sh;
   extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // ---- 0. the queue drained by the previous fill is free again (nobody
+  // ---- the queue drained by the previous fill is free again (nobody
   // produces into it until the fill after next consumes it: 3-queue ring).
   if (F.reset >= 0 && blockIdx.x == 0 && tid == 0) {
     const BuildQueue R = QueueOf(Bt, F.reset);
@@ -640,125 +974,114 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     *R.next_unit = 0u;
     *R.n_heavy = 0u;
   }
+  const BuildQueue Qc = QueueOf(Bt, F.consume);
+  const int bid = static_cast<int>(blockIdx.x);
+  const int tag = HeavyTag(F.fill_no, 0);
+  const int32_t* hidx = HeavyIndex(Bt, F.fill_no, Vv.nseg);
 
-  // 1-D grid: h_cap "heavy pass" CTAs (segments with CD walks or pending
-  // builds, listed by the lookups) are scheduled first, then one CTA per
-  // (sequence, segment) that skips pairs the heavy pass owns.
-  int seg, b;
-  {
-    const int bid = static_cast<int>(blockIdx.x);
-    const int tag = HeavyTag(F.fill_no, 0);
-    if (bid < Bt.h_cap) {
-      const BuildQueue Qc = QueueOf(Bt, F.consume);
-      if (static_cast<unsigned int>(bid) >= LoadRelaxed(Qc.n_heavy)) return;
-      const int2 hv = Qc.heavy[bid];
-      b = hv.x;
-      seg = hv.y;
-      if (HeavyIndex(Bt, F.fill_no, Vv.nseg)[static_cast<long long>(b) * Vv.nseg + seg] != (tag | bid)) return;
-    } else {
-      const int j = bid - Bt.h_cap;
-      b = j / Vv.nseg;
-      seg = j - b * Vv.nseg;
-      const int hi = HeavyIndex(Bt, F.fill_no, Vv.nseg)[static_cast<long long>(b) * Vv.nseg + seg];
-      if (hi >= 0 && (hi & ~0xffff) == tag) return;  // owned by the heavy pass
+  if (bid >= Bt.h_cap) {
+    // ---- light pass.  Loads that only depend on (b, seg) are issued together.
+    const int item = (bid - Bt.h_cap) * kWarps + warp;
+    const bool in_range = item < Bt.B * Vv.nseg;
+    const int b = in_range ? item / Vv.nseg : 0;
+    const int seg = item - b * Vv.nseg;
+    int hi = -1, slot = -2;
+    if (in_range) {
+      hi = hidx[static_cast<long long>(b) * Vv.nseg + seg];
+      slot = Bt.seq_slot[b];
     }
+    const unsigned int n_items = LoadRelaxed(Qc.n_items);
+    if (n_items != 0u) HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);  // CTA-uniform
+    if (!in_range || (hi >= 0 && (hi & ~0xffff) == tag)) return;  // owned by the heavy pass
+    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, lane);
+    return;
   }
+
+  // ---- heavy pass.
+  if (static_cast<unsigned int>(bid) >= LoadRelaxed(Qc.n_heavy)) return;
+  const int2 hv = Qc.heavy[bid];
+  const int b = hv.x;
+  const int seg = hv.y;
+  const int hi = hidx[static_cast<long long>(b) * Vv.nseg + seg];
+  int slot = Bt.seq_slot[b];
+  const unsigned int n_items = LoadRelaxed(Qc.n_items);
+  if (hi != (tag | bid)) return;
   const int w0 = seg * kSegWords;
   const int nwords = min(Vv.W - w0, kSegWords);
   const int t0 = w0 * 32;
   const int t1 = min(Vv.V + 1, t0 + nwords * 32);
   static_assert(kSegWords == kThreads, "one mask word per thread");
 
+  if (n_items != 0u) HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);
 
-  // ---- 1. help build (new contexts queued by the previous step).
-  HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);
-
-  // ---- 2. fill.  Independent loads first: structural word, slot -> {CI, CD count}.
+  // Thread tid owns mask word w0 + tid (register `mword`).
   const uint32_t sw = (F.seg_counts != nullptr && tid < nwords) ? __ldg(Vv.structural + w0 + tid) : 0u;
-  int slot = Bt.seq_slot[b];  // same address in every thread: one broadcast load
   const bool wait = slot >= 0 && (slot & kSlotWait);
   if (slot >= 0) slot &= ~kSlotWait;
   if (wait) {
-    if (tid == 0) {
-      // Wait for the build of the slot's segment.  Units of this batch's
-      // queue were all dequeued by running CTAs before any CTA got here, so
-      // they finish; a slot whose build sits in another batch's queue may
-      // not, so the wait is bounded and the segment is then filled directly.
-      const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg
-                                    : Bt.priv_done + static_cast<long long>(slot - Cc.C) * Vv.nseg + seg;
-      int ok = LoadAcquire(done) >= kChunksPerSeg;
-      if (!ok) {
-        unsigned long long t_start, t_now;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-        do {
-          __nanosleep(256);
-          ok = LoadAcquire(done) >= kChunksPerSeg;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
-        } while (!ok && t_now - t_start < 2000000ull);
-      }
-      sh.unit = ok;
-    }
+    if (tid == 0) sh.unit = WaitBuilt(Cc, Bt, slot, seg, Vv.nseg) ? 1 : 0;
     __syncthreads();
     if (!sh.unit) slot = -3;  // direct fill
   }
-  const int cd_cnt = (slot >= 0 && slot < Cc.C) ? __ldcg(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg) : 0;
   uint32_t mword = 0u;
-  if (slot >= 0 && tid < nwords) {
+  int cd_cnt = 0;
+  if (slot >= 0) {
     const uint32_t* src = slot < Cc.C ? Cc.ci + static_cast<long long>(slot) * Vv.W
                                       : Bt.priv + static_cast<long long>(slot - Cc.C) * Vv.W;
-    mword = __ldcg(src + w0 + tid);
+    if (tid < nwords) mword = __ldcg(src + w0 + tid);
+    if (slot < Cc.C) cd_cnt = __ldcg(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg);
   }
-  sh.mask[tid] = mword;
   unsigned long long n_walks = 0;
-  if (slot == -3) {
-    // Uncached: walk every token of the segment against the real stack.
+  if (slot == -3 || cd_cnt > 0) {
+    sh.mask[tid] = mword;
     const int depth = Bt.seq[b].depth;
     const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
     for (int i = tid; i < depth; i += kThreads) stack_s[i] = gstack[i];
-    __syncthreads();
-    for (int base_t = 0; base_t < nwords * 32; base_t += kThreads) {
-      const int t = t0 + base_t + tid;
-      const int r = t < t1 ? WalkToken(A, Vv, t, stack_s, depth, true) : kReject;
-      const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
-      if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(Bt.err, 1u);
-      if (lane == 0) sh.mask[(base_t >> 5) + warp] = acc;
-    }
-    n_walks = t1 - t0;
-  } else if (cd_cnt > 0) {
-    // Context-dependent tokens: walk them against the sequence's real stack.
-    const uint32_t* cdsrc = Cc.cdb + static_cast<long long>(slot) * Vv.W + w0;
-    const int depth = Bt.seq[b].depth;
-    const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
-    for (int i = tid; i < depth; i += kThreads) stack_s[i] = gstack[i];
-    const uint32_t x = tid < nwords ? __ldcg(cdsrc + tid) : 0u;
-    sh.cd[tid] = x;
-    int total = 0;
-    const int excl = BlockExclusiveScan(__popc(x), sh.scratch, &total);  // has barriers
-    sh.pre[tid] = excl;
-    __syncthreads();
-    for (int q = tid; q < total; q += kThreads) {
-      int lo = 0, hi = kThreads - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sh.pre[mid] <= q) lo = mid; else hi = mid - 1;
+    if (slot == -3) {
+      // Uncached: walk every token of the segment against the real stack.
+      __syncthreads();
+      for (int base_t = 0; base_t < nwords * 32; base_t += kThreads) {
+        const int t = t0 + base_t + tid;
+        const int r = t < t1 ? WalkToken(A, Vv, t, stack_s, depth, true) : kReject;
+        const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
+        if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(Bt.err, 1u);
+        if (lane == 0) sh.mask[(base_t >> 5) + warp] = acc;
       }
-      uint32_t bits = sh.cd[lo];
-      for (int r = q - sh.pre[lo]; r > 0; --r) bits &= bits - 1;
-      const int t = t0 + lo * 32 + (__ffs(bits) - 1);
-      const int r = WalkToken(A, Vv, t, stack_s, depth, true);
-      if (r == kAccept) atomicOr(&sh.mask[lo], 1u << ((t - t0) & 31));
-      if (r == kOverflow) atomicOr(Bt.err, 1u);
+      n_walks = t1 - t0;
+    } else {
+      // Context-dependent tokens: walk them against the sequence's real stack.
+      const uint32_t* cdsrc = Cc.cdb + static_cast<long long>(slot) * Vv.W + w0;
+      const uint32_t x = tid < nwords ? __ldcg(cdsrc + tid) : 0u;
+      sh.cd[tid] = x;
+      int total = 0;
+      const int excl = BlockExclusiveScan(__popc(x), sh.scratch, &total);  // has barriers
+      sh.pre[tid] = excl;
+      __syncthreads();
+      for (int q = tid; q < total; q += kThreads) {
+        int lo = 0, hi2 = kThreads - 1;
+        while (lo < hi2) {
+          const int mid = (lo + hi2 + 1) >> 1;
+          if (sh.pre[mid] <= q) lo = mid; else hi2 = mid - 1;
+        }
+        uint32_t bits = sh.cd[lo];
+        for (int r = q - sh.pre[lo]; r > 0; --r) bits &= bits - 1;
+        const int t = t0 + lo * 32 + (__ffs(bits) - 1);
+        const int r = WalkToken(A, Vv, t, stack_s, depth, true);
+        if (r == kAccept) atomicOr(&sh.mask[lo], 1u << ((t - t0) & 31));
+        if (r == kOverflow) atomicOr(Bt.err, 1u);
+      }
+      n_walks = total;
     }
-    n_walks = total;
+    __syncthreads();
+    mword = sh.mask[tid];
   }
-  __syncthreads();
 
   // ---- outputs: bitmask words, sampler counts, logits.
-  if (F.bitmask != nullptr && tid < nwords) F.bitmask[static_cast<long long>(b) * F.ldw + w0 + tid] = sh.mask[tid];
+  if (F.bitmask != nullptr && tid < nwords) F.bitmask[static_cast<long long>(b) * F.ldw + w0 + tid] = mword;
   if (F.seg_counts != nullptr) {
     int ca = 0, cs = 0;
     if (tid < nwords) {
-      uint32_t m = sh.mask[tid];
+      uint32_t m = mword;
       if (w0 + tid == (Vv.V >> 5)) m &= ~(1u << (Vv.V & 31));
       ca = __popc(m);
       cs = __popc(m & sw);
@@ -777,42 +1100,13 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
       F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = ts;
     }
   }
+  // Warp w covers words [32w, 32w+32) of the segment = one 1024-token span.
   unsigned long long rd = 0, wr = 0;
+  const int tw = t0 + warp * 1024;
   if (MODE == kFillGreedy) {
     const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
-    const int nchunks = (t1 - t0 + 7) >> 3;
-    unsigned long long mine = 0;
-    for (int c = tid; c < nchunks; c += kThreads) {
-      const int tb = t0 + c * 8;
-      const uint32_t byte = (sh.mask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
-      if (byte == 0u) continue;
-      const int valid = min(8, t1 - tb);
-      uint16_t vals[8];
-      if (valid == 8 && F.vec_ok) {
-        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(row + tb));
-        const uint16_t* pv = reinterpret_cast<const uint16_t*>(&v);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) vals[j] = pv[j];
-        rd += 16;
-      } else {
-        for (int j = 0; j < valid; ++j) vals[j] = row[tb + j];
-        rd += 2 * valid;
-      }
-      for (int j = 0; j < valid; ++j) {
-        if (!((byte >> j) & 1u)) continue;
-        const uint32_t bits = static_cast<uint32_t>(vals[j]) << 16;
-        const uint32_t key = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
-        const unsigned long long packed =
-            (static_cast<unsigned long long>(key) << 32) |
-            static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(tb + j));
-        mine = packed > mine ? packed : mine;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long y = __shfl_xor_sync(0xffffffffu, mine, o);
-      mine = y > mine ? y : mine;
-    }
+    unsigned long long mine = tw < t1 ? ArgmaxSpan(row, tw, t1, F.vec_ok, mword, lane, &rd) : 0ull;
+    mine = WarpMax64(mine);
     if (lane == 0) sh.best[warp] = mine;
     __syncthreads();
     if (tid == 0) {
@@ -822,7 +1116,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     }
   }
 
-  // ---- arrival: the sequence's last CTA runs the tail.  Only the mask
+  // ---- arrival: the sequence's last item runs the tail.  Only the mask
   // words, counts and argmax partials must be visible to it, so the fence
   // precedes the (bulk) logits stores below.
   bool last = false;
@@ -833,42 +1127,8 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     __syncthreads();
     last = sh.last;
   }
-
-  if (MODE == kFillMask && F.logits != nullptr) {
-    uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
-    const int nchunks = (t1 - t0 + 7) >> 3;
-    for (int c = tid; c < nchunks; c += kThreads) {
-      const int tb = t0 + c * 8;
-      const uint32_t byte = (sh.mask[c >> 2] >> ((c & 3) * 8)) & 0xffu;
-      const int valid = min(8, t1 - tb);
-      if (valid == 8 && F.vec_ok) {
-        if (byte == 0xffu) continue;
-        if (byte == 0u) {
-          __stcs(reinterpret_cast<uint4*>(row + tb), make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u));
-          wr += 16;
-        } else {
-          // Mixed chunk: store only the masked halves/pairs (no read of the
-          // row; L2 merges the partial sector).
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t pair = (byte >> (2 * j)) & 3u;
-            if (pair == 0u) {
-              __stcs(reinterpret_cast<uint32_t*>(row + tb) + j, 0xFF80FF80u);
-              wr += 4;
-            } else if (pair != 3u) {
-              __stcs(reinterpret_cast<unsigned short*>(row + tb + 2 * j + (pair == 2u ? 0 : 1)),
-                     static_cast<unsigned short>(0xFF80u));
-              wr += 2;
-            }
-          }
-        }
-      } else {
-        for (int j = 0; j < valid; ++j) {
-          if (!((byte >> j) & 1u)) row[tb + j] = 0xFF80u;
-        }
-        wr += 2 * valid;
-      }
-    }
+  if (MODE == kFillMask && F.logits != nullptr && tw < t1) {
+    MaskSpan(F.logits + static_cast<long long>(b) * F.ld, tw, t1, F.vec_ok, mword, lane, &rd, &wr);
   }
   if (Bt.stats_enabled) {
     rd = static_cast<unsigned long long>(WarpSum(static_cast<int>(rd)));
@@ -881,31 +1141,8 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     if (tid == 0 && slot >= Cc.C) atomicAdd(Bt.stats + 4, 1ull);
   }
   if (tid == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
-
-  // ---- 3. tail: the sequence's last CTA samples, accepts and looks up.
-  if (!last) return;
-  if (TAIL != kTailNone) {
-    if (warp == 0) {
-      __threadfence();
-      SeqState st = Bt.seq[b];
-      int tok;
-      if (TAIL == kTailGreedy) {
-        const unsigned long long p = __ldcg(F.best + b);
-        tok = p ? static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(p)) : -1;
-        if (lane == 0) F.best[b] = 0ull;
-      } else {
-        tok = SampleStreamWarp(Vv, b, F.bitmask + static_cast<long long>(b) * F.ldw,
-                               F.seg_counts + static_cast<long long>(b) * Vv.nseg * 2, F.seed, st.draws, lane);
-        st.draws += 1;
-        if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
-      }
-      if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
-      if (lane == 0) Bt.seq_arrive[b] = 0;
-      AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, F.fill_no + 1, lane);
-    }
-  }
+  if (TAIL != kTailNone && last && warp == 0) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
 }
-
 // ---------------------------------------------------------------------------
 // AcceptKernel: one warp per sequence (standalone accept / sample).
 // ---------------------------------------------------------------------------
@@ -979,7 +1216,8 @@ static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c
   if (dyn > 48 * 1024) {
     cudaFuncSetAttribute(FillKernel<MODE, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
   }
-  const unsigned grid = static_cast<unsigned>(b.h_cap) + static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
+  const unsigned items = static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
+  const unsigned grid = static_cast<unsigned>(b.h_cap) + (items + kWarps - 1) / kWarps;
   FillKernel<MODE, TAIL><<<grid, kThreads, dyn, s>>>(a, v, c, b, f);
 }
 
