@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--vocab", type=int, default=128255, help="regular tokens (EOS adds one bit)")
     p.add_argument("--grammar", default="json")
     p.add_argument("--context-depth", type=int, default=12)
-    p.add_argument("--prewarm-steps", type=int, default=400,
+    p.add_argument("--prewarm-steps", type=int, default=2000,
                    help="context-cache preprocessing: synthetic decode steps (other seed) before timing")
     p.add_argument("--prewarm-batch", type=int, default=1024)
     p.add_argument("--stack-cap", type=int, default=1024)

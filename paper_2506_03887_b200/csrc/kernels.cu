@@ -86,8 +86,27 @@ __device__ __forceinline__ int Lane4(const int4& q, int i) {
 // dynamic target read from below it, makes the outcome kUnknown.  Because
 // arbitration is first-match, an unknown earlier candidate is also unknown.
 // ---------------------------------------------------------------------------
-__device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
-                         bool complete) {
+// Out of line (one copy of the code, shared by the build, heavy and light
+// paths: the fill kernel is i-cache bound otherwise); the automaton and
+// vocabulary arrays are passed as scalars so no parameter struct is copied to
+// local memory.
+__device__ __noinline__ int WalkTokenImpl(const uint32_t* state_any, const int32_t* rec_begin, const CandRec* recs,
+                                          const int32_t* rec_cond, const int32_t* rec_push, const int32_t* shift,
+                                          const int32_t* tok_off, const uint8_t* tok_bytes, int32_t V, int32_t t,
+                                          const int32_t* base, int nb, bool complete) {
+  const struct {
+    const uint32_t* state_any;
+    const int32_t* rec_begin;
+    const CandRec* recs;
+    const int32_t* rec_cond;
+    const int32_t* rec_push;
+    const int32_t* shift;
+  } A{state_any, rec_begin, recs, rec_cond, rec_push, shift};
+  const struct {
+    const int32_t* tok_off;
+    const uint8_t* tok_bytes;
+    int32_t V;
+  } Vv{tok_off, tok_bytes, V};
   int32_t loc[kWalkOverlay];
   int nl = 0;
   const bool eos = t == Vv.V;
@@ -168,6 +187,12 @@ __device__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const
     }
   }
   return kAccept;
+}
+
+__device__ __forceinline__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
+                                         bool complete) {
+  return WalkTokenImpl(A.state_any, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_off, Vv.tok_bytes,
+                       Vv.V, t, base, nb, complete);
 }
 
 __device__ __forceinline__ int WarpSum(int v) {
@@ -620,6 +645,16 @@ namespace {
 constexpr int kWarps = kThreads / 32;     // light items per fill CTA
 constexpr int kSpans = kSegWords / 32;    // 1024-token spans per segment
 
+// m[i] for a loop-variable i without indexing the register array (a
+// dynamic index would move it to local memory).
+template <int N>
+__device__ __forceinline__ uint32_t Pick(const uint32_t (&m)[N], int i) {
+  uint32_t v = 0u;
+#pragma unroll
+  for (int k = 0; k < N; ++k) v = k == i ? m[k] : v;
+  return v;
+}
+
 // Greedy key of bf16 bits at token t: order-preserving float key in the high
 // word, 0xFFFFFFFF - t in the low word (ties -> lowest id).
 __device__ __forceinline__ unsigned long long GreedyKey(uint16_t v, int t) {
@@ -675,12 +710,13 @@ __device__ __forceinline__ void MaskSpan(uint16_t* row, int tw, int t1, bool vec
       __stcs(reinterpret_cast<uint4*>(row + tw + (32 * k + lane) * 8), o);
       *wr += 16;
     }
-  } else {
-#pragma unroll
+  } else {  // last (partial) span or unaligned rows: rare, kept compact
+#pragma unroll 1
     for (int k = 0; k < 4; ++k) {
       const int tb = tw + (32 * k + lane) * 8;
       if (byte[k] == 0xffu || tb >= t1) continue;
       const int valid = min(8, t1 - tb);
+#pragma unroll 1
       for (int j = 0; j < valid; ++j) {
         if (!((byte[k] >> j) & 1u)) {
           row[tb + j] = 0xFF80u;
@@ -688,6 +724,52 @@ __device__ __forceinline__ void MaskSpan(uint16_t* row, int tw, int t1, bool vec
         }
       }
     }
+  }
+}
+
+// cp.async (LDGSTS) helpers: 16-B global -> shared copies that need no
+// registers while in flight.
+__device__ __forceinline__ void CpAsync16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void CpAsyncCommit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void CpAsyncWait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// Mixed chunks of a full span -> this lane's slots of a span buffer.
+__device__ __forceinline__ void SpanPrefetch(const uint16_t* row, int tw, uint32_t mword, int lane,
+                                             uint4 (*buf)[32]) {
+  uint32_t byte[4];
+  SpanBytes(mword, lane, byte);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (byte[k] != 0u && byte[k] != 0xffu) CpAsync16(&buf[k][lane], row + tw + (32 * k + lane) * 8);
+  }
+}
+
+// Stores of a full span whose mixed chunks were prefetched into `buf`.
+__device__ __forceinline__ void SpanStore(uint16_t* row, int tw, uint32_t mword, int lane, const uint4 (*buf)[32],
+                                          unsigned long long* rd, unsigned long long* wr) {
+  uint32_t byte[4];
+  SpanBytes(mword, lane, byte);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (byte[k] == 0xffu) continue;
+    uint4 o = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+    if (byte[k] != 0u) {
+      const uint32_t x = byte[k];
+      const uint4 v = buf[k][lane];
+      uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+      const uint32_t* pv = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t keep = ((x >> (2 * j)) & 1u ? 0x0000FFFFu : 0u) | ((x >> (2 * j + 1)) & 1u ? 0xFFFF0000u : 0u);
+        po[j] = (pv[j] & keep) | (0xFF80FF80u & ~keep);
+      }
+      *rd += 16;
+    }
+    __stcs(reinterpret_cast<uint4*>(row + tw + (32 * k + lane) * 8), o);
+    *wr += 16;
   }
 }
 
@@ -719,12 +801,13 @@ __device__ __forceinline__ unsigned long long ArgmaxSpan(const uint16_t* row, in
         }
       }
     }
-  } else {
-#pragma unroll
+  } else {  // last (partial) span or unaligned rows: rare, kept compact
+#pragma unroll 1
     for (int k = 0; k < 4; ++k) {
       const int tb = tw + (32 * k + lane) * 8;
       if (!byte[k] || tb >= t1) continue;
       const int valid = min(8, t1 - tb);
+#pragma unroll 1
       for (int j = 0; j < valid; ++j) {
         if ((byte[k] >> j) & 1u) {
           const unsigned long long p = GreedyKey(row[tb + j], tb + j);
@@ -796,7 +879,7 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
 template <int MODE, int TAIL>
 __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                           const BatchView& Bt, const FillArgs& F, int b, int seg, int slot,
-                                          int lane) {
+                                          int lane, uint4 (*span_buf)[4][32]) {
   const int w0 = seg * kSegWords;
   const int nwords = min(Vv.W - w0, kSegWords);
   const int t0 = w0 * 32;
@@ -828,6 +911,11 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     // Rare in the light pass (the lookups list such segments for the heavy
     // pass; only a full heavy list lands them here): walk against the
     // sequence's stack in HBM.
+    // m[] is parked in this warp's (still unused) span buffer during the
+    // walks so no register array is live across the out-of-line walk calls.
+    uint32_t* wbuf = reinterpret_cast<uint32_t*>(span_buf);
+#pragma unroll
+    for (int i = 0; i < kSpans; ++i) wbuf[32 * i + lane] = m[i];
     const int depth = Bt.seq[b].depth;
     const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
     const uint32_t* cdsrc = Cc.cdb + static_cast<long long>(slot) * Vv.W + w0;
@@ -856,11 +944,11 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
           if (r == kOverflow) atomicOr(Bt.err, 1u);
         }
       }
-#pragma unroll
-      for (int k = 0; k < kSpans; ++k) {
-        if (k == i) m[k] |= add;
-      }
+      wbuf[32 * i + lane] |= add;  // lane-private word
     }
+#pragma unroll
+    for (int i = 0; i < kSpans; ++i) m[i] = wbuf[32 * i + lane];
+    __syncwarp();  // the buffer is reused for logits chunks below
   }
 
   // ---- bitmask words and sampler counts.
@@ -917,10 +1005,25 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   }
   if (MODE == kFillMask && F.logits != nullptr) {
     uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
-#pragma unroll
+    // Full spans, two in flight: the mixed chunks of spans i+1 and i+2 are
+    // being copied (cp.async, no registers held) while span i is blended and
+    // stored.  Then a partial last span, if any.
+    const int nfull = F.vec_ok ? (t1 - t0) >> 10 : 0;
+    uint4(*buf)[4][32] = span_buf;  // [2][4][32] of this warp
+    if (nfull > 0) SpanPrefetch(row, t0, m[0], lane, buf[0]);
+    CpAsyncCommit();
+    if (nfull > 1) SpanPrefetch(row, t0 + 1024, m[1], lane, buf[1]);
+    CpAsyncCommit();
+#pragma unroll 1
     for (int i = 0; i < kSpans; ++i) {
-      const int tw = t0 + 1024 * i;
-      if (tw < t1) MaskSpan(row, tw, t1, F.vec_ok, m[i], lane, &rd, &wr);
+      if (i < nfull) {
+        CpAsyncWait1();  // span i's group is complete (only i+1's may pend)
+        SpanStore(row, t0 + 1024 * i, Pick(m, i), lane, buf[i & 1], &rd, &wr);
+        if (i + 2 < nfull) SpanPrefetch(row, t0 + 1024 * (i + 2), Pick(m, i + 2), lane, buf[i & 1]);
+        CpAsyncCommit();
+      } else if (t0 + 1024 * i < t1) {
+        MaskSpan(row, t0 + 1024 * i, t1, F.vec_ok, Pick(m, i), lane, &rd, &wr);
+      }
     }
   }
   if (Bt.stats_enabled) {
@@ -963,6 +1066,7 @@ template <int MODE, int TAIL>
 __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                           FillArgs F) {
   __shared__ FillShared sh;
+  __shared__ uint4 span_buf[kWarps][2][4][32];  // light pass: per-warp double buffer of mixed chunks (32 KB)
   extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -993,7 +1097,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     const unsigned int n_items = LoadRelaxed(Qc.n_items);
     if (n_items != 0u) HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);  // CTA-uniform
     if (!in_range || (hi >= 0 && (hi & ~0xffff) == tag)) return;  // owned by the heavy pass
-    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, lane);
+    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, lane, span_buf[warp]);
     return;
   }
 
@@ -1213,8 +1317,12 @@ cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c
 template <int MODE, int TAIL>
 static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
                         const FillArgs& f, size_t dyn, cudaStream_t s) {
-  if (dyn > 48 * 1024) {
+  // Static shared memory (span buffers) + the dynamic stack copy may pass the
+  // 48 KB default: opt in to what this launch needs (once per size).
+  static size_t opted = 0;
+  if (dyn > 8 * 1024 && dyn > opted) {
     cudaFuncSetAttribute(FillKernel<MODE, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    opted = dyn;
   }
   const unsigned items = static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
   const unsigned grid = static_cast<unsigned>(b.h_cap) + (items + kWarps - 1) / kWarps;

@@ -11,7 +11,7 @@ timeout 300 python bench.py --batch 1024 --no-e2e --no-cpu-baseline ${BENCH_ARGS
 python -c "
 import json; d=json.load(open('gpurun_out/bench1024.json')); print('b1024 value', int(d['value']), d['step_breakdown_us'], 'frac', round(d['roofline']['frac'],3))"
 if [ "${PROFILE:-1}" = "1" ]; then
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 450 -c 100 --csv --log-file gpurun_out/launches.csv python bench.py --steps 60 --warmup 40 --no-e2e --no-cpu-baseline ${BENCH_ARGS:-} > /dev/null 2>&1; echo "ncu list rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 2050 -c 100 --csv --log-file gpurun_out/launches.csv python bench.py --steps 60 --warmup 40 --no-e2e --no-cpu-baseline ${BENCH_ARGS:-} > /dev/null 2>&1; echo "ncu list rc=$?"
 python scripts/launches.py gpurun_out/launches.csv
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:FillKernel -s 450 -c 1 -o gpurun_out/prof_fill1024 -f python bench.py --batch 1024 --steps 20 --warmup 60 --no-e2e --no-cpu-baseline ${BENCH_ARGS:-} > gpurun_out/ncu_full.log 2>&1; echo "ncu fill rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:FillKernel -s 2050 -c 1 -o gpurun_out/prof_fill1024 -f python bench.py --batch 1024 --steps 20 --warmup 60 --no-e2e --no-cpu-baseline ${BENCH_ARGS:-} > gpurun_out/ncu_full.log 2>&1; echo "ncu fill rc=$?"
 fi
