@@ -41,6 +41,7 @@ def parse():
     p.add_argument("--vocab", type=int, default=128255, help="regular tokens (EOS adds one bit)")
     p.add_argument("--grammar", default="json")
     p.add_argument("--context-depth", type=int, default=12)
+    p.add_argument("--context-slots", type=int, default=8192, help="context-cache hash table slots (power of two)")
     p.add_argument("--prewarm-steps", type=int, default=2000,
                    help="context-cache preprocessing: synthetic decode steps (other seed) before timing")
     p.add_argument("--prewarm-batch", type=int, default=1024)
@@ -224,7 +225,8 @@ def main():
     dev = torch.device(f"cuda:{local}")
     flat = automaton_bytes(args.grammar)
     vocab = pk.synth_vocab(args.vocab)
-    eng = pk.DeviceEngine(pk.Automaton.load(flat), vocab, device=local, context_depth=args.context_depth)
+    eng = pk.DeviceEngine(pk.Automaton.load(flat), vocab, device=local, context_depth=args.context_depth,
+                          context_slots=args.context_slots)
     t_pre = time.perf_counter()
     if args.prewarm_steps > 0:
         eng.prewarm(args.prewarm_batch, args.prewarm_steps, seed=0xC0FFEE + rank)

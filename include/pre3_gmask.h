@@ -188,6 +188,12 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, 
  * [4] = private segment fills, [5] = 0. */
 int gm_batch_fill_stats(gm_batch* b, int64_t stats[6]);
 int gm_batch_set_stats(gm_batch* b, int32_t enable);
+/* Diagnostics: per-item timing records of later fill / accept launches into
+ * a device buffer of 4 * (capacity + 1) uint64 (NULL turns tracing off).
+ * trace[0] counts records; record i at trace[4*(i+1)] = {kind | seg << 8 |
+ * seq << 32, start ns, end ns, extra}; kind 1 light fill item, 2 heavy fill
+ * item, 3 fused tail, 4 accept.  The caller zeroes trace[0]. */
+int gm_batch_set_trace(gm_batch* b, uint64_t* trace, int32_t capacity);
 
 #ifdef __cplusplus
 }

@@ -120,6 +120,7 @@ def lib() -> ctypes.CDLL:
             "gm_batch_counters": ([P, P], ctypes.c_int),
             "gm_batch_fill_stats": ([P, P], ctypes.c_int),
             "gm_batch_set_stats": ([P, I32], ctypes.c_int),
+            "gm_batch_set_trace": ([P, P, I32], ctypes.c_int),
             "gm_fill_next_token_bitmask": ([P, P, I64, P], ctypes.c_int),
             "gm_fill_and_mask_logits": ([P, P, I64, P, I64, P, P], ctypes.c_int),
             "gm_accept_tokens": ([P, P, P, I32, P], ctypes.c_int),
@@ -391,6 +392,14 @@ class Batch:
         out = np.zeros(4, np.int64)
         _check(lib().gm_batch_counters(self._h, _ptr(out)))
         return dict(zip(["restarts", "draws", "fills", "accepts"], (int(x) for x in out)))
+
+    def set_trace(self, buf=None):
+        """Diagnostics: per-item timing records into a torch uint64/int64
+        device tensor of 4 * (capacity + 1) entries (None turns it off)."""
+        if buf is None:
+            _check(lib().gm_batch_set_trace(self._h, None, 0))
+        else:
+            _check(lib().gm_batch_set_trace(self._h, ctypes.c_void_p(buf.data_ptr()), buf.numel() // 4 - 1))
 
     def set_stats(self, enable: bool):
         _check(lib().gm_batch_set_stats(self._h, int(enable)))

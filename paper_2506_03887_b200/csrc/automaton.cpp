@@ -190,15 +190,14 @@ FlatLayout Flatten(const Automaton& a) {
         CandRec r{};
         r.cond_len = static_cast<int16_t>(e.match_pop.size());
         r.cond_off = cond_at[static_cast<size_t>(i)];
-        r.c1 = e.match_pop.size() > 1 ? e.match_pop[1] : -1;
-        r.c2 = e.match_pop.size() > 2 ? e.match_pop[2] : -1;
-        r.flags = 0;
+        for (int j = 0; j < 16; ++j) {
+          r.cond[j] = static_cast<size_t>(j) + 1 < e.match_pop.size() ? e.match_pop[static_cast<size_t>(j) + 1] : -1;
+        }
         if (e.dynamic) {
           align4(&f.rec_push);
           r.push_off = static_cast<int32_t>(f.rec_push.size());
           f.rec_push.insert(f.rec_push.end(), e.push.begin(), e.push.end());
           if (e.push.empty()) {
-            r.flags = 1;
             r.new_state = -1;
           } else {
             const int32_t tgt = a.shift_targets[static_cast<size_t>(e.push.back()) * 256 + static_cast<size_t>(t)];
@@ -211,15 +210,19 @@ FlatLayout Flatten(const Automaton& a) {
           r.push_len = static_cast<int16_t>(e.push.size());
           r.new_state = e.push.back();
         }
-        r.edge = i;
+        for (int j = 0; j < 4; ++j) r.push[j] = j < r.push_len ? f.rec_push[static_cast<size_t>(r.push_off + j)] : -1;
         f.max_cond = std::max<int32_t>(f.max_cond, r.cond_len);
-        f.max_push = std::max<int32_t>(f.max_push, r.push_len + (r.flags & 1));
+        f.max_push = std::max<int32_t>(f.max_push, r.push_len + (r.new_state < 0 ? 1 : 0));
         f.recs.push_back(r);
         f.state_any[static_cast<size_t>(s) * 9 + static_cast<size_t>(t >> 5)] |= 1u << (t & 31);
       }
     }
   }
   f.rec_begin[static_cast<size_t>(S) * 257] = static_cast<int32_t>(f.recs.size());
+  f.first.assign(static_cast<size_t>(S) * 257, CandRec{});
+  for (size_t i = 0; i + 1 < f.rec_begin.size(); ++i) {
+    if (f.rec_begin[i] < f.rec_begin[i + 1]) f.first[i] = f.recs[static_cast<size_t>(f.rec_begin[i])];
+  }
   if (f.recs.empty()) f.recs.push_back(CandRec{});
   // Tail padding: vector reads of the last list stay in bounds.
   f.rec_cond.insert(f.rec_cond.end(), 16, -1);

@@ -249,6 +249,7 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     pre3::FlatLayout f = pre3::Flatten(a->a);
     e->aut.rec_begin = DevUpload(f.rec_begin, &e->owned);
     e->aut.recs = DevUpload(f.recs, &e->owned);
+    e->aut.first = DevUpload(f.first, &e->owned);
     e->aut.rec_cond = DevUpload(f.rec_cond, &e->owned);
     e->aut.rec_push = DevUpload(f.rec_push, &e->owned);
     e->aut.shift = DevUpload(a->a.shift_targets, &e->owned);
@@ -349,6 +350,8 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.stats = DevAlloc<unsigned long long>(8, &b->owned);
     v.counters = DevAlloc<unsigned long long>(4, &b->owned);
     v.stats_enabled = 0;
+    v.trace = nullptr;
+    v.trace_cap = 0;
     const size_t bn = static_cast<size_t>(std::max(batch, 1)) * static_cast<size_t>(e->nseg);
     v.nseg = e->nseg;
     v.seq_slot = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
@@ -483,6 +486,13 @@ int gm_batch_fill_stats(gm_batch* b, int64_t stats[6]) {
     Check(cudaMemset(b->view.stats, 0, 64), "memset");
     return GM_OK;
   });
+}
+
+int gm_batch_set_trace(gm_batch* b, uint64_t* trace, int32_t capacity) {
+  if (!b || (trace && capacity <= 0)) return Fail(GM_ERR_USAGE, "bad trace buffer");
+  b->view.trace = reinterpret_cast<unsigned long long*>(trace);
+  b->view.trace_cap = trace ? capacity : 0;
+  return GM_OK;
 }
 
 int gm_batch_set_stats(gm_batch* b, int32_t enable) {

@@ -61,19 +61,21 @@ Automaton CompileGrammar(const std::string& text, bool aggregate, bool merge);
 // first entry (always the current state, dpda.hpp:45 `front() == source`),
 // the push sequence with a dynamic edge's shift target resolved for that
 // terminal when the push prefix is non-empty (optimizer.cpp:33-76,
-// runtime.cpp:159-164), and the resulting state.
+// runtime.cpp:159-164), and the resulting state; the first 16 condition
+// entries and 4 pushed states are inlined in the record.
 struct CandRec {
-  int16_t cond_len;   // full |match_pop| (entry 0 implicit)
+  int16_t cond_len;   // full |match_pop| (entry 0 = the source state, implicit)
   int16_t push_len;   // entries to push (resolved dynamic target included)
   int32_t cond_off;   // rec_cond index of entry 1 (entries 1..cond_len-1, top first)
   int32_t push_off;   // rec_push index (bottom first)
-  int32_t flags;      // bit0: dynamic with empty push prefix (target from the exposed top)
-  int32_t new_state;  // top after apply, -1 when bit0
-  int32_t c1;         // match_pop[1] (valid when cond_len > 1)
-  int32_t c2;         // match_pop[2] (valid when cond_len > 2)
-  int32_t edge;       // index into Automaton::edges (diagnostics)
+  int32_t new_state;  // top after apply; -1: dynamic with an empty push prefix
+                      // (target read from the exposed top at apply time)
+  int32_t push[4];    // first four pushed entries, bottom first (-1 padded)
+  int32_t cond[16];   // condition entries 1..16, top first (-1 padded)
 };
-static_assert(sizeof(CandRec) == 32, "CandRec layout");
+// 96 B = 6 x 16 B: one round trip of independent vector loads gives a
+// candidate's whole condition (|match_pop| <= 17) and push list (<= 4).
+static_assert(sizeof(CandRec) == 96, "CandRec layout");
 
 struct FlatLayout {
   std::vector<int32_t> rec_begin;  // S*257 + 1
@@ -81,6 +83,10 @@ struct FlatLayout {
   std::vector<int32_t> rec_cond;
   std::vector<int32_t> rec_push;
   std::vector<uint32_t> state_any;  // S*9: bytes with any candidate (8 words) + bit0 of word 8 = '$'
+  // Dense copy of each (state, terminal)'s first candidate (cond_len 0: none):
+  // the candidate that wins ~2/3 of steps arrives in the same round trip as
+  // the candidate range, so most byte steps cost one L2 round trip.
+  std::vector<CandRec> first;
   int32_t max_cond = 0, max_push = 0;
 };
 

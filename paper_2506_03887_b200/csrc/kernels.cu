@@ -38,20 +38,36 @@ __device__ __forceinline__ unsigned long long Mix64(unsigned long long x) {
   return x ^ (x >> 31);
 }
 
-__device__ __forceinline__ CandRec LoadRec(const CandRec* p) {
-  const int4 a = __ldg(reinterpret_cast<const int4*>(p));
-  const int4 b = __ldg(reinterpret_cast<const int4*>(p) + 1);
-  CandRec r;
-  r.cond_len = static_cast<int16_t>(a.x & 0xffff);
-  r.push_len = static_cast<int16_t>(a.x >> 16);
-  r.cond_off = a.y;
-  r.push_off = a.z;
-  r.flags = a.w;
-  r.new_state = b.x;
-  r.c1 = b.y;
-  r.c2 = b.z;
-  r.edge = b.w;
+// A candidate record in registers: header, first 4 pushed states, condition
+// entries 1..16 — six independent 16-B loads (one round trip).
+struct Rec {
+  int cond_len, push_len, cond_off, push_off, new_state;
+  int4 p;     // push[0..3]
+  int4 c[4];  // cond entries 1..16
+};
+
+__device__ __forceinline__ Rec LoadRec(const CandRec* rp) {
+  const int4* q = reinterpret_cast<const int4*>(rp);
+  const int4 h = __ldg(q);
+  Rec r;
+  r.p = __ldg(q + 1);
+#pragma unroll
+  for (int v = 0; v < 4; ++v) r.c[v] = __ldg(q + 2 + v);
+  r.cond_len = h.x & 0xffff;
+  r.push_len = h.x >> 16;
+  r.cond_off = h.y;
+  r.push_off = h.z;
+  r.new_state = h.w;
   return r;
+}
+
+__device__ __forceinline__ int Lane4(const int4& q, int i) {
+  return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w;
+}
+
+// Condition entry j (1-based, j <= 16 inline, else from the pool).
+__device__ __forceinline__ int CondEntry(const Rec& r, const int32_t* rec_cond, int j) {
+  return j <= 16 ? Lane4(r.c[(j - 1) >> 2], (j - 1) & 3) : __ldg(rec_cond + r.cond_off + j - 1);
 }
 
 // Device-scope relaxed load (L2; neither a stale L1 hit nor a system-scope
@@ -72,8 +88,25 @@ __device__ __forceinline__ BuildQueue QueueOf(const BatchView& Bt, int q) {
   return q == 0 ? Bt.queue[0] : (q == 1 ? Bt.queue[1] : Bt.queue[2]);
 }
 
-__device__ __forceinline__ int Lane4(const int4& q, int i) {
-  return i == 0 ? q.x : i == 1 ? q.y : i == 2 ? q.z : q.w;
+
+__device__ __forceinline__ unsigned long long NowNs() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Appends one diagnostics record (BatchView::trace); call from one thread.
+__device__ __forceinline__ void TraceEvent(const BatchView& Bt, int kind, int b, int seg, unsigned long long t0,
+                                           unsigned long long extra) {
+  if (Bt.trace == nullptr) return;
+  const unsigned long long i = atomicAdd(Bt.trace, 1ull);
+  if (i >= static_cast<unsigned long long>(Bt.trace_cap)) return;
+  unsigned long long* r = Bt.trace + 4 * (i + 1);
+  r[0] = static_cast<unsigned long long>(kind) | (static_cast<unsigned long long>(seg & 0xffffff) << 8) |
+         (static_cast<unsigned long long>(static_cast<uint32_t>(b)) << 32);
+  r[1] = t0;
+  r[2] = NowNs();
+  r[3] = extra;
 }
 
 // ---------------------------------------------------------------------------
@@ -90,18 +123,18 @@ __device__ __forceinline__ int Lane4(const int4& q, int i) {
 // paths: the fill kernel is i-cache bound otherwise); the automaton and
 // vocabulary arrays are passed as scalars so no parameter struct is copied to
 // local memory.
-__device__ __noinline__ int WalkTokenImpl(const uint32_t* state_any, const int32_t* rec_begin, const CandRec* recs,
+__device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* rec_begin, const CandRec* recs,
                                           const int32_t* rec_cond, const int32_t* rec_push, const int32_t* shift,
                                           const int32_t* tok_off, const uint8_t* tok_bytes, int32_t V, int32_t t,
                                           const int32_t* base, int nb, bool complete) {
   const struct {
-    const uint32_t* state_any;
+    const CandRec* first;
     const int32_t* rec_begin;
     const CandRec* recs;
     const int32_t* rec_cond;
     const int32_t* rec_push;
     const int32_t* shift;
-  } A{state_any, rec_begin, recs, rec_cond, rec_push, shift};
+  } A{first, rec_begin, recs, rec_cond, rec_push, shift};
   const struct {
     const int32_t* tok_off;
     const uint8_t* tok_bytes;
@@ -114,41 +147,35 @@ __device__ __noinline__ int WalkTokenImpl(const uint32_t* state_any, const int32
   const int nterm = eos ? 1 : __ldg(Vv.tok_off + t + 1) - off;
   const uint8_t* bytes = Vv.tok_bytes + off;
   int state = base[nb - 1];
+  int x_next = eos ? 256 : static_cast<int>(__ldg(bytes));
   for (int i = 0; i < nterm; ++i) {
-    const int x = eos ? 256 : static_cast<int>(__ldg(bytes + i));
-    if (!((__ldg(A.state_any + state * 9 + (x >> 5)) >> (x & 31)) & 1u)) return kReject;
-    const int cb = __ldg(A.rec_begin + state * 257 + x);
-    const int ce = __ldg(A.rec_begin + state * 257 + x + 1);
+    const int x = x_next;
+    if (i + 1 < nterm) x_next = static_cast<int>(__ldg(bytes + i + 1));  // off the state chain
+    // Candidates of (state, x) in arbitration order (the first one from the
+    // dense table, in the same round trip as the range); none rejects.
+    const int idx = state * 257 + x;
+    const int cb = __ldg(A.rec_begin + idx);
+    const int ce = __ldg(A.rec_begin + idx + 1);
+    Rec r = LoadRec(A.first + idx);
     int found = -1;
-    CandRec fr;
+    Rec fr;
     for (int c = cb; c < ce; ++c) {
-      const CandRec r = LoadRec(A.recs + c);
+      if (c > cb) r = LoadRec(A.recs + c);
       // ConditionMatches (runtime.cpp:123-131) for entries 1..k-1 (entry 0 is
-      // the current state); the list is read 16 entries per round with
-      // independent int4 loads.
+      // the current state) against the overlay, then the known base.
       int verdict = 1;  // 1 match, 0 no match, 2 unknown
-      const int4* cp = reinterpret_cast<const int4*>(A.rec_cond + r.cond_off);
-      for (int j0 = 1; j0 < r.cond_len && verdict == 1; j0 += 16) {
-        int4 q[4];
-        const int nvec = min(4, (r.cond_len - j0 + 3) >> 2);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) q[v] = v < nvec ? __ldg(cp + ((j0 - 1) >> 2) + v) : make_int4(-1, -1, -1, -1);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int j = j0 + u;
-          if (j >= r.cond_len || verdict != 1) break;
-          const int want = Lane4(q[u >> 2], u & 3);
-          int have;
-          if (j < nl) {
-            have = loc[nl - 1 - j];
-          } else if (j - nl < nb) {
-            have = base[nb - 1 - (j - nl)];
-          } else {
-            verdict = complete ? 0 : 2;  // reaches below the known stack
-            break;
-          }
-          if (have != want) verdict = 0;
+      for (int j = 1; j < r.cond_len && verdict == 1; ++j) {
+        const int want = CondEntry(r, A.rec_cond, j);
+        int have;
+        if (j < nl) {
+          have = loc[nl - 1 - j];
+        } else if (j - nl < nb) {
+          have = base[nb - 1 - (j - nl)];
+        } else {
+          verdict = complete ? 0 : 2;  // reaches below the known stack
+          break;
         }
+        if (have != want) verdict = 0;
       }
       if (verdict == 2) return kUnknown;  // every known entry matched so far
       if (verdict == 1) {
@@ -168,15 +195,8 @@ __device__ __noinline__ int WalkTokenImpl(const uint32_t* state_any, const int32
       nl = 0;
     }
     if (nl + fr.push_len + 1 > kWalkOverlay) return kOverflow;
-    const int4* pp = reinterpret_cast<const int4*>(A.rec_push + fr.push_off);
-    for (int j0 = 0; j0 < fr.push_len; j0 += 4) {
-      const int4 q = __ldg(pp + (j0 >> 2));
-      loc[nl++] = q.x;
-      if (j0 + 1 < fr.push_len) loc[nl++] = q.y;
-      if (j0 + 2 < fr.push_len) loc[nl++] = q.z;
-      if (j0 + 3 < fr.push_len) loc[nl++] = q.w;
-    }
-    if (fr.flags & 1) {
+    for (int j = 0; j < fr.push_len; ++j) loc[nl++] = j < 4 ? Lane4(fr.p, j) : __ldg(A.rec_push + fr.push_off + j);
+    if (fr.new_state < 0) {
       const int top = nl > 0 ? loc[nl - 1] : (nb > 0 ? base[nb - 1] : -1);
       if (top < 0) return complete ? kReject : kUnknown;
       state = __ldg(A.shift + top * 256 + x);
@@ -191,8 +211,109 @@ __device__ __noinline__ int WalkTokenImpl(const uint32_t* state_any, const int32
 
 __device__ __forceinline__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
                                          bool complete) {
-  return WalkTokenImpl(A.state_any, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_off, Vv.tok_bytes,
+  return WalkTokenImpl(A.first, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_off, Vv.tok_bytes,
                        Vv.V, t, base, nb, complete);
+}
+
+// The same walk done by one warp for one token (complete stacks only): lanes
+// test the candidate edges of each byte in parallel (FindEdge), so a byte step
+// costs about one round trip instead of a serial scan; the pushed overlay
+// lives in registers (lane i = overlay entry i, bottom first), the base stack
+// in shared or global memory.  Used where few tokens need walking and their
+// latency is on the critical path (context-dependent tokens of a step).
+// Returns kOverflow when the overlay would pass 32 entries (the caller then
+// repeats the walk with WalkToken).
+__device__ int WalkWarp(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb, int lane) {
+  const bool eos = t == Vv.V;
+  const int off = eos ? 0 : __ldg(Vv.tok_off + t);
+  const int nterm = eos ? 1 : __ldg(Vv.tok_off + t + 1) - off;
+  const int xb = (!eos && lane < nterm) ? static_cast<int>(__ldg(Vv.tok_bytes + off + lane)) : 256;
+  int ov = -1;  // overlay entry `lane`
+  int nl = 0;
+  int state = base[nb - 1];
+  for (int i = 0; i < nterm; ++i) {
+    const int xs = __shfl_sync(0xffffffffu, xb, i & 31);
+    const int x = eos ? 256 : (i < 32 ? xs : static_cast<int>(__ldg(Vv.tok_bytes + off + i)));
+    const int idx = state * 257 + x;
+    const int cb = __ldg(A.rec_begin + idx);
+    const int ce = __ldg(A.rec_begin + idx + 1);
+    Rec r;
+    r.cond_len = 0;
+    r.push_len = 0;
+    if (lane == 0) r = LoadRec(A.first + idx);
+    int win = -1;
+    for (int cbase = cb, round = 0; cbase < ce; cbase = round == 1 ? cb + 1 : cbase + 32) {
+      const int c = round == 0 ? (lane == 0 ? cb : ce) : cbase + lane;
+      if (round++ > 0) {
+        r.cond_len = 0;
+        r.push_len = 0;
+        if (c < ce) r = LoadRec(A.recs + c);
+      }
+      bool match = c < ce && r.cond_len <= nl + nb;
+#pragma unroll
+      for (int j = 1; j <= 16; ++j) {
+        const int sh = __shfl_sync(0xffffffffu, ov, (nl - 1 - j) & 31);
+        if (match && j < r.cond_len) {
+          const int have = j < nl ? sh : base[nb - 1 - (j - nl)];
+          if (have != Lane4(r.c[(j - 1) >> 2], (j - 1) & 3)) match = false;
+        }
+      }
+      for (int j = 17; j < r.cond_len && match; ++j) {  // long conditions: overlay (<= 32) or base
+        const int have = j < nl ? -2 : base[nb - 1 - (j - nl)];
+        const int want = __ldg(A.rec_cond + r.cond_off + j - 1);
+        match = (j < nl) ? true : have == want;
+      }
+      // An overlay entry deeper than 16 under a long condition: resolve it
+      // with warp-uniform shuffles (rare).
+      {
+        const int maxlen = __reduce_max_sync(0xffffffffu, match ? static_cast<unsigned>(r.cond_len) : 0u);
+        for (int j = 17; j < maxlen && j < nl; ++j) {
+          const int sh = __shfl_sync(0xffffffffu, ov, (nl - 1 - j) & 31);
+          if (match && j < r.cond_len && sh != __ldg(A.rec_cond + r.cond_off + j - 1)) match = false;
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, match);
+      if (m) {
+        win = __ffs(m) - 1;
+        break;
+      }
+    }
+    if (win < 0) return kReject;
+    if (i == nterm - 1) return kAccept;
+    const int cond_len = __shfl_sync(0xffffffffu, r.cond_len, win);
+    const int push_len = __shfl_sync(0xffffffffu, r.push_len, win);
+    const int push_off = __shfl_sync(0xffffffffu, r.push_off, win);
+    const int new_state = __shfl_sync(0xffffffffu, r.new_state, win);
+    const int p0 = __shfl_sync(0xffffffffu, r.p.x, win);
+    const int p1 = __shfl_sync(0xffffffffu, r.p.y, win);
+    const int p2 = __shfl_sync(0xffffffffu, r.p.z, win);
+    const int p3 = __shfl_sync(0xffffffffu, r.p.w, win);
+    if (cond_len <= nl) {
+      nl -= cond_len;
+    } else {
+      nb -= cond_len - nl;
+      nl = 0;
+    }
+    const int dyn = new_state < 0 ? 1 : 0;
+    if (nl + push_len + dyn > 32) return kOverflow;
+    const int j = lane - nl;  // pushed entry this lane receives
+    if (j >= 0 && j < push_len) {
+      ov = j == 0 ? p0 : j == 1 ? p1 : j == 2 ? p2 : j == 3 ? p3 : __ldg(A.rec_push + push_off + j);
+    }
+    nl += push_len;
+    if (dyn) {
+      const int sh = __shfl_sync(0xffffffffu, ov, (nl - 1) & 31);
+      const int top = nl > 0 ? sh : (nb > 0 ? base[nb - 1] : -1);
+      if (top < 0) return kReject;
+      state = __ldg(A.shift + top * 256 + x);
+      if (state < 0) return kReject;  // unreachable for validated automata
+      if (lane == nl) ov = state;
+      ++nl;
+    } else {
+      state = new_state;
+    }
+  }
+  return kAccept;
 }
 
 __device__ __forceinline__ int WarpSum(int v) {
@@ -429,19 +550,31 @@ __device__ void HelpBuild(const AutView& A, const VocabView& Vv, const CacheView
 }
 
 // ---------------------------------------------------------------------------
-// Warp-level sampler + accept (+ lookup) of one sequence.
+// Warp-level sampler + accept (+ lookup) of one sequence.  Everything here is
+// a chain of dependent L2 round trips, so the code is arranged to issue each
+// round trip's loads together: ~2 per token byte, 2 for the sampler, 2 for
+// the context lookup.
 // ---------------------------------------------------------------------------
 // Synthetic stream; identical rule in oracle/gmask_port.c.
 __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row, const int32_t* counts,
                                 unsigned long long seed, uint32_t draw, int lane) {
-  int na = 0, ns = 0;
-  for (int s = lane; s < Vv.nseg; s += 32) {
+  // Round trip 1: the per-segment counts (segments 0..31 stay in registers)
+  // and the EOS word.
+  int c_all = 0, c_str = 0;
+  if (lane < Vv.nseg) {
+    const int2 v = __ldcg(reinterpret_cast<const int2*>(counts) + lane);
+    c_all = v.x;
+    c_str = v.y;
+  }
+  const uint32_t eos_word = __ldcg(row + (Vv.V >> 5));
+  int na = c_all, ns = c_str;
+  for (int s = lane + 32; s < Vv.nseg; s += 32) {
     na += __ldcg(counts + 2 * s);
     ns += __ldcg(counts + 2 * s + 1);
   }
   na = WarpSum(na);
   ns = WarpSum(ns);
-  const bool eos = (__ldcg(row + (Vv.V >> 5)) >> (Vv.V & 31)) & 1u;
+  const bool eos = (eos_word >> (Vv.V & 31)) & 1u;
   const unsigned long long u =
       Mix64(Mix64(seed ^ (static_cast<unsigned long long>(b) * 0xD1B54A32D192ED03ull)) ^
             static_cast<unsigned long long>(draw));
@@ -455,7 +588,8 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
   int seg = -1;
   for (int s0 = 0; s0 < Vv.nseg && seg < 0; s0 += 32) {
     const int s = s0 + lane;
-    const int c = s < Vv.nseg ? __ldcg(counts + 2 * s + (use_s ? 1 : 0)) : 0;
+    int c = use_s ? c_str : c_all;
+    if (s0 > 0) c = s < Vv.nseg ? __ldcg(counts + 2 * s + (use_s ? 1 : 0)) : 0;
     const int inc = WarpInclusiveScan(c, lane);
     const int total = __shfl_sync(0xffffffffu, inc, 31);
     if (r < static_cast<uint32_t>(total)) {
@@ -467,9 +601,9 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
     }
   }
   if (seg < 0) return -1;
+  // Round trip 2: all of the segment's words (and structural words).
   const int w0 = seg * kSegWords;
   const int w1 = min(Vv.W, w0 + kSegWords);
-  // All of the segment's words are loaded up front (independent loads).
   uint32_t xs[kSegWords / 32];
 #pragma unroll
   for (int j = 0; j < kSegWords / 32; ++j) {
@@ -502,80 +636,238 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
   return -1;
 }
 
-// Engine::Step over the bytes of `tok` (EOS = V) on the device stack; then
-// optional restart and (do_lookup) the context slot of the next fill.
+// Warp-cooperative LookupSlot: same table protocol (64 linear probes from
+// the key hash; insert = CAS on the hash, key row, then meta with the ready
+// bit, release), but 32 probes are read in one round trip and a hit is
+// verified — key row, meta, build progress and CD segment mask — in one
+// more.  `kv` = key entry `lane` (lanes < n).  Returns the slot (-1: table
+// full, or the key is being published right now); *created when this warp
+// inserted it; *built / *segmask of an existing slot.
+__device__ int LookupSlotWarp(const CacheView& C, int kv, int n, int complete, int lane, bool* created, int* built,
+                              uint32_t* segmask) {
+  unsigned long long h = Mix64(0x5ca1ab1eull ^ static_cast<unsigned long long>(n | (complete << 8)));
+  for (int i = 0; i < n; ++i) h = Mix64(h ^ static_cast<uint32_t>(__shfl_sync(0xffffffffu, kv, i)));
+  h |= 1ull;  // KeyHash
+  const int meta_want = n | (complete << 8);
+  *created = false;
+  const unsigned long long cmask = static_cast<unsigned long long>(C.C - 1);
+  for (int base = 0; base < 64; base += 32) {
+    for (int attempt = 0; attempt < 8; ++attempt) {  // re-read a window after a lost insert race
+      const int i = static_cast<int>((h + static_cast<unsigned long long>(base + lane)) & cmask);
+      const unsigned long long cur = LoadRelaxed(C.slot_hash + i);
+      const unsigned hit = __ballot_sync(0xffffffffu, cur == h);
+      const unsigned empty = __ballot_sync(0xffffffffu, cur == 0ull);
+      unsigned cand = hit & (empty ? ((1u << (__ffs(empty) - 1)) - 1u) : 0xffffffffu);
+      while (cand) {
+        const int src = __ffs(cand) - 1;
+        cand &= cand - 1;
+        const int slot = static_cast<int>((h + static_cast<unsigned long long>(base + src)) & cmask);
+        int v = 0;
+        if (lane < n) v = __ldcg(C.slot_keys + slot * kMaxContext + lane);
+        else if (lane == 29) v = LoadAcquire(C.slot_meta + slot);
+        else if (lane == 30) v = LoadAcquire(C.slot_built + slot);
+        else if (lane == 31) v = static_cast<int>(LoadRelaxed(C.cd_segmask + slot));
+        const int m = __shfl_sync(0xffffffffu, v, 29);
+        const int bt = __shfl_sync(0xffffffffu, v, 30);
+        const int sm = __shfl_sync(0xffffffffu, v, 31);
+        if (!(m & (1 << 16))) return -1;  // being published: private row this time
+        if ((m & 0xffff) != meta_want) continue;
+        if (__all_sync(0xffffffffu, lane >= n || v == kv)) {
+          *built = bt;
+          *segmask = static_cast<uint32_t>(sm);
+          return slot;
+        }
+      }
+      if (!empty) break;  // no free slot in this window: probe the next one
+      const int src = __ffs(empty) - 1;
+      const int slot = static_cast<int>((h + static_cast<unsigned long long>(base + src)) & cmask);
+      int won = 0;
+      if (lane == 0) won = atomicCAS(C.slot_hash + slot, 0ull, h) == 0ull;
+      if (__shfl_sync(0xffffffffu, won, 0)) {
+        if (lane < kMaxContext) C.slot_keys[slot * kMaxContext + lane] = lane < n ? kv : -1;
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          atomic_i32 meta(C.slot_meta[slot]);
+          meta.store(meta_want | (1 << 16), cuda::memory_order_release);
+          atomicAdd(C.counters + 0, 1ull);
+        }
+        *created = true;
+        return slot;
+      }
+    }
+  }
+  return -1;
+}
+
+// AssignSlotKey for a warp: the context slot of sequence b for the next fill
+// (seq_slot[b]); a new shared slot or a private row queues one build item per
+// segment into queue q.  Returns the segments the next fill must schedule in
+// its heavy pass (CD tokens or a pending build).
+__device__ uint32_t AssignSlotWarp(const CacheView& Cc, const BatchView& Bt, int q, int b, const SeqState& st,
+                                   int nseg, int kv, int lane) {
+  if (st.status != kAlive) {
+    if (lane == 0) Bt.seq_slot[b] = -2;
+    return 0u;
+  }
+  const int n = min(st.depth, Cc.K);
+  const int complete = st.depth <= Cc.K ? 1 : 0;
+  bool created = false;
+  int built = 0;
+  uint32_t segmask = 0u;
+  int slot = LookupSlotWarp(Cc, kv, n, complete, lane, &created, &built, &segmask);
+  bool wait = true;
+  if (slot < 0 || created) {
+    // Slots are never reused, so a new slot's counters are still zero.
+    if (slot < 0) {
+      slot = Cc.C + b;
+      for (int s = lane; s < nseg; s += 32) Bt.priv_done[static_cast<long long>(b) * nseg + s] = 0;
+      __threadfence();  // zeroed counters visible before the items
+      __syncwarp();
+      if (lane == 0) atomicAdd(Cc.counters + 2, 1ull);
+    } else if (lane == 0) {
+      atomicAdd(Cc.counters + 1, static_cast<unsigned long long>(nseg));
+    }
+    const BuildQueue Q = QueueOf(Bt, q);
+    unsigned int at = 0;
+    if (lane == 0) at = atomicAdd(Q.n_items, static_cast<unsigned int>(nseg));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    for (int s = lane; s < nseg; s += 32) Q.items[at + s] = make_int4(slot, s, b, 0);
+  } else {
+    // Existing slot: only one whose build is still queued needs a wait.
+    wait = built < nseg * kChunksPerSeg;
+  }
+  if (lane == 0) Bt.seq_slot[b] = slot | (wait ? kSlotWait : 0);
+  const uint32_t all = nseg >= 32 ? 0xffffffffu : ((1u << nseg) - 1u);
+  return (wait || slot >= Cc.C) ? all : (segmask & all);
+}
+
+// Engine::Step over the bytes of `tok` (EOS = V) on the device stack
+// (runtime.cpp:177-186), one warp; then optional restart and (lookup_queue
+// >= 0) the context slot of the next fill.
+//  * Stack window: lane j holds entry j from the top for j < wv; after each
+//    Step the new window is rebuilt by shuffles from the pushed entries and
+//    the surviving old entries, so the stack is written but never re-read in
+//    the common case (conditions reaching past the window read HBM).
+//  * FindEdge (runtime.cpp:138-146): lanes test candidate edges in
+//    arbitration order, 32 per round; each candidate lane loads its record,
+//    condition list and first four pushed states in one round trip; the
+//    winner's fields are broadcast by shuffles (Apply, runtime.cpp:148-168).
 __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int b,
                            SeqState st, int tok, int32_t* status_out, int restart, int lookup_queue, int lookup_tag,
                            int lane) {
   int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+  unsigned long long t_ph = Bt.trace ? NowNs() : 0ull;
+  int depth = st.depth;
+  int topv = lane < depth ? stack[depth - 1 - lane] : -1;
+  int wv = min(depth, 32);
   if (tok >= 0 && st.status == kAlive) {
     const bool eos = tok == Vv.V;
     const int off = eos ? 0 : __ldg(Vv.tok_off + tok);
     const int nterm = eos ? 1 : __ldg(Vv.tok_off + tok + 1) - off;
     const uint8_t* bytes = Vv.tok_bytes + off;
-    int depth = st.depth;
-    // Top 32 stack entries, lane j holding entry j (0 = top): one coalesced load.
-    int topv = lane < depth ? stack[depth - 1 - lane] : -1;
+    const int xb = (!eos && lane < nterm) ? static_cast<int>(__ldg(bytes + lane)) : 256;
     for (int i = 0; i < nterm; ++i) {
-      const int x = eos ? 256 : static_cast<int>(__ldg(bytes + i));
+      const int xs = __shfl_sync(0xffffffffu, xb, i & 31);
+      const int x = eos ? 256 : (i < 32 ? xs : static_cast<int>(__ldg(bytes + i)));
       const int state = __shfl_sync(0xffffffffu, topv, 0);
-      const int cb = __ldg(A.rec_begin + state * 257 + x);
-      const int ce = __ldg(A.rec_begin + state * 257 + x + 1);
-      int found = -1;
-      CandRec fr;
-      for (int c0 = cb; c0 < ce && found < 0; c0 += 32) {
-        const int c = c0 + lane;
-        CandRec r;
-        r.cond_len = 0;
-        int4 q[4];
-        if (c < ce) {
-          r = LoadRec(A.recs + c);
-          const int4* cp = reinterpret_cast<const int4*>(A.rec_cond + r.cond_off);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) q[v] = 4 * v + 1 < r.cond_len ? __ldg(cp + v) : make_int4(-1, -1, -1, -1);
+      const int idx = state * 257 + x;
+      const int cb = __ldg(A.rec_begin + idx);
+      const int ce = __ldg(A.rec_begin + idx + 1);
+      int win = -1;
+      Rec r;
+      r.cond_len = 0;
+      r.push_len = 0;
+      if (lane == 0) r = LoadRec(A.first + idx);  // same round trip as the range
+      // Round 0: the first candidate (lane 0); then the rest, 32 per round.
+      for (int cbase = cb, round = 0; cbase < ce; cbase = round == 1 ? cb + 1 : cbase + 32) {
+        const int c = round == 0 ? (lane == 0 ? cb : ce) : cbase + lane;
+        if (round++ > 0) {
+          r.cond_len = 0;
+          r.push_len = 0;
+          if (c < ce) r = LoadRec(A.recs + c);
         }
         bool match = c < ce && r.cond_len <= depth;
-        // Entries 1..16 from the register window (lane-indexed shuffles).
+        bool far = false;  // condition entries outside the register window
 #pragma unroll
         for (int j = 1; j <= 16; ++j) {
           const int have = __shfl_sync(0xffffffffu, topv, j);
-          if (j < r.cond_len && have != Lane4(q[(j - 1) >> 2], (j - 1) & 3)) match = false;
+          if (j < r.cond_len) {
+            if (j < wv) {
+              if (have != Lane4(r.c[(j - 1) >> 2], (j - 1) & 3)) match = false;
+            } else {
+              far = true;
+            }
+          }
         }
-        for (int j = 17; j < r.cond_len && match; ++j) {  // long conditions: rare
-          match = stack[depth - 1 - j] == __ldg(A.rec_cond + r.cond_off + j - 1);
+        if (match && (far || r.cond_len > 17)) {
+          for (int j = 1; j < r.cond_len && match; ++j) {
+            if (j <= 16 && j < wv) continue;
+            match = stack[depth - 1 - j] == __ldg(A.rec_cond + r.cond_off + j - 1);
+          }
         }
         const unsigned m = __ballot_sync(0xffffffffu, match);
         if (m) {
-          const int src = __ffs(m) - 1;
-          found = c0 + src;
+          win = __ffs(m) - 1;
+          break;
         }
       }
-      if (found < 0) {
+      if (win < 0) {
         st.status = kDead;  // earlier bytes stay applied (runtime.cpp:179-183)
         break;
       }
-      fr = LoadRec(A.recs + found);
-      const int dyn = fr.flags & 1;
-      const int nd = depth - fr.cond_len + fr.push_len + dyn;
-      const int base = depth - fr.cond_len;
+      const int cond_len = __shfl_sync(0xffffffffu, static_cast<int>(r.cond_len), win);
+      const int push_len = __shfl_sync(0xffffffffu, static_cast<int>(r.push_len), win);
+      const int push_off = __shfl_sync(0xffffffffu, r.push_off, win);
+      const int dyn = __shfl_sync(0xffffffffu, r.new_state, win) < 0 ? 1 : 0;
+      const int p0 = __shfl_sync(0xffffffffu, r.p.x, win);
+      const int p1 = __shfl_sync(0xffffffffu, r.p.y, win);
+      const int p2 = __shfl_sync(0xffffffffu, r.p.z, win);
+      const int p3 = __shfl_sync(0xffffffffu, r.p.w, win);
+      const int base = depth - cond_len;
+      const int P = push_len + dyn;
+      const int nd = base + P;
       if (nd > Bt.cap) {
         st.status = kStackOverflow;
         break;
       }
-      if (dyn && base + fr.push_len == 0) {
+      if (dyn && base + push_len == 0) {
         st.status = kDead;  // no exposed top: unreachable for validated automata
         break;
       }
-      for (int j = lane; j < fr.push_len; j += 32) stack[base + j] = __ldg(A.rec_push + fr.push_off + j);
-      __syncwarp();
-      if (dyn && lane == 0) {
-        const int top = stack[base + fr.push_len - 1];
-        stack[base + fr.push_len] = __ldg(A.shift + top * 256 + x);
+      if (P > 32) {
+        // Very long push (not produced by the fixture or workload grammars):
+        // write through memory and reload the window.
+        for (int j = lane; j < push_len; j += 32) stack[base + j] = __ldg(A.rec_push + push_off + j);
+        __syncwarp();
+        if (dyn && lane == 0) stack[base + push_len] = __ldg(A.shift + stack[base + push_len - 1] * 256 + x);
+        __syncwarp();
+        topv = lane < nd ? stack[nd - 1 - lane] : -1;
+        wv = min(nd, 32);
+      } else {
+        int pj = -1;  // pushed entry `lane` (bottom first)
+        if (lane < push_len) {
+          pj = lane == 0 ? p0 : lane == 1 ? p1 : lane == 2 ? p2 : lane == 3 ? p3 : __ldg(A.rec_push + push_off + lane);
+        }
+        if (dyn) {
+          // Dynamic target from the exposed top (optimizer.cpp:33-76).
+          const int last_pushed = __shfl_sync(0xffffffffu, pj, (push_len - 1) & 31);
+          const int below = __shfl_sync(0xffffffffu, topv, cond_len & 31);
+          int top = push_len > 0 ? last_pushed : (cond_len < wv ? below : -1);
+          if (top < 0) top = stack[base - 1];
+          const int tgt = __ldg(A.shift + top * 256 + x);
+          if (lane == push_len) pj = tgt;
+        }
+        if (lane < P) stack[base + lane] = pj;
+        const int k = cond_len + lane - P;  // old window index of new entry `lane`
+        const int old = __shfl_sync(0xffffffffu, topv, k & 31);
+        const int pushed = __shfl_sync(0xffffffffu, pj, (P - 1 - lane) & 31);
+        topv = lane < P ? pushed : (k < wv ? old : -1);
+        wv = min(32, P + max(0, wv - cond_len));
+        __syncwarp();  // stack writes visible to the warp's later reads
       }
-      __syncwarp();
       depth = nd;
       if (eos) st.status = kAccepted;
-      if (i + 1 < nterm) topv = lane < depth ? stack[depth - 1 - lane] : -1;
     }
     st.depth = depth;
   }
@@ -587,25 +879,24 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
     }
     st.depth = 1;
     st.status = kAlive;
+    topv = lane == 0 ? A.initial : -1;
+    wv = 1;
   }
   __syncwarp();
-  // Key of the next fill's context: lane i loads entry i, lane 0 gathers.
-  int32_t key[kMaxContext];
-  if (lookup_queue >= 0) {
-    const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
-    const int32_t kv = lane < n ? stack[st.depth - 1 - lane] : 0;
-#pragma unroll
-    for (int i = 0; i < kMaxContext; ++i) key[i] = __shfl_sync(0xffffffffu, kv, i);
-  }
-  int flagged = -2;
+  if (lane == 0 && Bt.trace) TraceEvent(Bt, 20, b, 0, t_ph, 0), t_ph = NowNs();
   if (lane == 0) {
     Bt.seq[b] = st;
     atomicAdd(Bt.counters + 3, 1ull);
-    if (lookup_queue >= 0) flagged = AssignSlotKey(Cc, Bt, lookup_queue, b, st, Vv.nseg, key);
   }
   if (lookup_queue >= 0) {
-    const uint32_t mask = __shfl_sync(0xffffffffu, lane == 0 ? HeavyMask(Cc, flagged, Vv.nseg) : 0u, 0);
+    // Key of the next fill's context: lane i holds entry i.
+    const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
+    int kv = topv;
+    if (n > wv) kv = lane < n ? stack[st.depth - 1 - lane] : 0;
+    const uint32_t mask = AssignSlotWarp(Cc, Bt, lookup_queue, b, st, Vv.nseg, kv, lane);
+    if (lane == 0 && Bt.trace) TraceEvent(Bt, 21, b, 0, t_ph, 0), t_ph = NowNs();
     PublishHeavy(Bt, lookup_queue, lookup_tag, b, mask, Vv.nseg, lane, 32);
+    if (lane == 0 && Bt.trace) TraceEvent(Bt, 22, b, 0, t_ph, 0), t_ph = NowNs();
   }
 }
 
@@ -854,6 +1145,7 @@ __device__ bool WaitBuilt(const CacheView& Cc, const BatchView& Bt, int slot, in
 template <int TAIL>
 __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                              const BatchView& Bt, const FillArgs& F, int b, int lane) {
+  const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   __threadfence();
   SeqState st = Bt.seq[b];
   int tok;
@@ -870,6 +1162,7 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
   if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
   if (lane == 0) Bt.seq_arrive[b] = 0;
   AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, F.fill_no + 1, lane);
+  if (lane == 0) TraceEvent(Bt, kTraceTail, b, 0, t_in, static_cast<unsigned long long>(tok + 1));
 }
 
 // Light item: one warp fills one (sequence, segment) — the steady state (a
@@ -880,6 +1173,7 @@ template <int MODE, int TAIL>
 __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                           const BatchView& Bt, const FillArgs& F, int b, int seg, int slot,
                                           int lane, uint4 (*span_buf)[4][32]) {
+  const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   const int w0 = seg * kSegWords;
   const int nwords = min(Vv.W - w0, kSegWords);
   const int t0 = w0 * 32;
@@ -1040,6 +1334,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     }
   }
   if (lane == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
+  if (lane == 0) TraceEvent(Bt, kTraceLight, b, seg, t_in, static_cast<unsigned long long>(n_walks));
   if (TAIL != kTailNone && last) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
 }
 
@@ -1102,6 +1397,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
   }
 
   // ---- heavy pass.
+  const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   if (static_cast<unsigned int>(bid) >= LoadRelaxed(Qc.n_heavy)) return;
   const int2 hv = Qc.heavy[bid];
   const int b = hv.x;
@@ -1116,7 +1412,9 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
   const int t1 = min(Vv.V + 1, t0 + nwords * 32);
   static_assert(kSegWords == kThreads, "one mask word per thread");
 
+  unsigned long long t_ph = t_in;
   if (n_items != 0u) HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);
+  if (tid == 0 && Bt.trace) TraceEvent(Bt, 10, b, seg, t_ph, 0), t_ph = NowNs();
 
   // Thread tid owns mask word w0 + tid (register `mword`).
   const uint32_t sw = (F.seg_counts != nullptr && tid < nwords) ? __ldg(Vv.structural + w0 + tid) : 0u;
@@ -1127,6 +1425,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     __syncthreads();
     if (!sh.unit) slot = -3;  // direct fill
   }
+  if (tid == 0 && Bt.trace) TraceEvent(Bt, 11, b, seg, t_ph, 0), t_ph = NowNs();
   uint32_t mword = 0u;
   int cd_cnt = 0;
   if (slot >= 0) {
@@ -1161,7 +1460,9 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
       const int excl = BlockExclusiveScan(__popc(x), sh.scratch, &total);  // has barriers
       sh.pre[tid] = excl;
       __syncthreads();
-      for (int q = tid; q < total; q += kThreads) {
+      if (tid == 0 && Bt.trace) TraceEvent(Bt, 12, b, seg, t_ph, 0), t_ph = NowNs();
+      const bool by_warp = total <= 2 * kWarps;  // few tokens: latency-bound, walk each with a warp
+      for (int q = by_warp ? warp : tid; q < total; q += by_warp ? kWarps : kThreads) {
         int lo = 0, hi2 = kThreads - 1;
         while (lo < hi2) {
           const int mid = (lo + hi2 + 1) >> 1;
@@ -1170,13 +1471,21 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
         uint32_t bits = sh.cd[lo];
         for (int r = q - sh.pre[lo]; r > 0; --r) bits &= bits - 1;
         const int t = t0 + lo * 32 + (__ffs(bits) - 1);
-        const int r = WalkToken(A, Vv, t, stack_s, depth, true);
+        int r;
+        if (by_warp) {
+          r = WalkWarp(A, Vv, t, stack_s, depth, lane);
+          if (r == kOverflow) r = WalkToken(A, Vv, t, stack_s, depth, true);
+          if (lane != 0) continue;
+        } else {
+          r = WalkToken(A, Vv, t, stack_s, depth, true);
+        }
         if (r == kAccept) atomicOr(&sh.mask[lo], 1u << ((t - t0) & 31));
         if (r == kOverflow) atomicOr(Bt.err, 1u);
       }
       n_walks = total;
     }
     __syncthreads();
+    if (tid == 0 && Bt.trace) TraceEvent(Bt, 13, b, seg, t_ph, 0), t_ph = NowNs();
     mword = sh.mask[tid];
   }
 
@@ -1245,6 +1554,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     if (tid == 0 && slot >= Cc.C) atomicAdd(Bt.stats + 4, 1ull);
   }
   if (tid == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
+  if (tid == 0) TraceEvent(Bt, kTraceHeavy, b, seg, t_in, n_walks);
   if (TAIL != kTailNone && last && warp == 0) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
 }
 // ---------------------------------------------------------------------------
@@ -1256,6 +1566,7 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
   const int lane = threadIdx.x & 31;
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= Bt.B) return;
+  const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   SeqState st = Bt.seq[b];
   int tok = -1;
   if (SAMPLE == kSampleGiven) {
@@ -1277,6 +1588,7 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
     return;
   }
   AcceptWarp(A, Vv, Cc, Bt, b, st, tok, G.status_out, G.restart, G.lookup_queue, G.lookup_tag, lane);
+  if (lane == 0) TraceEvent(Bt, kTraceAccept, b, 0, t_in, static_cast<unsigned long long>(tok + 1));
 }
 
 __global__ void ResetKernel(AutView A, BatchView Bt) {

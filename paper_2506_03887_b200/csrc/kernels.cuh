@@ -29,6 +29,7 @@ struct SeqState {
 struct AutView {
   const int32_t* rec_begin;  // S*257+1
   const CandRec* recs;
+  const CandRec* first;      // S*257 dense first candidates
   const int32_t* rec_cond;   // 16-B aligned lists
   const int32_t* rec_push;   // 16-B aligned lists
   const int32_t* shift;       // S*256
@@ -99,7 +100,13 @@ struct BatchView {
   unsigned long long* counters;       // [0] restarts, [1] draws, [2] fills, [3] accepts
   int32_t stats_enabled;
   int32_t build_grid;
+  // Diagnostics (null = off): per-event records {kind | seg << 8 | b << 32,
+  // t_start, t_end, extra} (globaltimer ns); trace[0..3] holds the count.
+  unsigned long long* trace;
+  int32_t trace_cap;
 };
+
+enum TraceKind { kTraceLight = 1, kTraceHeavy = 2, kTraceTail = 3, kTraceAccept = 4 };
 
 enum FillMode { kFillMask = 0, kFillGreedy = 1 };
 enum FillTail { kTailNone = 0, kTailStream = 1, kTailGreedy = 2 };

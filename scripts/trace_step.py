@@ -1,0 +1,72 @@
+"""Per-item timeline of one decode step (diagnostics; gm_batch_set_trace).
+
+    python scripts/trace_step.py [--batch 256] [--fused] [--grammar json]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_2506_03887_b200 as pk  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--batch", type=int, default=256)
+p.add_argument("--fused", action="store_true")
+p.add_argument("--grammar", default="json")
+p.add_argument("--steps", type=int, default=3)
+p.add_argument("--k", type=int, default=12)
+p.add_argument("--slots", type=int, default=8192)
+a = p.parse_args()
+flat = bench.automaton_bytes(a.grammar)
+vocab = pk.synth_vocab(128255)
+eng = pk.DeviceEngine(pk.Automaton.load(flat), vocab, device=0, context_depth=a.k, context_slots=a.slots)
+eng.prewarm(1024, 2000, seed=0xC0FFEE)
+B = a.batch
+batch = eng.batch(B, 1024)
+dev = torch.device("cuda:0")
+bm = torch.zeros((B, eng.W), dtype=torch.int32, device=dev)
+counts = torch.zeros((B, batch.nseg * 2), dtype=torch.int32, device=dev)
+toks = torch.zeros(B, dtype=torch.int32, device=dev)
+logits = [torch.randn((B, eng.V + 1), dtype=torch.bfloat16, device=dev) for _ in range(3)]
+
+
+def step(i):
+    if a.fused:
+        batch.decode_step_stream(1, bitmask=bm, logits=logits[i % 3], tokens_out=toks)
+    else:
+        batch.fill(bm, logits[i % 3], counts)
+        batch.sample_stream_and_accept(bm, counts, 1, toks)
+
+
+for i in range(40):
+    step(i)
+torch.cuda.synchronize()
+cap = 1 << 16
+tr = torch.zeros(4 * (cap + 1), dtype=torch.int64, device=dev)
+names = {1: "light", 2: "heavy", 3: "tail", 4: "accept", 10: "h:build", 11: "h:wait", 12: "h:cdscan", 13: "h:walks",
+         20: "a:step", 21: "a:lookup", 22: "a:publish"}
+for s in range(a.steps):
+    tr.zero_()
+    batch.set_trace(tr)
+    step(100 + s)
+    torch.cuda.synchronize()
+    batch.set_trace(None)
+    t = tr.cpu().numpy().view(np.uint64)
+    n = int(t[0])
+    rec = t[4:4 * (n + 1)].reshape(n, 4).astype(np.int64)
+    kind = rec[:, 0] & 0xff
+    t0 = rec[:, 1].min()
+    print(f"step {s}: {n} records, span {(rec[:, 2].max() - t0) / 1e3:.1f} us")
+    for k in sorted(set(kind.tolist())):
+        r = rec[kind == k]
+        st = (r[:, 1] - t0) / 1e3
+        du = (r[:, 2] - r[:, 1]) / 1e3
+        en = (r[:, 2] - t0) / 1e3
+        pct = lambda v: " ".join(f"{x:6.1f}" for x in np.percentile(v, [0, 50, 90, 99, 100]))
+        print(f"  {names[int(k)]:7s} n={len(r):6d} start[p0 p50 p90 p99 max] {pct(st)} | dur {pct(du)} | end max {en.max():6.1f}"
+              f" | extra sum {int(r[:, 3].sum())}")
