@@ -88,7 +88,7 @@ int gm_automaton_compile_stats(const gm_automaton* a, int64_t stats[4]);
 
 /* ------------------------------------------------------------ engine */
 typedef struct gm_engine_options {
-  int32_t context_depth;   /* K: stack entries keying the context cache (1..16; default 8) */
+  int32_t context_depth;   /* K: stack entries keying the context cache (1..32; default 8) */
   int32_t context_slots;   /* hash-table capacity, power of two (default 8192) */
   int64_t reserved;        /* must be 0 */
   int32_t segment_words;   /* vocab segment size in mask words (default 256) */

@@ -201,9 +201,11 @@ class Ref:
         return out
 
     def decode_run(self, structural: np.ndarray, batch: int, steps: int, seed: int, threads: int,
-                   stack_cap: int = 1024, logits_row: bool = True, want_tokens: bool = False,
+                   stack_cap: int = 1024, logits_row: int = 1, want_tokens: bool = False,
                    want_stacks: bool = False, warmup: int = 0):
-        """stats[0] = seconds of the `steps` timed steps (after `warmup`)."""
+        """stats[0] = seconds of the `steps` timed steps (after `warmup`).
+        logits_row: 0 mask only, 1 + bf16 -inf row (stream sampler),
+        2 greedy argmax over synthetic bf16 rows (config 5)."""
         stats = np.zeros(8, np.float64)
         toks = np.zeros((batch, warmup + steps), np.int32) if want_tokens else None
         stk = np.zeros((batch, stack_cap + 2), np.int32) if want_stacks else None

@@ -222,6 +222,23 @@ int32_t StreamPick(const uint32_t* mask, const uint32_t* structural, int32_t V, 
 }
 
 // bf16 -inf masking of one logits row (new work).
+// Argmax of the allowed bf16 logits (ties -> lowest id; -1 when nothing is
+// allowed) — the device greedy rule (kernels.cu GreedyKey).
+int32_t GreedyPick(const uint16_t* row, const uint32_t* mask, int32_t v1) {
+  int32_t best = -1;
+  uint32_t best_key = 0;
+  for (int32_t t = 0; t < v1; ++t) {
+    if (!((mask[t >> 5] >> (t & 31)) & 1u)) continue;
+    const uint32_t bits = static_cast<uint32_t>(row[t]) << 16;
+    const uint32_t key = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
+    if (best < 0 || key > best_key) {
+      best = t;
+      best_key = key;
+    }
+  }
+  return best;
+}
+
 void MaskRowBf16(uint16_t* row, const uint32_t* mask, int32_t v1) {
   for (int32_t t = 0; t < v1; ++t) {
     if (!((mask[t >> 5] >> (t & 31)) & 1u)) row[t] = 0xFF80u;
@@ -410,15 +427,35 @@ int ref_decode_run(void* e, void* trie, const uint32_t* structural, int32_t batc
   auto worker = [&](int32_t tid, int32_t s_begin, int32_t s_end) {
     std::vector<uint32_t> mask(static_cast<size_t>(nw));
     std::vector<uint16_t> row(logits_row ? static_cast<size_t>(v1) : 0, 0x3F80u);
+    // Greedy mode (logits_row == 2, config 5): four synthetic bf16 logit rows
+    // cycled per step (the device bench rotates its own buffers the same
+    // way); argmax over allowed ids, ties -> lowest id.
+    std::vector<std::vector<uint16_t>> grows;
+    if (logits_row == 2) {
+      for (int k = 0; k < 4; ++k) {
+        std::vector<uint16_t> g(static_cast<size_t>(v1));
+        uint64_t x = Mix64(seed ^ (0xA5A5ull + static_cast<uint64_t>(k)));
+        for (auto& v : g) {
+          x = Mix64(x);
+          v = static_cast<uint16_t>(0x3C00u + (x & 0x3FFu)) ^ ((x >> 20) & 1 ? 0x8000u : 0u);
+        }
+        grows.push_back(std::move(g));
+      }
+    }
     for (int32_t s = s_begin; s < s_end; ++s) {
       for (int32_t b = tid; b < batch; b += threads) {
         RuntimeConfig& cfg = cfgs[static_cast<size_t>(b)];
         TokenMask m = eng.ComputeMask(cfg, tr);
         MaskToWords(m, mask.data());
         pops[static_cast<size_t>(tid)] += m.CountSet();
-        if (logits_row) MaskRowBf16(row.data(), mask.data(), v1);
-        uint64_t u = StreamDraw(seed, static_cast<uint64_t>(b), draws[static_cast<size_t>(b)]++);
-        int32_t tok = StreamPick(mask.data(), structural, V, u);
+        int32_t tok;
+        if (logits_row == 2) {
+          tok = GreedyPick(grows[static_cast<size_t>(s & 3)].data(), mask.data(), v1);
+        } else {
+          if (logits_row) MaskRowBf16(row.data(), mask.data(), v1);
+          uint64_t u = StreamDraw(seed, static_cast<uint64_t>(b), draws[static_cast<size_t>(b)]++);
+          tok = StreamPick(mask.data(), structural, V, u);
+        }
         chosen[static_cast<size_t>(b)][static_cast<size_t>(s)] = tok;
         bool overflow = false;
         if (tok == V) {

@@ -212,7 +212,7 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
       if (opts->context_slots) o.context_slots = opts->context_slots;
       if (opts->segment_words) o.segment_words = opts->segment_words;
     }
-    if (o.context_depth < 1 || o.context_depth > pre3::kMaxContext) return Fail(GM_ERR_USAGE, "context_depth must be 1..16");
+    if (o.context_depth < 1 || o.context_depth > pre3::kMaxContext) return Fail(GM_ERR_USAGE, "context_depth must be 1..32");
     if (o.context_slots < 1 || (o.context_slots & (o.context_slots - 1))) return Fail(GM_ERR_USAGE, "context_slots must be a power of two");
     if (o.segment_words != pre3::kSegWords) return Fail(GM_ERR_USAGE, "segment_words must be 256");
     if (tok_offsets && tok_offsets[num_tokens] > (int64_t{1} << 31) - 1) return Fail(GM_ERR_USAGE, "vocabulary bytes exceed 2^31");

@@ -356,6 +356,18 @@ __device__ unsigned long long KeyHash(const int32_t* key, int n, int complete) {
   return h | 1ull;
 }
 
+// Meta word of slot i once its inserter has published the key row (the
+// ready bit follows the key stores immediately); bounded at ~0.5 ms, after
+// which the caller falls back to a private row.
+__device__ __forceinline__ int WaitReady(const CacheView& C, int i) {
+  int m = LoadAcquire(C.slot_meta + i);
+  for (int spin = 0; !(m & (1 << 16)) && spin < 4096; ++spin) {
+    __nanosleep(128);
+    m = LoadAcquire(C.slot_meta + i);
+  }
+  return m;
+}
+
 // Finds or inserts the slot of a key.  Returns the slot (created = true when
 // this thread inserted it) or -1 (table full, or the key is being published
 // by another thread right now).
@@ -380,11 +392,10 @@ __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int com
       cur = expect;
     }
     if (cur != h) continue;
-    atomic_i32 meta(C.slot_meta[i]);
-    const int m = meta.load(cuda::memory_order_acquire);
+    const int m = WaitReady(C, i);
     if (!(m & (1 << 16))) return -1;
     if ((m & 0xffff) != meta_want) continue;
-    // Whole 16-entry row in four independent loads.
+    // Whole key row in independent vector loads.
     const int4* row = reinterpret_cast<const int4*>(C.slot_keys + i * kMaxContext);
     int4 q[kMaxContext / 4];
 #pragma unroll
@@ -662,15 +673,14 @@ __device__ int LookupSlotWarp(const CacheView& C, int kv, int n, int complete, i
         const int src = __ffs(cand) - 1;
         cand &= cand - 1;
         const int slot = static_cast<int>((h + static_cast<unsigned long long>(base + src)) & cmask);
-        int v = 0;
-        if (lane < n) v = __ldcg(C.slot_keys + slot * kMaxContext + lane);
-        else if (lane == 29) v = LoadAcquire(C.slot_meta + slot);
-        else if (lane == 30) v = LoadAcquire(C.slot_built + slot);
-        else if (lane == 31) v = static_cast<int>(LoadRelaxed(C.cd_segmask + slot));
-        const int m = __shfl_sync(0xffffffffu, v, 29);
-        const int bt = __shfl_sync(0xffffffffu, v, 30);
-        const int sm = __shfl_sync(0xffffffffu, v, 31);
-        if (!(m & (1 << 16))) return -1;  // being published: private row this time
+        // Key row (lane i = entry i), meta, build progress, CD segments: one
+        // round trip (the last three are warp-broadcast loads).
+        const int v = lane < n ? __ldcg(C.slot_keys + slot * kMaxContext + lane) : 0;
+        int m = LoadAcquire(C.slot_meta + slot);
+        const int bt = LoadAcquire(C.slot_built + slot);
+        const int sm = static_cast<int>(LoadRelaxed(C.cd_segmask + slot));
+        if (!(m & (1 << 16))) m = WaitReady(C, slot);  // key row being published right now
+        if (!(m & (1 << 16))) return -1;
         if ((m & 0xffff) != meta_want) continue;
         if (__all_sync(0xffffffffu, lane >= n || v == kv)) {
           *built = bt;
@@ -1618,7 +1628,7 @@ cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int 
 
 cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,
                         cudaStream_t s) {
-  const size_t dyn = static_cast<size_t>(b.cap) * sizeof(int32_t);
+  const size_t dyn = static_cast<size_t>(b.cap > kMaxContext ? b.cap : kMaxContext) * sizeof(int32_t);
   if (dyn > 48 * 1024) {
     cudaFuncSetAttribute(DrainKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
   }
@@ -1645,7 +1655,7 @@ cudaError_t LaunchFill(int mode, int tail, const AutView& a, const VocabView& v,
                        const BatchView& b, FillArgs f, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
   f.vec_ok = f.logits != nullptr && (f.ld % 8) == 0 && (reinterpret_cast<uintptr_t>(f.logits) % 16) == 0;
-  const size_t dyn = static_cast<size_t>(b.cap) * sizeof(int32_t);
+  const size_t dyn = static_cast<size_t>(b.cap > kMaxContext ? b.cap : kMaxContext) * sizeof(int32_t);
   if (mode == kFillGreedy) {
     LaunchFillT<kFillGreedy, kTailGreedy>(a, v, c, b, f, dyn, s);
   } else if (tail == kTailStream) {

@@ -14,7 +14,7 @@ constexpr int kThreads = 256;                         // fill / build CTA size (
 constexpr int kSegWords = 256;                        // mask words per vocab segment
 constexpr int kSegTokens = kSegWords * 32;            // 8192 tokens per segment
 constexpr int kChunksPerSeg = kSegTokens / kThreads;  // build work units per segment
-constexpr int kMaxContext = 16;                       // max K
+constexpr int kMaxContext = 32;                       // max K (one warp lane per key entry)
 constexpr int kWalkOverlay = 64;                      // per-thread pushed-entry overlay in a mask walk
 constexpr int kSlotWait = 1 << 30;                    // seq_slot flag: wait for the slot's build
 

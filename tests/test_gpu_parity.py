@@ -22,6 +22,7 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 FIXTURES = ["paren", "list_left", "list_right", "digits", "expr", "json"]
 DEV = "cuda:0"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def flat(name):
@@ -276,3 +277,25 @@ def test_stack_overflow_status():
         batch.accept(t, st)
     batch.check()
     assert int(st.item()) == pk.OVERFLOW
+
+
+@pytest.mark.parametrize("name,flavor", [("schema", 0), ("sql", 1)])
+def test_workload_grammar_stream_matches_port(name, flavor):
+    """Configs 3/4: the repo-authored grammars, compiled by our own compiler
+    (byte-identical to the reference builder, test_compiler.py), drive the
+    GPU decode loop at 128k tokens; tokens every step and final stacks equal
+    the C port's."""
+    text = open(os.path.join(ROOT, "paper_2506_03887_b200", "grammars", name + ".bnf")).read()
+    f = pk.Automaton.compile(text).save()
+    vocab = pk.synth_vocab(128255, flavor)
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=12)
+    port = Port(f, vocab)
+    B, steps, seed = 16, 12, 9
+    for fused in (False, True):
+        batch, masks, tokens = run_stream(eng, B, steps, seed, fused=fused)
+        _, ptoks, pstacks = port.decode_run(eng.structural, B, steps, seed, want_tokens=True, want_stacks=True)
+        assert np.array_equal(tokens, ptoks), fused
+        for b in range(B):
+            d = pstacks[b, 0]
+            got = batch.get(b)
+            assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1]
