@@ -43,7 +43,7 @@ CONFIGS = {
     2: dict(grammar="json", flavor=0, batch=256, mode="stream", scaling="weak", K=12, slots=16384,
             desc="config2: JSON LR(1) grammar, 128256-bit vocab (synthetic 128k tokens), batch {b}/GPU, "
                  "fused mask-fill + in-place bf16 -inf logit masking + stream sample + accept_token"),
-    3: dict(grammar="schema", flavor=0, batch=1024, mode="stream", scaling="weak", K=12, slots=16384,
+    3: dict(grammar="schema", flavor=0, batch=1024, mode="stream", scaling="weak", K=16, slots=16384,
             desc="config3: JSON-schema-derived LR(1) grammar (nested objects/arrays), 128256-bit vocab, "
                  "batch {b}/GPU, fused mask-fill + bf16 -inf logit masking + stream sample + accept_token"),
     4: dict(grammar="sql", flavor=1, batch=4096, mode="stream", scaling="strong", K=20, slots=65536,

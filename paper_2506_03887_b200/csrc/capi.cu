@@ -378,6 +378,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
     v.build_grid = sms * 4;
+    v.h_grid = std::min(v.h_cap, 2 * sms);
     b->seg_counts = DevAlloc<int32_t>(bn * 2, &b->owned);
     b->scratch_mask = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     b->best = DevAlloc<unsigned long long>(static_cast<size_t>(batch), &b->owned);

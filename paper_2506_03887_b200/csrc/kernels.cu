@@ -1359,7 +1359,7 @@ struct FillShared {
   int unit, last;
 };
 
-// Grid: h_cap heavy CTAs, then ceil(B * nseg / kWarps) light CTAs.
+// Grid: h_grid (<= 2 per SM) heavy CTAs, then ceil(B * nseg / kWarps) light CTAs.
 //  * Heavy CTA: one (sequence, segment) listed by the lookups — a segment
 //    with context-dependent tokens or a pending build — 256 threads: CD
 //    tokens are walked one per thread, a direct fill walks 256 tokens a round.
@@ -1388,9 +1388,9 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
   const int tag = HeavyTag(F.fill_no, 0);
   const int32_t* hidx = HeavyIndex(Bt, F.fill_no, Vv.nseg);
 
-  if (bid >= Bt.h_cap) {
+  if (bid >= Bt.h_grid) {
     // ---- light pass.  Loads that only depend on (b, seg) are issued together.
-    const int item = (bid - Bt.h_cap) * kWarps + warp;
+    const int item = (bid - Bt.h_grid) * kWarps + warp;
     const bool in_range = item < Bt.B * Vv.nseg;
     const int b = in_range ? item / Vv.nseg : 0;
     const int seg = item - b * Vv.nseg;
@@ -1401,14 +1401,17 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     }
     const unsigned int n_items = LoadRelaxed(Qc.n_items);
     if (n_items != 0u) HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);  // CTA-uniform
-    if (!in_range || (hi >= 0 && (hi & ~0xffff) == tag)) return;  // owned by the heavy pass
+    // Owned by the heavy pass: listed for this fill at a position the grid's
+    // h_grid heavy CTAs cover (a longer list spills over to the light pass,
+    // whose warps take the rare CD/wait paths themselves).
+    if (!in_range || (hi >= 0 && (hi & ~0xffff) == tag && (hi & 0xffff) < Bt.h_grid)) return;
     LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, lane, span_buf[warp]);
     return;
   }
 
   // ---- heavy pass.
   const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
-  if (static_cast<unsigned int>(bid) >= LoadRelaxed(Qc.n_heavy)) return;
+  if (static_cast<unsigned int>(bid) >= LoadRelaxed(Qc.n_heavy)) return;  // (bid < h_grid <= h_cap)
   const int2 hv = Qc.heavy[bid];
   const int b = hv.x;
   const int seg = hv.y;
@@ -1647,7 +1650,7 @@ static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c
     opted = dyn;
   }
   const unsigned items = static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
-  const unsigned grid = static_cast<unsigned>(b.h_cap) + (items + kWarps - 1) / kWarps;
+  const unsigned grid = static_cast<unsigned>(b.h_grid) + (items + kWarps - 1) / kWarps;
   FillKernel<MODE, TAIL><<<grid, kThreads, dyn, s>>>(a, v, c, b, f);
 }
 

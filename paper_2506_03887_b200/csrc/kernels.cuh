@@ -91,7 +91,8 @@ struct BatchView {
   uint32_t* priv;           // B*W private (uncached) masks
   int32_t* priv_done;       // B*nseg build-completion counters of private rows
   int32_t* heavy_index;     // B*nseg: index in the consumed heavy list, or -1
-  int32_t h_cap;            // heavy list capacity (= heavy-pass CTAs of a fill grid)
+  int32_t h_cap;            // heavy list capacity
+  int32_t h_grid;           // heavy-pass CTAs of a fill grid (they loop over the list)
   BuildQueue queue[3];      // ring: lookups feed queue[p], fill drains it, the next fill resets it
   int32_t* seq_arrive;      // B: fill CTAs finished per sequence (fused tail)
   unsigned int* kernel_done;  // CTAs finished per launch (queue reset)
