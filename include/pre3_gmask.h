@@ -62,11 +62,22 @@ const char* gm_last_error(void);
 int gm_abi_version(void);
 
 /* ------------------------------------------------------------ automaton */
-/* Loads a compiled automaton in the flat P3DPDA v1 format —
- * the device-oriented counterpart of DeserializeDpda
- * (src/serialize.cpp:198-294): validates shapes, id ranges, per-state edge
- * ranges and arbitration order.  `data` is a host buffer. */
+/* Loads a compiled automaton from a host buffer in either format, told apart
+ * by the magic: the reference's GMASKDP1 (DeserializeDpda,
+ * src/serialize.cpp:198-294: sorted-key JSON; arbitration order re-derived
+ * and determinism re-checked; errors = SerializeError kinds) or the flat
+ * P3DPDA v1 of DESIGN.md §3 (shapes, id ranges, edge ranges validated). */
 int gm_automaton_load(const void* data, size_t bytes, gm_automaton** out);
+/* SerializeDpda (src/serialize.cpp:148-196): byte-identical GMASKDP1 text of
+ * an automaton (composites / cycles / stats are empty for one loaded from
+ * P3DPDA).  *size receives the length (buf = NULL to query). */
+int gm_automaton_save_gmaskdp1(const gm_automaton* a, void* buf, size_t cap, size_t* size);
+/* LoadVocabulary (src/serialize.cpp:348-364): a JSON array of strings, each
+ * `\xNN` / `\\` unescaped, into tok_bytes / tok_offsets[n+1] (host).  Call
+ * with tok_bytes = NULL to get *num_tokens and *total_bytes. */
+int gm_vocab_load_json(const void* data, size_t bytes, uint8_t* tok_bytes, int64_t bytes_cap,
+                       int64_t* tok_offsets, int32_t tokens_cap, int32_t* num_tokens,
+                       int64_t* total_bytes);
 /* Compiles grammar text (line-oriented BNF, grammar.hpp:1-10) into an
  * automaton: ParseGrammar + BuildDpda (src/dpda_builder.cpp:478-522).
  * aggregate/merge mirror BuildOptions (dpda.hpp:73-80). */

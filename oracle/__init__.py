@@ -82,12 +82,68 @@ class Ref:
                 "ref_decode_run": ([P, P, P, I32, I32, I32, U64, I32, I32, I32, P, P, P], ctypes.c_int),
                 "ref_sample_sentence": ([ctypes.c_char_p, U64, I32, ctypes.c_char_p, I32], I32),
             }
-            for n, (a, r) in sigs.items():
+            opt = {  # present when the reference's serialize.cpp was built (json.hpp found)
+                "ref_dpda_serialize": ([P, P, I64], I64),
+                "ref_dpda_deserialize": ([P, I64, ctypes.POINTER(P), ctypes.c_char_p, ctypes.c_int], ctypes.c_int),
+                "ref_load_vocabulary": ([P, I64, P, I64, P, I32, ctypes.c_char_p, ctypes.c_int], I32),
+            }
+            for n, (a, r) in list(sigs.items()) + [kv for kv in opt.items() if hasattr(L, kv[0])]:
                 f = getattr(L, n)
                 f.argtypes = a
                 f.restype = r
             cls._lib = L
         return cls._lib
+
+    @classmethod
+    def serialize_available(cls) -> bool:
+        return ref_available() and hasattr(cls.lib(), "ref_dpda_serialize")
+
+    @classmethod
+    def compile_gmaskdp1(cls, grammar_text: str, aggregate: bool = True, merge: bool = True) -> Tuple[int, bytes]:
+        """BuildDpda + SerializeDpda (serialize.cpp:148-196) -> (rc, GMASKDP1 bytes or error)."""
+        L = cls.lib()
+        d = P()
+        err = ctypes.create_string_buffer(4096)
+        rc = L.ref_compile(grammar_text.encode(), int(aggregate), int(merge), ctypes.byref(d), err, 4096)
+        if rc != 0:
+            return rc, err.value
+        n = L.ref_dpda_serialize(d, None, 0)
+        buf = ctypes.create_string_buffer(n)
+        L.ref_dpda_serialize(d, buf, n)
+        L.ref_dpda_free(d)
+        return 0, buf.raw[:n]
+
+    @classmethod
+    def roundtrip_gmaskdp1(cls, data: bytes) -> Tuple[int, bytes]:
+        """DeserializeDpda then SerializeDpda -> (rc, bytes or error message)."""
+        L = cls.lib()
+        d = P()
+        err = ctypes.create_string_buffer(4096)
+        src = ctypes.create_string_buffer(data, len(data))
+        rc = L.ref_dpda_deserialize(src, len(data), ctypes.byref(d), err, 4096)
+        if rc != 0:
+            return rc, err.value
+        n = L.ref_dpda_serialize(d, None, 0)
+        buf = ctypes.create_string_buffer(n)
+        L.ref_dpda_serialize(d, buf, n)
+        L.ref_dpda_free(d)
+        return 0, buf.raw[:n]
+
+    @classmethod
+    def load_vocabulary(cls, data: bytes):
+        """LoadVocabulary (serialize.cpp:348-364) -> list of bytes, or raises ValueError(message)."""
+        L = cls.lib()
+        err = ctypes.create_string_buffer(4096)
+        src = ctypes.create_string_buffer(data, len(data))
+        n = L.ref_load_vocabulary(src, len(data), None, 0, None, 0, err, 4096)
+        if n < 0:
+            raise ValueError(err.value.decode())
+        offs = np.zeros(n + 1, np.int64)
+        L.ref_load_vocabulary(src, len(data), None, 0, _ptr(offs), n, err, 4096)
+        buf = np.zeros(max(1, int(offs[n])), np.uint8)
+        L.ref_load_vocabulary(src, len(data), _ptr(buf), int(offs[n]), _ptr(offs), n, err, 4096)
+        raw = buf.tobytes()
+        return [raw[offs[i]:offs[i + 1]] for i in range(n)]
 
     # ---- automaton
     @classmethod

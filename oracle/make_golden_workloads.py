@@ -1,4 +1,4 @@
-"""oracle/make_golden_workloads.py — TEST INFRASTRUCTURE ONLY.
+r"""oracle/make_golden_workloads.py — TEST INFRASTRUCTURE ONLY.
 
 Golden vectors for the repo-authored workload grammars of configs 3 and 4
 (paper_2506_03887_b200/grammars/{schema,sql}.bnf), built by the UNMODIFIED
@@ -9,8 +9,14 @@ reference compiler (oracle/_ref/libgmask_ref.so).  Run here:
 Outputs
   tests/golden/schema.p3dpda      BuildDpda(default options) of schema.bnf
   tests/golden/workloads.json     per grammar: sha256 of the reference P3DPDA
-                                  (sql's is ~20 MB, so only its digest is
-                                  kept), BuildStats, composite/cycle counts.
+                                  and GMASKDP1 (sql's are 13 / 35 MB, so only
+                                  digests are kept), BuildStats, counts.
+  tests/golden/<fixture>.gmaskdp1 SerializeDpda of every fixture grammar
+                                  (needs the reference's serialize.cpp, built
+                                  by oracle/Makefile when json.hpp is found)
+  tests/golden/vocab_escapes.json LoadVocabulary known answer: a vocabulary
+                                  file with \xNN / \\ escapes and the bytes
+                                  the reference decodes it to (hex).
 """
 from __future__ import annotations
 
@@ -38,6 +44,24 @@ def main() -> None:
         if name == "schema":
             with open(os.path.join(OUT, name + ".p3dpda"), "wb") as f:
                 f.write(flat)
+        if Ref.serialize_available():
+            rc, dp1 = Ref.compile_gmaskdp1(text)
+            assert rc == 0
+            out[name]["gmaskdp1_sha256"] = hashlib.sha256(dp1).hexdigest()
+            out[name]["gmaskdp1_bytes"] = len(dp1)
+    if Ref.serialize_available():
+        from oracle import read_flat
+        for fx in ["paren", "list_left", "list_right", "digits", "expr", "json"]:
+            text = read_flat(open(os.path.join(OUT, fx + ".p3dpda"), "rb").read())["grammar_text"]
+            rc, dp1 = Ref.compile_gmaskdp1(text)
+            assert rc == 0
+            with open(os.path.join(OUT, fx + ".gmaskdp1"), "wb") as f:
+                f.write(dp1)
+        raw = ['a', '\\x41\\x00b', '\\\\', '\\xff\\xFE', 'tab\\x09', '"q"', 'caf\u00e9', '\\x7f']
+        vocab_text = json.dumps(raw)
+        toks = Ref.load_vocabulary(vocab_text.encode())
+        with open(os.path.join(OUT, "vocab_escapes.json"), "w") as f:
+            json.dump({"file": vocab_text, "tokens_hex": [t.hex() for t in toks]}, f, indent=1)
     with open(os.path.join(OUT, "workloads.json"), "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
     print(json.dumps(out, indent=1))

@@ -34,6 +34,9 @@
 #include "gmask/grammar.hpp"
 #include "gmask/lr1.hpp"
 #include "gmask/runtime.hpp"
+#ifdef GMASK_WITH_SERIALIZE
+#include "gmask/serialize.hpp"
+#endif
 #include "support/oracle.hpp"
 
 using namespace gmask;
@@ -277,6 +280,48 @@ int ref_compile(const char* text, int aggregate, int merge, void** out, char* er
 }
 
 void ref_dpda_free(void* d) { delete static_cast<Dpda*>(d); }
+
+#ifdef GMASK_WITH_SERIALIZE
+// SerializeDpda (serialize.cpp:148-196) -> GMASKDP1 bytes (size returned;
+// copied when cap suffices).
+int64_t ref_dpda_serialize(void* d, uint8_t* buf, int64_t cap) {
+  const std::string s = gmask::SerializeDpda(*static_cast<Dpda*>(d));
+  if (buf && cap >= static_cast<int64_t>(s.size())) std::memcpy(buf, s.data(), s.size());
+  return static_cast<int64_t>(s.size());
+}
+
+// DeserializeDpda (serialize.cpp:198-294): 0 ok, 4 SerializeError (message).
+int ref_dpda_deserialize(const uint8_t* data, int64_t n, void** out, char* err, int errlen) {
+  try {
+    *out = new Dpda(gmask::DeserializeDpda(std::string(reinterpret_cast<const char*>(data), static_cast<size_t>(n))));
+    return 0;
+  } catch (const std::exception& e) {
+    SetErr(err, errlen, e.what());
+    return 4;
+  }
+}
+
+// LoadVocabulary (serialize.cpp:348-364): tokens joined by offsets; returns
+// the token count (-1 on error, message in err).
+int32_t ref_load_vocabulary(const uint8_t* data, int64_t n, uint8_t* bytes, int64_t cap, int64_t* offs,
+                            int32_t max_tokens, char* err, int errlen) {
+  try {
+    std::vector<std::string> v =
+        gmask::LoadVocabulary(std::string(reinterpret_cast<const char*>(data), static_cast<size_t>(n)));
+    int64_t o = 0;
+    for (size_t i = 0; i < v.size() && static_cast<int32_t>(i) < max_tokens; ++i) {
+      if (offs) offs[i] = o;
+      if (bytes && o + static_cast<int64_t>(v[i].size()) <= cap) std::memcpy(bytes + o, v[i].data(), v[i].size());
+      o += static_cast<int64_t>(v[i].size());
+    }
+    if (offs && static_cast<int32_t>(v.size()) <= max_tokens) offs[v.size()] = o;
+    return static_cast<int32_t>(v.size());
+  } catch (const std::exception& e) {
+    SetErr(err, errlen, e.what());
+    return -1;
+  }
+}
+#endif
 
 int64_t ref_dpda_flat(void* d, uint8_t* buf, int64_t cap) {
   std::vector<uint8_t> v = ExportFlat(*static_cast<Dpda*>(d));

@@ -106,6 +106,8 @@ def lib() -> ctypes.CDLL:
             "gm_automaton_destroy": ([P], ctypes.c_int),
             "gm_automaton_info": ([P, P], ctypes.c_int),
             "gm_automaton_compile_stats": ([P, P], ctypes.c_int),
+            "gm_automaton_save_gmaskdp1": ([P, P, SZ, ctypes.POINTER(SZ)], ctypes.c_int),
+            "gm_vocab_load_json": ([P, SZ, P, I64, P, I32, ctypes.POINTER(I32), ctypes.POINTER(I64)], ctypes.c_int),
             "gm_engine_create": ([P, P, P, I32, P, ctypes.c_int, PP], ctypes.c_int),
             "gm_engine_destroy": ([P], ctypes.c_int),
             "gm_engine_info": ([P, P], ctypes.c_int),
@@ -173,6 +175,35 @@ def pack_vocab(tokens: Sequence[bytes]):
     return data, offs
 
 
+def load_vocabulary(data: bytes) -> List[bytes]:
+    """LoadVocabulary (serialize.cpp:348-364): JSON array of strings with
+    `\\xNN` / `\\\\` unescaping (raises SerializeError like the reference)."""
+    L = lib()
+    n, total = ctypes.c_int32(), ctypes.c_int64()
+    src = ctypes.create_string_buffer(data, len(data))
+    _check(L.gm_vocab_load_json(src, len(data), None, 0, None, 0, ctypes.byref(n), ctypes.byref(total)))
+    buf = np.zeros(max(1, total.value), np.uint8)
+    offs = np.zeros(n.value + 1, np.int64)
+    _check(L.gm_vocab_load_json(src, len(data), _ptr(buf), total.value, _ptr(offs), n.value, ctypes.byref(n),
+                                ctypes.byref(total)))
+    raw = buf.tobytes()
+    return [raw[offs[i]:offs[i + 1]] for i in range(n.value)]
+
+
+def escape_token(tok: bytes) -> str:
+    """EscapeToken (serialize.cpp:298-313): backslash and every byte outside
+    printable ASCII as \\xNN; inverse of the vocabulary unescape."""
+    out = []
+    for b in tok:
+        if b == 0x5C:
+            out.append("\\\\")
+        elif 0x20 <= b <= 0x7E:
+            out.append(chr(b))
+        else:
+            out.append("\\x%02x" % b)
+    return "".join(out)
+
+
 def structural_words(tokens: Sequence[bytes]) -> np.ndarray:
     data, offs = pack_vocab(tokens)
     words = np.zeros((len(tokens) + 1 + 31) // 32, np.uint32)
@@ -218,6 +249,14 @@ class Automaton:
         keys = ["num_states", "num_edges", "initial_state", "accept_state", "max_match_pop",
                 "max_push", "dynamic_edges", "grammar_hash"]
         return dict(zip(keys, (int(x) for x in out)))
+
+    def save_gmaskdp1(self) -> bytes:
+        """SerializeDpda (serialize.cpp:148-196): the reference's GMASKDP1 bytes."""
+        n = ctypes.c_size_t()
+        _check(lib().gm_automaton_save_gmaskdp1(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        _check(lib().gm_automaton_save_gmaskdp1(self._h, buf, n.value, ctypes.byref(n)))
+        return buf.raw[: n.value]
 
     def compile_stats(self) -> dict:
         out = np.zeros(4, np.int64)

@@ -137,7 +137,9 @@ int gm_abi_version(void) { return GM_ABI_VERSION; }
 int gm_automaton_load(const void* data, size_t bytes, gm_automaton** out) {
   return Guard([&]() -> int {
     if (!data || !out) return Fail(GM_ERR_USAGE, "null argument");
-    auto* a = new gm_automaton{pre3::LoadFlat(static_cast<const uint8_t*>(data), bytes)};
+    const auto* p = static_cast<const uint8_t*>(data);
+    const bool flat = bytes >= 6 && std::memcmp(p, "P3DPDA", 6) == 0;
+    auto* a = new gm_automaton{flat ? pre3::LoadFlat(p, bytes) : pre3::LoadGmaskdp1(p, bytes)};
     *out = a;
     return GM_OK;
   });
@@ -161,6 +163,43 @@ int gm_automaton_save(const gm_automaton* a, void* buf, size_t cap, size_t* size
       if (cap < v.size()) return Fail(GM_ERR_USAGE, "buffer too small");
       std::memcpy(buf, v.data(), v.size());
     }
+    return GM_OK;
+  });
+}
+
+int gm_automaton_save_gmaskdp1(const gm_automaton* a, void* buf, size_t cap, size_t* size) {
+  return Guard([&]() -> int {
+    if (!a || !size) return Fail(GM_ERR_USAGE, "null argument");
+    std::vector<uint8_t> v = pre3::SaveGmaskdp1(a->a);
+    *size = v.size();
+    if (buf) {
+      if (cap < v.size()) return Fail(GM_ERR_USAGE, "buffer too small");
+      std::memcpy(buf, v.data(), v.size());
+    }
+    return GM_OK;
+  });
+}
+
+int gm_vocab_load_json(const void* data, size_t bytes, uint8_t* tok_bytes, int64_t bytes_cap, int64_t* tok_offsets,
+                       int32_t tokens_cap, int32_t* num_tokens, int64_t* total_bytes) {
+  return Guard([&]() -> int {
+    if (!data || !num_tokens || !total_bytes) return Fail(GM_ERR_USAGE, "null argument");
+    const std::vector<std::string> v = pre3::LoadVocabularyJson(static_cast<const uint8_t*>(data), bytes);
+    int64_t total = 0;
+    for (const std::string& t : v) total += static_cast<int64_t>(t.size());
+    *num_tokens = static_cast<int32_t>(v.size());
+    *total_bytes = total;
+    if (tok_bytes == nullptr || tok_offsets == nullptr) return GM_OK;
+    if (bytes_cap < total || tokens_cap < static_cast<int32_t>(v.size())) {
+      return Fail(GM_ERR_USAGE, "buffer too small");
+    }
+    int64_t o = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+      tok_offsets[i] = o;
+      std::memcpy(tok_bytes + o, v[i].data(), v[i].size());
+      o += static_cast<int64_t>(v[i].size());
+    }
+    tok_offsets[v.size()] = o;
     return GM_OK;
   });
 }

@@ -21,8 +21,8 @@
 //   Aggregate      AggregateEdges        optimizer.cpp:33-76
 //   Order          EdgeOrderBefore / FinalizeEdgeOrder dpda_builder.cpp:327-338,450-467
 //   CheckDeterminism ValidateDeterminism dpda_builder.cpp:409-448
-//   CountComposites  MergeEdges          optimizer.cpp:78-136 (composites are
-//                                        sequence-runner only; not stored)
+//   MergeComposites  MergeEdges          optimizer.cpp:78-136 (composites are
+//                                        sequence-runner only; GMASKDP1 keeps them)
 //
 // Data structures are this file's own: 257-bit terminal sets in five words,
 // item sets as sorted (core, lookahead) arrays hashed by content, the action
@@ -586,6 +586,7 @@ Tables BuildTables(const Cfg& g, const Lr1& m) {
 struct BEdge {
   int32_t src = -1;
   TSet acc;                   // bytes + $
+  TSet acc2;                  // composites: second terminal
   std::vector<int32_t> pop;   // top first
   std::vector<int32_t> push;  // bottom first
   int32_t target = -1;
@@ -818,7 +819,7 @@ std::vector<Circuit> FindCycles(const Cfg& g, const Lr1& m, const Tables& tab) {
 
 // Groups single-byte shift-tailed edges by (source, origin, condition, push
 // prefix) into dynamic-target edges (optimizer.cpp:17-76).
-void Aggregate(const std::vector<int32_t>& shift, std::vector<BEdge>* edges) {
+int64_t Aggregate(const std::vector<int32_t>& shift, std::vector<BEdge>* edges) {
   using Key = std::tuple<int32_t, int, std::vector<int32_t>, std::vector<int32_t>>;
   std::map<Key, std::vector<size_t>> groups;
   std::vector<int> byte(edges->size(), -1);
@@ -850,13 +851,15 @@ void Aggregate(const std::vector<int32_t>& shift, std::vector<BEdge>* edges) {
     }
     made.push_back(std::move(d));
   }
-  if (made.empty()) return;
+  if (made.empty()) return 0;
+  const int64_t rewritten = static_cast<int64_t>(made.size());
   std::vector<BEdge> kept;
   for (size_t i = 0; i < edges->size(); ++i) {
     if (!gone[i]) kept.push_back(std::move((*edges)[i]));
   }
   for (BEdge& d : made) kept.push_back(std::move(d));
   edges->swap(kept);
+  return rewritten;
 }
 
 void CheckDeterminism(const std::vector<int32_t>& shift, int32_t accept, const std::vector<BEdge>& e,
@@ -894,9 +897,11 @@ void CheckDeterminism(const std::vector<int32_t>& shift, int32_t accept, const s
   }
 }
 
-// Number of two-terminal composites MergeEdges would build
-// (optimizer.cpp:78-136); composites are not part of the device automaton.
-int64_t CountComposites(const std::vector<BEdge>& e, int32_t S, int32_t accept) {
+// MergeEdges (optimizer.cpp:78-136): an edge whose target has exactly one
+// outgoing edge composes with it into one two-terminal edge; composites are
+// sequence-runner only (never read by Step / ComputeMask) and are kept for the
+// GMASKDP1 format.  `e` is in finalized order; output in generation order.
+std::vector<BEdge> MergeComposites(const std::vector<BEdge>& e, int32_t S, int32_t accept) {
   std::vector<int32_t> outdeg(S, 0), only(S, -1);
   std::vector<TSet> collapse(S);
   for (size_t i = 0; i < e.size(); ++i) {
@@ -904,7 +909,7 @@ int64_t CountComposites(const std::vector<BEdge>& e, int32_t S, int32_t accept) 
     only[e[i].src] = static_cast<int32_t>(i);
     if (e[i].origin == 2) collapse[e[i].src].Merge(e[i].acc);
   }
-  int64_t n = 0;
+  std::vector<BEdge> out;
   for (const BEdge& a : e) {
     if (a.dyn || a.acc.Has(kEnd) || a.target < 0 || a.target == accept || outdeg[a.target] != 1) continue;
     bool clash = false;
@@ -915,9 +920,57 @@ int64_t CountComposites(const std::vector<BEdge>& e, int32_t S, int32_t accept) 
     const size_t k = std::min(b.pop.size(), a.push.size());
     bool ok = true;
     for (size_t i = 0; i < k && ok; ++i) ok = b.pop[i] == a.push[a.push.size() - 1 - i];
-    n += ok ? 1 : 0;
+    if (!ok) continue;
+    BEdge c;
+    c.src = a.src;
+    c.origin = 3;
+    c.acc = a.acc;
+    c.acc2 = b.acc;
+    c.pop = a.pop;
+    c.pop.insert(c.pop.end(), b.pop.begin() + static_cast<int64_t>(k), b.pop.end());
+    c.push.assign(a.push.begin(), a.push.end() - static_cast<int64_t>(k));
+    c.push.insert(c.push.end(), b.push.begin(), b.push.end());
+    c.target = b.target;
+    out.push_back(std::move(c));
   }
-  return n;
+  return out;
+}
+
+Edge ToEdge(const BEdge& e) {
+  Edge o;
+  o.source = e.src;
+  std::memcpy(o.accepted, e.acc.w, sizeof(o.accepted));
+  o.dollar = e.acc.Has(kEnd);
+  o.origin = e.origin;
+  o.dynamic = e.dyn;
+  o.target = e.target;
+  o.match_pop = e.pop;
+  o.push = e.push;
+  std::memcpy(o.second, e.acc2.w, sizeof(o.second));
+  o.dollar_second = e.acc2.Has(kEnd);
+  return o;
+}
+
+BEdge FromEdge(const Edge& o) {
+  BEdge e;
+  e.src = o.source;
+  std::memcpy(e.acc.w, o.accepted, sizeof(o.accepted));
+  if (o.dollar) e.acc.Add(kEnd);
+  std::memcpy(e.acc2.w, o.second, sizeof(o.second));
+  if (o.dollar_second) e.acc2.Add(kEnd);
+  e.origin = o.origin;
+  e.dyn = o.dynamic;
+  e.target = o.target;
+  e.pop = o.match_pop;
+  e.push = o.push;
+  return e;
+}
+
+std::vector<int32_t> Ranges(const std::vector<BEdge>& edges, int32_t S) {
+  std::vector<int32_t> begin(static_cast<size_t>(S) + 1, 0);
+  for (const BEdge& e : edges) begin[e.src + 1]++;
+  for (int32_t s = 0; s < S; ++s) begin[s + 1] += begin[s];
+  return begin;
 }
 
 }  // namespace
@@ -975,29 +1028,49 @@ Automaton CompileGrammar(const std::string& text, bool aggregate, bool merge) {
     run.edges = &edges;
     run.Run();
   }
-  if (aggregate) Aggregate(a.shift_targets, &edges);
+  a.stats.states = S;
+  for (const BEdge& e : edges) {
+    a.stats.acceptance += e.origin == 0;
+    a.stats.reduction += e.origin == 1;
+    a.stats.cycle_back += e.origin == 2;
+  }
+  a.stats.edges_before_aggregation = static_cast<int64_t>(edges.size());
+  if (aggregate) a.stats.aggregated_groups = Aggregate(a.shift_targets, &edges);
   std::sort(edges.begin(), edges.end(), Before);
-  a.edge_begin.assign(static_cast<size_t>(S) + 1, 0);
-  for (const BEdge& e : edges) a.edge_begin[e.src + 1]++;
-  for (int32_t s = 0; s < S; ++s) a.edge_begin[s + 1] += a.edge_begin[s];
+  a.edge_begin = Ranges(edges, S);
   CheckDeterminism(a.shift_targets, m.accept, edges, a.edge_begin);
-  a.composites = merge ? CountComposites(edges, S, m.accept) : 0;
+  std::vector<BEdge> comps;
+  if (merge) {
+    comps = MergeComposites(edges, S, m.accept);
+    std::sort(comps.begin(), comps.end(), Before);
+  }
+  a.stats.merged = static_cast<int64_t>(comps.size());
+  a.composites = a.stats.merged;
 
   a.edges.reserve(edges.size());
-  for (const BEdge& e : edges) {
-    Edge o;
-    o.source = e.src;
-    std::memcpy(o.accepted, e.acc.w, sizeof(o.accepted));
-    o.dollar = e.acc.Has(kEnd);
-    o.origin = e.origin;
-    o.dynamic = e.dyn;
-    o.target = e.target;
-    o.match_pop = e.pop;
-    o.push = e.push;
-    a.edges.push_back(std::move(o));
-  }
+  for (const BEdge& e : edges) a.edges.push_back(ToEdge(e));
+  for (const BEdge& e : comps) a.composite_edges.push_back(ToEdge(e));
+  for (const Circuit& c : cycles) a.cycle_list.push_back(CycleRec{c.states, c.closing});
   a.cycles = static_cast<int64_t>(cycles.size());
   return a;
 }
+
+void FinalizeAndCheck(Automaton* a) {
+  std::vector<BEdge> edges, comps;
+  for (const Edge& e : a->edges) edges.push_back(FromEdge(e));
+  for (const Edge& e : a->composite_edges) comps.push_back(FromEdge(e));
+  std::sort(edges.begin(), edges.end(), Before);
+  std::sort(comps.begin(), comps.end(), Before);
+  a->edge_begin = Ranges(edges, a->num_states);
+  a->edges.clear();
+  a->composite_edges.clear();
+  for (const BEdge& e : edges) a->edges.push_back(ToEdge(e));
+  for (const BEdge& e : comps) a->composite_edges.push_back(ToEdge(e));
+  a->composites = static_cast<int64_t>(comps.size());
+  a->cycles = static_cast<int64_t>(a->cycle_list.size());
+  CheckDeterminism(a->shift_targets, a->accept_state, edges, a->edge_begin);
+}
+
+uint64_t GrammarHash(const std::string& normalized_text) { return Fnv1a(normalized_text); }
 
 }  // namespace pre3

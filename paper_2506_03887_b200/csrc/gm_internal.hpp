@@ -27,11 +27,26 @@ struct Edge {
   int32_t target = -1;
   std::vector<int32_t> match_pop;  // top first
   std::vector<int32_t> push;       // bottom first
+  // Composites only (origin 3): the second consumed terminal set.
+  uint64_t second[4] = {0, 0, 0, 0};
+  bool dollar_second = false;
 
   bool Accepts(int32_t terminal) const {
     if (terminal == 256) return dollar;
     return (accepted[terminal >> 6] >> (terminal & 63)) & 1u;
   }
+};
+
+// A rewritten pumping circuit (gmask::Cycle, dpda.hpp:62-70), bottom first.
+struct CycleRec {
+  std::vector<int32_t> states;
+  int closing_byte = 0;
+};
+
+// gmask::BuildStats (dpda.hpp:82-90).
+struct BuildStats {
+  int64_t states = 0, acceptance = 0, reduction = 0, cycle_back = 0, merged = 0, aggregated_groups = 0,
+          edges_before_aggregation = 0;
 };
 
 struct Automaton {
@@ -43,10 +58,14 @@ struct Automaton {
   std::vector<int32_t> shift_targets;  // S*256
   std::vector<Edge> edges;
   std::vector<int32_t> edge_begin;  // S+1
-  // Compile statistics (not serialized): two-terminal composites MergeEdges
-  // would build (sequence-runner only) and rewritten pumping circuits.
-  int64_t composites = 0;
-  int64_t cycles = 0;
+  // Build products the runtime never reads but the GMASKDP1 format carries
+  // (serialize.cpp:148-196): composites in arbitration order, rewritten
+  // circuits, BuildStats.  Absent (zero) for automata loaded from P3DPDA.
+  std::vector<Edge> composite_edges;
+  std::vector<CycleRec> cycle_list;
+  BuildStats stats;
+  int64_t composites = 0;  // composite_edges.size() (kept for P3DPDA-only automata: 0)
+  int64_t cycles = 0;      // cycle_list.size()
 
   void Validate() const;  // throws Error(GM_ERR_CORRUPT_INPUT)
 };
@@ -54,6 +73,17 @@ struct Automaton {
 Automaton LoadFlat(const uint8_t* data, size_t n);
 std::vector<uint8_t> SaveFlat(const Automaton& a);
 Automaton CompileGrammar(const std::string& text, bool aggregate, bool merge);
+// FinalizeEdgeOrder + ValidateDeterminism (dpda_builder.cpp:409-467) over an
+// automaton read from disk: edges and composites re-sorted in arbitration
+// order, ranges rebuilt; throws Error(GM_ERR_BUILD) when inconsistent.
+void FinalizeAndCheck(Automaton* a);
+uint64_t GrammarHash(const std::string& normalized_text);
+// GMASKDP1 (serialize.cpp): magic line + one sorted-key JSON object.
+std::vector<uint8_t> SaveGmaskdp1(const Automaton& a);
+Automaton LoadGmaskdp1(const uint8_t* data, size_t n);  // throws Error(GM_ERR_CORRUPT_INPUT)
+// LoadVocabulary / UnescapeToken / EscapeToken (serialize.cpp:298-364).
+std::vector<std::string> LoadVocabularyJson(const uint8_t* data, size_t n);
+std::string EscapeToken(const std::string& s);
 
 // Device-oriented flattening.  For every (state, terminal)
 // the candidate edges — those whose accepted set contains the terminal — in

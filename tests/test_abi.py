@@ -108,7 +108,7 @@ def test_usage_errors():
     a = pk.Automaton.load(flat("paren"))
     h = ctypes.c_void_p()
     data, offs = pk.pack_vocab([b"a"])
-    opts = pk._EngineOptions(17, 8192, 0, 256)
+    opts = pk._EngineOptions(33, 8192, 0, 256)  # K <= 32
     rc = pk.lib().gm_engine_create(a._h, data.ctypes.data, offs.ctypes.data, 1, ctypes.byref(opts), 0,
                                    ctypes.byref(h))
     assert rc == pk.GM_ERR_USAGE
