@@ -69,6 +69,9 @@ def parse(argv=None):
                    help="K: stack entries keying the context cache (default: the config's; SQL conditions pop up "
                         "to 34 entries, so config 4 keys deeper)")
     p.add_argument("--context-slots", type=int, default=None, help="context-cache hash table slots (power of two)")
+    p.add_argument("--parent-depth", type=int, default=0,
+                   help="R: new contexts are built from the context keyed R deep (0: engine default min(4, K-1); "
+                        "-1: full builds)")
     p.add_argument("--prewarm-steps", type=int, default=2000,
                    help="context-cache preprocessing: synthetic decode steps (other seed) before timing")
     p.add_argument("--prewarm-batch", type=int, default=1024)
@@ -298,7 +301,7 @@ def main(argv=None):
     vocab = pk.synth_vocab(args.vocab, args.flavor)
     automaton = pk.Automaton.load(flat)
     eng = pk.DeviceEngine(automaton, vocab, device=local, context_depth=args.context_depth,
-                          context_slots=args.context_slots)
+                          context_slots=args.context_slots, parent_depth=args.parent_depth)
     t_pre = time.perf_counter()
     if args.prewarm_steps > 0:
         eng.prewarm(args.prewarm_batch, args.prewarm_steps, seed=0xC0FFEE + rank)
@@ -471,7 +474,8 @@ def main(argv=None):
                           f"(seed differs from the timed streams)", "contexts_after_prewarm": pre_info["context_slots_used"],
                           "automaton": automaton.info()},
         "cache": {"contexts": info["context_slots_used"], "segment_builds": info["segment_builds"],
-                  "private_builds": info["private_builds"], "last_fill": fstats},
+                  "private_builds": info["private_builds"], "parent_builds": info["parent_builds"],
+                  "last_fill": fstats},
         "max_stack_depth_seen": max_depth,
     }
     print(json.dumps(line), flush=True)

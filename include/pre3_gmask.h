@@ -101,7 +101,9 @@ int gm_automaton_compile_stats(const gm_automaton* a, int64_t stats[4]);
 typedef struct gm_engine_options {
   int32_t context_depth;   /* K: stack entries keying the context cache (1..32; default 8) */
   int32_t context_slots;   /* hash-table capacity, power of two (default 8192) */
-  int64_t reserved;        /* must be 0 */
+  int64_t parent_depth;    /* R < K: a new context is built from the context of the same stack
+                              top keyed R deep, walking only that context's context-dependent
+                              tokens (0 = default min(4, K-1); negative = off) */
   int32_t segment_words;   /* vocab segment size in mask words (default 256) */
 } gm_engine_options;
 
@@ -115,7 +117,7 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes,
                      const gm_engine_options* opts, int device, gm_engine** out);
 int gm_engine_destroy(gm_engine* e);
 /* info[0..7] = V, W, num_segments, context slots used, segment builds,
- * private (uncached) rows built, 0, device */
+ * private (uncached) rows built, contexts built from a parent context, device */
 int gm_engine_info(gm_engine* e, int64_t info[8]);
 /* Host bitmask (W words) of "structural" tokens used by the synthetic
  * stream sampler (tokens containing any of {}[],:" ). */

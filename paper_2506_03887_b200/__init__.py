@@ -271,7 +271,7 @@ class Automaton:
 
 class _EngineOptions(ctypes.Structure):
     _fields_ = [("context_depth", ctypes.c_int32), ("context_slots", ctypes.c_int32),
-                ("reserved", ctypes.c_int64), ("segment_words", ctypes.c_int32)]
+                ("parent_depth", ctypes.c_int64), ("segment_words", ctypes.c_int32)]
 
 
 @dataclass
@@ -286,14 +286,14 @@ class DeviceEngine:
     """Engine::Engine + TokenTrie::Build on one CUDA device (runtime.cpp:18-113)."""
 
     def __init__(self, automaton: Automaton, tokens: Sequence[bytes], device: int = 0,
-                 context_depth: int = 8, context_slots: int = 8192):
+                 context_depth: int = 8, context_slots: int = 8192, parent_depth: int = 0):
         self.automaton = automaton
         self.tokens = list(tokens)
         self.V = len(self.tokens)
         self.W = (self.V + 1 + 31) // 32
         self.device = device
         data, offs = pack_vocab(self.tokens)
-        opts = _EngineOptions(context_depth, context_slots, 0, 256)
+        opts = _EngineOptions(context_depth, context_slots, parent_depth, 256)
         h = ctypes.c_void_p()
         _check(lib().gm_engine_create(automaton._h, _ptr(data), _ptr(offs), self.V, ctypes.byref(opts),
                                       device, ctypes.byref(h)))
@@ -306,7 +306,7 @@ class DeviceEngine:
         out = np.zeros(8, np.int64)
         _check(lib().gm_engine_info(self._h, _ptr(out)))
         keys = ["V", "W", "num_segments", "context_slots_used", "segment_builds", "private_builds",
-                "reserved", "device"]
+                "parent_builds", "device"]
         return dict(zip(keys, (int(x) for x in out)))
 
     def prewarm(self, batch: int = 1024, steps: int = 200, seed: int = 0x5EED, stream=None) -> None:

@@ -250,7 +250,14 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
       if (opts->context_depth) o.context_depth = opts->context_depth;
       if (opts->context_slots) o.context_slots = opts->context_slots;
       if (opts->segment_words) o.segment_words = opts->segment_words;
+      o.parent_depth = opts->parent_depth;
     }
+    // Parent key depth R: new contexts keyed K deep are built from the
+    // context of the same stack top keyed R deep (0 = default min(4, K-1);
+    // negative = off: every new context is built over the whole vocabulary).
+    if (o.parent_depth == 0) o.parent_depth = o.context_depth > 1 ? std::min<int64_t>(4, o.context_depth - 1) : -1;
+    if (o.parent_depth >= o.context_depth) return Fail(GM_ERR_USAGE, "parent_depth must be < context_depth");
+    if (o.parent_depth < 0) o.parent_depth = 0;
     if (o.context_depth < 1 || o.context_depth > pre3::kMaxContext) return Fail(GM_ERR_USAGE, "context_depth must be 1..32");
     if (o.context_slots < 1 || (o.context_slots & (o.context_slots - 1))) return Fail(GM_ERR_USAGE, "context_slots must be a power of two");
     if (o.segment_words != pre3::kSegWords) return Fail(GM_ERR_USAGE, "segment_words must be 256");
@@ -322,6 +329,9 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.cd_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.seg_done = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.slot_built = DevAlloc<int32_t>(C, &e->owned);
+    c.slot_parent = DevAlloc<int32_t>(C, &e->owned);
+    Check(cudaMemset(c.slot_parent, 0xff, C * 4), "memset");
+    c.R = static_cast<int32_t>(o.parent_depth);
     c.cd_segmask = DevAlloc<uint32_t>(C, &e->owned);
     Check(cudaMemset(c.cd_segmask, 0, C * 4), "memset");
     Check(cudaMemset(c.slot_built, 0, C * 4), "memset");
@@ -348,14 +358,13 @@ int gm_engine_info(gm_engine* e, int64_t info[8]) {
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     unsigned long long ctr[8];
     Check(cudaMemcpy(ctr, e->cache.counters, 64, cudaMemcpyDeviceToHost), "info");
-    const unsigned long long top = 0;
     info[0] = e->V;
     info[1] = e->W;
     info[2] = e->nseg;
     info[3] = static_cast<int64_t>(ctr[0]);
     info[4] = static_cast<int64_t>(ctr[1]);
     info[5] = static_cast<int64_t>(ctr[2]);
-    info[6] = static_cast<int64_t>(top);
+    info[6] = static_cast<int64_t>(ctr[3]);
     info[7] = e->device;
     return GM_OK;
   });
@@ -401,7 +410,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.h_cap = static_cast<int32_t>(std::min<size_t>(bn, std::max<size_t>(64, 2 * static_cast<size_t>(batch))));
     Check(cudaMemset(v.priv_done, 0, bn * 4), "memset");
     for (int q = 0; q < 3; ++q) {
-      v.queue[q].items = DevAlloc<int4>(2 * bn, &b->owned);
+      v.queue[q].items = DevAlloc<int4>(4 * bn, &b->owned);  // a new context may queue its parent too
       v.queue[q].n_items = DevAlloc<unsigned int>(1, &b->owned);
       v.queue[q].next_unit = DevAlloc<unsigned int>(1, &b->owned);
       v.queue[q].heavy = DevAlloc<int2>(static_cast<size_t>(v.h_cap), &b->owned);

@@ -426,6 +426,7 @@ __device__ int AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, in
   bool wait = true;
   if (slot < 0 || created) {
     // Slots are never reused, so a new slot's counters are still zero.
+    const BuildQueue Q = QueueOf(Bt, q);
     if (slot < 0) {
       slot = Cc.C + b;
       for (int s = 0; s < nseg; ++s) Bt.priv_done[static_cast<long long>(b) * nseg + s] = 0;
@@ -433,8 +434,21 @@ __device__ int AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, in
       __threadfence();  // zeroed counters visible before the items
     } else {
       atomicAdd(Cc.counters + 1, static_cast<unsigned long long>(nseg));
+      if (Cc.R > 0 && n > Cc.R) {
+        // Parent: the same top keyed R deep (queued first, so its units are
+        // dequeued before the child's).
+        bool pc = false;
+        const int parent = LookupSlot(Cc, key, Cc.R, 0, &pc);
+        if (pc) {
+          atomicAdd(Cc.counters + 1, static_cast<unsigned long long>(nseg));
+          const unsigned int pat = atomicAdd(Q.n_items, static_cast<unsigned int>(nseg));
+          for (int s = 0; s < nseg; ++s) Q.items[pat + s] = make_int4(parent, s, b, 0);
+        }
+        Cc.slot_parent[slot] = parent;
+        if (parent >= 0) atomicAdd(Cc.counters + 3, 1ull);
+        __threadfence();  // parent link visible before the child's items
+      }
     }
-    const BuildQueue Q = QueueOf(Bt, q);
     const unsigned int at = atomicAdd(Q.n_items, static_cast<unsigned int>(nseg));
     for (int s = 0; s < nseg; ++s) Q.items[at + s] = make_int4(slot, s, b, 0);
   } else {
@@ -488,16 +502,49 @@ __device__ void PublishHeavy(const BatchView& Bt, int q, int tag, int b, uint32_
   }
 }
 
+// Bounded wait (one thread) for the build of (slot, seg).  Units of this
+// batch's queue were all dequeued by running CTAs before any fill item got
+// here, so they finish; a slot whose build sits in another batch's queue may
+// not, so the wait gives up after 2 ms and the caller fills directly.
+__device__ bool WaitBuilt(const CacheView& Cc, const BatchView& Bt, int slot, int seg, int nseg) {
+  const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * nseg + seg
+                                : Bt.priv_done + static_cast<long long>(slot - Cc.C) * nseg + seg;
+  bool ok = LoadAcquire(done) >= kChunksPerSeg;
+  if (!ok) {
+    unsigned long long t_start, t_now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    do {
+      __nanosleep(256);
+      ok = LoadAcquire(done) >= kChunksPerSeg;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+    } while (!ok && t_now - t_start < 2000000ull);
+  }
+  return ok;
+}
+
 // ---------------------------------------------------------------------------
 // Build unit: 256 tokens of one (slot, segment) item, one per thread.
 // ---------------------------------------------------------------------------
 __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt,
-                          const int4 it, int chunk, int32_t* base_s) {
+                          const int4 it, int chunk, int32_t* base_s, int* sh_flag) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int slot = it.x, seg = it.y, b = it.z;
   const bool priv = slot >= Cc.C;
+  const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   int nb;
   bool complete;
+  // Incremental build from the parent context (the same stack top keyed R
+  // deep): every token the parent decided keeps its verdict (its walk never
+  // looked below the top R entries the child key shares); only the parent's
+  // context-dependent tokens are walked with the child's deeper key.
+  // A parent whose segment is not built yet (new in the same step) is not
+  // waited for: blocking a CTA on another unit's progress costs more than
+  // walking this unit's 256 tokens in full.
+  int parent = priv ? -1 : __ldcg(Cc.slot_parent + slot);
+  if (parent >= 0 && LoadAcquire(Cc.seg_done + static_cast<long long>(parent) * Vv.nseg + seg) < kChunksPerSeg) {
+    parent = -1;
+  }
+  (void)sh_flag;
   __syncthreads();  // base_s reuse
   if (priv) {
     // Private row: the sequence's whole current stack (always complete).
@@ -515,7 +562,16 @@ __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView
   __syncthreads();
   const int t = seg * kSegTokens + chunk * kThreads + tid;
   int r = kReject;
-  if (t <= Vv.V) r = WalkToken(A, Vv, t, base_s, nb, complete);
+  if (t <= Vv.V) {
+    if (parent >= 0) {
+      const uint32_t pcd = __ldcg(Cc.cdb + static_cast<long long>(parent) * Vv.W + (t >> 5));
+      const uint32_t pci = __ldcg(Cc.ci + static_cast<long long>(parent) * Vv.W + (t >> 5));
+      if ((pcd >> (t & 31)) & 1u) r = WalkToken(A, Vv, t, base_s, nb, complete);
+      else r = ((pci >> (t & 31)) & 1u) ? kAccept : kReject;
+    } else {
+      r = WalkToken(A, Vv, t, base_s, nb, complete);
+    }
+  }
   const unsigned acc = __ballot_sync(0xffffffffu, r == kAccept);
   const unsigned cd = __ballot_sync(0xffffffffu, r == kUnknown);
   if (__any_sync(0xffffffffu, r == kOverflow) && lane == 0) atomicOr(Bt.err, 1u);
@@ -539,6 +595,7 @@ __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView
                      : Cc.seg_done + static_cast<long long>(slot) * Vv.nseg + seg;
     atomicAdd(done, 1);
     if (!priv) atomicAdd(Cc.slot_built + slot, 1);
+    TraceEvent(Bt, 5, slot, seg, t_in, static_cast<unsigned long long>(parent >= 0));
   }
 }
 
@@ -556,7 +613,7 @@ __device__ void HelpBuild(const AutView& A, const VocabView& Vv, const CacheView
     const unsigned int u = static_cast<unsigned int>(*sh_unit);
     __syncthreads();
     if (u >= units) break;
-    BuildUnit(A, Vv, Cc, Bt, Q.items[u / kChunksPerSeg], static_cast<int>(u % kChunksPerSeg), base_s);
+    BuildUnit(A, Vv, Cc, Bt, Q.items[u / kChunksPerSeg], static_cast<int>(u % kChunksPerSeg), base_s, sh_unit);
   }
 }
 
@@ -729,16 +786,39 @@ __device__ uint32_t AssignSlotWarp(const CacheView& Cc, const BatchView& Bt, int
   bool wait = true;
   if (slot < 0 || created) {
     // Slots are never reused, so a new slot's counters are still zero.
+    const BuildQueue Q = QueueOf(Bt, q);
     if (slot < 0) {
       slot = Cc.C + b;
       for (int s = lane; s < nseg; s += 32) Bt.priv_done[static_cast<long long>(b) * nseg + s] = 0;
       __threadfence();  // zeroed counters visible before the items
       __syncwarp();
       if (lane == 0) atomicAdd(Cc.counters + 2, 1ull);
-    } else if (lane == 0) {
-      atomicAdd(Cc.counters + 1, static_cast<unsigned long long>(nseg));
+    } else {
+      if (lane == 0) atomicAdd(Cc.counters + 1, static_cast<unsigned long long>(nseg));
+      if (Cc.R > 0 && n > Cc.R) {
+        // Parent: the same top keyed R deep (queued first, so its units are
+        // dequeued before the child's); the child walks only its CD tokens.
+        bool pc = false;
+        int pbuilt = 0;
+        uint32_t psm = 0u;
+        const int parent = LookupSlotWarp(Cc, kv, Cc.R, 0, lane, &pc, &pbuilt, &psm);
+        if (pc) {
+          unsigned int pat = 0;
+          if (lane == 0) {
+            atomicAdd(Cc.counters + 1, static_cast<unsigned long long>(nseg));
+            pat = atomicAdd(Q.n_items, static_cast<unsigned int>(nseg));
+          }
+          pat = __shfl_sync(0xffffffffu, pat, 0);
+          for (int s = lane; s < nseg; s += 32) Q.items[pat + s] = make_int4(parent, s, b, 0);
+        }
+        if (lane == 0) {
+          Cc.slot_parent[slot] = parent;
+          if (parent >= 0) atomicAdd(Cc.counters + 3, 1ull);
+        }
+        __threadfence();  // parent link visible before the child's items
+        __syncwarp();
+      }
     }
-    const BuildQueue Q = QueueOf(Bt, q);
     unsigned int at = 0;
     if (lane == 0) at = atomicAdd(Q.n_items, static_cast<unsigned int>(nseg));
     at = __shfl_sync(0xffffffffu, at, 0);
@@ -1128,26 +1208,6 @@ __device__ __forceinline__ unsigned long long WarpMax64(unsigned long long v) {
     v = y > v ? y : v;
   }
   return v;
-}
-
-// Bounded wait (one thread) for the build of (slot, seg).  Units of this
-// batch's queue were all dequeued by running CTAs before any fill item got
-// here, so they finish; a slot whose build sits in another batch's queue may
-// not, so the wait gives up after 2 ms and the caller fills directly.
-__device__ bool WaitBuilt(const CacheView& Cc, const BatchView& Bt, int slot, int seg, int nseg) {
-  const int* done = slot < Cc.C ? Cc.seg_done + static_cast<long long>(slot) * nseg + seg
-                                : Bt.priv_done + static_cast<long long>(slot - Cc.C) * nseg + seg;
-  bool ok = LoadAcquire(done) >= kChunksPerSeg;
-  if (!ok) {
-    unsigned long long t_start, t_now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    do {
-      __nanosleep(256);
-      ok = LoadAcquire(done) >= kChunksPerSeg;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
-    } while (!ok && t_now - t_start < 2000000ull);
-  }
-  return ok;
 }
 
 // The sequence's last finished fill item: sample (stream or greedy), accept,

@@ -62,9 +62,11 @@ struct CacheView {
   int32_t* seg_done;              // C*nseg completed build units (kChunksPerSeg = built)
   int32_t* slot_built;            // C completed build units over all segments
   uint32_t* cd_segmask;           // C: bit s set when segment s has context-dependent tokens
-  unsigned long long* counters;   // [0] slots, [1] segment builds, [2] private builds
+  int32_t* slot_parent;           // C: context a new one is built from (-1: full build)
+  unsigned long long* counters;   // [0] slots, [1] segment builds, [2] private builds, [3] parent-based builds
   int32_t C;
   int32_t K;
+  int32_t R;                      // parent key depth (0: no parents)
 };
 
 // Build work queue: items {slot, seg, seq, 0}; units = items * kChunksPerSeg.

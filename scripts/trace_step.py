@@ -18,13 +18,16 @@ p = argparse.ArgumentParser()
 p.add_argument("--batch", type=int, default=256)
 p.add_argument("--fused", action="store_true")
 p.add_argument("--grammar", default="json")
+p.add_argument("--flavor", type=int, default=0)
+p.add_argument("--parent", type=int, default=0)
 p.add_argument("--steps", type=int, default=3)
 p.add_argument("--k", type=int, default=12)
 p.add_argument("--slots", type=int, default=8192)
 a = p.parse_args()
 flat = bench.automaton_bytes(a.grammar)
-vocab = pk.synth_vocab(128255)
-eng = pk.DeviceEngine(pk.Automaton.load(flat), vocab, device=0, context_depth=a.k, context_slots=a.slots)
+vocab = pk.synth_vocab(128255, a.flavor)
+eng = pk.DeviceEngine(pk.Automaton.load(flat), vocab, device=0, context_depth=a.k, context_slots=a.slots,
+                      parent_depth=a.parent)
 eng.prewarm(1024, 2000, seed=0xC0FFEE)
 B = a.batch
 batch = eng.batch(B, 1024)
@@ -46,9 +49,9 @@ def step(i):
 for i in range(40):
     step(i)
 torch.cuda.synchronize()
-cap = 1 << 16
+cap = 1 << 20
 tr = torch.zeros(4 * (cap + 1), dtype=torch.int64, device=dev)
-names = {1: "light", 2: "heavy", 3: "tail", 4: "accept", 10: "h:build", 11: "h:wait", 12: "h:cdscan", 13: "h:walks",
+names = {1: "light", 2: "heavy", 3: "tail", 4: "accept", 5: "build", 10: "h:build", 11: "h:wait", 12: "h:cdscan", 13: "h:walks",
          20: "a:step", 21: "a:lookup", 22: "a:publish"}
 for s in range(a.steps):
     tr.zero_()
@@ -57,11 +60,11 @@ for s in range(a.steps):
     torch.cuda.synchronize()
     batch.set_trace(None)
     t = tr.cpu().numpy().view(np.uint64)
-    n = int(t[0])
+    n = min(int(t[0]), cap)
     rec = t[4:4 * (n + 1)].reshape(n, 4).astype(np.int64)
     kind = rec[:, 0] & 0xff
     t0 = rec[:, 1].min()
-    print(f"step {s}: {n} records, span {(rec[:, 2].max() - t0) / 1e3:.1f} us")
+    print(f"step {s}: {n} records, span {(rec[:, 2].max() - t0) / 1e3:.1f} us, contexts {eng.info()['context_slots_used']}")
     for k in sorted(set(kind.tolist())):
         r = rec[kind == k]
         st = (r[:, 1] - t0) / 1e3

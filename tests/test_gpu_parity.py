@@ -299,3 +299,25 @@ def test_workload_grammar_stream_matches_port(name, flavor):
             d = pstacks[b, 0]
             got = batch.get(b)
             assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1]
+
+
+@pytest.mark.parametrize("K,R", [(12, -1), (12, 1), (12, 3), (12, 8), (16, 4), (6, 5)])
+def test_parent_based_context_builds(K, R):
+    """New contexts built from their parent context (same stack top keyed R
+    deep; only the parent's context-dependent tokens re-walked) give the same
+    decode loop as full builds: tokens every step and final stacks equal the
+    C port's."""
+    vocab = pk.synth_vocab(128255)
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K, parent_depth=R)
+    port = Port(f, vocab)
+    B, steps, seed = 24, 20, 11
+    batch, masks, tokens = run_stream(eng, B, steps, seed, fused=True)
+    _, ptoks, pstacks = port.decode_run(eng.structural, B, steps, seed, want_tokens=True, want_stacks=True)
+    assert np.array_equal(tokens, ptoks)
+    for b in range(B):
+        d = pstacks[b, 0]
+        got = batch.get(b)
+        assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1]
+    info = eng.info()
+    assert (info["parent_builds"] > 0) == (R > 0)
