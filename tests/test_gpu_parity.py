@@ -321,3 +321,32 @@ def test_parent_based_context_builds(K, R):
         assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1]
     info = eng.info()
     assert (info["parent_builds"] > 0) == (R > 0)
+
+
+def test_tokenizer_json_vocabulary_on_device():
+    """A byte-level BPE vocabulary ingested from a tokenizer.json
+    (paper_2506_03887_b200/tokenizer.py) drives the device loop exactly like
+    the C port (tokens every step, final stacks)."""
+    tokenizers = pytest.importorskip("tokenizers")
+    from tokenizers import Tokenizer, decoders, models, pre_tokenizers, trainers
+    from paper_2506_03887_b200 import tokenizer as tk
+    corpus = ['{"name": "ada", "tags": ["x", "y"], "n": [1, 2, 30], "ok": true, "z": null}',
+              '[{"a": {"b": []}}, "s p a c e", -12]'] * 50
+    tok = Tokenizer(models.BPE())
+    tok.pre_tokenizer = pre_tokenizers.ByteLevel(add_prefix_space=False)
+    tok.decoder = decoders.ByteLevel()
+    tok.train_from_iterator(corpus, trainers.BpeTrainer(vocab_size=1500, show_progress=False,
+                                                        initial_alphabet=pre_tokenizers.ByteLevel.alphabet()))
+    tok.add_special_tokens(["<|endoftext|>"])
+    tv = tk.from_tokenizer_json(tok.to_str())
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), tv.tokens, context_depth=12)
+    port = Port(f, tv.tokens)
+    B, steps, seed = 16, 24, 3
+    batch, masks, tokens = run_stream(eng, B, steps, seed, fused=True)
+    _, ptoks, pstacks = port.decode_run(eng.structural, B, steps, seed, want_tokens=True, want_stacks=True)
+    assert np.array_equal(tokens, ptoks)
+    for b in range(B):
+        d = pstacks[b, 0]
+        got = batch.get(b)
+        assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1]
