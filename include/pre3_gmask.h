@@ -195,6 +195,25 @@ int gm_sample_stream(gm_batch* b, const uint32_t* bitmask, int64_t ld_words, con
 int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, uint32_t* bitmask,
                           int64_t ld_words, int32_t* tokens_out, void* stream);
 
+/* Temperature / top-k / top-p sampling over each sequence's allowed tokens
+ * (new work): keep the allowed tokens whose logit is among the
+ * top_k largest (0 = all; ties at the threshold kept), weight them by
+ * exp((logit - max) / temperature) in exact 2^-32 fixed point, keep the
+ * smallest key-descending prefix holding top_p of the weight (ties kept),
+ * and draw from it with the sequence's stream draw (seed, draws).  Integer
+ * results are bit-exact with oracle/gmask_port.c gp_sample_pick.  accept != 0
+ * also accepts the token (Engine::Step per byte), restarts finished sequences
+ * and looks up the next context — no host round trip.  bitmask comes from a
+ * preceding fill of the same batch. */
+int gm_sample_tokens(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, const uint32_t* bitmask,
+                     int64_t ld_words, float temperature, int32_t top_k, float top_p, uint64_t seed,
+                     int32_t* tokens_out, int32_t accept, void* stream);
+/* One decode step with that sampler: gm_fill_next_token_bitmask (bitmask may
+ * be NULL) then gm_sample_tokens(accept = 1). */
+int gm_decode_step_sample(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, uint32_t* bitmask,
+                          int64_t ld_words, float temperature, int32_t top_k, float top_p, uint64_t seed,
+                          int32_t* tokens_out, void* stream);
+
 /* Statistics accumulated while enabled (gm_batch_set_stats), reset on read:
  * stats[0] = logits bytes read, [1] = logits bytes written (16-B chunk
  * granularity), [2] = context-dependent token walks, [3] = build items,

@@ -310,6 +310,8 @@ class Port:
                 "gp_stream_draw": ([U64, U64, U64], U64),
                 "gp_stream_pick": ([P, P, I32, U64], I32),
                 "gp_greedy_pick": ([P, P, I32], I32),
+                "gp_sample_pick": ([P, P, I32, ctypes.c_float, I32, ctypes.c_uint32, U64], I32),
+                "gp_sample_weight": ([ctypes.c_uint32, ctypes.c_float, ctypes.c_float], U64),
                 "gp_decode_run": ([P, P, P, P, P, I32, I32, U64, I32, P, P, P], ctypes.c_int),
             }
             for n, (a, r) in sigs.items():
@@ -398,6 +400,14 @@ class Port:
     @classmethod
     def stream_draw(cls, seed: int, seq: int, draw: int) -> int:
         return cls.lib().gp_stream_draw(seed, seq, draw)
+
+    def sample_pick(self, mask: np.ndarray, logits_bf16: np.ndarray, temperature: float, top_k: int, top_p: float,
+                    u: int) -> int:
+        """Temperature / top-k / top-p pick (the SampleKernel rule)."""
+        p24 = (1 << 24) if top_p >= 1.0 else max(1, int(np.floor(np.float64(np.float32(top_p)) * 16777216.0)))
+        return int(self.lib().gp_sample_pick(_ptr(np.ascontiguousarray(mask, np.uint32)),
+                                             _ptr(np.ascontiguousarray(logits_bf16, np.uint16)), self.V,
+                                             float(temperature), int(top_k), p24, u & (2**64 - 1)))
 
     def greedy_pick(self, mask: np.ndarray, logits_bf16: np.ndarray) -> int:
         return self.lib().gp_greedy_pick(_ptr(mask), _ptr(logits_bf16), self.V)

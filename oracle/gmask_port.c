@@ -15,6 +15,7 @@
 #define _POSIX_C_SOURCE 199309L
 #include "gmask_port.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
@@ -405,6 +406,114 @@ int32_t gp_greedy_pick(const uint32_t* mask, const uint16_t* logits, int32_t V) 
     if (best < 0 || k > best_key) { best = t; best_key = k; }
   }
   return best;
+}
+
+/* ------------------------------------------------------------ sampler
+ * Temperature / top-k / top-p sampling over the allowed tokens — the rule of
+ * kernels.cu SampleKernel, restated with one full 16-bit key
+ * histogram instead of the device's two-level one.  Compiled with
+ * -ffp-contract=off: the weight is the same sequence of correctly rounded
+ * fp32 operations as on the device. */
+static uint32_t sample_key(uint32_t bits16) {
+  return (bits16 & 0x8000u) ? (~bits16 & 0xFFFFu) : (bits16 | 0x8000u);
+}
+
+static float key_value(uint32_t key) {
+  uint32_t bits = ((key & 0x8000u) ? (key & 0x7FFFu) : (~key & 0xFFFFu)) << 16;
+  float f;
+  memcpy(&f, &bits, 4);
+  return f;
+}
+
+uint64_t gp_sample_weight(uint32_t key, float vmax, float temperature) {
+  float v = key_value(key);
+  float d = v - vmax;
+  float x = d / temperature;
+  float y = x * 1.44269502f;
+  if (!(y >= -64.0f)) return 0;
+  if (y > 0.0f) return 0;
+  float fl = floorf(y);
+  int n = (int)fl;
+  float f = y - fl;
+  float p = 1.54035304e-4f;
+  p = fmaf(p, f, 1.33335581e-3f);
+  p = fmaf(p, f, 9.61812911e-3f);
+  p = fmaf(p, f, 5.55041087e-2f);
+  p = fmaf(p, f, 2.40226507e-1f);
+  p = fmaf(p, f, 6.93147181e-1f);
+  p = fmaf(p, f, 1.0f);
+  uint32_t sbits = (uint32_t)(n + 32 + 127) << 23;
+  float scale;
+  memcpy(&scale, &sbits, 4);
+  return (uint64_t)llrintf(p * scale);
+}
+
+int32_t gp_sample_pick(const uint32_t* mask, const uint16_t* logits, int32_t V, float temperature, int32_t top_k,
+                       uint32_t top_p24, uint64_t u) {
+  int32_t v1 = V + 1;
+  uint32_t* cnt = (uint32_t*)calloc(65536, sizeof(uint32_t));
+  uint32_t n_allowed = 0, kmax = 0;
+  for (int32_t t = 0; t < v1; ++t) {
+    if (!((mask[t >> 5] >> (t & 31)) & 1u)) continue;
+    uint32_t k = sample_key(logits[t]);
+    cnt[k]++;
+    n_allowed++;
+    if (k > kmax) kmax = k;
+  }
+  int32_t tok = -1;
+  if (n_allowed > 0) {
+    float vmax = key_value(kmax);
+    /* kept_k: keys >= the k-th largest key (ties kept) */
+    uint32_t tau_k = 0;
+    if (top_k > 0 && (uint32_t)top_k < n_allowed) {
+      uint32_t cum = 0;
+      for (int32_t k = 65535; k >= 0; --k) {
+        cum += cnt[k];
+        if (cum >= (uint32_t)top_k) { tau_k = (uint32_t)k; break; }
+      }
+    }
+    unsigned __int128 s_k = 0;
+    for (int32_t k = 65535; k >= (int32_t)tau_k; --k) {
+      if (cnt[k]) s_k += (unsigned __int128)cnt[k] * gp_sample_weight((uint32_t)k, vmax, temperature);
+    }
+    uint32_t tau_p = tau_k;
+    unsigned __int128 s_p = s_k;
+    if (s_k > 0 && top_p24 < (1u << 24)) {
+      unsigned __int128 prod = s_k * top_p24;
+      unsigned __int128 target = (prod >> 24) + ((prod & 0xFFFFFFu) ? 1 : 0);
+      unsigned __int128 cum = 0;
+      for (int32_t k = 65535; k >= (int32_t)tau_k; --k) {
+        if (!cnt[k]) continue;
+        cum += (unsigned __int128)cnt[k] * gp_sample_weight((uint32_t)k, vmax, temperature);
+        if (cum >= target) { tau_p = (uint32_t)k; s_p = cum; break; }
+      }
+    }
+    uint32_t kappa = kmax;
+    uint64_t jth = 0;
+    if (s_p > 0) {
+      uint64_t r = (uint64_t)((s_p * (uint32_t)u) >> 32);
+      unsigned __int128 cum = 0;
+      for (int32_t k = 65535; k >= (int32_t)tau_p; --k) {
+        if (!cnt[k]) continue;
+        uint64_t w = gp_sample_weight((uint32_t)k, vmax, temperature);
+        unsigned __int128 wb = (unsigned __int128)cnt[k] * w;
+        if ((unsigned __int128)r < cum + wb) {
+          kappa = (uint32_t)k;
+          jth = (uint64_t)(((unsigned __int128)r - cum) / w);
+          break;
+        }
+        cum += wb;
+      }
+    }
+    for (int32_t t = 0; t < v1; ++t) {
+      if (!((mask[t >> 5] >> (t & 31)) & 1u)) continue;
+      if (sample_key(logits[t]) != kappa) continue;
+      if (jth == 0) { tok = t; break; }
+      --jth;
+    }
+  }
+  free(cnt);
+  return tok;
 }
 
 /* ------------------------------------------------------------ decode loop */

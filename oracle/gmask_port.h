@@ -58,6 +58,11 @@ void gp_mask_naive(const gp_automaton* a, const gp_config* c, const uint8_t* byt
 uint64_t gp_stream_draw(uint64_t seed, uint64_t seq, uint64_t draw);
 int32_t gp_stream_pick(const uint32_t* mask, const uint32_t* structural, int32_t V, uint64_t u);
 int32_t gp_greedy_pick(const uint32_t* mask, const uint16_t* logits_bf16, int32_t V);
+/* Temperature / top-k / top-p pick (kernels.cu SampleKernel rule); u = the
+ * sequence's stream draw; top_p24 = floor(top_p * 2^24) (2^24 = off). */
+int32_t gp_sample_pick(const uint32_t* mask, const uint16_t* logits_bf16, int32_t V, float temperature,
+                       int32_t top_k, uint32_t top_p24, uint64_t u);
+uint64_t gp_sample_weight(uint32_t key, float vmax, float temperature);
 
 /* Decode loop over `batch` sequences, `steps` steps, restart on finish (same
  * contract as ref_decode_run in oracle/ref_shim.cpp, single thread).

@@ -130,6 +130,10 @@ def lib() -> ctypes.CDLL:
             "gm_sample_stream": ([P, P, I64, P, U64, P, P], ctypes.c_int),
             "gm_decode_step_stream": ([P, P, I64, P, I64, U64, P, P], ctypes.c_int),
             "gm_decode_step_greedy": ([P, P, I64, P, I64, P, P], ctypes.c_int),
+            "gm_sample_tokens": ([P, P, I64, P, I64, ctypes.c_float, I32, ctypes.c_float, U64, P, I32, P],
+                                 ctypes.c_int),
+            "gm_decode_step_sample": ([P, P, I64, P, I64, ctypes.c_float, I32, ctypes.c_float, U64, P, P],
+                                      ctypes.c_int),
             "gmw_synth_vocab": ([I32, I32, P, I64, P], I64),
             "gmw_structural_words": ([P, P, I32, P], I32),
         }
@@ -353,6 +357,10 @@ class DeviceEngine:
             self._h = ctypes.c_void_p()
 
 
+def _dptr(t) -> Optional[int]:
+    return t.data_ptr() if t is not None else None
+
+
 def _stream(stream) -> Optional[int]:
     if stream is None:
         import torch
@@ -422,6 +430,21 @@ class Batch:
         bm = bitmask.data_ptr() if bitmask is not None else None
         ldw = bitmask.stride(0) if bitmask is not None else 0
         _check(lib().gm_decode_step_greedy(self._h, logits.data_ptr(), logits.stride(0), bm, ldw, to,
+                                           _stream(stream)))
+
+    def sample(self, logits, bitmask, temperature: float = 1.0, top_k: int = 0, top_p: float = 1.0, seed: int = 0,
+               tokens_out=None, accept: bool = True, stream=None):
+        """gm_sample_tokens: temperature / top-k / top-p over the allowed tokens (+ accept)."""
+        _check(lib().gm_sample_tokens(self._h, _dptr(logits), logits.stride(0), _dptr(bitmask), bitmask.stride(0),
+                                      float(temperature), int(top_k), float(top_p), seed & (2**64 - 1),
+                                      _dptr(tokens_out), int(accept), _stream(stream)))
+
+    def decode_step_sample(self, logits, temperature: float = 1.0, top_k: int = 0, top_p: float = 1.0,
+                           seed: int = 0, tokens_out=None, bitmask=None, stream=None):
+        """gm_decode_step_sample: fill + sample + accept, no host round trip."""
+        _check(lib().gm_decode_step_sample(self._h, _dptr(logits), logits.stride(0), _dptr(bitmask),
+                                           bitmask.stride(0) if bitmask is not None else 0, float(temperature),
+                                           int(top_k), float(top_p), seed & (2**64 - 1), _dptr(tokens_out),
                                            _stream(stream)))
 
     def check(self, stream=None):

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -697,6 +698,66 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
           "greedy decode launch");
     b->EndFill(true);
     return GM_OK;
+  });
+}
+
+namespace {
+int SampleCommon(gm_batch* b, const uint16_t* logits, int64_t ld, const uint32_t* bitmask, int64_t ld_words,
+                 float temperature, int32_t top_k, float top_p, uint64_t seed, int32_t* tokens_out, bool accept,
+                 cudaStream_t s) {
+  gm_engine* e = b->engine;
+  if (!(temperature > 0.0f) || top_k < 0 || !(top_p > 0.0f)) {
+    return Fail(GM_ERR_USAGE, "temperature > 0, top_k >= 0, top_p in (0, 1] required");
+  }
+  pre3::SampleArgs g{};
+  g.bitmask = bitmask;
+  g.ldw = ld_words;
+  g.logits = logits;
+  g.ld = ld;
+  g.temperature = temperature;
+  g.top_k = top_k;
+  g.top_p24 = top_p >= 1.0f ? (1u << 24) : static_cast<uint32_t>(std::floor(static_cast<double>(top_p) * 16777216.0));
+  if (g.top_p24 == 0u) g.top_p24 = 1u;
+  g.seed = seed;
+  g.tokens_out = tokens_out;
+  g.do_accept = accept ? 1 : 0;
+  g.restart = 1;
+  g.lookup_queue = accept ? b->AcceptLookupQueue() : -1;
+  g.lookup_tag = b->fill_seq;
+  Check(pre3::LaunchSample(e->aut, e->vocab, e->cache, b->view, g, s), "sample launch");
+  return GM_OK;
+}
+}  // namespace
+
+int gm_sample_tokens(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, const uint32_t* bitmask,
+                     int64_t ld_words, float temperature, int32_t top_k, float top_p, uint64_t seed,
+                     int32_t* tokens_out, int32_t accept, void* stream) {
+  return Guard([&]() -> int {
+    if (!b || !logits_bf16 || !bitmask) return Fail(GM_ERR_USAGE, "null argument");
+    gm_engine* e = b->engine;
+    if (ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    return SampleCommon(b, logits_bf16, ld, bitmask, ld_words, temperature, top_k, top_p, seed, tokens_out,
+                        accept != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int gm_decode_step_sample(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, uint32_t* bitmask,
+                          int64_t ld_words, float temperature, int32_t top_k, float top_p, uint64_t seed,
+                          int32_t* tokens_out, void* stream) {
+  return Guard([&]() -> int {
+    if (!b || !logits_bf16) return Fail(GM_ERR_USAGE, "null argument");
+    gm_engine* e = b->engine;
+    if (ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t* bm = bitmask ? bitmask : b->scratch_mask;
+    const int64_t ldw = bitmask ? ld_words : e->W;
+    int rc = gm_fill_next_token_bitmask(b, bm, ldw, stream);
+    if (rc != GM_OK) return rc;
+    return SampleCommon(b, logits_bf16, ld, bm, ldw, temperature, top_k, top_p, seed, tokens_out, true, s);
   });
 }
 

@@ -1677,6 +1677,354 @@ __global__ void ResetKernel(AutView A, BatchView Bt) {
 }
 
 // ---------------------------------------------------------------------------
+// SampleKernel: temperature / top-k / top-p sampling over the allowed tokens
+// of each sequence, fused with accept (new work — the
+// reference has no sampler).  One CTA per sequence.  Exact integer semantics
+// (restated in oracle/gmask_port.c gp_sample_pick):
+//   key(t)   16-bit order key of the bf16 logit (monotone in value)
+//   kept_k   allowed tokens with key >= the k-th largest key (ties kept;
+//            k = 0 or k >= |allowed|: all allowed)
+//   W(key)   round(2^32 * 2^(((v - v_max) / T) * log2 e)) with a fixed
+//            sequence of correctly rounded fp32 operations (deterministic
+//            software exp2), v_max = the largest allowed logit
+//   kept_p   kept_k tokens with key >= tau_p, tau_p = the largest key whose
+//            weight above-or-at it reaches ceil(S_K * P24 / 2^24)
+//   token    r = (u32 * S_P) >> 32 for the sequence's next stream draw u;
+//            the token where the cumulative weight in (key desc, id asc)
+//            order first exceeds r; S_P = 0 (all weights underflow): the
+//            lowest-id token with the largest key.
+// Every pass reads only the 16-B logit chunks that hold allowed tokens; the
+// histograms are two-level (high byte, low byte of the key), so 3-5 passes
+// replace a sort.
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ uint32_t SampleKey(uint32_t bits16) {
+  return (bits16 & 0x8000u) ? (~bits16 & 0xFFFFu) : (bits16 | 0x8000u);
+}
+
+__device__ __forceinline__ float KeyValue(uint32_t key) {
+  const uint32_t bits = (key & 0x8000u) ? (key & 0x7FFFu) : (~key & 0xFFFFu);
+  return __uint_as_float(bits << 16);
+}
+
+// Deterministic weight (identical bit-for-bit to the C restatement).
+__device__ unsigned long long SampleWeight(uint32_t key, float vmax, float temperature) {
+  const float v = KeyValue(key);
+  const float d = __fsub_rn(v, vmax);
+  const float x = __fdiv_rn(d, temperature);
+  const float y = __fmul_rn(x, 1.44269502f);
+  if (!(y >= -64.0f)) return 0ull;  // underflow, NaN
+  if (y > 0.0f) return 0ull;        // only v <= vmax
+  const float fl = floorf(y);
+  const int n = static_cast<int>(fl);
+  const float f = __fsub_rn(y, fl);
+  float p = 1.54035304e-4f;
+  p = __fmaf_rn(p, f, 1.33335581e-3f);
+  p = __fmaf_rn(p, f, 9.61812911e-3f);
+  p = __fmaf_rn(p, f, 5.55041087e-2f);
+  p = __fmaf_rn(p, f, 2.40226507e-1f);
+  p = __fmaf_rn(p, f, 6.93147181e-1f);
+  p = __fmaf_rn(p, f, 1.0f);
+  const float scale = __uint_as_float(static_cast<uint32_t>(n + 32 + 127) << 23);  // 2^(n+32), exact
+  return __float2ull_rn(__fmul_rn(p, scale));
+}
+
+struct SampleShared {
+  unsigned int cnt_hi[256];
+  unsigned long long w_hi[256];
+  unsigned int cnt_lo[256];
+  unsigned long long w_lo[256];
+  unsigned int cnt_lo2[256];
+  unsigned long long w_lo2[256];
+  unsigned int red[kThreads / 32 + 1];
+  unsigned long long red64[kThreads / 32];
+  int found;
+};
+
+enum : int { kPassHi = 0, kPassWeights = 1, kPassLoBin = 2 };
+
+// One pass over the allowed tokens of row b (chunks of 8 tokens whose mask
+// byte is non-zero).  fn(t, key) per allowed token.
+template <typename Fn>
+__device__ __forceinline__ void ForAllowed(const uint32_t* mrow, const uint16_t* row, int V1, bool vec_ok, int c_begin,
+                                           int c_end, int c_step, Fn&& fn) {
+  for (int c = c_begin; c < c_end; c += c_step) {
+    const uint32_t byte = (__ldg(mrow + (c >> 2)) >> ((c & 3) * 8)) & 0xffu;
+    if (!byte) continue;
+    const int tb = c * 8;
+    if (vec_ok && tb + 8 <= V1) {
+      const uint4 q = __ldcg(reinterpret_cast<const uint4*>(row + tb));
+      const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if ((byte >> j) & 1u) fn(tb + j, SampleKey((w4[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu));
+      }
+    } else {
+      for (int j = 0; j < 8 && tb + j < V1; ++j) {
+        if ((byte >> j) & 1u) fn(tb + j, SampleKey(row[tb + j]));
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long MulHi32(unsigned long long a, uint32_t u) {
+  // (a * u) >> 32 for a < 2^63
+  return __umul64hi(a, static_cast<unsigned long long>(u) << 32);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+                                                         SampleArgs S) {
+  __shared__ SampleShared sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x;
+  const int V1 = Vv.V + 1;
+  const int nchunks = (V1 + 7) >> 3;
+  const uint32_t* mrow = S.bitmask + static_cast<long long>(b) * S.ldw;
+  const uint16_t* row = S.logits + static_cast<long long>(b) * S.ld;
+  for (int i = tid; i < 256; i += kThreads) {
+    sh.cnt_hi[i] = 0u;
+    sh.w_hi[i] = 0ull;
+    sh.cnt_lo[i] = 0u;
+    sh.w_lo[i] = 0ull;
+    sh.cnt_lo2[i] = 0u;
+    sh.w_lo2[i] = 0ull;
+  }
+  __syncthreads();
+  // ---- pass 1: high-byte counts, max key, |allowed|.
+  unsigned int kmax = 0u, n_allowed = 0u;
+  ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+    atomicAdd(&sh.cnt_hi[key >> 8], 1u);
+    kmax = key > kmax ? key : kmax;
+    ++n_allowed;
+  });
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  n_allowed = __reduce_add_sync(0xffffffffu, n_allowed);
+  if (lane == 0) sh.red[warp] = kmax;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned int m = 0u;
+    for (int i = 0; i < kThreads / 32; ++i) m = sh.red[i] > m ? sh.red[i] : m;
+    sh.red[0] = m;
+  }
+  __syncthreads();
+  kmax = sh.red[0];
+  __syncthreads();
+  if (lane == 0) sh.red[warp] = n_allowed;
+  __syncthreads();
+  unsigned int total_allowed = 0u;
+  for (int i = 0; i < kThreads / 32; ++i) total_allowed += sh.red[i];
+  __syncthreads();
+
+  SeqState st = Bt.seq[b];
+  int tok = -1;
+  // Per-thread uniform decisions below are computed by every thread from
+  // shared histograms (identical results, no broadcast needed).
+  if (total_allowed > 0u) {
+    const float vmax = KeyValue(kmax);
+    const unsigned int k = static_cast<unsigned int>(S.top_k);
+    int hi_k = -1;       // bin holding the top-k threshold (-1: everything kept)
+    unsigned int need_k = 0u;
+    if (k > 0u && k < total_allowed) {
+      unsigned int cum = 0u;
+      for (int h = 255; h >= 0; --h) {
+        if (cum + sh.cnt_hi[h] >= k) {
+          hi_k = h;
+          need_k = k - cum;
+          break;
+        }
+        cum += sh.cnt_hi[h];
+      }
+    }
+    // ---- pass 2: weights per high bin above hi_k; counts + weights per low
+    // byte inside hi_k.
+    ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+      const int h = static_cast<int>(key >> 8);
+      if (h > hi_k) {
+        atomicAdd(&sh.w_hi[h], SampleWeight(key, vmax, S.temperature));
+      } else if (h == hi_k) {
+        atomicAdd(&sh.cnt_lo[key & 0xffu], 1u);
+        atomicAdd(&sh.w_lo[key & 0xffu], SampleWeight(key, vmax, S.temperature));
+      }
+    });
+    __syncthreads();
+    int lo_k = 0;
+    if (hi_k >= 0) {
+      unsigned int cum = 0u;
+      for (int l = 255; l >= 0; --l) {
+        cum += sh.cnt_lo[l];
+        if (cum >= need_k) {
+          lo_k = l;
+          break;
+        }
+      }
+    }
+    unsigned long long s_k = 0ull;
+    for (int h = 255; h > hi_k; --h) s_k += sh.w_hi[h];
+    if (hi_k >= 0) {
+      for (int l = 255; l >= lo_k; --l) s_k += sh.w_lo[l];
+    }
+    // Threshold tau_p as (bin, low byte); lo_p < 0 = resolve with pass 3.
+    int hi_p = hi_k, lo_p = lo_k;
+    unsigned long long s_p = s_k;
+    if (s_k > 0ull && S.top_p24 < (1u << 24)) {
+      const unsigned long long target =
+          (__umul64hi(s_k, static_cast<unsigned long long>(S.top_p24) << 40) + (((s_k * S.top_p24) & 0xFFFFFFull) ? 1ull : 0ull));
+      // target = ceil(s_k * P24 / 2^24): high part via umul64hi of the product shifted by 40 (2^64 / 2^24)
+      unsigned long long cum = 0ull;
+      bool done = false;
+      for (int h = 255; h > hi_k && !done; --h) {
+        if (cum + sh.w_hi[h] >= target) {
+          hi_p = h;
+          lo_p = -1;
+          s_p = cum;  // plus the bin's part, after pass 3
+          done = true;
+        } else {
+          cum += sh.w_hi[h];
+        }
+      }
+      if (!done && hi_k >= 0) {
+        for (int l = 255; l >= lo_k; --l) {
+          cum += sh.w_lo[l];
+          if (cum >= target) {
+            lo_p = l;
+            s_p = cum;
+            done = true;
+            break;
+          }
+        }
+      }
+      if (lo_p < 0) {
+        // ---- pass 3: low-byte weights inside bin hi_p (fully kept_k).
+        const int hp = hi_p;
+        ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+          if (static_cast<int>(key >> 8) == hp) {
+            atomicAdd(&sh.cnt_lo2[key & 0xffu], 1u);
+            atomicAdd(&sh.w_lo2[key & 0xffu], SampleWeight(key, vmax, S.temperature));
+          }
+        });
+        __syncthreads();
+        unsigned long long c2 = cum;
+        for (int l = 255; l >= 0; --l) {
+          c2 += sh.w_lo2[l];
+          if (c2 >= target) {
+            lo_p = l;
+            s_p = c2;
+            break;
+          }
+        }
+      }
+    }
+    // ---- the drawn key: (bin, low byte) and the index within its ties.
+    uint32_t kappa = kmax;
+    unsigned long long jth = 0ull;
+    if (s_p > 0ull) {
+      const unsigned long long u =
+          Mix64(Mix64(S.seed ^ (static_cast<unsigned long long>(b) * 0xD1B54A32D192ED03ull)) ^
+                static_cast<unsigned long long>(st.draws));
+      const unsigned long long r = MulHi32(s_p, static_cast<uint32_t>(u));
+      // Walk kept_p in key-descending order: bins above the threshold bin
+      // are whole; the threshold bin counts low bytes >= lo_p.
+      const int hb = hi_p;  // threshold bin (hi_p == hi_k when top-p is off)
+      unsigned long long cum = 0ull;
+      int h_sel = -1;
+      for (int h = 255; h > hb; --h) {
+        const unsigned long long w = (hb == hi_k || h > hi_k) ? sh.w_hi[h] : 0ull;
+        if (r < cum + w) {
+          h_sel = h;
+          break;
+        }
+        cum += w;
+      }
+      const unsigned int* cl;
+      const unsigned long long* wl;
+      int lmin = 0;
+      if (h_sel < 0) {
+        h_sel = hb;
+        lmin = lo_p;
+        if (hb == hi_k && hi_k >= 0) {
+          cl = sh.cnt_lo;
+          wl = sh.w_lo;
+        } else {
+          cl = sh.cnt_lo2;
+          wl = sh.w_lo2;
+        }
+      } else {
+        // ---- pass 4: low-byte histogram of the selected whole bin.
+        __syncthreads();
+        for (int i = tid; i < 256; i += kThreads) {
+          sh.cnt_lo2[i] = 0u;
+          sh.w_lo2[i] = 0ull;
+        }
+        __syncthreads();
+        const int hs = h_sel;
+        ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+          if (static_cast<int>(key >> 8) == hs) {
+            atomicAdd(&sh.cnt_lo2[key & 0xffu], 1u);
+            atomicAdd(&sh.w_lo2[key & 0xffu], SampleWeight(key, vmax, S.temperature));
+          }
+        });
+        __syncthreads();
+        cl = sh.cnt_lo2;
+        wl = sh.w_lo2;
+      }
+      for (int l = 255; l >= lmin; --l) {
+        if (r < cum + wl[l]) {
+          kappa = (static_cast<uint32_t>(h_sel) << 8) | static_cast<uint32_t>(l);
+          jth = (r - cum) / SampleWeight(kappa, vmax, S.temperature);
+          break;
+        }
+        cum += wl[l];
+      }
+      (void)cl;
+    }
+    // ---- pass 5: the jth token (id order) with key kappa: contiguous chunk
+    // ranges per thread, counts scanned across the CTA.
+    const int per = (nchunks + kThreads - 1) / kThreads;
+    const int c0 = tid * per, c1 = min(nchunks, c0 + per);
+    unsigned int mine = 0u;
+    ForAllowed(mrow, row, V1, S.vec_ok, c0, c1, 1, [&](int, uint32_t key) { mine += key == kappa; });
+    int total = 0;
+    const int excl = BlockExclusiveScan(static_cast<int>(mine), reinterpret_cast<int*>(sh.red), &total);
+    if (tid == 0) sh.found = -1;
+    __syncthreads();
+    if (jth >= static_cast<unsigned long long>(excl) && jth < static_cast<unsigned long long>(excl) + mine) {
+      unsigned int want = static_cast<unsigned int>(jth) - static_cast<unsigned int>(excl);
+      int hit = -1;
+      ForAllowed(mrow, row, V1, S.vec_ok, c0, c1, 1, [&](int t, uint32_t key) {
+        if (key == kappa) {
+          if (want == 0u && hit < 0) hit = t;
+          --want;
+        }
+      });
+      sh.found = hit;
+    }
+    __syncthreads();
+    tok = sh.found;
+  }
+  // ---- accept (warp 0): Step per byte, restart, next context lookup.
+  if (warp == 0) {
+    st.draws += 1;
+    if (S.tokens_out != nullptr && lane == 0) S.tokens_out[b] = tok;
+    if (S.do_accept) {
+      AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, S.restart, S.lookup_queue, S.lookup_tag, lane);
+    } else if (lane == 0) {
+      Bt.seq[b].draws = st.draws;
+    }
+  }
+}
+
+cudaError_t LaunchSample(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
+                         SampleArgs s, cudaStream_t st) {
+  if (b.B == 0) return cudaSuccess;
+  s.vec_ok = (s.ld % 8) == 0 && (reinterpret_cast<uintptr_t>(s.logits) % 16) == 0;
+  SampleKernel<<<b.B, kThreads, 0, st>>>(a, v, c, b, s);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
   ResetKernel<<<(b.B + 127) / 128, 128, 0, s>>>(a, b);

@@ -146,6 +146,26 @@ struct AcceptArgs {
   int lookup_tag;    // number of the fill that consumes it
 };
 
+struct SampleArgs {
+  const uint32_t* bitmask;   // [B][ldw], from a preceding fill
+  long long ldw;
+  const uint16_t* logits;    // bf16 [B][ld]
+  long long ld;
+  float temperature;         // > 0
+  int top_k;                 // 0 = off
+  uint32_t top_p24;          // floor(top_p * 2^24); 2^24 = off
+  unsigned long long seed;
+  int32_t* tokens_out;
+  int do_accept;
+  int restart;
+  int lookup_queue;
+  int lookup_tag;
+  int vec_ok;                // set by LaunchSample
+};
+
+// Temperature / top-k / top-p sampling over the allowed tokens (+ accept).
+cudaError_t LaunchSample(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
+                         SampleArgs s, cudaStream_t st);
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s);
 cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s);
 cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,

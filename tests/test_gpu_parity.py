@@ -350,3 +350,44 @@ def test_tokenizer_json_vocabulary_on_device():
         d = pstacks[b, 0]
         got = batch.get(b)
         assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1]
+
+
+@pytest.mark.parametrize("T,k,p,ties", [(1.0, 0, 1.0, False), (0.7, 50, 1.0, False), (1.3, 0, 0.9, False),
+                                        (0.5, 20, 0.8, False), (2.0, 3, 0.5, True), (1.0, 0, 0.95, True),
+                                        (0.05, 0, 1.0, False), (1.0, 1, 1.0, True)])
+def test_sample_decode_step_matches_port(T, k, p, ties):
+    """gm_decode_step_sample (fill + temperature/top-k/top-p sampler + accept,
+    one host call, no round trip) == the C port's rule step by step: masks,
+    sampled tokens, stacks.  `ties` quantizes the logits to few values so the
+    tie rules (thresholds keep ties, draws walk ties in id order) are hit."""
+    vocab = pk.synth_vocab(128255)
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=12)
+    port = Port(f, vocab)
+    B, steps, seed = 12, 10, 77
+    batch = eng.batch(B)
+    bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
+    toks = torch.zeros(B, dtype=torch.int32, device=DEV)
+    cfgs = [port.initial() for _ in range(B)]
+    g = torch.Generator(device=DEV).manual_seed(5)
+    for s in range(steps):
+        lg = torch.randn((B, eng.V + 1), dtype=torch.float32, device=DEV, generator=g)
+        if ties:
+            lg = torch.round(lg * 2) / 2
+        lg = lg.to(torch.bfloat16)
+        batch.decode_step_sample(lg, temperature=T, top_k=k, top_p=p, seed=seed, tokens_out=toks, bitmask=bm)
+        batch.check()
+        got = bm.cpu().numpy().view(np.uint32)
+        rows = lg.view(torch.int16).cpu().numpy().view(np.uint16)
+        tk = toks.cpu().numpy()
+        for b in range(B):
+            want = port.mask(cfgs[b])
+            assert np.array_equal(got[b], want), (b, s)
+            tok = port.sample_pick(want, rows[b], T, k, p, Port.stream_draw(seed, b, s))
+            assert tok == tk[b], (b, s, tok, tk[b])
+            if tok >= 0:
+                port.accept_token(cfgs[b], tok)
+            if tok < 0 or cfgs[b].status != 0:
+                port.free(cfgs[b])
+                cfgs[b] = port.initial()
+            assert batch.get(b).stack == port.get(cfgs[b])[2], (b, s)
