@@ -85,6 +85,8 @@ def parse(argv=None):
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    p.add_argument("--no-north-star", action="store_true",
+                   help="skip the extra batch-1024 fill-kernel roofline measurement of the default config")
     a = p.parse_args(argv)
     cfg = CONFIGS[a.config]
     a.mode = cfg["mode"]
@@ -369,6 +371,42 @@ def main(argv=None):
     elapsed_ms, kern_ms = max_over_ranks([elapsed_ms, kern_ms], dev, world)
     value = aggregate_rate(world, B * K, elapsed_ms / 1e3)
 
+    # North-star check (BASELINE.json: >= 60 % of HBM bandwidth at batch >= 1024):
+    # the same grammar and step at 1,024 sequences, fill kernel timed alone
+    # (outside the headline timed region; its own warm-up and rotation).
+    north = None
+    if (world == 1 and not args.no_north_star and not greedy and B < 1024 and args.config == 2):
+        Bn = 1024
+        bn = eng.batch(Bn, args.stack_cap)
+        bmn = torch.zeros((Bn, W), dtype=torch.int32, device=dev)
+        cn = torch.zeros((Bn, bn.nseg * 2), dtype=torch.int32, device=dev)
+        tn = torch.zeros(Bn, dtype=torch.int32, device=dev)
+        Rn = max(2, -(-3 * L2_BYTES // (Bn * V1 * 2)))
+        lgn = [torch.randn((Bn, V1), dtype=torch.bfloat16, device=dev) for _ in range(Rn)]
+        for i in range(30):
+            bn.fill(bmn, lgn[i % Rn], cn)
+            bn.sample_stream_and_accept(bmn, cn, seed, tn)
+        torch.cuda.synchronize()
+        Kn = 100
+        evn = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(Kn)]
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for i in range(Kn):
+            evn[i][0].record(stream)
+            bn.fill(bmn, lgn[i % Rn], cn)
+            evn[i][1].record(stream)
+            bn.sample_stream_and_accept(bmn, cn, seed, tn)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        bn.check()
+        fill_ms_n = sum(a.elapsed_time(c) for a, c in evn) / Kn
+        pk_gbs, _, _ = peaks()
+        ach_n = Bn * (2 * V1 + 8 * W) / (fill_ms_n / 1e3) / 1e9
+        north = {"batch": Bn, "step": "gm_fill_and_mask_logits + gm_sample_stream_and_accept",
+                 "fill_kernel_us": 1e3 * fill_ms_n, "achieved_gbs": ach_n, "frac": ach_n / pk_gbs,
+                 "seq_steps_per_s": Bn * Kn / (f0.elapsed_time(f1) / 1e3), "steps": Kn}
+        del bn, lgn
+
     # Device-counted logit bytes of one more step (outside the timed region).
     batch.set_stats(True)
     step(K)
@@ -477,6 +515,7 @@ def main(argv=None):
                   "private_builds": info["private_builds"], "parent_builds": info["parent_builds"],
                   "last_fill": fstats},
         "max_stack_depth_seen": max_depth,
+        "north_star_batch1024": north,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
