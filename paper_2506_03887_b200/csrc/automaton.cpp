@@ -160,6 +160,70 @@ void Automaton::Validate() const {
   }
 }
 
+namespace {
+
+// Open-addressing insert (linear probing); key 0 = empty.  `pairs`: entries
+// are {key, value} pairs.
+void HashInsert(std::vector<uint64_t>* tab, size_t slots, bool pairs, uint64_t key, uint64_t value) {
+  const size_t stride = pairs ? 2 : 1;
+  for (size_t i = key & (slots - 1);; i = (i + 1) & (slots - 1)) {
+    uint64_t& k = (*tab)[i * stride];
+    if (k == key) return;  // first inserted wins (arbitration order)
+    if (k == 0) {
+      k = key;
+      if (pairs) (*tab)[i * stride + 1] = value;
+      return;
+    }
+  }
+}
+
+size_t Pow2Slots(size_t n) {
+  size_t s = 16;
+  while (s < 2 * n) s <<= 1;
+  return s;
+}
+
+void BuildConditionIndex(const Automaton& a, FlatLayout* f) {
+  const int32_t S = a.num_states;
+  f->hidx_meta.assign(static_cast<size_t>(S) * 257 * 2, 0);
+  std::vector<std::pair<uint64_t, uint64_t>> exact;
+  std::vector<uint64_t> prefix;
+  for (int32_t s = 0; s < S; ++s) {
+    for (int32_t t = 0; t < 257; ++t) {
+      const size_t idx = static_cast<size_t>(s) * 257 + static_cast<size_t>(t);
+      const int32_t cb = f->rec_begin[idx], ce = f->rec_begin[idx + 1];
+      if (ce - cb <= kHashMin) continue;
+      std::vector<int16_t> lens;
+      for (int32_t c = cb; c < ce; ++c) {
+        const CandRec& r = f->recs[static_cast<size_t>(c)];
+        (void)r;
+        const Edge& e = a.edges[static_cast<size_t>(f->rec_edge[static_cast<size_t>(c)])];
+        const int L = static_cast<int>(e.match_pop.size());
+        if (lens.empty() || lens.back() != L) lens.push_back(static_cast<int16_t>(L));  // descending (arbitration)
+        uint64_t h = CondSeed(s, t);
+        for (int j = 1; j <= L; ++j) {
+          h = CondMix(h ^ static_cast<uint32_t>(e.match_pop[static_cast<size_t>(j - 1)]));
+          if (j < L) prefix.push_back(CondKey(h, kSaltPrefix, j));  // a shorter known stack matches this prefix
+        }
+        exact.emplace_back(CondKey(h, kSaltExact, L), static_cast<uint64_t>(c));
+      }
+      f->hidx_meta[idx * 2] = static_cast<int32_t>(f->hidx_lens.size());
+      f->hidx_meta[idx * 2 + 1] = static_cast<int32_t>(lens.size()) | (static_cast<int32_t>(lens.front()) << 16);
+      f->hidx_lens.insert(f->hidx_lens.end(), lens.begin(), lens.end());
+    }
+  }
+  std::sort(prefix.begin(), prefix.end());
+  prefix.erase(std::unique(prefix.begin(), prefix.end()), prefix.end());
+  const size_t es = Pow2Slots(exact.size()), ps = Pow2Slots(prefix.size());
+  f->hidx_exact.assign(es * 2, 0);
+  f->hidx_prefix.assign(ps, 0);
+  for (const auto& kv : exact) HashInsert(&f->hidx_exact, es, true, kv.first, kv.second);
+  for (uint64_t k : prefix) HashInsert(&f->hidx_prefix, ps, false, k, 0);
+  if (f->hidx_lens.empty()) f->hidx_lens.push_back(0);
+}
+
+}  // namespace
+
 FlatLayout Flatten(const Automaton& a) {
   FlatLayout f;
   const int32_t S = a.num_states;
@@ -214,6 +278,7 @@ FlatLayout Flatten(const Automaton& a) {
         f.max_cond = std::max<int32_t>(f.max_cond, r.cond_len);
         f.max_push = std::max<int32_t>(f.max_push, r.push_len + (r.new_state < 0 ? 1 : 0));
         f.recs.push_back(r);
+        f.rec_edge.push_back(i);
         f.state_any[static_cast<size_t>(s) * 9 + static_cast<size_t>(t >> 5)] |= 1u << (t & 31);
       }
     }
@@ -223,6 +288,7 @@ FlatLayout Flatten(const Automaton& a) {
   for (size_t i = 0; i + 1 < f.rec_begin.size(); ++i) {
     if (f.rec_begin[i] < f.rec_begin[i + 1]) f.first[i] = f.recs[static_cast<size_t>(f.rec_begin[i])];
   }
+  BuildConditionIndex(a, &f);
   if (f.recs.empty()) f.recs.push_back(CandRec{});
   // Tail padding: vector reads of the last list stay in bounds.
   f.rec_cond.insert(f.rec_cond.end(), 16, -1);

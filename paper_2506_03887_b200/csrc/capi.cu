@@ -297,6 +297,12 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     e->aut.rec_begin = DevUpload(f.rec_begin, &e->owned);
     e->aut.recs = DevUpload(f.recs, &e->owned);
     e->aut.first = DevUpload(f.first, &e->owned);
+    e->aut.hidx_meta = reinterpret_cast<const int2*>(DevUpload(f.hidx_meta, &e->owned));
+    e->aut.hidx_lens = DevUpload(f.hidx_lens, &e->owned);
+    e->aut.hidx_exact = reinterpret_cast<const unsigned long long*>(DevUpload(f.hidx_exact, &e->owned));
+    e->aut.hidx_prefix = reinterpret_cast<const unsigned long long*>(DevUpload(f.hidx_prefix, &e->owned));
+    e->aut.hidx_exact_mask = f.hidx_exact.size() / 2 - 1;
+    e->aut.hidx_prefix_mask = f.hidx_prefix.size() - 1;
     e->aut.rec_cond = DevUpload(f.rec_cond, &e->owned);
     e->aut.rec_push = DevUpload(f.rec_push, &e->owned);
     e->aut.shift = DevUpload(a->a.shift_targets, &e->owned);

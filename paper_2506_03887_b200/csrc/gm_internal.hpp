@@ -110,6 +110,7 @@ static_assert(sizeof(CandRec) == 96, "CandRec layout");
 struct FlatLayout {
   std::vector<int32_t> rec_begin;  // S*257 + 1
   std::vector<CandRec> recs;
+  std::vector<int32_t> rec_edge;   // host only: the edge of each record
   std::vector<int32_t> rec_cond;
   std::vector<int32_t> rec_push;
   std::vector<uint32_t> state_any;  // S*9: bytes with any candidate (8 words) + bit0 of word 8 = '$'
@@ -117,8 +118,49 @@ struct FlatLayout {
   // the candidate that wins ~2/3 of steps arrives in the same round trip as
   // the candidate range, so most byte steps cost one L2 round trip.
   std::vector<CandRec> first;
+  // Condition index (FindEdge in O(distinct condition lengths)): for a
+  // (state, terminal) with more than kHashMin candidates, the winner is the
+  // candidate whose whole condition equals the stack top for the LONGEST
+  // such length (arbitration: longer conditions first, dpda_builder.cpp:
+  // 327-338; equal conditions keep the lower origin rank, listed first), so
+  // a probe per distinct length replaces a serial scan (SQL: up to 864
+  // candidates, 20 lengths).  hidx_meta[s*257+t] = {lens offset, count | max
+  // length << 16}; lens descending in hidx_lens; hidx_exact maps
+  // CondHash(s, t, L, condition) -> candidate; hidx_prefix holds
+  // CondHash'(s, t, D, first D entries) of every longer condition (a walk
+  // against a key that ends D entries down is undecidable when one matches).
+  std::vector<int32_t> hidx_meta;   // S*257*2
+  std::vector<int16_t> hidx_lens;
+  std::vector<uint64_t> hidx_exact;  // pairs {key, candidate}, power-of-two slots
+  std::vector<uint64_t> hidx_prefix; // keys, power-of-two slots
   int32_t max_cond = 0, max_push = 0;
 };
+
+constexpr int kHashMin = 6;  // candidates above which a (state, terminal) is indexed
+
+#ifdef __CUDACC__
+#define GM_HD __host__ __device__ __forceinline__
+#else
+#define GM_HD inline
+#endif
+
+// Hash of a condition prefix (shared by host and device; identical bits).
+GM_HD uint64_t CondMix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+// Running hash r_0 = CondSeed(s, t); r_j = CondMix(r_{j-1} ^ entry_{j-1}) over
+// the stack top (entry 0 = the state); keys finish r_L with a salt and L.
+GM_HD uint64_t CondSeed(int32_t s, int32_t t) {
+  return CondMix(0x3c6ef372fe94f82bull ^ (static_cast<uint64_t>(static_cast<uint32_t>(s)) << 24) ^
+                 static_cast<uint64_t>(static_cast<uint32_t>(t)));
+}
+constexpr uint64_t kSaltExact = 0x6a09e667f3bcc909ull, kSaltPrefix = 0xbb67ae8584caa73bull;
+GM_HD uint64_t CondKey(uint64_t running, uint64_t salt, int32_t len) {
+  return CondMix(running ^ salt ^ static_cast<uint64_t>(len)) | 1ull;
+}
 
 FlatLayout Flatten(const Automaton& a);
 

@@ -123,10 +123,60 @@ __device__ __forceinline__ void TraceEvent(const BatchView& Bt, int kind, int b,
 // paths: the fill kernel is i-cache bound otherwise); the automaton and
 // vocabulary arrays are passed as scalars so no parameter struct is copied to
 // local memory.
+// Indexed FindEdge for a (state, terminal) with many candidates (the
+// FlatLayout::hidx_* tables): the winner is the candidate whose condition
+// equals the stack top for the longest such length; with an incomplete stack
+// of D known entries, a longer condition whose first D entries match makes
+// the outcome unknown (it comes first in arbitration order).  Returns the
+// candidate index, -1 (no edge), -2 (unknown) or -3 (hash collision: scan).
+// Entry j of the virtual stack: j < nl ? loc[nl-1-j] : base[nb-1-(j-nl)].
+__device__ __forceinline__ int IndexedFindEdge(const int2* hmeta, const int16_t* hlens,
+                                               const unsigned long long* hexact, unsigned long long emask,
+                                               const unsigned long long* hprefix, unsigned long long pmask,
+                                               int2 meta, int state, int x, const int32_t* loc, int nl,
+                                               const int32_t* base, int nb, bool complete) {
+  (void)hmeta;
+  const int nlen = meta.y & 0xffff;
+  const int maxl = meta.y >> 16;
+  const int D = nl + nb;
+  const int H = min(maxl, D);
+  unsigned long long r = CondSeed(state, x);
+  int li = nlen - 1;  // lens are descending: walk from the shortest
+  int best = -1;
+  for (int j = 1; j <= H; ++j) {
+    const int e = j - 1 < nl ? loc[nl - j] : base[nb - 1 - (j - 1 - nl)];
+    r = CondMix(r ^ static_cast<uint32_t>(e));
+    while (li >= 0 && __ldg(hlens + meta.x + li) < j) --li;
+    if (li >= 0 && __ldg(hlens + meta.x + li) == j) {
+      const unsigned long long key = CondKey(r, kSaltExact, j);
+      for (unsigned long long i = key & emask;; i = (i + 1) & emask) {
+        const unsigned long long k = __ldg(hexact + 2 * i);
+        if (k == key) {
+          best = static_cast<int>(__ldg(hexact + 2 * i + 1));  // longer hits overwrite shorter ones
+          break;
+        }
+        if (k == 0ull) break;
+      }
+    }
+  }
+  if (!complete && maxl > D) {
+    const unsigned long long key = CondKey(r, kSaltPrefix, D);
+    for (unsigned long long i = key & pmask;; i = (i + 1) & pmask) {
+      const unsigned long long k = __ldg(hprefix + i);
+      if (k == key) return -2;
+      if (k == 0ull) break;
+    }
+  }
+  return best;
+}
+
 __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* rec_begin, const CandRec* recs,
                                           const int32_t* rec_cond, const int32_t* rec_push, const int32_t* shift,
                                           const int32_t* tok_off, const uint8_t* tok_bytes, int32_t V, int32_t t,
-                                          const int32_t* base, int nb, bool complete) {
+                                          const int32_t* base, int nb, bool complete, const int2* hmeta,
+                                          const int16_t* hlens, const unsigned long long* hexact,
+                                          unsigned long long emask, const unsigned long long* hprefix,
+                                          unsigned long long pmask) {
   const struct {
     const CandRec* first;
     const int32_t* rec_begin;
@@ -156,10 +206,33 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
     const int idx = state * 257 + x;
     const int cb = __ldg(A.rec_begin + idx);
     const int ce = __ldg(A.rec_begin + idx + 1);
-    Rec r = LoadRec(A.first + idx);
+    const int2 meta = __ldg(hmeta + idx);
     int found = -1;
     Rec fr;
-    for (int c = cb; c < ce; ++c) {
+    int c_scan = cb;  // first candidate of the linear scan (ce: none)
+    if (meta.y != 0) {
+      const int c = IndexedFindEdge(hmeta, hlens, hexact, emask, hprefix, pmask, meta, state, x, loc, nl, base, nb,
+                                    complete);
+      if (c == -2) return kUnknown;
+      c_scan = ce;
+      if (c >= 0) {
+        // Verify the hit exactly (a 64-bit key collision falls back to the scan).
+        const Rec h = LoadRec(A.recs + c);
+        bool same = h.cond_len <= nl + nb;
+        for (int j = 1; j < h.cond_len && same; ++j) {
+          const int have = j < nl ? loc[nl - 1 - j] : base[nb - 1 - (j - nl)];
+          same = have == CondEntry(h, A.rec_cond, j);
+        }
+        if (same) {
+          found = c;
+          fr = h;
+        } else {
+          c_scan = cb;
+        }
+      }
+    }
+    Rec r = LoadRec(A.first + idx);
+    for (int c = c_scan; c < ce; ++c) {
       if (c > cb) r = LoadRec(A.recs + c);
       // ConditionMatches (runtime.cpp:123-131) for entries 1..k-1 (entry 0 is
       // the current state) against the overlay, then the known base.
@@ -212,7 +285,8 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
 __device__ __forceinline__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
                                          bool complete) {
   return WalkTokenImpl(A.first, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_off, Vv.tok_bytes,
-                       Vv.V, t, base, nb, complete);
+                       Vv.V, t, base, nb, complete, A.hidx_meta, A.hidx_lens, A.hidx_exact, A.hidx_exact_mask,
+                       A.hidx_prefix, A.hidx_prefix_mask);
 }
 
 // The same walk done by one warp for one token (complete stacks only): lanes
@@ -1938,19 +2012,12 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
         }
         cum += w;
       }
-      const unsigned int* cl;
       const unsigned long long* wl;
       int lmin = 0;
       if (h_sel < 0) {
         h_sel = hb;
         lmin = lo_p;
-        if (hb == hi_k && hi_k >= 0) {
-          cl = sh.cnt_lo;
-          wl = sh.w_lo;
-        } else {
-          cl = sh.cnt_lo2;
-          wl = sh.w_lo2;
-        }
+        wl = (hb == hi_k && hi_k >= 0) ? sh.w_lo : sh.w_lo2;
       } else {
         // ---- pass 4: low-byte histogram of the selected whole bin.
         __syncthreads();
@@ -1967,7 +2034,6 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
           }
         });
         __syncthreads();
-        cl = sh.cnt_lo2;
         wl = sh.w_lo2;
       }
       for (int l = 255; l >= lmin; --l) {
@@ -1978,7 +2044,6 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
         }
         cum += wl[l];
       }
-      (void)cl;
     }
     // ---- pass 5: the jth token (id order) with key kappa: contiguous chunk
     // ranges per thread, counts scanned across the CTA.

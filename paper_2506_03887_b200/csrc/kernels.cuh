@@ -30,6 +30,14 @@ struct AutView {
   const int32_t* rec_begin;  // S*257+1
   const CandRec* recs;
   const CandRec* first;      // S*257 dense first candidates
+  // Condition index (FlatLayout::hidx_*): {lens offset, count | max len << 16}
+  // per (state, terminal) (count 0 = scan), lengths, exact and prefix tables.
+  const int2* hidx_meta;
+  const int16_t* hidx_lens;
+  const unsigned long long* hidx_exact;   // {key, candidate} pairs
+  const unsigned long long* hidx_prefix;  // keys
+  unsigned long long hidx_exact_mask;     // slots - 1
+  unsigned long long hidx_prefix_mask;
   const int32_t* rec_cond;   // 16-B aligned lists
   const int32_t* rec_push;   // 16-B aligned lists
   const int32_t* shift;       // S*256
