@@ -19,6 +19,7 @@
 //
 // Integer/bit work only: no tensor cores (nothing here is a contraction).
 #include <cuda/atomic>
+#include <utility>
 
 #include "kernels.cuh"
 
@@ -88,6 +89,15 @@ __device__ __forceinline__ BuildQueue QueueOf(const BatchView& Bt, int q) {
   return q == 0 ? Bt.queue[0] : (q == 1 ? Bt.queue[1] : Bt.queue[2]);
 }
 
+
+// Programmatic dependent launch: every kernel of a step waits here for the
+// previous kernel on the stream to finish (its memory visible), then lets the
+// next one be scheduled — so a kernel's launch and CTA ramp-up overlap the
+// tail of its predecessor instead of following it.
+__device__ __forceinline__ void PdlEnter() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
 
 __device__ __forceinline__ unsigned long long NowNs() {
   unsigned long long t;
@@ -1068,6 +1078,7 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, int q, int tag) {
+  PdlEnter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= Bt.B) return;
   const SeqState st = Bt.seq[b];
@@ -1082,6 +1093,7 @@ __global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, 
 // Builds everything queued in q, then empties q (used when a batch goes away
 // or before a standalone fill should not pay for builds).
 __global__ void __launch_bounds__(kThreads) DrainKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt, int q) {
+  PdlEnter();
   extern __shared__ int32_t base_s[];
   __shared__ int unit;
   HelpBuild(A, Vv, Cc, Bt, q, base_s, &unit);
@@ -1504,6 +1516,7 @@ struct FillShared {
 template <int MODE, int TAIL>
 __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                           FillArgs F) {
+  PdlEnter();
   __shared__ FillShared sh;
   __shared__ uint4 span_buf[kWarps][2][4][32];  // light pass: per-warp double buffer of mixed chunks (32 KB)
   extern __shared__ int32_t stack_s[];
@@ -1710,6 +1723,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
 template <int SAMPLE>
 __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                     AcceptArgs G) {
+  PdlEnter();
   const int lane = threadIdx.x & 31;
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= Bt.B) return;
@@ -1739,6 +1753,7 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
 }
 
 __global__ void ResetKernel(AutView A, BatchView Bt) {
+  PdlEnter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= Bt.B) return;
   Bt.stacks[static_cast<long long>(b) * Bt.cap] = A.initial;
@@ -1851,6 +1866,7 @@ __device__ __forceinline__ unsigned long long MulHi32(unsigned long long a, uint
 
 __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                          SampleArgs S) {
+  PdlEnter();
   __shared__ SampleShared sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
@@ -2081,25 +2097,39 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   }
 }
 
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute.
+template <typename... KArgs, typename... Args>
+static cudaError_t Launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 cudaError_t LaunchSample(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
                          SampleArgs s, cudaStream_t st) {
   if (b.B == 0) return cudaSuccess;
   s.vec_ok = (s.ld % 8) == 0 && (reinterpret_cast<uintptr_t>(s.logits) % 16) == 0;
-  SampleKernel<<<b.B, kThreads, 0, st>>>(a, v, c, b, s);
-  return cudaGetLastError();
+  return Launch(SampleKernel, dim3(b.B), dim3(kThreads), 0, st, a, v, c, b, s);
 }
 
 // ---------------------------------------------------------------------------
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
-  ResetKernel<<<(b.B + 127) / 128, 128, 0, s>>>(a, b);
-  return cudaGetLastError();
+  return Launch(ResetKernel, dim3((b.B + 127) / 128), dim3(128), 0, s, a, b);
 }
 
 cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
-  LookupKernel<<<(b.B + 127) / 128, 128, 0, s>>>(c, b, queue, tag);
-  return cudaGetLastError();
+  return Launch(LookupKernel, dim3((b.B + 127) / 128), dim3(128), 0, s, c, b, queue, tag);
 }
 
 cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,
@@ -2108,8 +2138,7 @@ cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c
   if (dyn > 48 * 1024) {
     cudaFuncSetAttribute(DrainKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
   }
-  DrainKernel<<<b.build_grid, kThreads, dyn, s>>>(a, v, c, b, queue);
-  return cudaGetLastError();
+  return Launch(DrainKernel, dim3(b.build_grid), dim3(kThreads), dyn, s, a, v, c, b, queue);
 }
 
 template <int MODE, int TAIL>
@@ -2124,7 +2153,7 @@ static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c
   }
   const unsigned items = static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
   const unsigned grid = static_cast<unsigned>(b.h_grid) + (items + kWarps - 1) / kWarps;
-  FillKernel<MODE, TAIL><<<grid, kThreads, dyn, s>>>(a, v, c, b, f);
+  Launch(FillKernel<MODE, TAIL>, dim3(grid), dim3(kThreads), dyn, s, a, v, c, b, f);
 }
 
 cudaError_t LaunchFill(int mode, int tail, const AutView& a, const VocabView& v, const CacheView& c,
@@ -2149,13 +2178,13 @@ cudaError_t LaunchAccept(int sample, const AutView& a, const VocabView& v, const
   const int blocks = (b.B * 32 + threads - 1) / threads;
   switch (sample) {
     case kSampleGiven:
-      AcceptKernel<kSampleGiven><<<blocks, threads, 0, s>>>(a, v, c, b, g);
+      Launch(AcceptKernel<kSampleGiven>, dim3(blocks), dim3(threads), 0, s, a, v, c, b, g);
       break;
     case kSampleStream:
-      AcceptKernel<kSampleStream><<<blocks, threads, 0, s>>>(a, v, c, b, g);
+      Launch(AcceptKernel<kSampleStream>, dim3(blocks), dim3(threads), 0, s, a, v, c, b, g);
       break;
     default:
-      AcceptKernel<kSampleGreedy><<<blocks, threads, 0, s>>>(a, v, c, b, g);
+      Launch(AcceptKernel<kSampleGreedy>, dim3(blocks), dim3(threads), 0, s, a, v, c, b, g);
       break;
   }
   return cudaGetLastError();
