@@ -415,44 +415,65 @@ def main(argv=None):
     batch.set_stats(False)
     max_depth = max(batch.get(b).stack.__len__() for b in range(min(B, 256)))
 
-    # ---- e2e through the public API with host buffers.
+    # ---- e2e through the public API with host buffers.  Every step: H2D of
+    # the host-held token ids, the C-ABI calls, D2H of the step's sampled ids
+    # (waited for: the next step needs them) and of its full bitmask — the
+    # 4 MB bitmask copy runs on a copy stream into double-buffered pinned
+    # memory so it overlaps the next step's kernels; the timed region ends
+    # after the last copy lands.
     e2e = None
     if not args.no_e2e:
-        bm_host = torch.empty((B, W), dtype=torch.int32, pin_memory=True)
+        copy_stream = torch.cuda.Stream(device=dev)
+        bm2 = [bm, torch.zeros_like(bm)]
+        bm_host = [torch.empty((B, W), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        mask_ready = [torch.cuda.Event() for _ in range(2)]
+        copy_done = [torch.cuda.Event() for _ in range(2)]
         picked_host = torch.empty((B,), dtype=torch.int32, pin_memory=True)
         picked_dev = torch.empty(B, dtype=torch.int32, device=dev)
+        tok_host = torch.full((B,), -1, dtype=torch.int32, pin_memory=True)
+        tok_dev = torch.empty(B, dtype=torch.int32, device=dev)
         Ke = max(10, min(K, 200))
-        if greedy:
-            # Logits come from the model on the device; per step the chosen
-            # ids and the bitmask are read back to the host.
-            def e2e_step(i):
-                batch.decode_step_greedy(logits[i % R], tokens_out=picked_dev, bitmask=bm)
-                bm_host.copy_(bm, non_blocking=True)
-                picked_host.copy_(picked_dev, non_blocking=True)
-                stream.synchronize()
-            h2d, path = 0, "gm_decode_step_greedy(device logits) → D2H bitmask+ids"
-        else:
-            tok_host = torch.full((B,), -1, dtype=torch.int32, pin_memory=True)
-            tok_dev = torch.empty(B, dtype=torch.int32, device=dev)
 
+        def ship_mask(i):
+            j = i & 1
+            mask_ready[j].record(stream)
+            copy_stream.wait_event(mask_ready[j])
+            with torch.cuda.stream(copy_stream):
+                bm_host[j].copy_(bm2[j], non_blocking=True)            # D2H: the bitmask (overlapped)
+            copy_done[j].record(copy_stream)
+
+        if greedy:
+            # Logits come from the model on the device; the chosen ids and the
+            # bitmask are read back to the host.
             def e2e_step(i):
-                tok_dev.copy_(tok_host, non_blocking=True)                 # H2D: last step's tokens
-                batch.accept(tok_dev, restart=True)                        # accept_token
-                batch.fill(bm, logits[i % R], counts)                      # fill + -inf logits
-                batch.sample_stream(bm, counts, seed, picked_dev)          # sampler (device)
-                bm_host.copy_(bm, non_blocking=True)                       # D2H: the bitmask
-                picked_host.copy_(picked_dev, non_blocking=True)           # D2H: sampled ids
+                stream.wait_event(copy_done[i & 1])                      # bitmask buffer free again
+                batch.decode_step_greedy(logits[i % R], tokens_out=picked_dev, bitmask=bm2[i & 1])
+                ship_mask(i)
+                picked_host.copy_(picked_dev, non_blocking=True)         # D2H: chosen ids
+                stream.synchronize()
+            h2d, path = 0, "gm_decode_step_greedy(device logits) → D2H ids; D2H bitmask on a copy stream"
+        else:
+            def e2e_step(i):
+                stream.wait_event(copy_done[i & 1])
+                tok_dev.copy_(tok_host, non_blocking=True)               # H2D: last step's tokens
+                batch.accept(tok_dev, restart=True)                      # accept_token
+                batch.fill(bm2[i & 1], logits[i % R], counts)            # fill + -inf logits
+                ship_mask(i)
+                batch.sample_stream(bm2[i & 1], counts, seed, picked_dev)  # sampler (device)
+                picked_host.copy_(picked_dev, non_blocking=True)         # D2H: sampled ids
                 stream.synchronize()
                 tok_host.copy_(picked_host)
             h2d, path = B * 4, ("gm_accept_tokens(H2D ids) → gm_fill_and_mask_logits → gm_sample_stream → "
-                                "D2H bitmask+ids")
+                                "D2H ids; D2H bitmask on a copy stream (double-buffered)")
         for i in range(3):
             e2e_step(i)
+        copy_stream.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for i in range(Ke):
             e2e_step(i)
+        copy_stream.synchronize()
         t_e2e = time.perf_counter() - t0
         batch.check()
         (t_e2e,) = max_over_ranks([t_e2e], dev, world)
