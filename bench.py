@@ -415,70 +415,49 @@ def main(argv=None):
     batch.set_stats(False)
     max_depth = max(batch.get(b).stack.__len__() for b in range(min(B, 256)))
 
-    # ---- e2e through the public API with host buffers.  Every step: H2D of
-    # the host-held token ids, the C-ABI calls, D2H of the step's sampled ids
-    # (waited for: the next step needs them) and of its full bitmask — the
-    # 4 MB bitmask copy runs on a copy stream into double-buffered pinned
-    # memory so it overlaps the next step's kernels; the timed region ends
-    # after the last copy lands.
+    # ---- e2e through the public C ABI with host buffers, driven by a C++
+    # caller (paper_2506_03887_b200/tools/e2e_driver.cpp; Python's per-call
+    # overhead would otherwise dominate).  Every step: H2D of the host-held
+    # token ids, gm_accept_tokens + gm_fill_and_mask_logits + gm_sample_stream
+    # (greedy: gm_decode_step_greedy), D2H of the sampled ids (waited for: the
+    # next step needs them) and of the full bitmask (a copy stream into
+    # double-buffered pinned memory, overlapping the next step); the timed
+    # region ends after the last copy lands.
     e2e = None
     if not args.no_e2e:
-        copy_stream = torch.cuda.Stream(device=dev)
-        bm2 = [bm, torch.zeros_like(bm)]
-        bm_host = [torch.empty((B, W), dtype=torch.int32, pin_memory=True) for _ in range(2)]
-        mask_ready = [torch.cuda.Event() for _ in range(2)]
-        copy_done = [torch.cuda.Event() for _ in range(2)]
-        picked_host = torch.empty((B,), dtype=torch.int32, pin_memory=True)
-        picked_dev = torch.empty(B, dtype=torch.int32, device=dev)
-        tok_host = torch.full((B,), -1, dtype=torch.int32, pin_memory=True)
-        tok_dev = torch.empty(B, dtype=torch.int32, device=dev)
+        import ctypes
+        drv = ctypes.CDLL(os.path.join(ROOT, "paper_2506_03887_b200", "libpre3e2e.so"))
+        drv.e2e_run.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32,
+                                ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
+        drv.e2e_run.restype = ctypes.c_int
         Ke = max(10, min(K, 200))
-
-        def ship_mask(i):
-            j = i & 1
-            mask_ready[j].record(stream)
-            copy_stream.wait_event(mask_ready[j])
-            with torch.cuda.stream(copy_stream):
-                bm_host[j].copy_(bm2[j], non_blocking=True)            # D2H: the bitmask (overlapped)
-            copy_done[j].record(copy_stream)
-
-        if greedy:
-            # Logits come from the model on the device; the chosen ids and the
-            # bitmask are read back to the host.
-            def e2e_step(i):
-                stream.wait_event(copy_done[i & 1])                      # bitmask buffer free again
-                batch.decode_step_greedy(logits[i % R], tokens_out=picked_dev, bitmask=bm2[i & 1])
-                ship_mask(i)
-                picked_host.copy_(picked_dev, non_blocking=True)         # D2H: chosen ids
-                stream.synchronize()
-            h2d, path = 0, "gm_decode_step_greedy(device logits) → D2H ids; D2H bitmask on a copy stream"
-        else:
-            def e2e_step(i):
-                stream.wait_event(copy_done[i & 1])
-                tok_dev.copy_(tok_host, non_blocking=True)               # H2D: last step's tokens
-                batch.accept(tok_dev, restart=True)                      # accept_token
-                batch.fill(bm2[i & 1], logits[i % R], counts)            # fill + -inf logits
-                ship_mask(i)
-                batch.sample_stream(bm2[i & 1], counts, seed, picked_dev)  # sampler (device)
-                picked_host.copy_(picked_dev, non_blocking=True)         # D2H: sampled ids
-                stream.synchronize()
-                tok_host.copy_(picked_host)
-            h2d, path = B * 4, ("gm_accept_tokens(H2D ids) → gm_fill_and_mask_logits → gm_sample_stream → "
-                                "D2H ids; D2H bitmask on a copy stream (double-buffered)")
-        for i in range(3):
-            e2e_step(i)
-        copy_stream.synchronize()
+        ptrs = (ctypes.c_uint64 * R)(*[t.data_ptr() for t in logits])
+        secs = ctypes.c_double()
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        t0 = time.perf_counter()
-        for i in range(Ke):
-            e2e_step(i)
-        copy_stream.synchronize()
-        t_e2e = time.perf_counter() - t0
-        batch.check()
-        (t_e2e,) = max_over_ranks([t_e2e], dev, world)
-        e2e = {"value": aggregate_rate(world, B * Ke, t_e2e), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": B * W * 4 + B * 4, "steps": Ke, "path": path}
+        rc = drv.e2e_run(batch._h, 1 if greedy else 0, B, W, batch.nseg, ptrs, R, V1, seed & (2**64 - 1), 3, Ke,
+                         local, 1, ctypes.byref(secs))
+        if rc != 0:
+            raise RuntimeError(f"e2e driver failed: {rc} {pk.lib().gm_last_error().decode()}")
+        t_full = secs.value
+        # The same loop without the 16 KB/sequence bitmask read-back (the mask
+        # consumed only on the device): reported beside, not as the headline.
+        rc = drv.e2e_run(batch._h, 1 if greedy else 0, B, W, batch.nseg, ptrs, R, V1, seed & (2**64 - 1), 3, Ke,
+                         local, 0, ctypes.byref(secs))
+        if rc != 0:
+            raise RuntimeError(f"e2e driver failed: {rc} {pk.lib().gm_last_error().decode()}")
+        t_full, t_ids = max_over_ranks([t_full, secs.value], dev, world)
+        t_e2e = t_full
+        path = ("C++ caller: gm_decode_step_greedy(device logits) → D2H ids; D2H bitmask on a copy stream"
+                if greedy else "C++ caller: H2D ids → gm_accept_tokens → gm_fill_and_mask_logits → "
+                "gm_sample_stream → D2H ids; D2H bitmask on a copy stream (double-buffered)")
+        e2e = {"value": aggregate_rate(world, B * Ke, t_e2e), "unit": UNIT,
+               "h2d_bytes_per_step": 0 if greedy else B * 4, "d2h_bytes_per_step": B * W * 4 + B * 4,
+               "steps": Ke, "path": path,
+               "ids_only": {"value": aggregate_rate(world, B * Ke, t_ids), "d2h_bytes_per_step": B * 4,
+                            "note": "same loop without the bitmask read-back (mask consumed on the device)"}}
 
     if rank != 0:
         if world > 1:
