@@ -168,6 +168,13 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
 int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
                           int64_t ld, uint64_t seed, int32_t* tokens_out, void* stream);
 
+/* Engine::AllowedTerminals (runtime.cpp:188-208) for every sequence: the
+ * exact next-byte set plus $ — terminal t is allowed iff an edge of the
+ * current state accepting t has a condition matching the stack.  out is a
+ * device array of B x 9 words: bit t of word t/32 for bytes t < 256, $ = bit 0
+ * of word 8.  Non-alive sequences get all zero. */
+int gm_allowed_terminals(gm_batch* b, uint32_t* out, void* stream);
+
 /* Engine::Step over every byte of tokens[b] (runtime.cpp:177-186; callers'
  * loop gmask_main.cpp:113-118); tokens[b] == V steps kEndMarker; tokens[b] < 0
  * is a no-op.  status_out (may be NULL) receives gm_seq_status per sequence.

@@ -126,6 +126,7 @@ def lib() -> ctypes.CDLL:
             "gm_fill_next_token_bitmask": ([P, P, I64, P], ctypes.c_int),
             "gm_fill_and_mask_logits": ([P, P, I64, P, I64, P, P], ctypes.c_int),
             "gm_accept_tokens": ([P, P, P, I32, P], ctypes.c_int),
+            "gm_allowed_terminals": ([P, P, P], ctypes.c_int),
             "gm_sample_stream_and_accept": ([P, P, I64, P, U64, P, P], ctypes.c_int),
             "gm_sample_stream": ([P, P, I64, P, U64, P, P], ctypes.c_int),
             "gm_decode_step_stream": ([P, P, I64, P, I64, U64, P, P], ctypes.c_int),
@@ -340,6 +341,19 @@ class DeviceEngine:
         b.check()
         return out.cpu().numpy().view(np.uint32)[0].copy()
 
+    def AllowedTerminals(self, cfg: RuntimeConfig):
+        """Engine::AllowedTerminals (runtime.cpp:188-208) -> (byte set as int, end_marker)."""
+        import torch
+        b = self._one()
+        b.set(0, cfg)
+        out = torch.zeros((1, 9), dtype=torch.int32, device=f"cuda:{self.device}")
+        b.allowed_terminals(out)
+        w = out.cpu().numpy().view(np.uint32)[0]
+        byteset = 0
+        for i in range(8):
+            byteset |= int(w[i]) << (32 * i)
+        return byteset, bool(w[8] & 1)
+
     def AcceptToken(self, cfg: RuntimeConfig, token: int) -> RuntimeConfig:
         """Engine::Step over the token's bytes (EOS = id V) via the accept kernel."""
         import torch
@@ -402,6 +416,10 @@ class Batch:
         ld = logits.stride(0) if logits is not None else 0
         sc = seg_counts.data_ptr() if seg_counts is not None else None
         _check(lib().gm_fill_and_mask_logits(self._h, bm, ldw, lg, ld, sc, _stream(stream)))
+
+    def allowed_terminals(self, out, stream=None):
+        """Engine::AllowedTerminals per sequence into out: int32 CUDA tensor [B, 9]."""
+        _check(lib().gm_allowed_terminals(self._h, out.data_ptr(), _stream(stream)))
 
     def accept(self, tokens, status_out=None, restart: bool = False, stream=None):
         so = status_out.data_ptr() if status_out is not None else None

@@ -615,6 +615,16 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
   });
 }
 
+int gm_allowed_terminals(gm_batch* b, uint32_t* out, void* stream) {
+  return Guard([&]() -> int {
+    if (!b || !out) return Fail(GM_ERR_USAGE, "null argument");
+    gm_engine* e = b->engine;
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    Check(pre3::LaunchAllowed(e->aut, b->view, out, static_cast<cudaStream_t>(stream)), "allowed launch");
+    return GM_OK;
+  });
+}
+
 int gm_accept_tokens(gm_batch* b, const int32_t* tokens, int32_t* status_out, int32_t restart,
                      void* stream) {
   return Guard([&]() -> int {

@@ -2122,6 +2122,53 @@ cudaError_t LaunchSample(const AutView& a, const VocabView& v, const CacheView& 
 }
 
 // ---------------------------------------------------------------------------
+// AllowedTerminalsKernel: Engine::AllowedTerminals (runtime.cpp:188-208) for
+// every sequence — terminal t (byte or $) is allowed iff some edge of the
+// current state accepting t has a condition matching the stack (the OR of the
+// accepted sets of all condition-matching edges).  One CTA per sequence,
+// thread t scans the candidates of (state, t) against the stack in shared
+// memory.  out[b*9 + w]: bytes in words 0..7, $ = bit 0 of word 8.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(288) AllowedTerminalsKernel(AutView A, BatchView Bt, uint32_t* out) {
+  PdlEnter();
+  extern __shared__ int32_t stk[];
+  __shared__ uint32_t words[9];
+  const int b = blockIdx.x, t = threadIdx.x;
+  const SeqState st = Bt.seq[b];
+  const int depth = st.depth;
+  const int32_t* gstack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
+  for (int i = t; i < depth; i += blockDim.x) stk[i] = gstack[i];
+  if (t < 9) words[t] = 0u;
+  __syncthreads();
+  if (st.status == kAlive && t < 257) {
+    const int state = stk[depth - 1];
+    const int idx = state * 257 + t;
+    const int cb = __ldg(A.rec_begin + idx), ce = __ldg(A.rec_begin + idx + 1);
+    bool any = false;
+    for (int c = cb; c < ce && !any; ++c) {
+      const Rec r = LoadRec(A.recs + c);
+      bool match = r.cond_len <= depth;  // ConditionMatches (runtime.cpp:123-131)
+      for (int j = 1; j < r.cond_len && match; ++j) match = stk[depth - 1 - j] == CondEntry(r, A.rec_cond, j);
+      any = match;
+    }
+    if (any) atomicOr(&words[t >> 5], 1u << (t & 31));
+  }
+  __syncthreads();
+  if (t < 9) out[static_cast<long long>(b) * 9 + t] = words[t];
+}
+
+cudaError_t LaunchAllowed(const AutView& a, const BatchView& b, uint32_t* out, cudaStream_t s) {
+  if (b.B == 0) return cudaSuccess;
+  const size_t dyn = static_cast<size_t>(b.cap) * sizeof(int32_t);
+  static size_t opted = 0;
+  if (dyn > 48 * 1024 && dyn > opted) {
+    cudaFuncSetAttribute(AllowedTerminalsKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    opted = dyn;
+  }
+  return Launch(AllowedTerminalsKernel, dim3(b.B), dim3(288), dyn, s, a, b, out);
+}
+
+// ---------------------------------------------------------------------------
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
   return Launch(ResetKernel, dim3((b.B + 127) / 128), dim3(128), 0, s, a, b);

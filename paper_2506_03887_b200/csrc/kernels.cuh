@@ -175,6 +175,8 @@ struct SampleArgs {
 cudaError_t LaunchSample(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
                          SampleArgs s, cudaStream_t st);
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s);
+// Engine::AllowedTerminals per sequence: out[b*9 .. b*9+8].
+cudaError_t LaunchAllowed(const AutView& a, const BatchView& b, uint32_t* out, cudaStream_t s);
 cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s);
 cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,
                         cudaStream_t s);

@@ -391,3 +391,22 @@ def test_sample_decode_step_matches_port(T, k, p, ties):
                 port.free(cfgs[b])
                 cfgs[b] = port.initial()
             assert batch.get(b).stack == port.get(cfgs[b])[2], (b, s)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_allowed_terminals_matches_port(vectors, name):
+    """Engine::AllowedTerminals on the device (gm_allowed_terminals) == the C
+    port's on every sampled configuration (test_runtime.cpp:116-137 pins the
+    reference's own against viability)."""
+    case = vectors["mask_agreement"][name]
+    vocab = [bytes.fromhex(h) for h in case["vocab_hex"]]
+    f = flat(name)
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab)
+    port = Port(f, vocab)
+    for c in case["cases"]:
+        cfg = pk.RuntimeConfig(c["stack"][-1], c["status"], c["stack"])
+        got = eng.AllowedTerminals(cfg)
+        pc = port.config(c["status"], c["stack"])
+        want = port.allowed(pc) if c["status"] == 0 else (0, False)
+        port.free(pc)
+        assert got == want, (c["stack"], got, want)
