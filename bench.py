@@ -40,13 +40,13 @@ L2_BYTES = 126 * 1024 * 1024
 
 # BASELINE.json configs (index 1.. = config 2..5).
 CONFIGS = {
-    2: dict(grammar="json", flavor=0, batch=256, mode="stream", scaling="weak", K=12, slots=16384,
+    2: dict(grammar="json", flavor=0, batch=256, mode="stream", scaling="weak", K=16, slots=65536,
             desc="config2: JSON LR(1) grammar, 128256-bit vocab (synthetic 128k tokens), batch {b}/GPU, "
                  "fused mask-fill + in-place bf16 -inf logit masking + stream sample + accept_token"),
     3: dict(grammar="schema", flavor=0, batch=1024, mode="stream", scaling="weak", K=16, slots=16384,
             desc="config3: JSON-schema-derived LR(1) grammar (nested objects/arrays), 128256-bit vocab, "
                  "batch {b}/GPU, fused mask-fill + bf16 -inf logit masking + stream sample + accept_token"),
-    4: dict(grammar="sql", flavor=1, batch=4096, mode="stream", scaling="strong", K=20, slots=65536,
+    4: dict(grammar="sql", flavor=1, batch=4096, mode="stream", scaling="strong", K=20, slots=131072,
             desc="config4: SQL-subset LR(1) grammar, 128256-bit SQL-flavoured vocab, 4096 sequences in total "
                  "({b}/GPU), fused mask-fill + bf16 -inf logit masking + stream sample + accept_token"),
     5: dict(grammar="json", flavor=0, batch=512, mode="greedy", scaling="weak", K=12, slots=16384,
@@ -72,7 +72,7 @@ def parse(argv=None):
     p.add_argument("--parent-depth", type=int, default=0,
                    help="R: new contexts are built from the context keyed R deep (0: engine default min(4, K-1); "
                         "-1: full builds)")
-    p.add_argument("--prewarm-steps", type=int, default=2000,
+    p.add_argument("--prewarm-steps", type=int, default=10000,
                    help="context-cache preprocessing: synthetic decode steps (other seed) before timing")
     p.add_argument("--prewarm-batch", type=int, default=1024)
     p.add_argument("--stack-cap", type=int, default=1024)
