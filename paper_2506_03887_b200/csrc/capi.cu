@@ -93,6 +93,15 @@ struct gm_batch {
   int fill_seq = 0;                       // number of the next fill (heavy-list tags)
   bool slots_valid = false;               // seq_slot matches the stacks
   bool lookup_pending = false;            // queue[prod] got a lookup pass since the last fill
+  bool arrivals_pending = false;          // a fill published per-sequence arrivals nobody consumed yet
+
+  // seq_arrive must start at zero for a fused tail or a publishing fill.
+  void ClearArrivals(cudaStream_t s) {
+    if (arrivals_pending) {
+      Check(cudaMemsetAsync(view.seq_arrive, 0, static_cast<size_t>(view.B) * 4, s), "memset");
+      arrivals_pending = false;
+    }
+  }
 
   // Queue roles of a fill launch (3-queue ring, see kernels.cuh BatchView).
   void BeginFill(pre3::FillArgs* f) const {
@@ -579,9 +588,12 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     f.ld = ld;
     f.seg_counts = seg_counts;
     f.best = b->best;
+    f.publish_arrival = 1;  // lets a following sample/accept start per sequence
+    b->ClearArrivals(s);
     b->BeginFill(&f);
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s), "fill launch");
     b->EndFill(false);
+    b->arrivals_pending = true;
     return GM_OK;
   });
 }
@@ -607,6 +619,7 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
     f.best = b->best;
     f.tokens_out = tokens_out;
     f.seed = seed;
+    b->ClearArrivals(s);
     b->BeginFill(&f);
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailStream, e->aut, e->vocab, e->cache, b->view, f, s),
           "decode launch");
@@ -663,6 +676,8 @@ int gm_sample_stream_and_accept(gm_batch* b, const uint32_t* bitmask, int64_t ld
     g.do_accept = 1;
     g.lookup_queue = b->AcceptLookupQueue();
     g.lookup_tag = b->fill_seq;
+    g.wait_fill = b->arrivals_pending ? 1 : 0;  // start per sequence while the fill finishes
+    b->arrivals_pending = false;
     Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, g,
                              static_cast<cudaStream_t>(stream)),
           "sample launch");
@@ -685,6 +700,8 @@ int gm_sample_stream(gm_batch* b, const uint32_t* bitmask, int64_t ld_words, con
     g.tokens_out = tokens_out;
     g.do_accept = 0;
     g.lookup_queue = -1;
+    g.wait_fill = b->arrivals_pending ? 1 : 0;
+    b->arrivals_pending = false;
     Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, g,
                              static_cast<cudaStream_t>(stream)),
           "sample launch");
@@ -709,6 +726,7 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     f.ld = ld;
     f.best = b->best;
     f.tokens_out = tokens_out;
+    b->ClearArrivals(s);
     b->BeginFill(&f);
     Check(pre3::LaunchFill(pre3::kFillGreedy, pre3::kTailGreedy, e->aut, e->vocab, e->cache, b->view, f, s),
           "greedy decode launch");

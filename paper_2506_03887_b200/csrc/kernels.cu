@@ -1446,7 +1446,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   // ---- arrival (fused tail): mask words, counts and argmax partials are
   // made visible first; the bulk logits stores follow.
   bool last = false;
-  if (TAIL != kTailNone) {
+  if (TAIL != kTailNone || F.publish_arrival) {
     __threadfence();
     __syncwarp();
     int l = 0;
@@ -1693,7 +1693,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
   // words, counts and argmax partials must be visible to it, so the fence
   // precedes the (bulk) logits stores below.
   bool last = false;
-  if (TAIL != kTailNone) {
+  if (TAIL != kTailNone || F.publish_arrival) {
     __threadfence();
     __syncthreads();
     if (tid == 0) sh.last = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
@@ -1721,12 +1721,37 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
 // AcceptKernel: one warp per sequence (standalone accept / sample).
 // ---------------------------------------------------------------------------
 template <int SAMPLE>
+__device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv, const CacheView& Cc,
+                                           const BatchView& Bt, const AcceptArgs& G, int b, int lane);
+
+template <int SAMPLE>
 __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                     AcceptArgs G) {
-  PdlEnter();
+  // wait_fill: the preceding fill (launched just before, publishing
+  // per-sequence arrivals) may still be running — each warp starts as soon as
+  // its own sequence's items are in; the grid-wide wait moves to the end, so
+  // this grid still completes after the fill (the next kernel relies on it).
+  if (G.wait_fill) {
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  } else {
+    PdlEnter();
+  }
   const int lane = threadIdx.x & 31;
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (b >= Bt.B) return;
+  if (b < Bt.B) {
+    if (G.wait_fill) {
+      while (LoadAcquire(Bt.seq_arrive + b) < Vv.nseg) __nanosleep(64);
+      __syncwarp();
+      if (lane == 0) Bt.seq_arrive[b] = 0;
+    }
+    AcceptBody<SAMPLE>(A, Vv, Cc, Bt, G, b, lane);
+  }
+  if (G.wait_fill) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+template <int SAMPLE>
+__device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv, const CacheView& Cc,
+                                           const BatchView& Bt, const AcceptArgs& G, int b, int lane) {
   const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   SeqState st = Bt.seq[b];
   int tok = -1;

@@ -136,6 +136,8 @@ struct FillArgs {
   int produce;              // build queue fed by the tail's lookups
   int reset;                // queue drained by the previous fill, emptied here (-1: none)
   int fill_no;              // this fill's number (heavy_index tags; the tail tags fill_no + 1)
+  int publish_arrival;      // no tail: still count finished items per sequence (seq_arrive) so a
+                            // following AcceptKernel with wait_fill can start per sequence
   int vec_ok;               // set by LaunchFill
 };
 
@@ -152,6 +154,7 @@ struct AcceptArgs {
   int do_accept;     // 0: sample only
   int lookup_queue;  // >= 0: assign next-fill context slots into this queue
   int lookup_tag;    // number of the fill that consumes it
+  int wait_fill;     // overlap the preceding fill (publish_arrival): per-sequence start
 };
 
 struct SampleArgs {
