@@ -78,8 +78,7 @@ def parse(argv=None):
     p.add_argument("--stack-cap", type=int, default=1024)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--separate", action="store_true",
-                   help="stream mode: two launches per step (fill+mask logits, then sample+accept); "
-                        "the default above 512 sequences per GPU")
+                   help="stream mode: two launches per step (fill+mask logits, then sample+accept; the default)")
     p.add_argument("--one-launch", action="store_true", help="stream mode: force the one-launch fused step")
     p.add_argument("--fused", action="store_true", help=argparse.SUPPRESS)  # the default; kept for scripts
     p.add_argument("--no-e2e", action="store_true")
@@ -247,9 +246,10 @@ def workload_config(args, world, B):
     return {"workload": cfg["desc"].format(b=B), "config_index": args.config, "grammar": args.grammar,
             "vocab_bits": args.vocab + 1, "batch_per_gpu": B, "global_batch": B * world,
             "context_depth": args.context_depth, "mode": args.mode,
-            "step": ("gm_decode_step_greedy (one launch)" if args.mode == "greedy" else
-                     "gm_fill_and_mask_logits + gm_sample_stream_and_accept"
-                     if (args.separate or (B > 512 and not args.one_launch)) else "gm_decode_step_stream (one launch)"),
+            "step": ("gm_decode_step_greedy (argmax fill + accept kernels)" if args.mode == "greedy" else
+                     "gm_decode_step_stream (one launch)" if args.one_launch else
+                     "gm_fill_and_mask_logits + gm_sample_stream_and_accept (the accept starts per sequence "
+                     "under the fill's last wave)"),
             "context_slots": args.context_slots,
             "parallelism": f"dp{world} (sequence shards, no hot-path collective)"}
 
@@ -324,7 +324,7 @@ def main(argv=None):
     greedy = args.mode == "greedy"
     # One launch per step wins while the batch leaves the GPU latency-bound;
     # above 512 sequences the standalone accept kernel's parallelism wins.
-    separate = not greedy and (args.separate or (B > 512 and not args.one_launch))
+    separate = not greedy and not args.one_launch
 
     def step(i):
         if greedy:
@@ -497,7 +497,7 @@ def main(argv=None):
                          f"threads={cores}, per seq-step {cpu_step_rule(args.mode)}"}
 
     info = eng.info()
-    kname = ("FillKernel<greedy> (one-launch step: fill + argmax + accept tail)" if greedy else
+    kname = ("FillKernel<greedy> + AcceptKernel<greedy> (the whole step, sampled)" if greedy else
              "FillKernel (fill + -inf logits; accept runs in AcceptKernel)" if separate else
              "FillKernel (one-launch step: fill + -inf logits + sample/accept tail)")
     line = {

@@ -725,12 +725,24 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     f.logits = const_cast<uint16_t*>(logits);
     f.ld = ld;
     f.best = b->best;
-    f.tokens_out = tokens_out;
+    f.publish_arrival = 1;
     b->ClearArrivals(s);
     b->BeginFill(&f);
-    Check(pre3::LaunchFill(pre3::kFillGreedy, pre3::kTailGreedy, e->aut, e->vocab, e->cache, b->view, f, s),
-          "greedy decode launch");
-    b->EndFill(true);
+    // Two kernels: the argmax fill, then the accept kernel, which starts per
+    // sequence while the fill's last wave runs (measured faster than the
+    // one-launch fused tail, whose tails hold fill CTA slots).
+    Check(pre3::LaunchFill(pre3::kFillGreedy, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s),
+          "greedy fill launch");
+    b->EndFill(false);
+    pre3::AcceptArgs g{};
+    g.best = b->best;
+    g.tokens_out = tokens_out;
+    g.restart = 1;
+    g.do_accept = 1;
+    g.lookup_queue = b->AcceptLookupQueue();
+    g.lookup_tag = b->fill_seq;
+    g.wait_fill = 1;
+    Check(pre3::LaunchAccept(pre3::kSampleGreedy, e->aut, e->vocab, e->cache, b->view, g, s), "greedy accept launch");
     return GM_OK;
   });
 }

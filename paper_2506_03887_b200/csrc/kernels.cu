@@ -2234,7 +2234,11 @@ cudaError_t LaunchFill(int mode, int tail, const AutView& a, const VocabView& v,
   f.vec_ok = f.logits != nullptr && (f.ld % 8) == 0 && (reinterpret_cast<uintptr_t>(f.logits) % 16) == 0;
   const size_t dyn = static_cast<size_t>(b.cap > kMaxContext ? b.cap : kMaxContext) * sizeof(int32_t);
   if (mode == kFillGreedy) {
-    LaunchFillT<kFillGreedy, kTailGreedy>(a, v, c, b, f, dyn, s);
+    if (tail == kTailGreedy) {
+      LaunchFillT<kFillGreedy, kTailGreedy>(a, v, c, b, f, dyn, s);
+    } else {
+      LaunchFillT<kFillGreedy, kTailNone>(a, v, c, b, f, dyn, s);
+    }
   } else if (tail == kTailStream) {
     LaunchFillT<kFillMask, kTailStream>(a, v, c, b, f, dyn, s);
   } else {
