@@ -38,7 +38,7 @@ def dram(rep):
     return int(mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"))
 F = "gpurun_out/final"
 t = {
- "json:128255:256:stream:fused": {"dram_bytes_per_launch": dram(F + "/c2_fill.ncu-rep"), "source": "ncu --set full, FillKernel<0,1> one-launch step (profiles/r01_c2_fill_summary.txt)", "note": "the masked logits mostly stay dirty in the 126 MB L2 when the kernel ends; their write-back is not attributed to the launch, so DRAM writes under-count"},
+ "json:128255:256:stream:separate": {"dram_bytes_per_launch": dram(F + "/c2_fill.ncu-rep"), "source": "ncu --set full, FillKernel<0,0> (profiles/r01_c2_fill_summary.txt)", "note": "at 256 sequences the masked logits (63 MB) mostly stay dirty in the 126 MB L2 when the kernel ends; their write-back is not attributed to the launch, so DRAM writes under-count"},
  "schema:128255:1024:stream:separate": {"dram_bytes_per_launch": dram(F + "/c3_fill.ncu-rep"), "source": "ncu --set full, FillKernel<0,0> (profiles/r01_c3_fill_summary.txt)"},
  "json:128255:1024:stream:separate": {"dram_bytes_per_launch": dram(F + "/json1024_fill.ncu-rep"), "source": "ncu --set full, FillKernel<0,0> (profiles/r01_json1024_fill_summary.txt)"},
 }
