@@ -248,8 +248,10 @@ def workload_config(args, world, B):
             "context_depth": args.context_depth, "mode": args.mode,
             "step": ("gm_decode_step_greedy (argmax fill + accept kernels)" if args.mode == "greedy" else
                      "gm_decode_step_stream (one launch)" if args.one_launch else
-                     "gm_fill_and_mask_logits + gm_sample_stream_and_accept (the accept starts per sequence "
-                     "under the fill's last wave)"),
+                     "gm_decode_step_stream_split (fill + overlapped sample/accept kernel: pure-CI sequences "
+                     "sample from their cached context row at once, the rest as their fill items arrive); "
+                     "every 8th step as gm_fill_and_mask_logits + gm_sample_stream_and_accept with events "
+                     "around the fill"),
             "context_slots": args.context_slots,
             "parallelism": f"dp{world} (sequence shards, no hot-path collective)"}
 
@@ -330,8 +332,7 @@ def main(argv=None):
         if greedy:
             batch.decode_step_greedy(logits[i % R], tokens_out=toks, bitmask=bm)
         elif separate:
-            batch.fill(bm, logits[i % R], counts)
-            batch.sample_stream_and_accept(bm, counts, seed, toks)
+            batch.decode_step_stream_split(seed, bitmask=bm, logits=logits[i % R], seg_counts=counts, tokens_out=toks)
         else:
             batch.decode_step_stream(seed, bitmask=bm, logits=logits[i % R], tokens_out=toks)
 
@@ -357,10 +358,9 @@ def main(argv=None):
             timed = i % SAMPLE_EVERY == 0
             if timed:
                 ev[i // SAMPLE_EVERY][0].record(stream)
-            if separate:  # events bracket the fill kernel alone (the roofline kernel)
+            if separate and timed:  # events bracket the fill kernel alone (the roofline kernel)
                 batch.fill(bm, logits[i % R], counts)
-                if timed:
-                    ev[i // SAMPLE_EVERY][1].record(stream)
+                ev[i // SAMPLE_EVERY][1].record(stream)
                 batch.sample_stream_and_accept(bm, counts, seed, toks)
             else:
                 step(i)
@@ -393,8 +393,7 @@ def main(argv=None):
         Rn = max(2, -(-3 * L2_BYTES // (Bn * V1 * 2)))
         lgn = [torch.randn((Bn, V1), dtype=torch.bfloat16, device=dev) for _ in range(Rn)]
         for i in range(30):
-            bn.fill(bmn, lgn[i % Rn], cn)
-            bn.sample_stream_and_accept(bmn, cn, seed, tn)
+            bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn)
         torch.cuda.synchronize()
         Kn = 120
         evn = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(0, Kn, 8)]
@@ -403,17 +402,19 @@ def main(argv=None):
         for i in range(Kn):
             if i % 8 == 0:
                 evn[i // 8][0].record(stream)
-            bn.fill(bmn, lgn[i % Rn], cn)
-            if i % 8 == 0:
+                bn.fill(bmn, lgn[i % Rn], cn)
                 evn[i // 8][1].record(stream)
-            bn.sample_stream_and_accept(bmn, cn, seed, tn)
+                bn.sample_stream_and_accept(bmn, cn, seed, tn)
+            else:
+                bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn)
         f1.record(stream)
         torch.cuda.synchronize()
         bn.check()
         fill_ms_n = sum(a.elapsed_time(c) for a, c in evn) / len(evn)
         pk_gbs, _, _ = peaks()
         ach_n = Bn * (2 * V1 + 8 * W) / (fill_ms_n / 1e3) / 1e9
-        north = {"batch": Bn, "step": "gm_fill_and_mask_logits + gm_sample_stream_and_accept",
+        north = {"batch": Bn, "step": "gm_decode_step_stream_split (every 8th step: fill + sample/accept with "
+                 "events around the fill)",
                  "fill_kernel_us": 1e3 * fill_ms_n, "achieved_gbs": ach_n, "frac": ach_n / pk_gbs,
                  "seq_steps_per_s": Bn * Kn / (f0.elapsed_time(f1) / 1e3), "steps": Kn}
         del bn, lgn

@@ -168,6 +168,17 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
 int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
                           int64_t ld, uint64_t seed, int32_t* tokens_out, void* stream);
 
+/* The same step as two kernels: the fill, then the sample/accept/lookup
+ * kernel, which overlaps it — a sequence whose mask is exactly its context's
+ * cached CI row (no context-dependent tokens) samples from that
+ * row at once; the others start as soon as their own fill items are in.
+ * Same results as gm_decode_step_stream.  seg_counts may be NULL (internal
+ * buffer); when given it receives the fill's counts as in
+ * gm_fill_and_mask_logits. */
+int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
+                                int64_t ld, int32_t* seg_counts, uint64_t seed, int32_t* tokens_out,
+                                void* stream);
+
 /* Engine::AllowedTerminals (runtime.cpp:188-208) for every sequence: the
  * exact next-byte set plus $ — terminal t is allowed iff an edge of the
  * current state accepting t has a condition matching the stack.  out is a

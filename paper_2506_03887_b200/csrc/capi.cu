@@ -326,6 +326,21 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
                                num_tokens ? tok_bytes + tok_offsets[num_tokens] : tok_bytes);
     e->vocab.tok_off = DevUpload(offs, &e->owned);
     e->vocab.tok_bytes = DevUpload(bytes, &e->owned);
+    // Token records: offset, length and the first 8 bytes in one 16-B load
+    // (a walk's first round trip; longer tokens read the rest from tok_bytes).
+    // Entry V is EOS: length 1, no bytes.
+    std::vector<int32_t> recs(4 * (static_cast<size_t>(num_tokens) + 1), 0);
+    for (int32_t i = 0; i < num_tokens; ++i) {
+      const int32_t lo = offs[static_cast<size_t>(i)], len = offs[static_cast<size_t>(i) + 1] - lo;
+      uint32_t w[2] = {0u, 0u};
+      for (int32_t j = 0; j < len && j < 8; ++j) w[j >> 2] |= static_cast<uint32_t>(bytes[static_cast<size_t>(lo + j)]) << (8 * (j & 3));
+      recs[4 * static_cast<size_t>(i) + 0] = lo;
+      recs[4 * static_cast<size_t>(i) + 1] = len;
+      recs[4 * static_cast<size_t>(i) + 2] = static_cast<int32_t>(w[0]);
+      recs[4 * static_cast<size_t>(i) + 3] = static_cast<int32_t>(w[1]);
+    }
+    recs[4 * static_cast<size_t>(num_tokens) + 1] = 1;
+    e->vocab.tok_rec = reinterpret_cast<const int4*>(DevUpload(recs, &e->owned));
     e->structural = DevAlloc<uint32_t>(static_cast<size_t>(e->W), &e->owned);
     Check(cudaMemset(e->structural, 0, sizeof(uint32_t) * static_cast<size_t>(e->W)), "memset");
     e->vocab.structural = e->structural;
@@ -350,6 +365,8 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.R = static_cast<int32_t>(o.parent_depth);
     c.cd_segmask = DevAlloc<uint32_t>(C, &e->owned);
     Check(cudaMemset(c.cd_segmask, 0, C * 4), "memset");
+    c.ci_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg) * 2, &e->owned);
+    Check(cudaMemset(c.ci_cnt, 0, C * static_cast<size_t>(e->nseg) * 8), "memset");
     Check(cudaMemset(c.slot_built, 0, C * 4), "memset");
     c.counters = DevAlloc<unsigned long long>(8, &e->owned);
     Check(cudaMemset(c.slot_hash, 0, C * 8), "memset");
@@ -392,7 +409,11 @@ int gm_engine_set_structural(gm_engine* e, const uint32_t* host_words) {
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     std::vector<uint32_t> w(host_words, host_words + e->W);
     w[static_cast<size_t>(e->V >> 5)] &= ~(1u << (e->V & 31));  // EOS is never structural
+    Check(cudaDeviceSynchronize(), "structural: fills in flight");
     Check(cudaMemcpy(e->structural, w.data(), w.size() * 4, cudaMemcpyHostToDevice), "structural");
+    // Contexts built before this call counted the old set.
+    Check(pre3::LaunchRecountStructural(e->cache, e->vocab), "structural recount");
+    Check(cudaDeviceSynchronize(), "structural recount");
     return GM_OK;
   });
 }
@@ -418,7 +439,9 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.trace_cap = 0;
     const size_t bn = static_cast<size_t>(std::max(batch, 1)) * static_cast<size_t>(e->nseg);
     v.nseg = e->nseg;
-    v.seq_slot = DevAlloc<int32_t>(static_cast<size_t>(batch), &b->owned);
+    v.seq_slot = DevAlloc<int32_t>(2 * static_cast<size_t>(batch), &b->owned);  // by fill parity
+    v.seq_hmask = DevAlloc<uint32_t>(2 * static_cast<size_t>(batch), &b->owned);
+    Check(cudaMemset(v.seq_hmask, 0xff, 2 * static_cast<size_t>(batch) * 4), "memset");
     v.priv = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     v.priv_done = DevAlloc<int32_t>(bn, &b->owned);
     v.heavy_index = DevAlloc<int32_t>(2 * bn, &b->owned);  // double-buffered by fill parity
@@ -624,6 +647,50 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailStream, e->aut, e->vocab, e->cache, b->view, f, s),
           "decode launch");
     b->EndFill(true);
+    return GM_OK;
+  });
+}
+
+// Two-kernel decode step: fill (arrivals only for sequences that are not
+// pure CI), then the overlapping sample/accept/lookup kernel, which samples a
+// pure-CI sequence from its slot's CI row and counts (the fill writes the same
+// words and counts into bitmask/seg_counts) without waiting for the fill.
+int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits, int64_t ld,
+                                int32_t* seg_counts, uint64_t seed, int32_t* tokens_out, void* stream) {
+  return Guard([&]() -> int {
+    if (!b) return Fail(GM_ERR_USAGE, "null batch");
+    gm_engine* e = b->engine;
+    if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
+    if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
+    pre3::FillArgs f{};
+    f.bitmask = bitmask ? bitmask : b->scratch_mask;
+    f.ldw = bitmask ? ld_words : e->W;
+    f.logits = logits;
+    f.ld = ld;
+    f.seg_counts = seg_counts ? seg_counts : b->seg_counts;
+    f.best = b->best;
+    f.publish_arrival = 2;
+    b->ClearArrivals(s);
+    b->BeginFill(&f);
+    Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s),
+          "fill launch");
+    b->EndFill(false);
+    pre3::AcceptArgs g{};
+    g.restart = 1;
+    g.bitmask = f.bitmask;
+    g.ldw = f.ldw;
+    g.seg_counts = f.seg_counts;
+    g.seed = seed;
+    g.tokens_out = tokens_out;
+    g.do_accept = 1;
+    g.lookup_queue = b->AcceptLookupQueue();
+    g.lookup_tag = b->fill_seq;
+    g.wait_fill = 1;
+    g.ci_shortcut = 1;
+    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, g, s), "accept launch");
     return GM_OK;
   });
 }

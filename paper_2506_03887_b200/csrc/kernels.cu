@@ -23,6 +23,13 @@
 
 #include "kernels.cuh"
 
+#ifndef PRE3_FILL_MIN_BLOCKS
+#define PRE3_FILL_MIN_BLOCKS 4  // fill CTAs resident per SM (64 registers)
+#endif
+#ifndef PRE3_BULK_MASKED
+#define PRE3_BULK_MASKED 1  // fully masked spans as one bulk (TMA) store
+#endif
+
 namespace pre3 {
 namespace {
 
@@ -67,6 +74,18 @@ __device__ __forceinline__ int Lane4(const int4& q, int i) {
 }
 
 // Condition entry j (1-based, j <= 16 inline, else from the pool).
+// Byte j (< 8) of a token record (VocabView::tok_rec).
+__device__ __forceinline__ int TokByte(const int4& tr, int j) {
+  return static_cast<int>(((j < 4 ? static_cast<uint32_t>(tr.z) : static_cast<uint32_t>(tr.w)) >> (8 * (j & 3))) & 0xffu);
+}
+
+// Byte `lane` of a token for a warp walk (256 past the end / for EOS): the
+// first 8 from the record, the rest from tok_bytes.
+__device__ __forceinline__ int TokLaneByte(const int4& tr, const uint8_t* tok_bytes, int lane, int nterm, bool eos) {
+  if (eos || lane >= nterm) return 256;
+  return lane < 8 ? TokByte(tr, lane) : static_cast<int>(__ldg(tok_bytes + tr.x + lane));
+}
+
 __device__ __forceinline__ int CondEntry(const Rec& r, const int32_t* rec_cond, int j) {
   return j <= 16 ? Lane4(r.c[(j - 1) >> 2], (j - 1) & 3) : __ldg(rec_cond + r.cond_off + j - 1);
 }
@@ -182,7 +201,7 @@ __device__ __forceinline__ int IndexedFindEdge(const int2* hmeta, const int16_t*
 
 __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* rec_begin, const CandRec* recs,
                                           const int32_t* rec_cond, const int32_t* rec_push, const int32_t* shift,
-                                          const int32_t* tok_off, const uint8_t* tok_bytes, int32_t V, int32_t t,
+                                          const int4* tok_rec, const uint8_t* tok_bytes, int32_t V, int32_t t,
                                           const int32_t* base, int nb, bool complete, const int2* hmeta,
                                           const int16_t* hlens, const unsigned long long* hexact,
                                           unsigned long long emask, const unsigned long long* hprefix,
@@ -195,22 +214,17 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
     const int32_t* rec_push;
     const int32_t* shift;
   } A{first, rec_begin, recs, rec_cond, rec_push, shift};
-  const struct {
-    const int32_t* tok_off;
-    const uint8_t* tok_bytes;
-    int32_t V;
-  } Vv{tok_off, tok_bytes, V};
   int32_t loc[kWalkOverlay];
   int nl = 0;
-  const bool eos = t == Vv.V;
-  const int off = eos ? 0 : __ldg(Vv.tok_off + t);
-  const int nterm = eos ? 1 : __ldg(Vv.tok_off + t + 1) - off;
-  const uint8_t* bytes = Vv.tok_bytes + off;
+  const bool eos = t == V;
+  const int4 tr = __ldg(tok_rec + t);  // offset, length, first 8 bytes: one round trip
+  const int nterm = tr.y;
+  const uint8_t* bytes = tok_bytes + tr.x;
   int state = base[nb - 1];
-  int x_next = eos ? 256 : static_cast<int>(__ldg(bytes));
+  int x_next = eos ? 256 : TokByte(tr, 0);
   for (int i = 0; i < nterm; ++i) {
     const int x = x_next;
-    if (i + 1 < nterm) x_next = static_cast<int>(__ldg(bytes + i + 1));  // off the state chain
+    if (i + 1 < nterm) x_next = i + 1 < 8 ? TokByte(tr, i + 1) : static_cast<int>(__ldg(bytes + i + 1));
     // Candidates of (state, x) in arbitration order (the first one from the
     // dense table, in the same round trip as the range); none rejects.
     const int idx = state * 257 + x;
@@ -294,7 +308,7 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
 
 __device__ __forceinline__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
                                          bool complete) {
-  return WalkTokenImpl(A.first, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_off, Vv.tok_bytes,
+  return WalkTokenImpl(A.first, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_rec, Vv.tok_bytes,
                        Vv.V, t, base, nb, complete, A.hidx_meta, A.hidx_lens, A.hidx_exact, A.hidx_exact_mask,
                        A.hidx_prefix, A.hidx_prefix_mask);
 }
@@ -309,9 +323,10 @@ __device__ __forceinline__ int WalkToken(const AutView& A, const VocabView& Vv, 
 // repeats the walk with WalkToken).
 __device__ int WalkWarp(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb, int lane) {
   const bool eos = t == Vv.V;
-  const int off = eos ? 0 : __ldg(Vv.tok_off + t);
-  const int nterm = eos ? 1 : __ldg(Vv.tok_off + t + 1) - off;
-  const int xb = (!eos && lane < nterm) ? static_cast<int>(__ldg(Vv.tok_bytes + off + lane)) : 256;
+  const int4 tr = __ldg(Vv.tok_rec + t);
+  const int off = tr.x;
+  const int nterm = tr.y;
+  const int xb = TokLaneByte(tr, Vv.tok_bytes, lane, nterm, eos);
   int ov = -1;  // overlay entry `lane`
   int nl = 0;
   int state = base[nb - 1];
@@ -334,8 +349,10 @@ __device__ int WalkWarp(const AutView& A, const VocabView& Vv, int32_t t, const 
         if (c < ce) r = LoadRec(A.recs + c);
       }
       bool match = c < ce && r.cond_len <= nl + nb;
+      const int jmax = static_cast<int>(__reduce_max_sync(0xffffffffu, match ? static_cast<unsigned>(r.cond_len) : 1u));
 #pragma unroll
       for (int j = 1; j <= 16; ++j) {
+        if (j >= jmax) break;
         const int sh = __shfl_sync(0xffffffffu, ov, (nl - 1 - j) & 31);
         if (match && j < r.cond_len) {
           const int have = j < nl ? sh : base[nb - 1 - (j - nl)];
@@ -434,10 +451,27 @@ __device__ int BlockExclusiveScan(int v, int* scratch, int* total) {
   return out;
 }
 
+// Hash of a context key: entries mixed independently (position-salted) and
+// XOR-combined, so a warp computes it with one Mix64 per lane and a
+// butterfly (KeyHashWarp) instead of a serial chain of n.
+__device__ __forceinline__ unsigned long long KeyEntryMix(int32_t v, int i) {
+  return Mix64((static_cast<unsigned long long>(static_cast<uint32_t>(v)) << 32) |
+               static_cast<unsigned long long>(i + 1));
+}
+__device__ __forceinline__ unsigned long long KeyHashFinish(unsigned long long x, int n, int complete) {
+  return Mix64(x ^ Mix64(0x5ca1ab1eull ^ static_cast<unsigned long long>(n | (complete << 8)))) | 1ull;
+}
 __device__ unsigned long long KeyHash(const int32_t* key, int n, int complete) {
-  unsigned long long h = Mix64(0x5ca1ab1eull ^ static_cast<unsigned long long>(n | (complete << 8)));
-  for (int i = 0; i < n; ++i) h = Mix64(h ^ static_cast<uint32_t>(key[i]));
-  return h | 1ull;
+  unsigned long long x = 0ull;
+  for (int i = 0; i < n; ++i) x ^= KeyEntryMix(key[i], i);
+  return KeyHashFinish(x, n, complete);
+}
+// The same for a warp holding entry `lane` in kv (lanes < n).
+__device__ __forceinline__ unsigned long long KeyHashWarp(int kv, int n, int complete, int lane) {
+  unsigned long long x = lane < n ? KeyEntryMix(kv, lane) : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(0xffffffffu, x, o);
+  return KeyHashFinish(x, n, complete);
 }
 
 // Meta word of slot i once its inserter has published the key row (the
@@ -494,13 +528,24 @@ __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int com
   return -1;
 }
 
+// seq_slot / seq_hmask rows of fill `fill_no` (double-buffered like
+// heavy_index: an accept that overlaps a fill writes the next fill's row
+// while that fill's items may still read their own).
+__device__ __forceinline__ int32_t* SeqSlot(const BatchView& Bt, int fill_no) {
+  return Bt.seq_slot + static_cast<long long>(fill_no & 1) * Bt.B;
+}
+__device__ __forceinline__ uint32_t* SeqHmask(const BatchView& Bt, int fill_no) {
+  return Bt.seq_hmask + static_cast<long long>(fill_no & 1) * Bt.B;
+}
+
 // Context slot of sequence b for the next fill (seq_slot[b]); a new shared
 // slot or a private row queues one build item per segment into `q`.
 // `key` = the top min(depth, K) stack entries, top first.  Returns seq_slot[b].
-__device__ int AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, int b, const SeqState& st,
+__device__ int AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, int tag, int b, const SeqState& st,
                              int nseg, const int32_t* key) {
+  int32_t* slot_out = SeqSlot(Bt, tag) + b;
   if (st.status != kAlive) {
-    Bt.seq_slot[b] = -2;
+    *slot_out = -2;
     return -2;
   }
   const int n = min(st.depth, Cc.K);
@@ -540,7 +585,7 @@ __device__ int AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, in
     wait = LoadAcquire(Cc.slot_built + slot) < nseg * kChunksPerSeg;
   }
   const int flagged = slot | (wait ? kSlotWait : 0);
-  Bt.seq_slot[b] = flagged;
+  *slot_out = flagged;
   return flagged;
 }
 
@@ -584,6 +629,7 @@ __device__ void PublishHeavy(const BatchView& Bt, int q, int tag, int b, uint32_
     }
     HeavyIndex(Bt, tag, nseg)[static_cast<long long>(b) * nseg + s] = idx;
   }
+  if (lane == 0) SeqHmask(Bt, tag)[b] = mask;
 }
 
 // Bounded wait (one thread) for the build of (slot, seg).  Units of this
@@ -666,6 +712,13 @@ __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView
     } else {
       Cc.ci[static_cast<long long>(slot) * Vv.W + w] = acc;
       Cc.cdb[static_cast<long long>(slot) * Vv.W + w] = cd;
+      // The segment's sampler counts of the CI bits (EOS excluded), the
+      // counts of a pure-CI mask (LightItem, AcceptKernel's ci_shortcut).
+      const uint32_t a = w == (Vv.V >> 5) ? acc & ~(1u << (Vv.V & 31)) : acc;
+      const int2 n = make_int2(__popc(a), __popc(a & __ldg(Vv.structural + w)));
+      int32_t* cnt = Cc.ci_cnt + (static_cast<long long>(slot) * Vv.nseg + seg) * 2;
+      if (n.x) atomicAdd(cnt, n.x);
+      if (n.y) atomicAdd(cnt + 1, n.y);
       if (cd) {
         atomicAdd(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg, __popc(cd));
         if (seg < 32) atomicOr(Cc.cd_segmask + slot, 1u << seg);
@@ -724,8 +777,8 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
     na += __ldcg(counts + 2 * s);
     ns += __ldcg(counts + 2 * s + 1);
   }
-  na = WarpSum(na);
-  ns = WarpSum(ns);
+  na = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(na)));
+  ns = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(ns)));
   const bool eos = (eos_word >> (Vv.V & 31)) & 1u;
   const unsigned long long u =
       Mix64(Mix64(seed ^ (static_cast<unsigned long long>(b) * 0xD1B54A32D192ED03ull)) ^
@@ -753,13 +806,16 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
     }
   }
   if (seg < 0) return -1;
-  // Round trip 2: all of the segment's words (and structural words).
+  // Round trip 2: all of the segment's words (and structural words); lane l
+  // holds words 8l..8l+7 of the segment, so one warp scan of the per-lane
+  // counts finds the lane, which finds the word and bit alone.
   const int w0 = seg * kSegWords;
   const int w1 = min(Vv.W, w0 + kSegWords);
   uint32_t xs[kSegWords / 32];
+  int c = 0;
 #pragma unroll
   for (int j = 0; j < kSegWords / 32; ++j) {
-    const int w = w0 + j * 32 + lane;
+    const int w = w0 + lane * (kSegWords / 32) + j;
     uint32_t x = 0;
     if (w < w1) {
       x = __ldcg(row + w);
@@ -767,25 +823,23 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
       if (use_s) x &= __ldg(Vv.structural + w);
     }
     xs[j] = x;
+    c += __popc(x);
   }
+  const int inc = WarpInclusiveScan(c, lane);
+  const int total = __shfl_sync(0xffffffffu, inc, 31);
+  if (r >= static_cast<uint32_t>(total)) return -1;
+  const int src = __ffs(__ballot_sync(0xffffffffu, static_cast<uint32_t>(inc) > r)) - 1;
+  int tok = -1;
+  if (lane == src) {
+    uint32_t rr = r - static_cast<uint32_t>(inc - c);
 #pragma unroll
-  for (int j = 0; j < kSegWords / 32; ++j) {
-    const int c = __popc(xs[j]);
-    const int inc = WarpInclusiveScan(c, lane);
-    const int total = __shfl_sync(0xffffffffu, inc, 31);
-    if (r < static_cast<uint32_t>(total)) {
-      const int src = __ffs(__ballot_sync(0xffffffffu, static_cast<uint32_t>(inc) > r)) - 1;
-      int tok = -1;
-      if (lane == src) {
-        uint32_t x = xs[j];
-        for (uint32_t rr = r - static_cast<uint32_t>(inc - c); rr > 0; --rr) x &= x - 1;
-        tok = (w0 + j * 32 + lane) * 32 + __ffs(x) - 1;
-      }
-      return __shfl_sync(0xffffffffu, tok, src);
+    for (int j = 0; j < kSegWords / 32; ++j) {
+      const uint32_t pc = static_cast<uint32_t>(__popc(xs[j]));
+      if (tok < 0 && rr < pc) tok = (w0 + lane * (kSegWords / 32) + j) * 32 + static_cast<int>(__fns(xs[j], 0, rr + 1));
+      if (tok < 0) rr -= pc;
     }
-    r -= static_cast<uint32_t>(total);
   }
-  return -1;
+  return __shfl_sync(0xffffffffu, tok, src);
 }
 
 // Warp-cooperative LookupSlot: same table protocol (64 linear probes from
@@ -797,9 +851,7 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
 // inserted it; *built / *segmask of an existing slot.
 __device__ int LookupSlotWarp(const CacheView& C, int kv, int n, int complete, int lane, bool* created, int* built,
                               uint32_t* segmask) {
-  unsigned long long h = Mix64(0x5ca1ab1eull ^ static_cast<unsigned long long>(n | (complete << 8)));
-  for (int i = 0; i < n; ++i) h = Mix64(h ^ static_cast<uint32_t>(__shfl_sync(0xffffffffu, kv, i)));
-  h |= 1ull;  // KeyHash
+  const unsigned long long h = KeyHashWarp(kv, n, complete, lane);
   const int meta_want = n | (complete << 8);
   *created = false;
   const unsigned long long cmask = static_cast<unsigned long long>(C.C - 1);
@@ -855,10 +907,11 @@ __device__ int LookupSlotWarp(const CacheView& C, int kv, int n, int complete, i
 // (seq_slot[b]); a new shared slot or a private row queues one build item per
 // segment into queue q.  Returns the segments the next fill must schedule in
 // its heavy pass (CD tokens or a pending build).
-__device__ uint32_t AssignSlotWarp(const CacheView& Cc, const BatchView& Bt, int q, int b, const SeqState& st,
-                                   int nseg, int kv, int lane) {
+__device__ uint32_t AssignSlotWarp(const CacheView& Cc, const BatchView& Bt, int q, int tag, int b,
+                                   const SeqState& st, int nseg, int kv, int lane) {
+  int32_t* slot_out = SeqSlot(Bt, tag) + b;
   if (st.status != kAlive) {
-    if (lane == 0) Bt.seq_slot[b] = -2;
+    if (lane == 0) *slot_out = -2;
     return 0u;
   }
   const int n = min(st.depth, Cc.K);
@@ -911,7 +964,7 @@ __device__ uint32_t AssignSlotWarp(const CacheView& Cc, const BatchView& Bt, int
     // Existing slot: only one whose build is still queued needs a wait.
     wait = built < nseg * kChunksPerSeg;
   }
-  if (lane == 0) Bt.seq_slot[b] = slot | (wait ? kSlotWait : 0);
+  if (lane == 0) *slot_out = slot | (wait ? kSlotWait : 0);
   const uint32_t all = nseg >= 32 ? 0xffffffffu : ((1u << nseg) - 1u);
   return (wait || slot >= Cc.C) ? all : (segmask & all);
 }
@@ -927,20 +980,25 @@ __device__ uint32_t AssignSlotWarp(const CacheView& Cc, const BatchView& Bt, int
 //    arbitration order, 32 per round; each candidate lane loads its record,
 //    condition list and first four pushed states in one round trip; the
 //    winner's fields are broadcast by shuffles (Apply, runtime.cpp:148-168).
+// Stack window of sequence b (lane j = entry j from the top, -1 below the
+// bottom): AcceptWarp's starting registers, loadable ahead of the sample.
+__device__ __forceinline__ int StackWindow(const BatchView& Bt, int b, int depth, int lane) {
+  return lane < depth ? Bt.stacks[static_cast<long long>(b) * Bt.cap + depth - 1 - lane] : -1;
+}
+
 __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int b,
-                           SeqState st, int tok, int32_t* status_out, int restart, int lookup_queue, int lookup_tag,
-                           int lane) {
+                           SeqState st, int topv, int tok, int32_t* status_out, int restart, int lookup_queue,
+                           int lookup_tag, int lane) {
   int32_t* stack = Bt.stacks + static_cast<long long>(b) * Bt.cap;
   unsigned long long t_ph = Bt.trace ? NowNs() : 0ull;
   int depth = st.depth;
-  int topv = lane < depth ? stack[depth - 1 - lane] : -1;
   int wv = min(depth, 32);
   if (tok >= 0 && st.status == kAlive) {
     const bool eos = tok == Vv.V;
-    const int off = eos ? 0 : __ldg(Vv.tok_off + tok);
-    const int nterm = eos ? 1 : __ldg(Vv.tok_off + tok + 1) - off;
-    const uint8_t* bytes = Vv.tok_bytes + off;
-    const int xb = (!eos && lane < nterm) ? static_cast<int>(__ldg(bytes + lane)) : 256;
+    const int4 tr = __ldg(Vv.tok_rec + tok);
+    const int nterm = tr.y;
+    const uint8_t* bytes = Vv.tok_bytes + tr.x;
+    const int xb = TokLaneByte(tr, Vv.tok_bytes, lane, nterm, eos);
     for (int i = 0; i < nterm; ++i) {
       const int xs = __shfl_sync(0xffffffffu, xb, i & 31);
       const int x = eos ? 256 : (i < 32 ? xs : static_cast<int>(__ldg(bytes + i)));
@@ -963,8 +1021,11 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
         }
         bool match = c < ce && r.cond_len <= depth;
         bool far = false;  // condition entries outside the register window
+        // Entries 1..16 against the window, up to the longest live condition.
+        const int jmax = static_cast<int>(__reduce_max_sync(0xffffffffu, match ? static_cast<unsigned>(r.cond_len) : 1u));
 #pragma unroll
         for (int j = 1; j <= 16; ++j) {
+          if (j >= jmax) break;
           const int have = __shfl_sync(0xffffffffu, topv, j);
           if (j < r.cond_len) {
             if (j < wv) {
@@ -1067,7 +1128,7 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
     const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
     int kv = topv;
     if (n > wv) kv = lane < n ? stack[st.depth - 1 - lane] : 0;
-    const uint32_t mask = AssignSlotWarp(Cc, Bt, lookup_queue, b, st, Vv.nseg, kv, lane);
+    const uint32_t mask = AssignSlotWarp(Cc, Bt, lookup_queue, lookup_tag, b, st, Vv.nseg, kv, lane);
     if (lane == 0 && Bt.trace) TraceEvent(Bt, 21, b, 0, t_ph, 0), t_ph = NowNs();
     PublishHeavy(Bt, lookup_queue, lookup_tag, b, mask, Vv.nseg, lane, 32);
     if (lane == 0 && Bt.trace) TraceEvent(Bt, 22, b, 0, t_ph, 0), t_ph = NowNs();
@@ -1086,7 +1147,7 @@ __global__ void __launch_bounds__(128) LookupKernel(CacheView Cc, BatchView Bt, 
   int32_t key[kMaxContext];
   const int n = st.status == kAlive ? min(st.depth, Cc.K) : 0;
   for (int i = 0; i < n; ++i) key[i] = stack[st.depth - 1 - i];
-  const int flagged = AssignSlotKey(Cc, Bt, q, b, st, Bt.nseg, key);
+  const int flagged = AssignSlotKey(Cc, Bt, q, tag, b, st, Bt.nseg, key);
   PublishHeavy(Bt, q, tag, b, HeavyMask(Cc, flagged, Bt.nseg), Bt.nseg, 0, 1);
 }
 
@@ -1203,6 +1264,22 @@ __device__ __forceinline__ void CpAsync16(void* smem, const void* gmem) {
 __device__ __forceinline__ void CpAsyncCommit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void CpAsyncWait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+// Bulk (TMA) shared -> global copies: one instruction stores a whole span of
+// -inf from a CTA-shared source, L2 evict-first like the __stcs stores.
+__device__ __forceinline__ unsigned long long EvictFirstPolicy() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void BulkStore(void* gmem, const void* smem, int bytes, unsigned long long policy) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(gmem),
+               "r"(sa), "r"(bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void BulkCommit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void BulkWaitRead() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
 // Mixed chunks of a full span -> this lane's slots of a span buffer.
 __device__ __forceinline__ void SpanPrefetch(const uint16_t* row, int tw, uint32_t mword, int lane,
                                              uint4 (*buf)[32]) {
@@ -1317,7 +1394,8 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
   }
   if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
   if (lane == 0) Bt.seq_arrive[b] = 0;
-  AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, 1, F.produce, F.fill_no + 1, lane);
+  AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, 1, F.produce, F.fill_no + 1,
+             lane);
   if (lane == 0) TraceEvent(Bt, kTraceTail, b, 0, t_in, static_cast<unsigned long long>(tok + 1));
 }
 
@@ -1328,7 +1406,7 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
 template <int MODE, int TAIL>
 __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                           const BatchView& Bt, const FillArgs& F, int b, int seg, int slot,
-                                          int lane, uint4 (*span_buf)[4][32]) {
+                                          bool pure, int lane, uint4 (*span_buf)[4][32], const uint4* ninf) {
   const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   const int w0 = seg * kSegWords;
   const int nwords = min(Vv.W - w0, kSegWords);
@@ -1343,6 +1421,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   }
   uint32_t m[kSpans];
   int cd_cnt = 0;
+  int2 pc = make_int2(0, 0);  // pure: the slot's counts of this segment
   if (slot >= 0) {
     const uint32_t* src = slot < Cc.C ? Cc.ci + static_cast<long long>(slot) * Vv.W
                                       : Bt.priv + static_cast<long long>(slot - Cc.C) * Vv.W;
@@ -1351,7 +1430,11 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       const int w = 32 * i + lane;
       m[i] = w < nwords ? __ldcg(src + w0 + w) : 0u;
     }
-    if (slot < Cc.C) cd_cnt = __ldcg(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg);
+    if (pure) {
+      pc = __ldcg(reinterpret_cast<const int2*>(Cc.ci_cnt) + static_cast<long long>(slot) * Vv.nseg + seg);
+    } else if (slot < Cc.C) {
+      cd_cnt = __ldcg(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg);
+    }
   } else {
 #pragma unroll
     for (int i = 0; i < kSpans; ++i) m[i] = 0u;
@@ -1401,7 +1484,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     __syncwarp();  // the buffer is reused for logits chunks below
   }
 
-  // ---- bitmask words and sampler counts.
+  // ---- bitmask words and sampler counts (a pure item's are the slot's).
   const int eos_word = Vv.V >> 5;
   int ca = 0, cs = 0;
 #pragma unroll
@@ -1409,7 +1492,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     const int w = 32 * i + lane;
     if (w < nwords) {
       if (F.bitmask != nullptr) F.bitmask[static_cast<long long>(b) * F.ldw + w0 + w] = m[i];
-      if (F.seg_counts != nullptr) {
+      if (F.seg_counts != nullptr && !pure) {
         uint32_t mm = m[i];
         if (w0 + w == eos_word) mm &= ~(1u << (Vv.V & 31));
         ca += __popc(mm);
@@ -1418,8 +1501,13 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     }
   }
   if (F.seg_counts != nullptr) {
-    ca = WarpSum(ca);
-    cs = WarpSum(cs);
+    if (pure) {
+      ca = pc.x;
+      cs = pc.y;
+    } else {
+      ca = WarpSum(ca);
+      cs = WarpSum(cs);
+    }
     if (lane == 0) {
       F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 0] = ca;
       F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = cs;
@@ -1446,7 +1534,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   // ---- arrival (fused tail): mask words, counts and argmax partials are
   // made visible first; the bulk logits stores follow.
   bool last = false;
-  if (TAIL != kTailNone || F.publish_arrival) {
+  if (TAIL != kTailNone || F.publish_arrival == 1 || (F.publish_arrival == 2 && !pure)) {
     __threadfence();
     __syncwarp();
     int l = 0;
@@ -1455,26 +1543,57 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   }
   if (MODE == kFillMask && F.logits != nullptr) {
     uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
-    // Full spans, two in flight: the mixed chunks of spans i+1 and i+2 are
-    // being copied (cp.async, no registers held) while span i is blended and
-    // stored.  Then a partial last span, if any.
+    // Full spans by class: all allowed -> untouched; all masked -> one bulk
+    // (TMA) store of 2 KB of -inf from shared memory, issued by lane 0;
+    // mixed -> 16-B chunks, two spans in flight: the mixed chunks of the next
+    // two mixed spans are being copied (cp.async, no registers held) while
+    // one is blended and stored.  Then a partial last span, if any.
     const int nfull = F.vec_ok ? (t1 - t0) >> 10 : 0;
-    uint4(*buf)[4][32] = span_buf;  // [2][4][32] of this warp
-    if (nfull > 0) SpanPrefetch(row, t0, m[0], lane, buf[0]);
-    CpAsyncCommit();
-    if (nfull > 1) SpanPrefetch(row, t0 + 1024, m[1], lane, buf[1]);
-    CpAsyncCommit();
-#pragma unroll 1
+    uint32_t masked = 0u, mixed = 0u;
+#pragma unroll
     for (int i = 0; i < kSpans; ++i) {
+      const unsigned nz = __ballot_sync(0xffffffffu, m[i] != 0u);
+      const unsigned nf = __ballot_sync(0xffffffffu, m[i] != 0xffffffffu);
       if (i < nfull) {
-        CpAsyncWait1();  // span i's group is complete (only i+1's may pend)
-        SpanStore(row, t0 + 1024 * i, Pick(m, i), lane, buf[i & 1], &rd, &wr);
-        if (i + 2 < nfull) SpanPrefetch(row, t0 + 1024 * (i + 2), Pick(m, i + 2), lane, buf[i & 1]);
-        CpAsyncCommit();
-      } else if (t0 + 1024 * i < t1) {
-        MaskSpan(row, t0 + 1024 * i, t1, F.vec_ok, Pick(m, i), lane, &rd, &wr);
+        if (!nz && PRE3_BULK_MASKED) masked |= 1u << i;
+        else if (nf) mixed |= 1u << i;
       }
     }
+    if (masked && lane == 0) {
+      const unsigned long long pol = EvictFirstPolicy();
+      for (uint32_t x = masked; x; x &= x - 1) BulkStore(row + t0 + 1024 * (__ffs(x) - 1), ninf, 2048, pol);
+      BulkCommit();
+      wr += 2048ull * static_cast<unsigned>(__popc(masked));
+    }
+    uint4(*buf)[4][32] = span_buf;  // [2][4][32] of this warp
+    uint32_t pend = mixed;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (pend) {
+        const int i = __ffs(pend) - 1;
+        pend &= pend - 1;
+        SpanPrefetch(row, t0 + 1024 * i, Pick(m, i), lane, buf[q]);
+      }
+      CpAsyncCommit();
+    }
+    int q = 0;
+#pragma unroll 1
+    for (uint32_t todo = mixed; todo; todo &= todo - 1, q ^= 1) {
+      const int i = __ffs(todo) - 1;
+      CpAsyncWait1();  // this span's group is complete (only the next one's may pend)
+      SpanStore(row, t0 + 1024 * i, Pick(m, i), lane, buf[q], &rd, &wr);
+      if (pend) {
+        const int j = __ffs(pend) - 1;
+        pend &= pend - 1;
+        SpanPrefetch(row, t0 + 1024 * j, Pick(m, j), lane, buf[q]);
+      }
+      CpAsyncCommit();
+    }
+#pragma unroll 1
+    for (int i = nfull; i < kSpans; ++i) {
+      if (t0 + 1024 * i < t1) MaskSpan(row, t0 + 1024 * i, t1, F.vec_ok, Pick(m, i), lane, &rd, &wr);
+    }
+    if (masked && lane == 0) BulkWaitRead();  // the -inf source outlives the reads
   }
   if (Bt.stats_enabled) {
     rd = static_cast<unsigned long long>(WarpSum(static_cast<int>(rd)));
@@ -1514,11 +1633,12 @@ struct FillShared {
 // Every CTA first helps drain the build queue of new contexts (empty in the
 // steady state).
 template <int MODE, int TAIL>
-__global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+__global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                           FillArgs F) {
   PdlEnter();
   __shared__ FillShared sh;
   __shared__ uint4 span_buf[kWarps][2][4][32];  // light pass: per-warp double buffer of mixed chunks (32 KB)
+  __shared__ __align__(128) uint4 ninf_buf[128];  // 2 KB of bf16 -inf: the bulk-store source
   extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -1530,6 +1650,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     *R.next_unit = 0u;
     *R.n_heavy = 0u;
   }
+
   const BuildQueue Qc = QueueOf(Bt, F.consume);
   const int bid = static_cast<int>(blockIdx.x);
   const int tag = HeavyTag(F.fill_no, 0);
@@ -1537,14 +1658,23 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
 
   if (bid >= Bt.h_grid) {
     // ---- light pass.  Loads that only depend on (b, seg) are issued together.
+    if (MODE == kFillMask && F.logits != nullptr) {
+      if (tid < 128) {
+        ninf_buf[tid] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // visible to the bulk copies
+      }
+      __syncthreads();
+    }
     const int item = (bid - Bt.h_grid) * kWarps + warp;
     const bool in_range = item < Bt.B * Vv.nseg;
     const int b = in_range ? item / Vv.nseg : 0;
     const int seg = item - b * Vv.nseg;
     int hi = -1, slot = -2;
+    uint32_t hmask = ~0u;
     if (in_range) {
       hi = hidx[static_cast<long long>(b) * Vv.nseg + seg];
-      slot = Bt.seq_slot[b];
+      slot = SeqSlot(Bt, F.fill_no)[b];
+      hmask = SeqHmask(Bt, F.fill_no)[b];
     }
     const unsigned int n_items = LoadRelaxed(Qc.n_items);
     if (n_items != 0u) HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);  // CTA-uniform
@@ -1552,7 +1682,11 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
     // h_grid heavy CTAs cover (a longer list spills over to the light pass,
     // whose warps take the rare CD/wait paths themselves).
     if (!in_range || (hi >= 0 && (hi & ~0xffff) == tag && (hi & 0xffff) < Bt.h_grid)) return;
-    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, lane, span_buf[warp]);
+    // Pure CI: a built shared slot and no heavy segment — the mask is the CI
+    // row, the counts are the slot's (and with publish_arrival 2 nobody
+    // waits for this sequence's items).
+    const bool pure = hmask == 0u && slot >= 0 && slot < Cc.C && Vv.nseg <= 32;
+    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, lane, span_buf[warp], ninf_buf);
     return;
   }
 
@@ -1563,7 +1697,7 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
   const int b = hv.x;
   const int seg = hv.y;
   const int hi = hidx[static_cast<long long>(b) * Vv.nseg + seg];
-  int slot = Bt.seq_slot[b];
+  int slot = SeqSlot(Bt, F.fill_no)[b];
   const unsigned int n_items = LoadRelaxed(Qc.n_items);
   if (hi != (tag | bid)) return;
   const int w0 = seg * kSegWords;
@@ -1722,7 +1856,9 @@ __global__ void __launch_bounds__(kThreads, 4) FillKernel(AutView A, VocabView V
 // ---------------------------------------------------------------------------
 template <int SAMPLE>
 __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv, const CacheView& Cc,
-                                           const BatchView& Bt, const AcceptArgs& G, int b, int lane);
+                                           const BatchView& Bt, const AcceptArgs& G, int b, SeqState st, int topv,
+                                           const uint32_t* row, const int32_t* counts, int lane,
+                                           unsigned long long t_in);
 
 template <int SAMPLE>
 __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
@@ -1739,21 +1875,39 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
   const int lane = threadIdx.x & 31;
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b < Bt.B) {
-    if (G.wait_fill) {
+    // The sequence's state and stack window are not written by the fill:
+    // their loads overlap the wait for its items.
+    const SeqState st = Bt.seq[b];
+    const int topv = StackWindow(Bt, b, st.depth, lane);
+    const uint32_t* row = G.bitmask + static_cast<long long>(b) * G.ldw;
+    const int32_t* counts = G.seg_counts + static_cast<long long>(b) * Vv.nseg * 2;
+    bool pure = false;
+    if (G.ci_shortcut) {
+      // Pure CI (the fill's own test, LightItem): its bitmask row is the
+      // slot's CI row and its counts the slot's — sample from those now.
+      const int slot = SeqSlot(Bt, G.lookup_tag - 1)[b];
+      const uint32_t hm = SeqHmask(Bt, G.lookup_tag - 1)[b];
+      pure = hm == 0u && slot >= 0 && slot < Cc.C && Vv.nseg <= 32;
+      if (pure) {
+        row = Cc.ci + static_cast<long long>(slot) * Vv.W;
+        counts = Cc.ci_cnt + static_cast<long long>(slot) * Vv.nseg * 2;
+      }
+    }
+    if (G.wait_fill && !pure) {
       while (LoadAcquire(Bt.seq_arrive + b) < Vv.nseg) __nanosleep(64);
       __syncwarp();
       if (lane == 0) Bt.seq_arrive[b] = 0;
     }
-    AcceptBody<SAMPLE>(A, Vv, Cc, Bt, G, b, lane);
+    AcceptBody<SAMPLE>(A, Vv, Cc, Bt, G, b, st, topv, row, counts, lane, Bt.trace ? NowNs() : 0ull);
   }
   if (G.wait_fill) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
 template <int SAMPLE>
 __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv, const CacheView& Cc,
-                                           const BatchView& Bt, const AcceptArgs& G, int b, int lane) {
-  const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
-  SeqState st = Bt.seq[b];
+                                           const BatchView& Bt, const AcceptArgs& G, int b, SeqState st, int topv,
+                                           const uint32_t* row, const int32_t* counts, int lane,
+                                           unsigned long long t_in) {
   int tok = -1;
   if (SAMPLE == kSampleGiven) {
     tok = G.tokens[b];
@@ -1763,8 +1917,7 @@ __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv
     __syncwarp();
     if (lane == 0) G.best[b] = 0ull;
   } else {
-    tok = SampleStreamWarp(Vv, b, G.bitmask + static_cast<long long>(b) * G.ldw,
-                           G.seg_counts + static_cast<long long>(b) * Vv.nseg * 2, G.seed, st.draws, lane);
+    tok = SampleStreamWarp(Vv, b, row, counts, G.seed, st.draws, lane);
     st.draws += 1;
     if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
   }
@@ -1773,7 +1926,7 @@ __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv
     if (lane == 0) Bt.seq[b].draws = st.draws;
     return;
   }
-  AcceptWarp(A, Vv, Cc, Bt, b, st, tok, G.status_out, G.restart, G.lookup_queue, G.lookup_tag, lane);
+  AcceptWarp(A, Vv, Cc, Bt, b, st, topv, tok, G.status_out, G.restart, G.lookup_queue, G.lookup_tag, lane);
   if (lane == 0) TraceEvent(Bt, kTraceAccept, b, 0, t_in, static_cast<unsigned long long>(tok + 1));
 }
 
@@ -2115,7 +2268,8 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     st.draws += 1;
     if (S.tokens_out != nullptr && lane == 0) S.tokens_out[b] = tok;
     if (S.do_accept) {
-      AcceptWarp(A, Vv, Cc, Bt, b, st, tok, nullptr, S.restart, S.lookup_queue, S.lookup_tag, lane);
+      AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, S.restart, S.lookup_queue,
+                 S.lookup_tag, lane);
     } else if (lane == 0) {
       Bt.seq[b].draws = st.draws;
     }
@@ -2197,6 +2351,30 @@ cudaError_t LaunchAllowed(const AutView& a, const BatchView& b, uint32_t* out, c
 cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
   return Launch(ResetKernel, dim3((b.B + 127) / 128), dim3(128), 0, s, a, b);
+}
+
+// Structural counts of every built context (CacheView::ci_cnt[.][.][1]) after
+// the structural token set changed: one warp per (slot, segment).
+__global__ void __launch_bounds__(256) RecountStructuralKernel(CacheView Cc, VocabView Vv) {
+  const int lane = threadIdx.x & 31;
+  const long long units = static_cast<long long>(Cc.C) * Vv.nseg;
+  for (long long u = (blockIdx.x * 256ll + threadIdx.x) >> 5; u < units; u += (gridDim.x * 256ll) >> 5) {
+    const int slot = static_cast<int>(u / Vv.nseg), seg = static_cast<int>(u % Vv.nseg);
+    if (!(__ldcg(Cc.slot_meta + slot) & (1 << 16))) continue;
+    int cs = 0;
+    for (int w = seg * kSegWords + lane; w < min(Vv.W, (seg + 1) * kSegWords); w += 32) {
+      uint32_t a = __ldcg(Cc.ci + static_cast<long long>(slot) * Vv.W + w);
+      if (w == (Vv.V >> 5)) a &= ~(1u << (Vv.V & 31));
+      cs += __popc(a & Vv.structural[w]);
+    }
+    cs = WarpSum(cs);
+    if (lane == 0) Cc.ci_cnt[u * 2 + 1] = cs;
+  }
+}
+
+cudaError_t LaunchRecountStructural(const CacheView& c, const VocabView& v) {
+  RecountStructuralKernel<<<1184, 256>>>(c, v);
+  return cudaGetLastError();
 }
 
 cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s) {

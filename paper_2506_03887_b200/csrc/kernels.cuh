@@ -49,6 +49,7 @@ struct AutView {
 struct VocabView {
   const int32_t* tok_off;  // V+1 byte offsets
   const uint8_t* tok_bytes;
+  const int4* tok_rec;         // V+1: {offset, length, bytes 0-3, bytes 4-7} (entry V: EOS, length 1)
   const uint32_t* structural;  // W words
   int32_t V;                   // regular tokens; EOS = V
   int32_t W;                   // ceil((V+1)/32)
@@ -70,6 +71,7 @@ struct CacheView {
   int32_t* seg_done;              // C*nseg completed build units (kChunksPerSeg = built)
   int32_t* slot_built;            // C completed build units over all segments
   uint32_t* cd_segmask;           // C: bit s set when segment s has context-dependent tokens
+  int32_t* ci_cnt;                // C*nseg*2: per segment, CI tokens (EOS excluded) and CI ∩ structural
   int32_t* slot_parent;           // C: context a new one is built from (-1: full build)
   unsigned long long* counters;   // [0] slots, [1] segment builds, [2] private builds, [3] parent-based builds
   int32_t C;
@@ -96,8 +98,10 @@ struct BatchView {
   int32_t cap;
   int32_t B;
   int32_t nseg;
-  int32_t* seq_slot;        // B: cache slot, C+b = private row, -2 = not alive; | kSlotWait
-                            //    when the slot's build may still be pending
+  int32_t* seq_slot;        // [2][B] by fill parity: cache slot, C+b = private row, -2 = not alive;
+                            //    | kSlotWait when the slot's build may still be pending
+  uint32_t* seq_hmask;      // [2][B] by fill parity: the sequence's heavy segments (0: pure CI —
+                            //    its mask is the slot's CI row)
   uint32_t* priv;           // B*W private (uncached) masks
   int32_t* priv_done;       // B*nseg build-completion counters of private rows
   int32_t* heavy_index;     // B*nseg: index in the consumed heavy list, or -1
@@ -137,7 +141,9 @@ struct FillArgs {
   int reset;                // queue drained by the previous fill, emptied here (-1: none)
   int fill_no;              // this fill's number (heavy_index tags; the tail tags fill_no + 1)
   int publish_arrival;      // no tail: still count finished items per sequence (seq_arrive) so a
-                            // following AcceptKernel with wait_fill can start per sequence
+                            // following AcceptKernel with wait_fill can start per sequence;
+                            // 2: only sequences that are not pure CI (seq_hmask != 0; the
+                            // accept's ci_shortcut skips the others)
   int vec_ok;               // set by LaunchFill
 };
 
@@ -155,6 +161,8 @@ struct AcceptArgs {
   int lookup_queue;  // >= 0: assign next-fill context slots into this queue
   int lookup_tag;    // number of the fill that consumes it
   int wait_fill;     // overlap the preceding fill (publish_arrival): per-sequence start
+  int ci_shortcut;   // with wait_fill, bitmask/seg_counts from that fill, unmodified: a pure-CI
+                     // sequence samples from its slot's CI row and counts without waiting
 };
 
 struct SampleArgs {
@@ -181,6 +189,7 @@ cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s);
 // Engine::AllowedTerminals per sequence: out[b*9 .. b*9+8].
 cudaError_t LaunchAllowed(const AutView& a, const BatchView& b, uint32_t* out, cudaStream_t s);
 cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s);
+cudaError_t LaunchRecountStructural(const CacheView& c, const VocabView& v);
 cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,
                         cudaStream_t s);
 // Help-build + fill (+ bf16 -inf masking or greedy argmax) (+ fused tail).

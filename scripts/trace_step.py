@@ -17,12 +17,15 @@ import paper_2506_03887_b200 as pk  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--batch", type=int, default=256)
 p.add_argument("--fused", action="store_true")
+p.add_argument("--split", action="store_true", help="gm_decode_step_stream_split")
 p.add_argument("--grammar", default="json")
 p.add_argument("--flavor", type=int, default=0)
 p.add_argument("--parent", type=int, default=0)
 p.add_argument("--steps", type=int, default=3)
 p.add_argument("--k", type=int, default=12)
 p.add_argument("--slots", type=int, default=8192)
+p.add_argument("--no-logits", action="store_true", help="bitmask-only fill (no logits stream)")
+p.add_argument("--queue", action="store_true", help="spin the GPU first so the host enqueues the whole step before it starts (steady-state launch overlap)")
 a = p.parse_args()
 flat = bench.automaton_bytes(a.grammar)
 vocab = pk.synth_vocab(128255, a.flavor)
@@ -41,8 +44,11 @@ logits = [torch.randn((B, eng.V + 1), dtype=torch.bfloat16, device=dev) for _ in
 def step(i):
     if a.fused:
         batch.decode_step_stream(1, bitmask=bm, logits=logits[i % 3], tokens_out=toks)
+    elif a.split:
+        batch.decode_step_stream_split(1, bitmask=bm, logits=None if a.no_logits else logits[i % 3],
+                                       seg_counts=counts, tokens_out=toks)
     else:
-        batch.fill(bm, logits[i % 3], counts)
+        batch.fill(bm, None if a.no_logits else logits[i % 3], counts)
         batch.sample_stream_and_accept(bm, counts, 1, toks)
 
 
@@ -56,6 +62,8 @@ names = {1: "light", 2: "heavy", 3: "tail", 4: "accept", 5: "build", 10: "h:buil
 for s in range(a.steps):
     tr.zero_()
     batch.set_trace(tr)
+    if a.queue:
+        torch.cuda._sleep(400000)
     step(100 + s)
     torch.cuda.synchronize()
     batch.set_trace(None)
@@ -73,3 +81,7 @@ for s in range(a.steps):
         pct = lambda v: " ".join(f"{x:6.1f}" for x in np.percentile(v, [0, 50, 90, 99, 100]))
         print(f"  {names[int(k)]:7s} n={len(r):6d} start[p0 p50 p90 p99 max] {pct(st)} | dur {pct(du)} | end max {en.max():6.1f}"
               f" | extra sum {int(r[:, 3].sum())}")
+    if s == a.steps - 1:
+        lo = np.unique(rec[:, 1] % 1024)
+        print(f"  globaltimer granularity probe: {len(lo)} distinct values of t mod 1024 ns; min step "
+              f"{np.diff(np.unique(rec[:, 1])).min()} ns")

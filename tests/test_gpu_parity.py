@@ -99,9 +99,24 @@ def test_dead_and_accepted_rows_are_empty():
     assert np.all(np.isneginf(lgf[0])) and np.all(np.isneginf(lgf[1]))
 
 
+def host_seg_counts(eng, m, nseg):
+    """Per (sequence, segment) {allowed regular tokens, allowed structural
+    tokens} of bitmask rows m (EOS bit excluded): the fill's seg_counts."""
+    bits = np.unpackbits(m.view(np.uint8), axis=1, bitorder="little")[:, : eng.V + 1].astype(np.int64)
+    bits[:, eng.V] = 0
+    sbits = np.unpackbits(eng.structural.view(np.uint8), bitorder="little")[: eng.V + 1].astype(np.int64)
+    out = np.zeros((m.shape[0], nseg * 2), dtype=np.int64)
+    for s in range(nseg):
+        lo, hi = s * 8192, min(eng.V + 1, (s + 1) * 8192)
+        out[:, 2 * s] = bits[:, lo:hi].sum(1)
+        out[:, 2 * s + 1] = (bits[:, lo:hi] * sbits[lo:hi]).sum(1)
+    return out
+
+
 def run_stream(eng, B, steps, seed, cap=1024, check_logits=False, fused=False):
     """Device decode loop: fill (+logits) then stream-sample + accept, as two
-    API calls or (fused=True) one gm_decode_step_stream launch."""
+    API calls, (fused=True) one gm_decode_step_stream launch or
+    (fused="split") gm_decode_step_stream_split."""
     batch = eng.batch(B, cap)
     bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
     counts = torch.zeros((B, batch.nseg * 2), dtype=torch.int32, device=DEV)
@@ -112,13 +127,17 @@ def run_stream(eng, B, steps, seed, cap=1024, check_logits=False, fused=False):
         if lg is not None:
             lg.normal_()
             before = lg.clone()
-        if fused:
+        if fused == "split":
+            batch.decode_step_stream_split(seed, bitmask=bm, logits=lg, seg_counts=counts, tokens_out=toks)
+        elif fused:
             batch.decode_step_stream(seed, bitmask=bm, logits=lg, tokens_out=toks)
         else:
             batch.fill(bm, lg, counts)
             batch.sample_stream_and_accept(bm, counts, seed, toks)
         batch.check()
         m = bm.cpu().numpy().view(np.uint32).copy()
+        if fused in (False, "split"):
+            assert np.array_equal(counts.cpu().numpy(), host_seg_counts(eng, m, batch.nseg))
         masks.append(m)
         tokens.append(toks.cpu().numpy().copy())
         if lg is not None:
@@ -129,7 +148,7 @@ def run_stream(eng, B, steps, seed, cap=1024, check_logits=False, fused=False):
     return batch, np.stack(masks, 1), np.stack(tokens, 1)
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [False, True, "split"])
 def test_json32k_stream_matches_golden(vectors, fused):
     """Config 1 replayed on the GPU: every mask digest, token and the final
     stacks equal the reference's (golden)."""
@@ -146,7 +165,8 @@ def test_json32k_stream_matches_golden(vectors, fused):
         assert got.stack == fin["stack"] and got.status == fin["status"]
 
 
-@pytest.mark.parametrize("K,fused", [(2, False), (8, False), (12, True), (16, True), (16, False)])
+@pytest.mark.parametrize("K,fused", [(2, False), (8, False), (12, True), (16, True), (16, False), (2, "split"),
+                                     (12, "split"), (16, "split")])
 def test_json128k_stream_matches_port(K, fused):
     """Config 2 shape (JSON, 128,255 tokens): GPU decode loop == C port loop
     (tokens every step, final stacks) for 24 sequences x 16 steps."""
@@ -177,6 +197,8 @@ def test_cache_pressure_paths():
         _, _, tokens = run_stream(eng, B, steps, seed)
         assert np.array_equal(tokens, ptoks), slots
         _, _, tokens = run_stream(eng, B, steps, seed, fused=True)  # warm cache, second batch
+        assert np.array_equal(tokens, ptoks), slots
+        _, _, tokens = run_stream(eng, B, steps, seed, fused="split")
         assert np.array_equal(tokens, ptoks), slots
         if slots <= 4:
             assert eng.info()["private_builds"] > 0
@@ -291,7 +313,7 @@ def test_workload_grammar_stream_matches_port(name, flavor):
     eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=12)
     port = Port(f, vocab)
     B, steps, seed = 16, 12, 9
-    for fused in (False, True):
+    for fused in (False, True, "split"):
         batch, masks, tokens = run_stream(eng, B, steps, seed, fused=fused)
         _, ptoks, pstacks = port.decode_run(eng.structural, B, steps, seed, want_tokens=True, want_stacks=True)
         assert np.array_equal(tokens, ptoks), fused
@@ -410,3 +432,30 @@ def test_allowed_terminals_matches_port(vectors, name):
         want = port.allowed(pc) if c["status"] == 0 else (0, False)
         port.free(pc)
         assert got == want, (c["stack"], got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grammar,flavor,K", [("json", 0, 16), ("schema", 0, 16)])
+def test_split_step_large_batch(grammar, flavor, K):
+    """gm_decode_step_stream_split at a batch that fills several waves (the
+    accept kernel overlaps the fill and pure-CI sequences sample from the
+    context cache): tokens, masks and stacks equal the two-call loop's, and
+    the first 48 sequences' tokens equal the C port's."""
+    if grammar == "json":
+        f = flat("json")
+    else:
+        text = open(os.path.join(ROOT, "paper_2506_03887_b200", "grammars", grammar + ".bnf")).read()
+        f = pk.Automaton.compile(text).save()
+    vocab = pk.synth_vocab(128255, flavor)
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
+    eng.prewarm(512, 200, seed=0xC0FFEE)
+    B, steps, seed = 1024, 8, 13
+    b1, m1, t1 = run_stream(eng, B, steps, seed, fused="split", check_logits=True)
+    b2, m2, t2 = run_stream(eng, B, steps, seed)
+    assert np.array_equal(t1, t2)
+    assert np.array_equal(m1, m2)
+    for b in range(0, B, 37):
+        assert b1.get(b).stack == b2.get(b).stack
+    port = Port(f, vocab)
+    _, ptoks, _ = port.decode_run(eng.structural, 48, steps, seed, want_tokens=True)
+    assert np.array_equal(t1[:48], ptoks)
