@@ -19,6 +19,10 @@ struct gm_automaton {
   pre3::Automaton a;
 };
 
+#ifndef PRE3_HEAVY_PER_SM
+#define PRE3_HEAVY_PER_SM 2  // heavy-pass (and first builder) CTAs of a fill grid per SM
+#endif
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -465,7 +469,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
     v.build_grid = sms * 4;
-    v.h_grid = std::min(v.h_cap, 2 * sms);
+    v.h_grid = std::min(v.h_cap, PRE3_HEAVY_PER_SM * sms);
     b->seg_counts = DevAlloc<int32_t>(bn * 2, &b->owned);
     b->scratch_mask = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     b->best = DevAlloc<unsigned long long>(static_cast<size_t>(batch), &b->owned);

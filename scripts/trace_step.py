@@ -25,13 +25,14 @@ p.add_argument("--steps", type=int, default=3)
 p.add_argument("--k", type=int, default=12)
 p.add_argument("--slots", type=int, default=8192)
 p.add_argument("--no-logits", action="store_true", help="bitmask-only fill (no logits stream)")
+p.add_argument("--prewarm", type=int, default=2000)
 p.add_argument("--queue", action="store_true", help="spin the GPU first so the host enqueues the whole step before it starts (steady-state launch overlap)")
 a = p.parse_args()
 flat = bench.automaton_bytes(a.grammar)
 vocab = pk.synth_vocab(128255, a.flavor)
 eng = pk.DeviceEngine(pk.Automaton.load(flat), vocab, device=0, context_depth=a.k, context_slots=a.slots,
                       parent_depth=a.parent)
-eng.prewarm(1024, 2000, seed=0xC0FFEE)
+eng.prewarm(1024, a.prewarm, seed=0xC0FFEE)
 B = a.batch
 batch = eng.batch(B, 1024)
 dev = torch.device("cuda:0")
