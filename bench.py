@@ -46,7 +46,7 @@ CONFIGS = {
     3: dict(grammar="schema", flavor=0, batch=1024, mode="stream", scaling="weak", K=16, slots=16384,
             desc="config3: JSON-schema-derived LR(1) grammar (nested objects/arrays), 128256-bit vocab, "
                  "batch {b}/GPU, fused mask-fill + bf16 -inf logit masking + stream sample + accept_token"),
-    4: dict(grammar="sql", flavor=1, batch=4096, mode="stream", scaling="strong", K=20, slots=131072,
+    4: dict(grammar="sql", flavor=1, batch=4096, mode="stream", scaling="strong", K=20, slots=131072, R=6,
             desc="config4: SQL-subset LR(1) grammar, 128256-bit SQL-flavoured vocab, 4096 sequences in total "
                  "({b}/GPU), fused mask-fill + bf16 -inf logit masking + stream sample + accept_token"),
     5: dict(grammar="json", flavor=0, batch=512, mode="greedy", scaling="weak", K=12, slots=16384,
@@ -69,9 +69,9 @@ def parse(argv=None):
                    help="K: stack entries keying the context cache (default: the config's; SQL conditions pop up "
                         "to 34 entries, so config 4 keys deeper)")
     p.add_argument("--context-slots", type=int, default=None, help="context-cache hash table slots (power of two)")
-    p.add_argument("--parent-depth", type=int, default=0,
-                   help="R: new contexts are built from the context keyed R deep (0: engine default min(4, K-1); "
-                        "-1: full builds)")
+    p.add_argument("--parent-depth", type=int, default=None,
+                   help="R: new contexts are built from the context keyed R deep (default: the config's, else the "
+                        "engine default min(4, K-1); -1: full builds)")
     p.add_argument("--prewarm-steps", type=int, default=10000,
                    help="context-cache preprocessing: synthetic decode steps (other seed) before timing")
     p.add_argument("--prewarm-batch", type=int, default=1024)
@@ -80,6 +80,9 @@ def parse(argv=None):
     p.add_argument("--separate", action="store_true",
                    help="stream mode: two launches per step (fill+mask logits, then sample+accept; the default)")
     p.add_argument("--one-launch", action="store_true", help="stream mode: force the one-launch fused step")
+    p.add_argument("--sample-every", type=int, default=16,
+                   help="bracket the roofline kernel with events on every Nth timed step (diagnostics: a large N "
+                        "shows the step rate without the sampled steps)")
     p.add_argument("--fused", action="store_true", help=argparse.SUPPRESS)  # the default; kept for scripts
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -97,6 +100,8 @@ def parse(argv=None):
         a.context_depth = cfg["K"]
     if a.context_slots is None:
         a.context_slots = cfg["slots"]
+    if a.parent_depth is None:
+        a.parent_depth = cfg.get("R", 0)  # SQL: parents keyed 6 deep leave fewer tokens to re-walk
     a.batch_given = a.batch is not None
     return a
 
@@ -245,12 +250,12 @@ def workload_config(args, world, B):
     cfg = CONFIGS[args.config]
     return {"workload": cfg["desc"].format(b=B), "config_index": args.config, "grammar": args.grammar,
             "vocab_bits": args.vocab + 1, "batch_per_gpu": B, "global_batch": B * world,
-            "context_depth": args.context_depth, "mode": args.mode,
+            "context_depth": args.context_depth, "parent_depth": args.parent_depth, "mode": args.mode,
             "step": ("gm_decode_step_greedy (argmax fill + accept kernels)" if args.mode == "greedy" else
                      "gm_decode_step_stream (one launch)" if args.one_launch else
                      "gm_decode_step_stream_split (fill + overlapped sample/accept kernel: pure-CI sequences "
                      "sample from their cached context row at once, the rest as their fill items arrive); "
-                     "every 8th step as gm_fill_and_mask_logits + gm_sample_stream_and_accept with events "
+                     f"every {args.sample_every}th step as gm_fill_and_mask_logits + gm_sample_stream_and_accept with events "
                      "around the fill"),
             "context_slots": args.context_slots,
             "parallelism": f"dp{world} (sequence shards, no hot-path collective)"}
@@ -344,11 +349,11 @@ def main(argv=None):
         dist.barrier()
     torch.cuda.synchronize()
     K = args.steps
-    # The roofline kernel is bracketed by events on every 8th step only: an
+    # The roofline kernel is bracketed by events on every 16th step only: an
     # event between two launches stops the next kernel from starting under the
     # previous one's last wave (programmatic dependent launch), which the
     # other steps keep.
-    SAMPLE_EVERY = 8
+    SAMPLE_EVERY = max(1, args.sample_every)
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(0, K, SAMPLE_EVERY)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:

@@ -308,6 +308,16 @@ class DeviceEngine:
         _check(lib().gm_engine_set_structural(self._h, _ptr(self.structural)))
         self._single: Optional[Batch] = None
 
+    def set_structural(self, words: np.ndarray) -> None:
+        """Replaces the sampler's structural token set (W uint32 words; the EOS
+        bit is ignored); contexts built so far get their counts recomputed."""
+        w = np.ascontiguousarray(words, dtype=np.uint32)
+        if w.shape != (self.W,):
+            raise ValueError(f"structural words must have shape ({self.W},)")
+        _check(lib().gm_engine_set_structural(self._h, _ptr(w)))
+        self.structural = w.copy()
+        self.structural[self.V >> 5] &= np.uint32(~(1 << (self.V & 31)) & 0xFFFFFFFF)
+
     def info(self) -> dict:
         out = np.zeros(8, np.int64)
         _check(lib().gm_engine_info(self._h, _ptr(out)))

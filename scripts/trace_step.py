@@ -26,6 +26,7 @@ p.add_argument("--k", type=int, default=12)
 p.add_argument("--slots", type=int, default=8192)
 p.add_argument("--no-logits", action="store_true", help="bitmask-only fill (no logits stream)")
 p.add_argument("--prewarm", type=int, default=2000)
+p.add_argument("--chain", type=int, default=0, help="also trace N back-to-back steps")
 p.add_argument("--queue", action="store_true", help="spin the GPU first so the host enqueues the whole step before it starts (steady-state launch overlap)")
 a = p.parse_args()
 flat = bench.automaton_bytes(a.grammar)
@@ -86,3 +87,33 @@ for s in range(a.steps):
         lo = np.unique(rec[:, 1] % 1024)
         print(f"  globaltimer granularity probe: {len(lo)} distinct values of t mod 1024 ns; min step "
               f"{np.diff(np.unique(rec[:, 1])).min()} ns")
+
+if a.chain:
+    # Back-to-back steps (the bench's steady state): light-item start clusters
+    # mark the fills; per step, when its fill items start/end and when its
+    # accepts end.
+    tr.zero_()
+    batch.set_trace(tr)
+    torch.cuda._sleep(2000000)
+    for s in range(a.chain):
+        step(200 + s)
+    torch.cuda.synchronize()
+    batch.set_trace(None)
+    t = tr.cpu().numpy().view(np.uint64)
+    n = min(int(t[0]), cap)
+    rec = t[4:4 * (n + 1)].reshape(n, 4).astype(np.int64)
+    kind = rec[:, 0] & 0xff
+    t0 = rec[:, 1].min()
+    light = np.sort((rec[kind == 1, 1] - t0) / 1e3)
+    cuts = [0] + [i + 1 for i in range(len(light) - 1) if light[i + 1] - light[i] > 3.0] + [len(light)]
+    acc_end = np.sort((rec[kind == 4, 2] - t0) / 1e3)
+    lend = (rec[kind == 1, 2] - t0) / 1e3
+    lst = (rec[kind == 1, 1] - t0) / 1e3
+    print(f"chain of {a.chain} steps: {len(cuts) - 1} light clusters")
+    for k in range(len(cuts) - 1):
+        lo, hi = light[cuts[k]], light[cuts[k + 1] - 1]
+        sel = (lst >= lo) & (lst <= hi)
+        ae = acc_end[(acc_end > lo)]
+        print(f"  fill {k}: light start {lo:7.1f}..{hi:7.1f}  light end max {lend[sel].max():7.1f}  "
+              f"accepts ended by then: {int((acc_end <= lo).sum())}")
+    print("  accept end times (sorted, every 256th):", " ".join(f"{x:.1f}" for x in acc_end[::256]))

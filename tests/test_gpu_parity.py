@@ -459,3 +459,21 @@ def test_split_step_large_batch(grammar, flavor, K):
     port = Port(f, vocab)
     _, ptoks, _ = port.decode_run(eng.structural, 48, steps, seed, want_tokens=True)
     assert np.array_equal(t1[:48], ptoks)
+
+
+def test_structural_change_recounts_built_contexts():
+    """Changing the structural token set after contexts were built recounts
+    their per-segment counts (the split step samples pure-CI sequences from
+    them): the decode loop still equals the C port's under the new set."""
+    vocab = pk.synth_vocab(128255)
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=12)
+    eng.prewarm(256, 100, seed=3)
+    rng = np.random.default_rng(5)
+    words = rng.integers(0, 2**32, size=eng.W, dtype=np.uint64).astype(np.uint32) & eng.structural
+    eng.set_structural(words)
+    port = Port(f, vocab)
+    B, steps, seed = 32, 12, 21
+    _, _, tokens = run_stream(eng, B, steps, seed, fused="split")
+    _, ptoks, _ = port.decode_run(eng.structural, B, steps, seed, want_tokens=True)
+    assert np.array_equal(tokens, ptoks)
