@@ -1317,6 +1317,43 @@ __device__ __forceinline__ void SpanStore(uint16_t* row, int tw, uint32_t mword,
   }
 }
 
+// Chunks of a full span holding any allowed token -> this lane's slots of a
+// span buffer (greedy argmax).
+__device__ __forceinline__ void SpanPrefetchAllowed(const uint16_t* row, int tw, uint32_t mword, int lane,
+                                                    uint4 (*buf)[32]) {
+  uint32_t byte[4];
+  SpanBytes(mword, lane, byte);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (byte[k] != 0u) CpAsync16(&buf[k][lane], row + tw + (32 * k + lane) * 8);
+  }
+}
+
+// This lane's best allowed (key, token) of a full span prefetched by
+// SpanPrefetchAllowed (0 when none).
+__device__ __forceinline__ unsigned long long ArgmaxBuffered(int tw, uint32_t mword, int lane,
+                                                             const uint4 (*buf)[32], unsigned long long* rd) {
+  uint32_t byte[4];
+  SpanBytes(mword, lane, byte);
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (!byte[k]) continue;
+    const uint4 v = buf[k][lane];
+    const uint16_t* pv = reinterpret_cast<const uint16_t*>(&v);
+    const int tb = tw + (32 * k + lane) * 8;
+    *rd += 16;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if ((byte[k] >> j) & 1u) {
+        const unsigned long long p = GreedyKey(pv[j], tb + j);
+        mine = p > mine ? p : mine;
+      }
+    }
+  }
+  return mine;
+}
+
 // This lane's best allowed (key, token) of the span (0 when none).
 __device__ __forceinline__ unsigned long long ArgmaxSpan(const uint16_t* row, int tw, int t1, bool vec_ok,
                                                          uint32_t mword, int lane, unsigned long long* rd) {
@@ -1515,16 +1552,47 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   }
   unsigned long long rd = 0, wr = 0;
   if (MODE == kFillGreedy) {
+    // Argmax over the allowed entries: only 16-B chunks holding an allowed
+    // token are read, two spans in flight (cp.async into the warp's span
+    // buffer) so a span's round trip overlaps the previous span's compare.
     const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
     unsigned long long mine = 0;
-#pragma unroll 1
+    const int nfull = F.vec_ok ? (t1 - t0) >> 10 : 0;
+    uint32_t live = 0u;
+#pragma unroll
     for (int i = 0; i < kSpans; ++i) {
+      if (i < nfull && __ballot_sync(0xffffffffu, m[i] != 0u)) live |= 1u << i;
+    }
+    uint4(*buf)[4][32] = span_buf;
+    uint32_t pend = live;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (pend) {
+        const int i = __ffs(pend) - 1;
+        pend &= pend - 1;
+        SpanPrefetchAllowed(row, t0 + 1024 * i, Pick(m, i), lane, buf[q]);
+      }
+      CpAsyncCommit();
+    }
+    int q = 0;
+#pragma unroll 1
+    for (uint32_t todo = live; todo; todo &= todo - 1, q ^= 1) {
+      const int i = __ffs(todo) - 1;
+      CpAsyncWait1();
+      const unsigned long long p = ArgmaxBuffered(t0 + 1024 * i, Pick(m, i), lane, buf[q], &rd);
+      mine = p > mine ? p : mine;
+      if (pend) {
+        const int j = __ffs(pend) - 1;
+        pend &= pend - 1;
+        SpanPrefetchAllowed(row, t0 + 1024 * j, Pick(m, j), lane, buf[q]);
+      }
+      CpAsyncCommit();
+    }
+#pragma unroll 1
+    for (int i = nfull; i < kSpans; ++i) {
       const int tw = t0 + 1024 * i;
       if (tw >= t1) break;
-      uint32_t mi = 0u;
-#pragma unroll
-      for (int k = 0; k < kSpans; ++k) mi = k == i ? m[k] : mi;
-      const unsigned long long p = ArgmaxSpan(row, tw, t1, F.vec_ok, mi, lane, &rd);
+      const unsigned long long p = ArgmaxSpan(row, tw, t1, F.vec_ok, Pick(m, i), lane, &rd);
       mine = p > mine ? p : mine;
     }
     mine = WarpMax64(mine);

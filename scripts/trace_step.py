@@ -18,6 +18,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--batch", type=int, default=256)
 p.add_argument("--fused", action="store_true")
 p.add_argument("--split", action="store_true", help="gm_decode_step_stream_split")
+p.add_argument("--greedy", action="store_true", help="gm_decode_step_greedy")
 p.add_argument("--grammar", default="json")
 p.add_argument("--flavor", type=int, default=0)
 p.add_argument("--parent", type=int, default=0)
@@ -44,7 +45,9 @@ logits = [torch.randn((B, eng.V + 1), dtype=torch.bfloat16, device=dev) for _ in
 
 
 def step(i):
-    if a.fused:
+    if a.greedy:
+        batch.decode_step_greedy(logits[i % 3], tokens_out=toks, bitmask=bm)
+    elif a.fused:
         batch.decode_step_stream(1, bitmask=bm, logits=logits[i % 3], tokens_out=toks)
     elif a.split:
         batch.decode_step_stream_split(1, bitmask=bm, logits=None if a.no_logits else logits[i % 3],
