@@ -477,3 +477,57 @@ def test_structural_change_recounts_built_contexts():
     _, _, tokens = run_stream(eng, B, steps, seed, fused="split")
     _, ptoks, _ = port.decode_run(eng.structural, B, steps, seed, want_tokens=True)
     assert np.array_equal(tokens, ptoks)
+
+
+def _random_grammar(rng):
+    """Same generator as test_compiler.py's differential fuzzing: small
+    grammars over the terminals a b c ( ) , with epsilon rules, recursion
+    and conflicts (the ones that do not compile are skipped)."""
+    names = ["A", "B", "C", "D", "E"][: rng.randint(1, 5)]
+    lines = []
+    for n in names:
+        alts = []
+        for _ in range(rng.randint(1, 3)):
+            syms = []
+            for _ in range(rng.randint(0, 4)):
+                if rng.random() < 0.45:
+                    syms.append(rng.choice(names))
+                else:
+                    syms.append('"' + rng.choice("abc(),") + '"')
+            alts.append(" ".join(syms))
+        lines.append(n + " -> " + " | ".join(alts))
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_grammars_decode_matches_port(seed):
+    """Random grammars compiled by our compiler, a vocabulary of every string
+    of 1-3 characters over the grammar's alphabet (258 tokens): the device
+    decode loop in all three step forms, with context keys 1 and 3 deep (so
+    context-dependent walks are common), equals the C port's — tokens every
+    step, final stacks and statuses."""
+    import itertools
+    rng = random.Random(7000 + seed)
+    alphabet = [bytes([c]) for c in b"abc(),"]
+    vocab = [b"".join(p) for n in (1, 2, 3) for p in itertools.product(alphabet, repeat=n)]
+    done = 0
+    while done < 12:
+        text = _random_grammar(rng)
+        try:
+            a = pk.Automaton.compile(text)
+        except pk.GmError:
+            continue
+        f = a.save()
+        port = Port(f, vocab)
+        B, steps, s = 8, 12, rng.randrange(1 << 30)
+        for K in (1, 3):
+            eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
+            _, ptoks, pstacks = port.decode_run(eng.structural, B, steps, s, want_tokens=True, want_stacks=True)
+            for mode in (False, True, "split"):
+                batch, _, tokens = run_stream(eng, B, steps, s, fused=mode, check_logits=True)
+                assert np.array_equal(tokens, ptoks), (text, K, mode)
+                for b in range(B):
+                    d = pstacks[b, 0]
+                    got = batch.get(b)
+                    assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1], (text, K, mode)
+        done += 1
