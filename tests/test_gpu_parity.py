@@ -531,3 +531,35 @@ def test_random_grammars_decode_matches_port(seed):
                     got = batch.get(b)
                     assert got.stack == pstacks[b, 2:2 + d].tolist() and got.status == pstacks[b, 1], (text, K, mode)
         done += 1
+
+
+@pytest.mark.parametrize("grammar,flavor,K,B", [("json", 0, 16, 1024), ("sql", 1, 20, 2048)])
+def test_split_step_soak_matches_two_call_loop(grammar, flavor, K, B):
+    """Race check of the overlapped split step (the accept kernel runs under
+    the fill; pure-CI sequences sample from the context cache while the fill
+    writes their bitmask rows): 400 steps of B sequences give the same token
+    every step as the serial two-call loop on the same engine."""
+    if grammar == "json":
+        f = flat("json")
+    else:
+        text = open(os.path.join(ROOT, "paper_2506_03887_b200", "grammars", grammar + ".bnf")).read()
+        f = pk.Automaton.compile(text).save()
+    vocab = pk.synth_vocab(128255, flavor)
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K, context_slots=1 << 17)
+    steps, seed = 400, 77
+    runs = []
+    for split in (True, False):
+        batch = eng.batch(B, 1024)
+        bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
+        counts = torch.zeros((B, batch.nseg * 2), dtype=torch.int32, device=DEV)
+        lg = torch.randn((B, eng.V + 1), dtype=torch.bfloat16, device=DEV)
+        toks = torch.zeros((steps, B), dtype=torch.int32, device=DEV)
+        for s in range(steps):
+            if split:
+                batch.decode_step_stream_split(seed, bitmask=bm, logits=lg, seg_counts=counts, tokens_out=toks[s])
+            else:
+                batch.fill(bm, lg, counts)
+                batch.sample_stream_and_accept(bm, counts, seed, toks[s])
+        batch.check()
+        runs.append(toks.cpu().numpy())
+    assert np.array_equal(runs[0], runs[1])
