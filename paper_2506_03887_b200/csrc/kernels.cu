@@ -1677,7 +1677,17 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     }
   }
   if (lane == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
-  if (lane == 0) TraceEvent(Bt, kTraceLight, b, seg, t_in, static_cast<unsigned long long>(n_walks));
+  if (Bt.trace) {
+    // extra: walks | SM id << 32 | the warp's logits bytes << 40 (diagnostics)
+    const unsigned bytes = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(rd + wr));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (lane == 0) {
+      TraceEvent(Bt, kTraceLight, b, seg, t_in,
+                 static_cast<unsigned long long>(n_walks & 0xffffffff) | (static_cast<unsigned long long>(smid) << 32) |
+                     (static_cast<unsigned long long>(bytes) << 40));
+    }
+  }
   if (TAIL != kTailNone && last) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
 }
 

@@ -28,6 +28,7 @@ p.add_argument("--slots", type=int, default=8192)
 p.add_argument("--no-logits", action="store_true", help="bitmask-only fill (no logits stream)")
 p.add_argument("--prewarm", type=int, default=2000)
 p.add_argument("--chain", type=int, default=0, help="also trace N back-to-back steps")
+p.add_argument("--per-sm", action="store_true", help="per-SM summary of the last traced step")
 p.add_argument("--queue", action="store_true", help="spin the GPU first so the host enqueues the whole step before it starts (steady-state launch overlap)")
 a = p.parse_args()
 flat = bench.automaton_bytes(a.grammar)
@@ -120,3 +121,22 @@ if a.chain:
         print(f"  fill {k}: light start {lo:7.1f}..{hi:7.1f}  light end max {lend[sel].max():7.1f}  "
               f"accepts ended by then: {int((acc_end <= lo).sum())}")
     print("  accept end times (sorted, every 256th):", " ".join(f"{x:.1f}" for x in acc_end[::256]))
+
+if a.per_sm:
+    # Per-SM view of the last traced step's light items (extra = walks |
+    # smid << 32 | bytes << 40): items, bytes and last end per SM.
+    light = rec[kind == 1]
+    sm = (light[:, 3] >> 32) & 0xff
+    by = light[:, 3] >> 40
+    end = (light[:, 2] - t0) / 1e3
+    rows = []
+    for k in np.unique(sm):
+        sel = sm == k
+        rows.append((end[sel].max(), int(sel.sum()), int(by[sel].sum()), int(k)))
+    rows.sort()
+    arr = np.array(rows)
+    print(f"per-SM light: {len(rows)} SMs; items/SM min {arr[:,1].min()} max {arr[:,1].max()}; "
+          f"KB/SM min {arr[:,2].min()/1e3:.0f} max {arr[:,2].max()/1e3:.0f}; end min {arr[:,0].min():.1f} max {arr[:,0].max():.1f} us")
+    for q in (0, len(rows) // 4, len(rows) // 2, 3 * len(rows) // 4, len(rows) - 1):
+        e, n_i, b_, k = rows[q]
+        print(f"  SM {k:3d}: end {e:6.1f} us  items {n_i:3d}  {b_/1e3:7.0f} KB  -> {b_/max(e,1e-3)/1e3:6.1f} GB/s")
