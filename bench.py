@@ -46,7 +46,8 @@ CONFIGS = {
     3: dict(grammar="schema", flavor=0, batch=1024, mode="stream", scaling="weak", K=16, slots=16384,
             desc="config3: JSON-schema-derived LR(1) grammar (nested objects/arrays), 128256-bit vocab, "
                  "batch {b}/GPU, fused mask-fill + bf16 -inf logit masking + stream sample + accept_token"),
-    4: dict(grammar="sql", flavor=1, batch=4096, mode="stream", scaling="strong", K=20, slots=131072, R=6,
+    4: dict(grammar="sql", flavor=1, batch=4096, mode="stream", scaling="strong", K=20, slots=262144, R=6,
+            prewarm=30000,
             desc="config4: SQL-subset LR(1) grammar, 128256-bit SQL-flavoured vocab, 4096 sequences in total "
                  "({b}/GPU), fused mask-fill + bf16 -inf logit masking + stream sample + accept_token"),
     5: dict(grammar="json", flavor=0, batch=512, mode="greedy", scaling="weak", K=12, slots=16384,
@@ -72,8 +73,9 @@ def parse(argv=None):
     p.add_argument("--parent-depth", type=int, default=None,
                    help="R: new contexts are built from the context keyed R deep (default: the config's, else the "
                         "engine default min(4, K-1); -1: full builds)")
-    p.add_argument("--prewarm-steps", type=int, default=10000,
-                   help="context-cache preprocessing: synthetic decode steps (other seed) before timing")
+    p.add_argument("--prewarm-steps", type=int, default=None,
+                   help="context-cache preprocessing: synthetic decode steps (other seed) before timing (default: "
+                        "the config's — 10,000; 30,000 for SQL, whose context space is ~6x JSON's)")
     p.add_argument("--prewarm-batch", type=int, default=1024)
     p.add_argument("--stack-cap", type=int, default=1024)
     p.add_argument("--seed", type=int, default=1)
@@ -100,6 +102,8 @@ def parse(argv=None):
         a.context_depth = cfg["K"]
     if a.context_slots is None:
         a.context_slots = cfg["slots"]
+    if a.prewarm_steps is None:
+        a.prewarm_steps = cfg.get("prewarm", 10000)
     if a.parent_depth is None:
         a.parent_depth = cfg.get("R", 0)  # SQL: parents keyed 6 deep leave fewer tokens to re-walk
     a.batch_given = a.batch is not None
