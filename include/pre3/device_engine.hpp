@@ -15,6 +15,14 @@
 
 #include "pre3_gmask.h"
 
+// The single-sequence calls below (ComputeMask, AllowedTerminals,
+// AcceptToken) move one configuration through device memory; they are
+// available when the CUDA runtime headers are on the include path.
+#if __has_include(<cuda_runtime.h>)
+#include <cuda_runtime.h>
+#define PRE3_DEVICE_ENGINE_SINGLE 1
+#endif
+
 namespace pre3 {
 
 class DeviceError : public std::runtime_error {
@@ -55,6 +63,9 @@ class DeviceEngine {
     num_tokens_ = static_cast<int32_t>(vocab.size());
   }
   ~DeviceEngine() {
+#ifdef PRE3_DEVICE_ENGINE_SINGLE
+    if (dev_words_) cudaFree(dev_words_);
+#endif
     if (one_) gm_batch_destroy(one_);
     if (engine_) gm_engine_destroy(engine_);
     if (automaton_) gm_automaton_destroy(automaton_);
@@ -83,7 +94,67 @@ class DeviceEngine {
     return b;
   }
 
+#ifdef PRE3_DEVICE_ENGINE_SINGLE
+  // Engine::ComputeMask (runtime.cpp:280-287) for one configuration: V+1
+  // bits in 32-bit words (bit t of word t/32; bit V = EOS), the reference's
+  // TokenMask layout.  Runs the CUDA fill on a batch of one.
+  std::vector<uint32_t> ComputeMask(const RuntimeConfig& cfg) {
+    Load(cfg);
+    const int32_t W = mask_words();
+    Check(gm_fill_next_token_bitmask(one_, dev_words_, W, nullptr));
+    Check(gm_batch_check(one_, nullptr));
+    std::vector<uint32_t> out(static_cast<size_t>(W));
+    CudaCheck(cudaMemcpy(out.data(), dev_words_, out.size() * 4, cudaMemcpyDeviceToHost));
+    return out;
+  }
+
+  // Engine::AllowedTerminals (runtime.cpp:188-208): the 256-bit next-byte set
+  // (4 x u64) and the end-marker flag.
+  std::pair<std::vector<uint64_t>, bool> AllowedTerminals(const RuntimeConfig& cfg) {
+    Load(cfg);
+    Check(gm_allowed_terminals(one_, dev_words_, nullptr));
+    uint32_t w[9];
+    CudaCheck(cudaMemcpy(w, dev_words_, sizeof(w), cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> set(4);
+    for (int i = 0; i < 4; ++i) set[i] = static_cast<uint64_t>(w[2 * i]) | (static_cast<uint64_t>(w[2 * i + 1]) << 32);
+    return {set, (w[8] & 1u) != 0};
+  }
+
+  // Engine::Step over every byte of `token` (EOS = id V), like the
+  // reference callers' loop (tools/gmask_main.cpp:113-118); returns the new
+  // configuration (status Dead when a byte has no edge).
+  RuntimeConfig AcceptToken(const RuntimeConfig& cfg, int32_t token) {
+    Load(cfg);
+    CudaCheck(cudaMemcpy(dev_words_, &token, 4, cudaMemcpyHostToDevice));
+    Check(gm_accept_tokens(one_, reinterpret_cast<const int32_t*>(dev_words_), nullptr, 0, nullptr));
+    Check(gm_batch_check(one_, nullptr));
+    RuntimeConfig out;
+    out.stack.resize(static_cast<size_t>(capacity_));
+    int32_t depth = 0;
+    Check(gm_batch_download(one_, 0, &out.state, &out.status, out.stack.data(), capacity_, &depth));
+    out.stack.resize(static_cast<size_t>(depth));
+    return out;
+  }
+#endif
+
  private:
+#ifdef PRE3_DEVICE_ENGINE_SINGLE
+  static void CudaCheck(cudaError_t e) {
+    if (e != cudaSuccess) throw DeviceError(GM_ERR_CUDA, cudaGetErrorString(e));
+  }
+  // Batch of one holding `cfg`, and a device scratch of max(W, 9) words.
+  void Load(const RuntimeConfig& cfg) {
+    if (!one_) {
+      Check(gm_batch_create(engine_, 1, capacity_, &one_));
+      const size_t words = static_cast<size_t>(mask_words() > 9 ? mask_words() : 9);
+      CudaCheck(cudaMalloc(reinterpret_cast<void**>(&dev_words_), words * 4));
+    }
+    Check(gm_batch_upload(one_, 0, cfg.status, cfg.stack.data(), static_cast<int32_t>(cfg.stack.size())));
+  }
+  uint32_t* dev_words_ = nullptr;
+  int32_t capacity_ = 1024;
+#endif
+
   gm_automaton* automaton_ = nullptr;
   gm_engine* engine_ = nullptr;
   gm_batch* one_ = nullptr;

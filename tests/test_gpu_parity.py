@@ -563,3 +563,39 @@ def test_split_step_soak_matches_two_call_loop(grammar, flavor, K, B):
         batch.check()
         runs.append(toks.cpu().numpy())
     assert np.array_equal(runs[0], runs[1])
+
+
+def test_cpp_device_engine_known_answers(vectors, tmp_path):
+    """The reference-side C++ binding (include/pre3/device_engine.hpp:
+    InitialConfig / AcceptToken / ComputeMask / AllowedTerminals on the GPU)
+    reproduces the reference's paren known answers (test_runtime.cpp:184-206:
+    masks b2, 40, eos-only) and the C port's stacks, built with g++ against
+    the C ABI."""
+    import subprocess
+    lib_dir = os.path.join(ROOT, "paper_2506_03887_b200")
+    exe = tmp_path / "engine_cli"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                    os.path.join(ROOT, "tests", "cpp", "engine_cli.cpp"), "-o", str(exe), "-L", lib_dir,
+                    "-lpre3gmask", f"-Wl,-rpath,{lib_dir}", "-L/usr/local/cuda/lib64", "-lcudart",
+                    "-Wl,-rpath,/usr/local/cuda/lib64"], check=True)
+    vocab = vectors["paren7"]["vocab"]
+    prefixes = [""] + sorted(vectors["paren7"]["masks"])
+    lines = [" ".join(str(vocab.index(c)) for c in p) for p in prefixes]
+    path = tmp_path / "paren.p3dpda"
+    path.write_bytes(flat("paren"))
+    out = subprocess.run([str(exe), str(path)] + vocab, input="\n".join(lines) + "\n", capture_output=True,
+                         text=True, check=True).stdout.splitlines()
+    assert len(out) == len(prefixes)
+    port = Port(flat("paren"), [t.encode() for t in vocab])
+    for p, row in zip(prefixes, out):
+        f = row.split()
+        words = np.array([int(x, 16) for x in f[1:f.index("eos")]], dtype=np.uint32)
+        want = "b2" if p == "" else vectors["paren7"]["masks"][p]["hex"]
+        assert mask_hex(words, 7) == want, p
+        assert int(f[f.index("eos") + 1]) == int(words[0] >> 7 & 1), p
+        c = port.initial()
+        for ch in p:
+            port.accept_token(c, vocab.index(ch))
+        _, status, stack = port.get(c)
+        assert int(f[f.index("status") + 1]) == status, p
+        assert [int(x) for x in f[f.index("stack") + 1:]] == stack, p
