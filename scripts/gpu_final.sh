@@ -13,3 +13,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 10100 -
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:FillKernel -s 10040 -c 1 -o $F/c2_fill -f python bench.py --steps 10 --warmup 40 --no-e2e --no-cpu-baseline --no-north-star > $F/c2_full.log 2>&1; echo "c2 full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:FillKernel -s 10040 -c 1 -o $F/c3_fill -f python bench.py --config 3 --steps 10 --warmup 40 --no-e2e --no-cpu-baseline > $F/c3_full.log 2>&1; echo "c3 full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:FillKernel -s 10040 -c 1 -o $F/json1024_fill -f python bench.py --batch 1024 --steps 10 --warmup 40 --no-e2e --no-cpu-baseline > $F/j1024_full.log 2>&1; echo "j1024 full rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:FillKernelILi0ELi0E -s 40 -c 1 -o $F/c4_fill -f python bench.py --config 4 --steps 10 --warmup 40 --no-e2e --no-cpu-baseline > $F/c4_full.log 2>&1; echo "c4 full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:FillKernelILi1ELi0E -s 40 -c 1 -o $F/c5_fill -f python bench.py --config 5 --steps 10 --warmup 40 --no-e2e --no-cpu-baseline > $F/c5_full.log 2>&1; echo "c5 full rc=$?"

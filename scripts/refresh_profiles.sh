@@ -12,7 +12,7 @@ for c in c2 c3; do
   cp $F/${c}_launches.csv $P/${R}_${c}_launches.csv
   python scripts/launches.py $F/${c}_launches.csv > $P/${R}_${c}_launches_summary.txt
 done
-for r in c2_fill c3_fill json1024_fill; do
+for r in c2_fill c3_fill json1024_fill c4_fill c5_fill; do
   (python scripts/ncu_summary.py $F/$r.ncu-rep 2>/dev/null; echo; echo "stall reasons:";
    ncu -i $F/$r.ncu-rep --page raw --csv 2>/dev/null | python -c "
 import csv,sys
@@ -41,6 +41,8 @@ t = {
  "json:128255:256:stream:separate": {"dram_bytes_per_launch": dram(F + "/c2_fill.ncu-rep"), "source": "ncu --set full, FillKernel<0,0> (profiles/r01_c2_fill_summary.txt)", "note": "at 256 sequences the masked logits (63 MB) mostly stay dirty in the 126 MB L2 when the kernel ends; their write-back is not attributed to the launch, so DRAM writes under-count"},
  "schema:128255:1024:stream:separate": {"dram_bytes_per_launch": dram(F + "/c3_fill.ncu-rep"), "source": "ncu --set full, FillKernel<0,0> (profiles/r01_c3_fill_summary.txt)"},
  "json:128255:1024:stream:separate": {"dram_bytes_per_launch": dram(F + "/json1024_fill.ncu-rep"), "source": "ncu --set full, FillKernel<0,0> (profiles/r01_json1024_fill_summary.txt)"},
+ "sql:128255:4096:stream:separate": {"dram_bytes_per_launch": dram(F + "/c4_fill.ncu-rep"), "source": "ncu --set full, FillKernel<0,0> (profiles/r01_c4_fill_summary.txt)"},
+ "json:128255:512:greedy:fused": {"dram_bytes_per_launch": dram(F + "/c5_fill.ncu-rep"), "source": "ncu --set full, FillKernel<1,0> (profiles/r01_c5_fill_summary.txt)", "note": "greedy reads only the 16-B logit chunks holding allowed tokens"},
 }
 json.dump(t, open("profiles/traffic.json", "w"), indent=1)
 print(t)
