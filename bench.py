@@ -259,8 +259,8 @@ def workload_config(args, world, B):
                      "gm_decode_step_stream (one launch)" if args.one_launch else
                      "gm_decode_step_stream_split (fill + overlapped sample/accept kernel: pure-CI sequences "
                      "sample from their cached context row at once, the rest as their fill items arrive); "
-                     f"every {args.sample_every}th step as gm_fill_and_mask_logits + gm_sample_stream_and_accept with events "
-                     "around the fill"),
+                     f"every {args.sample_every}th step with events around its fill kernel (no overlap "
+                     "in that step)"),
             "context_slots": args.context_slots,
             "parallelism": f"dp{world} (sequence shards, no hot-path collective)"}
 
@@ -359,18 +359,21 @@ def main(argv=None):
     # other steps keep.
     SAMPLE_EVERY = max(1, args.sample_every)
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(0, K, SAMPLE_EVERY)]
+    for pair in ev:  # create the CUDA events (their handles go through the C ABI)
+        for e_ in pair:
+            e_.record(stream)
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         h0 = time.perf_counter()
         e0.record(stream)
         for i in range(K):
             timed = i % SAMPLE_EVERY == 0
-            if timed:
+            if timed and not separate:
                 ev[i // SAMPLE_EVERY][0].record(stream)
-            if separate and timed:  # events bracket the fill kernel alone (the roofline kernel)
-                batch.fill(bm, logits[i % R], counts)
-                ev[i // SAMPLE_EVERY][1].record(stream)
-                batch.sample_stream_and_accept(bm, counts, seed, toks)
+            if separate and timed:  # events bracket the step's fill kernel alone (the roofline kernel)
+                batch.decode_step_stream_split(seed, bitmask=bm, logits=logits[i % R], seg_counts=counts,
+                                               tokens_out=toks, fill_events=ev[i // SAMPLE_EVERY])
             else:
                 step(i)
                 if timed:
@@ -406,14 +409,16 @@ def main(argv=None):
         torch.cuda.synchronize()
         Kn = 120
         evn = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(0, Kn, 8)]
+        for pair in evn:
+            for e_ in pair:
+                e_.record(stream)
+        torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for i in range(Kn):
             if i % 8 == 0:
-                evn[i // 8][0].record(stream)
-                bn.fill(bmn, lgn[i % Rn], cn)
-                evn[i // 8][1].record(stream)
-                bn.sample_stream_and_accept(bmn, cn, seed, tn)
+                bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn,
+                                            fill_events=evn[i // 8])
             else:
                 bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn)
         f1.record(stream)
@@ -422,8 +427,7 @@ def main(argv=None):
         fill_ms_n = sum(a.elapsed_time(c) for a, c in evn) / len(evn)
         pk_gbs, _, _ = peaks()
         ach_n = Bn * (2 * V1 + 8 * W) / (fill_ms_n / 1e3) / 1e9
-        north = {"batch": Bn, "step": "gm_decode_step_stream_split (every 8th step: fill + sample/accept with "
-                 "events around the fill)",
+        north = {"batch": Bn, "step": "gm_decode_step_stream_split (every 8th step with events around its fill)",
                  "fill_kernel_us": 1e3 * fill_ms_n, "achieved_gbs": ach_n, "frac": ach_n / pk_gbs,
                  "seq_steps_per_s": Bn * Kn / (f0.elapsed_time(f1) / 1e3), "steps": Kn}
         del bn, lgn

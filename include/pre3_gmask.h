@@ -177,7 +177,7 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
  * gm_fill_and_mask_logits. */
 int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
                                 int64_t ld, int32_t* seg_counts, uint64_t seed, int32_t* tokens_out,
-                                void* stream);
+                                void* stream, void* fill_start_event, void* fill_end_event);
 
 /* Engine::AllowedTerminals (runtime.cpp:188-208) for every sequence: the
  * exact next-byte set plus $ — terminal t is allowed iff an edge of the

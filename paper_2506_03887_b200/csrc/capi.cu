@@ -660,7 +660,8 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
 // pure-CI sequence from its slot's CI row and counts (the fill writes the same
 // words and counts into bitmask/seg_counts) without waiting for the fill.
 int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits, int64_t ld,
-                                int32_t* seg_counts, uint64_t seed, int32_t* tokens_out, void* stream) {
+                                int32_t* seg_counts, uint64_t seed, int32_t* tokens_out, void* stream,
+                                void* fill_start_event, void* fill_end_event) {
   return Guard([&]() -> int {
     if (!b) return Fail(GM_ERR_USAGE, "null batch");
     gm_engine* e = b->engine;
@@ -679,8 +680,12 @@ int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words
     f.publish_arrival = 2;
     b->ClearArrivals(s);
     b->BeginFill(&f);
+    // Optional events around the fill alone (measurement; the accept then
+    // cannot start under the fill for this step).
+    if (fill_start_event) Check(cudaEventRecord(static_cast<cudaEvent_t>(fill_start_event), s), "event");
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s),
           "fill launch");
+    if (fill_end_event) Check(cudaEventRecord(static_cast<cudaEvent_t>(fill_end_event), s), "event");
     b->EndFill(false);
     pre3::AcceptArgs g{};
     g.restart = 1;
