@@ -255,7 +255,8 @@ def workload_config(args, world, B):
     return {"workload": cfg["desc"].format(b=B), "config_index": args.config, "grammar": args.grammar,
             "vocab_bits": args.vocab + 1, "batch_per_gpu": B, "global_batch": B * world,
             "context_depth": args.context_depth, "parent_depth": args.parent_depth, "mode": args.mode,
-            "step": ("gm_decode_step_greedy (argmax fill + accept kernels)" if args.mode == "greedy" else
+            "step": (f"gm_decode_step_greedy (argmax fill + accept kernels; every {args.sample_every}th step with "
+                     "events around its fill kernel)" if args.mode == "greedy" else
                      "gm_decode_step_stream (one launch)" if args.one_launch else
                      "gm_decode_step_stream_split (fill + overlapped sample/accept kernel: pure-CI sequences "
                      "sample from their cached context row at once, the rest as their fill items arrive); "
@@ -369,15 +370,9 @@ def main(argv=None):
         e0.record(stream)
         for i in range(K):
             timed = i % SAMPLE_EVERY == 0
-            if timed and not separate:
-                ev[i // SAMPLE_EVERY][0].record(stream)
-            if separate and timed:  # events bracket the step's fill kernel alone (the roofline kernel)
-                batch.decode_step_stream_split(seed, bitmask=bm, logits=logits[i % R], seg_counts=counts,
-                                               tokens_out=toks, fill_events=ev[i // SAMPLE_EVERY])
-            else:
-                step(i)
-                if timed:
-                    ev[i // SAMPLE_EVERY][1].record(stream)
+            if timed:  # events bracket the step's fill kernel alone (the roofline kernel)
+                batch.time_next_fill(*ev[i // SAMPLE_EVERY])
+            step(i)
         e1.record(stream)
         h1 = time.perf_counter()
         torch.cuda.synchronize()
@@ -417,10 +412,8 @@ def main(argv=None):
         f0.record(stream)
         for i in range(Kn):
             if i % 8 == 0:
-                bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn,
-                                            fill_events=evn[i // 8])
-            else:
-                bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn)
+                bn.time_next_fill(*evn[i // 8])
+            bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn)
         f1.record(stream)
         torch.cuda.synchronize()
         bn.check()
@@ -511,7 +504,7 @@ def main(argv=None):
                          f"threads={cores}, per seq-step {cpu_step_rule(args.mode)}"}
 
     info = eng.info()
-    kname = ("FillKernel<greedy> + AcceptKernel<greedy> (the whole step, sampled)" if greedy else
+    kname = ("FillKernel<greedy> (mask + argmax over allowed logits; accept runs in AcceptKernel)" if greedy else
              "FillKernel (fill + -inf logits; accept runs in AcceptKernel)" if separate else
              "FillKernel (one-launch step: fill + -inf logits + sample/accept tail)")
     line = {

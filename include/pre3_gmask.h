@@ -177,7 +177,7 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
  * gm_fill_and_mask_logits. */
 int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
                                 int64_t ld, int32_t* seg_counts, uint64_t seed, int32_t* tokens_out,
-                                void* stream, void* fill_start_event, void* fill_end_event);
+                                void* stream);
 
 /* Engine::AllowedTerminals (runtime.cpp:188-208) for every sequence: the
  * exact next-byte set plus $ — terminal t is allowed iff an edge of the
@@ -231,6 +231,12 @@ int gm_sample_tokens(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, const
 int gm_decode_step_sample(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, uint32_t* bitmask,
                           int64_t ld_words, float temperature, int32_t top_k, float top_p, uint64_t seed,
                           int32_t* tokens_out, void* stream);
+
+/* Measurement hook (diagnostics): the next fill kernel launched for this
+ * batch, by any call, is bracketed by cudaEventRecord(start_event) and
+ * cudaEventRecord(end_event) on its stream (cudaEvent_t handles; one-shot).
+ * In an overlapped step the following kernel then cannot start under it. */
+int gm_batch_time_next_fill(gm_batch* b, void* start_event, void* end_event);
 
 /* Statistics accumulated while enabled (gm_batch_set_stats), reset on read:
  * stats[0] = logits bytes read, [1] = logits bytes written (16-B chunk

@@ -130,7 +130,8 @@ def lib() -> ctypes.CDLL:
             "gm_sample_stream_and_accept": ([P, P, I64, P, U64, P, P], ctypes.c_int),
             "gm_sample_stream": ([P, P, I64, P, U64, P, P], ctypes.c_int),
             "gm_decode_step_stream": ([P, P, I64, P, I64, U64, P, P], ctypes.c_int),
-            "gm_decode_step_stream_split": ([P, P, I64, P, I64, P, U64, P, P, P, P], ctypes.c_int),
+            "gm_decode_step_stream_split": ([P, P, I64, P, I64, P, U64, P, P], ctypes.c_int),
+            "gm_batch_time_next_fill": ([P, P, P], ctypes.c_int),
             "gm_decode_step_greedy": ([P, P, I64, P, I64, P, P], ctypes.c_int),
             "gm_sample_tokens": ([P, P, I64, P, I64, ctypes.c_float, I32, ctypes.c_float, U64, P, I32, P],
                                  ctypes.c_int),
@@ -455,19 +456,20 @@ class Batch:
         _check(lib().gm_decode_step_stream(self._h, bm, ldw, lg, ld, seed, to, _stream(stream)))
 
     def decode_step_stream_split(self, seed: int, bitmask=None, logits=None, seg_counts=None, tokens_out=None,
-                                 stream=None, fill_events=None):
-        """The same step as two overlapping kernels (gm_decode_step_stream_split);
-        fill_events = (start, end) torch.cuda.Events recorded around the fill alone."""
+                                 stream=None):
+        """The same step as two overlapping kernels (gm_decode_step_stream_split)."""
         bm = bitmask.data_ptr() if bitmask is not None else None
         ldw = bitmask.stride(0) if bitmask is not None else 0
         lg = logits.data_ptr() if logits is not None else None
         ld = logits.stride(0) if logits is not None else 0
         sc = seg_counts.data_ptr() if seg_counts is not None else None
         to = tokens_out.data_ptr() if tokens_out is not None else None
-        e0 = e1 = None
-        if fill_events is not None:
-            e0, e1 = (e.cuda_event for e in fill_events)
-        _check(lib().gm_decode_step_stream_split(self._h, bm, ldw, lg, ld, sc, seed, to, _stream(stream), e0, e1))
+        _check(lib().gm_decode_step_stream_split(self._h, bm, ldw, lg, ld, sc, seed, to, _stream(stream)))
+
+    def time_next_fill(self, start, end) -> None:
+        """Brackets the next fill kernel (whatever call launches it) with two
+        torch.cuda.Events (gm_batch_time_next_fill; created ones: record once first)."""
+        _check(lib().gm_batch_time_next_fill(self._h, start.cuda_event, end.cuda_event))
 
     def decode_step_greedy(self, logits, tokens_out=None, bitmask=None, stream=None):
         to = tokens_out.data_ptr() if tokens_out is not None else None

@@ -88,6 +88,16 @@ struct gm_engine {
 // (capacity 2*B*nseg items).
 struct gm_batch {
   gm_engine* engine = nullptr;
+  // One-shot measurement hook (gm_batch_time_next_fill): events recorded
+  // around the next fill kernel launch on its stream, whatever call makes it.
+  cudaEvent_t time_fill[2] = {nullptr, nullptr};
+  void FillStart(cudaStream_t s) {
+    if (time_fill[0]) Check(cudaEventRecord(time_fill[0], s), "event record");
+  }
+  void FillEnd(cudaStream_t s) {
+    if (time_fill[1]) Check(cudaEventRecord(time_fill[1], s), "event record");
+    time_fill[0] = time_fill[1] = nullptr;
+  }
   pre3::BatchView view{};
   int32_t* seg_counts = nullptr;          // internal scratch for fused decode
   uint32_t* scratch_mask = nullptr;       // internal bitmask when the caller passes none
@@ -580,6 +590,15 @@ int gm_batch_fill_stats(gm_batch* b, int64_t stats[6]) {
   });
 }
 
+int gm_batch_time_next_fill(gm_batch* b, void* start_event, void* end_event) {
+  return Guard([&]() -> int {
+    if (!b) return Fail(GM_ERR_USAGE, "null batch");
+    b->time_fill[0] = static_cast<cudaEvent_t>(start_event);
+    b->time_fill[1] = static_cast<cudaEvent_t>(end_event);
+    return GM_OK;
+  });
+}
+
 int gm_batch_set_trace(gm_batch* b, uint64_t* trace, int32_t capacity) {
   if (!b || (trace && capacity <= 0)) return Fail(GM_ERR_USAGE, "bad trace buffer");
   b->view.trace = reinterpret_cast<unsigned long long*>(trace);
@@ -618,7 +637,9 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     f.publish_arrival = 1;  // lets a following sample/accept start per sequence
     b->ClearArrivals(s);
     b->BeginFill(&f);
+    b->FillStart(s);
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s), "fill launch");
+    b->FillEnd(s);
     b->EndFill(false);
     b->arrivals_pending = true;
     return GM_OK;
@@ -648,8 +669,10 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
     f.seed = seed;
     b->ClearArrivals(s);
     b->BeginFill(&f);
+    b->FillStart(s);
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailStream, e->aut, e->vocab, e->cache, b->view, f, s),
           "decode launch");
+    b->FillEnd(s);
     b->EndFill(true);
     return GM_OK;
   });
@@ -660,8 +683,7 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
 // pure-CI sequence from its slot's CI row and counts (the fill writes the same
 // words and counts into bitmask/seg_counts) without waiting for the fill.
 int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits, int64_t ld,
-                                int32_t* seg_counts, uint64_t seed, int32_t* tokens_out, void* stream,
-                                void* fill_start_event, void* fill_end_event) {
+                                int32_t* seg_counts, uint64_t seed, int32_t* tokens_out, void* stream) {
   return Guard([&]() -> int {
     if (!b) return Fail(GM_ERR_USAGE, "null batch");
     gm_engine* e = b->engine;
@@ -680,12 +702,10 @@ int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words
     f.publish_arrival = 2;
     b->ClearArrivals(s);
     b->BeginFill(&f);
-    // Optional events around the fill alone (measurement; the accept then
-    // cannot start under the fill for this step).
-    if (fill_start_event) Check(cudaEventRecord(static_cast<cudaEvent_t>(fill_start_event), s), "event");
+    b->FillStart(s);
     Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s),
           "fill launch");
-    if (fill_end_event) Check(cudaEventRecord(static_cast<cudaEvent_t>(fill_end_event), s), "event");
+    b->FillEnd(s);
     b->EndFill(false);
     pre3::AcceptArgs g{};
     g.restart = 1;
@@ -807,8 +827,10 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     // Two kernels: the argmax fill, then the accept kernel, which starts per
     // sequence while the fill's last wave runs (measured faster than the
     // one-launch fused tail, whose tails hold fill CTA slots).
+    b->FillStart(s);
     Check(pre3::LaunchFill(pre3::kFillGreedy, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s),
           "greedy fill launch");
+    b->FillEnd(s);
     b->EndFill(false);
     pre3::AcceptArgs g{};
     g.best = b->best;
