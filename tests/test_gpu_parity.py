@@ -599,3 +599,26 @@ def test_cpp_device_engine_known_answers(vectors, tmp_path):
         _, status, stack = port.get(c)
         assert int(f[f.index("status") + 1]) == status, p
         assert [int(x) for x in f[f.index("stack") + 1:]] == stack, p
+
+
+def test_time_next_fill_brackets_one_fill():
+    """gm_batch_time_next_fill: the next fill kernel (here inside the split
+    step) is bracketed by the two events; the hook is one-shot."""
+    vocab = pk.synth_vocab(32000)
+    eng = pk.DeviceEngine(pk.Automaton.load(flat("json")), vocab)
+    B = 64
+    batch = eng.batch(B)
+    bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
+    toks = torch.zeros(B, dtype=torch.int32, device=DEV)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    e1.record()
+    torch.cuda.synchronize()
+    batch.time_next_fill(e0, e1)
+    batch.decode_step_stream_split(3, bitmask=bm, tokens_out=toks)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1)
+    assert 0.0 < t < 50.0
+    batch.decode_step_stream_split(3, bitmask=bm, tokens_out=toks)  # not timed: the events stay put
+    torch.cuda.synchronize()
+    assert e0.elapsed_time(e1) == t
