@@ -1107,7 +1107,10 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
     st.depth = depth;
   }
   if (status_out != nullptr && lane == 0) status_out[b] = st.status;
-  if (restart && st.status != kAlive) {
+  // restart 1: finished sequences (accepted, dead, overflow) start over;
+  // 2 (a sampled token): so does a dead end — no allowed token and no EOS
+  // (tok < 0), like the decode loops of the oracle (gmask_port.c gp_decode_run).
+  if (restart && (st.status != kAlive || (restart == 2 && tok < 0))) {
     if (lane == 0) {
       stack[0] = A.initial;
       atomicAdd(Bt.counters + 0, 1ull);
@@ -1431,7 +1434,7 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
   }
   if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
   if (lane == 0) Bt.seq_arrive[b] = 0;
-  AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, 1, F.produce, F.fill_no + 1,
+  AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, 2, F.produce, F.fill_no + 1,
              lane);
   if (lane == 0) TraceEvent(Bt, kTraceTail, b, 0, t_in, static_cast<unsigned long long>(tok + 1));
 }
@@ -2004,7 +2007,8 @@ __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv
     if (lane == 0) Bt.seq[b].draws = st.draws;
     return;
   }
-  AcceptWarp(A, Vv, Cc, Bt, b, st, topv, tok, G.status_out, G.restart, G.lookup_queue, G.lookup_tag, lane);
+  AcceptWarp(A, Vv, Cc, Bt, b, st, topv, tok, G.status_out, (SAMPLE != kSampleGiven && G.restart) ? 2 : G.restart,
+             G.lookup_queue, G.lookup_tag, lane);
   if (lane == 0) TraceEvent(Bt, kTraceAccept, b, 0, t_in, static_cast<unsigned long long>(tok + 1));
 }
 
@@ -2346,7 +2350,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     st.draws += 1;
     if (S.tokens_out != nullptr && lane == 0) S.tokens_out[b] = tok;
     if (S.do_accept) {
-      AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, S.restart, S.lookup_queue,
+      AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, S.restart ? 2 : 0, S.lookup_queue,
                  S.lookup_tag, lane);
     } else if (lane == 0) {
       Bt.seq[b].draws = st.draws;

@@ -622,3 +622,23 @@ def test_time_next_fill_brackets_one_fill():
     batch.decode_step_stream_split(3, bitmask=bm, tokens_out=toks)  # not timed: the events stay put
     torch.cuda.synchronize()
     assert e0.elapsed_time(e1) == t
+
+
+def test_dead_end_restarts_like_the_port():
+    """A grammar whose non-productive rules lead to configurations with no
+    allowed token and no EOS (found by scripts/gpu_fuzz.py): the sampled token
+    is -1 and the sequence restarts from InitialConfig in every step form,
+    as in the C port's decode loop."""
+    import itertools
+    text = 'A -> "a" "c" ")" | D D "b" | "(" B B\nB -> D "a"\nC ->  | \nD -> D "c" D A\n'
+    alphabet = [bytes([c]) for c in b"abc(),"]
+    vocab = [b"".join(p) for n in (1, 2, 3) for p in itertools.product(alphabet, repeat=n)]
+    f = pk.Automaton.compile(text).save()
+    port = Port(f, vocab)
+    for K in (1, 8):
+        eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
+        _, ptoks, _ = port.decode_run(eng.structural, 16, 16, 1000, want_tokens=True, want_stacks=True)
+        assert (ptoks < 0).any()  # the dead end is reached
+        for mode in (False, True, "split"):
+            _, _, tokens = run_stream(eng, 16, 16, 1000, fused=mode)
+            assert np.array_equal(tokens, ptoks), (K, mode)
