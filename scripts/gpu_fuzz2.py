@@ -118,6 +118,55 @@ def greedy_run(eng, port, vocab_of, B, steps, cap, gseed):
     return True
 
 
+def sample_run(eng, port, vocab_of, B, steps, cap, gseed, T_, k_, p_):
+    """Device gm_decode_step_sample (temperature/top-k/top-p) vs the port's
+    rule, step by step, plus AllowedTerminals of every configuration."""
+    batch = eng.batch(B, cap)
+    bm = torch.zeros((B, eng.W), dtype=torch.int32, device="cuda")
+    toks = torch.zeros(B, dtype=torch.int32, device="cuda")
+    at = torch.zeros((B, 9), dtype=torch.int32, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(gseed)
+    cfgs = [port.initial() for _ in range(B)]
+    for s in range(steps):
+        batch.allowed_terminals(at)
+        atw = at.cpu().numpy().view(np.uint32)
+        for b in range(B):
+            byteset, eos = port.allowed(cfgs[b])
+            got = sum(int(atw[b, i]) << (32 * i) for i in range(8))
+            if got != byteset or bool(atw[b, 8] & 1) != eos:
+                return False
+        lg = torch.randn((B, eng.V + 1), dtype=torch.float32, device="cuda", generator=g)
+        lg = (torch.round(lg * 2) / 2).to(torch.bfloat16)
+        batch.decode_step_sample(lg, temperature=T_, top_k=k_, top_p=p_, seed=gseed, tokens_out=toks, bitmask=bm)
+        batch.check()
+        got = bm.cpu().numpy().view(np.uint32)
+        rows = lg.view(torch.int16).cpu().numpy().view(np.uint16)
+        tk = toks.cpu().numpy()
+        for b in range(B):
+            want = port.mask(cfgs[b])
+            if not np.array_equal(got[b], want):
+                return False
+            tok = port.sample_pick(want, rows[b], T_, k_, p_, Port.stream_draw(gseed, b, s))
+            if tok != tk[b]:
+                return False
+            overflow = False
+            if tok == eng.V:
+                port.step(cfgs[b], 256)
+            elif tok >= 0:
+                for byte in vocab_of[tok]:
+                    if not port.step(cfgs[b], byte):
+                        break
+                    if len(port.get(cfgs[b])[2]) > cap:
+                        overflow = True
+                        break
+            if tok < 0 or overflow or cfgs[b].status != 0:
+                port.free(cfgs[b])
+                cfgs[b] = port.initial()
+            if batch.get(b).stack != port.get(cfgs[b])[2]:
+                return False
+    return True
+
+
 done = skipped = runs = 0
 while done < N:
     text = grammar(rng)
@@ -165,7 +214,21 @@ while done < N:
             if not greedy_run(eng, port, vocab, B, 12, cap, s & 0xffff):
                 print("MISMATCH greedy", K, cap, repr(text), len(vocab))
                 sys.exit(1)
+            runs += 1
+            T_, k_, p_ = rng.choice([0.7, 1.0, 1.6]), rng.choice([0, 1, 5]), rng.choice([1.0, 0.9, 0.5])
+            if not sample_run(eng, port, vocab, B, 10, cap, s & 0xffff, T_, k_, p_):
+                print("MISMATCH sample/allowed", K, cap, T_, k_, p_, repr(text), len(vocab))
+                sys.exit(1)
+    # Context-cache pressure: 4 slots (private rows) and parent depths.
+    for slots, R in ((4, 0), (64, 1), (1 << 12, 3), (1 << 12, -1)):
+        eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=6, context_slots=slots, parent_depth=R)
+        batch, masks, tokens = T.run_stream(eng, B, steps, s, cap=cap, fused="split")
+        runs += 1
+        if not (np.array_equal(tokens, ptoks) and np.array_equal(masks, pm)):
+            print("MISMATCH cache", slots, R, cap, repr(text), len(vocab))
+            sys.exit(1)
     done += 1
 print(f"wide random-grammar parity: {done} grammars ({skipped} rejected by the compiler), {runs} device runs "
-      f"(K 1/4/12 x separate/fused/split + greedy, random 60-400-token vocabularies, stack capacity 6/12/1024): "
-      f"masks, -inf logits, tokens and stacks all equal to the C port's")
+      f"(K 1/4/12 x separate/fused/split + greedy + temperature/top-k/top-p with AllowedTerminals, context tables "
+      f"of 4/64/4096 slots and parent depths -1/1/3, random 60-400-token vocabularies, stack capacity 6/12/1024): "
+      f"masks, -inf logits, tokens, terminal sets and stacks all equal to the C port's")
