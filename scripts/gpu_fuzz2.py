@@ -219,6 +219,16 @@ while done < N:
             if not sample_run(eng, port, vocab, B, 10, cap, s & 0xffff, T_, k_, p_):
                 print("MISMATCH sample/allowed", K, cap, T_, k_, p_, repr(text), len(vocab))
                 sys.exit(1)
+    # Overlap race check at a multi-wave batch: the split step equals the
+    # serial two-call loop token for token (device vs device).
+    if done % 10 == 0:
+        eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=rng.choice([1, 4, 12]))
+        _, _, t_split = T.run_stream(eng, 1024, 40, s, cap=cap, fused="split")
+        _, _, t_two = T.run_stream(eng, 1024, 40, s, cap=cap, fused=False)
+        runs += 2
+        if not np.array_equal(t_split, t_two):
+            print("MISMATCH split vs two-call at 1024", cap, repr(text), len(vocab))
+            sys.exit(1)
     # Context-cache pressure: 4 slots (private rows) and parent depths.
     for slots, R in ((4, 0), (64, 1), (1 << 12, 3), (1 << 12, -1)):
         eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=6, context_slots=slots, parent_depth=R)
@@ -230,5 +240,6 @@ while done < N:
     done += 1
 print(f"wide random-grammar parity: {done} grammars ({skipped} rejected by the compiler), {runs} device runs "
       f"(K 1/4/12 x separate/fused/split + greedy + temperature/top-k/top-p with AllowedTerminals, context tables "
-      f"of 4/64/4096 slots and parent depths -1/1/3, random 60-400-token vocabularies, stack capacity 6/12/1024): "
+      f"of 4/64/4096 slots and parent depths -1/1/3, 1024-sequence split-vs-two-call runs every 10th grammar, "
+      f"random 60-400-token vocabularies, stack capacity 6/12/1024): "
       f"masks, -inf logits, tokens, terminal sets and stacks all equal to the C port's")
