@@ -21,8 +21,6 @@ import paper_2506_03887_b200 as pk  # noqa: E402
 from oracle import Port  # noqa: E402
 import test_gpu_parity as T  # noqa: E402
 
-N = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
 ALPHA = "ab{}[],: x1"
 
 
@@ -167,79 +165,90 @@ def sample_run(eng, port, vocab_of, B, steps, cap, gseed, T_, k_, p_):
     return True
 
 
-done = skipped = runs = 0
-while done < N:
-    text = grammar(rng)
-    try:
-        a = pk.Automaton.compile(text)
-    except pk.GmError:
-        skipped += 1
-        continue
-    f = a.save()
-    vocab = vocab_for(rng)
-    port = Port(f, vocab)
-    B, steps, s = 24, 20, rng.randrange(1 << 30)
-    cap = rng.choice([6, 12, 1024])
-    eng0 = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=1)
-    _, ptoks, pstacks = port.decode_run(eng0.structural, B, steps, s, stack_cap=cap, want_tokens=True,
-                                        want_stacks=True)
-    pm = port_masks(port, vocab, ptoks, B, steps, eng0.W, cap)
-    for K in (1, 4, 12):
-        eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
-        for mode in (False, True, "split"):
-            batch, masks, tokens = T.run_stream(eng, B, steps, s, cap=cap, fused=mode, check_logits=True)
-            ok = np.array_equal(tokens, ptoks) and np.array_equal(masks, pm)
-            for b in range(B):
-                d = pstacks[b, 0]
-                got = batch.get(b)
-                ok = ok and got.stack == pstacks[b, 2:2 + d].tolist()
-            runs += 1
-            if not ok:
-                print("MISMATCH stream", K, mode, cap, repr(text), len(vocab))
-                dt = np.argwhere(tokens != ptoks)
-                dm = np.argwhere((masks != pm).any(axis=2))
-                print("  first token diff", dt[:1].tolist(), "first mask diff", dm[:1].tolist())
-                if len(dt):
-                    bb, ss = [int(x) for x in dt[0]]
-                    print("  dev toks", tokens[bb, :ss + 1].tolist(), "port toks", ptoks[bb, :ss + 1].tolist())
-                    print("  tokens:", [vocab[t] if 0 <= t < len(vocab) else t for t in ptoks[bb, :ss + 1].tolist()])
+def run(N, seed):
+    """Returns (grammars, rejected, runs); exits on the first mismatch."""
+    rng = random.Random(seed)
+    done = skipped = runs = 0
+    while done < N:
+        text = grammar(rng)
+        try:
+            a = pk.Automaton.compile(text)
+        except pk.GmError:
+            skipped += 1
+            continue
+        f = a.save()
+        vocab = vocab_for(rng)
+        port = Port(f, vocab)
+        B, steps, s = 24, 20, rng.randrange(1 << 30)
+        cap = rng.choice([6, 12, 1024])
+        eng0 = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=1)
+        _, ptoks, pstacks = port.decode_run(eng0.structural, B, steps, s, stack_cap=cap, want_tokens=True,
+                                            want_stacks=True)
+        pm = port_masks(port, vocab, ptoks, B, steps, eng0.W, cap)
+        for K in (1, 4, 12):
+            eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
+            for mode in (False, True, "split"):
+                batch, masks, tokens = T.run_stream(eng, B, steps, s, cap=cap, fused=mode, check_logits=True)
+                ok = np.array_equal(tokens, ptoks) and np.array_equal(masks, pm)
                 for b in range(B):
                     d = pstacks[b, 0]
-                    if batch.get(b).stack != pstacks[b, 2:2 + d].tolist():
-                        print("  stack diff seq", b, batch.get(b).stack, batch.get(b).status, pstacks[b, 2:2 + d].tolist(), pstacks[b, 1])
-                        break
-                sys.exit(1)
-        if K == 4:
+                    got = batch.get(b)
+                    ok = ok and got.stack == pstacks[b, 2:2 + d].tolist()
+                runs += 1
+                if not ok:
+                    print("MISMATCH stream", K, mode, cap, repr(text), len(vocab))
+                    dt = np.argwhere(tokens != ptoks)
+                    dm = np.argwhere((masks != pm).any(axis=2))
+                    print("  first token diff", dt[:1].tolist(), "first mask diff", dm[:1].tolist())
+                    if len(dt):
+                        bb, ss = [int(x) for x in dt[0]]
+                        print("  dev toks", tokens[bb, :ss + 1].tolist(), "port toks", ptoks[bb, :ss + 1].tolist())
+                        print("  tokens:", [vocab[t] if 0 <= t < len(vocab) else t for t in ptoks[bb, :ss + 1].tolist()])
+                    for b in range(B):
+                        d = pstacks[b, 0]
+                        if batch.get(b).stack != pstacks[b, 2:2 + d].tolist():
+                            print("  stack diff seq", b, batch.get(b).stack, batch.get(b).status, pstacks[b, 2:2 + d].tolist(), pstacks[b, 1])
+                            break
+                    raise AssertionError("device and C port differ (details above)")
+            if K == 4:
+                runs += 1
+                if not greedy_run(eng, port, vocab, B, 12, cap, s & 0xffff):
+                    print("MISMATCH greedy", K, cap, repr(text), len(vocab))
+                    raise AssertionError("device and C port differ (details above)")
+                runs += 1
+                T_, k_, p_ = rng.choice([0.7, 1.0, 1.6]), rng.choice([0, 1, 5]), rng.choice([1.0, 0.9, 0.5])
+                if not sample_run(eng, port, vocab, B, 10, cap, s & 0xffff, T_, k_, p_):
+                    print("MISMATCH sample/allowed", K, cap, T_, k_, p_, repr(text), len(vocab))
+                    raise AssertionError("device and C port differ (details above)")
+        # Overlap race check at a multi-wave batch: the split step equals the
+        # serial two-call loop token for token (device vs device).
+        if done % 10 == 0:
+            eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=rng.choice([1, 4, 12]))
+            _, _, t_split = T.run_stream(eng, 1024, 40, s, cap=cap, fused="split")
+            _, _, t_two = T.run_stream(eng, 1024, 40, s, cap=cap, fused=False)
+            runs += 2
+            if not np.array_equal(t_split, t_two):
+                print("MISMATCH split vs two-call at 1024", cap, repr(text), len(vocab))
+                raise AssertionError("device and C port differ (details above)")
+        # Context-cache pressure: 4 slots (private rows) and parent depths.
+        for slots, R in ((4, 0), (64, 1), (1 << 12, 3), (1 << 12, -1)):
+            eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=6, context_slots=slots, parent_depth=R)
+            batch, masks, tokens = T.run_stream(eng, B, steps, s, cap=cap, fused="split")
             runs += 1
-            if not greedy_run(eng, port, vocab, B, 12, cap, s & 0xffff):
-                print("MISMATCH greedy", K, cap, repr(text), len(vocab))
-                sys.exit(1)
-            runs += 1
-            T_, k_, p_ = rng.choice([0.7, 1.0, 1.6]), rng.choice([0, 1, 5]), rng.choice([1.0, 0.9, 0.5])
-            if not sample_run(eng, port, vocab, B, 10, cap, s & 0xffff, T_, k_, p_):
-                print("MISMATCH sample/allowed", K, cap, T_, k_, p_, repr(text), len(vocab))
-                sys.exit(1)
-    # Overlap race check at a multi-wave batch: the split step equals the
-    # serial two-call loop token for token (device vs device).
-    if done % 10 == 0:
-        eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=rng.choice([1, 4, 12]))
-        _, _, t_split = T.run_stream(eng, 1024, 40, s, cap=cap, fused="split")
-        _, _, t_two = T.run_stream(eng, 1024, 40, s, cap=cap, fused=False)
-        runs += 2
-        if not np.array_equal(t_split, t_two):
-            print("MISMATCH split vs two-call at 1024", cap, repr(text), len(vocab))
-            sys.exit(1)
-    # Context-cache pressure: 4 slots (private rows) and parent depths.
-    for slots, R in ((4, 0), (64, 1), (1 << 12, 3), (1 << 12, -1)):
-        eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=6, context_slots=slots, parent_depth=R)
-        batch, masks, tokens = T.run_stream(eng, B, steps, s, cap=cap, fused="split")
-        runs += 1
-        if not (np.array_equal(tokens, ptoks) and np.array_equal(masks, pm)):
-            print("MISMATCH cache", slots, R, cap, repr(text), len(vocab))
-            sys.exit(1)
-    done += 1
-print(f"wide random-grammar parity: {done} grammars ({skipped} rejected by the compiler), {runs} device runs "
-      f"(K 1/4/12 x separate/fused/split + greedy + temperature/top-k/top-p with AllowedTerminals, context tables "
-      f"of 4/64/4096 slots and parent depths -1/1/3, 1024-sequence split-vs-two-call runs every 10th grammar, "
-      f"random 60-400-token vocabularies, stack capacity 6/12/1024): "
-      f"masks, -inf logits, tokens, terminal sets and stacks all equal to the C port's")
+            if not (np.array_equal(tokens, ptoks) and np.array_equal(masks, pm)):
+                print("MISMATCH cache", slots, R, cap, repr(text), len(vocab))
+                raise AssertionError("device and C port differ (details above)")
+        done += 1
+    return done, skipped, runs
+
+
+def report(done, skipped, runs):
+    print(f"wide random-grammar parity: {done} grammars ({skipped} rejected by the compiler), {runs} device runs "
+          f"(K 1/4/12 x separate/fused/split + greedy + temperature/top-k/top-p with AllowedTerminals, context tables "
+          f"of 4/64/4096 slots and parent depths -1/1/3, 1024-sequence split-vs-two-call runs every 10th grammar, "
+          f"random 60-400-token vocabularies, stack capacity 6/12/1024): "
+          f"masks, -inf logits, tokens, terminal sets and stacks all equal to the C port's")
+
+
+if __name__ == "__main__":
+    report(*run(int(sys.argv[1]) if len(sys.argv) > 1 else 100, int(sys.argv[2]) if len(sys.argv) > 2 else 7))

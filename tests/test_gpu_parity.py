@@ -642,3 +642,16 @@ def test_dead_end_restarts_like_the_port():
         for mode in (False, True, "split"):
             _, _, tokens = run_stream(eng, 16, 16, 1000, fused=mode)
             assert np.array_equal(tokens, ptoks), (K, mode)
+
+
+def test_wide_random_grammar_fuzz_sample():
+    """A 12-grammar sample of scripts/gpu_fuzz2.py (multi-byte literals,
+    random vocabularies, small stack capacities; stream/greedy/temperature
+    steps, AllowedTerminals, tiny context tables, a 1,024-sequence
+    split-vs-two-call check) — the full sweeps are recorded in profiles/."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("gpu_fuzz2", os.path.join(ROOT, "scripts", "gpu_fuzz2.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    done, _, runs = m.run(12, 31337)
+    assert done == 12 and runs > 100
