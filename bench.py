@@ -437,10 +437,11 @@ def main(argv=None):
     # caller (paper_2506_03887_b200/tools/e2e_driver.cpp; Python's per-call
     # overhead would otherwise dominate).  Every step: H2D of the host-held
     # token ids, gm_accept_tokens + gm_fill_and_mask_logits + gm_sample_stream
-    # (greedy: gm_decode_step_greedy), D2H of the sampled ids (waited for: the
-    # next step needs them) and of the full bitmask (a copy stream into
-    # double-buffered pinned memory, overlapping the next step); the timed
-    # region ends after the last copy lands.
+    # (greedy: gm_decode_step_greedy), D2H of the sampled ids (stored by the
+    # kernel straight into mapped pinned memory, waited for: the next step
+    # needs them) and of the full bitmask (a copy stream into double-buffered
+    # pinned memory, overlapping the next step); the timed region ends after
+    # the last copy lands.
     e2e = None
     if not args.no_e2e:
         import ctypes
@@ -468,9 +469,10 @@ def main(argv=None):
             raise RuntimeError(f"e2e driver failed: {rc} {pk.lib().gm_last_error().decode()}")
         t_full, t_ids = max_over_ranks([t_full, secs.value], dev, world)
         t_e2e = t_full
-        path = ("C++ caller: gm_decode_step_greedy(device logits) → D2H ids; D2H bitmask on a copy stream"
-                if greedy else "C++ caller: H2D ids → gm_accept_tokens → gm_fill_and_mask_logits → "
-                "gm_sample_stream → D2H ids; D2H bitmask on a copy stream (double-buffered)")
+        path = ("C++ caller: gm_decode_step_greedy(device logits) → ids into mapped host memory; D2H bitmask "
+                "on a copy stream" if greedy else "C++ caller: H2D ids → gm_accept_tokens → "
+                "gm_fill_and_mask_logits → gm_sample_stream (ids into mapped host memory) → stream sync; D2H "
+                "bitmask on a copy stream (double-buffered)")
         e2e = {"value": aggregate_rate(world, B * Ke, t_e2e), "unit": UNIT,
                "h2d_bytes_per_step": 0 if greedy else B * 4, "d2h_bytes_per_step": B * W * 4 + B * 4,
                "steps": Ke, "path": path,

@@ -29,7 +29,7 @@ struct Bufs {
   int32_t* picked_host = nullptr;
   uint32_t* bm_host[2] = {nullptr, nullptr};
   int32_t* tok_dev = nullptr;
-  int32_t* picked_dev = nullptr;
+  int32_t* picked_map = nullptr;  // device alias of picked_host (mapped)
   uint32_t* bm_dev[2] = {nullptr, nullptr};
   int32_t* counts = nullptr;
   cudaStream_t s = nullptr, cs = nullptr;
@@ -45,7 +45,6 @@ struct Bufs {
       if (done[i]) cudaEventDestroy(done[i]);
     }
     cudaFree(tok_dev);
-    cudaFree(picked_dev);
     cudaFree(counts);
     if (s) cudaStreamDestroy(s);
     if (cs) cudaStreamDestroy(cs);
@@ -79,9 +78,12 @@ int e2e_run(gm_batch* b, int32_t mode, int32_t B, int32_t W, int32_t nseg, const
   Bufs m;
   const size_t mask_bytes = static_cast<size_t>(B) * static_cast<size_t>(W) * 4;
   CK(cudaHostAlloc(&m.tok_host, B * 4, cudaHostAllocDefault));
-  CK(cudaHostAlloc(&m.picked_host, B * 4, cudaHostAllocDefault));
+  // The sampled ids come back zero-copy: the kernel stores them straight
+  // into mapped pinned memory, so the small read-back never queues behind the
+  // 16 KB/sequence bitmask copy on the device-to-host copy engine.
+  CK(cudaHostAlloc(&m.picked_host, B * 4, cudaHostAllocMapped));
   CK(cudaMalloc(&m.tok_dev, B * 4));
-  CK(cudaMalloc(&m.picked_dev, B * 4));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&m.picked_map), m.picked_host, 0));
   CK(cudaMalloc(&m.counts, static_cast<size_t>(B) * nseg * 2 * 4));
   for (int i = 0; i < 2; ++i) {
     CK(cudaHostAlloc(&m.bm_host[i], mask_bytes, cudaHostAllocDefault));
@@ -103,9 +105,9 @@ int e2e_run(gm_batch* b, int32_t mode, int32_t B, int32_t W, int32_t nseg, const
       GK(gm_accept_tokens(b, m.tok_dev, nullptr, 1, m.s));
       GK(gm_fill_and_mask_logits(b, m.bm_dev[j], W, lg, ld, m.counts, m.s));
       CK(cudaEventRecord(m.ready[j], m.s));
-      GK(gm_sample_stream(b, m.bm_dev[j], W, m.counts, seed, m.picked_dev, m.s));
+      GK(gm_sample_stream(b, m.bm_dev[j], W, m.counts, seed, m.picked_map, m.s));
     } else {
-      GK(gm_decode_step_greedy(b, lg, ld, m.bm_dev[j], W, m.picked_dev, m.s));
+      GK(gm_decode_step_greedy(b, lg, ld, m.bm_dev[j], W, m.picked_map, m.s));
       CK(cudaEventRecord(m.ready[j], m.s));
     }
     if (copy_mask) {
@@ -113,7 +115,6 @@ int e2e_run(gm_batch* b, int32_t mode, int32_t B, int32_t W, int32_t nseg, const
       CK(cudaMemcpyAsync(m.bm_host[j], m.bm_dev[j], mask_bytes, cudaMemcpyDeviceToHost, m.cs));
       CK(cudaEventRecord(m.done[j], m.cs));
     }
-    CK(cudaMemcpyAsync(m.picked_host, m.picked_dev, B * 4, cudaMemcpyDeviceToHost, m.s));
     CK(cudaStreamSynchronize(m.s));
     if (mode == 0) {
       for (int k = 0; k < B; ++k) m.tok_host[k] = m.picked_host[k];
