@@ -655,3 +655,19 @@ def test_wide_random_grammar_fuzz_sample():
     spec.loader.exec_module(m)
     done, _, runs = m.run(12, 31337)
     assert done == 12 and runs > 100
+
+
+@pytest.mark.parametrize("B", [1, 3, 33])
+def test_split_step_odd_batches(B):
+    """Batch sizes that leave partial CTAs (accept: 4 warps per CTA; fill: 8
+    items per CTA): the split step still equals the C port."""
+    vocab = pk.synth_vocab(40000)
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=8)
+    port = Port(f, vocab)
+    _, ptoks, pstacks = port.decode_run(eng.structural, B, 14, 23, want_tokens=True, want_stacks=True)
+    batch, _, tokens = run_stream(eng, B, 14, 23, fused="split", check_logits=True)
+    assert np.array_equal(tokens, ptoks)
+    for b in range(B):
+        d = pstacks[b, 0]
+        assert batch.get(b).stack == pstacks[b, 2:2 + d].tolist()
