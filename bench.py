@@ -525,7 +525,7 @@ def main(argv=None):
                                                                  fstats["logit_bytes_written"]) / B},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": K * (2 if separate else 1),
+        "gpu_launches": K * (1 if args.one_launch else 2),  # split / greedy: fill + accept per step
         "clocks": clocks.summary(),
         "preprocessing": {"compile_s": t_comp, "prewarm_s": t_pre,
                           "prewarm": f"{args.prewarm_steps} steps x {args.prewarm_batch} seqs "
