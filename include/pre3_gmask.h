@@ -196,7 +196,9 @@ int gm_accept_tokens(gm_batch* b, const int32_t* tokens, int32_t* status_out, in
 /* Synthetic-stream sampler fused with accept: picks each
  * sequence's token from the bitmask + seg_counts of the preceding
  * gm_fill_and_mask_logits, writes it to tokens_out (may be NULL), accepts it
- * and restarts finished sequences.  `seed` keys the per-sequence streams. */
+ * and restarts finished sequences (accepted, dead, overflow) and dead ends
+ * (nothing allowed: token -1) from InitialConfig.  `seed` keys the
+ * per-sequence streams. */
 int gm_sample_stream_and_accept(gm_batch* b, const uint32_t* bitmask, int64_t ld_words,
                                 const int32_t* seg_counts, uint64_t seed, int32_t* tokens_out,
                                 void* stream);
@@ -208,8 +210,9 @@ int gm_sample_stream(gm_batch* b, const uint32_t* bitmask, int64_t ld_words, con
                      uint64_t seed, int32_t* tokens_out, void* stream);
 
 /* Greedy decode step (config 5): fill + argmax over allowed bf16 logits (the
- * row is read, not written; ties -> lowest id) + accept + restart.
- * tokens_out receives the chosen ids (-1 when nothing is allowed). */
+ * row is read, not written; ties -> lowest id) + accept + restart (finished
+ * sequences and dead ends).  tokens_out receives the chosen ids (-1 when
+ * nothing is allowed). */
 int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, uint32_t* bitmask,
                           int64_t ld_words, int32_t* tokens_out, void* stream);
 
