@@ -159,12 +159,11 @@ __device__ __forceinline__ void TraceEvent(const BatchView& Bt, int kind, int b,
 // the outcome unknown (it comes first in arbitration order).  Returns the
 // candidate index, -1 (no edge), -2 (unknown) or -3 (hash collision: scan).
 // Entry j of the virtual stack: j < nl ? loc[nl-1-j] : base[nb-1-(j-nl)].
-__device__ __forceinline__ int IndexedFindEdge(const int2* hmeta, const int16_t* hlens,
+__device__ __forceinline__ int IndexedFindEdge(const int16_t* hlens,
                                                const unsigned long long* hexact, unsigned long long emask,
                                                const unsigned long long* hprefix, unsigned long long pmask,
                                                int2 meta, int state, int x, const int32_t* loc, int nl,
                                                const int32_t* base, int nb, bool complete) {
-  (void)hmeta;
   const int nlen = meta.y & 0xffff;
   const int maxl = meta.y >> 16;
   const int D = nl + nb;
@@ -235,7 +234,7 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
     Rec fr;
     int c_scan = cb;  // first candidate of the linear scan (ce: none)
     if (meta.y != 0) {
-      const int c = IndexedFindEdge(hmeta, hlens, hexact, emask, hprefix, pmask, meta, state, x, loc, nl, base, nb,
+      const int c = IndexedFindEdge(hlens, hexact, emask, hprefix, pmask, meta, state, x, loc, nl, base, nb,
                                     complete);
       if (c == -2) return kUnknown;
       c_scan = ce;
