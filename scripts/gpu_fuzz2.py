@@ -42,10 +42,15 @@ def grammar(rng):
     return "\n".join(lines) + "\n"
 
 
+VOCAB_RANGE = (60, 400)  # tokens per random vocabulary (gpu_fuzz2.py N seed [min max])
+
+
 def vocab_for(rng):
     v = {c.encode() for c in ALPHA}
-    while len(v) < rng.randint(60, 400):
-        v.add("".join(rng.choice(ALPHA) for _ in range(rng.randint(2, 5))).encode())
+    want = rng.randint(*VOCAB_RANGE)
+    longest = 5 if VOCAB_RANGE[1] <= 400 else 8
+    while len(v) < want:
+        v.add("".join(rng.choice(ALPHA) for _ in range(rng.randint(2, longest))).encode())
     return sorted(v)
 
 
@@ -246,9 +251,11 @@ def report(done, skipped, runs):
     print(f"wide random-grammar parity: {done} grammars ({skipped} rejected by the compiler), {runs} device runs "
           f"(K 1/4/12 x separate/fused/split + greedy + temperature/top-k/top-p with AllowedTerminals, context tables "
           f"of 4/64/4096 slots and parent depths -1/1/3, 1024-sequence split-vs-two-call runs every 10th grammar, "
-          f"random 60-400-token vocabularies, stack capacity 6/12/1024): "
+          f"random {VOCAB_RANGE[0]}-{VOCAB_RANGE[1]}-token vocabularies, stack capacity 6/12/1024): "
           f"masks, -inf logits, tokens, terminal sets and stacks all equal to the C port's")
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 4:
+        VOCAB_RANGE = (int(sys.argv[3]), int(sys.argv[4]))
     report(*run(int(sys.argv[1]) if len(sys.argv) > 1 else 100, int(sys.argv[2]) if len(sys.argv) > 2 else 7))
