@@ -40,7 +40,7 @@ L2_BYTES = 126 * 1024 * 1024
 
 # BASELINE.json configs (index 1.. = config 2..5).
 CONFIGS = {
-    2: dict(grammar="json", flavor=0, batch=256, mode="stream", scaling="weak", K=16, slots=65536,
+    2: dict(grammar="json", flavor=0, batch=256, mode="stream", scaling="weak", K=20, slots=65536,
             desc="config2: JSON LR(1) grammar, 128256-bit vocab (synthetic 128k tokens), batch {b}/GPU, "
                  "fused mask-fill + in-place bf16 -inf logit masking + stream sample + accept_token"),
     3: dict(grammar="schema", flavor=0, batch=1024, mode="stream", scaling="weak", K=16, slots=16384,
