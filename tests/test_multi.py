@@ -62,3 +62,17 @@ def test_reference_arm_under_torchrun_prints_once():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+def test_bench_config_defaults():
+    """bench.py's per-config settings: context depth, parent
+    depth, table size, prewarm; the default run is config 2 on one GPU."""
+    import bench
+    a = bench.parse([])
+    assert (a.config, a.context_depth, a.context_slots, a.prewarm_steps, a.mode) == (2, 20, 65536, 10000, "stream")
+    a = bench.parse(["--config", "4"])
+    assert (a.context_depth, a.parent_depth, a.context_slots, a.prewarm_steps) == (20, 6, 262144, 30000)
+    a = bench.parse(["--config", "5"])
+    assert (a.mode, a.context_depth) == ("greedy", 12)
+    a = bench.parse(["--config", "3", "--context-depth", "12"])
+    assert a.context_depth == 12 and a.sample_every == 16
