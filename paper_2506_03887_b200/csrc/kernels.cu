@@ -2081,6 +2081,11 @@ __device__ unsigned long long SampleWeight(uint32_t key, float vmax, float tempe
 struct SampleShared {
   unsigned int cnt_hi[256];
   unsigned long long w_hi[256];
+  // Per-warp copies of the two dense histograms: an allowed token's high byte
+  // (sign + exponent) takes few values, so one shared copy serializes the
+  // CTA's atomics; the copies are summed after each pass (exact: integers).
+  unsigned int cnt_hi_w[kThreads / 32][256];
+  unsigned long long w_hi_w[kThreads / 32][256];
   unsigned int cnt_lo[256];
   unsigned long long w_lo[256];
   unsigned int cnt_lo2[256];
@@ -2133,6 +2138,10 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   const int nchunks = (V1 + 7) >> 3;
   const uint32_t* mrow = S.bitmask + static_cast<long long>(b) * S.ldw;
   const uint16_t* row = S.logits + static_cast<long long>(b) * S.ld;
+  for (int i = tid; i < 256 * (kThreads / 32); i += kThreads) {
+    sh.cnt_hi_w[i >> 8][i & 255] = 0u;
+    sh.w_hi_w[i >> 8][i & 255] = 0ull;
+  }
   for (int i = tid; i < 256; i += kThreads) {
     sh.cnt_hi[i] = 0u;
     sh.w_hi[i] = 0ull;
@@ -2145,7 +2154,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   // ---- pass 1: high-byte counts, max key, |allowed|.
   unsigned int kmax = 0u, n_allowed = 0u;
   ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
-    atomicAdd(&sh.cnt_hi[key >> 8], 1u);
+    atomicAdd(&sh.cnt_hi_w[warp][key >> 8], 1u);
     kmax = key > kmax ? key : kmax;
     ++n_allowed;
   });
@@ -2153,6 +2162,12 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   n_allowed = __reduce_add_sync(0xffffffffu, n_allowed);
   if (lane == 0) sh.red[warp] = kmax;
   __syncthreads();
+  for (int i = tid; i < 256; i += kThreads) {
+    unsigned int c = 0u;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) c += sh.cnt_hi_w[w][i];
+    sh.cnt_hi[i] = c;
+  }
   if (tid == 0) {
     unsigned int m = 0u;
     for (int i = 0; i < kThreads / 32; ++i) m = sh.red[i] > m ? sh.red[i] : m;
@@ -2192,12 +2207,19 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
       const int h = static_cast<int>(key >> 8);
       if (h > hi_k) {
-        atomicAdd(&sh.w_hi[h], SampleWeight(key, vmax, S.temperature));
+        atomicAdd(&sh.w_hi_w[warp][h], SampleWeight(key, vmax, S.temperature));
       } else if (h == hi_k) {
         atomicAdd(&sh.cnt_lo[key & 0xffu], 1u);
         atomicAdd(&sh.w_lo[key & 0xffu], SampleWeight(key, vmax, S.temperature));
       }
     });
+    __syncthreads();
+    for (int i = tid; i < 256; i += kThreads) {
+      unsigned long long w = 0ull;
+#pragma unroll
+      for (int ww = 0; ww < kThreads / 32; ++ww) w += sh.w_hi_w[ww][i];
+      sh.w_hi[i] = w;
+    }
     __syncthreads();
     int lo_k = 0;
     if (hi_k >= 0) {
