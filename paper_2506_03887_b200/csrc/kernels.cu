@@ -2078,14 +2078,26 @@ __device__ unsigned long long SampleWeight(uint32_t key, float vmax, float tempe
   return __float2ull_rn(__fmul_rn(p, scale));
 }
 
+constexpr int kSampleKeySlots = 24;  // kcnt rows: 24 x 256 x 4 B = the per-warp histograms' 24 KB
+
 struct SampleShared {
   unsigned int cnt_hi[256];
   unsigned long long w_hi[256];
   // Per-warp copies of the two dense histograms: an allowed token's high byte
   // (sign + exponent) takes few values, so one shared copy serializes the
   // CTA's atomics; the copies are summed after each pass (exact: integers).
-  unsigned int cnt_hi_w[kThreads / 32][256];
-  unsigned long long w_hi_w[kThreads / 32][256];
+  // Dense rows with few high bytes instead count every 16-bit key (kcnt) and
+  // weigh each distinct key once: sum_t W(key_t) = sum_key cnt(key) * W(key).
+  union {
+    struct {
+      unsigned int cnt_hi_w[kThreads / 32][256];
+      unsigned long long w_hi_w[kThreads / 32][256];
+    } pw;
+    unsigned int kcnt[kSampleKeySlots][256];
+  } u;
+  signed char hslot[256];          // high byte -> kcnt row (-1: none)
+  unsigned char slot_h[kSampleKeySlots];
+  int nslots;
   unsigned int cnt_lo[256];
   unsigned long long w_lo[256];
   unsigned int cnt_lo2[256];
@@ -2139,8 +2151,8 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   const uint32_t* mrow = S.bitmask + static_cast<long long>(b) * S.ldw;
   const uint16_t* row = S.logits + static_cast<long long>(b) * S.ld;
   for (int i = tid; i < 256 * (kThreads / 32); i += kThreads) {
-    sh.cnt_hi_w[i >> 8][i & 255] = 0u;
-    sh.w_hi_w[i >> 8][i & 255] = 0ull;
+    sh.u.pw.cnt_hi_w[i >> 8][i & 255] = 0u;
+    sh.u.pw.w_hi_w[i >> 8][i & 255] = 0ull;
   }
   for (int i = tid; i < 256; i += kThreads) {
     sh.cnt_hi[i] = 0u;
@@ -2154,7 +2166,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   // ---- pass 1: high-byte counts, max key, |allowed|.
   unsigned int kmax = 0u, n_allowed = 0u;
   ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
-    atomicAdd(&sh.cnt_hi_w[warp][key >> 8], 1u);
+    atomicAdd(&sh.u.pw.cnt_hi_w[warp][key >> 8], 1u);
     kmax = key > kmax ? key : kmax;
     ++n_allowed;
   });
@@ -2165,7 +2177,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   for (int i = tid; i < 256; i += kThreads) {
     unsigned int c = 0u;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) c += sh.cnt_hi_w[w][i];
+    for (int w = 0; w < kThreads / 32; ++w) c += sh.u.pw.cnt_hi_w[w][i];
     sh.cnt_hi[i] = c;
   }
   if (tid == 0) {
@@ -2203,22 +2215,56 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
       }
     }
     // ---- pass 2: weights per high bin above hi_k; counts + weights per low
-    // byte inside hi_k.
+    // byte inside hi_k.  Key-count mode: dense rows whose high bytes above
+    // hi_k fit kSampleKeySlots rows of kcnt.
+    if (tid == 0) {
+      int n = 0;
+      for (int h = 0; h < 256; ++h) {
+        const bool act = h > hi_k && sh.cnt_hi[h] > 0u;
+        sh.hslot[h] = static_cast<signed char>(act && n < kSampleKeySlots ? n : -1);
+        if (act) {
+          if (n < kSampleKeySlots) sh.slot_h[n] = static_cast<unsigned char>(h);
+          ++n;
+        }
+      }
+      sh.nslots = (total_allowed >= 2048u && n <= kSampleKeySlots) ? n : -1;
+    }
+    __syncthreads();
+    const int nslots = sh.nslots;
+    if (nslots >= 0) {
+      for (int i = tid; i < kSampleKeySlots * 256; i += kThreads) sh.u.kcnt[i >> 8][i & 255] = 0u;
+      __syncthreads();
+    }
     ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
       const int h = static_cast<int>(key >> 8);
       if (h > hi_k) {
-        atomicAdd(&sh.w_hi_w[warp][h], SampleWeight(key, vmax, S.temperature));
+        if (nslots >= 0) atomicAdd(&sh.u.kcnt[sh.hslot[h]][key & 0xffu], 1u);
+        else atomicAdd(&sh.u.pw.w_hi_w[warp][h], SampleWeight(key, vmax, S.temperature));
       } else if (h == hi_k) {
         atomicAdd(&sh.cnt_lo[key & 0xffu], 1u);
         atomicAdd(&sh.w_lo[key & 0xffu], SampleWeight(key, vmax, S.temperature));
       }
     });
     __syncthreads();
-    for (int i = tid; i < 256; i += kThreads) {
-      unsigned long long w = 0ull;
+    if (nslots >= 0) {
+      // Thread t = low byte t: weigh each (high byte, t) key once.
+      for (int sl = 0; sl < nslots; ++sl) {
+        const uint32_t c = sh.u.kcnt[sl][tid];
+        unsigned long long w =
+            c ? static_cast<unsigned long long>(c) * SampleWeight((static_cast<uint32_t>(sh.slot_h[sl]) << 8) | tid,
+                                                                 vmax, S.temperature)
+              : 0ull;
 #pragma unroll
-      for (int ww = 0; ww < kThreads / 32; ++ww) w += sh.w_hi_w[ww][i];
-      sh.w_hi[i] = w;
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (lane == 0 && w) atomicAdd(&sh.w_hi[sh.slot_h[sl]], w);
+      }
+    } else {
+      for (int i = tid; i < 256; i += kThreads) {
+        unsigned long long w = 0ull;
+#pragma unroll
+        for (int ww = 0; ww < kThreads / 32; ++ww) w += sh.u.pw.w_hi_w[ww][i];
+        sh.w_hi[i] = w;
+      }
     }
     __syncthreads();
     int lo_k = 0;
