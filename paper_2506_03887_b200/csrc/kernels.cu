@@ -2316,12 +2316,20 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
       if (lo_p < 0) {
         // ---- pass 3: low-byte weights inside bin hi_p (fully kept_k).
         const int hp = hi_p;
-        ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
-          if (static_cast<int>(key >> 8) == hp) {
-            atomicAdd(&sh.cnt_lo2[key & 0xffu], 1u);
-            atomicAdd(&sh.w_lo2[key & 0xffu], SampleWeight(key, vmax, S.temperature));
-          }
-        });
+        if (nslots >= 0) {  // key counts of bin hp are on chip (kcnt)
+          const uint32_t c = sh.u.kcnt[sh.hslot[hp]][tid];
+          sh.cnt_lo2[tid] = c;
+          sh.w_lo2[tid] = c ? static_cast<unsigned long long>(c) *
+                                  SampleWeight((static_cast<uint32_t>(hp) << 8) | tid, vmax, S.temperature)
+                            : 0ull;
+        } else {
+          ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+            if (static_cast<int>(key >> 8) == hp) {
+              atomicAdd(&sh.cnt_lo2[key & 0xffu], 1u);
+              atomicAdd(&sh.w_lo2[key & 0xffu], SampleWeight(key, vmax, S.temperature));
+            }
+          });
+        }
         __syncthreads();
         unsigned long long c2 = cum;
         for (int l = 255; l >= 0; --l) {
@@ -2370,12 +2378,20 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
         }
         __syncthreads();
         const int hs = h_sel;
-        ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
-          if (static_cast<int>(key >> 8) == hs) {
-            atomicAdd(&sh.cnt_lo2[key & 0xffu], 1u);
-            atomicAdd(&sh.w_lo2[key & 0xffu], SampleWeight(key, vmax, S.temperature));
-          }
-        });
+        if (nslots >= 0) {  // key counts of bin hs are on chip (kcnt)
+          const uint32_t c = sh.u.kcnt[sh.hslot[hs]][tid];
+          sh.cnt_lo2[tid] = c;
+          sh.w_lo2[tid] = c ? static_cast<unsigned long long>(c) *
+                                  SampleWeight((static_cast<uint32_t>(hs) << 8) | tid, vmax, S.temperature)
+                            : 0ull;
+        } else {
+          ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+            if (static_cast<int>(key >> 8) == hs) {
+              atomicAdd(&sh.cnt_lo2[key & 0xffu], 1u);
+              atomicAdd(&sh.w_lo2[key & 0xffu], SampleWeight(key, vmax, S.temperature));
+            }
+          });
+        }
         __syncthreads();
         wl = sh.w_lo2;
       }
