@@ -1,15 +1,15 @@
 #!/usr/bin/env python
 """bench.py — masked decode steps/sec of the constrained-decoding hot path.
 
-Default workload (BASELINE.json configs[1], "config 2"): JSON LR(1) grammar,
-Llama-3-sized vocabulary (128,255 tokens + EOS = 128,256 mask bits), batch
-256 sequences per GPU.  One step = mask fill + in-place bf16 -inf logit
-masking + synthetic-stream sampling + accept_token with restart, for every
-sequence of the batch, as one launch (gm_decode_step_stream; --separate: the
-reference-shaped two calls gm_fill_and_mask_logits + gm_sample_stream_and_accept).
+Default workload (the largest single-GPU BASELINE.json config, "config 3"):
+JSON-schema-derived LR(1) grammar, Llama-3-sized vocabulary (128,255 tokens +
+EOS = 128,256 mask bits), batch 1024 sequences per GPU.  One step = mask fill
++ in-place bf16 -inf logit masking + synthetic-stream sampling + accept_token
+with restart, for every sequence of the batch (gm_decode_step_stream_split:
+the fill and the overlapping sample/accept kernel).
 
-Other BASELINE configs (parity cases for the judge's scaling / extra lines):
-    --config 3   schema grammar (repo-authored, compiled here), batch 1024
+Other BASELINE configs:
+    --config 2   JSON grammar, batch 256/GPU
     --config 4   SQL-subset grammar, 4096 sequences in total split over the
                  GPUs (strong scaling)
     --config 5   JSON, 512/GPU, greedy decode: mask + argmax over the allowed
@@ -18,14 +18,19 @@ Other BASELINE configs (parity cases for the judge's scaling / extra lines):
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
 Under torchrun each rank drives one GPU with its own sequences (no collective
-on the hot path — NCCL only reduces the final timings).  Prints ONE JSON line
-on rank 0.  See DESIGN.md §7 for every field.
+on the hot path — NCCL only reduces the final timings and counters).  Prints
+ONE JSON line on rank 0.  See DESIGN.md §7 for every field.
+
+Both arms print `check`: an FNV-1a digest of the token ids sequences 0..31
+chose in the timed steps and the sum of their mask popcounts (EOS excluded) —
+the GPU arm's timed output must equal the CPU reference's on the same streams.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import sys
 import threading
@@ -37,6 +42,8 @@ sys.path.insert(0, ROOT)
 METRIC = "masked decode steps/sec (batch×steps) and per-step mask latency at 128k vocab"
 UNIT = "seq-steps/s"
 L2_BYTES = 126 * 1024 * 1024
+DIGEST_SEQS = 32
+LOGIT_SEED = 0x5EED10C175  # config 5's synthetic logits (gp_synth_logit)
 
 # BASELINE.json configs (index 1.. = config 2..5).
 CONFIGS = {
@@ -54,6 +61,7 @@ CONFIGS = {
             desc="config5: simulated decode loop, JSON grammar, 128256-bit vocab, batch {b}/GPU: synthetic bf16 "
                  "logits, mask + greedy argmax over allowed ids + DPDA advance"),
 }
+DEFAULT_CONFIG = 3
 
 
 def parse(argv=None):
@@ -62,7 +70,7 @@ def parse(argv=None):
     p.add_argument("--steps", type=int, default=300)
     p.add_argument("--warmup", type=int, default=30)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", type=int, choices=sorted(CONFIGS), default=2)
+    p.add_argument("--config", type=int, choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     p.add_argument("--batch", type=int, default=None, help="sequences per GPU (default: the config's)")
     p.add_argument("--vocab", type=int, default=128255, help="regular tokens (EOS adds one bit)")
     p.add_argument("--grammar", default=None, help="override the config's grammar")
@@ -79,18 +87,17 @@ def parse(argv=None):
     p.add_argument("--prewarm-batch", type=int, default=1024)
     p.add_argument("--stack-cap", type=int, default=1024)
     p.add_argument("--seed", type=int, default=1)
-    p.add_argument("--separate", action="store_true",
-                   help="stream mode: two launches per step (fill+mask logits, then sample+accept; the default)")
-    p.add_argument("--one-launch", action="store_true", help="stream mode: force the one-launch fused step")
-    p.add_argument("--sample-every", type=int, default=16,
-                   help="bracket the roofline kernel with events on every Nth timed step (diagnostics: a large N "
-                        "shows the step rate without the sampled steps)")
-    p.add_argument("--fused", action="store_true", help=argparse.SUPPRESS)  # the default; kept for scripts
+    p.add_argument("--one-launch", action="store_true", help="stream mode: the one-launch fused step")
+    p.add_argument("--no-graph", action="store_true",
+                   help="enqueue every step from Python instead of replaying a captured CUDA graph")
+    p.add_argument("--fill-samples", type=int, default=24,
+                   help="steps of the roofline sub-loop (the fill kernel bracketed by events every step)")
+    p.add_argument("--latency-samples", type=int, default=64,
+                   help="steps of the latency sub-loop (events between steps: per-step latency p50/p99)")
+    p.add_argument("--cold-steps", type=int, default=100, help="steps timed from an empty context table")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
-    p.add_argument("--no-north-star", action="store_true",
-                   help="skip the extra batch-1024 fill-kernel roofline measurement of the default config")
     a = p.parse_args(argv)
     cfg = CONFIGS[a.config]
     a.mode = cfg["mode"]
@@ -122,6 +129,18 @@ def per_gpu_batch(args, world):
     return max(1, b // world) if args.scaling == "strong" else b
 
 
+def rank_seed(seed, rank):
+    """Sequence streams of rank r (sequences are independent: each rank's
+    batch is its own shard; rank 0's equal the CPU reference arm's)."""
+    return seed + 7919 * rank
+
+
+def logits_buffers(B, V1):
+    """Rotating logits buffers: >= 3 x L2 of rows, so no step reads a row
+    still resident in the 126 MB L2."""
+    return max(2, -(-3 * L2_BYTES // (B * V1 * 2)))
+
+
 def max_over_ranks(values, device, world):
     """Max of each timing over all ranks (NCCL on the GPUs, gloo in tests)."""
     if world <= 1:
@@ -133,10 +152,45 @@ def max_over_ranks(values, device, world):
     return [float(v) for v in t]
 
 
+def sum_over_ranks(values, device, world):
+    """Sum of integer counters over all ranks (exact in int64)."""
+    if world <= 1:
+        return [int(v) for v in values]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [int(v) for v in t]
+
+
 def aggregate_rate(world, units_per_rank, seconds):
     """Whole-job throughput: every rank's units over the slowest rank's time
     (each rank owns its own sequences)."""
     return world * units_per_rank / seconds
+
+
+def token_digest(tokens):
+    """FNV-1a over the int32 ids of tokens[seq][step] in (sequence, step)
+    order, 4 little-endian bytes each, >> 11 (ref_decode_run stats[5])."""
+    h = 1469598103934665603
+    for row in tokens:
+        for v in row:
+            v = int(v) & 0xFFFFFFFF
+            for k in range(4):
+                h = ((h ^ ((v >> (8 * k)) & 0xFF)) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h >> 11
+
+
+def summarize(samples):
+    """Summarize (tools/gmask_main.cpp:135-149): mean, and p50/p99 by the
+    rank rule idx = ceil(q*n) - 1."""
+    s = sorted(samples)
+    n = len(s)
+
+    def rank(q):
+        idx = max(0, int(q * n + 0.999999) - 1)
+        return s[min(idx, n - 1)]
+    return {"mean": sum(s) / n, "p50": rank(0.50), "p99": rank(0.99), "n": n}
 
 
 def automaton_bytes(grammar: str) -> bytes:
@@ -152,6 +206,22 @@ def automaton_bytes(grammar: str) -> bytes:
         return f.read()
 
 
+def reference_automaton_bytes(grammar: str) -> bytes:
+    """The CPU arm's automaton, built without the product: the reference's
+    own BuildDpda (oracle/_ref) for the repo-authored grammars, the
+    reference-built fixture otherwise."""
+    bnf = os.path.join(ROOT, "paper_2506_03887_b200", "grammars", grammar + ".bnf")
+    if os.path.exists(bnf):
+        import oracle
+        if oracle.ref_available():
+            rc, flat, _ = oracle.Ref.compile_flat(open(bnf).read())
+            if rc == 0:
+                return flat
+        return automaton_bytes(grammar)
+    with open(os.path.join(ROOT, "tests", "golden", grammar + ".p3dpda"), "rb") as f:
+        return f.read()
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -160,6 +230,17 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -216,18 +297,23 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+# --------------------------------------------------------------------------- CPU reference
 def cpu_reference_run(flat: bytes, vocab, structural, batch_cpu: int, warmup: int, steps: int, seed: int,
-                      threads: int, stack_cap: int, mode: str):
+                      threads: int, stack_cap: int, mode: str, rows: int):
     """The reference matcher (oracle/_ref, built from the reference's own
     sources) or, when absent, the C port — the only oracle use in bench.py."""
     import oracle
+    greedy = mode == "greedy"
     if oracle.ref_available():
         eng = oracle.Ref(flat, vocab)
         stats, _, _ = eng.decode_run(structural, batch_cpu, steps, seed, threads=threads, stack_cap=stack_cap,
-                                     warmup=warmup, logits_row=2 if mode == "greedy" else 1)
+                                     warmup=warmup, logits_row=2 if greedy else 1, rows=rows,
+                                     logit_seed=LOGIT_SEED, digest_seqs=DIGEST_SEQS)
         return stats, "reference", threads
     eng = oracle.Port(flat, vocab)
-    stats, _, _ = eng.decode_run(structural, batch_cpu, warmup + steps, seed, stack_cap=stack_cap)
+    stats, _, _ = eng.decode_run(structural, batch_cpu, warmup + steps, seed, stack_cap=stack_cap,
+                                 greedy_rows=rows if greedy else 0, logit_seed=LOGIT_SEED, warmup=warmup,
+                                 digest_seqs=DIGEST_SEQS)
     stats[0] *= steps / max(1, warmup + steps)
     stats[1] = batch_cpu * steps
     return stats, "port", 1
@@ -239,68 +325,68 @@ def cpu_step_rule(mode):
     return "Engine::ComputeMask + bf16 -inf row mask + stream sample + Step per byte"
 
 
-def calibrated_cpu_sample(flat, vocab, structural, seed, stack_cap, budget_s, mode):
-    threads = os.cpu_count() or 1
-    batch_cpu = 2 * threads
-    st, kind, cores = cpu_reference_run(flat, vocab, structural, batch_cpu, 0, 1, seed, threads, stack_cap, mode)
-    per_step = max(st[0], 1e-4)
-    steps = int(max(2, min(200, budget_s / per_step)))
-    st, kind, cores = cpu_reference_run(flat, vocab, structural, batch_cpu, 1, steps, seed, threads, stack_cap,
-                                        mode)
-    return st, kind, cores, batch_cpu, steps
+def cpu_inputs(args):
+    """The CPU arm's inputs, built from the oracle only (no product code)."""
+    import oracle
+    flat = reference_automaton_bytes(args.grammar)
+    vocab = oracle.synth_vocab(args.vocab, args.flavor)
+    return flat, vocab, oracle.structural_words(vocab)
 
 
-def workload_config(args, world, B):
+def workload_config(args, world, B, R):
     cfg = CONFIGS[args.config]
+    step = ("gm_decode_step_greedy (argmax fill + accept kernels)" if args.mode == "greedy" else
+            "gm_decode_step_stream (one launch)" if args.one_launch else
+            "gm_decode_step_stream_split (fill + overlapped sample/accept kernel: pure-CI sequences sample from "
+            "their cached context row at once, the rest as their fill items arrive)")
     return {"workload": cfg["desc"].format(b=B), "config_index": args.config, "grammar": args.grammar,
             "vocab_bits": args.vocab + 1, "batch_per_gpu": B, "global_batch": B * world,
             "context_depth": args.context_depth, "parent_depth": args.parent_depth, "mode": args.mode,
-            "step": (f"gm_decode_step_greedy (argmax fill + accept kernels; every {args.sample_every}th step with "
-                     "events around its fill kernel)" if args.mode == "greedy" else
-                     "gm_decode_step_stream (one launch)" if args.one_launch else
-                     "gm_decode_step_stream_split (fill + overlapped sample/accept kernel: pure-CI sequences "
-                     "sample from their cached context row at once, the rest as their fill items arrive); "
-                     f"every {args.sample_every}th step with events around its fill kernel (no overlap "
-                     "in that step)"),
-            "context_slots": args.context_slots,
+            "step": step, "context_slots": args.context_slots,
+            "l2": f"inputs larger than L2: {R} rotating logits buffers of {B * (args.vocab + 1) * 2 / 2**20:.0f} MiB "
+                  f"(> 3 x 126 MB L2 in total)",
             "parallelism": f"dp{world} (sequence shards, no hot-path collective)"}
 
 
 def reference_arm(args):
+    """`--impl reference`: the reference's own CPU matcher (oracle/_ref) on
+    all host cores, on this config's streams; rank 0 only."""
     rank, _, world = dist_env()
     if rank != 0:
         return
-    import paper_2506_03887_b200 as pk
-    flat = automaton_bytes(args.grammar)
-    vocab = pk.synth_vocab(args.vocab, args.flavor)
-    structural = pk.structural_words(vocab)
+    flat, vocab, structural = cpu_inputs(args)
     threads = os.cpu_count() or 1
-    batch_cpu = 2 * threads
-    st, kind, cores = cpu_reference_run(flat, vocab, structural, batch_cpu, args.warmup, args.steps, args.seed,
-                                        threads, args.stack_cap, args.mode)
+    batch_cpu = max(DIGEST_SEQS, 2 * threads)
+    B = per_gpu_batch(args, world)
+    R = logits_buffers(B, args.vocab + 1)
+    st, kind, cores = cpu_reference_run(flat, vocab, structural, batch_cpu, args.warmup, args.steps,
+                                        rank_seed(args.seed, 0), threads, args.stack_cap, args.mode, R)
     value = st[1] / st[0]
     sample = (f"{batch_cpu} sequences x {args.steps} timed steps (+{args.warmup} warm-up) of the same "
-              f"workload; per seq-step: {cpu_step_rule(args.mode)}")
-    B = per_gpu_batch(args, world)
+              f"workload (sequences 0..{batch_cpu - 1} of rank 0's streams); per seq-step: "
+              f"{cpu_step_rule(args.mode)}; {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * st[0] / args.steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic", "config": workload_config(args, world, B),
+        "data": "synthetic", "config": workload_config(args, world, B, R),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "mask_latency_us_mean": 1e6 * st[0] / st[1] * cores,
+        "check": {"token_digest": int(st[5]), "popcount_sum": int(st[6]), "sequences": DIGEST_SEQS,
+                  "steps": args.steps, "after_warmup": args.warmup},
     }
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- GPU arm
 def main(argv=None):
     args = parse(argv)
     if args.impl == "reference":
         reference_arm(args)
         return
     rank, local, world = dist_env()
-    import numpy as np  # noqa: F401
+    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2506_03887_b200 as pk
@@ -316,63 +402,99 @@ def main(argv=None):
     automaton = pk.Automaton.load(flat)
     eng = pk.DeviceEngine(automaton, vocab, device=local, context_depth=args.context_depth,
                           context_slots=args.context_slots, parent_depth=args.parent_depth)
+    B = per_gpu_batch(args, world)
+    V, W = eng.V, eng.W
+    V1 = V + 1
+    seed = rank_seed(args.seed, rank)
+    stream = torch.cuda.current_stream()
+    greedy = args.mode == "greedy"
+    R = logits_buffers(B, V1)
+    logits = [torch.empty((B, V1), dtype=torch.bfloat16, device=dev) for _ in range(R)]
+    for k, t in enumerate(logits):
+        if greedy:  # the CPU reference arm reads the same rows (gp_synth_logit)
+            pk.synth_logits(t, k, LOGIT_SEED)
+        else:
+            t.normal_()
+    nseg = eng.info()["num_segments"]
+
+    def make_step(batch, bm, counts, toks):
+        def step(g, bm_=None, counts_=None, toks_=None):
+            """Global step g reads logits buffer g % R (as the CPU arm does)."""
+            bm_ = bm if bm_ is None else bm_
+            counts_ = counts if counts_ is None else counts_
+            toks_ = toks if toks_ is None else toks_
+            if greedy:
+                batch.decode_step_greedy(logits[g % R], tokens_out=toks_, bitmask=bm_)
+            elif args.one_launch:
+                batch.decode_step_stream(seed, bitmask=bm_, logits=logits[g % R], tokens_out=toks_)
+            else:
+                batch.decode_step_stream_split(seed, bitmask=bm_, logits=logits[g % R], seg_counts=counts_,
+                                               tokens_out=toks_)
+        return step
+
+    # ---- cold cache: the first steps from an EMPTY context table (every
+    # context met is built on the device inside the step), events between
+    # steps; other streams than the timed ones.
+    cold = None
+    if args.cold_steps > 0:
+        cb = eng.batch(B, args.stack_cap)
+        cbm = torch.zeros((B, W), dtype=torch.int32, device=dev)
+        ccn = torch.zeros((B, nseg * 2), dtype=torch.int32, device=dev)
+        ctk = torch.zeros(B, dtype=torch.int32, device=dev)
+        cstep = make_step(cb, cbm, ccn, ctk)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.cold_steps + 1)]
+        evs[0].record(stream)
+        seed_saved = seed
+        seed = seed ^ 0xC01DCAFE
+        for i in range(args.cold_steps):
+            cstep(i)
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        seed = seed_saved
+        cb.check()
+        lat = [1e3 * evs[i].elapsed_time(evs[i + 1]) for i in range(args.cold_steps)]
+        cold = dict(summarize(lat), first_step_us=lat[0], unit="us",
+                    contexts_built=eng.info()["context_slots_used"],
+                    note=f"{args.cold_steps} steps of {B} sequences from an empty context table (before the "
+                         "prewarm; streams seeded apart from the timed ones)")
+        del cb, cbm, ccn, ctk
+
     t_pre = time.perf_counter()
     if args.prewarm_steps > 0:
         eng.prewarm(args.prewarm_batch, args.prewarm_steps, seed=0xC0FFEE + rank)
     t_pre = time.perf_counter() - t_pre
     pre_info = eng.info()
-    B = per_gpu_batch(args, world)
-    V, W = eng.V, eng.W
-    V1 = V + 1
+
     batch = eng.batch(B, args.stack_cap)
-    seed = args.seed + 7919 * rank
-    stream = torch.cuda.current_stream()
+    K, Wm = args.steps, args.warmup
     bm = torch.zeros((B, W), dtype=torch.int32, device=dev)
-    counts = torch.zeros((B, batch.nseg * 2), dtype=torch.int32, device=dev)
     toks = torch.zeros(B, dtype=torch.int32, device=dev)
-    row_bytes = B * V1 * 2
-    R = max(2, -(-3 * L2_BYTES // row_bytes))
-    logits = [torch.randn((B, V1), dtype=torch.bfloat16, device=dev) for _ in range(R)]
-    greedy = args.mode == "greedy"
-    # One launch per step wins while the batch leaves the GPU latency-bound;
-    # above 512 sequences the standalone accept kernel's parallelism wins.
-    separate = not greedy and not args.one_launch
+    # Per-timed-step outputs, so the timed region leaves its own evidence:
+    # token ids [K][B] and sampler counts [K][B][nseg][2] (greedy: bitmask
+    # rows [K][B][W] when they fit 8 GB) — written by the kernels in place of
+    # the single buffers, no extra work in the step.
+    toks_all = torch.zeros((K, B), dtype=torch.int32, device=dev)
+    counts_all = None if greedy else torch.zeros((K, B, nseg * 2), dtype=torch.int32, device=dev)
+    counts = torch.zeros((B, nseg * 2), dtype=torch.int32, device=dev)
+    bm_all = None
+    if greedy and K * B * W * 4 <= 8 << 30:
+        bm_all = torch.zeros((K, B, W), dtype=torch.int32, device=dev)
+    step = make_step(batch, bm, counts, toks)
 
-    def step(i):
-        if greedy:
-            batch.decode_step_greedy(logits[i % R], tokens_out=toks, bitmask=bm)
-        elif separate:
-            batch.decode_step_stream_split(seed, bitmask=bm, logits=logits[i % R], seg_counts=counts, tokens_out=toks)
-        else:
-            batch.decode_step_stream(seed, bitmask=bm, logits=logits[i % R], tokens_out=toks)
-
-    for i in range(args.warmup):
+    for i in range(Wm):
         step(i)
     batch.check()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    K = args.steps
-    # The roofline kernel is bracketed by events on every 16th step only: an
-    # event between two launches stops the next kernel from starting under the
-    # previous one's last wave (programmatic dependent launch), which the
-    # other steps keep.
-    SAMPLE_EVERY = max(1, args.sample_every)
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(0, K, SAMPLE_EVERY)]
-    for pair in ev:  # create the CUDA events (their handles go through the C ABI)
-        for e_ in pair:
-            e_.record(stream)
-    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         h0 = time.perf_counter()
         e0.record(stream)
         for i in range(K):
-            timed = i % SAMPLE_EVERY == 0
-            if timed:  # events bracket the step's fill kernel alone (the roofline kernel)
-                batch.time_next_fill(*ev[i // SAMPLE_EVERY])
-            step(i)
+            step(Wm + i, bm_=bm_all[i] if bm_all is not None else None,
+                 counts_=counts_all[i] if counts_all is not None else None, toks_=toks_all[i])
         e1.record(stream)
         h1 = time.perf_counter()
         torch.cuda.synchronize()
@@ -380,58 +502,70 @@ def main(argv=None):
     if world > 1:
         dist.barrier()
     elapsed_ms = e0.elapsed_time(e1)
-    kern = sorted(a.elapsed_time(b) for a, b in ev)
-    kern_ms = sum(kern) / len(kern)
-    kern_p50 = kern[len(kern) // 2]
     host_ms = (h1 - h0) * 1e3 / K
-    elapsed_ms, kern_ms = max_over_ranks([elapsed_ms, kern_ms], dev, world)
-    value = aggregate_rate(world, B * K, elapsed_ms / 1e3)
+    g = Wm + K  # next global step
 
-    # North-star check (BASELINE.json: >= 60 % of HBM bandwidth at batch >= 1024):
-    # the same grammar and step at 1,024 sequences, fill kernel timed alone
-    # (outside the headline timed region; its own warm-up and rotation).
-    north = None
-    if (world == 1 and not args.no_north_star and not greedy and B < 1024 and args.config == 2):
-        Bn = 1024
-        bn = eng.batch(Bn, args.stack_cap)
-        bmn = torch.zeros((Bn, W), dtype=torch.int32, device=dev)
-        cn = torch.zeros((Bn, bn.nseg * 2), dtype=torch.int32, device=dev)
-        tn = torch.zeros(Bn, dtype=torch.int32, device=dev)
-        Rn = max(2, -(-3 * L2_BYTES // (Bn * V1 * 2)))
-        lgn = [torch.randn((Bn, V1), dtype=torch.bfloat16, device=dev) for _ in range(Rn)]
-        for i in range(30):
-            bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn)
-        torch.cuda.synchronize()
-        Kn = 120
-        evn = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(0, Kn, 8)]
-        for pair in evn:
-            for e_ in pair:
-                e_.record(stream)
-        torch.cuda.synchronize()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for i in range(Kn):
-            if i % 8 == 0:
-                bn.time_next_fill(*evn[i // 8])
-            bn.decode_step_stream_split(seed, bitmask=bmn, logits=lgn[i % Rn], seg_counts=cn, tokens_out=tn)
-        f1.record(stream)
-        torch.cuda.synchronize()
-        bn.check()
-        fill_ms_n = sum(a.elapsed_time(c) for a, c in evn) / len(evn)
-        pk_gbs, _, _ = peaks()
-        ach_n = Bn * (2 * V1 + 8 * W) / (fill_ms_n / 1e3) / 1e9
-        north = {"batch": Bn, "step": "gm_decode_step_stream_split (every 8th step with events around its fill)",
-                 "fill_kernel_us": 1e3 * fill_ms_n, "achieved_gbs": ach_n, "frac": ach_n / pk_gbs,
-                 "seq_steps_per_s": Bn * Kn / (f0.elapsed_time(f1) / 1e3), "steps": Kn}
-        del bn, lgn
+    # ---- in-run evidence of the timed steps (sequences 0..31).
+    tk = toks_all[:, :DIGEST_SEQS].cpu().numpy().T  # [seq][step]
+    digest = token_digest(tk)
+    if counts_all is not None:
+        pop = int(counts_all[:, :DIGEST_SEQS, 0::2].to(torch.int64).sum().item())
+    elif bm_all is not None:
+        rows = bm_all[:, :DIGEST_SEQS].cpu().numpy().view(np.uint32).copy()
+        rows[:, :, V >> 5] &= np.uint32(~(1 << (V & 31)) & 0xFFFFFFFF)  # EOS excluded
+        pop = int(np.unpackbits(rows.view(np.uint8)).sum())
+    else:
+        pop = None
+    del bm_all, counts_all
 
-    # Device-counted logit bytes of one more step (outside the timed region).
+    # ---- roofline sub-loop: every step's fill kernel bracketed by events
+    # (an event between two launches stops the accept from overlapping that
+    # fill, so this runs apart from the timed loop).
+    nf = max(10, args.fill_samples)
+    fev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(nf)]
+    for pair in fev:  # create the CUDA events (their handles go through the C ABI)
+        for e_ in pair:
+            e_.record(stream)
+    torch.cuda.synchronize()
+    for i in range(nf):
+        batch.time_next_fill(*fev[i])
+        step(g)
+        g += 1
+    torch.cuda.synchronize()
+    fill = [a.elapsed_time(b) for a, b in fev]
+    fill_ms = sum(fill) / len(fill)
+    fill_s = summarize([1e3 * x for x in fill])
+
+    # ---- latency sub-loop: events between steps (per-step latency, no
+    # overlap with the neighbouring steps).
+    nl = max(10, args.latency_samples)
+    lev = [torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)]
+    lev[0].record(stream)
+    for i in range(nl):
+        step(g)
+        g += 1
+        lev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    step_lat = summarize([1e3 * lev[i].elapsed_time(lev[i + 1]) for i in range(nl)])
+
+    # ---- device-counted logit bytes per sequence-step (stats on, apart).
     batch.set_stats(True)
-    step(K)
+    ns = 8
+    for i in range(ns):
+        step(g)
+        g += 1
     batch.check()
     fstats = batch.fill_stats()
     batch.set_stats(False)
-    max_depth = max(batch.get(b).stack.__len__() for b in range(min(B, 256)))
+    logit_rd = fstats["logit_bytes_read"] / (B * ns)
+    logit_wr = fstats["logit_bytes_written"] / (B * ns)
+    max_depth = max(len(batch.get(b).stack) for b in range(min(B, 256)))
+    counters = batch.counters()
+
+    elapsed_ms, fill_ms = max_over_ranks([elapsed_ms, fill_ms], dev, world)
+    value = aggregate_rate(world, B * K, elapsed_ms / 1e3)
+    tot_seq_steps, tot_restarts, digest_sum = sum_over_ranks(
+        [B * K, counters["restarts"], digest], dev, world)
 
     # ---- e2e through the public C ABI with host buffers, driven by a C++
     # caller (paper_2506_03887_b200/tools/e2e_driver.cpp; Python's per-call
@@ -468,12 +602,11 @@ def main(argv=None):
         if rc != 0:
             raise RuntimeError(f"e2e driver failed: {rc} {pk.lib().gm_last_error().decode()}")
         t_full, t_ids = max_over_ranks([t_full, secs.value], dev, world)
-        t_e2e = t_full
         path = ("C++ caller: gm_decode_step_greedy(device logits) → ids into mapped host memory; D2H bitmask "
                 "on a copy stream" if greedy else "C++ caller: H2D ids → gm_accept_tokens → "
                 "gm_fill_and_mask_logits → gm_sample_stream (ids into mapped host memory) → stream sync; D2H "
                 "bitmask on a copy stream (double-buffered)")
-        e2e = {"value": aggregate_rate(world, B * Ke, t_e2e), "unit": UNIT,
+        e2e = {"value": aggregate_rate(world, B * Ke, t_full), "unit": UNIT,
                "h2d_bytes_per_step": 0 if greedy else B * 4, "d2h_bytes_per_step": B * W * 4 + B * 4,
                "steps": Ke, "path": path,
                "ids_only": {"value": aggregate_rate(world, B * Ke, t_ids), "d2h_bytes_per_step": B * 4,
@@ -485,57 +618,87 @@ def main(argv=None):
         return
 
     peak, peak_src, _ = peaks()
-    alg_bytes_seq = 2 * V1 + 8 * W          # write-only -inf / read-once argmax formulation
-    achieved = B * alg_bytes_seq / (kern_ms / 1e3) / 1e9
+    if greedy:
+        # Bytes the argmax formulation moves (never count bytes
+        # it does not have to move): bitmask write + context bitset read + the
+        # 16-B logit chunks holding an allowed token (device-counted).
+        alg_bytes_seq = 8 * W + logit_rd
+        alg_rule = "8W (bitmask write + CI read) + device-counted allowed-chunk logit reads"
+    else:
+        alg_bytes_seq = 2 * V1 + 8 * W  # write-only -inf formulation
+        alg_rule = "2(V+1) (-inf row write) + 8W (bitmask write + CI read); mixed-chunk reads not counted"
+    achieved = B * alg_bytes_seq / (fill_ms / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            key = f"{args.grammar}:{args.vocab}:{B}:{args.mode}:{'separate' if separate else 'fused'}"
+            key = f"{args.grammar}:{args.vocab}:{B}:{args.mode}:{'fused' if args.one_launch else 'separate'}"
             entry = json.load(open(tpath)).get(key)
             traffic = entry["dram_bytes_per_launch"] if entry else None
         except Exception:
             traffic = None
 
+    # ---- CPU reference beside the GPU (rank 0, N=1): the reference matcher
+    # on the host cores over a bounded sample, and its digest of the SAME
+    # timed steps of sequences 0..31 (the parity check of the timed output).
     cpu = None
+    check = {"token_digest": digest, "popcount_sum": pop, "sequences": DIGEST_SEQS, "steps": K,
+             "after_warmup": Wm}
     if world == 1 and not args.no_cpu_baseline:
-        st, kind, cores, bcpu, steps_cpu = calibrated_cpu_sample(flat, vocab, eng.structural, args.seed,
-                                                                 args.stack_cap, args.cpu_seconds, args.mode)
+        cflat, cvocab, cstruct = cpu_inputs(args)
+        threads = os.cpu_count() or 1
+        st, kind, cores = cpu_reference_run(cflat, cvocab, cstruct, DIGEST_SEQS, Wm, K, seed, threads,
+                                            args.stack_cap, args.mode, R)
+        check.update(cpu_reference_digest=int(st[5]), cpu_reference_popcount=int(st[6]), cpu_kind=kind,
+                     equal=(int(st[5]) == digest and (pop is None or int(st[6]) == pop)))
+        bcpu = max(DIGEST_SEQS, 2 * threads)
+        st, kind, cores = cpu_reference_run(cflat, cvocab, cstruct, bcpu, 0, 1, seed, threads, args.stack_cap,
+                                            args.mode, R)
+        steps_cpu = int(max(2, min(200, args.cpu_seconds / max(st[0], 1e-4))))
+        st, kind, cores = cpu_reference_run(cflat, cvocab, cstruct, bcpu, 1, steps_cpu, seed, threads,
+                                            args.stack_cap, args.mode, R)
+        st1, _, _ = cpu_reference_run(cflat, cvocab, cstruct, 4, 1, max(2, steps_cpu // 4), seed, 1,
+                                      args.stack_cap, args.mode, R)
         cpu = {"value": st[1] / st[0], "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{bcpu} sequences x {steps_cpu} steps of the same workload ({st[0]:.1f} s), "
-                         f"threads={cores}, per seq-step {cpu_step_rule(args.mode)}"}
+                         f"threads={cores}, per seq-step {cpu_step_rule(args.mode)}",
+               "cpu_model": cpu_model(), "one_core": {"value": st1[1] / st1[0], "unit": UNIT,
+                                                      "sample": f"4 sequences x {max(2, steps_cpu // 4)} steps"}}
 
     info = eng.info()
     kname = ("FillKernel<greedy> (mask + argmax over allowed logits; accept runs in AcceptKernel)" if greedy else
-             "FillKernel (fill + -inf logits; accept runs in AcceptKernel)" if separate else
-             "FillKernel (one-launch step: fill + -inf logits + sample/accept tail)")
+             "FillKernel (one-launch step: fill + -inf logits + sample/accept tail)" if args.one_launch else
+             "FillKernel (fill + -inf logits; accept runs in AcceptKernel)")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wm,
         "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-        "dtype": "int32", "data": "synthetic (seeded token-level streams, random bf16 logits)",
-        "config": dict(workload_config(args, world, B),
-                       l2=f"rotating {R} logits buffers of {row_bytes / 2**20:.0f} MiB (> 126 MB L2)"),
-        "mask_latency_us": 1e3 * kern_ms,
-        "step_breakdown_us": {"roofline_kernel_mean": 1e3 * kern_ms, "roofline_kernel_p50": 1e3 * kern_p50,
+        "dtype": "int32", "data": "synthetic (seeded token-level streams, "
+                                  + ("gp_synth_logit bf16 logits)" if greedy else "random bf16 logits)"),
+        "config": workload_config(args, world, B, R),
+        "mask_latency_us": 1e3 * fill_ms,
+        "step_latency_us": step_lat,
+        "step_breakdown_us": {"step_mean_timed_loop": 1e3 * elapsed_ms / K, "roofline_kernel": fill_s,
                               "host_enqueue_per_step": 1e3 * host_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": kname,
-                     "alg_bytes_per_seq_step": alg_bytes_seq,
-                     "device_counted_logit_bytes_per_seq_step": (fstats["logit_bytes_read"] +
-                                                                 fstats["logit_bytes_written"]) / B},
+                     "samples": nf, "alg_bytes_per_seq_step": alg_bytes_seq, "alg_bytes_rule": alg_rule,
+                     "device_counted_logit_bytes_per_seq_step": {"read": logit_rd, "written": logit_wr}},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "check": check,
         "gpu_launches": K * (1 if args.one_launch else 2),  # split / greedy: fill + accept per step
         "clocks": clocks.summary(),
+        "cold_cache": cold,
         "preprocessing": {"compile_s": t_comp, "prewarm_s": t_pre,
                           "prewarm": f"{args.prewarm_steps} steps x {args.prewarm_batch} seqs "
-                          f"(seed differs from the timed streams)", "contexts_after_prewarm": pre_info["context_slots_used"],
+                          f"(seed differs from the timed streams)",
+                          "contexts_after_prewarm": pre_info["context_slots_used"],
                           "automaton": automaton.info()},
         "cache": {"contexts": info["context_slots_used"], "segment_builds": info["segment_builds"],
                   "private_builds": info["private_builds"], "parent_builds": info["parent_builds"],
                   "last_fill": fstats},
+        "totals": {"seq_steps": tot_seq_steps, "restarts": tot_restarts, "digest_sum_over_ranks": digest_sum},
         "max_stack_depth_seen": max_depth,
-        "north_star_batch1024": north,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -79,7 +79,7 @@ class Ref:
                 "ref_allowed": ([P, P, P, P], None),
                 "ref_mask": ([P, P, P, P], None),
                 "ref_mask_naive": ([P, P, P, P, I32, P], None),
-                "ref_decode_run": ([P, P, P, I32, I32, I32, U64, I32, I32, I32, P, P, P], ctypes.c_int),
+                "ref_decode_run": ([P, P, P, I32, I32, I32, U64, I32, I32, I32, P, P, P, I32, U64, I32], ctypes.c_int),
                 "ref_sample_sentence": ([ctypes.c_char_p, U64, I32, ctypes.c_char_p, I32], I32),
             }
             opt = {  # present when the reference's serialize.cpp was built (json.hpp found)
@@ -258,16 +258,20 @@ class Ref:
 
     def decode_run(self, structural: np.ndarray, batch: int, steps: int, seed: int, threads: int,
                    stack_cap: int = 1024, logits_row: int = 1, want_tokens: bool = False,
-                   want_stacks: bool = False, warmup: int = 0):
-        """stats[0] = seconds of the `steps` timed steps (after `warmup`).
-        logits_row: 0 mask only, 1 + bf16 -inf row (stream sampler),
-        2 greedy argmax over synthetic bf16 rows (config 5)."""
+                   want_stacks: bool = False, warmup: int = 0, rows: int = 1, logit_seed: int = 0,
+                   digest_seqs: int = 32):
+        """stats[0] = seconds of the `steps` timed steps (after `warmup`);
+        [5]/[6] = token digest / mask popcount (EOS excluded) of sequences
+        < digest_seqs over the timed steps.  logits_row: 0 mask only, 1 +
+        bf16 -inf row (stream sampler), 2 greedy argmax over synthetic bf16
+        rows (config 5; buffer step % rows, gp_synth_logit)."""
         stats = np.zeros(8, np.float64)
         toks = np.zeros((batch, warmup + steps), np.int32) if want_tokens else None
         stk = np.zeros((batch, stack_cap + 2), np.int32) if want_stacks else None
         self.lib().ref_decode_run(self.h, self.trie, _ptr(structural), batch, warmup, steps, seed, threads, stack_cap,
                                   int(logits_row), _ptr(stats), _ptr(toks) if toks is not None else None,
-                                  _ptr(stk) if stk is not None else None)
+                                  _ptr(stk) if stk is not None else None, rows, logit_seed & (2**64 - 1),
+                                  digest_seqs)
         return stats, toks, stk
 
     def __del__(self):
@@ -277,6 +281,66 @@ class Ref:
                 L.ref_trie_free(self.trie)
             if getattr(self, "h", None):
                 L.ref_engine_free(self.h)
+
+
+class _RunOpts(ctypes.Structure):
+    _fields_ = [("mode", I32), ("rows", I32), ("logit_seed", U64), ("warmup", I32), ("digest_seqs", I32),
+                ("mask_hash", ctypes.c_void_p)]
+
+
+def _port_lib():
+    return Port.lib()
+
+
+def synth_vocab(num_tokens: int, flavor: int = 0) -> List[bytes]:
+    """The bench vocabulary restated in the C port (gp_synth_vocab:
+    WriteBenchVocab, acceptance_main.cpp:341-359, continued) — the CPU arm's
+    own input, independent of the product library."""
+    L = _port_lib()
+    n = L.gp_synth_vocab(num_tokens, flavor, None, 0, None)
+    if n < 0:
+        raise ValueError("bad vocabulary size")
+    buf = np.zeros(max(n, 1), np.uint8)
+    offs = np.zeros(num_tokens + 1, np.int64)
+    L.gp_synth_vocab(num_tokens, flavor, _ptr(buf), n, _ptr(offs))
+    raw = buf.tobytes()
+    return [raw[offs[i]:offs[i + 1]] for i in range(num_tokens)]
+
+
+def structural_words(tokens: Sequence[bytes]) -> np.ndarray:
+    data, offs = pack(tokens)
+    words = np.zeros((len(tokens) + 1 + 31) // 32, np.uint32)
+    _port_lib().gp_structural_words(_ptr(data), _ptr(offs), len(tokens), _ptr(words))
+    return words
+
+
+def synth_logit_row(seed: int, k: int, b: int, n: int) -> np.ndarray:
+    """gp_synth_logit row (config 5's synthetic bf16 logits), uint16 bits."""
+    row = np.zeros(n, np.uint16)
+    _port_lib().gp_synth_logit_row(seed & (2**64 - 1), k, b, n, _ptr(row))
+    return row
+
+
+_HASH_POW = {}
+
+
+def mask_hashes(masks: np.ndarray) -> np.ndarray:
+    """gp_mask_hash of every row of a [..., nw] uint32 mask array (numpy,
+    wrapping uint64 arithmetic)."""
+    m = np.ascontiguousarray(masks).view(np.uint32)
+    nw = m.shape[-1]
+    pw = _HASH_POW.get(nw)
+    if pw is None:
+        pw = np.zeros(nw, np.uint64)
+        M = np.uint64(0x9E3779B97F4A7C15)
+        p = M
+        with np.errstate(over="ignore"):
+            for i in range(nw):
+                pw[i] = p
+                p = p * M
+        _HASH_POW[nw] = pw
+    with np.errstate(over="ignore"):
+        return (m.astype(np.uint64) * pw).sum(axis=-1, dtype=np.uint64)
 
 
 class _Cfg(ctypes.Structure):
@@ -312,7 +376,11 @@ class Port:
                 "gp_greedy_pick": ([P, P, I32], I32),
                 "gp_sample_pick": ([P, P, I32, ctypes.c_float, I32, ctypes.c_uint32, U64], I32),
                 "gp_sample_weight": ([ctypes.c_uint32, ctypes.c_float, ctypes.c_float], U64),
-                "gp_decode_run": ([P, P, P, P, P, I32, I32, U64, I32, P, P, P], ctypes.c_int),
+                "gp_decode_run": ([P, P, P, P, P, I32, I32, U64, I32, P, P, P, P], ctypes.c_int),
+                "gp_synth_vocab": ([I32, I32, P, I64, P], I64),
+                "gp_structural_words": ([P, P, I32, P], I32),
+                "gp_synth_logit_row": ([U64, I32, I32, I32, P], None),
+                "gp_mask_hash": ([P, I32], U64),
             }
             for n, (a, r) in sigs.items():
                 f = getattr(L, n)
@@ -413,13 +481,23 @@ class Port:
         return self.lib().gp_greedy_pick(_ptr(mask), _ptr(logits_bf16), self.V)
 
     def decode_run(self, structural: np.ndarray, batch: int, steps: int, seed: int, stack_cap: int = 1024,
-                   want_tokens: bool = False, want_stacks: bool = False):
+                   want_tokens: bool = False, want_stacks: bool = False, want_mask_hashes: bool = False,
+                   greedy_rows: int = 0, logit_seed: int = 0, warmup: int = 0, digest_seqs: int = 0):
+        """The C port's decode loop.  greedy_rows > 0: greedy over
+        gp_synth_logit rows (buffer step % greedy_rows) instead of the stream
+        sampler.  want_mask_hashes: [batch][steps] gp_mask_hash of every
+        mask (compare with mask_hashes() of device bitmasks)."""
         stats = np.zeros(8, np.float64)
         toks = np.zeros((batch, steps), np.int32) if want_tokens else None
         stk = np.zeros((batch, stack_cap + 2), np.int32) if want_stacks else None
+        mh = np.zeros((batch, steps), np.uint64) if want_mask_hashes else None
+        opts = _RunOpts(1 if greedy_rows > 0 else 0, max(1, greedy_rows), logit_seed & (2**64 - 1), warmup,
+                        digest_seqs, mh.ctypes.data if mh is not None else None)
         self.lib().gp_decode_run(self.a, self.trie, _ptr(self._data), _ptr(self._offs), _ptr(structural), batch,
                                  steps, seed, stack_cap, _ptr(stats), _ptr(toks) if toks is not None else None,
-                                 _ptr(stk) if stk is not None else None)
+                                 _ptr(stk) if stk is not None else None, ctypes.byref(opts))
+        if want_mask_hashes:
+            return stats, toks, stk, mh
         return stats, toks, stk
 
     def __del__(self):

@@ -383,7 +383,7 @@ int32_t gp_stream_pick(const uint32_t* mask, const uint32_t* structural, int32_t
   int32_t n_all = count_bits(mask, NULL, V);
   int eos = (int)((mask[V >> 5] >> (V & 31)) & 1u);
   if (n_all == 0) return eos ? V : -1;
-  if (eos && ((u >> 32) & 3u) != 0) return V;
+  if (eos && ((u >> 32) & 3u) == 0) return V; /* EOS with probability 1/4 */
   uint32_t lo = (uint32_t)u;
   if ((u >> 34) & 1u) {
     int32_t n_s = structural ? count_bits(mask, structural, V) : 0;
@@ -516,11 +516,178 @@ int32_t gp_sample_pick(const uint32_t* mask, const uint16_t* logits, int32_t V, 
   return tok;
 }
 
+/* ------------------------------------------------------------ workload restatements
+ * Synthetic inputs restated here so the CPU arm of bench.py needs nothing
+ * from the product library (tests check both generators agree byte for
+ * byte, and make_golden.py checks the 32k vocabulary against the reference's
+ * own WriteBenchVocab, tests/acceptance/acceptance_main.cpp:341-359). */
+
+/* std::mt19937_64 (the reference's generator). */
+typedef struct { uint64_t mt[312]; int i; } mt64;
+static void mt64_seed(mt64* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < 312; ++i) g->mt[i] = 6364136223846793005ull * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->i = 312;
+}
+static uint64_t mt64_next(mt64* g) {
+  if (g->i >= 312) {
+    for (int k = 0; k < 312; ++k) {
+      uint64_t x = (g->mt[k] & 0xFFFFFFFF80000000ull) | (g->mt[(k + 1) % 312] & 0x7FFFFFFFull);
+      uint64_t xa = x >> 1;
+      if (x & 1u) xa ^= 0xB5026F5AA96619E9ull;
+      g->mt[k] = g->mt[(k + 156) % 312] ^ xa;
+    }
+    g->i = 0;
+  }
+  uint64_t y = g->mt[g->i++];
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  y ^= y >> 43;
+  return y;
+}
+
+typedef struct { char s[16]; int32_t n; } vtok;
+
+static int vtok_cmp(const void* x, const void* y) {
+  const vtok* a = (const vtok*)x;
+  const vtok* b = (const vtok*)y;
+  int32_t m = a->n < b->n ? a->n : b->n;
+  int c = memcmp(a->s, b->s, (size_t)m);
+  return c ? c : (a->n > b->n) - (a->n < b->n);
+}
+
+static uint64_t vtok_hash(const char* s, int32_t n) {
+  uint64_t h = 1469598103934665603ull;
+  for (int32_t i = 0; i < n; ++i) h = (h ^ (uint8_t)s[i]) * 1099511628211ull;
+  return h | 1u;
+}
+
+/* WriteBenchVocab (acceptance_main.cpp:341-359), continued past 32,000 and
+ * with the SQL flavour (flavor 1) of the product's workload generator:
+ * fragments, then mt19937_64(424242) tokens until `n` distinct, sorted
+ * (std::set order).  Returns the byte total; bytes/offs may be NULL. */
+int64_t gp_synth_vocab(int32_t n, int32_t flavor, uint8_t* bytes, int64_t cap, int64_t* offs) {
+  static const char* frags[] = {"true", "false", "null", "{\"", " \"", "\":", "\",", "\"}", "},", "],", "[{", "}}",
+                                "]}", "0.", "e+", ", ", "\": \"", "0", "1", "2", "3", "4", "5", "6", "7", "8", "9"};
+  static const char* sql[] = {"SELECT ", "FROM ", "WHERE ", "AND ", "OR ", "ORDER ", "BY ", "ASC", "DESC",
+                              "COUNT", "SUM", "MAX", "MIN", "(", ")", "* ", "= ", "< ", "> ", ", "};
+  char alphabet[128] = "abcdefghijklmnopqrstuvwxyz0123456789{}[],:\" .-+eE_";
+  if (n < 27) return -1;
+  if (flavor == 1) strcat(alphabet, "ABCDEFGHIJKLMNOPQRSTUVWXYZ()*=<>");
+  const uint64_t na = (uint64_t)strlen(alphabet);
+  size_t slots = 16;
+  while (slots < (size_t)n * 2) slots <<= 1;
+  uint64_t* hs = (uint64_t*)calloc(slots, sizeof(uint64_t));
+  int32_t* hi = (int32_t*)malloc(sizeof(int32_t) * slots);
+  vtok* toks = (vtok*)malloc(sizeof(vtok) * (size_t)n);
+  int32_t count = 0;
+  /* insert: returns 1 when new */
+#define GP_INSERT(str, len)                                                              \
+  do {                                                                                   \
+    uint64_t h_ = vtok_hash((str), (len));                                               \
+    size_t j_ = (size_t)h_ & (slots - 1);                                                \
+    int dup_ = 0;                                                                        \
+    while (hs[j_]) {                                                                     \
+      if (hs[j_] == h_ && toks[hi[j_]].n == (len) && !memcmp(toks[hi[j_]].s, (str), (size_t)(len))) { \
+        dup_ = 1;                                                                        \
+        break;                                                                           \
+      }                                                                                  \
+      j_ = (j_ + 1) & (slots - 1);                                                       \
+    }                                                                                    \
+    if (!dup_ && count < n) {                                                            \
+      hs[j_] = h_;                                                                       \
+      hi[j_] = count;                                                                    \
+      memcpy(toks[count].s, (str), (size_t)(len));                                       \
+      toks[count].n = (len);                                                             \
+      ++count;                                                                           \
+    }                                                                                    \
+  } while (0)
+  for (size_t k = 0; k < sizeof(frags) / sizeof(frags[0]); ++k) GP_INSERT(frags[k], (int32_t)strlen(frags[k]));
+  if (flavor == 1) {
+    for (size_t k = 0; k < sizeof(sql) / sizeof(sql[0]); ++k) GP_INSERT(sql[k], (int32_t)strlen(sql[k]));
+  }
+  mt64 g;
+  mt64_seed(&g, 424242u);
+  static const int32_t lens[] = {1, 2, 2, 3, 3, 4, 5, 6, 8};
+  while (count < n) {
+    int32_t len = lens[mt64_next(&g) % 9u];
+    char t[16];
+    for (int32_t i = 0; i < len; ++i) t[i] = alphabet[mt64_next(&g) % na];
+    GP_INSERT(t, len);
+  }
+#undef GP_INSERT
+  qsort(toks, (size_t)n, sizeof(vtok), vtok_cmp);
+  int64_t total = 0;
+  for (int32_t i = 0; i < n; ++i) total += toks[i].n;
+  if (bytes && offs) {
+    if (cap < total) total = -2;
+    else {
+      int64_t o = 0;
+      for (int32_t i = 0; i < n; ++i) {
+        offs[i] = o;
+        memcpy(bytes + o, toks[i].s, (size_t)toks[i].n);
+        o += toks[i].n;
+      }
+      offs[n] = o;
+    }
+  }
+  free(hs); free(hi); free(toks);
+  return total;
+}
+
+/* Tokens holding any of {}[],:" (the stream sampler's structural set). */
+int32_t gp_structural_words(const uint8_t* bytes, const int64_t* offs, int32_t n, uint32_t* words) {
+  int32_t nw = (n + 1 + 31) / 32, c = 0;
+  memset(words, 0, sizeof(uint32_t) * (size_t)nw);
+  for (int32_t t = 0; t < n; ++t) {
+    for (int64_t i = offs[t]; i < offs[t + 1]; ++i) {
+      if (bytes[i] && strchr("{}[],:\"", bytes[i])) {
+        words[t >> 5] |= 1u << (t & 31);
+        ++c;
+        break;
+      }
+    }
+  }
+  return c;
+}
+
+/* Synthetic bf16 logit of token t in row b of rotating buffer k (config 5's
+ * greedy decode loop; the device bench fills its buffers with the same
+ * function, kernels in workload.cu).  Values in (-2, 2), 2,048 distinct, so
+ * ties (broken by the lowest id) are common. */
+uint16_t gp_synth_logit(uint64_t seed, int32_t k, int32_t b, int32_t t) {
+  uint64_t h = mix64(seed ^ 0x6C6F67697473ull ^ ((uint64_t)(uint32_t)k * 0xA24BAED4963EE407ull) ^
+                     ((uint64_t)(uint32_t)b * 0xD1B54A32D192ED03ull));
+  uint64_t x = mix64(h ^ (uint64_t)(uint32_t)t);
+  return (uint16_t)((0x3C00u + (uint32_t)(x & 0x3FFu)) ^ (((x >> 20) & 1u) ? 0x8000u : 0u));
+}
+
+void gp_synth_logit_row(uint64_t seed, int32_t k, int32_t b, int32_t n, uint16_t* row) {
+  for (int32_t t = 0; t < n; ++t) row[t] = gp_synth_logit(seed, k, b, t);
+}
+
+/* Polynomial hash of a mask row (sum of w_i * M^(i+1) mod 2^64): the
+ * per-step mask digests of the decode loop, recomputed by the tests from
+ * device bitmasks with numpy. */
+uint64_t gp_mask_hash(const uint32_t* words, int32_t nw) {
+  const uint64_t M = 0x9E3779B97F4A7C15ull;
+  uint64_t h = 0, p = M;
+  for (int32_t i = 0; i < nw; ++i) {
+    h += (uint64_t)words[i] * p;
+    p *= M;
+  }
+  return h;
+}
+
 /* ------------------------------------------------------------ decode loop */
 int gp_decode_run(const gp_automaton* a, const gp_trie* t, const uint8_t* bytes,
                   const int64_t* offs, const uint32_t* structural, int32_t batch, int32_t steps,
                   uint64_t seed, int32_t stack_cap, double* stats, int32_t* tokens_out,
-                  int32_t* final_stacks) {
+                  int32_t* final_stacks, const gp_run_opts* opts) {
+  gp_run_opts o;
+  memset(&o, 0, sizeof(o));
+  if (opts) o = *opts;
   int32_t V = t->num_tokens;
   int32_t nw = (V + 1 + 31) / 32;
   uint32_t* mask = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nw);
@@ -528,7 +695,7 @@ int gp_decode_run(const gp_automaton* a, const gp_trie* t, const uint8_t* bytes,
   gp_config* cfgs = (gp_config*)calloc((size_t)batch, sizeof(gp_config));
   int32_t* chosen = (int32_t*)malloc(sizeof(int32_t) * (size_t)batch * (size_t)steps);
   for (int32_t b = 0; b < batch; ++b) gp_config_init(a, &cfgs[b]);
-  int64_t restarts = 0, pops = 0;
+  int64_t restarts = 0, pops = 0, wpops = 0;
   struct timespec t0, t1;
   clock_gettime(CLOCK_MONOTONIC, &t0);
   for (int32_t s = 0; s < steps; ++s) {
@@ -536,10 +703,18 @@ int gp_decode_run(const gp_automaton* a, const gp_trie* t, const uint8_t* bytes,
       gp_config* c = &cfgs[b];
       gp_mask(a, c, t, mask);
       pops += count_bits(mask, NULL, V + 1);
-      for (int32_t i = 0; i <= V; ++i) {
-        if (!((mask[i >> 5] >> (i & 31)) & 1u)) row[i] = 0xFF80u;
+      if (b < o.digest_seqs && s >= o.warmup) wpops += count_bits(mask, NULL, V);
+      if (o.mask_hash) o.mask_hash[(int64_t)b * steps + s] = gp_mask_hash(mask, nw);
+      int32_t tok;
+      if (o.mode == 1) {
+        gp_synth_logit_row(o.logit_seed, s % (o.rows > 0 ? o.rows : 1), b, V + 1, row);
+        tok = gp_greedy_pick(mask, row, V);
+      } else {
+        for (int32_t i = 0; i <= V; ++i) {
+          if (!((mask[i >> 5] >> (i & 31)) & 1u)) row[i] = 0xFF80u;
+        }
+        tok = gp_stream_pick(mask, structural, V, gp_stream_draw(seed, (uint64_t)b, (uint64_t)s));
       }
-      int32_t tok = gp_stream_pick(mask, structural, V, gp_stream_draw(seed, (uint64_t)b, (uint64_t)s));
       chosen[(int64_t)b * steps + s] = tok;
       int overflow = 0;
       if (tok == V) {
@@ -557,17 +732,25 @@ int gp_decode_run(const gp_automaton* a, const gp_trie* t, const uint8_t* bytes,
     }
   }
   clock_gettime(CLOCK_MONOTONIC, &t1);
-  uint64_t digest = 1469598103934665603ull;
+  uint64_t digest = 1469598103934665603ull, wdigest = 1469598103934665603ull;
   for (int64_t i = 0; i < (int64_t)batch * steps; ++i) {
     uint32_t v = (uint32_t)chosen[i];
     for (int k = 0; k < 4; ++k) digest = (digest ^ ((v >> (8 * k)) & 0xffu)) * 1099511628211ull;
     if (tokens_out) tokens_out[i] = chosen[i];
+  }
+  for (int32_t b = 0; b < batch && b < o.digest_seqs; ++b) {
+    for (int32_t s = o.warmup; s < steps; ++s) {
+      uint32_t v = (uint32_t)chosen[(int64_t)b * steps + s];
+      for (int k = 0; k < 4; ++k) wdigest = (wdigest ^ ((v >> (8 * k)) & 0xffu)) * 1099511628211ull;
+    }
   }
   stats[0] = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
   stats[1] = (double)batch * steps;
   stats[2] = (double)restarts;
   stats[3] = (double)(digest >> 11);
   stats[4] = (double)pops;
+  stats[5] = (double)(wdigest >> 11);
+  stats[6] = (double)wpops;
   if (final_stacks) {
     for (int32_t b = 0; b < batch; ++b) {
       int32_t* r = final_stacks + (int64_t)b * (stack_cap + 2);

@@ -64,14 +64,32 @@ int32_t gp_sample_pick(const uint32_t* mask, const uint16_t* logits_bf16, int32_
                        int32_t top_k, uint32_t top_p24, uint64_t u);
 uint64_t gp_sample_weight(uint32_t key, float vmax, float temperature);
 
+/* Options of gp_decode_run (NULL = stream sampler, no window digests). */
+typedef struct gp_run_opts {
+  int32_t mode;          /* 0: stream sampler; 1: greedy over gp_synth_logit rows */
+  int32_t rows;          /* greedy: rotating buffers, step s reads buffer s % rows */
+  uint64_t logit_seed;   /* greedy: gp_synth_logit seed */
+  int32_t warmup;        /* steps before the digest window */
+  int32_t digest_seqs;   /* sequences [0, n) enter stats[5] and stats[6] */
+  uint64_t* mask_hash;   /* [batch][steps] gp_mask_hash of every mask, or NULL */
+} gp_run_opts;
+
 /* Decode loop over `batch` sequences, `steps` steps, restart on finish (same
  * contract as ref_decode_run in oracle/ref_shim.cpp, single thread).
  * stats: [0] seconds, [1] seq-steps, [2] restarts, [3] token digest>>11,
- * [4] mask popcount sum. */
+ * [4] mask popcount sum, [5] token digest>>11 of sequences < digest_seqs over
+ * steps >= warmup, [6] their mask popcounts (EOS excluded). */
 int gp_decode_run(const gp_automaton* a, const gp_trie* t, const uint8_t* bytes,
                   const int64_t* offs, const uint32_t* structural, int32_t batch, int32_t steps,
                   uint64_t seed, int32_t stack_cap, double* stats, int32_t* tokens_out,
-                  int32_t* final_stacks);
+                  int32_t* final_stacks, const gp_run_opts* opts);
+
+/* Workload restatements (see gmask_port.c). */
+int64_t gp_synth_vocab(int32_t n, int32_t flavor, uint8_t* bytes, int64_t cap, int64_t* offs);
+int32_t gp_structural_words(const uint8_t* bytes, const int64_t* offs, int32_t n, uint32_t* words);
+uint16_t gp_synth_logit(uint64_t seed, int32_t k, int32_t b, int32_t t);
+void gp_synth_logit_row(uint64_t seed, int32_t k, int32_t b, int32_t n, uint16_t* row);
+uint64_t gp_mask_hash(const uint32_t* words, int32_t nw);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,12 @@ Outputs
                                   exported to the flat P3DPDA v1 format;
                                   digits_noagg.p3dpda = aggregate off.
   tests/golden/vectors.json       known-answer tests (see keys below).
+  tests/golden/acceptance_masks.json
+                                  acceptance criterion 3 at the reference's own
+                                  scale and seeds (acceptance_main.cpp:202-219,
+                                  through oracle/_ref/libgmask_acc.so): per
+                                  fixture the 1,000-token SampleVocab, the 200
+                                  SampleConfigs and their reference masks.
 """
 from __future__ import annotations
 
@@ -26,8 +32,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import oracle  # noqa: E402
 from oracle import Ref, read_flat  # noqa: E402
-import paper_2506_03887_b200 as pk  # noqa: E402  (synthetic vocab generator only)
+import paper_2506_03887_b200 as pk  # noqa: E402  (cross-check of the product's vocab generator only)
 
 GRAMMARS = os.environ.get("GMASK_GRAMMAR_DIR", "/root/reference/proj/grammars")
 OUT = os.path.join(ROOT, "tests", "golden")
@@ -83,6 +90,63 @@ def sample_configs(ref: Ref, count: int, max_prefix: int, rng: random.Random):
         ref.step(c, bytes_[rng.randrange(len(bytes_))])
     ref.free_cfg(c)
     return out
+
+
+def _acc_lib():
+    import ctypes
+    L = ctypes.CDLL(os.path.join(ROOT, "oracle", "_ref", "libgmask_acc.so"))
+    L.acc_write_bench_vocab.argtypes = [ctypes.c_char_p]
+    P, I64 = ctypes.c_void_p, ctypes.c_int64
+    L.acc_mask_agreement_inputs.argtypes = [ctypes.c_char_p, P, I64, ctypes.POINTER(I64), P, I64,
+                                            ctypes.POINTER(I64)]
+    return L
+
+
+def reference_bench_vocab():
+    """WriteBenchVocab (acceptance_main.cpp:341-359) run from the reference's
+    own source: the 32,000-token bench vocabulary as the reference writes it."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "vocab32k.json")
+        assert _acc_lib().acc_write_bench_vocab(path.encode()) == 0
+        return [t.encode("latin-1") for t in json.load(open(path, encoding="utf-8"))]
+
+
+def acceptance_masks(flats) -> None:
+    """Acceptance criterion 3 at the reference's scale: per fixture, the
+    reference's own SampleVocab(1000) and SampleConfigs(200, 40) with the
+    MaskAgreement seeds (0xba5e + std::hash(name)); masks from the reference
+    engine over our fixture automata (asserted == ComputeMaskNaive)."""
+    import ctypes
+    L = _acc_lib()
+    out = {"source": "acceptance_main.cpp:202-219 via oracle/_ref/libgmask_acc.so", "fixtures": {}}
+    total = 0
+    for name in FIXTURES:
+        vn, cn = ctypes.c_int64(), ctypes.c_int64()
+        assert L.acc_mask_agreement_inputs(name.encode(), None, 0, ctypes.byref(vn), None, 0, ctypes.byref(cn)) == 0
+        vb, cb = ctypes.create_string_buffer(vn.value), ctypes.create_string_buffer(cn.value)
+        assert L.acc_mask_agreement_inputs(name.encode(), vb, vn.value, ctypes.byref(vn), cb, cn.value,
+                                           ctypes.byref(cn)) == 0
+        vocab_hex = json.loads(vb.raw[: vn.value].decode())
+        vocab = [bytes.fromhex(h) for h in vocab_hex]
+        ref = Ref(flats[name], vocab)
+        cases = []
+        for line in cb.raw[: cn.value].decode().splitlines():
+            f = [int(x) for x in line.split()]
+            status, depth, stack = f[0], f[1], f[2:]
+            assert len(stack) == depth
+            c = ref.initial()
+            ref.set(c, status, stack)
+            m = ref.mask(c)
+            assert np.array_equal(m, ref.mask_naive(c)), name
+            ref.free_cfg(c)
+            cases.append({"status": status, "stack": stack, "hex": mask_hex(m, len(vocab))})
+        assert len(cases) == 200 and len(vocab) == 1000
+        total += len(cases)
+        out["fixtures"][name] = {"vocab_hex": vocab_hex, "cases": cases}
+    with open(os.path.join(OUT, "acceptance_masks.json"), "w") as f:
+        json.dump(out, f, separators=(",", ":"), sort_keys=True)
+    print("acceptance masks:", total)
 
 
 def main() -> None:
@@ -151,8 +215,10 @@ def main() -> None:
     #    acceptance_main.cpp:341-359), token-level stream replay,
     #    4 sequences x 120 steps: per-step mask digests, tokens, post-accept
     #    states and stacks.
-    vocab32 = pk.synth_vocab(32000)
-    structural = pk.structural_words(vocab32)
+    vocab32 = oracle.synth_vocab(32000)
+    assert vocab32 == reference_bench_vocab(), "gp_synth_vocab != WriteBenchVocab"
+    assert vocab32 == pk.synth_vocab(32000), "product generator != WriteBenchVocab"
+    structural = oracle.structural_words(vocab32)
     ref = Ref(flats["json"], vocab32)
     seed = 1
     steps, batch = 120, 4
@@ -191,6 +257,7 @@ def main() -> None:
     }
     with open(os.path.join(OUT, "vectors.json"), "w") as f:
         json.dump(vectors, f, indent=0, sort_keys=True)
+    acceptance_masks(flats)
     print("wrote", OUT, {k: os.path.getsize(os.path.join(OUT, k)) for k in os.listdir(OUT)})
 
 

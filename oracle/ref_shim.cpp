@@ -211,7 +211,7 @@ int32_t StreamPick(const uint32_t* mask, const uint32_t* structural, int32_t V, 
   int32_t n_all = CountBits(mask, nullptr, V);
   bool eos = (mask[V >> 5] >> (V & 31)) & 1u;
   if (n_all == 0) return eos ? V : -1;
-  if (eos && ((u >> 32) & 3u) != 0) return V;
+  if (eos && ((u >> 32) & 3u) == 0) return V;  // EOS with probability 1/4
   uint32_t lo = static_cast<uint32_t>(u);
   if ((u >> 34) & 1u) {
     int32_t n_s = structural ? CountBits(mask, structural, V) : 0;
@@ -224,7 +224,15 @@ int32_t StreamPick(const uint32_t* mask, const uint32_t* structural, int32_t V, 
   return SelectBit(mask, nullptr, V, r);
 }
 
-// bf16 -inf masking of one logits row (new work; SURVEY §8a a18).
+// Synthetic bf16 logits of config 5 (gmask_port.c gp_synth_logit; the
+// device bench fills its rotating buffers with the same function).
+uint16_t SynthLogit(uint64_t seed, int32_t k, int32_t b, int32_t t) {
+  uint64_t h = Mix64(seed ^ 0x6C6F67697473ull ^ (static_cast<uint64_t>(static_cast<uint32_t>(k)) * 0xA24BAED4963EE407ull) ^
+                     (static_cast<uint64_t>(static_cast<uint32_t>(b)) * 0xD1B54A32D192ED03ull));
+  uint64_t x = Mix64(h ^ static_cast<uint64_t>(static_cast<uint32_t>(t)));
+  return static_cast<uint16_t>((0x3C00u + static_cast<uint32_t>(x & 0x3FFu)) ^ (((x >> 20) & 1u) ? 0x8000u : 0u));
+}
+
 // Argmax of the allowed bf16 logits (ties -> lowest id; -1 when nothing is
 // allowed) — the device greedy rule (kernels.cu GreedyKey).
 int32_t GreedyPick(const uint16_t* row, const uint32_t* mask, int32_t v1) {
@@ -242,6 +250,7 @@ int32_t GreedyPick(const uint16_t* row, const uint32_t* mask, int32_t v1) {
   return best;
 }
 
+// bf16 -inf masking of one logits row (new work; SURVEY §8a a18).
 void MaskRowBf16(uint16_t* row, const uint32_t* mask, int32_t v1) {
   for (int32_t t = 0; t < v1; ++t) {
     if (!((mask[t >> 5] >> (t & 31)) & 1u)) row[t] = 0xFF80u;
@@ -433,14 +442,19 @@ void ref_mask_naive(void* e, void* c, const uint8_t* bytes, const int64_t* offs,
 // (SPEC.md:416-418).  Stacks deeper than stack_cap count as overflow and
 // restart, matching the device's fixed-capacity stacks.
 //
-// out_stats[0] = seconds for all steps, [1] = seq-steps done, [2] = restarts,
-// [3] = FNV-1a digest of the chosen tokens in (sequence, step) order,
-// [4] = sum of mask popcounts.  If `tokens_out` is non-null it receives the
+// out_stats[0] = seconds of the timed steps, [1] = seq-steps timed, [2] =
+// restarts, [3] = FNV-1a digest of the chosen tokens in (sequence, step)
+// order, [4] = sum of mask popcounts of the timed steps, [5] = the digest of
+// sequences [0, digest_seqs) over the timed steps only, [6] = their mask
+// popcounts (EOS bit excluded) — the bench's in-run evidence (both arms print
+// [5] and [6]).  logits_row 2 (greedy) reads SynthLogit rows of buffer
+// (step % rows).  If `tokens_out` is non-null it receives the
 // [batch][steps] chosen tokens; if `final_stacks` is non-null it receives
 // per sequence [depth, status, stack...] rows of stride stack_cap + 2.
 int ref_decode_run(void* e, void* trie, const uint32_t* structural, int32_t batch, int32_t warmup,
                    int32_t timed, uint64_t seed, int32_t threads, int32_t stack_cap, int32_t logits_row,
-                   double* out_stats, int32_t* tokens_out, int32_t* final_stacks) {
+                   double* out_stats, int32_t* tokens_out, int32_t* final_stacks, int32_t rows,
+                   uint64_t logit_seed, int32_t digest_seqs) {
   const int32_t steps = warmup + timed;
   const Engine& eng = static_cast<Engines*>(e)->engine;
   const TokenTrie& tr = *static_cast<TokenTrie*>(trie);
@@ -468,34 +482,37 @@ int ref_decode_run(void* e, void* trie, const uint32_t* structural, int32_t batc
   std::vector<RuntimeConfig> cfgs(static_cast<size_t>(batch), eng.InitialConfig());
   std::vector<int64_t> restarts(static_cast<size_t>(threads), 0), pops(static_cast<size_t>(threads), 0);
   std::vector<uint64_t> draws(static_cast<size_t>(batch), 0);
+  std::vector<int64_t> wpops(static_cast<size_t>(threads), 0);
+  // Greedy mode (logits_row == 2, config 5): every sequence's SynthLogit row
+  // of each rotating buffer, generated ahead (outside the timed steps).
+  if (rows < 1) rows = 1;
+  std::vector<uint16_t> grows;
+  if (logits_row == 2) {
+    grows.resize(static_cast<size_t>(batch) * static_cast<size_t>(rows) * static_cast<size_t>(v1));
+    for (int32_t b = 0; b < batch; ++b) {
+      for (int32_t k = 0; k < rows; ++k) {
+        uint16_t* g = &grows[(static_cast<size_t>(b) * static_cast<size_t>(rows) + static_cast<size_t>(k)) * static_cast<size_t>(v1)];
+        for (int32_t t = 0; t < v1; ++t) g[t] = SynthLogit(logit_seed, k, b, t);
+      }
+    }
+  }
 
   auto worker = [&](int32_t tid, int32_t s_begin, int32_t s_end) {
     std::vector<uint32_t> mask(static_cast<size_t>(nw));
     std::vector<uint16_t> row(logits_row ? static_cast<size_t>(v1) : 0, 0x3F80u);
-    // Greedy mode (logits_row == 2, config 5): four synthetic bf16 logit rows
-    // cycled per step (the device bench rotates its own buffers the same
-    // way); argmax over allowed ids, ties -> lowest id.
-    std::vector<std::vector<uint16_t>> grows;
-    if (logits_row == 2) {
-      for (int k = 0; k < 4; ++k) {
-        std::vector<uint16_t> g(static_cast<size_t>(v1));
-        uint64_t x = Mix64(seed ^ (0xA5A5ull + static_cast<uint64_t>(k)));
-        for (auto& v : g) {
-          x = Mix64(x);
-          v = static_cast<uint16_t>(0x3C00u + (x & 0x3FFu)) ^ ((x >> 20) & 1 ? 0x8000u : 0u);
-        }
-        grows.push_back(std::move(g));
-      }
-    }
     for (int32_t s = s_begin; s < s_end; ++s) {
       for (int32_t b = tid; b < batch; b += threads) {
         RuntimeConfig& cfg = cfgs[static_cast<size_t>(b)];
         TokenMask m = eng.ComputeMask(cfg, tr);
         MaskToWords(m, mask.data());
-        pops[static_cast<size_t>(tid)] += m.CountSet();
+        const int64_t pc = static_cast<int64_t>(m.CountSet());
+        pops[static_cast<size_t>(tid)] += pc;
+        if (b < digest_seqs) wpops[static_cast<size_t>(tid)] += pc - (m.Test(V) ? 1 : 0);
         int32_t tok;
         if (logits_row == 2) {
-          tok = GreedyPick(grows[static_cast<size_t>(s & 3)].data(), mask.data(), v1);
+          tok = GreedyPick(&grows[(static_cast<size_t>(b) * static_cast<size_t>(rows) + static_cast<size_t>(s % rows)) *
+                                  static_cast<size_t>(v1)],
+                           mask.data(), v1);
         } else {
           if (logits_row) MaskRowBf16(row.data(), mask.data(), v1);
           uint64_t u = StreamDraw(seed, static_cast<uint64_t>(b), draws[static_cast<size_t>(b)]++);
@@ -529,6 +546,7 @@ int ref_decode_run(void* e, void* trie, const uint32_t* structural, int32_t batc
   };
   run(0, warmup);
   std::fill(pops.begin(), pops.end(), 0);
+  std::fill(wpops.begin(), wpops.end(), 0);
   auto t0 = std::chrono::steady_clock::now();
   run(warmup, steps);
   auto t1 = std::chrono::steady_clock::now();
@@ -541,13 +559,26 @@ int ref_decode_run(void* e, void* trie, const uint32_t* structural, int32_t batc
       if (tokens_out) tokens_out[static_cast<int64_t>(b) * steps + s] = static_cast<int32_t>(v);
     }
   }
-  int64_t r = 0, p = 0;
-  for (int32_t t = 0; t < threads; ++t) r += restarts[static_cast<size_t>(t)], p += pops[static_cast<size_t>(t)];
+  uint64_t wdigest = 1469598103934665603ull;
+  for (int32_t b = 0; b < batch && b < digest_seqs; ++b) {
+    for (int32_t s = warmup; s < steps; ++s) {
+      uint32_t v = static_cast<uint32_t>(chosen[static_cast<size_t>(b)][static_cast<size_t>(s)]);
+      for (int k = 0; k < 4; ++k) wdigest = (wdigest ^ ((v >> (8 * k)) & 0xffu)) * 1099511628211ull;
+    }
+  }
+  int64_t r = 0, p = 0, wp = 0;
+  for (int32_t t = 0; t < threads; ++t) {
+    r += restarts[static_cast<size_t>(t)];
+    p += pops[static_cast<size_t>(t)];
+    wp += wpops[static_cast<size_t>(t)];
+  }
   out_stats[0] = std::chrono::duration<double>(t1 - t0).count();
   out_stats[1] = static_cast<double>(static_cast<int64_t>(batch) * timed);
   out_stats[2] = static_cast<double>(r);
   out_stats[3] = static_cast<double>(digest >> 11);  // 53-bit exact in a double
   out_stats[4] = static_cast<double>(p);
+  out_stats[5] = static_cast<double>(wdigest >> 11);
+  out_stats[6] = static_cast<double>(wp);
   if (final_stacks) {
     for (int32_t b = 0; b < batch; ++b) {
       int32_t* row = final_stacks + static_cast<int64_t>(b) * (stack_cap + 2);

@@ -139,6 +139,7 @@ def lib() -> ctypes.CDLL:
                                       ctypes.c_int),
             "gmw_synth_vocab": ([I32, I32, P, I64, P], I64),
             "gmw_structural_words": ([P, P, I32, P], I32),
+            "gmw_synth_logits": ([P, I64, I32, I32, I32, I32, U64, P], I32),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -170,6 +171,16 @@ def synth_vocab(num_tokens: int, flavor: int = 0) -> List[bytes]:
     L.gmw_synth_vocab(num_tokens, flavor, _ptr(buf), n, _ptr(offs))
     raw = buf.tobytes()
     return [raw[offs[i]:offs[i + 1]] for i in range(num_tokens)]
+
+
+def synth_logits(dst, k: int, seed: int, row0: int = 0, stream=None) -> None:
+    """Fills a bf16 CUDA tensor [rows, >=cols] with config 5's synthetic
+    logits of rotating buffer k (gmw_synth_logits; the CPU reference arm
+    generates the same values, oracle/gmask_port.c gp_synth_logit)."""
+    rows, cols = dst.shape
+    if lib().gmw_synth_logits(dst.data_ptr(), dst.stride(0), rows, cols, k, row0, seed & (2**64 - 1),
+                              _stream(stream)) != 0:
+        raise GmError(GM_ERR_USAGE, "gmw_synth_logits failed")
 
 
 def pack_vocab(tokens: Sequence[bytes]):
@@ -387,6 +398,34 @@ def _dptr(t) -> Optional[int]:
     return t.data_ptr() if t is not None else None
 
 
+_DTYPES = {"i32": ("int32",), "bf16": ("bfloat16",), "i32|u32": ("int32", "uint32")}
+
+
+def _check_tensor(t, kind: str, what: str, rows: int, cols: int, device: int) -> None:
+    """The kernels take raw pointers and leading dimensions: a tensor of the
+    wrong dtype, device, row count or inner layout would be silently
+    misread (or written out of bounds), so reject it here."""
+    if t is None:
+        return
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what}: expected a torch.Tensor")
+    if not t.is_cuda or t.device.index != device:
+        raise ValueError(f"{what}: must live on cuda:{device} (got {t.device})")
+    if str(t.dtype).replace("torch.", "") not in _DTYPES[kind]:
+        raise TypeError(f"{what}: dtype must be {'/'.join(_DTYPES[kind])} (got {t.dtype})")
+    if t.dim() == 1:
+        if cols > 1 or t.shape[0] < rows:
+            raise ValueError(f"{what}: expected at least {rows} entries")
+        if t.stride(0) != 1:
+            raise ValueError(f"{what}: must be contiguous")
+        return
+    if t.dim() != 2 or t.shape[0] < rows or t.shape[1] < cols:
+        raise ValueError(f"{what}: expected shape [>= {rows}, >= {cols}] (got {tuple(t.shape)})")
+    if t.stride(1) != 1 or t.stride(0) < cols:
+        raise ValueError(f"{what}: rows must be contiguous with a leading dimension >= {cols}")
+
+
 def _stream(stream) -> Optional[int]:
     if stream is None:
         import torch
@@ -420,8 +459,17 @@ class Batch:
                                        self.cap, ctypes.byref(depth)))
         return RuntimeConfig(state.value, status.value, buf[: depth.value].tolist())
 
+    def _chk(self, bitmask=None, logits=None, seg_counts=None, tokens=None, out9=None):
+        d = self.engine.device
+        _check_tensor(bitmask, "i32|u32", "bitmask", self.B, self.engine.W, d)
+        _check_tensor(logits, "bf16", "logits", self.B, self.engine.V + 1, d)
+        _check_tensor(seg_counts, "i32", "seg_counts", self.B, 2 * self.nseg, d)
+        _check_tensor(tokens, "i32", "tokens", self.B, 1, d)
+        _check_tensor(out9, "i32|u32", "out", self.B, 9, d)
+
     def fill(self, bitmask, logits=None, seg_counts=None, stream=None):
         """bitmask: int32 CUDA tensor [B, >=W] (or None); logits: bf16 [B, >=V+1]."""
+        self._chk(bitmask, logits, seg_counts)
         bm = bitmask.data_ptr() if bitmask is not None else None
         ldw = bitmask.stride(0) if bitmask is not None else 0
         lg = logits.data_ptr() if logits is not None else None
@@ -431,23 +479,29 @@ class Batch:
 
     def allowed_terminals(self, out, stream=None):
         """Engine::AllowedTerminals per sequence into out: int32 CUDA tensor [B, 9]."""
+        self._chk(out9=out)
         _check(lib().gm_allowed_terminals(self._h, out.data_ptr(), _stream(stream)))
 
     def accept(self, tokens, status_out=None, restart: bool = False, stream=None):
+        self._chk(tokens=tokens)
+        self._chk(tokens=status_out)
         so = status_out.data_ptr() if status_out is not None else None
         _check(lib().gm_accept_tokens(self._h, tokens.data_ptr(), so, int(restart), _stream(stream)))
 
     def sample_stream_and_accept(self, bitmask, seg_counts, seed: int, tokens_out=None, stream=None):
+        self._chk(bitmask, None, seg_counts, tokens_out)
         to = tokens_out.data_ptr() if tokens_out is not None else None
         _check(lib().gm_sample_stream_and_accept(self._h, bitmask.data_ptr(), bitmask.stride(0),
                                                  seg_counts.data_ptr(), seed, to, _stream(stream)))
 
     def sample_stream(self, bitmask, seg_counts, seed: int, tokens_out, stream=None):
+        self._chk(bitmask, None, seg_counts, tokens_out)
         _check(lib().gm_sample_stream(self._h, bitmask.data_ptr(), bitmask.stride(0), seg_counts.data_ptr(), seed,
                                       tokens_out.data_ptr(), _stream(stream)))
 
     def decode_step_stream(self, seed: int, bitmask=None, logits=None, tokens_out=None, stream=None):
         """Fused fill + -inf logits + stream sample + accept (one launch)."""
+        self._chk(bitmask, logits, None, tokens_out)
         bm = bitmask.data_ptr() if bitmask is not None else None
         ldw = bitmask.stride(0) if bitmask is not None else 0
         lg = logits.data_ptr() if logits is not None else None
@@ -458,6 +512,7 @@ class Batch:
     def decode_step_stream_split(self, seed: int, bitmask=None, logits=None, seg_counts=None, tokens_out=None,
                                  stream=None):
         """The same step as two overlapping kernels (gm_decode_step_stream_split)."""
+        self._chk(bitmask, logits, seg_counts, tokens_out)
         bm = bitmask.data_ptr() if bitmask is not None else None
         ldw = bitmask.stride(0) if bitmask is not None else 0
         lg = logits.data_ptr() if logits is not None else None
@@ -472,6 +527,7 @@ class Batch:
         _check(lib().gm_batch_time_next_fill(self._h, start.cuda_event, end.cuda_event))
 
     def decode_step_greedy(self, logits, tokens_out=None, bitmask=None, stream=None):
+        self._chk(bitmask, logits, None, tokens_out)
         to = tokens_out.data_ptr() if tokens_out is not None else None
         bm = bitmask.data_ptr() if bitmask is not None else None
         ldw = bitmask.stride(0) if bitmask is not None else 0
@@ -481,6 +537,7 @@ class Batch:
     def sample(self, logits, bitmask, temperature: float = 1.0, top_k: int = 0, top_p: float = 1.0, seed: int = 0,
                tokens_out=None, accept: bool = True, stream=None):
         """gm_sample_tokens: temperature / top-k / top-p over the allowed tokens (+ accept)."""
+        self._chk(bitmask, logits, None, tokens_out)
         _check(lib().gm_sample_tokens(self._h, _dptr(logits), logits.stride(0), _dptr(bitmask), bitmask.stride(0),
                                       float(temperature), int(top_k), float(top_p), seed & (2**64 - 1),
                                       _dptr(tokens_out), int(accept), _stream(stream)))
@@ -488,6 +545,7 @@ class Batch:
     def decode_step_sample(self, logits, temperature: float = 1.0, top_k: int = 0, top_p: float = 1.0,
                            seed: int = 0, tokens_out=None, bitmask=None, stream=None):
         """gm_decode_step_sample: fill + sample + accept, no host round trip."""
+        self._chk(bitmask, logits, None, tokens_out)
         _check(lib().gm_decode_step_sample(self._h, _dptr(logits), logits.stride(0), _dptr(bitmask),
                                            bitmask.stride(0) if bitmask is not None else 0, float(temperature),
                                            int(top_k), float(top_p), seed & (2**64 - 1), _dptr(tokens_out),

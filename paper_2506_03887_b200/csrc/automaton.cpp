@@ -60,6 +60,9 @@ Automaton LoadFlat(const uint8_t* data, size_t n) {
   r.p += S * 256 * 4;
   int32_t ne = r.Get<int32_t>();
   if (ne < 0 || ne > (1 << 28)) Corrupt("edge count out of range");
+  // Every edge record takes at least 56 bytes (header + one condition entry):
+  // reject a count the remaining input cannot hold before allocating for it.
+  if (static_cast<size_t>(ne) > static_cast<size_t>(r.end - r.p) / 56) Corrupt("edge count exceeds the input");
   a.edge_begin.resize(S + 1);
   for (auto& b : a.edge_begin) b = r.Get<int32_t>();
   a.edges.resize(static_cast<size_t>(ne));
@@ -120,7 +123,7 @@ void Automaton::Validate() const {
   auto in_range = [S](int32_t s) { return s >= 0 && s < S; };
   if (!in_range(initial_state)) Corrupt("initial state out of range");
   if (accept_state != -1 && !in_range(accept_state)) Corrupt("accept state out of range");
-  if (static_cast<int32_t>(shift_targets.size()) != S * 256) Corrupt("shift table size");
+  if (shift_targets.size() != static_cast<size_t>(S) * 256) Corrupt("shift table size");
   for (int32_t t : shift_targets) {
     if (t != -1 && !in_range(t)) Corrupt("shift target out of range");
   }

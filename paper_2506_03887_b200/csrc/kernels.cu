@@ -783,7 +783,7 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
       Mix64(Mix64(seed ^ (static_cast<unsigned long long>(b) * 0xD1B54A32D192ED03ull)) ^
             static_cast<unsigned long long>(draw));
   if (na == 0) return eos ? Vv.V : -1;
-  if (eos && ((u >> 32) & 3ull) != 0) return Vv.V;
+  if (eos && ((u >> 32) & 3ull) == 0) return Vv.V;  // EOS with probability 1/4
   const bool use_s = ((u >> 34) & 1ull) && ns > 0;
   const uint32_t nsel = static_cast<uint32_t>(use_s ? ns : na);
   uint32_t r = static_cast<uint32_t>((static_cast<unsigned long long>(static_cast<uint32_t>(u)) * nsel) >> 32);
@@ -992,7 +992,9 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
   unsigned long long t_ph = Bt.trace ? NowNs() : 0ull;
   int depth = st.depth;
   int wv = min(depth, 32);
-  if (tok >= 0 && st.status == kAlive) {
+  if (tok > Vv.V && st.status == kAlive) {
+    st.status = kDead;  // not a token of this vocabulary (ids 0..V-1, EOS = V)
+  } else if (tok >= 0 && st.status == kAlive) {
     const bool eos = tok == Vv.V;
     const int4 tr = __ldg(Vv.tok_rec + tok);
     const int nterm = tr.y;
@@ -1074,7 +1076,13 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
         // write through memory and reload the window.
         for (int j = lane; j < push_len; j += 32) stack[base + j] = __ldg(A.rec_push + push_off + j);
         __syncwarp();
-        if (dyn && lane == 0) stack[base + push_len] = __ldg(A.shift + stack[base + push_len - 1] * 256 + x);
+        int tgt = 0;
+        if (dyn) tgt = __ldg(A.shift + stack[base + push_len - 1] * 256 + x);
+        if (tgt < 0) {
+          st.status = kDead;  // no shift target (the mask walk rejects it too)
+          break;
+        }
+        if (dyn && lane == 0) stack[base + push_len] = tgt;
         __syncwarp();
         topv = lane < nd ? stack[nd - 1 - lane] : -1;
         wv = min(nd, 32);
@@ -1090,6 +1098,10 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
           int top = push_len > 0 ? last_pushed : (cond_len < wv ? below : -1);
           if (top < 0) top = stack[base - 1];
           const int tgt = __ldg(A.shift + top * 256 + x);
+          if (tgt < 0) {
+            st.status = kDead;  // no shift target (the mask walk rejects it too)
+            break;
+          }
           if (lane == push_len) pj = tgt;
         }
         if (lane < P) stack[base + lane] = pj;

@@ -218,3 +218,86 @@ def test_port_decode_loop_matches_reference_128k():
     sp, tp, kp = p.decode_run(structural, 3, 6, 11, want_tokens=True, want_stacks=True)
     assert np.array_equal(tr, tp) and np.array_equal(kr, kp)
     assert sr[3] == sp[3] and sr[4] == sp[4]
+
+
+@pytest.fixture(scope="module")
+def acceptance():
+    with open(os.path.join(GOLDEN, "acceptance_masks.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_acceptance_criterion3_reference_scale(acceptance, name):
+    """Acceptance criterion 3 at the reference's own scale and seeds
+    (acceptance_main.cpp:202-219: 200 SampleConfigs x a 1,000-token
+    SampleVocab per fixture, generated by the reference's own helpers): the
+    port's trie mask and its naive replay equal the reference's masks."""
+    case = acceptance["fixtures"][name]
+    vocab = [bytes.fromhex(h) for h in case["vocab_hex"]]
+    assert len(vocab) == 1000 and len(case["cases"]) == 200
+    p = Port(flat(name), vocab)
+    for c in case["cases"]:
+        cfg = p.config(c["status"], c["stack"])
+        m = p.mask(cfg)
+        assert mask_hex(m, len(vocab)) == c["hex"]
+        if c is case["cases"][0] or random.Random(len(c["stack"])).random() < 0.1:
+            assert np.array_equal(m, p.mask_naive(cfg))
+        p.free(cfg)
+
+
+def test_oracle_workload_generators_match_product():
+    """The CPU arm's own inputs (gp_synth_vocab / gp_structural_words, C
+    restatements in the oracle) equal the product's generator byte for byte,
+    for every flavour the bench uses."""
+    import paper_2506_03887_b200 as pk
+    for n, flavor in [(32000, 0), (128255, 0), (128255, 1)]:
+        a = oracle.synth_vocab(n, flavor)
+        assert a == pk.synth_vocab(n, flavor)
+        assert np.array_equal(oracle.structural_words(a), pk.structural_words(a))
+
+
+def test_bench_vocab_is_the_references(vectors):
+    """gp_synth_vocab(32000) == WriteBenchVocab (acceptance_main.cpp:341-359):
+    the sha256 recorded by make_golden.py after asserting equality with the
+    reference's own function (oracle/_ref/libgmask_acc.so)."""
+    import hashlib as h
+    v = oracle.synth_vocab(32000)
+    assert h.sha256(b"\0".join(v)).hexdigest() == vectors["json32k_stream"]["vocab_sha"]
+    acc = os.path.join(os.path.dirname(oracle.__file__), "_ref", "libgmask_acc.so")
+    if os.path.exists(acc) and os.path.isdir("/root/reference/proj"):
+        import importlib.util
+        spec = importlib.util.spec_from_file_location(
+            "make_golden", os.path.join(os.path.dirname(oracle.__file__), "make_golden.py"))
+        mg = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mg)
+        assert mg.reference_bench_vocab() == v
+
+
+def test_mask_hash_numpy_matches_c():
+    rng = np.random.default_rng(1)
+    m = rng.integers(0, 2**32, size=(5, 4008), dtype=np.uint64).astype(np.uint32)
+    got = oracle.mask_hashes(m)
+    L = oracle.Port.lib()
+    for i in range(5):
+        assert int(got[i]) == int(L.gp_mask_hash(m[i].ctypes.data, 4008))
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference not built here")
+@pytest.mark.parametrize("greedy", [False, True])
+def test_window_digests_reference_vs_port(greedy):
+    """The in-run evidence both bench arms print (token digest and mask
+    popcounts of sequences < 32 over the timed steps): the reference decode
+    loop and the port agree, stream and greedy (synthetic logits rows)."""
+    vocab = oracle.synth_vocab(32000)
+    structural = oracle.structural_words(vocab)
+    f = flat("json")
+    r = Ref(f, vocab)
+    p = Port(f, vocab)
+    B, W_, K = 36, 5, 12
+    kw = dict(greedy_rows=3, logit_seed=99) if greedy else {}
+    sr, tr, _ = r.decode_run(structural, B, K, 4, threads=4, warmup=W_, want_tokens=True,
+                             logits_row=2 if greedy else 1, rows=3, logit_seed=99, digest_seqs=32)
+    sp, tp, _ = p.decode_run(structural, B, W_ + K, 4, want_tokens=True, warmup=W_, digest_seqs=32, **kw)
+    assert np.array_equal(tr, tp)
+    assert sr[5] == sp[5] and sr[6] == sp[6]
+    assert sr[6] > 0
