@@ -671,3 +671,51 @@ def test_split_step_odd_batches(B):
     for b in range(B):
         d = pstacks[b, 0]
         assert batch.get(b).stack == pstacks[b, 2:2 + d].tolist()
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("K", [1, 8])
+def test_acceptance_criterion3_on_device(name, K):
+    """Acceptance criterion 3 at the reference's own scale and seeds
+    (acceptance_main.cpp:202-219; tests/golden/acceptance_masks.json from the
+    reference's SampleVocab/SampleConfigs): all 200 configurations x 1,000
+    tokens per fixture, device masks == the reference's, at context depths 1
+    (most tokens context-dependent) and 8."""
+    with open(os.path.join(GOLDEN, "acceptance_masks.json")) as f:
+        case = json.load(f)["fixtures"][name]
+    vocab = [bytes.fromhex(h) for h in case["vocab_hex"]]
+    eng = pk.DeviceEngine(pk.Automaton.load(flat(name)), vocab, context_depth=K)
+    cfgs = [pk.RuntimeConfig(c["stack"][-1], c["status"], c["stack"]) for c in case["cases"]]
+    masks, _ = fill_batch(eng, cfgs, logits=True)
+    for m, c in zip(masks, case["cases"]):
+        assert mask_hex(m, len(vocab)) == c["hex"], c["stack"]
+
+
+def test_python_binding_rejects_bad_tensors():
+    """The binding checks dtype, device, row count and inner layout before a
+    raw pointer reaches a kernel (a float32 logits row would otherwise be
+    read as bf16, a short tensor written out of bounds)."""
+    eng = pk.DeviceEngine(pk.Automaton.load(flat("paren")), [b"a", b"("])
+    b = eng.batch(4)
+    bm = torch.zeros((4, eng.W), dtype=torch.int32, device=DEV)
+    with pytest.raises(TypeError):
+        b.fill(bm, torch.zeros((4, 3), dtype=torch.float32, device=DEV))
+    with pytest.raises(ValueError):
+        b.fill(torch.zeros((3, eng.W), dtype=torch.int32, device=DEV))
+    with pytest.raises(ValueError):
+        b.fill(bm.cpu())
+    with pytest.raises(ValueError):
+        b.accept(torch.zeros(2, dtype=torch.int32, device=DEV))
+    b.fill(bm, torch.zeros((4, 3), dtype=torch.bfloat16, device=DEV))
+    b.check()
+
+
+def test_token_id_beyond_vocabulary_kills_the_sequence():
+    """an id > V (a model special the caller did not remap) makes
+    the sequence dead instead of reading past the token tables."""
+    eng = pk.DeviceEngine(pk.Automaton.load(flat("paren")), [b"a", b"(", b")"])
+    b = eng.batch(2)
+    st = torch.zeros(2, dtype=torch.int32, device=DEV)
+    b.accept(torch.tensor([4, 1 << 30], dtype=torch.int32, device=DEV), st)
+    b.check()
+    assert st.cpu().tolist() == [pk.DEAD, pk.DEAD]
