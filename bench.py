@@ -484,6 +484,17 @@ def main(argv=None):
     for i in range(Wm):
         step(i)
     batch.check()
+    # The timed steps as one captured CUDA graph (gm_decode_graph_create; a
+    # multiple of 6 steps, the rest enqueued eagerly): one host call launches
+    # them, with every step's own buffers baked in.
+    Kg = 0 if (args.no_graph or args.one_launch) else K - K % 6
+    graph = None
+    if Kg:
+        graph = batch.capture_steps(
+            Kg, greedy=greedy, seed=seed, logits=[logits[(Wm + i) % R] for i in range(Kg)],
+            bitmask=[bm_all[i] for i in range(Kg)] if bm_all is not None else bm,
+            seg_counts=None if greedy else [counts_all[i] for i in range(Kg)],
+            tokens_out=[toks_all[i] for i in range(Kg)])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -492,12 +503,15 @@ def main(argv=None):
     with ClockSampler(local) as clocks:
         h0 = time.perf_counter()
         e0.record(stream)
-        for i in range(K):
+        if graph is not None:
+            graph.launch()
+        for i in range(Kg, K):
             step(Wm + i, bm_=bm_all[i] if bm_all is not None else None,
                  counts_=counts_all[i] if counts_all is not None else None, toks_=toks_all[i])
         e1.record(stream)
         h1 = time.perf_counter()
         torch.cuda.synchronize()
+    del graph
     batch.check()
     if world > 1:
         dist.barrier()
@@ -687,6 +701,8 @@ def main(argv=None):
         "e2e": e2e,
         "check": check,
         "gpu_launches": K * (1 if args.one_launch else 2),  # split / greedy: fill + accept per step
+        "launch": (f"CUDA graph of {Kg} steps (one gm_graph_launch)" + (f" + {K - Kg} eager steps" if K > Kg else "")
+                   if Kg else "eager, one ABI call per step"),
         "clocks": clocks.summary(),
         "cold_cache": cold,
         "preprocessing": {"compile_s": t_comp, "prewarm_s": t_pre,

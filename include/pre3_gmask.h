@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define GM_ABI_VERSION 1
+#define GM_ABI_VERSION 2
 
 enum gm_status_code {
   GM_OK = 0,
@@ -57,6 +57,7 @@ enum gm_seq_status {
 typedef struct gm_automaton gm_automaton; /* host: compiled DPDA (gmask::Dpda) */
 typedef struct gm_engine gm_engine;       /* device: automaton + vocab + context cache */
 typedef struct gm_batch gm_batch;         /* device: B sequences' (state, status, stack) */
+typedef struct gm_graph gm_graph;         /* a captured CUDA graph of decode steps of one batch */
 
 const char* gm_last_error(void);
 int gm_abi_version(void);
@@ -105,13 +106,30 @@ typedef struct gm_engine_options {
                               top keyed R deep, walking only that context's context-dependent
                               tokens (0 = default min(4, K-1); negative = off) */
   int32_t segment_words;   /* vocab segment size in mask words (default 256) */
+  /* ABI v2: the model's logit-row layout (all zero = the
+   * reference's: V + 1 columns, EOS in column V). */
+  int32_t num_columns;     /* logit columns per row (0 = V + 1) */
+  int32_t eos_column;      /* column of the EOS logit = mask bit V (used when num_columns > 0) */
+  const uint32_t* disabled; /* host bitmask (W words) of token ids < V that are never allowed (model
+                               specials or alias ids among the regular ids; their bytes are ignored
+                               and may be empty), or NULL */
 } gm_engine_options;
 
 /* Engine::Engine (runtime.cpp:92-113) + TokenTrie::Build (runtime.cpp:18-61)
  * on `device`: uploads the flattened automaton, the vocabulary (host
  * `tok_bytes`, `tok_offsets[num_tokens+1]`) and allocates the context cache.
  * Empty / duplicate tokens fail with GM_ERR_VOCAB_* exactly where
- * TokenTrie::Build throws.  opts may be NULL. */
+ * TokenTrie::Build throws (disabled ids are exempt).  opts may be NULL.
+ *
+ * Logit layout (opts->num_columns > 0): every fused logits call (mask,
+ * greedy, sample) reads/writes columns [0, num_columns): column eos_column
+ * carries mask bit V (EOS), columns c < V carry bit c, every other column is
+ * a special token and gets -inf (never sampled).  eos_column < V requires
+ * that id to be disabled.  Token ids at the ABI (tokens_out, gm_accept_tokens)
+ * are then model columns: EOS = eos_column; ids >= V other than eos_column
+ * and disabled ids are invalid (the sequence goes GM_DEAD).  Bitmask rows
+ * keep the reference layout (bit V = EOS).  Greedy/sampler ties are broken
+ * in mask-bit order (EOS last). */
 int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes,
                      const int64_t* tok_offsets, int32_t num_tokens,
                      const gm_engine_options* opts, int device, gm_engine** out);
@@ -234,6 +252,23 @@ int gm_sample_tokens(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, const
 int gm_decode_step_sample(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, uint32_t* bitmask,
                           int64_t ld_words, float temperature, int32_t top_k, float top_p, uint64_t seed,
                           int32_t* tokens_out, void* stream);
+
+/* CUDA graph of `steps` decode steps of batch b (a positive multiple of 6:
+ * the period of the step bookkeeping), so a serving loop launches N steps
+ * with one host call.  kind 0 = gm_decode_step_stream_split, 1 =
+ * gm_decode_step_greedy; step i uses bitmask[i], logits[i], seg_counts[i],
+ * tokens_out[i] (each array may be NULL: no bitmask output / internal
+ * scratch / no ids; logits may be NULL for kind 0 = mask only).  The
+ * pointers are baked into the graph.  Capture runs on an internal stream and
+ * executes nothing except, if needed, the context lookup of the next step.
+ * gm_graph_launch replays the steps on `stream`; the batch must be at the
+ * state the graph was captured from (true after every replay and after any
+ * 6k eager steps of the same kind), else GM_ERR_USAGE. */
+int gm_decode_graph_create(gm_batch* b, int32_t kind, int32_t steps, uint32_t* const* bitmask, int64_t ld_words,
+                           const uint16_t* const* logits, int64_t ld, int32_t* const* seg_counts, uint64_t seed,
+                           int32_t* const* tokens_out, gm_graph** out);
+int gm_graph_launch(gm_graph* g, void* stream);
+int gm_graph_destroy(gm_graph* g);
 
 /* Measurement hook (diagnostics): the next fill kernel launched for this
  * batch, by any call, is bracketed by cudaEventRecord(start_event) and

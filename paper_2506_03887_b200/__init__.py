@@ -133,6 +133,9 @@ def lib() -> ctypes.CDLL:
             "gm_decode_step_stream_split": ([P, P, I64, P, I64, P, U64, P, P], ctypes.c_int),
             "gm_batch_time_next_fill": ([P, P, P], ctypes.c_int),
             "gm_decode_step_greedy": ([P, P, I64, P, I64, P, P], ctypes.c_int),
+            "gm_decode_graph_create": ([P, I32, I32, P, I64, P, I64, P, U64, P, PP], ctypes.c_int),
+            "gm_graph_launch": ([P, P], ctypes.c_int),
+            "gm_graph_destroy": ([P], ctypes.c_int),
             "gm_sample_tokens": ([P, P, I64, P, I64, ctypes.c_float, I32, ctypes.c_float, U64, P, I32, P],
                                  ctypes.c_int),
             "gm_decode_step_sample": ([P, P, I64, P, I64, ctypes.c_float, I32, ctypes.c_float, U64, P, P],
@@ -289,7 +292,9 @@ class Automaton:
 
 class _EngineOptions(ctypes.Structure):
     _fields_ = [("context_depth", ctypes.c_int32), ("context_slots", ctypes.c_int32),
-                ("parent_depth", ctypes.c_int64), ("segment_words", ctypes.c_int32)]
+                ("parent_depth", ctypes.c_int64), ("segment_words", ctypes.c_int32),
+                ("num_columns", ctypes.c_int32), ("eos_column", ctypes.c_int32),
+                ("disabled", ctypes.c_void_p)]
 
 
 @dataclass
@@ -304,19 +309,33 @@ class DeviceEngine:
     """Engine::Engine + TokenTrie::Build on one CUDA device (runtime.cpp:18-113)."""
 
     def __init__(self, automaton: Automaton, tokens: Sequence[bytes], device: int = 0,
-                 context_depth: int = 8, context_slots: int = 8192, parent_depth: int = 0):
+                 context_depth: int = 8, context_slots: int = 8192, parent_depth: int = 0,
+                 num_columns: int = 0, eos_column: int = 0, disabled: Optional[Sequence[int]] = None):
+        """num_columns / eos_column / disabled: the model's logit layout
+        (gm_engine_options; tokenizer.TokenizerVocab.engine_options() fills
+        them from a tokenizer.json): logit rows have num_columns columns, EOS
+        is column eos_column, other columns >= V are specials (-inf), and the
+        ids in `disabled` (< V) are never allowed."""
         self.automaton = automaton
         self.tokens = list(tokens)
         self.V = len(self.tokens)
         self.W = (self.V + 1 + 31) // 32
         self.device = device
+        self.num_columns = num_columns if num_columns > 0 else self.V + 1
+        self.eos_column = eos_column if num_columns > 0 else self.V
+        self.disabled_words = np.zeros(self.W, np.uint32)
+        for i in disabled or ():
+            if not 0 <= i < self.V:
+                raise ValueError(f"disabled id {i} out of range")
+            self.disabled_words[i >> 5] |= np.uint32(1 << (i & 31))
         data, offs = pack_vocab(self.tokens)
-        opts = _EngineOptions(context_depth, context_slots, parent_depth, 256)
+        opts = _EngineOptions(context_depth, context_slots, parent_depth, 256, num_columns, eos_column,
+                              self.disabled_words.ctypes.data if disabled else None)
         h = ctypes.c_void_p()
         _check(lib().gm_engine_create(automaton._h, _ptr(data), _ptr(offs), self.V, ctypes.byref(opts),
                                       device, ctypes.byref(h)))
         self._h = h
-        self.structural = structural_words(self.tokens)
+        self.structural = structural_words(self.tokens) & ~self.disabled_words
         _check(lib().gm_engine_set_structural(self._h, _ptr(self.structural)))
         self._single: Optional[Batch] = None
 
@@ -433,6 +452,23 @@ def _stream(stream) -> Optional[int]:
     return stream
 
 
+class StepGraph:
+    """A captured CUDA graph of decode steps (gm_graph); launch() replays them."""
+
+    def __init__(self, handle, batch, keep):
+        self._h = handle
+        self.batch = batch
+        self._keep = keep  # the baked-in buffers must outlive the graph
+
+    def launch(self, stream=None) -> None:
+        _check(lib().gm_graph_launch(self._h, _stream(stream)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.gm_graph_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
 class Batch:
     """B in-flight sequences on the device (gm_batch)."""
 
@@ -462,7 +498,7 @@ class Batch:
     def _chk(self, bitmask=None, logits=None, seg_counts=None, tokens=None, out9=None):
         d = self.engine.device
         _check_tensor(bitmask, "i32|u32", "bitmask", self.B, self.engine.W, d)
-        _check_tensor(logits, "bf16", "logits", self.B, self.engine.V + 1, d)
+        _check_tensor(logits, "bf16", "logits", self.B, self.engine.num_columns, d)
         _check_tensor(seg_counts, "i32", "seg_counts", self.B, 2 * self.nseg, d)
         _check_tensor(tokens, "i32", "tokens", self.B, 1, d)
         _check_tensor(out9, "i32|u32", "out", self.B, 9, d)
@@ -550,6 +586,30 @@ class Batch:
                                            bitmask.stride(0) if bitmask is not None else 0, float(temperature),
                                            int(top_k), float(top_p), seed & (2**64 - 1), _dptr(tokens_out),
                                            _stream(stream)))
+
+    def capture_steps(self, steps: int, greedy: bool = False, seed: int = 0, bitmask=None, logits=None,
+                      seg_counts=None, tokens_out=None) -> "StepGraph":
+        """gm_decode_graph_create: a CUDA graph of `steps` (multiple of 6)
+        decode steps.  Each of bitmask / logits / seg_counts / tokens_out is
+        None, one tensor (every step) or a list of `steps` tensors."""
+        def ptrs(x, kind, what, cols):
+            if x is None:
+                return None, 0
+            xs = list(x) if isinstance(x, (list, tuple)) else [x] * steps
+            if len(xs) != steps:
+                raise ValueError(f"{what}: expected {steps} tensors")
+            for t in xs:
+                _check_tensor(t, kind, what, self.B, cols, self.engine.device)
+            arr = (ctypes.c_void_p * steps)(*[t.data_ptr() for t in xs])
+            return arr, (xs[0].stride(0) if xs[0].dim() == 2 else 0)
+        bm, ldw = ptrs(bitmask, "i32|u32", "bitmask", self.engine.W)
+        lg, ld = ptrs(logits, "bf16", "logits", self.engine.num_columns)
+        sc, _ = ptrs(seg_counts, "i32", "seg_counts", 2 * self.nseg)
+        to, _ = ptrs(tokens_out, "i32", "tokens_out", 1)
+        h = ctypes.c_void_p()
+        _check(lib().gm_decode_graph_create(self._h, int(greedy), steps, bm, ldw, lg, ld, sc, seed & (2**64 - 1), to,
+                                            ctypes.byref(h)))
+        return StepGraph(h, self, (bm, lg, sc, to, bitmask, logits, seg_counts, tokens_out))
 
     def check(self, stream=None):
         _check(lib().gm_batch_check(self._h, _stream(stream)))

@@ -75,6 +75,7 @@ struct gm_engine {
   pre3::VocabView vocab{};
   pre3::CacheView cache{};
   uint32_t* structural = nullptr;
+  std::vector<uint32_t> disabled;  // host copy (W words) or empty
   std::vector<void*> owned;
   ~gm_engine() {
     cudaSetDevice(device);
@@ -125,7 +126,7 @@ struct gm_batch {
     f->fill_no = fill_seq;
   }
   void EndFill(bool tail) {
-    ++fill_seq;
+    fill_seq = (fill_seq + 1) % pre3::kFillPeriod;
     last_consumed = prod;
     prod = (prod + 1) % 3;
     slots_valid = true;
@@ -142,9 +143,11 @@ struct gm_batch {
     slots_valid = true;
     return prod;
   }
+  cudaStream_t capture_stream = nullptr;  // graph capture (the legacy stream cannot capture)
   std::vector<void*> owned;
   ~gm_batch() {
     cudaSetDevice(engine->device);
+    if (capture_stream) cudaStreamDestroy(capture_stream);
     // Builds still queued belong to contexts other batches may already use.
     for (int q = 0; q < 3; ++q) pre3::LaunchDrain(engine->aut, engine->vocab, engine->cache, view, q, nullptr);
     cudaDeviceSynchronize();
@@ -269,12 +272,25 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     if (!a || !out || num_tokens < 0 || (num_tokens > 0 && (!tok_bytes || !tok_offsets))) {
       return Fail(GM_ERR_USAGE, "bad argument");
     }
-    gm_engine_options o{8, 8192, 0, pre3::kSegWords};
+    gm_engine_options o{8, 8192, 0, pre3::kSegWords, 0, 0, nullptr};
     if (opts) {
       if (opts->context_depth) o.context_depth = opts->context_depth;
       if (opts->context_slots) o.context_slots = opts->context_slots;
       if (opts->segment_words) o.segment_words = opts->segment_words;
       o.parent_depth = opts->parent_depth;
+      o.num_columns = opts->num_columns;
+      o.eos_column = opts->eos_column;
+      o.disabled = opts->disabled;
+    }
+    const int32_t W = (num_tokens + 1 + 31) / 32;
+    auto is_disabled = [&](int32_t i) { return o.disabled && ((o.disabled[i >> 5] >> (i & 31)) & 1u); };
+    if (o.num_columns < 0) return Fail(GM_ERR_USAGE, "num_columns must be >= 0");
+    if (o.num_columns > 0) {
+      if (o.eos_column < 0 || o.eos_column >= o.num_columns) return Fail(GM_ERR_USAGE, "eos_column out of range");
+      if (o.num_columns < num_tokens) return Fail(GM_ERR_USAGE, "num_columns < V");
+      if (o.eos_column < num_tokens && !is_disabled(o.eos_column)) {
+        return Fail(GM_ERR_USAGE, "eos_column < V must name a disabled id");
+      }
     }
     // Parent key depth R: new contexts keyed K deep are built from the
     // context of the same stack top keyed R deep (0 = default min(4, K-1);
@@ -295,11 +311,14 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     for (int32_t i = 0; i < num_tokens; ++i) {
       const int64_t lo = tok_offsets[i], hi = tok_offsets[i + 1];
       if (hi < lo) return Fail(GM_ERR_USAGE, "token offsets not monotone");
+      offs[static_cast<size_t>(i)] = static_cast<int32_t>(lo - tok_offsets[0]);
+      if (is_disabled(i)) continue;  // never allowed: bytes ignored, exempt from the trie rules
       if (hi == lo) return Fail(GM_ERR_VOCAB_EMPTY, "EmptyToken: token " + std::to_string(i) + " has no bytes");
       std::string_view sv(reinterpret_cast<const char*>(tok_bytes + lo), static_cast<size_t>(hi - lo));
       if (!seen.insert(sv).second) {
         int32_t first = -1;
         for (int32_t j = 0; j < i; ++j) {
+          if (is_disabled(j)) continue;
           if (std::string_view(reinterpret_cast<const char*>(tok_bytes + tok_offsets[j]),
                                static_cast<size_t>(tok_offsets[j + 1] - tok_offsets[j])) == sv) {
             first = j;
@@ -309,7 +328,6 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
         return Fail(GM_ERR_VOCAB_DUPLICATE, "DuplicateToken: tokens " + std::to_string(first) + " and " +
                                                 std::to_string(i) + " are identical");
       }
-      offs[static_cast<size_t>(i)] = static_cast<int32_t>(lo - tok_offsets[0]);
     }
     offs[static_cast<size_t>(num_tokens)] = num_tokens ? static_cast<int32_t>(tok_offsets[num_tokens] - tok_offsets[0]) : 0;
 
@@ -344,8 +362,11 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     // (a walk's first round trip; longer tokens read the rest from tok_bytes).
     // Entry V is EOS: length 1, no bytes.
     std::vector<int32_t> recs(4 * (static_cast<size_t>(num_tokens) + 1), 0);
+    // A disabled id keeps length 0: every walk of it rejects, accepting it
+    // kills the sequence.
     for (int32_t i = 0; i < num_tokens; ++i) {
-      const int32_t lo = offs[static_cast<size_t>(i)], len = offs[static_cast<size_t>(i) + 1] - lo;
+      const int32_t lo = offs[static_cast<size_t>(i)];
+      const int32_t len = is_disabled(i) ? 0 : offs[static_cast<size_t>(i) + 1] - lo;
       uint32_t w[2] = {0u, 0u};
       for (int32_t j = 0; j < len && j < 8; ++j) w[j >> 2] |= static_cast<uint32_t>(bytes[static_cast<size_t>(lo + j)]) << (8 * (j & 3));
       recs[4 * static_cast<size_t>(i) + 0] = lo;
@@ -361,6 +382,13 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     e->vocab.V = e->V;
     e->vocab.W = e->W;
     e->vocab.nseg = e->nseg;
+    e->vocab.layout = o.num_columns > 0 && !(o.num_columns == num_tokens + 1 && o.eos_column == num_tokens);
+    e->vocab.ncols = e->vocab.layout ? o.num_columns : num_tokens + 1;
+    e->vocab.eos_col = e->vocab.layout ? o.eos_column : num_tokens;
+    if (o.disabled) {
+      e->disabled.assign(o.disabled, o.disabled + W);
+      e->disabled[static_cast<size_t>(num_tokens >> 5)] &= (1u << (num_tokens & 31)) - 1u;  // ids < V only
+    }
 
     const size_t C = static_cast<size_t>(o.context_slots);
     auto& c = e->cache;
@@ -423,6 +451,7 @@ int gm_engine_set_structural(gm_engine* e, const uint32_t* host_words) {
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     std::vector<uint32_t> w(host_words, host_words + e->W);
     w[static_cast<size_t>(e->V >> 5)] &= ~(1u << (e->V & 31));  // EOS is never structural
+    for (size_t i = 0; i < e->disabled.size(); ++i) w[i] &= ~e->disabled[i];
     Check(cudaDeviceSynchronize(), "structural: fills in flight");
     Check(cudaMemcpy(e->structural, w.data(), w.size() * 4, cudaMemcpyHostToDevice), "structural");
     // Contexts built before this call counted the old set.
@@ -623,7 +652,7 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     if (!b) return Fail(GM_ERR_USAGE, "null batch");
     gm_engine* e = b->engine;
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
-    if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (logits && ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
@@ -654,7 +683,7 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
     if (!b) return Fail(GM_ERR_USAGE, "null batch");
     gm_engine* e = b->engine;
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
-    if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (logits && ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
@@ -688,7 +717,7 @@ int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words
     if (!b) return Fail(GM_ERR_USAGE, "null batch");
     gm_engine* e = b->engine;
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
-    if (logits && ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (logits && ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
@@ -810,7 +839,7 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
   return Guard([&]() -> int {
     if (!b || !logits) return Fail(GM_ERR_USAGE, "null argument");
     gm_engine* e = b->engine;
-    if (ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -879,7 +908,7 @@ int gm_sample_tokens(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, const
   return Guard([&]() -> int {
     if (!b || !logits_bf16 || !bitmask) return Fail(GM_ERR_USAGE, "null argument");
     gm_engine* e = b->engine;
-    if (ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     if (ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     return SampleCommon(b, logits_bf16, ld, bitmask, ld_words, temperature, top_k, top_p, seed, tokens_out,
@@ -893,7 +922,7 @@ int gm_decode_step_sample(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, 
   return Guard([&]() -> int {
     if (!b || !logits_bf16) return Fail(GM_ERR_USAGE, "null argument");
     gm_engine* e = b->engine;
-    if (ld < e->V + 1) return Fail(GM_ERR_USAGE, "ld < V + 1");
+    if (ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -903,6 +932,100 @@ int gm_decode_step_sample(gm_batch* b, const uint16_t* logits_bf16, int64_t ld, 
     if (rc != GM_OK) return rc;
     return SampleCommon(b, logits_bf16, ld, bm, ldw, temperature, top_k, top_p, seed, tokens_out, true, s);
   });
+}
+
+// ---------------------------------------------------------------- CUDA graphs
+struct gm_graph {
+  gm_batch* batch = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int prod0 = 0, last0 = 0, fill0 = 0, steps = 0;
+  ~gm_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+int gm_decode_graph_create(gm_batch* b, int32_t kind, int32_t steps, uint32_t* const* bitmask, int64_t ld_words,
+                           const uint16_t* const* logits, int64_t ld, int32_t* const* seg_counts, uint64_t seed,
+                           int32_t* const* tokens_out, gm_graph** out) {
+  return Guard([&]() -> int {
+    if (!b || !out || steps <= 0 || steps % pre3::kFillPeriod != 0) {
+      return Fail(GM_ERR_USAGE, "steps must be a positive multiple of 6");
+    }
+    if (kind != 0 && kind != 1) return Fail(GM_ERR_USAGE, "kind must be 0 (stream split step) or 1 (greedy)");
+    if (kind == 1 && !logits) return Fail(GM_ERR_USAGE, "the greedy step needs logits");
+    gm_engine* e = b->engine;
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    if (!b->capture_stream) Check(cudaStreamCreateWithFlags(&b->capture_stream, cudaStreamNonBlocking), "stream");
+    cudaStream_t cs = b->capture_stream;
+    // Steady state first (not captured): the next fill's context slots are
+    // looked up and no arrivals are pending, as after any decode step — so
+    // the captured steps launch exactly the fill + accept kernels.
+    Check(cudaDeviceSynchronize(), "sync");
+    if (!b->slots_valid) {
+      Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, cs), "lookup launch");
+      b->slots_valid = true;
+      b->lookup_pending = true;
+    }
+    b->ClearArrivals(cs);
+    Check(cudaStreamSynchronize(cs), "sync");
+    auto g = std::make_unique<gm_graph>();
+    g->batch = b;
+    g->prod0 = b->prod;
+    g->last0 = b->last_consumed;
+    g->fill0 = b->fill_seq;
+    g->steps = steps;
+    cudaGraph_t graph = nullptr;
+    Check(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+    int rc = GM_OK;
+    for (int32_t i = 0; i < steps && rc == GM_OK; ++i) {
+      uint32_t* bm = bitmask ? bitmask[i] : nullptr;
+      int32_t* to = tokens_out ? tokens_out[i] : nullptr;
+      if (kind == 1) {
+        rc = gm_decode_step_greedy(b, logits[i], ld, bm, ld_words, to, cs);
+      } else {
+        rc = gm_decode_step_stream_split(b, bm, ld_words, logits ? const_cast<uint16_t*>(logits[i]) : nullptr, ld,
+                                         seg_counts ? seg_counts[i] : nullptr, seed, to, cs);
+      }
+    }
+    const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+    if (rc != GM_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    Check(ec, "end capture");
+    const cudaError_t ei = cudaGraphInstantiate(&g->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    Check(ei, "graph instantiate");
+    // The host bookkeeping advanced by `steps` (a multiple of the period):
+    // it is back at the state the graph starts from.
+    if (b->prod != g->prod0 || b->fill_seq != g->fill0 || !b->slots_valid || !b->lookup_pending) {
+      return Fail(GM_ERR_USAGE, "internal: step bookkeeping not periodic");
+    }
+    *out = g.release();
+    return GM_OK;
+  });
+}
+
+int gm_graph_launch(gm_graph* g, void* stream) {
+  return Guard([&]() -> int {
+    if (!g || !g->exec) return Fail(GM_ERR_USAGE, "null graph");
+    gm_batch* b = g->batch;
+    // The graph bakes in the queue ring position and fill numbers of its
+    // capture: replay only from that state (any 6k eager steps return to it).
+    if (b->prod != g->prod0 || b->last_consumed != g->last0 || b->fill_seq != g->fill0 || !b->slots_valid ||
+        !b->lookup_pending || b->arrivals_pending) {
+      return Fail(GM_ERR_USAGE, "batch is not at the graph's start state (run a multiple of 6 eager steps of the "
+                                "same kind, or re-capture)");
+    }
+    Check(cudaSetDevice(b->engine->device), "cudaSetDevice");
+    Check(cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)), "graph launch");
+    return GM_OK;
+  });
+}
+
+int gm_graph_destroy(gm_graph* g) {
+  delete g;
+  return GM_OK;
 }
 
 int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed, void* stream) {

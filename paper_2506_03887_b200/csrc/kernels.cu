@@ -46,6 +46,16 @@ __device__ __forceinline__ unsigned long long Mix64(unsigned long long x) {
   return x ^ (x >> 31);
 }
 
+// Token ids at the ABI vs mask bits (VocabView::layout): with a model logit
+// layout the ABI speaks columns (EOS = eos_col); bits stay the reference's
+// (EOS = V).  An id that is no token maps past V (the accept kills it).
+__device__ __forceinline__ int IdToBit(const VocabView& Vv, int id) {
+  if (!Vv.layout || id < 0) return id;
+  if (id == Vv.eos_col) return Vv.V;
+  return id < Vv.V ? id : Vv.V + 1;
+}
+__device__ __forceinline__ int BitToId(const VocabView& Vv, int t) { return (Vv.layout && t == Vv.V) ? Vv.eos_col : t; }
+
 // A candidate record in registers: header, first 4 pushed states, condition
 // entries 1..16 — six independent 16-B loads (one round trip).
 struct Rec {
@@ -218,6 +228,7 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
   const bool eos = t == V;
   const int4 tr = __ldg(tok_rec + t);  // offset, length, first 8 bytes: one round trip
   const int nterm = tr.y;
+  if (nterm == 0) return kReject;  // a disabled id (gm_engine_options::disabled)
   const uint8_t* bytes = tok_bytes + tr.x;
   int state = base[nb - 1];
   int x_next = eos ? 256 : TokByte(tr, 0);
@@ -325,6 +336,7 @@ __device__ int WalkWarp(const AutView& A, const VocabView& Vv, int32_t t, const 
   const int4 tr = __ldg(Vv.tok_rec + t);
   const int off = tr.x;
   const int nterm = tr.y;
+  if (nterm == 0) return kReject;  // a disabled id
   const int xb = TokLaneByte(tr, Vv.tok_bytes, lane, nterm, eos);
   int ov = -1;  // overlay entry `lane`
   int nl = 0;
@@ -592,6 +604,8 @@ __device__ int AssignSlotKey(const CacheView& Cc, const BatchView& Bt, int q, in
 // lookup pass rewrites all entries, so an entry is at most one fill stale and
 // the tag tells the fill whether it was written for it.
 __device__ __forceinline__ int HeavyTag(int fill_no, int idx) { return ((fill_no & 0x7fff) << 16) | idx; }
+__device__ __forceinline__ int NextFill(int fill_no) { return fill_no + 1 == kFillPeriod ? 0 : fill_no + 1; }
+__device__ __forceinline__ int PrevFill(int fill_no) { return fill_no == 0 ? kFillPeriod - 1 : fill_no - 1; }
 
 // heavy_index is double-buffered by fill parity: the fused tail of fill N
 // writes fill N+1's entries while fill N's CTAs may still read their own.
@@ -998,6 +1012,7 @@ __device__ void AcceptWarp(const AutView& A, const VocabView& Vv, const CacheVie
     const bool eos = tok == Vv.V;
     const int4 tr = __ldg(Vv.tok_rec + tok);
     const int nterm = tr.y;
+    if (nterm == 0) st.status = kDead;  // a disabled id: never allowed (the loop below is skipped)
     const uint8_t* bytes = Vv.tok_bytes + tr.x;
     const int xb = TokLaneByte(tr, Vv.tok_bytes, lane, nterm, eos);
     for (int i = 0; i < nterm; ++i) {
@@ -1424,6 +1439,31 @@ __device__ __forceinline__ unsigned long long WarpMax64(unsigned long long v) {
   return v;
 }
 
+// The EOS bit (mask bit V) of sequence b for an item of another segment
+// (logit layouts whose EOS column lies among the regular ids): a pure-CI
+// sequence's is its slot's CI bit (its stack may already be changing under
+// the overlapped accept); any other sequence's accept waits for this item's
+// arrival, so its stack is stable and EOS (one terminal) is walked on it —
+// Step(kEndMarker) succeeds iff AllowedTerminals reports the end marker.
+__device__ __forceinline__ int EosBitOf(const AutView& A, const VocabView& Vv, const CacheView& Cc,
+                                        const BatchView& Bt, int b, int slot, bool pure) {
+  if (pure) return static_cast<int>((__ldcg(Cc.ci + static_cast<long long>(slot) * Vv.W + (Vv.V >> 5)) >> (Vv.V & 31)) & 1u);
+  const SeqState st = Bt.seq[b];
+  if (st.status != kAlive) return 0;
+  return WalkToken(A, Vv, Vv.V, Bt.stacks + static_cast<long long>(b) * Bt.cap, st.depth, true) == kAccept ? 1 : 0;
+}
+
+// Logit columns [V, ncols) of a model layout (specials, EOS column): -inf,
+// except the EOS column when EOS is allowed.  Lanes stride the columns.
+__device__ __forceinline__ void TailColumns(const VocabView& Vv, uint16_t* row, int eos_bit, int lane, int nlanes,
+                                            unsigned long long* wr) {
+  for (int c = Vv.V + lane; c < Vv.ncols; c += nlanes) {
+    if (c == Vv.eos_col && eos_bit) continue;
+    row[c] = 0xFF80u;
+    *wr += 2;
+  }
+}
+
 // The sequence's last finished fill item: sample (stream or greedy), accept,
 // restart, and look up the next step's context slot.  One warp.
 template <int TAIL>
@@ -1443,9 +1483,9 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
     st.draws += 1;
     if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
   }
-  if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = tok;
+  if (F.tokens_out != nullptr && lane == 0) F.tokens_out[b] = BitToId(Vv, tok);
   if (lane == 0) Bt.seq_arrive[b] = 0;
-  AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, 2, F.produce, F.fill_no + 1,
+  AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, 2, F.produce, NextFill(F.fill_no),
              lane);
   if (lane == 0) TraceEvent(Bt, kTraceTail, b, 0, t_in, static_cast<unsigned long long>(tok + 1));
 }
@@ -1463,6 +1503,11 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   const int nwords = min(Vv.W - w0, kSegWords);
   const int t0 = w0 * 32;
   const int t1 = min(Vv.V + 1, t0 + nwords * 32);
+  // Logit columns mapped 1:1 to mask bits (a model layout maps bit V to its
+  // EOS column and masks the columns >= V itself, TailColumns).
+  const int tl1 = Vv.layout ? min(Vv.V, t1) : t1;
+  const bool last_seg = seg == Vv.nseg - 1;
+  const bool eos_in_seg = Vv.layout && Vv.eos_col < Vv.V && Vv.eos_col >= t0 && Vv.eos_col < tl1;
   const bool wait = slot >= 0 && (slot & kSlotWait);
   if (slot >= 0) slot &= ~kSlotWait;
   if (wait) {
@@ -1564,6 +1609,20 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = cs;
     }
   }
+  // ---- model logit layout: the EOS bit where this item needs it (the last
+  // segment holds bit V; an EOS column among the regular ids is patched into
+  // this item's words for the logits pass below — bitmask rows keep the
+  // reference layout).
+  int eos_bit = 0;
+  if (Vv.layout && (last_seg || eos_in_seg)) {
+    if (last_seg) {
+      const int we = (Vv.V >> 5) - w0;
+      eos_bit = static_cast<int>((__shfl_sync(0xffffffffu, Pick(m, we >> 5), we & 31) >> (Vv.V & 31)) & 1u);
+    } else {
+      if (lane == 0) eos_bit = slot == -2 ? 0 : EosBitOf(A, Vv, Cc, Bt, b, slot, pure);
+      eos_bit = __shfl_sync(0xffffffffu, eos_bit, 0);
+    }
+  }
   unsigned long long rd = 0, wr = 0;
   if (MODE == kFillGreedy) {
     // Argmax over the allowed entries: only 16-B chunks holding an allowed
@@ -1571,7 +1630,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     // buffer) so a span's round trip overlaps the previous span's compare.
     const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
     unsigned long long mine = 0;
-    const int nfull = F.vec_ok ? (t1 - t0) >> 10 : 0;
+    const int nfull = F.vec_ok ? (tl1 - t0) >> 10 : 0;
     uint32_t live = 0u;
 #pragma unroll
     for (int i = 0; i < kSpans; ++i) {
@@ -1605,8 +1664,13 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
 #pragma unroll 1
     for (int i = nfull; i < kSpans; ++i) {
       const int tw = t0 + 1024 * i;
-      if (tw >= t1) break;
-      const unsigned long long p = ArgmaxSpan(row, tw, t1, F.vec_ok, Pick(m, i), lane, &rd);
+      if (tw >= tl1) break;
+      const unsigned long long p = ArgmaxSpan(row, tw, tl1, F.vec_ok, Pick(m, i), lane, &rd);
+      mine = p > mine ? p : mine;
+    }
+    if (Vv.layout && last_seg && eos_bit && lane == 0) {  // EOS competes with its column's logit, as bit V
+      const unsigned long long p = GreedyKey(row[Vv.eos_col], Vv.V);
+      rd += 2;
       mine = p > mine ? p : mine;
     }
     mine = WarpMax64(mine);
@@ -1625,12 +1689,20 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   }
   if (MODE == kFillMask && F.logits != nullptr) {
     uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
+    if (eos_in_seg) {  // the EOS column carries bit V, not its (disabled) id's bit
+      const int wi = (Vv.eos_col - t0) >> 5;
+      const uint32_t bit = 1u << (Vv.eos_col & 31);
+#pragma unroll
+      for (int i = 0; i < kSpans; ++i) {
+        if (i == (wi >> 5) && lane == (wi & 31)) m[i] = eos_bit ? (m[i] | bit) : (m[i] & ~bit);
+      }
+    }
     // Full spans by class: all allowed -> untouched; all masked -> one bulk
     // (TMA) store of 2 KB of -inf from shared memory, issued by lane 0;
     // mixed -> 16-B chunks, two spans in flight: the mixed chunks of the next
     // two mixed spans are being copied (cp.async, no registers held) while
     // one is blended and stored.  Then a partial last span, if any.
-    const int nfull = F.vec_ok ? (t1 - t0) >> 10 : 0;
+    const int nfull = F.vec_ok ? (tl1 - t0) >> 10 : 0;
     uint32_t masked = 0u, mixed = 0u;
 #pragma unroll
     for (int i = 0; i < kSpans; ++i) {
@@ -1673,8 +1745,9 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     }
 #pragma unroll 1
     for (int i = nfull; i < kSpans; ++i) {
-      if (t0 + 1024 * i < t1) MaskSpan(row, t0 + 1024 * i, t1, F.vec_ok, Pick(m, i), lane, &rd, &wr);
+      if (t0 + 1024 * i < tl1) MaskSpan(row, t0 + 1024 * i, tl1, F.vec_ok, Pick(m, i), lane, &rd, &wr);
     }
+    if (Vv.layout && last_seg) TailColumns(Vv, row, eos_bit, lane, 32, &wr);
     if (masked && lane == 0) BulkWaitRead();  // the -inf source outlives the reads
   }
   if (Bt.stats_enabled) {
@@ -1713,7 +1786,7 @@ struct FillShared {
   int pre[kSegWords];
   int scratch[kThreads / 32 + 1];
   unsigned long long best[kThreads / 32];
-  int unit, last;
+  int unit, last, eos;
 };
 
 // Grid: h_grid (<= 2 per SM) heavy CTAs, then ceil(B * nseg / kWarps) light CTAs.
@@ -1899,12 +1972,31 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
       F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = ts;
     }
   }
+  // Model logit layout (LightItem): the EOS bit where the logits need it.
+  const int tl1 = Vv.layout ? min(Vv.V, t1) : t1;
+  const bool last_seg = seg == Vv.nseg - 1;
+  const bool eos_in_seg = Vv.layout && Vv.eos_col < Vv.V && Vv.eos_col >= t0 && Vv.eos_col < tl1;
+  if (Vv.layout && (last_seg || eos_in_seg)) {
+    if (last_seg) {
+      if (w0 + tid == (Vv.V >> 5)) sh.eos = static_cast<int>((mword >> (Vv.V & 31)) & 1u);
+    } else if (tid == 0) {
+      const int sl = SeqSlot(Bt, F.fill_no)[b];
+      sh.eos = sl == -2 ? 0 : EosBitOf(A, Vv, Cc, Bt, b, sl & ~kSlotWait, false);
+    }
+  }
+  __syncthreads();
+  const int eos_bit = Vv.layout && (last_seg || eos_in_seg) ? sh.eos : 0;
   // Warp w covers words [32w, 32w+32) of the segment = one 1024-token span.
   unsigned long long rd = 0, wr = 0;
   const int tw = t0 + warp * 1024;
   if (MODE == kFillGreedy) {
     const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
-    unsigned long long mine = tw < t1 ? ArgmaxSpan(row, tw, t1, F.vec_ok, mword, lane, &rd) : 0ull;
+    unsigned long long mine = tw < tl1 ? ArgmaxSpan(row, tw, tl1, F.vec_ok, mword, lane, &rd) : 0ull;
+    if (Vv.layout && last_seg && eos_bit && tid == 0) {  // EOS competes with its column's logit, as bit V
+      const unsigned long long p = GreedyKey(row[Vv.eos_col], Vv.V);
+      rd += 2;
+      mine = p > mine ? p : mine;
+    }
     mine = WarpMax64(mine);
     if (lane == 0) sh.best[warp] = mine;
     __syncthreads();
@@ -1926,8 +2018,14 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
     __syncthreads();
     last = sh.last;
   }
-  if (MODE == kFillMask && F.logits != nullptr && tw < t1) {
-    MaskSpan(F.logits + static_cast<long long>(b) * F.ld, tw, t1, F.vec_ok, mword, lane, &rd, &wr);
+  if (MODE == kFillMask && F.logits != nullptr) {
+    uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
+    if (eos_in_seg && w0 + tid == (Vv.eos_col >> 5)) {  // the EOS column carries bit V
+      const uint32_t bit = 1u << (Vv.eos_col & 31);
+      mword = eos_bit ? (mword | bit) : (mword & ~bit);
+    }
+    if (tw < tl1) MaskSpan(row, tw, tl1, F.vec_ok, mword, lane, &rd, &wr);
+    if (Vv.layout && last_seg && warp == 0) TailColumns(Vv, row, eos_bit, lane, 32, &wr);
   }
   if (Bt.stats_enabled) {
     rd = static_cast<unsigned long long>(WarpSum(static_cast<int>(rd)));
@@ -1977,8 +2075,8 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
     if (G.ci_shortcut) {
       // Pure CI (the fill's own test, LightItem): its bitmask row is the
       // slot's CI row and its counts the slot's — sample from those now.
-      const int slot = SeqSlot(Bt, G.lookup_tag - 1)[b];
-      const uint32_t hm = SeqHmask(Bt, G.lookup_tag - 1)[b];
+      const int slot = SeqSlot(Bt, PrevFill(G.lookup_tag))[b];
+      const uint32_t hm = SeqHmask(Bt, PrevFill(G.lookup_tag))[b];
       pure = hm == 0u && slot >= 0 && slot < Cc.C && Vv.nseg <= 32;
       if (pure) {
         row = Cc.ci + static_cast<long long>(slot) * Vv.W;
@@ -2002,7 +2100,7 @@ __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv
                                            unsigned long long t_in) {
   int tok = -1;
   if (SAMPLE == kSampleGiven) {
-    tok = G.tokens[b];
+    tok = IdToBit(Vv, G.tokens[b]);
   } else if (SAMPLE == kSampleGreedy) {
     const unsigned long long p = G.best[b];
     tok = p ? static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(p)) : -1;
@@ -2013,7 +2111,7 @@ __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv
     st.draws += 1;
     if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
   }
-  if (G.tokens_out != nullptr && lane == 0) G.tokens_out[b] = tok;
+  if (G.tokens_out != nullptr && lane == 0) G.tokens_out[b] = BitToId(Vv, tok);
   if (!G.do_accept) {
     if (lane == 0) Bt.seq[b].draws = st.draws;
     return;
@@ -2123,14 +2221,16 @@ enum : int { kPassHi = 0, kPassWeights = 1, kPassLoBin = 2 };
 
 // One pass over the allowed tokens of row b (chunks of 8 tokens whose mask
 // byte is non-zero).  fn(t, key) per allowed token.
+// Bit t's logit is column t, except EOS (bit V): column eos_col (the model
+// logit layout, VocabView; eos_col = V in the reference layout).
 template <typename Fn>
-__device__ __forceinline__ void ForAllowed(const uint32_t* mrow, const uint16_t* row, int V1, bool vec_ok, int c_begin,
-                                           int c_end, int c_step, Fn&& fn) {
+__device__ __forceinline__ void ForAllowed(const uint32_t* mrow, const uint16_t* row, int V, int eos_col, bool vec_ok,
+                                           int c_begin, int c_end, int c_step, Fn&& fn) {
   for (int c = c_begin; c < c_end; c += c_step) {
     const uint32_t byte = (__ldg(mrow + (c >> 2)) >> ((c & 3) * 8)) & 0xffu;
     if (!byte) continue;
     const int tb = c * 8;
-    if (vec_ok && tb + 8 <= V1) {
+    if (vec_ok && tb + 8 <= V) {
       const uint4 q = __ldcg(reinterpret_cast<const uint4*>(row + tb));
       const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -2138,8 +2238,8 @@ __device__ __forceinline__ void ForAllowed(const uint32_t* mrow, const uint16_t*
         if ((byte >> j) & 1u) fn(tb + j, SampleKey((w4[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu));
       }
     } else {
-      for (int j = 0; j < 8 && tb + j < V1; ++j) {
-        if ((byte >> j) & 1u) fn(tb + j, SampleKey(row[tb + j]));
+      for (int j = 0; j < 8 && tb + j <= V; ++j) {
+        if ((byte >> j) & 1u) fn(tb + j, SampleKey(row[tb + j == V ? eos_col : tb + j]));
       }
     }
   }
@@ -2177,7 +2277,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   __syncthreads();
   // ---- pass 1: high-byte counts, max key, |allowed|.
   unsigned int kmax = 0u, n_allowed = 0u;
-  ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+  ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
     atomicAdd(&sh.u.pw.cnt_hi_w[warp][key >> 8], 1u);
     kmax = key > kmax ? key : kmax;
     ++n_allowed;
@@ -2247,7 +2347,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
       for (int i = tid; i < kSampleKeySlots * 256; i += kThreads) sh.u.kcnt[i >> 8][i & 255] = 0u;
       __syncthreads();
     }
-    ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+    ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
       const int h = static_cast<int>(key >> 8);
       if (h > hi_k) {
         if (nslots >= 0) atomicAdd(&sh.u.kcnt[sh.hslot[h]][key & 0xffu], 1u);
@@ -2335,7 +2435,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
                                   SampleWeight((static_cast<uint32_t>(hp) << 8) | tid, vmax, S.temperature)
                             : 0ull;
         } else {
-          ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+          ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
             if (static_cast<int>(key >> 8) == hp) {
               atomicAdd(&sh.cnt_lo2[key & 0xffu], 1u);
               atomicAdd(&sh.w_lo2[key & 0xffu], SampleWeight(key, vmax, S.temperature));
@@ -2397,7 +2497,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
                                   SampleWeight((static_cast<uint32_t>(hs) << 8) | tid, vmax, S.temperature)
                             : 0ull;
         } else {
-          ForAllowed(mrow, row, V1, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+          ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
             if (static_cast<int>(key >> 8) == hs) {
               atomicAdd(&sh.cnt_lo2[key & 0xffu], 1u);
               atomicAdd(&sh.w_lo2[key & 0xffu], SampleWeight(key, vmax, S.temperature));
@@ -2421,7 +2521,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     const int per = (nchunks + kThreads - 1) / kThreads;
     const int c0 = tid * per, c1 = min(nchunks, c0 + per);
     unsigned int mine = 0u;
-    ForAllowed(mrow, row, V1, S.vec_ok, c0, c1, 1, [&](int, uint32_t key) { mine += key == kappa; });
+    ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, c0, c1, 1, [&](int, uint32_t key) { mine += key == kappa; });
     int total = 0;
     const int excl = BlockExclusiveScan(static_cast<int>(mine), reinterpret_cast<int*>(sh.red), &total);
     if (tid == 0) sh.found = -1;
@@ -2429,7 +2529,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     if (jth >= static_cast<unsigned long long>(excl) && jth < static_cast<unsigned long long>(excl) + mine) {
       unsigned int want = static_cast<unsigned int>(jth) - static_cast<unsigned int>(excl);
       int hit = -1;
-      ForAllowed(mrow, row, V1, S.vec_ok, c0, c1, 1, [&](int t, uint32_t key) {
+      ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, c0, c1, 1, [&](int t, uint32_t key) {
         if (key == kappa) {
           if (want == 0u && hit < 0) hit = t;
           --want;
@@ -2443,7 +2543,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   // ---- accept (warp 0): Step per byte, restart, next context lookup.
   if (warp == 0) {
     st.draws += 1;
-    if (S.tokens_out != nullptr && lane == 0) S.tokens_out[b] = tok;
+    if (S.tokens_out != nullptr && lane == 0) S.tokens_out[b] = BitToId(Vv, tok);
     if (S.do_accept) {
       AcceptWarp(A, Vv, Cc, Bt, b, st, StackWindow(Bt, b, st.depth, lane), tok, nullptr, S.restart ? 2 : 0, S.lookup_queue,
                  S.lookup_tag, lane);

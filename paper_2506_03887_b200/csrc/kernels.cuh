@@ -17,6 +17,11 @@ constexpr int kChunksPerSeg = kSegTokens / kThreads;  // build work units per se
 constexpr int kMaxContext = 32;                       // max K (one warp lane per key entry)
 constexpr int kWalkOverlay = 64;                      // per-thread pushed-entry overlay in a mask walk
 constexpr int kSlotWait = 1 << 30;                    // seq_slot flag: wait for the slot's build
+// Fill numbers (heavy-list tags, double-buffer parity) count modulo 6: a tag
+// only has to tell a fill from its neighbours, and a period dividing the
+// 3-queue ring and the parity makes the host bookkeeping of any 6k steps
+// return to its start state — so captured CUDA graphs of 6k steps replay.
+constexpr int kFillPeriod = 6;
 
 // Per-sequence device state: {depth, status, draws, reserved}.
 struct SeqState {
@@ -54,6 +59,14 @@ struct VocabView {
   int32_t V;                   // regular tokens; EOS = V
   int32_t W;                   // ceil((V+1)/32)
   int32_t nseg;                // ceil(W / kSegWords)
+  // The model's logit-row layout (gm_engine_options num_columns/eos_column):
+  // column c < ncols holds mask bit V if c == eos_col, else bit c if c < V,
+  // else a special token (-inf in every fused logits call).  layout == 0:
+  // the reference layout (ncols = V + 1, eos_col = V).  Token ids at the ABI
+  // are columns (EOS = eos_col) once a layout is set.
+  int32_t ncols;
+  int32_t eos_col;
+  int32_t layout;
 };
 
 // Context cache (engine-wide, shared by batches on the device).  Key =

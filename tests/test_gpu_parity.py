@@ -719,3 +719,62 @@ def test_token_id_beyond_vocabulary_kills_the_sequence():
     b.accept(torch.tensor([4, 1 << 30], dtype=torch.int32, device=DEV), st)
     b.check()
     assert st.cpu().tolist() == [pk.DEAD, pk.DEAD]
+
+
+@pytest.mark.parametrize("greedy", [False, True])
+def test_captured_graph_steps_match_eager_and_port(greedy):
+    """gm_decode_graph_create / gm_graph_launch: 12 captured steps replayed
+    twice (24 steps) give, step for step, the eager loop's tokens and the C
+    port's; a replay from a state the graph was not captured at is refused."""
+    vocab = pk.synth_vocab(40000)
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=12)
+    port = Port(f, vocab)
+    B, G, seed = 48, 12, 31
+    V1 = eng.V + 1
+    logits = [torch.empty((B, V1), dtype=torch.bfloat16, device=DEV) for _ in range(3)]
+    for k, t in enumerate(logits):
+        pk.synth_logits(t, k, 77)
+    kw = dict(greedy_rows=3, logit_seed=77) if greedy else {}
+    _, ptoks, pstacks = port.decode_run(eng.structural, B, 2 * G, seed, want_tokens=True, want_stacks=True, **kw)
+    batch = eng.batch(B)
+    bms = [torch.zeros((B, eng.W), dtype=torch.int32, device=DEV) for _ in range(G)]
+    cnt = [torch.zeros((B, 2 * batch.nseg), dtype=torch.int32, device=DEV) for _ in range(G)]
+    tks = [torch.zeros(B, dtype=torch.int32, device=DEV) for _ in range(G)]
+    graph = batch.capture_steps(G, greedy=greedy, seed=seed, bitmask=bms, logits=[logits[i % 3] for i in range(G)],
+                                seg_counts=None if greedy else cnt, tokens_out=tks)
+    got = []
+    for rep in range(2):
+        graph.launch()
+        batch.check()
+        got.append(torch.stack(tks, 1).cpu().numpy())
+        for i in (0, G - 1):
+            m = bms[i].cpu().numpy().view(np.uint32)
+            assert np.array_equal(oracle_mask_hashes(m), port_hashes(port, eng, B, 2 * G, seed, kw)[:, rep * G + i])
+    assert np.array_equal(np.concatenate(got, 1), ptoks)
+    for b in range(B):
+        d = pstacks[b, 0]
+        assert batch.get(b).stack == pstacks[b, 2:2 + d].tolist()
+    # one eager step moves the batch off the graph's start state
+    toks = torch.zeros(B, dtype=torch.int32, device=DEV)
+    if greedy:
+        batch.decode_step_greedy(logits[0], tokens_out=toks)
+    else:
+        batch.decode_step_stream_split(seed, tokens_out=toks)
+    with pytest.raises(pk.GmError):
+        graph.launch()
+
+
+_PORT_HASHES = {}
+
+
+def port_hashes(port, eng, B, steps, seed, kw):
+    key = (id(port), B, steps, seed, tuple(sorted(kw.items())))
+    if key not in _PORT_HASHES:
+        _PORT_HASHES[key] = port.decode_run(eng.structural, B, steps, seed, want_mask_hashes=True, **kw)[3]
+    return _PORT_HASHES[key]
+
+
+def oracle_mask_hashes(m):
+    import oracle
+    return oracle.mask_hashes(m)
