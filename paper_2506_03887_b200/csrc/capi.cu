@@ -967,6 +967,11 @@ int gm_decode_graph_create(gm_batch* b, int32_t kind, int32_t steps, uint32_t* c
       b->lookup_pending = true;
     }
     b->ClearArrivals(cs);
+    // A fresh batch has no previously drained queue (reset = -1); every later
+    // fill resets the queue drained before it.  Name that ring position now
+    // (resetting the untouched queue is a no-op) so the captured first fill
+    // is the same as at every replay start.
+    if (b->last_consumed < 0) b->last_consumed = (b->prod + 2) % 3;
     Check(cudaStreamSynchronize(cs), "sync");
     auto g = std::make_unique<gm_graph>();
     g->batch = b;
@@ -998,7 +1003,8 @@ int gm_decode_graph_create(gm_batch* b, int32_t kind, int32_t steps, uint32_t* c
     Check(ei, "graph instantiate");
     // The host bookkeeping advanced by `steps` (a multiple of the period):
     // it is back at the state the graph starts from.
-    if (b->prod != g->prod0 || b->fill_seq != g->fill0 || !b->slots_valid || !b->lookup_pending) {
+    if (b->prod != g->prod0 || b->last_consumed != g->last0 || b->fill_seq != g->fill0 || !b->slots_valid ||
+        !b->lookup_pending || b->arrivals_pending) {
       return Fail(GM_ERR_USAGE, "internal: step bookkeeping not periodic");
     }
     *out = g.release();

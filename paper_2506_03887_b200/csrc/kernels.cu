@@ -208,6 +208,7 @@ __device__ __forceinline__ int IndexedFindEdge(const int16_t* hlens,
   return best;
 }
 
+template <int kOverlay>
 __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* rec_begin, const CandRec* recs,
                                           const int32_t* rec_cond, const int32_t* rec_push, const int32_t* shift,
                                           const int4* tok_rec, const uint8_t* tok_bytes, int32_t V, int32_t t,
@@ -223,7 +224,7 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
     const int32_t* rec_push;
     const int32_t* shift;
   } A{first, rec_begin, recs, rec_cond, rec_push, shift};
-  int32_t loc[kWalkOverlay];
+  int32_t loc[kOverlay];
   int nl = 0;
   const bool eos = t == V;
   const int4 tr = __ldg(tok_rec + t);  // offset, length, first 8 bytes: one round trip
@@ -301,7 +302,16 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
       nb -= k - nl;
       nl = 0;
     }
-    if (nl + fr.push_len + 1 > kWalkOverlay) return kOverflow;
+    if (nl + fr.push_len + 1 > kOverlay) {
+      // Retry policy: see WalkToken.
+      if constexpr (kOverlay < kDeepOverlay) {
+        if (!complete) return kUnknown;
+        return WalkTokenImpl<kDeepOverlay>(first, rec_begin, recs, rec_cond, rec_push, shift, tok_rec, tok_bytes, V,
+                                           t, base, nb, complete, hmeta, hlens, hexact, emask, hprefix, pmask);
+      } else {
+        return kOverflow;
+      }
+    }
     for (int j = 0; j < fr.push_len; ++j) loc[nl++] = j < 4 ? Lane4(fr.p, j) : __ldg(A.rec_push + fr.push_off + j);
     if (fr.new_state < 0) {
       const int top = nl > 0 ? loc[nl - 1] : (nb > 0 ? base[nb - 1] : -1);
@@ -316,11 +326,17 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
   return kAccept;
 }
 
+// A walk whose pushes pass the 64-entry overlay is retried with a 1,024-entry
+// one (local memory; long BPE tokens that open many nested values).  On a
+// partial key (a shared context slot) an overflowing token is context-
+// dependent instead: the cached row must not reject it for good — each fill
+// then walks it on the sequence's whole stack.  Only a walk that overflows
+// the deep overlay too returns kOverflow (the caller raises Bt.err).
 __device__ __forceinline__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
                                          bool complete) {
-  return WalkTokenImpl(A.first, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_rec, Vv.tok_bytes,
-                       Vv.V, t, base, nb, complete, A.hidx_meta, A.hidx_lens, A.hidx_exact, A.hidx_exact_mask,
-                       A.hidx_prefix, A.hidx_prefix_mask);
+  return WalkTokenImpl<kWalkOverlay>(A.first, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_rec,
+                                     Vv.tok_bytes, Vv.V, t, base, nb, complete, A.hidx_meta, A.hidx_lens,
+                                     A.hidx_exact, A.hidx_exact_mask, A.hidx_prefix, A.hidx_prefix_mask);
 }
 
 // The same walk done by one warp for one token (complete stacks only): lanes

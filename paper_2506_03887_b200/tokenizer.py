@@ -14,10 +14,23 @@ Supported token encodings:
 
 Added / special tokens (``added_tokens`` with ``special: true``) have no
 byte form: they are never allowed by a grammar, except the EOS token, which
-the engine represents as mask bit V (``TokenMask::SetEos``, runtime.hpp:62-85).
-The regular tokens must occupy ids 0..V-1 (true for the tokenizers above), so
-the mask's bit t is the model's logit t for every regular token; the caller
-maps EOS (model id ``eos_model_id``) to bit V.
+the reference represents as mask bit V (``TokenMask::SetEos``,
+runtime.hpp:62-85).  The engine speaks the model's logit layout
+(``gm_engine_options``): engine token id t < V is model column t, columns
+>= V are specials (-inf), and mask bit V lands on the EOS column.  So:
+
+* V = 1 + the largest id of a regular token; a special or an unused id below
+  V (Llama-2 / Mistral put ``<unk> <s> </s>`` at ids 0..2) is a *disabled*
+  id, never allowed;
+* two ids with the same bytes (SentencePiece ``<0xNN>`` byte-fallback pieces
+  next to the single-character piece, ``▁`` next to ``<0x20>``) would break
+  TokenTrie::Build's no-duplicate rule (runtime.cpp:23-53): one canonical id
+  keeps the bytes (the ordinary piece before a ``<0xNN>`` piece, then the
+  lower id) and the others become disabled aliases (``aliases``: alias ->
+  canonical), so a constrained sampler emits the canonical id.
+
+``TokenizerVocab.engine_options()`` gives the DeviceEngine keyword arguments
+for this layout.
 """
 from __future__ import annotations
 
@@ -44,15 +57,33 @@ _UNICODE_TO_BYTE = {v: k for k, v in bytes_to_unicode().items()}
 
 @dataclass
 class TokenizerVocab:
-    tokens: List[bytes]                       # regular tokens, ids 0..V-1
-    eos_model_id: Optional[int]               # model id of EOS (mask bit V)
+    tokens: List[bytes]                       # engine ids 0..V-1 = model columns 0..V-1 (b"" if disabled)
+    eos_model_id: Optional[int]               # model column of EOS (mask bit V)
     specials: Dict[int, str] = field(default_factory=dict)  # model id -> content (never allowed)
     encoding: str = "byte_level"              # or "sentencepiece"
-    model_vocab_size: int = 0                 # regular + special ids
+    model_vocab_size: int = 0                 # logit columns: regular + special ids
+    disabled: List[int] = field(default_factory=list)     # ids < V never allowed (specials, holes, aliases)
+    aliases: Dict[int, int] = field(default_factory=dict)  # duplicate-bytes id -> canonical id
 
     @property
     def V(self) -> int:
         return len(self.tokens)
+
+    def token_bytes(self, model_id: int) -> bytes:
+        """The bytes of a model token id (an alias decodes as its canonical id)."""
+        return self.tokens[self.aliases.get(model_id, model_id)]
+
+    def engine_options(self) -> Dict[str, object]:
+        """DeviceEngine(num_columns=, eos_column=, disabled=) for this model's
+        logit layout.  Without an EOS token the EOS bit goes to an extra
+        column V (the reference layout) when no special sits there."""
+        ncols = max(self.model_vocab_size, self.V)
+        eos = self.eos_model_id
+        if eos is None:
+            if ncols == self.V:
+                return dict(num_columns=0, eos_column=0, disabled=list(self.disabled))
+            raise ValueError("this vocabulary has special columns but no EOS token; pass eos_token=")
+        return dict(num_columns=ncols, eos_column=eos, disabled=list(self.disabled))
 
 
 def _walk(node, kinds):
@@ -111,11 +142,32 @@ def from_tokenizer_json(source: Union[str, bytes, dict], eos_token: Optional[str
         if i not in specials:
             id_of.setdefault(t["content"], i)
     regular = {i: s for s, i in id_of.items() if i not in specials}
-    V = len(regular)
-    if sorted(regular) != list(range(V)):
-        raise ValueError("regular tokens must occupy ids 0..V-1 (specials after them)")
+    if not regular:
+        raise ValueError("tokenizer.json has no regular tokens")
+    if min(regular) < 0 or min(specials, default=0) < 0:
+        raise ValueError("negative token id")
+    V = max(regular) + 1
     conv = _byte_level_bytes if byte_level else _sentencepiece_bytes
-    tokens = [conv(regular[i]) for i in range(V)]
+    tokens: List[bytes] = [b""] * V
+    disabled = set(range(V)) - set(regular)  # specials and unused ids below V
+    aliases: Dict[int, int] = {}
+    canon: Dict[bytes, int] = {}
+
+    def rank(i: int):  # the canonical id of a byte string: ordinary piece first, then the lower id
+        p = regular[i]
+        return (len(p) == 6 and p.startswith("<0x") and p.endswith(">"), i)
+
+    for i in sorted(regular, key=rank):
+        b = conv(regular[i])
+        if not b:
+            disabled.add(i)  # an empty piece can never be a TokenTrie token
+            continue
+        if b in canon:
+            aliases[i] = canon[b]
+            disabled.add(i)
+            continue
+        canon[b] = i
+        tokens[i] = b
     eos_id = None
     if eos_token is not None:
         for i, c in specials.items():
@@ -131,7 +183,7 @@ def from_tokenizer_json(source: Union[str, bytes, dict], eos_token: Optional[str
                 break
     all_ids = set(regular) | set(specials)
     return TokenizerVocab(tokens=tokens, eos_model_id=eos_id, specials=specials, encoding=encoding,
-                          model_vocab_size=(max(all_ids) + 1) if all_ids else 0)
+                          model_vocab_size=max(all_ids) + 1, disabled=sorted(disabled), aliases=aliases)
 
 
 def vocabulary_json(tokens: List[bytes]) -> str:

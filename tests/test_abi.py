@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 25
     for n in sorted(names):
         assert hasattr(lib, n), f"{n} declared in include/ but not exported"
-    assert lib.gm_abi_version() == 1
+    assert lib.gm_abi_version() == 2
 
 
 @pytest.mark.parametrize("name", FIXTURES)

@@ -53,9 +53,10 @@ def sentencepiece_json():
     tok.pre_tokenizer = pre_tokenizers.Metaspace(replacement="▁", prepend_scheme="never")
     tok.decoder = decoders.Sequence([decoders.Replace("▁", " "), decoders.ByteFallback(), decoders.Fuse()])
     byte_tokens = [f"<0x{b:02X}>" for b in range(256)]
-    trainer = trainers.BpeTrainer(vocab_size=800, special_tokens=byte_tokens, show_progress=False)
+    # Llama-2 layout: <unk> <s> </s> at ids 0..2, then the byte-fallback pieces, then the merges
+    trainer = trainers.BpeTrainer(vocab_size=800, special_tokens=["<unk>", "<s>", "</s>"] + byte_tokens,
+                                  show_progress=False)
     tok.train_from_iterator(CORPUS, trainer)
-    tok.add_special_tokens(["</s>"])
     data = json.loads(tok.to_str())
     # the byte-fallback pieces are ordinary vocabulary entries in real files
     data["added_tokens"] = [t for t in data["added_tokens"] if not t["content"].startswith("<0x")]
@@ -78,11 +79,30 @@ def test_sentencepiece_byte_fallback_roundtrip(sentencepiece_json):
     tok, text = sentencepiece_json
     tv = tk.from_tokenizer_json(text)
     assert tv.encoding == "sentencepiece"
-    assert tv.eos_model_id == tok.token_to_id("</s>")
-    assert tv.tokens[tok.token_to_id("<0x0A>")] == b"\n"
+    assert tv.eos_model_id == tok.token_to_id("</s>") == 2
+    assert tv.token_bytes(tok.token_to_id("<0x0A>")) == b"\n"
+    # specials below V and duplicate byte strings are disabled ids, leaving
+    # a TokenTrie-valid vocabulary ('<0x61>' vs 'a', '<0x20>' vs '▁')
+    assert {0, 1, 2} <= set(tv.disabled)
+    assert tv.aliases and all(tv.tokens[a] == b"" and tv.tokens[c] for a, c in tv.aliases.items())
+    assert tv.aliases.get(tok.token_to_id("<0x20>")) == tok.token_to_id("▁")
+    live = [t for i, t in enumerate(tv.tokens) if i not in set(tv.disabled)]
+    assert len(live) == len(set(live)) == tv.V - len(tv.disabled) and all(live)
+    opts = tv.engine_options()
+    assert opts["eos_column"] == 2 and opts["num_columns"] == tv.model_vocab_size == tv.V
     for s in random_texts(300, seed=1):
         ids = tok.encode(s).ids
-        assert b"".join(tv.tokens[i] for i in ids) == s.encode("utf-8"), s
+        assert b"".join(tv.token_bytes(i) for i in ids) == s.encode("utf-8"), s
+    port = oracle.Port(open(__file__.replace("test_tokenizer.py", "golden/json.p3dpda"), "rb").read(),
+                       port_vocab(tv))
+    m = port.mask(port.initial())
+    assert not any((int(m[i >> 5]) >> (i & 31)) & 1 for i in tv.disabled)
+
+
+def port_vocab(tv):
+    """The engine vocabulary for the C port, which has no disabled ids: each
+    disabled id gets unique bytes the JSON grammar can never accept."""
+    return [t if t else b"\x01\x02" + i.to_bytes(4, "little") for i, t in enumerate(tv.tokens)]
 
 
 def test_vocabulary_file_roundtrip(byte_level_json):
@@ -108,8 +128,12 @@ def test_tokenizer_vocab_drives_the_reference_matcher(byte_level_json):
 def test_errors():
     with pytest.raises(ValueError):
         tk.from_tokenizer_json({"model": {}})
-    bad = {"model": {"type": "BPE", "vocab": {"a": 0, "b": 2}}, "added_tokens": []}
+    holes = tk.from_tokenizer_json({"model": {"type": "BPE", "vocab": {"a": 0, "b": 2}}, "added_tokens": []})
+    assert holes.V == 3 and holes.disabled == [1]  # an unused id below V is disabled
+    assert holes.engine_options()["num_columns"] == 0  # no specials: the reference layout (EOS = column V)
+    pad_only = tk.from_tokenizer_json({"model": {"type": "BPE", "vocab": {"a": 0}},
+                                       "added_tokens": [{"id": 1, "content": "<pad>", "special": True}]})
     with pytest.raises(ValueError):
-        tk.from_tokenizer_json(bad)  # regular ids must be contiguous
+        pad_only.engine_options()  # special columns but no EOS column to put bit V on
     with pytest.raises(ValueError):
         tk.from_tokenizer_json({"model": {"type": "BPE", "vocab": {"a": 0}}, "added_tokens": []}, eos_token="</s>")
