@@ -457,11 +457,11 @@ def main(argv=None):
                     contexts_built=eng.info()["context_slots_used"],
                     note=f"{args.cold_steps} steps of {B} sequences from an empty context table (before the "
                          "prewarm; streams seeded apart from the timed ones)")
-        del cb, cbm, ccn, ctk
+        del cstep, cb, cbm, ccn, ctk  # the batch goes away: its queued builds are drained
 
     t_pre = time.perf_counter()
     if args.prewarm_steps > 0:
-        eng.prewarm(args.prewarm_batch, args.prewarm_steps, seed=0xC0FFEE + rank)
+        eng.prewarm(args.prewarm_batch, args.prewarm_steps, seed=0xC0FFEE + rank, stack_capacity=args.stack_cap)
     t_pre = time.perf_counter() - t_pre
     pre_info = eng.info()
 

@@ -43,6 +43,7 @@ enum gm_status_code {
   GM_ERR_STACK_OVERFLOW = 6,  /* a device stack or walk overlay overflowed */
   GM_ERR_VOCAB_EMPTY = 7,     /* VocabError::kEmptyToken (runtime.hpp:29-37) */
   GM_ERR_VOCAB_DUPLICATE = 8, /* VocabError::kDuplicateToken */
+  GM_ERR_SNAPSHOT_MISMATCH = 9, /* a context snapshot taken for another automaton / vocabulary / K, R, slots */
   GM_ERR_USAGE = 64           /* bad argument (CLI exit 64) */
 };
 
@@ -142,9 +143,24 @@ int gm_engine_info(gm_engine* e, int64_t info[8]);
 int gm_engine_set_structural(gm_engine* e, const uint32_t* host_words);
 /* Preprocessing: populates the context cache by running `steps` synthetic
  * stream decode steps over `batch` scratch sequences (seeded by `seed`) on
- * the device; synchronizes `stream`.  Results of later fills are identical
- * with or without it (the cache only changes speed). */
-int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed, void* stream);
+ * the device, stacks of `stack_capacity` entries (<= 0: 1024; overflow
+ * restarts a sequence); synchronizes `stream`.  Results of later fills are
+ * identical with or without it (the cache only changes speed). */
+int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed, int32_t stack_capacity,
+                      void* stream);
+
+/* Context-table snapshot "P3GMCTX1" (the reference's cache
+ * precedent: SerializeDpda / DeserializeDpda, src/serialize.cpp:148-294).
+ * save: every fully built context slot into a host buffer (buf = NULL:
+ * query *size); synchronizes the device.  load: into an engine whose
+ * context table is still empty, created from the same automaton (grammar
+ * hash, dpda_builder.cpp:469-476, + device-layout hash), vocabulary and
+ * logit layout, K, R and slot count — else GM_ERR_SNAPSHOT_MISMATCH;
+ * truncated or altered data -> GM_ERR_CORRUPT_INPUT (checksummed).  A loaded
+ * table gives the same masks as the prewarm that built it (the cache only
+ * changes speed), without running it. */
+int gm_engine_snapshot_save(gm_engine* e, void* buf, uint64_t cap, uint64_t* size);
+int gm_engine_snapshot_load(gm_engine* e, const void* buf, uint64_t bytes);
 
 /* ------------------------------------------------------------ batch */
 /* B sequences with fixed-capacity device stacks (reference stacks are
@@ -279,7 +295,9 @@ int gm_batch_time_next_fill(gm_batch* b, void* start_event, void* end_event);
 /* Statistics accumulated while enabled (gm_batch_set_stats), reset on read:
  * stats[0] = logits bytes read, [1] = logits bytes written (16-B chunk
  * granularity), [2] = context-dependent token walks, [3] = build items,
- * [4] = private segment fills, [5] = 0. */
+ * [4] = private segment fills, [5] = segment fills that gave up waiting
+ * for a context build and walked every token (should stay 0: a fill builds
+ * any unclaimed chunk itself, whichever batch queued it). */
 int gm_batch_fill_stats(gm_batch* b, int64_t stats[6]);
 int gm_batch_set_stats(gm_batch* b, int32_t enable);
 /* Diagnostics: per-item timing records of later fill / accept launches into

@@ -31,6 +31,7 @@ GM_ERR_CUDA = 5
 GM_ERR_STACK_OVERFLOW = 6
 GM_ERR_VOCAB_EMPTY = 7
 GM_ERR_VOCAB_DUPLICATE = 8
+GM_ERR_SNAPSHOT_MISMATCH = 9
 GM_ERR_USAGE = 64
 
 ALIVE, DEAD, ACCEPTED, OVERFLOW = 0, 1, 2, 3
@@ -73,6 +74,10 @@ class StackOverflowError(GmError):
     pass
 
 
+class SnapshotMismatchError(GmError):
+    """A context snapshot taken for another automaton / vocabulary / K, R, slots."""
+
+
 _ERRORS = {
     GM_ERR_GRAMMAR: GrammarError,
     GM_ERR_BUILD: BuildError,
@@ -81,6 +86,7 @@ _ERRORS = {
     GM_ERR_STACK_OVERFLOW: StackOverflowError,
     GM_ERR_VOCAB_EMPTY: VocabError,
     GM_ERR_VOCAB_DUPLICATE: VocabError,
+    GM_ERR_SNAPSHOT_MISMATCH: SnapshotMismatchError,
 }
 
 _lib = None
@@ -112,7 +118,9 @@ def lib() -> ctypes.CDLL:
             "gm_engine_destroy": ([P], ctypes.c_int),
             "gm_engine_info": ([P, P], ctypes.c_int),
             "gm_engine_set_structural": ([P, P], ctypes.c_int),
-            "gm_engine_prewarm": ([P, I32, I32, U64, P], ctypes.c_int),
+            "gm_engine_prewarm": ([P, I32, I32, U64, I32, P], ctypes.c_int),
+            "gm_engine_snapshot_save": ([P, P, U64, ctypes.POINTER(U64)], ctypes.c_int),
+            "gm_engine_snapshot_load": ([P, P, U64], ctypes.c_int),
             "gm_batch_create": ([P, I32, I32, PP], ctypes.c_int),
             "gm_batch_destroy": ([P], ctypes.c_int),
             "gm_batch_reset": ([P, P], ctypes.c_int),
@@ -356,9 +364,36 @@ class DeviceEngine:
                 "parent_builds", "device"]
         return dict(zip(keys, (int(x) for x in out)))
 
-    def prewarm(self, batch: int = 1024, steps: int = 200, seed: int = 0x5EED, stream=None) -> None:
-        """Populates the context cache with synthetic decode streams (preprocessing)."""
-        _check(lib().gm_engine_prewarm(self._h, batch, steps, seed, _stream(stream)))
+    def prewarm(self, batch: int = 1024, steps: int = 200, seed: int = 0x5EED, stack_capacity: int = 1024,
+                 stream=None) -> None:
+        """Populates the context cache with synthetic decode streams (preprocessing)
+        over sequences of the given stack capacity (overflow restarts them)."""
+        _check(lib().gm_engine_prewarm(self._h, batch, steps, seed, stack_capacity, _stream(stream)))
+
+    def save_contexts(self, path: Optional[str] = None):
+        """gm_engine_snapshot_save: the built context table ("P3GMCTX1") into
+        `path` (written through a memory map), or returned as bytes."""
+        size = ctypes.c_uint64()
+        _check(lib().gm_engine_snapshot_save(self._h, None, 0, ctypes.byref(size)))
+        if path is None:
+            buf = np.empty(size.value, np.uint8)
+        else:
+            buf = np.memmap(path, np.uint8, "w+", shape=(max(size.value, 1),))
+        _check(lib().gm_engine_snapshot_save(self._h, _ptr(buf), size.value, ctypes.byref(size)))
+        if path is None:
+            return buf.tobytes()
+        buf.flush()
+        del buf
+        return size.value
+
+    def load_contexts(self, source) -> None:
+        """gm_engine_snapshot_load from a path or bytes (instead of a prewarm;
+        the table must still be empty)."""
+        if isinstance(source, (bytes, bytearray)):
+            buf = np.frombuffer(source, np.uint8)
+        else:
+            buf = np.memmap(source, np.uint8, "r")
+        _check(lib().gm_engine_snapshot_load(self._h, _ptr(buf) if buf.size else None, buf.size))
 
     def batch(self, size: int, stack_capacity: int = 1024) -> "Batch":
         return Batch(self, size, stack_capacity)
@@ -634,7 +669,7 @@ class Batch:
         out = np.zeros(6, np.int64)
         _check(lib().gm_batch_fill_stats(self._h, _ptr(out)))
         return dict(zip(["logit_bytes_read", "logit_bytes_written", "cd_walks", "build_items",
-                         "private_fills", "reserved"], (int(x) for x in out)))
+                         "private_fills", "build_wait_timeouts"], (int(x) for x in out)))
 
     def __del__(self):
         if getattr(self, "_h", None) and self._h.value and _lib is not None:

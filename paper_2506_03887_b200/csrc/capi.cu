@@ -66,6 +66,32 @@ int Guard(F&& f) {
   }
 }
 
+// Word-wise 64-bit hash (multiply-xorshift) for snapshot keys and checksums.
+uint64_t Hash64(const void* data, size_t n, uint64_t h = 0x243F6A8885A308D3ull) {
+  const uint8_t* p = static_cast<const uint8_t*>(data);
+  auto mix = [](uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    return x ^ (x >> 33);
+  };
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    uint64_t w;
+    std::memcpy(&w, p + i, 8);
+    h = (h ^ mix(w)) * 0x9E3779B97F4A7C15ull;
+  }
+  uint64_t t = 0;
+  std::memcpy(&t, p + i, n - i);
+  return mix(h ^ mix(t ^ (static_cast<uint64_t>(n) << 3)));
+}
+
+template <typename T>
+uint64_t HashVec(const std::vector<T>& v, uint64_t h) {
+  return Hash64(v.data(), v.size() * sizeof(T), h);
+}
+
 }  // namespace
 
 struct gm_engine {
@@ -76,6 +102,9 @@ struct gm_engine {
   pre3::CacheView cache{};
   uint32_t* structural = nullptr;
   std::vector<uint32_t> disabled;  // host copy (W words) or empty
+  // Snapshot key (gm_engine_snapshot_*): the automaton's grammar hash, a hash
+  // of the flattened device layout and one of the vocabulary + logit layout.
+  uint64_t grammar_hash = 0, layout_hash = 0, vocab_hash = 0;
   std::vector<void*> owned;
   ~gm_engine() {
     cudaSetDevice(device);
@@ -350,6 +379,16 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     e->aut.state_any = DevUpload(f.state_any, &e->owned);
     e->aut.num_states = a->a.num_states;
     e->aut.initial = a->a.initial_state;
+    e->grammar_hash = a->a.grammar_hash;
+    {
+      uint64_t h = HashVec(f.rec_begin, 1);
+      h = HashVec(f.recs, h);
+      h = HashVec(f.rec_cond, h);
+      h = HashVec(f.rec_push, h);
+      h = HashVec(a->a.shift_targets, h);
+      const int64_t ids[2] = {a->a.num_states, a->a.initial_state};
+      e->layout_hash = Hash64(ids, sizeof ids, h);
+    }
 
     e->V = num_tokens;
     e->W = (num_tokens + 1 + 31) / 32;
@@ -389,6 +428,12 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
       e->disabled.assign(o.disabled, o.disabled + W);
       e->disabled[static_cast<size_t>(num_tokens >> 5)] &= (1u << (num_tokens & 31)) - 1u;  // ids < V only
     }
+    {
+      uint64_t h = HashVec(bytes, 2);
+      h = HashVec(recs, h);  // offsets and lengths (0 = disabled)
+      const int32_t lay[3] = {e->vocab.ncols, e->vocab.eos_col, num_tokens};
+      e->vocab_hash = Hash64(lay, sizeof lay, h);
+    }
 
     const size_t C = static_cast<size_t>(o.context_slots);
     auto& c = e->cache;
@@ -401,6 +446,8 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.cdb = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
     c.cd_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
     c.seg_done = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
+    c.seg_claim = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg), &e->owned);
+    Check(cudaMemset(c.seg_claim, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
     c.slot_built = DevAlloc<int32_t>(C, &e->owned);
     c.slot_parent = DevAlloc<int32_t>(C, &e->owned);
     Check(cudaMemset(c.slot_parent, 0xff, C * 4), "memset");
@@ -590,7 +637,7 @@ int gm_batch_check(gm_batch* b, void* stream) {
     Check(cudaMemcpy(&err, b->view.err, 4, cudaMemcpyDeviceToHost), "check");
     if (err) {
       Check(cudaMemset(b->view.err, 0, 4), "memset");
-      return Fail(GM_ERR_STACK_OVERFLOW, "a mask walk exceeded its 64-entry push overlay");
+      return Fail(GM_ERR_STACK_OVERFLOW, "a mask walk pushed more than 1,024 entries above the stack (walk overlay)");
     }
     return GM_OK;
   });
@@ -1034,11 +1081,248 @@ int gm_graph_destroy(gm_graph* g) {
   return GM_OK;
 }
 
-int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed, void* stream) {
+// ---------------------------------------------------------------- snapshots
+// Context-table snapshot "P3GMCTX1" (the reference's cache
+// precedent is SerializeDpda/DeserializeDpda, src/serialize.cpp:148-294):
+// every fully built context slot, keyed by (grammar hash
+// (dpda_builder.cpp:469-476), device-layout hash, vocabulary + logit-layout
+// hash, K, R, C).  Little-endian:
+//   header: magic[8] "P3GMCTX1", u32 version 1, u32 header bytes (96),
+//           u64 grammar_hash, u64 layout_hash, u64 vocab_hash,
+//           i32 K, R, C, V, W, nseg, n (slots), kMaxContext,
+//           u64 payload bytes, u64 payload checksum (Hash64), u64 0 (reserved)
+//   payload: i32 slot[n], i32 meta[n], i32 parent[n], u32 cd_segmask[n],
+//            u64 hash[n], then per slot a block of kMaxContext + 3*nseg + 2*W
+//            words: key row, cd_cnt[nseg], ci_cnt[nseg][2], ci[W], cdb[W].
+namespace {
+
+constexpr char kSnapMagic[8] = {'P', '3', 'G', 'M', 'C', 'T', 'X', '1'};
+constexpr uint32_t kSnapHeader = 96;
+
+struct SnapHeader {
+  char magic[8];
+  uint32_t version, header_bytes;
+  uint64_t grammar_hash, layout_hash, vocab_hash;
+  int32_t K, R, C, V, W, nseg, n, max_context;
+  uint64_t payload_bytes, checksum, reserved;
+};
+static_assert(sizeof(SnapHeader) == kSnapHeader, "snapshot header layout");
+
+constexpr int kSnapChunk = 1024;  // slots per gather/scatter launch
+
+struct SlotTables {
+  std::vector<unsigned long long> hash;
+  std::vector<int32_t> meta, built, parent;
+  std::vector<uint32_t> segmask;
+};
+
+SlotTables ReadSlotTables(const gm_engine* e) {
+  const size_t C = static_cast<size_t>(e->cache.C);
+  SlotTables t;
+  t.hash.resize(C);
+  t.meta.resize(C);
+  t.built.resize(C);
+  t.parent.resize(C);
+  t.segmask.resize(C);
+  Check(cudaMemcpy(t.hash.data(), e->cache.slot_hash, C * 8, cudaMemcpyDeviceToHost), "snapshot read");
+  Check(cudaMemcpy(t.meta.data(), e->cache.slot_meta, C * 4, cudaMemcpyDeviceToHost), "snapshot read");
+  Check(cudaMemcpy(t.built.data(), e->cache.slot_built, C * 4, cudaMemcpyDeviceToHost), "snapshot read");
+  Check(cudaMemcpy(t.parent.data(), e->cache.slot_parent, C * 4, cudaMemcpyDeviceToHost), "snapshot read");
+  Check(cudaMemcpy(t.segmask.data(), e->cache.cd_segmask, C * 4, cudaMemcpyDeviceToHost), "snapshot read");
+  return t;
+}
+
+size_t SnapBlockWords(const gm_engine* e) {
+  return static_cast<size_t>(pre3::kMaxContext) + 3 * static_cast<size_t>(e->nseg) + 2 * static_cast<size_t>(e->W);
+}
+
+}  // namespace
+
+int gm_engine_snapshot_save(gm_engine* e, void* buf, uint64_t cap, uint64_t* size) {
+  return Guard([&]() -> int {
+    if (!e || !size) return Fail(GM_ERR_USAGE, "null argument");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    Check(cudaDeviceSynchronize(), "snapshot: work in flight");
+    const SlotTables t = ReadSlotTables(e);
+    const int32_t full = e->nseg * pre3::kChunksPerSeg;
+    std::vector<int32_t> ids;
+    for (int32_t i = 0; i < e->cache.C; ++i) {
+      if (t.hash[static_cast<size_t>(i)] != 0ull && (t.meta[static_cast<size_t>(i)] & (1 << 16)) &&
+          t.built[static_cast<size_t>(i)] == full) {
+        ids.push_back(i);
+      }
+    }
+    const size_t n = ids.size(), blk = SnapBlockWords(e);
+    const uint64_t payload = n * (4 * 4 + 8) + n * blk * 4;
+    *size = kSnapHeader + payload;
+    if (!buf) return GM_OK;
+    if (cap < *size) return Fail(GM_ERR_USAGE, "buffer too small");
+    uint8_t* out = static_cast<uint8_t*>(buf);
+    uint8_t* p = out + kSnapHeader;
+    auto put = [&p](const void* src, size_t bytes) {
+      if (bytes) std::memcpy(p, src, bytes);
+      p += bytes;
+    };
+    std::vector<int32_t> meta(n), parent(n);
+    std::vector<uint32_t> segmask(n);
+    std::vector<unsigned long long> hash(n);
+    std::unordered_set<int32_t> saved(ids.begin(), ids.end());
+    for (size_t k = 0; k < n; ++k) {
+      const size_t i = static_cast<size_t>(ids[k]);
+      meta[k] = t.meta[i];
+      parent[k] = saved.count(t.parent[i]) ? t.parent[i] : -1;  // a link only matters while building
+      segmask[k] = t.segmask[i];
+      hash[k] = t.hash[i];
+    }
+    put(ids.data(), n * 4);
+    put(meta.data(), n * 4);
+    put(parent.data(), n * 4);
+    put(segmask.data(), n * 4);
+    put(hash.data(), n * 8);
+    if (n) {
+      std::vector<void*> tmp;
+      int32_t* d_ids = DevAlloc<int32_t>(kSnapChunk, &tmp);
+      uint32_t* d_blk = DevAlloc<uint32_t>(kSnapChunk * blk, &tmp);
+      try {
+        for (size_t k0 = 0; k0 < n; k0 += kSnapChunk) {
+          const int m = static_cast<int>(std::min<size_t>(kSnapChunk, n - k0));
+          Check(cudaMemcpy(d_ids, ids.data() + k0, static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice), "snapshot");
+          Check(pre3::LaunchSnapshotRows(e->cache, e->W, e->nseg, d_ids, m, d_blk, false, nullptr), "snapshot gather");
+          Check(cudaMemcpy(p, d_blk, static_cast<size_t>(m) * blk * 4, cudaMemcpyDeviceToHost), "snapshot");
+          p += static_cast<size_t>(m) * blk * 4;
+        }
+      } catch (...) {
+        for (void* q : tmp) cudaFree(q);
+        throw;
+      }
+      for (void* q : tmp) cudaFree(q);
+    }
+    SnapHeader h{};
+    std::memcpy(h.magic, kSnapMagic, 8);
+    h.version = 1;
+    h.header_bytes = kSnapHeader;
+    h.grammar_hash = e->grammar_hash;
+    h.layout_hash = e->layout_hash;
+    h.vocab_hash = e->vocab_hash;
+    h.K = e->cache.K;
+    h.R = e->cache.R;
+    h.C = e->cache.C;
+    h.V = e->V;
+    h.W = e->W;
+    h.nseg = e->nseg;
+    h.n = static_cast<int32_t>(n);
+    h.max_context = pre3::kMaxContext;
+    h.payload_bytes = payload;
+    h.checksum = Hash64(out + kSnapHeader, payload);
+    std::memcpy(out, &h, sizeof h);
+    return GM_OK;
+  });
+}
+
+int gm_engine_snapshot_load(gm_engine* e, const void* buf, uint64_t bytes) {
+  return Guard([&]() -> int {
+    if (!e || !buf) return Fail(GM_ERR_USAGE, "null argument");
+    if (bytes < kSnapHeader) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: truncated header");
+    SnapHeader h;
+    std::memcpy(&h, buf, sizeof h);
+    if (std::memcmp(h.magic, kSnapMagic, 8) != 0) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: bad magic");
+    if (h.version != 1 || h.header_bytes != kSnapHeader) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: unknown version");
+    const uint8_t* in = static_cast<const uint8_t*>(buf);
+    if (h.payload_bytes != bytes - kSnapHeader) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: size mismatch");
+    if (Hash64(in + kSnapHeader, h.payload_bytes) != h.checksum) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: checksum");
+    if (h.grammar_hash != e->grammar_hash || h.layout_hash != e->layout_hash) {
+      return Fail(GM_ERR_SNAPSHOT_MISMATCH, "snapshot: taken for another automaton");
+    }
+    if (h.vocab_hash != e->vocab_hash || h.V != e->V || h.W != e->W || h.nseg != e->nseg) {
+      return Fail(GM_ERR_SNAPSHOT_MISMATCH, "snapshot: taken for another vocabulary or logit layout");
+    }
+    if (h.K != e->cache.K || h.R != e->cache.R || h.C != e->cache.C || h.max_context != pre3::kMaxContext) {
+      return Fail(GM_ERR_SNAPSHOT_MISMATCH, "snapshot: taken with other context options (K, R, slots)");
+    }
+    const size_t n = static_cast<size_t>(h.n), blk = SnapBlockWords(e);
+    if (h.n < 0 || h.n > h.C || h.payload_bytes != n * (4 * 4 + 8) + n * blk * 4) {
+      return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: slot count");
+    }
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    Check(cudaDeviceSynchronize(), "snapshot: work in flight");
+    unsigned long long ctr[8];
+    Check(cudaMemcpy(ctr, e->cache.counters, 64, cudaMemcpyDeviceToHost), "snapshot");
+    if (ctr[0] != 0 || ctr[2] != 0) return Fail(GM_ERR_USAGE, "snapshot: the context table is not empty");
+    const uint8_t* p = in + kSnapHeader;
+    std::vector<int32_t> ids(n), meta(n), parent(n);
+    std::vector<uint32_t> segmask(n);
+    std::vector<unsigned long long> hash(n);
+    auto get = [&p](void* dst, size_t b) {
+      if (b) std::memcpy(dst, p, b);
+      p += b;
+    };
+    get(ids.data(), n * 4);
+    get(meta.data(), n * 4);
+    get(parent.data(), n * 4);
+    get(segmask.data(), n * 4);
+    get(hash.data(), n * 8);
+    SlotTables t = ReadSlotTables(e);
+    const int32_t full = e->nseg * pre3::kChunksPerSeg;
+    for (size_t k = 0; k < n; ++k) {
+      const int32_t i = ids[k];
+      if (i < 0 || i >= h.C || t.hash[static_cast<size_t>(i)] != 0ull || hash[k] == 0ull ||
+          !(meta[k] & (1 << 16)) || (meta[k] & 0xff) > e->cache.K || parent[k] < -1 || parent[k] >= h.C) {
+        return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: bad slot record");
+      }
+      t.hash[static_cast<size_t>(i)] = hash[k];
+      t.meta[static_cast<size_t>(i)] = meta[k];
+      t.built[static_cast<size_t>(i)] = full;
+      t.parent[static_cast<size_t>(i)] = parent[k];
+      t.segmask[static_cast<size_t>(i)] = segmask[k];
+    }
+    // Rows first, then the tables that publish them.
+    if (n) {
+      std::vector<void*> tmp;
+      int32_t* d_ids = DevAlloc<int32_t>(kSnapChunk, &tmp);
+      uint32_t* d_blk = DevAlloc<uint32_t>(kSnapChunk * blk, &tmp);
+      try {
+        for (size_t k0 = 0; k0 < n; k0 += kSnapChunk) {
+          const int m = static_cast<int>(std::min<size_t>(kSnapChunk, n - k0));
+          Check(cudaMemcpy(d_ids, ids.data() + k0, static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice), "snapshot");
+          Check(cudaMemcpy(d_blk, p, static_cast<size_t>(m) * blk * 4, cudaMemcpyHostToDevice), "snapshot");
+          Check(pre3::LaunchSnapshotRows(e->cache, e->W, e->nseg, d_ids, m, d_blk, true, nullptr), "snapshot scatter");
+          Check(cudaDeviceSynchronize(), "snapshot scatter");
+          p += static_cast<size_t>(m) * blk * 4;
+        }
+      } catch (...) {
+        for (void* q : tmp) cudaFree(q);
+        throw;
+      }
+      for (void* q : tmp) cudaFree(q);
+    }
+    const size_t C = static_cast<size_t>(e->cache.C);
+    std::vector<int32_t> seg_done(C * static_cast<size_t>(e->nseg), 0);
+    for (size_t k = 0; k < n; ++k) {
+      std::fill_n(seg_done.begin() + static_cast<ptrdiff_t>(static_cast<size_t>(ids[k]) * e->nseg), e->nseg,
+                  pre3::kChunksPerSeg);
+    }
+    Check(cudaMemcpy(e->cache.seg_done, seg_done.data(), seg_done.size() * 4, cudaMemcpyHostToDevice), "snapshot");
+    Check(cudaMemcpy(e->cache.seg_claim, seg_done.data(), seg_done.size() * 4, cudaMemcpyHostToDevice), "snapshot");
+    Check(cudaMemcpy(e->cache.slot_built, t.built.data(), C * 4, cudaMemcpyHostToDevice), "snapshot");
+    Check(cudaMemcpy(e->cache.slot_parent, t.parent.data(), C * 4, cudaMemcpyHostToDevice), "snapshot");
+    Check(cudaMemcpy(e->cache.cd_segmask, t.segmask.data(), C * 4, cudaMemcpyHostToDevice), "snapshot");
+    Check(cudaMemcpy(e->cache.slot_meta, t.meta.data(), C * 4, cudaMemcpyHostToDevice), "snapshot");
+    Check(cudaMemcpy(e->cache.slot_hash, t.hash.data(), C * 8, cudaMemcpyHostToDevice), "snapshot");
+    ctr[0] = n;
+    Check(cudaMemcpy(e->cache.counters, ctr, 64, cudaMemcpyHostToDevice), "snapshot");
+    // The CI ∩ structural counts follow the engine's current structural set.
+    Check(pre3::LaunchRecountStructural(e->cache, e->vocab), "snapshot recount");
+    Check(cudaDeviceSynchronize(), "snapshot load");
+    return GM_OK;
+  });
+}
+
+int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed, int32_t stack_capacity,
+                      void* stream) {
   return Guard([&]() -> int {
     if (!e || batch < 1 || steps < 0) return Fail(GM_ERR_USAGE, "bad argument");
     gm_batch* b = nullptr;
-    int rc = gm_batch_create(e, batch, 1024, &b);
+    int rc = gm_batch_create(e, batch, stack_capacity > 0 ? stack_capacity : 1024, &b);
     if (rc != GM_OK) return rc;
     std::unique_ptr<gm_batch> guard(b);
     for (int32_t s = 0; s < steps; ++s) {

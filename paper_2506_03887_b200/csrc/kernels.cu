@@ -226,6 +226,7 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
   } A{first, rec_begin, recs, rec_cond, rec_push, shift};
   int32_t loc[kOverlay];
   int nl = 0;
+  const int nb0 = nb;  // the walk pops base entries (nb shrinks); a retry starts over
   const bool eos = t == V;
   const int4 tr = __ldg(tok_rec + t);  // offset, length, first 8 bytes: one round trip
   const int nterm = tr.y;
@@ -307,7 +308,7 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
       if constexpr (kOverlay < kDeepOverlay) {
         if (!complete) return kUnknown;
         return WalkTokenImpl<kDeepOverlay>(first, rec_begin, recs, rec_cond, rec_push, shift, tok_rec, tok_bytes, V,
-                                           t, base, nb, complete, hmeta, hlens, hexact, emask, hprefix, pmask);
+                                           t, base, nb0, complete, hmeta, hlens, hexact, emask, hprefix, pmask);
       } else {
         return kOverflow;
       }
@@ -779,7 +780,37 @@ __device__ void HelpBuild(const AutView& A, const VocabView& Vv, const CacheView
     const unsigned int u = static_cast<unsigned int>(*sh_unit);
     __syncthreads();
     if (u >= units) break;
-    BuildUnit(A, Vv, Cc, Bt, Q.items[u / kChunksPerSeg], static_cast<int>(u % kChunksPerSeg), base_s, sh_unit);
+    const int4 it = Q.items[u / kChunksPerSeg];
+    int chunk = static_cast<int>(u % kChunksPerSeg);
+    if (it.x < Cc.C) {
+      // A shared slot's chunks go to whoever claims them first (this queue's
+      // units or a helper, HelpSegment): a unit whose claim comes too late
+      // has nothing left to build.
+      if (threadIdx.x == 0) *sh_unit = atomicAdd(Cc.seg_claim + static_cast<long long>(it.x) * Vv.nseg + it.y, 1);
+      __syncthreads();
+      chunk = *sh_unit;
+      __syncthreads();
+      if (chunk >= kChunksPerSeg) continue;
+    }
+    BuildUnit(A, Vv, Cc, Bt, it, chunk, base_s, sh_unit);
+  }
+}
+
+// A CTA that needs (slot, seg) built now builds every chunk nobody has
+// claimed yet, whichever batch's queue listed it (a batch that stopped
+// stepping leaves its queued builds unclaimed; other batches must not wait
+// on them).  Chunks claimed by others are being built by running CTAs, so
+// the caller's bounded wait then completes.  CTA-cooperative.
+__device__ void HelpSegment(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int slot,
+                            int seg, int b, int32_t* base_s, int* sh_unit) {
+  int* claim = Cc.seg_claim + static_cast<long long>(slot) * Vv.nseg + seg;
+  for (;;) {
+    if (threadIdx.x == 0) *sh_unit = LoadRelaxed(claim) < kChunksPerSeg ? atomicAdd(claim, 1) : kChunksPerSeg;
+    __syncthreads();
+    const int chunk = *sh_unit;
+    __syncthreads();
+    if (chunk >= kChunksPerSeg) break;
+    BuildUnit(A, Vv, Cc, Bt, make_int4(slot, seg, b, 0), chunk, base_s, sh_unit);
   }
 }
 
@@ -1777,6 +1808,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       }
       if (n_walks) atomicAdd(Bt.stats + 2, static_cast<unsigned long long>(n_walks));
       if (slot >= Cc.C) atomicAdd(Bt.stats + 4, 1ull);
+      if (slot == -3) atomicAdd(Bt.stats + 5, 1ull);  // gave up waiting for a build
     }
   }
   if (lane == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
@@ -1896,6 +1928,7 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
   const bool wait = slot >= 0 && (slot & kSlotWait);
   if (slot >= 0) slot &= ~kSlotWait;
   if (wait) {
+    if (slot < Cc.C) HelpSegment(A, Vv, Cc, Bt, slot, seg, b, stack_s, &sh.unit);
     if (tid == 0) sh.unit = WaitBuilt(Cc, Bt, slot, seg, Vv.nseg) ? 1 : 0;
     __syncthreads();
     if (!sh.unit) slot = -3;  // direct fill
@@ -2052,6 +2085,7 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
     }
     if (tid == 0 && n_walks) atomicAdd(Bt.stats + 2, n_walks);
     if (tid == 0 && slot >= Cc.C) atomicAdd(Bt.stats + 4, 1ull);
+    if (tid == 0 && slot == -3) atomicAdd(Bt.stats + 5, 1ull);  // gave up waiting for a build
   }
   if (tid == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
   if (tid == 0) TraceEvent(Bt, kTraceHeavy, b, seg, t_in, n_walks);
@@ -2663,6 +2697,42 @@ __global__ void __launch_bounds__(256) RecountStructuralKernel(CacheView Cc, Voc
     cs = WarpSum(cs);
     if (lane == 0) Cc.ci_cnt[u * 2 + 1] = cs;
   }
+}
+
+// Context-table snapshots (capi.cu gm_engine_snapshot_*): a slot's rows —
+// key row, cd_cnt, ci_cnt, ci, cdb — packed into one block of `blk` words per
+// listed slot (gather) or unpacked from it (scatter).  One CTA per slot.
+__global__ void SnapshotRowsKernel(CacheView c, int W, int nseg, const int32_t* __restrict__ ids, int n,
+                                   uint32_t* __restrict__ blocks, int scatter) {
+  const int r = static_cast<int>(blockIdx.x);
+  if (r >= n) return;
+  const long long slot = ids[r];
+  const long long blk = kMaxContext + 3LL * nseg + 2LL * W;
+  uint32_t* out = blocks + r * blk;
+  struct Part {
+    uint32_t* base;
+    long long len;
+  } parts[5] = {{reinterpret_cast<uint32_t*>(c.slot_keys) + slot * kMaxContext, kMaxContext},
+                {reinterpret_cast<uint32_t*>(c.cd_cnt) + slot * nseg, nseg},
+                {reinterpret_cast<uint32_t*>(c.ci_cnt) + slot * 2 * nseg, 2LL * nseg},
+                {c.ci + slot * W, W},
+                {c.cdb + slot * W, W}};
+  long long off = 0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    for (long long i = threadIdx.x; i < parts[k].len; i += blockDim.x) {
+      if (scatter) parts[k].base[i] = out[off + i];
+      else out[off + i] = parts[k].base[i];
+    }
+    off += parts[k].len;
+  }
+}
+
+cudaError_t LaunchSnapshotRows(const CacheView& c, int W, int nseg, const int32_t* ids, int n, uint32_t* blocks,
+                               bool scatter, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  SnapshotRowsKernel<<<n, 256, 0, s>>>(c, W, nseg, ids, n, blocks, scatter ? 1 : 0);
+  return cudaGetLastError();
 }
 
 cudaError_t LaunchRecountStructural(const CacheView& c, const VocabView& v) {

@@ -83,6 +83,9 @@ struct CacheView {
   uint32_t* cdb;                  // C*W
   int32_t* cd_cnt;                // C*nseg
   int32_t* seg_done;              // C*nseg completed build units (kChunksPerSeg = built)
+  int32_t* seg_claim;             // C*nseg build chunks claimed (queue units and helpers draw from it,
+                                  //    so each chunk of a shared slot is built exactly once by whoever
+                                  //    gets there first — a batch never waits on another batch's queue)
   int32_t* slot_built;            // C completed build units over all segments
   uint32_t* cd_segmask;           // C: bit s set when segment s has context-dependent tokens
   int32_t* ci_cnt;                // C*nseg*2: per segment, CI tokens (EOS excluded) and CI ∩ structural
@@ -204,6 +207,9 @@ cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s);
 cudaError_t LaunchAllowed(const AutView& a, const BatchView& b, uint32_t* out, cudaStream_t s);
 cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s);
 cudaError_t LaunchRecountStructural(const CacheView& c, const VocabView& v);
+// Snapshot rows of n listed slots <-> blocks of kMaxContext + 3*nseg + 2*W words.
+cudaError_t LaunchSnapshotRows(const CacheView& c, int W, int nseg, const int32_t* ids, int n, uint32_t* blocks,
+                               bool scatter, cudaStream_t s);
 cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b, int queue,
                         cudaStream_t s);
 // Help-build + fill (+ bf16 -inf masking or greedy argmax) (+ fused tail).

@@ -35,7 +35,7 @@ def bench_engine(config):
     vocab = pk.synth_vocab(a.vocab, a.flavor)
     eng = pk.DeviceEngine(pk.Automaton.load(flat), vocab, context_depth=a.context_depth,
                           context_slots=a.context_slots, parent_depth=a.parent_depth)
-    eng.prewarm(a.prewarm_batch, a.prewarm_steps, seed=0xC0FFEE)  # bench.py's rank-0 prewarm
+    eng.prewarm(a.prewarm_batch, a.prewarm_steps, seed=0xC0FFEE, stack_capacity=a.stack_cap)  # bench.py's rank-0 prewarm
     return a, flat, vocab, eng
 
 
