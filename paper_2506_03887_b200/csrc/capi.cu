@@ -637,7 +637,7 @@ int gm_batch_check(gm_batch* b, void* stream) {
     Check(cudaMemcpy(&err, b->view.err, 4, cudaMemcpyDeviceToHost), "check");
     if (err) {
       Check(cudaMemset(b->view.err, 0, 4), "memset");
-      return Fail(GM_ERR_STACK_OVERFLOW, "a mask walk pushed more than 1,024 entries above the stack (walk overlay)");
+      return Fail(GM_ERR_STACK_OVERFLOW, "a mask walk pushed more than 256 entries above the stack (walk overlay)");
     }
     return GM_OK;
   });

@@ -26,6 +26,12 @@
 #ifndef PRE3_FILL_MIN_BLOCKS
 #define PRE3_FILL_MIN_BLOCKS 4  // fill CTAs resident per SM (64 registers)
 #endif
+#ifndef PRE3_COMPACT_GREEDY
+#define PRE3_COMPACT_GREEDY 0  // greedy light pass: allowed chunks in one round trip, packed 16-bit keys
+#endif
+#ifndef PRE3_COMPACT_MIXED
+#define PRE3_COMPACT_MIXED 0  // light pass: all mixed chunks of a segment copied in one round trip
+#endif
 #ifndef PRE3_BULK_MASKED
 #define PRE3_BULK_MASKED 1  // fully masked spans as one bulk (TMA) store
 #endif
@@ -208,7 +214,6 @@ __device__ __forceinline__ int IndexedFindEdge(const int16_t* hlens,
   return best;
 }
 
-template <int kOverlay>
 __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* rec_begin, const CandRec* recs,
                                           const int32_t* rec_cond, const int32_t* rec_push, const int32_t* shift,
                                           const int4* tok_rec, const uint8_t* tok_bytes, int32_t V, int32_t t,
@@ -224,9 +229,8 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
     const int32_t* rec_push;
     const int32_t* shift;
   } A{first, rec_begin, recs, rec_cond, rec_push, shift};
-  int32_t loc[kOverlay];
+  int32_t loc[kWalkOverlay];
   int nl = 0;
-  const int nb0 = nb;  // the walk pops base entries (nb shrinks); a retry starts over
   const bool eos = t == V;
   const int4 tr = __ldg(tok_rec + t);  // offset, length, first 8 bytes: one round trip
   const int nterm = tr.y;
@@ -303,16 +307,11 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
       nb -= k - nl;
       nl = 0;
     }
-    if (nl + fr.push_len + 1 > kOverlay) {
-      // Retry policy: see WalkToken.
-      if constexpr (kOverlay < kDeepOverlay) {
-        if (!complete) return kUnknown;
-        return WalkTokenImpl<kDeepOverlay>(first, rec_begin, recs, rec_cond, rec_push, shift, tok_rec, tok_bytes, V,
-                                           t, base, nb0, complete, hmeta, hlens, hexact, emask, hprefix, pmask);
-      } else {
-        return kOverflow;
-      }
-    }
+    // Past the overlay: on a partial key (a shared context slot) the token
+    // is context-dependent — the cached row must not reject it for good; each
+    // fill then walks it on the sequence's whole stack, where overflowing
+    // the overlay again is an error (kOverflow: the caller raises Bt.err).
+    if (nl + fr.push_len + 1 > kWalkOverlay) return complete ? kOverflow : kUnknown;
     for (int j = 0; j < fr.push_len; ++j) loc[nl++] = j < 4 ? Lane4(fr.p, j) : __ldg(A.rec_push + fr.push_off + j);
     if (fr.new_state < 0) {
       const int top = nl > 0 ? loc[nl - 1] : (nb > 0 ? base[nb - 1] : -1);
@@ -327,15 +326,9 @@ __device__ __noinline__ int WalkTokenImpl(const CandRec* first, const int32_t* r
   return kAccept;
 }
 
-// A walk whose pushes pass the 64-entry overlay is retried with a 1,024-entry
-// one (local memory; long BPE tokens that open many nested values).  On a
-// partial key (a shared context slot) an overflowing token is context-
-// dependent instead: the cached row must not reject it for good — each fill
-// then walks it on the sequence's whole stack.  Only a walk that overflows
-// the deep overlay too returns kOverflow (the caller raises Bt.err).
 __device__ __forceinline__ int WalkToken(const AutView& A, const VocabView& Vv, int32_t t, const int32_t* base, int nb,
                                          bool complete) {
-  return WalkTokenImpl<kWalkOverlay>(A.first, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_rec,
+  return WalkTokenImpl(A.first, A.rec_begin, A.recs, A.rec_cond, A.rec_push, A.shift, Vv.tok_rec,
                                      Vv.tok_bytes, Vv.V, t, base, nb, complete, A.hidx_meta, A.hidx_lens,
                                      A.hidx_exact, A.hidx_exact_mask, A.hidx_prefix, A.hidx_prefix_mask);
 }
@@ -1267,6 +1260,22 @@ __device__ __forceinline__ unsigned long long GreedyKey(uint16_t v, int t) {
   return (static_cast<unsigned long long>(key) << 32) | static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(t));
 }
 
+// 16-bit order keys of the two bf16 logits in w (low half = lower token),
+// 0 for a masked token (bits0/1 of `bits` = the two tokens' mask bits): key =
+// h ^ 0xFFFF for a negative value, h ^ 0x8000 otherwise — the top half of
+// GreedyKey's high word (Key32 restores it), so comparing keys compares
+// values, and every allowed key is > 0 (the key 0x0000 would be a NaN with
+// all payload bits set, 0xFFFF).
+__device__ __forceinline__ uint32_t PairKeys(uint32_t w, uint32_t bits) {
+  const uint32_t neg = ((w >> 15) & 0x00010001u) * 0x7FFFu;
+  const uint32_t key = w ^ (0x80008000u | neg);
+  const uint32_t keep = ((bits & 1u) ? 0x0000FFFFu : 0u) | ((bits & 2u) ? 0xFFFF0000u : 0u);
+  return key & keep;
+}
+// GreedyKey's high word from a 16-bit key: (key << 16), low half all ones
+// for a negative value (the complement of its zero low bits).
+__device__ __forceinline__ uint32_t Key32(uint32_t k16) { return (k16 << 16) | ((k16 & 0x8000u) ? 0u : 0xFFFFu); }
+
 // Mask byte of chunk c = 32k + lane of a 1024-token span whose 32 mask words
 // are spread one per lane (`mword`): word c/4, byte c%4.
 __device__ __forceinline__ void SpanBytes(uint32_t mword, int lane, uint32_t byte[4]) {
@@ -1339,6 +1348,12 @@ __device__ __forceinline__ void CpAsync16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void CpAsyncCommit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void CpAsyncWait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void CpAsyncWait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ unsigned LaneMaskLt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
 
 // Bulk (TMA) shared -> global copies: one instruction stores a whole span of
 // -inf from a CTA-shared source, L2 evict-first like the __stcs stores.
@@ -1683,6 +1698,124 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     for (int i = 0; i < kSpans; ++i) {
       if (i < nfull && __ballot_sync(0xffffffffu, m[i] != 0u)) live |= 1u << i;
     }
+#if PRE3_COMPACT_GREEDY
+    // Every 16-B chunk holding an allowed token, packed (span, round, lane)
+    // into the warp's 256-chunk buffer and copied in ONE round trip; then the
+    // max 16-bit order key two tokens at a time (__vmaxu2 over key pairs,
+    // masked tokens key 0), a warp max, and the lowest id holding it.
+    uint4* cbuf = &span_buf[0][0][0];
+    const unsigned lt = LaneMaskLt();
+#pragma unroll 1
+    for (uint32_t todo = live; todo;) {
+      uint32_t batch = 0u;
+      int n = 0;
+#pragma unroll 1
+      for (uint32_t t = todo; t; t &= t - 1) {
+        const int i = __ffs(t) - 1;
+        uint32_t byte[4];
+        SpanBytes(Pick(m, i), lane, byte);
+        unsigned bal[4];
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          bal[k] = __ballot_sync(0xffffffffu, byte[k] != 0u);
+          cnt += __popc(bal[k]);
+        }
+        if (n + cnt > 256) break;  // a span holds <= 128 chunks: a batch takes >= 1 span
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if ((bal[k] >> lane) & 1u) CpAsync16(&cbuf[n + __popc(bal[k] & lt)], row + t0 + 1024 * i + (32 * k + lane) * 8);
+          n += __popc(bal[k]);
+        }
+        batch |= 1u << i;
+      }
+      CpAsyncCommit();
+      CpAsyncWait0();
+      // Pass 1: this lane's max key over its chunks of the batch.
+      uint32_t acc = 0u;
+      n = 0;
+#pragma unroll 1
+      for (uint32_t t = batch; t; t &= t - 1) {
+        const int i = __ffs(t) - 1;
+        uint32_t byte[4];
+        SpanBytes(Pick(m, i), lane, byte);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const unsigned bal = __ballot_sync(0xffffffffu, byte[k] != 0u);
+          if (byte[k] != 0u) {
+            const uint4 v = cbuf[n + __popc(bal & lt)];
+            const uint32_t* pv = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              acc = __vmaxu2(acc, PairKeys(pv[j], byte[k] >> (2 * j)));
+            }
+            rd += 16;
+          }
+          n += __popc(bal);
+        }
+      }
+      const uint32_t lmax = max(acc & 0xffffu, acc >> 16);
+      const uint32_t kmax = __reduce_max_sync(0xffffffffu, lmax);
+      // Pass 2 (lanes holding kmax): the lowest token id with that key.
+      uint32_t tmin = 0xffffffffu;
+      if (kmax != 0u) {
+        n = 0;
+#pragma unroll 1
+        for (uint32_t t = batch; t; t &= t - 1) {
+          const int i = __ffs(t) - 1;
+          uint32_t byte[4];
+          SpanBytes(Pick(m, i), lane, byte);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const unsigned bal = __ballot_sync(0xffffffffu, byte[k] != 0u);
+            if (lmax == kmax && byte[k] != 0u && tmin == 0xffffffffu) {
+              const uint4 v = cbuf[n + __popc(bal & lt)];
+              const uint32_t* pv = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t kk = PairKeys(pv[j], byte[k] >> (2 * j));
+                const uint32_t tb = static_cast<uint32_t>(t0 + 1024 * i + (32 * k + lane) * 8 + 2 * j);
+                if (tmin == 0xffffffffu && (kk & 0xffffu) == kmax) tmin = tb;
+                if (tmin == 0xffffffffu && (kk >> 16) == kmax) tmin = tb + 1;
+              }
+            }
+            n += __popc(bal);
+          }
+        }
+        tmin = __reduce_min_sync(0xffffffffu, tmin);
+        const unsigned long long p = (static_cast<unsigned long long>(Key32(kmax)) << 32) |
+                                     static_cast<unsigned long long>(0xFFFFFFFFu - tmin);
+        mine = p > mine ? p : mine;
+      } else if (n > 0) {
+        // Only 0xFFFF NaNs allowed (their key is 0, like a masked token's):
+        // the exact 64-bit keys, token by token.
+        n = 0;
+#pragma unroll 1
+        for (uint32_t t = batch; t; t &= t - 1) {
+          const int i = __ffs(t) - 1;
+          uint32_t byte[4];
+          SpanBytes(Pick(m, i), lane, byte);
+#pragma unroll 1
+          for (int k = 0; k < 4; ++k) {
+            const unsigned bal = __ballot_sync(0xffffffffu, byte[k] != 0u);
+            if (byte[k] != 0u) {
+              const uint4 v = cbuf[n + __popc(bal & lt)];
+              const uint16_t* ph = reinterpret_cast<const uint16_t*>(&v);
+              for (int j = 0; j < 8; ++j) {
+                if ((byte[k] >> j) & 1u) {
+                  const unsigned long long p = GreedyKey(ph[j], t0 + 1024 * i + (32 * k + lane) * 8 + j);
+                  mine = p > mine ? p : mine;
+                }
+              }
+            }
+            n += __popc(bal);
+          }
+        }
+      }
+      todo &= ~batch;
+      __syncwarp();  // the buffer is refilled by the next batch
+    }
+#else
     uint4(*buf)[4][32] = span_buf;
     uint32_t pend = live;
 #pragma unroll
@@ -1708,6 +1841,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       }
       CpAsyncCommit();
     }
+#endif
 #pragma unroll 1
     for (int i = nfull; i < kSpans; ++i) {
       const int tw = t0 + 1024 * i;
@@ -1766,6 +1900,76 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       BulkCommit();
       wr += 2048ull * static_cast<unsigned>(__popc(masked));
     }
+#if PRE3_COMPACT_MIXED
+    // Mixed chunks of as many mixed spans as fit the warp's 256-chunk buffer,
+    // packed in (span, round, lane) order, are all copied in ONE round trip
+    // (cp.async: no registers held), then blended and stored span by span; a
+    // segment with more mixed chunks takes another batch.  Each lane reads
+    // back only the chunks it copied itself.
+    uint4* cbuf = &span_buf[0][0][0];  // 2 * 4 * 32 = 256 chunks
+    const unsigned lt = LaneMaskLt();
+#pragma unroll 1
+    for (uint32_t todo = mixed; todo;) {
+      uint32_t batch = 0u;
+      int n = 0;
+#pragma unroll 1
+      for (uint32_t t = todo; t; t &= t - 1) {
+        const int i = __ffs(t) - 1;
+        uint32_t byte[4];
+        SpanBytes(Pick(m, i), lane, byte);
+        unsigned bal[4];
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          bal[k] = __ballot_sync(0xffffffffu, byte[k] != 0u && byte[k] != 0xffu);
+          cnt += __popc(bal[k]);
+        }
+        if (n + cnt > 256) break;  // a span holds <= 128 mixed chunks: a batch takes >= 1 span
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if ((bal[k] >> lane) & 1u) CpAsync16(&cbuf[n + __popc(bal[k] & lt)], row + t0 + 1024 * i + (32 * k + lane) * 8);
+          n += __popc(bal[k]);
+        }
+        batch |= 1u << i;
+      }
+      CpAsyncCommit();
+      CpAsyncWait0();
+      n = 0;
+#pragma unroll 1
+      for (uint32_t t = batch; t; t &= t - 1) {
+        const int i = __ffs(t) - 1;
+        const int tw = t0 + 1024 * i;
+        uint32_t byte[4];
+        SpanBytes(Pick(m, i), lane, byte);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool mix = byte[k] != 0u && byte[k] != 0xffu;
+          const unsigned bal = __ballot_sync(0xffffffffu, mix);
+          if (byte[k] != 0xffu) {
+            uint4 o = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+            if (mix) {
+              const uint32_t x = byte[k];
+              const uint4 v = cbuf[n + __popc(bal & lt)];
+              uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+              const uint32_t* pv = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t keep =
+                    ((x >> (2 * j)) & 1u ? 0x0000FFFFu : 0u) | ((x >> (2 * j + 1)) & 1u ? 0xFFFF0000u : 0u);
+                po[j] = (pv[j] & keep) | (0xFF80FF80u & ~keep);
+              }
+              rd += 16;
+            }
+            __stcs(reinterpret_cast<uint4*>(row + tw + (32 * k + lane) * 8), o);
+            wr += 16;
+          }
+          n += __popc(bal);
+        }
+      }
+      todo &= ~batch;
+      __syncwarp();  // the buffer is refilled by the next batch
+    }
+#else
     uint4(*buf)[4][32] = span_buf;  // [2][4][32] of this warp
     uint32_t pend = mixed;
 #pragma unroll
@@ -1790,6 +1994,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       }
       CpAsyncCommit();
     }
+#endif
 #pragma unroll 1
     for (int i = nfull; i < kSpans; ++i) {
       if (t0 + 1024 * i < tl1) MaskSpan(row, t0 + 1024 * i, tl1, F.vec_ok, Pick(m, i), lane, &rd, &wr);

@@ -15,8 +15,7 @@ constexpr int kSegWords = 256;                        // mask words per vocab se
 constexpr int kSegTokens = kSegWords * 32;            // 8192 tokens per segment
 constexpr int kChunksPerSeg = kSegTokens / kThreads;  // build work units per segment
 constexpr int kMaxContext = 32;                       // max K (one warp lane per key entry)
-constexpr int kWalkOverlay = 64;                      // per-thread pushed-entry overlay in a mask walk
-constexpr int kDeepOverlay = 1024;                    // the retry overlay of a walk that overflowed kWalkOverlay
+constexpr int kWalkOverlay = 256;                     // per-thread pushed-entry overlay in a mask walk
 constexpr int kSlotWait = 1 << 30;                    // seq_slot flag: wait for the slot's build
 // Fill numbers (heavy-list tags, double-buffer parity) count modulo 6: a tag
 // only has to tell a fill from its neighbours, and a period dividing the

@@ -6,9 +6,10 @@
   options are refused, altered or truncated data is rejected;
 * builds queued by a batch that stops stepping are built by whichever batch
   needs them (no fill gives up waiting and walks a whole segment);
-* tokens whose walk pushes past the 64-entry overlay are never cached as
-  rejects: a shared slot marks them context-dependent and the full-stack walk
-  retries with the 1,024-entry overlay — masks equal the port's.
+* tokens whose walk pushes up to the 256-entry walk overlay (60 opening
+  brackets) give the port's masks; past it, a shared slot marks the token
+  context-dependent (never a cached reject) and the full-stack walk raises
+  GM_ERR_STACK_OVERFLOW — loudly, not a wrong mask.
 """
 import os
 
@@ -128,14 +129,14 @@ def test_builds_queued_by_an_idle_batch_are_built_by_others(vocab):
 
 def deep_vocab(base, n):
     """The JSON test vocabulary plus tokens of n opening brackets (each '['
-    pushes several entries: n = 40 passes the 64-entry walk overlay)."""
+    pushes 2 entries: n = 60 passes the old 64-entry walk overlay)."""
     extra = [b"[" * k for k in range(2, n + 1)] + [b"[" * k + b"1" for k in (n // 2, n)]
     return [t for t in base if t not in set(extra)] + extra
 
 
 @pytest.mark.parametrize("K", [4, 12])
 def test_long_pushing_tokens_match_the_port(vocab, K):
-    voc = deep_vocab(vocab[:8000], 40)
+    voc = deep_vocab(vocab[:8000], 60)
     eng = engine(voc, K=K, slots=1024)
     B, steps, seed = 32, 20, 5
     batch, hashes, toks = split_loop(eng, B, steps, seed)
@@ -144,7 +145,16 @@ def test_long_pushing_tokens_match_the_port(vocab, K):
     # the long tokens were allowed on the way (the mask really exercised them)
     port = Port(flat("json"), voc)
     m = port.mask(port.initial())
-    t40 = voc.index(b"[" * 40)
+    t40 = voc.index(b"[" * 60)
     assert (int(m[t40 >> 5]) >> (t40 & 31)) & 1
     dev = eng.ComputeMask(eng.InitialConfig())
     assert np.array_equal(dev, m)
+
+
+def test_walk_past_the_overlay_fails_loudly(vocab):
+    """A token pushing more than 256 entries (400 '[') cannot be walked: the
+    fill raises GM_ERR_STACK_OVERFLOW instead of returning a wrong mask."""
+    voc = vocab[:2000] + [b"[" * 400]
+    eng = engine(voc, K=4, slots=256)
+    with pytest.raises(pk.StackOverflowError):
+        eng.ComputeMask(eng.InitialConfig())

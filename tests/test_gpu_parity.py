@@ -286,6 +286,43 @@ def test_greedy_decode_matches_port():
             assert batch.get(b).stack == port.get(cfgs[b])[2]
 
 
+@pytest.mark.parametrize("kind", ["zeros", "few_values", "specials"])
+def test_greedy_ties_and_special_values(kind):
+    """The packed 16-bit-key argmax (PairKeys): all-equal rows (lowest
+    allowed id wins), few distinct values, and rows holding +-inf, -0.0 and
+    NaNs (0xFFFF keys like a masked token) — equal to the port's 32-bit keys."""
+    vocab = pk.synth_vocab(40000)
+    f = flat("json")
+    eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=8)
+    port = Port(f, vocab)
+    B = 24
+    batch = eng.batch(B)
+    cfgs = [port.initial() for _ in range(B)]
+    rng = np.random.default_rng({"zeros": 1, "few_values": 2, "specials": 3}[kind])
+    toks = torch.zeros(B, dtype=torch.int32, device=DEV)
+    for s in range(10):
+        if kind == "zeros":
+            host = np.zeros((B, eng.V + 1), np.uint16)
+        elif kind == "few_values":
+            host = rng.choice(np.array([0xBF80, 0x0000, 0x3F80, 0x4000], np.uint16), size=(B, eng.V + 1))
+        else:
+            host = rng.choice(np.array([0xFFFF, 0x7FC0, 0x7F80, 0xFF80, 0x8000, 0x0000, 0xC000], np.uint16),
+                              size=(B, eng.V + 1), p=[0.3, 0.1, 0.02, 0.2, 0.18, 0.1, 0.1])
+            host[: B // 3] = 0xFFFF  # rows of NaN 0xFFFF only
+        lg = torch.from_numpy(host.view(np.int16)).to(DEV).view(torch.bfloat16)
+        batch.decode_step_greedy(lg, toks)
+        batch.check()
+        tk = toks.cpu().numpy()
+        for b in range(B):
+            t = port.greedy_pick(port.mask(cfgs[b]), np.ascontiguousarray(host[b]))
+            assert t == tk[b], (kind, s, b)
+            if t >= 0:
+                port.accept_token(cfgs[b], t)
+            if t < 0 or cfgs[b].status != 0:
+                port.free(cfgs[b])
+                cfgs[b] = port.initial()
+
+
 def test_stack_overflow_status():
     """A stack beyond the batch capacity yields GM_OVERFLOW, never a write
     past the end."""
