@@ -95,6 +95,9 @@ def parse(argv=None):
     p.add_argument("--latency-samples", type=int, default=64,
                    help="steps of the latency sub-loop (events between steps: per-step latency p50/p99)")
     p.add_argument("--cold-steps", type=int, default=100, help="steps timed from an empty context table")
+    p.add_argument("--no-snapshot", action="store_true",
+                   help="time on the prewarmed engine itself (default: save its context table and run on a fresh "
+                        "engine loaded from the snapshot)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
@@ -464,6 +467,30 @@ def main(argv=None):
         eng.prewarm(args.prewarm_batch, args.prewarm_steps, seed=0xC0FFEE + rank, stack_capacity=args.stack_cap)
     t_pre = time.perf_counter() - t_pre
     pre_info = eng.info()
+    # The prewarmed context table as a snapshot file (gm_engine_snapshot_*,
+    # "P3GMCTX1"): saved, then loaded into a fresh engine that runs everything
+    # below — the load a restarted server (or every rank of a node) does
+    # instead of the prewarm; the timed digests check the loaded table.
+    snap = None
+    if args.prewarm_steps > 0 and not args.no_snapshot:
+        import tempfile
+        path = os.path.join(tempfile.gettempdir(), f"pre3_contexts_rank{rank}.p3gmctx")
+        t0 = time.perf_counter()
+        nbytes = eng.save_contexts(path)
+        t_save = time.perf_counter() - t0
+        del eng
+        t0 = time.perf_counter()
+        eng = pk.DeviceEngine(automaton, vocab, device=local, context_depth=args.context_depth,
+                              context_slots=args.context_slots, parent_depth=args.parent_depth)
+        t_create = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        eng.load_contexts(path)
+        torch.cuda.synchronize()
+        t_load = time.perf_counter() - t0
+        os.unlink(path)
+        snap = {"bytes": int(nbytes), "contexts": eng.info()["context_slots_used"], "save_s": t_save,
+                "engine_create_s": t_create, "load_s": t_load,
+                "note": "the timed engine was created fresh and loaded from the prewarmed engine's snapshot"}
 
     batch = eng.batch(B, args.stack_cap)
     K, Wm = args.steps, args.warmup
@@ -705,7 +732,7 @@ def main(argv=None):
                    if Kg else "eager, one ABI call per step"),
         "clocks": clocks.summary(),
         "cold_cache": cold,
-        "preprocessing": {"compile_s": t_comp, "prewarm_s": t_pre,
+        "preprocessing": {"compile_s": t_comp, "prewarm_s": t_pre, "snapshot": snap,
                           "prewarm": f"{args.prewarm_steps} steps x {args.prewarm_batch} seqs "
                           f"(seed differs from the timed streams)",
                           "contexts_after_prewarm": pre_info["context_slots_used"],

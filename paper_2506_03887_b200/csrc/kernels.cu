@@ -26,6 +26,15 @@
 #ifndef PRE3_FILL_MIN_BLOCKS
 #define PRE3_FILL_MIN_BLOCKS 4  // fill CTAs resident per SM (64 registers)
 #endif
+#ifndef PRE3_BULK_SPANS
+#define PRE3_BULK_SPANS 0xFF  // span positions whose fully masked spans go to the TMA engine (the rest: LSU stores)
+#endif
+#ifndef PRE3_BULK_RUN
+#define PRE3_BULK_RUN 1  // masked spans per bulk store (a run of adjacent ones: one TMA op)
+#endif
+#ifndef PRE3_BULK_EVICT_FIRST
+#define PRE3_BULK_EVICT_FIRST 1  // -inf bulk stores with an L2 evict-first hint
+#endif
 #ifndef PRE3_COMPACT_GREEDY
 #define PRE3_COMPACT_GREEDY 0  // greedy light pass: allowed chunks in one round trip, packed 16-bit keys
 #endif
@@ -1364,9 +1373,15 @@ __device__ __forceinline__ unsigned long long EvictFirstPolicy() {
 }
 __device__ __forceinline__ void BulkStore(void* gmem, const void* smem, int bytes, unsigned long long policy) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+#if PRE3_BULK_EVICT_FIRST
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(gmem),
                "r"(sa), "r"(bytes), "l"(policy)
                : "memory");
+#else
+  (void)policy;
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gmem), "r"(sa), "r"(bytes)
+               : "memory");
+#endif
 }
 __device__ __forceinline__ void BulkCommit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void BulkWaitRead() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
@@ -1671,6 +1686,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       F.seg_counts[(static_cast<long long>(b) * Vv.nseg + seg) * 2 + 1] = cs;
     }
   }
+  if (Bt.trace && lane == 0) TraceEvent(Bt, 14, b, seg, t_in, 0);  // l:head (slot, CI loads, bitmask, counts)
   // ---- model logit layout: the EOS bit where this item needs it (the last
   // segment holds bit V; an EOS column among the regular ids is patched into
   // this item's words for the logits pass below — bitmask rows keep the
@@ -1890,13 +1906,24 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       const unsigned nz = __ballot_sync(0xffffffffu, m[i] != 0u);
       const unsigned nf = __ballot_sync(0xffffffffu, m[i] != 0xffffffffu);
       if (i < nfull) {
-        if (!nz && PRE3_BULK_MASKED) masked |= 1u << i;
-        else if (nf) mixed |= 1u << i;
+        if (!nz && PRE3_BULK_MASKED && ((PRE3_BULK_SPANS >> i) & 1)) masked |= 1u << i;
+        else if (nf) mixed |= 1u << i;  // (a masked span left to the LSU path: -inf chunk stores)
       }
     }
     if (masked && lane == 0) {
       const unsigned long long pol = EvictFirstPolicy();
+#if PRE3_BULK_RUN > 1
+      // Runs of adjacent masked spans as one bulk store (up to PRE3_BULK_RUN spans).
+      for (uint32_t x = masked; x;) {
+        const int i = __ffs(x) - 1;
+        int len = 1;
+        while (len < PRE3_BULK_RUN && ((x >> (i + len)) & 1u)) ++len;
+        BulkStore(row + t0 + 1024 * i, ninf, 2048 * len, pol);
+        x &= ~(((1u << len) - 1u) << i);
+      }
+#else
       for (uint32_t x = masked; x; x &= x - 1) BulkStore(row + t0 + 1024 * (__ffs(x) - 1), ninf, 2048, pol);
+#endif
       BulkCommit();
       wr += 2048ull * static_cast<unsigned>(__popc(masked));
     }
@@ -1970,6 +1997,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       __syncwarp();  // the buffer is refilled by the next batch
     }
 #else
+    const unsigned long long t_mx = Bt.trace ? NowNs() : 0ull;
     uint4(*buf)[4][32] = span_buf;  // [2][4][32] of this warp
     uint32_t pend = mixed;
 #pragma unroll
@@ -2000,7 +2028,12 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       if (t0 + 1024 * i < tl1) MaskSpan(row, t0 + 1024 * i, tl1, F.vec_ok, Pick(m, i), lane, &rd, &wr);
     }
     if (Vv.layout && last_seg) TailColumns(Vv, row, eos_bit, lane, 32, &wr);
+    const unsigned long long t_bw = Bt.trace ? NowNs() : 0ull;
     if (masked && lane == 0) BulkWaitRead();  // the -inf source outlives the reads
+    if (Bt.trace && lane == 0) {
+      TraceEvent(Bt, 15, b, seg, t_mx, static_cast<unsigned long long>(__popc(mixed)));  // l:mixed spans
+      TraceEvent(Bt, 16, b, seg, t_bw, static_cast<unsigned long long>(__popc(masked)));  // l:bulk wait
+    }
   }
   if (Bt.stats_enabled) {
     rd = static_cast<unsigned long long>(WarpSum(static_cast<int>(rd)));
@@ -2056,7 +2089,7 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
   PdlEnter();
   __shared__ FillShared sh;
   __shared__ uint4 span_buf[kWarps][2][4][32];  // light pass: per-warp double buffer of mixed chunks (32 KB)
-  __shared__ __align__(128) uint4 ninf_buf[128];  // 2 KB of bf16 -inf: the bulk-store source
+  __shared__ __align__(128) uint4 ninf_buf[128 * PRE3_BULK_RUN];  // bf16 -inf: the bulk-store source
   extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -2077,8 +2110,10 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
   if (bid >= Bt.h_grid) {
     // ---- light pass.  Loads that only depend on (b, seg) are issued together.
     if (MODE == kFillMask && F.logits != nullptr) {
-      if (tid < 128) {
-        ninf_buf[tid] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+      for (int i = tid; i < 128 * PRE3_BULK_RUN; i += kThreads) {
+        ninf_buf[i] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+      }
+      {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // visible to the bulk copies
       }
       __syncthreads();

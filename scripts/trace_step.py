@@ -64,7 +64,7 @@ torch.cuda.synchronize()
 cap = 1 << 20
 tr = torch.zeros(4 * (cap + 1), dtype=torch.int64, device=dev)
 names = {1: "light", 2: "heavy", 3: "tail", 4: "accept", 5: "build", 10: "h:build", 11: "h:wait", 12: "h:cdscan", 13: "h:walks",
-         20: "a:step", 21: "a:lookup", 22: "a:publish"}
+         20: "a:step", 21: "a:lookup", 22: "a:publish", 14: "l:head", 15: "l:mixed", 16: "l:bwait"}
 for s in range(a.steps):
     tr.zero_()
     batch.set_trace(tr)
