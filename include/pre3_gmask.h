@@ -102,7 +102,8 @@ int gm_automaton_compile_stats(const gm_automaton* a, int64_t stats[4]);
 /* ------------------------------------------------------------ engine */
 typedef struct gm_engine_options {
   int32_t context_depth;   /* K: stack entries keying the context cache (1..32; default 8) */
-  int32_t context_slots;   /* hash-table capacity, power of two (default 8192) */
+  int32_t context_slots;   /* context rows (the cache's capacity), power of two (default 8192); the
+                              row index has 2x as many positions */
   int64_t parent_depth;    /* R < K: a new context is built from the context of the same stack
                               top keyed R deep, walking only that context's context-dependent
                               tokens (0 = default min(4, K-1); negative = off) */
@@ -114,6 +115,13 @@ typedef struct gm_engine_options {
   const uint32_t* disabled; /* host bitmask (W words) of token ids < V that are never allowed (model
                                specials or alias ids among the regular ids; their bytes are ignored
                                and may be empty), or NULL */
+  /* Context eviction (CLOCK): when fewer than auto_evict_free rows are free
+   * at the start of a batch's fill, rows not referenced since the previous
+   * eviction — and not read by any batch's next fill or a pending build —
+   * are freed for reuse (gm_engine_evict, run on that batch's stream; the
+   * engine's other batches must be idle then).  0 = off: a full table falls
+   * back to per-sequence private rows (correct, slower). */
+  int32_t auto_evict_free;
 } gm_engine_options;
 
 /* Engine::Engine (runtime.cpp:92-113) + TokenTrie::Build (runtime.cpp:18-61)
@@ -148,6 +156,17 @@ int gm_engine_set_structural(gm_engine* e, const uint32_t* host_words);
  * identical with or without it (the cache only changes speed). */
 int gm_engine_prewarm(gm_engine* e, int32_t batch, int32_t steps, uint64_t seed, int32_t stack_capacity,
                       void* stream);
+
+/* Context eviction now (see gm_engine_options::auto_evict_free): every
+ * batch of the engine must be idle (their streams synchronized, or all
+ * work on `stream`).  Rows never move, so batches, captured graphs and
+ * pending builds stay valid; later fills rebuild any evicted context they
+ * meet.  Results are unchanged (the cache only changes speed). */
+int gm_engine_evict(gm_engine* e, void* stream);
+/* Context-table counters: [0] rows, [1] rows in use, [2] free rows,
+ * [3] index positions, [4] evictions, [5] rows evicted, [6] private-row
+ * builds (table full), [7] segment builds. */
+int gm_engine_cache_stats(gm_engine* e, int64_t out[8]);
 
 /* Context-table snapshot "P3GMCTX1" (the reference's cache
  * precedent: SerializeDpda / DeserializeDpda, src/serialize.cpp:148-294).

@@ -120,6 +120,8 @@ def lib() -> ctypes.CDLL:
             "gm_engine_set_structural": ([P, P], ctypes.c_int),
             "gm_engine_prewarm": ([P, I32, I32, U64, I32, P], ctypes.c_int),
             "gm_engine_snapshot_save": ([P, P, U64, ctypes.POINTER(U64)], ctypes.c_int),
+            "gm_engine_evict": ([P, P], ctypes.c_int),
+            "gm_engine_cache_stats": ([P, P], ctypes.c_int),
             "gm_engine_snapshot_load": ([P, P, U64], ctypes.c_int),
             "gm_batch_create": ([P, I32, I32, PP], ctypes.c_int),
             "gm_batch_destroy": ([P], ctypes.c_int),
@@ -302,7 +304,7 @@ class _EngineOptions(ctypes.Structure):
     _fields_ = [("context_depth", ctypes.c_int32), ("context_slots", ctypes.c_int32),
                 ("parent_depth", ctypes.c_int64), ("segment_words", ctypes.c_int32),
                 ("num_columns", ctypes.c_int32), ("eos_column", ctypes.c_int32),
-                ("disabled", ctypes.c_void_p)]
+                ("disabled", ctypes.c_void_p), ("auto_evict_free", ctypes.c_int32)]
 
 
 @dataclass
@@ -318,7 +320,8 @@ class DeviceEngine:
 
     def __init__(self, automaton: Automaton, tokens: Sequence[bytes], device: int = 0,
                  context_depth: int = 8, context_slots: int = 8192, parent_depth: int = 0,
-                 num_columns: int = 0, eos_column: int = 0, disabled: Optional[Sequence[int]] = None):
+                 num_columns: int = 0, eos_column: int = 0, disabled: Optional[Sequence[int]] = None,
+                 auto_evict_free: int = 0):
         """num_columns / eos_column / disabled: the model's logit layout
         (gm_engine_options; tokenizer.TokenizerVocab.engine_options() fills
         them from a tokenizer.json): logit rows have num_columns columns, EOS
@@ -338,7 +341,7 @@ class DeviceEngine:
             self.disabled_words[i >> 5] |= np.uint32(1 << (i & 31))
         data, offs = pack_vocab(self.tokens)
         opts = _EngineOptions(context_depth, context_slots, parent_depth, 256, num_columns, eos_column,
-                              self.disabled_words.ctypes.data if disabled else None)
+                              self.disabled_words.ctypes.data if disabled else None, auto_evict_free)
         h = ctypes.c_void_p()
         _check(lib().gm_engine_create(automaton._h, _ptr(data), _ptr(offs), self.V, ctypes.byref(opts),
                                       device, ctypes.byref(h)))
@@ -369,6 +372,18 @@ class DeviceEngine:
         """Populates the context cache with synthetic decode streams (preprocessing)
         over sequences of the given stack capacity (overflow restarts them)."""
         _check(lib().gm_engine_prewarm(self._h, batch, steps, seed, stack_capacity, _stream(stream)))
+
+    def evict(self, stream=None) -> None:
+        """gm_engine_evict: frees context rows not referenced since the last
+        eviction (every batch of the engine must be idle)."""
+        _check(lib().gm_engine_evict(self._h, _stream(stream)))
+
+    def cache_stats(self) -> dict:
+        out = np.zeros(8, np.int64)
+        _check(lib().gm_engine_cache_stats(self._h, _ptr(out)))
+        keys = ["rows", "rows_in_use", "rows_free", "index_positions", "evictions", "rows_evicted",
+                "private_builds", "segment_builds"]
+        return dict(zip(keys, (int(x) for x in out)))
 
     def save_contexts(self, path: Optional[str] = None):
         """gm_engine_snapshot_save: the built context table ("P3GMCTX1") into

@@ -105,10 +105,17 @@ struct gm_engine {
   // Snapshot key (gm_engine_snapshot_*): the automaton's grammar hash, a hash
   // of the flattened device layout and one of the vocabulary + logit layout.
   uint64_t grammar_hash = 0, layout_hash = 0, vocab_hash = 0;
+  // Eviction: the engine's batches (their seq_slot rows are kept), the keep
+  // bytes, the host-mapped free-row count and the auto-eviction threshold.
+  std::vector<gm_batch*> batches;
+  uint8_t* evict_keep = nullptr;
+  int32_t* host_free = nullptr;  // cudaHostAlloc(mapped)
+  int32_t auto_evict_free = 0;
   std::vector<void*> owned;
   ~gm_engine() {
     cudaSetDevice(device);
     for (void* p : owned) cudaFree(p);
+    if (host_free) cudaFreeHost(host_free);
   }
 };
 
@@ -176,6 +183,8 @@ struct gm_batch {
   std::vector<void*> owned;
   ~gm_batch() {
     cudaSetDevice(engine->device);
+    auto& bs = engine->batches;
+    bs.erase(std::remove(bs.begin(), bs.end(), this), bs.end());
     if (capture_stream) cudaStreamDestroy(capture_stream);
     // Builds still queued belong to contexts other batches may already use.
     for (int q = 0; q < 3; ++q) pre3::LaunchDrain(engine->aut, engine->vocab, engine->cache, view, q, nullptr);
@@ -183,6 +192,37 @@ struct gm_batch {
     for (void* p : owned) cudaFree(p);
   }
 };
+
+namespace {
+
+// gm_engine_evict's work, on stream s (every batch of the engine idle).
+void Evict(gm_engine* e, cudaStream_t s) {
+  std::vector<const int32_t*> ptrs;
+  std::vector<int> counts;
+  for (gm_batch* b : e->batches) {
+    ptrs.push_back(b->view.seq_slot);
+    counts.push_back(2 * b->view.B);  // both fill parities
+  }
+  Check(pre3::LaunchEvict(e->cache, e->nseg, ptrs.data(), counts.data(), static_cast<int>(ptrs.size()),
+                          e->evict_keep, s),
+        "evict launch");
+}
+
+// Auto-eviction check at the start of a batch's fill (never while the
+// stream is being captured into a graph): the free-row count the device
+// mirrored at its latest pop (or eviction).
+void MaybeEvict(gm_batch* b, cudaStream_t s) {
+  gm_engine* e = b->engine;
+  if (e->auto_evict_free <= 0) return;
+  if (*reinterpret_cast<volatile int32_t*>(e->host_free) >= e->auto_evict_free) return;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  Check(cudaStreamIsCapturing(s, &cap), "capture status");
+  if (cap != cudaStreamCaptureStatusNone) return;
+  *reinterpret_cast<volatile int32_t*>(e->host_free) = e->cache.C;  // until the eviction writes the real count
+  Evict(e, s);
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -301,7 +341,7 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     if (!a || !out || num_tokens < 0 || (num_tokens > 0 && (!tok_bytes || !tok_offsets))) {
       return Fail(GM_ERR_USAGE, "bad argument");
     }
-    gm_engine_options o{8, 8192, 0, pre3::kSegWords, 0, 0, nullptr};
+    gm_engine_options o{8, 8192, 0, pre3::kSegWords, 0, 0, nullptr, 0};
     if (opts) {
       if (opts->context_depth) o.context_depth = opts->context_depth;
       if (opts->context_slots) o.context_slots = opts->context_slots;
@@ -310,7 +350,9 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
       o.num_columns = opts->num_columns;
       o.eos_column = opts->eos_column;
       o.disabled = opts->disabled;
+      o.auto_evict_free = opts->auto_evict_free;
     }
+    if (o.auto_evict_free < 0) return Fail(GM_ERR_USAGE, "auto_evict_free must be >= 0");
     const int32_t W = (num_tokens + 1 + 31) / 32;
     auto is_disabled = [&](int32_t i) { return o.disabled && ((o.disabled[i >> 5] >> (i & 31)) & 1u); };
     if (o.num_columns < 0) return Fail(GM_ERR_USAGE, "num_columns must be >= 0");
@@ -438,8 +480,24 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     const size_t C = static_cast<size_t>(o.context_slots);
     auto& c = e->cache;
     c.C = o.context_slots;
+    c.IC = 2 * o.context_slots;
     c.K = o.context_depth;
-    c.slot_hash = DevAlloc<unsigned long long>(C, &e->owned);
+    c.slot_hash = DevAlloc<unsigned long long>(2 * C, &e->owned);
+    Check(cudaMemset(c.slot_hash, 0, 2 * C * 8), "memset");
+    {
+      std::vector<int32_t> fr(C);
+      for (size_t i = 0; i < C; ++i) fr[i] = static_cast<int32_t>(C - 1 - i);  // pops hand out rows 0, 1, ...
+      c.row_free = DevUpload(fr, &e->owned);
+      const int32_t n = o.context_slots;
+      c.row_free_n = DevUpload(std::vector<int32_t>{n}, &e->owned);
+    }
+    c.row_ref = DevAlloc<uint8_t>(C, &e->owned);
+    Check(cudaMemset(c.row_ref, 0, C), "memset");
+    e->evict_keep = DevAlloc<uint8_t>(C, &e->owned);
+    e->auto_evict_free = o.auto_evict_free;
+    Check(cudaHostAlloc(reinterpret_cast<void**>(&e->host_free), 4, cudaHostAllocMapped), "host alloc");
+    *e->host_free = o.context_slots;
+    Check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.host_free), e->host_free, 0), "mapped pointer");
     c.slot_meta = DevAlloc<int32_t>(C, &e->owned);
     c.slot_keys = DevAlloc<int32_t>(C * static_cast<size_t>(pre3::kMaxContext), &e->owned);
     c.ci = DevAlloc<uint32_t>(C * static_cast<size_t>(e->W), &e->owned);
@@ -458,7 +516,6 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     Check(cudaMemset(c.ci_cnt, 0, C * static_cast<size_t>(e->nseg) * 8), "memset");
     Check(cudaMemset(c.slot_built, 0, C * 4), "memset");
     c.counters = DevAlloc<unsigned long long>(8, &e->owned);
-    Check(cudaMemset(c.slot_hash, 0, C * 8), "memset");
     Check(cudaMemset(c.slot_meta, 0, C * 4), "memset");
     Check(cudaMemset(c.cd_cnt, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
     Check(cudaMemset(c.seg_done, 0, C * static_cast<size_t>(e->nseg) * 4), "memset");
@@ -565,6 +622,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     Check(cudaMemset(b->best, 0, static_cast<size_t>(batch) * 8), "memset");
     Check(pre3::LaunchReset(e->aut, v, nullptr), "reset");
     Check(cudaDeviceSynchronize(), "batch create");
+    e->batches.push_back(b.get());
     *out = b.release();
     return GM_OK;
   });
@@ -702,6 +760,7 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
     if (logits && ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    MaybeEvict(b, s);
     if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
     pre3::FillArgs f{};
     f.bitmask = bitmask;
@@ -733,6 +792,7 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
     if (logits && ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    MaybeEvict(b, s);
     if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
     pre3::FillArgs f{};
     f.bitmask = bitmask ? bitmask : b->scratch_mask;
@@ -767,6 +827,7 @@ int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words
     if (logits && ld < e->vocab.ncols) return Fail(GM_ERR_USAGE, "ld < the row's logit columns");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    MaybeEvict(b, s);
     if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
     pre3::FillArgs f{};
     f.bitmask = bitmask ? bitmask : b->scratch_mask;
@@ -890,6 +951,7 @@ int gm_decode_step_greedy(gm_batch* b, const uint16_t* logits, int64_t ld, uint3
     if (bitmask && ld_words < e->W) return Fail(GM_ERR_USAGE, "ld_words < W");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    MaybeEvict(b, s);
     if (!b->slots_valid) Check(pre3::LaunchLookup(e->cache, b->view, b->prod, b->fill_seq, s), "lookup launch");
     pre3::FillArgs f{};
     f.bitmask = bitmask ? bitmask : b->scratch_mask;
@@ -1084,20 +1146,22 @@ int gm_graph_destroy(gm_graph* g) {
 // ---------------------------------------------------------------- snapshots
 // Context-table snapshot "P3GMCTX1" (the reference's cache
 // precedent is SerializeDpda/DeserializeDpda, src/serialize.cpp:148-294):
-// every fully built context slot, keyed by (grammar hash
+// every fully built context row, keyed by (grammar hash
 // (dpda_builder.cpp:469-476), device-layout hash, vocabulary + logit-layout
-// hash, K, R, C).  Little-endian:
-//   header: magic[8] "P3GMCTX1", u32 version 1, u32 header bytes (96),
+// hash, K, R, rows).  Little-endian:
+//   header: magic[8] "P3GMCTX1", u32 version 2, u32 header bytes (96),
 //           u64 grammar_hash, u64 layout_hash, u64 vocab_hash,
-//           i32 K, R, C, V, W, nseg, n (slots), kMaxContext,
+//           i32 K, R, C (rows), V, W, nseg, n (rows saved), kMaxContext,
 //           u64 payload bytes, u64 payload checksum (Hash64), u64 0 (reserved)
-//   payload: i32 slot[n], i32 meta[n], i32 parent[n], u32 cd_segmask[n],
-//            u64 hash[n], then per slot a block of kMaxContext + 3*nseg + 2*W
-//            words: key row, cd_cnt[nseg], ci_cnt[nseg][2], ci[W], cdb[W].
+//   payload: i32 row[n], i32 meta[n], i32 parent[n], u32 cd_segmask[n], then
+//            per row a block of kMaxContext + 3*nseg + 2*W words: key row,
+//            cd_cnt[nseg], ci_cnt[nseg][2], ci[W], cdb[W].
+// Loading restores the rows at their ids and rebuilds the row index.
 namespace {
 
 constexpr char kSnapMagic[8] = {'P', '3', 'G', 'M', 'C', 'T', 'X', '1'};
 constexpr uint32_t kSnapHeader = 96;
+constexpr uint32_t kSnapVersion = 2;
 
 struct SnapHeader {
   char magic[8];
@@ -1108,23 +1172,20 @@ struct SnapHeader {
 };
 static_assert(sizeof(SnapHeader) == kSnapHeader, "snapshot header layout");
 
-constexpr int kSnapChunk = 1024;  // slots per gather/scatter launch
+constexpr int kSnapChunk = 1024;  // rows per gather/scatter launch
 
-struct SlotTables {
-  std::vector<unsigned long long> hash;
+struct RowTables {
   std::vector<int32_t> meta, built, parent;
   std::vector<uint32_t> segmask;
 };
 
-SlotTables ReadSlotTables(const gm_engine* e) {
+RowTables ReadRowTables(const gm_engine* e) {
   const size_t C = static_cast<size_t>(e->cache.C);
-  SlotTables t;
-  t.hash.resize(C);
+  RowTables t;
   t.meta.resize(C);
   t.built.resize(C);
   t.parent.resize(C);
   t.segmask.resize(C);
-  Check(cudaMemcpy(t.hash.data(), e->cache.slot_hash, C * 8, cudaMemcpyDeviceToHost), "snapshot read");
   Check(cudaMemcpy(t.meta.data(), e->cache.slot_meta, C * 4, cudaMemcpyDeviceToHost), "snapshot read");
   Check(cudaMemcpy(t.built.data(), e->cache.slot_built, C * 4, cudaMemcpyDeviceToHost), "snapshot read");
   Check(cudaMemcpy(t.parent.data(), e->cache.slot_parent, C * 4, cudaMemcpyDeviceToHost), "snapshot read");
@@ -1136,6 +1197,32 @@ size_t SnapBlockWords(const gm_engine* e) {
   return static_cast<size_t>(pre3::kMaxContext) + 3 * static_cast<size_t>(e->nseg) + 2 * static_cast<size_t>(e->W);
 }
 
+// Gathers (scatter = false: device -> host blocks) or scatters the rows'
+// blocks, kSnapChunk rows per launch through a device staging buffer.
+void SnapshotRows(gm_engine* e, const std::vector<int32_t>& ids, uint8_t* host, bool scatter) {
+  const size_t n = ids.size(), blk = SnapBlockWords(e);
+  if (!n) return;
+  std::vector<void*> tmp;
+  try {
+    int32_t* d_ids = DevAlloc<int32_t>(kSnapChunk, &tmp);
+    uint32_t* d_blk = DevAlloc<uint32_t>(kSnapChunk * blk, &tmp);
+    for (size_t k0 = 0; k0 < n; k0 += kSnapChunk) {
+      const int m = static_cast<int>(std::min<size_t>(kSnapChunk, n - k0));
+      const size_t bytes = static_cast<size_t>(m) * blk * 4;
+      Check(cudaMemcpy(d_ids, ids.data() + k0, static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice), "snapshot");
+      if (scatter) Check(cudaMemcpy(d_blk, host, bytes, cudaMemcpyHostToDevice), "snapshot");
+      Check(pre3::LaunchSnapshotRows(e->cache, e->W, e->nseg, d_ids, m, d_blk, scatter, nullptr), "snapshot rows");
+      if (!scatter) Check(cudaMemcpy(host, d_blk, bytes, cudaMemcpyDeviceToHost), "snapshot");
+      Check(cudaDeviceSynchronize(), "snapshot rows");
+      host += bytes;
+    }
+  } catch (...) {
+    for (void* q : tmp) cudaFree(q);
+    throw;
+  }
+  for (void* q : tmp) cudaFree(q);
+}
+
 }  // namespace
 
 int gm_engine_snapshot_save(gm_engine* e, void* buf, uint64_t cap, uint64_t* size) {
@@ -1143,17 +1230,14 @@ int gm_engine_snapshot_save(gm_engine* e, void* buf, uint64_t cap, uint64_t* siz
     if (!e || !size) return Fail(GM_ERR_USAGE, "null argument");
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     Check(cudaDeviceSynchronize(), "snapshot: work in flight");
-    const SlotTables t = ReadSlotTables(e);
+    const RowTables t = ReadRowTables(e);
     const int32_t full = e->nseg * pre3::kChunksPerSeg;
     std::vector<int32_t> ids;
     for (int32_t i = 0; i < e->cache.C; ++i) {
-      if (t.hash[static_cast<size_t>(i)] != 0ull && (t.meta[static_cast<size_t>(i)] & (1 << 16)) &&
-          t.built[static_cast<size_t>(i)] == full) {
-        ids.push_back(i);
-      }
+      if ((t.meta[static_cast<size_t>(i)] & (1 << 16)) && t.built[static_cast<size_t>(i)] == full) ids.push_back(i);
     }
     const size_t n = ids.size(), blk = SnapBlockWords(e);
-    const uint64_t payload = n * (4 * 4 + 8) + n * blk * 4;
+    const uint64_t payload = n * 16 + n * blk * 4;
     *size = kSnapHeader + payload;
     if (!buf) return GM_OK;
     if (cap < *size) return Fail(GM_ERR_USAGE, "buffer too small");
@@ -1165,41 +1249,21 @@ int gm_engine_snapshot_save(gm_engine* e, void* buf, uint64_t cap, uint64_t* siz
     };
     std::vector<int32_t> meta(n), parent(n);
     std::vector<uint32_t> segmask(n);
-    std::vector<unsigned long long> hash(n);
     std::unordered_set<int32_t> saved(ids.begin(), ids.end());
     for (size_t k = 0; k < n; ++k) {
       const size_t i = static_cast<size_t>(ids[k]);
       meta[k] = t.meta[i];
       parent[k] = saved.count(t.parent[i]) ? t.parent[i] : -1;  // a link only matters while building
       segmask[k] = t.segmask[i];
-      hash[k] = t.hash[i];
     }
     put(ids.data(), n * 4);
     put(meta.data(), n * 4);
     put(parent.data(), n * 4);
     put(segmask.data(), n * 4);
-    put(hash.data(), n * 8);
-    if (n) {
-      std::vector<void*> tmp;
-      int32_t* d_ids = DevAlloc<int32_t>(kSnapChunk, &tmp);
-      uint32_t* d_blk = DevAlloc<uint32_t>(kSnapChunk * blk, &tmp);
-      try {
-        for (size_t k0 = 0; k0 < n; k0 += kSnapChunk) {
-          const int m = static_cast<int>(std::min<size_t>(kSnapChunk, n - k0));
-          Check(cudaMemcpy(d_ids, ids.data() + k0, static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice), "snapshot");
-          Check(pre3::LaunchSnapshotRows(e->cache, e->W, e->nseg, d_ids, m, d_blk, false, nullptr), "snapshot gather");
-          Check(cudaMemcpy(p, d_blk, static_cast<size_t>(m) * blk * 4, cudaMemcpyDeviceToHost), "snapshot");
-          p += static_cast<size_t>(m) * blk * 4;
-        }
-      } catch (...) {
-        for (void* q : tmp) cudaFree(q);
-        throw;
-      }
-      for (void* q : tmp) cudaFree(q);
-    }
+    SnapshotRows(e, ids, p, false);
     SnapHeader h{};
     std::memcpy(h.magic, kSnapMagic, 8);
-    h.version = 1;
+    h.version = kSnapVersion;
     h.header_bytes = kSnapHeader;
     h.grammar_hash = e->grammar_hash;
     h.layout_hash = e->layout_hash;
@@ -1226,7 +1290,9 @@ int gm_engine_snapshot_load(gm_engine* e, const void* buf, uint64_t bytes) {
     SnapHeader h;
     std::memcpy(&h, buf, sizeof h);
     if (std::memcmp(h.magic, kSnapMagic, 8) != 0) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: bad magic");
-    if (h.version != 1 || h.header_bytes != kSnapHeader) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: unknown version");
+    if (h.version != kSnapVersion || h.header_bytes != kSnapHeader) {
+      return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: unknown version");
+    }
     const uint8_t* in = static_cast<const uint8_t*>(buf);
     if (h.payload_bytes != bytes - kSnapHeader) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: size mismatch");
     if (Hash64(in + kSnapHeader, h.payload_bytes) != h.checksum) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: checksum");
@@ -1237,11 +1303,11 @@ int gm_engine_snapshot_load(gm_engine* e, const void* buf, uint64_t bytes) {
       return Fail(GM_ERR_SNAPSHOT_MISMATCH, "snapshot: taken for another vocabulary or logit layout");
     }
     if (h.K != e->cache.K || h.R != e->cache.R || h.C != e->cache.C || h.max_context != pre3::kMaxContext) {
-      return Fail(GM_ERR_SNAPSHOT_MISMATCH, "snapshot: taken with other context options (K, R, slots)");
+      return Fail(GM_ERR_SNAPSHOT_MISMATCH, "snapshot: taken with other context options (K, R, rows)");
     }
     const size_t n = static_cast<size_t>(h.n), blk = SnapBlockWords(e);
-    if (h.n < 0 || h.n > h.C || h.payload_bytes != n * (4 * 4 + 8) + n * blk * 4) {
-      return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: slot count");
+    if (h.n < 0 || h.n > h.C || h.payload_bytes != n * 16 + n * blk * 4) {
+      return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: row count");
     }
     Check(cudaSetDevice(e->device), "cudaSetDevice");
     Check(cudaDeviceSynchronize(), "snapshot: work in flight");
@@ -1251,7 +1317,6 @@ int gm_engine_snapshot_load(gm_engine* e, const void* buf, uint64_t bytes) {
     const uint8_t* p = in + kSnapHeader;
     std::vector<int32_t> ids(n), meta(n), parent(n);
     std::vector<uint32_t> segmask(n);
-    std::vector<unsigned long long> hash(n);
     auto get = [&p](void* dst, size_t b) {
       if (b) std::memcpy(dst, p, b);
       p += b;
@@ -1260,41 +1325,20 @@ int gm_engine_snapshot_load(gm_engine* e, const void* buf, uint64_t bytes) {
     get(meta.data(), n * 4);
     get(parent.data(), n * 4);
     get(segmask.data(), n * 4);
-    get(hash.data(), n * 8);
-    SlotTables t = ReadSlotTables(e);
+    RowTables t = ReadRowTables(e);
     const int32_t full = e->nseg * pre3::kChunksPerSeg;
     for (size_t k = 0; k < n; ++k) {
       const int32_t i = ids[k];
-      if (i < 0 || i >= h.C || t.hash[static_cast<size_t>(i)] != 0ull || hash[k] == 0ull ||
-          !(meta[k] & (1 << 16)) || (meta[k] & 0xff) > e->cache.K || parent[k] < -1 || parent[k] >= h.C) {
-        return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: bad slot record");
+      if (i < 0 || i >= h.C || (t.meta[static_cast<size_t>(i)] & (1 << 16)) || !(meta[k] & (1 << 16)) ||
+          (meta[k] & 0xff) > e->cache.K || parent[k] < -1 || parent[k] >= h.C) {
+        return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: bad row record");
       }
-      t.hash[static_cast<size_t>(i)] = hash[k];
       t.meta[static_cast<size_t>(i)] = meta[k];
       t.built[static_cast<size_t>(i)] = full;
       t.parent[static_cast<size_t>(i)] = parent[k];
       t.segmask[static_cast<size_t>(i)] = segmask[k];
     }
-    // Rows first, then the tables that publish them.
-    if (n) {
-      std::vector<void*> tmp;
-      int32_t* d_ids = DevAlloc<int32_t>(kSnapChunk, &tmp);
-      uint32_t* d_blk = DevAlloc<uint32_t>(kSnapChunk * blk, &tmp);
-      try {
-        for (size_t k0 = 0; k0 < n; k0 += kSnapChunk) {
-          const int m = static_cast<int>(std::min<size_t>(kSnapChunk, n - k0));
-          Check(cudaMemcpy(d_ids, ids.data() + k0, static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice), "snapshot");
-          Check(cudaMemcpy(d_blk, p, static_cast<size_t>(m) * blk * 4, cudaMemcpyHostToDevice), "snapshot");
-          Check(pre3::LaunchSnapshotRows(e->cache, e->W, e->nseg, d_ids, m, d_blk, true, nullptr), "snapshot scatter");
-          Check(cudaDeviceSynchronize(), "snapshot scatter");
-          p += static_cast<size_t>(m) * blk * 4;
-        }
-      } catch (...) {
-        for (void* q : tmp) cudaFree(q);
-        throw;
-      }
-      for (void* q : tmp) cudaFree(q);
-    }
+    SnapshotRows(e, ids, const_cast<uint8_t*>(p), true);
     const size_t C = static_cast<size_t>(e->cache.C);
     std::vector<int32_t> seg_done(C * static_cast<size_t>(e->nseg), 0);
     for (size_t k = 0; k < n; ++k) {
@@ -1307,12 +1351,51 @@ int gm_engine_snapshot_load(gm_engine* e, const void* buf, uint64_t bytes) {
     Check(cudaMemcpy(e->cache.slot_parent, t.parent.data(), C * 4, cudaMemcpyHostToDevice), "snapshot");
     Check(cudaMemcpy(e->cache.cd_segmask, t.segmask.data(), C * 4, cudaMemcpyHostToDevice), "snapshot");
     Check(cudaMemcpy(e->cache.slot_meta, t.meta.data(), C * 4, cudaMemcpyHostToDevice), "snapshot");
-    Check(cudaMemcpy(e->cache.slot_hash, t.hash.data(), C * 8, cudaMemcpyHostToDevice), "snapshot");
+    // Free list: every row not loaded (in id order: pops hand out the lowest first).
+    std::vector<int32_t> fr;
+    fr.reserve(C - n);
+    for (size_t i = C; i-- > 0;) {
+      if (!(t.meta[i] & (1 << 16))) fr.push_back(static_cast<int32_t>(i));
+    }
+    const int32_t nfree = static_cast<int32_t>(fr.size());
+    if (!fr.empty()) Check(cudaMemcpy(e->cache.row_free, fr.data(), fr.size() * 4, cudaMemcpyHostToDevice), "snapshot");
+    Check(cudaMemcpy(e->cache.row_free_n, &nfree, 4, cudaMemcpyHostToDevice), "snapshot");
+    *e->host_free = nfree;
     ctr[0] = n;
     Check(cudaMemcpy(e->cache.counters, ctr, 64, cudaMemcpyHostToDevice), "snapshot");
+    Check(pre3::LaunchReindex(e->cache, nullptr), "snapshot reindex");
     // The CI ∩ structural counts follow the engine's current structural set.
     Check(pre3::LaunchRecountStructural(e->cache, e->vocab), "snapshot recount");
     Check(cudaDeviceSynchronize(), "snapshot load");
+    return GM_OK;
+  });
+}
+
+int gm_engine_evict(gm_engine* e, void* stream) {
+  return Guard([&]() -> int {
+    if (!e) return Fail(GM_ERR_USAGE, "null engine");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    Evict(e, static_cast<cudaStream_t>(stream));
+    return GM_OK;
+  });
+}
+
+int gm_engine_cache_stats(gm_engine* e, int64_t out[8]) {
+  return Guard([&]() -> int {
+    if (!e || !out) return Fail(GM_ERR_USAGE, "null argument");
+    Check(cudaSetDevice(e->device), "cudaSetDevice");
+    unsigned long long ctr[8];
+    int32_t nfree = 0;
+    Check(cudaMemcpy(ctr, e->cache.counters, 64, cudaMemcpyDeviceToHost), "cache stats");
+    Check(cudaMemcpy(&nfree, e->cache.row_free_n, 4, cudaMemcpyDeviceToHost), "cache stats");
+    out[0] = e->cache.C;
+    out[1] = static_cast<int64_t>(ctr[0]);
+    out[2] = std::max(nfree, 0);
+    out[3] = e->cache.IC;
+    out[4] = static_cast<int64_t>(ctr[4]);
+    out[5] = static_cast<int64_t>(ctr[5]);
+    out[6] = static_cast<int64_t>(ctr[2]);
+    out[7] = static_cast<int64_t>(ctr[1]);
     return GM_OK;
   });
 }

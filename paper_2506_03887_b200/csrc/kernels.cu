@@ -127,6 +127,11 @@ __device__ __forceinline__ T LoadAcquire(const T* p) {
   return cuda::atomic_ref<T, cuda::thread_scope_device>(*const_cast<T*>(p)).load(cuda::memory_order_acquire);
 }
 
+template <typename T>
+__device__ __forceinline__ void StoreRelease(T* p, T v) {
+  cuda::atomic_ref<T, cuda::thread_scope_device>(*p).store(v, cuda::memory_order_release);
+}
+
 // Queue q of the batch, selected without indexing the by-value parameter
 // struct (a dynamic index would copy the whole BatchView to local memory).
 __device__ __forceinline__ BuildQueue QueueOf(const BatchView& Bt, int q) {
@@ -504,56 +509,89 @@ __device__ __forceinline__ unsigned long long KeyHashWarp(int kv, int n, int com
   return KeyHashFinish(x, n, complete);
 }
 
-// Meta word of slot i once its inserter has published the key row (the
-// ready bit follows the key stores immediately); bounded at ~0.5 ms, after
-// which the caller falls back to a private row.
-__device__ __forceinline__ int WaitReady(const CacheView& C, int i) {
-  int m = LoadAcquire(C.slot_meta + i);
-  for (int spin = 0; !(m & (1 << 16)) && spin < 4096; ++spin) {
-    __nanosleep(128);
-    m = LoadAcquire(C.slot_meta + i);
-  }
-  return m;
+// Index entry tag of a key hash (bit 63 set: never 0 = empty).
+__device__ __forceinline__ unsigned long long EntryTag(unsigned long long h) { return (h | (1ull << 63)) & ~kRowMask; }
+
+// Pops a free row (-1: none left: the caller uses a private row).  The
+// count is mirrored to host-mapped memory for the auto-eviction check.
+__device__ __forceinline__ int PopRow(const CacheView& C) {
+  const int k = atomicSub(C.row_free_n, 1);
+  if (k <= 0) return -1;
+  if (C.host_free != nullptr) *reinterpret_cast<volatile int32_t*>(C.host_free) = k - 1;
+  return __ldcg(C.row_free + (k - 1));
 }
 
-// Finds or inserts the slot of a key.  Returns the slot (created = true when
-// this thread inserted it) or -1 (table full, or the key is being published
+// Index entry at position i once its claimant has published the row (the
+// row and its key follow the claim immediately); bounded at ~0.5 ms, after
+// which the caller falls back to a private row.
+__device__ __forceinline__ unsigned long long WaitPublished(const CacheView& C, int i, unsigned long long e) {
+  for (int spin = 0; (e & kRowMask) == static_cast<unsigned long long>(kRowPending) && spin < 4096; ++spin) {
+    __nanosleep(128);
+    e = LoadAcquire(C.slot_hash + i);
+  }
+  return e;
+}
+
+// Claims index position i for `tag`, pops a row, writes its key row and
+// meta, publishes tag | row.  Returns the row, -1 when the position was
+// taken by someone else, -2 when no row is free (the claim is withdrawn).
+__device__ int InsertRow(const CacheView& C, int i, unsigned long long tag, const int32_t* key, int n, int complete) {
+  if (atomicCAS(C.slot_hash + i, 0ull, tag | static_cast<unsigned long long>(kRowPending)) != 0ull) return -1;
+  const int row = PopRow(C);
+  if (row < 0) {
+    StoreRelease(C.slot_hash + i, 0ull);
+    return -2;
+  }
+  for (int j = 0; j < kMaxContext; ++j) C.slot_keys[row * kMaxContext + j] = j < n ? key[j] : -1;
+  atomic_i32 meta(C.slot_meta[row]);
+  meta.store(n | (complete << 8) | (1 << 16), cuda::memory_order_release);
+  C.row_ref[row] = 1;
+  atomicAdd(C.counters + 0, 1ull);
+  StoreRelease(C.slot_hash + i, tag | static_cast<unsigned long long>(row));
+  return row;
+}
+
+// Finds or inserts the row of a key.  Returns the row (created = true when
+// this thread inserted it) or -1 (no free row, or the key is being published
 // by another thread right now).
 __device__ int LookupSlot(const CacheView& C, const int32_t* key, int n, int complete, bool* created) {
   const unsigned long long h = KeyHash(key, n, complete);
+  const unsigned long long tag = EntryTag(h);
   const int meta_want = n | (complete << 8);
   *created = false;
+  const unsigned long long imask = static_cast<unsigned long long>(C.IC - 1);
   for (int p = 0; p < 64; ++p) {
-    const int i = static_cast<int>((h + static_cast<unsigned long long>(p)) & static_cast<unsigned long long>(C.C - 1));
-    atomic_u64 slot(C.slot_hash[i]);
-    unsigned long long cur = slot.load(cuda::memory_order_relaxed);
-    if (cur == 0) {
-      unsigned long long expect = 0;
-      if (slot.compare_exchange_strong(expect, h, cuda::memory_order_relaxed)) {
-        for (int j = 0; j < kMaxContext; ++j) C.slot_keys[i * kMaxContext + j] = j < n ? key[j] : -1;
-        atomic_i32 meta(C.slot_meta[i]);
-        meta.store(meta_want | (1 << 16), cuda::memory_order_release);
-        atomicAdd(C.counters + 0, 1ull);
+    const int i = static_cast<int>((h + static_cast<unsigned long long>(p)) & imask);
+    unsigned long long cur = LoadAcquire(C.slot_hash + i);
+    if (cur == 0ull) {
+      const int r = InsertRow(C, i, tag, key, n, complete);
+      if (r >= 0) {
         *created = true;
-        return i;
+        return r;
       }
-      cur = expect;
+      if (r == -2) return -1;
+      cur = LoadAcquire(C.slot_hash + i);
     }
-    if (cur != h) continue;
-    const int m = WaitReady(C, i);
-    if (!(m & (1 << 16))) return -1;
-    if ((m & 0xffff) != meta_want) continue;
+    if ((cur & ~kRowMask) != tag) continue;
+    cur = WaitPublished(C, i, cur);
+    if ((cur & ~kRowMask) != tag || (cur & kRowMask) == static_cast<unsigned long long>(kRowPending)) return -1;
+    const int row = static_cast<int>(cur & kRowMask);
+    const int m = LoadAcquire(C.slot_meta + row);
+    if ((m & 0x1ffff) != (meta_want | (1 << 16))) continue;
     // Whole key row in independent vector loads.
-    const int4* row = reinterpret_cast<const int4*>(C.slot_keys + i * kMaxContext);
+    const int4* krow = reinterpret_cast<const int4*>(C.slot_keys + row * kMaxContext);
     int4 q[kMaxContext / 4];
 #pragma unroll
-    for (int v = 0; v < kMaxContext / 4; ++v) q[v] = 4 * v < n ? __ldcg(row + v) : make_int4(-1, -1, -1, -1);
+    for (int v = 0; v < kMaxContext / 4; ++v) q[v] = 4 * v < n ? __ldcg(krow + v) : make_int4(-1, -1, -1, -1);
     bool same = true;
 #pragma unroll
     for (int j = 0; j < kMaxContext; ++j) {
       if (j < n && Lane4(q[j >> 2], j & 3) != key[j]) same = false;
     }
-    if (same) return i;
+    if (same) {
+      C.row_ref[row] = 1;
+      return row;
+    }
   }
   return -1;
 }
@@ -904,61 +942,81 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
   return __shfl_sync(0xffffffffu, tok, src);
 }
 
-// Warp-cooperative LookupSlot: same table protocol (64 linear probes from
-// the key hash; insert = CAS on the hash, key row, then meta with the ready
-// bit, release), but 32 probes are read in one round trip and a hit is
-// verified — key row, meta, build progress and CD segment mask — in one
-// more.  `kv` = key entry `lane` (lanes < n).  Returns the slot (-1: table
-// full, or the key is being published right now); *created when this warp
-// inserted it; *built / *segmask of an existing slot.
+// Warp-cooperative LookupSlot: same index protocol (64 linear probes from
+// the key hash; insert = claim the position, pop a row, key row + meta, then
+// publish tag | row, release), but 32 probes are read in one round trip and
+// a hit is verified — key row, meta, build progress and CD segment mask — in
+// one more.  `kv` = key entry `lane` (lanes < n).  Returns the row (-1: no
+// free row, or the key is being published right now); *created when this
+// warp inserted it; *built / *segmask of an existing row.
 __device__ int LookupSlotWarp(const CacheView& C, int kv, int n, int complete, int lane, bool* created, int* built,
                               uint32_t* segmask) {
   const unsigned long long h = KeyHashWarp(kv, n, complete, lane);
-  const int meta_want = n | (complete << 8);
+  const unsigned long long tag = EntryTag(h);
+  const int meta_want = n | (complete << 8) | (1 << 16);
   *created = false;
-  const unsigned long long cmask = static_cast<unsigned long long>(C.C - 1);
+  const unsigned long long imask = static_cast<unsigned long long>(C.IC - 1);
   for (int base = 0; base < 64; base += 32) {
     for (int attempt = 0; attempt < 8; ++attempt) {  // re-read a window after a lost insert race
-      const int i = static_cast<int>((h + static_cast<unsigned long long>(base + lane)) & cmask);
+      const int i = static_cast<int>((h + static_cast<unsigned long long>(base + lane)) & imask);
       const unsigned long long cur = LoadRelaxed(C.slot_hash + i);
-      const unsigned hit = __ballot_sync(0xffffffffu, cur == h);
+      const unsigned hit = __ballot_sync(0xffffffffu, (cur & ~kRowMask) == tag);
       const unsigned empty = __ballot_sync(0xffffffffu, cur == 0ull);
       unsigned cand = hit & (empty ? ((1u << (__ffs(empty) - 1)) - 1u) : 0xffffffffu);
       while (cand) {
         const int src = __ffs(cand) - 1;
         cand &= cand - 1;
-        const int slot = static_cast<int>((h + static_cast<unsigned long long>(base + src)) & cmask);
+        unsigned long long e = __shfl_sync(0xffffffffu, cur, src);
+        if ((e & kRowMask) == static_cast<unsigned long long>(kRowPending)) {  // being published right now
+          if (lane == 0) e = WaitPublished(C, static_cast<int>((h + static_cast<unsigned long long>(base + src)) & imask), e);
+          e = __shfl_sync(0xffffffffu, e, 0);
+          if ((e & ~kRowMask) != tag || (e & kRowMask) == static_cast<unsigned long long>(kRowPending)) return -1;
+        }
+        const int row = static_cast<int>(e & kRowMask);
         // Key row (lane i = entry i), meta, build progress, CD segments: one
-        // round trip (the last three are warp-broadcast loads).
-        const int v = lane < n ? __ldcg(C.slot_keys + slot * kMaxContext + lane) : 0;
-        int m = LoadAcquire(C.slot_meta + slot);
-        const int bt = LoadAcquire(C.slot_built + slot);
-        const int sm = static_cast<int>(LoadRelaxed(C.cd_segmask + slot));
-        if (!(m & (1 << 16))) m = WaitReady(C, slot);  // key row being published right now
-        if (!(m & (1 << 16))) return -1;
-        if ((m & 0xffff) != meta_want) continue;
+        // round trip (the last three are warp-broadcast loads; the row id
+        // they index arrived with the published entry).
+        const int v = lane < n ? __ldcg(C.slot_keys + row * kMaxContext + lane) : 0;
+        const int m = LoadAcquire(C.slot_meta + row);
+        const int bt = LoadAcquire(C.slot_built + row);
+        const int sm = static_cast<int>(LoadRelaxed(C.cd_segmask + row));
+        if ((m & 0x1ffff) != meta_want) continue;
         if (__all_sync(0xffffffffu, lane >= n || v == kv)) {
+          if (lane == 0) C.row_ref[row] = 1;
           *built = bt;
           *segmask = static_cast<uint32_t>(sm);
-          return slot;
+          return row;
         }
       }
-      if (!empty) break;  // no free slot in this window: probe the next one
+      if (!empty) break;  // no free position in this window: probe the next one
       const int src = __ffs(empty) - 1;
-      const int slot = static_cast<int>((h + static_cast<unsigned long long>(base + src)) & cmask);
-      int won = 0;
-      if (lane == 0) won = atomicCAS(C.slot_hash + slot, 0ull, h) == 0ull;
-      if (__shfl_sync(0xffffffffu, won, 0)) {
-        if (lane < kMaxContext) C.slot_keys[slot * kMaxContext + lane] = lane < n ? kv : -1;
+      const int pos = static_cast<int>((h + static_cast<unsigned long long>(base + src)) & imask);
+      int row = -1;
+      if (lane == 0) {
+        row = atomicCAS(C.slot_hash + pos, 0ull, tag | static_cast<unsigned long long>(kRowPending)) == 0ull ? -3 : -1;
+        if (row == -3) {
+          row = PopRow(C);
+          if (row < 0) {
+            StoreRelease(C.slot_hash + pos, 0ull);  // withdraw the claim: the table is full
+            row = -2;
+          }
+        }
+      }
+      row = __shfl_sync(0xffffffffu, row, 0);
+      if (row == -2) return -1;
+      if (row >= 0) {
+        if (lane < kMaxContext) C.slot_keys[row * kMaxContext + lane] = lane < n ? kv : -1;
         __threadfence();
         __syncwarp();
         if (lane == 0) {
-          atomic_i32 meta(C.slot_meta[slot]);
-          meta.store(meta_want | (1 << 16), cuda::memory_order_release);
+          atomic_i32 meta(C.slot_meta[row]);
+          meta.store(meta_want, cuda::memory_order_release);
+          C.row_ref[row] = 1;
           atomicAdd(C.counters + 0, 1ull);
+          StoreRelease(C.slot_hash + pos, tag | static_cast<unsigned long long>(row));
         }
         *created = true;
-        return slot;
+        return row;
       }
     }
   }
@@ -2966,6 +3024,111 @@ __global__ void SnapshotRowsKernel(CacheView c, int W, int nseg, const int32_t* 
     }
     off += parts[k].len;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Eviction (CLOCK over rows; the engine is quiescent: no fill, accept or
+// lookup of any of its batches in flight).
+// ---------------------------------------------------------------------------
+// keep[row] for rows in use: referenced since the last eviction, or a build
+// still pending (its parent too: the child's build reads the parent's rows).
+// Clears the reference bits.
+__global__ void EvictMarkRowsKernel(CacheView c, int full, uint8_t* keep) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < c.C; r += gridDim.x * blockDim.x) {
+    if (!(c.slot_meta[r] & (1 << 16))) continue;
+    const bool pending = c.slot_built[r] < full;
+    if (c.row_ref[r] || pending) keep[r] = 1;
+    if (pending && c.slot_parent[r] >= 0) keep[c.slot_parent[r]] = 1;
+    c.row_ref[r] = 0;
+  }
+}
+
+// Rows a batch's next fill (or the one in flight, other parity) will read.
+__global__ void EvictMarkBatchKernel(CacheView c, const int32_t* seq_slot, int n, uint8_t* keep) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int s = seq_slot[i];
+    if (s < 0) continue;
+    s &= ~kSlotWait;
+    if (s < c.C) keep[s] = 1;
+  }
+}
+
+__global__ void EvictRepairFreeKernel(CacheView c) {
+  if (threadIdx.x == 0 && *c.row_free_n < 0) *c.row_free_n = 0;
+}
+
+// Resets and frees every row in use that is not kept.
+__global__ void EvictFreeKernel(CacheView c, int nseg, const uint8_t* keep) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < c.C; r += gridDim.x * blockDim.x) {
+    if (!(c.slot_meta[r] & (1 << 16)) || keep[r]) continue;
+    c.slot_meta[r] = 0;
+    c.slot_built[r] = 0;
+    c.cd_segmask[r] = 0u;
+    c.slot_parent[r] = -1;
+    for (int g = 0; g < nseg; ++g) {
+      const long long k = static_cast<long long>(r) * nseg + g;
+      c.seg_done[k] = 0;
+      c.seg_claim[k] = 0;
+      c.cd_cnt[k] = 0;
+      c.ci_cnt[2 * k] = 0;
+      c.ci_cnt[2 * k + 1] = 0;
+    }
+    c.row_free[atomicAdd(c.row_free_n, 1)] = r;
+    atomicAdd(c.counters + 5, 1ull);
+    atomicAdd(c.counters + 0, ~0ull);  // one row fewer in use
+  }
+}
+
+// Index rebuild: one warp per row in use inserts tag | row (the key hash
+// of its stored key row).
+__global__ void ReindexKernel(CacheView c) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < c.C; r += nw) {
+    const int m = c.slot_meta[r];
+    if (!(m & (1 << 16))) continue;
+    const int n = m & 0xff, complete = (m >> 8) & 1;
+    const int kv = lane < n ? c.slot_keys[r * kMaxContext + lane] : 0;
+    const unsigned long long h = KeyHashWarp(kv, n, complete, lane);
+    if (lane == 0) {
+      const unsigned long long e = EntryTag(h) | static_cast<unsigned long long>(r);
+      for (unsigned long long p = 0;; ++p) {
+        const unsigned long long i = (h + p) & static_cast<unsigned long long>(c.IC - 1);
+        if (atomicCAS(c.slot_hash + i, 0ull, e) == 0ull) break;
+      }
+    }
+  }
+}
+
+__global__ void EvictFinishKernel(CacheView c) {
+  if (threadIdx.x == 0) {
+    atomicAdd(c.counters + 4, 1ull);
+    if (c.host_free != nullptr) *reinterpret_cast<volatile int32_t*>(c.host_free) = *c.row_free_n;
+  }
+}
+
+cudaError_t LaunchReindex(const CacheView& c, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(c.slot_hash, 0, static_cast<size_t>(c.IC) * 8, s);
+  if (e != cudaSuccess) return e;
+  ReindexKernel<<<(c.C + 7) / 8, 256, 0, s>>>(c);
+  return cudaGetLastError();
+}
+
+cudaError_t LaunchEvict(const CacheView& c, int nseg, const int32_t* const* seq_slots, const int* counts, int nb,
+                        uint8_t* keep, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(keep, 0, static_cast<size_t>(c.C), s);
+  if (e != cudaSuccess) return e;
+  const int grid = (c.C + 255) / 256;
+  EvictMarkRowsKernel<<<grid, 256, 0, s>>>(c, nseg * kChunksPerSeg, keep);
+  for (int i = 0; i < nb; ++i) {
+    if (counts[i] > 0) EvictMarkBatchKernel<<<(counts[i] + 255) / 256, 256, 0, s>>>(c, seq_slots[i], counts[i], keep);
+  }
+  EvictRepairFreeKernel<<<1, 32, 0, s>>>(c);
+  EvictFreeKernel<<<grid, 256, 0, s>>>(c, nseg, keep);
+  e = LaunchReindex(c, s);
+  if (e != cudaSuccess) return e;
+  EvictFinishKernel<<<1, 32, 0, s>>>(c);
+  return cudaGetLastError();
 }
 
 cudaError_t LaunchSnapshotRows(const CacheView& c, int W, int nseg, const int32_t* ids, int n, uint32_t* blocks,

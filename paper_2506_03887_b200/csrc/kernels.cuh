@@ -74,9 +74,16 @@ struct VocabView {
 // {CI: tokens accepted whatever lies below the key, CD: tokens whose walk
 // reaches below the key} as two W-word bitsets, plus per-segment CD counts
 // and build-completion counters.
+// Rows (the "slots" every other array indexes, seq_slot values) are reached
+// through an open-addressing index of IC = 2C positions holding
+// tag << 24 | row (0: empty; row kRowPending: claimed, row being published),
+// so a row can be evicted and reused without moving any data: eviction
+// (EvictKernels, gm_engine_evict) rebuilds the index from the live rows.
+constexpr unsigned long long kRowMask = 0xFFFFFFull;
+constexpr int kRowPending = 0xFFFFFF;
 struct CacheView {
-  unsigned long long* slot_hash;  // C; 0 = empty
-  int32_t* slot_meta;             // C; n | complete << 8 | ready << 16
+  unsigned long long* slot_hash;  // IC index entries
+  int32_t* slot_meta;             // C; n | complete << 8 | ready << 16 (0: a free row)
   int32_t* slot_keys;             // C*kMaxContext (rows padded with -1)
   uint32_t* ci;                   // C*W
   uint32_t* cdb;                  // C*W
@@ -89,8 +96,14 @@ struct CacheView {
   uint32_t* cd_segmask;           // C: bit s set when segment s has context-dependent tokens
   int32_t* ci_cnt;                // C*nseg*2: per segment, CI tokens (EOS excluded) and CI ∩ structural
   int32_t* slot_parent;           // C: context a new one is built from (-1: full build)
-  unsigned long long* counters;   // [0] slots, [1] segment builds, [2] private builds, [3] parent-based builds
+  int32_t* row_free;              // C: free-row stack, entries [0, *row_free_n)
+  int32_t* row_free_n;            // free rows left (dips below 0 while pops fail; eviction repairs it)
+  uint8_t* row_ref;               // C: reference bits (lookups set, eviction clears: CLOCK)
+  int32_t* host_free;             // host-mapped: free rows after the latest pop (auto-eviction trigger)
+  unsigned long long* counters;   // [0] rows in use, [1] segment builds, [2] private builds, [3] parent-based
+                                  // builds, [4] evictions, [5] rows evicted
   int32_t C;
+  int32_t IC;                     // index positions (power of two, 2C)
   int32_t K;
   int32_t R;                      // parent key depth (0: no parents)
 };
@@ -206,6 +219,14 @@ cudaError_t LaunchReset(const AutView& a, const BatchView& b, cudaStream_t s);
 cudaError_t LaunchAllowed(const AutView& a, const BatchView& b, uint32_t* out, cudaStream_t s);
 cudaError_t LaunchLookup(const CacheView& c, const BatchView& b, int queue, int tag, cudaStream_t s);
 cudaError_t LaunchRecountStructural(const CacheView& c, const VocabView& v);
+// Eviction (quiescent engine): keep = rows referenced since the last
+// eviction, rows with builds pending and their parents, and rows named by
+// the given seq_slot arrays; the rest are reset and freed, then the index is
+// rebuilt from the live rows.  Returns the launch error.
+cudaError_t LaunchEvict(const CacheView& c, int nseg, const int32_t* const* seq_slots, const int* counts, int nb,
+                        uint8_t* keep, cudaStream_t s);
+// Rebuilds the index from the rows in use (snapshot loads).
+cudaError_t LaunchReindex(const CacheView& c, cudaStream_t s);
 // Snapshot rows of n listed slots <-> blocks of kMaxContext + 3*nseg + 2*W words.
 cudaError_t LaunchSnapshotRows(const CacheView& c, int W, int nseg, const int32_t* ids, int n, uint32_t* blocks,
                                bool scatter, cudaStream_t s);

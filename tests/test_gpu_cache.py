@@ -158,3 +158,64 @@ def test_walk_past_the_overlay_fails_loudly(vocab):
     eng = engine(voc, K=4, slots=256)
     with pytest.raises(pk.StackOverflowError):
         eng.ComputeMask(eng.InitialConfig())
+
+
+# ---------------------------------------------------------------- eviction
+def test_auto_eviction_keeps_every_mask_exact(vocab):
+    """A 64-row table that keeps evicting (CLOCK: rows not referenced since
+    the previous eviction, never those a fill is about to read or a pending
+    build needs): every step's masks and tokens equal the port's."""
+    eng = pk.DeviceEngine(pk.Automaton.load(flat("json")), vocab, context_depth=8, context_slots=64,
+                          auto_evict_free=24)
+    B, steps, seed = 40, 48, 29
+    batch, hashes, toks = split_loop(eng, B, steps, seed)
+    ptoks, pstk, phashes = port_run(vocab, eng.structural, B, steps, seed)
+    assert np.array_equal(hashes, phashes) and np.array_equal(toks, ptoks)
+    for i in range(B):
+        assert batch.get(i).stack == pstk[i, 2:2 + pstk[i, 0]].tolist()
+    st = eng.cache_stats()
+    assert st["evictions"] > 0 and st["rows_evicted"] > 0, st
+    assert st["rows_in_use"] + st["rows_free"] == st["rows"] == 64, st
+
+
+def test_explicit_eviction_between_steps_and_graph_replays(vocab):
+    """gm_engine_evict between eager steps and between replays of a captured
+    graph (rows never move, so the graph's baked-in state stays valid)."""
+    eng = engine(vocab, K=8, slots=256)
+    B, G, seed = 32, 6, 41
+    batch = eng.batch(B)
+    tks = [torch.zeros(B, dtype=torch.int32, device=DEV) for _ in range(G)]
+    graph = batch.capture_steps(G, seed=seed, tokens_out=tks)
+    got = []
+    for rep in range(4):
+        graph.launch()
+        batch.check()
+        got.append(torch.stack(tks, 1).cpu().numpy())
+        used = eng.cache_stats()["rows_in_use"]
+        eng.evict()
+        torch.cuda.synchronize()
+        st = eng.cache_stats()
+        assert st["rows_in_use"] <= used and st["rows_in_use"] + st["rows_free"] == 256
+    ptoks, pstk, _ = port_run(vocab, eng.structural, B, 4 * G, seed)
+    assert np.array_equal(np.concatenate(got, 1), ptoks)
+    for i in range(B):
+        assert batch.get(i).stack == pstk[i, 2:2 + pstk[i, 0]].tolist()
+    # two evictions in a row with nothing referenced in between: the second
+    # frees what the first kept only for its reference bit
+    eng.evict()
+    eng.evict()
+    torch.cuda.synchronize()
+    assert eng.cache_stats()["rows_in_use"] <= 2 * B  # next-fill rows and their parents
+
+
+def test_table_full_at_128k_matches_the_port():
+    """Configs' vocabulary size with an 8-row table and no eviction: most
+    sequences fall back to private rows (built from their whole stack every
+    step) and the masks stay exact."""
+    voc = pk.synth_vocab(128255)
+    eng = pk.DeviceEngine(pk.Automaton.load(flat("json")), voc, context_depth=8, context_slots=8)
+    B, steps, seed = 16, 10, 3
+    batch, hashes, toks = split_loop(eng, B, steps, seed, stats=True)
+    assert batch.fill_stats()["private_fills"] > 0
+    ptoks, _, phashes = port_run(voc, eng.structural, B, steps, seed)
+    assert np.array_equal(hashes, phashes) and np.array_equal(toks, ptoks)
