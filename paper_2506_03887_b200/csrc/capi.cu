@@ -165,7 +165,13 @@ struct gm_batch {
     fill_seq = (fill_seq + 1) % pre3::kFillPeriod;
     last_consumed = prod;
     prod = (prod + 1) % 3;
-    slots_valid = true;
+    // seq_slot / seq_hmask / heavy_index are double-buffered by fill parity
+    // and their heavy-list tags recur every kFillPeriod fills: the next fill's
+    // rows hold this batch's current contexts only when a lookup pass wrote
+    // them for it — the fused tail's, or a later accept's (AcceptLookupQueue).
+    // Otherwise the next fill runs LookupKernel first (two fills in a row,
+    // a sample without accept), never reading rows written for an older fill.
+    slots_valid = tail;
     lookup_pending = tail;  // the tail fed the new queue[prod]
   }
 
@@ -695,6 +701,7 @@ int gm_batch_check(gm_batch* b, void* stream) {
     Check(cudaMemcpy(&err, b->view.err, 4, cudaMemcpyDeviceToHost), "check");
     if (err) {
       Check(cudaMemset(b->view.err, 0, 4), "memset");
+      if (err & 2u) return Fail(GM_ERR_CUDA, "internal: an accept timed out waiting for its fill's items");
       return Fail(GM_ERR_STACK_OVERFLOW, "a mask walk pushed more than 256 entries above the stack (walk overlay)");
     }
     return GM_OK;

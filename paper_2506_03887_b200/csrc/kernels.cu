@@ -2432,7 +2432,17 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
       }
     }
     if (G.wait_fill && !pure) {
-      while (LoadAcquire(Bt.seq_arrive + b) < Vv.nseg) __nanosleep(64);
+      // Bounded (200 ms): a fill that never delivers the items would be an
+      // internal error — reported through gm_batch_check, never a hung GPU.
+      if (LoadAcquire(Bt.seq_arrive + b) < Vv.nseg) {
+        unsigned long long t_start, t_now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        do {
+          __nanosleep(64);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+        } while (LoadAcquire(Bt.seq_arrive + b) < Vv.nseg && t_now - t_start < 200000000ull);
+        if (t_now - t_start >= 200000000ull && lane == 0) atomicOr(Bt.err, 2u);
+      }
       __syncwarp();
       if (lane == 0) Bt.seq_arrive[b] = 0;
     }
