@@ -511,6 +511,20 @@ def main(argv=None):
     for i in range(Wm):
         step(i)
     batch.check()
+    if os.environ.get("PRE3_DIAG_FILL_FIRST"):  # diagnostics: the roofline sub-loop before the timed loop too
+        fe = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(40)]
+        for pair in fe:
+            for e_ in pair:
+                e_.record(stream)
+        torch.cuda.synchronize()
+        for i in range(40):
+            batch.time_next_fill(*fe[i])
+            step(Wm + i)
+        torch.cuda.synchronize()
+        print("diag fill-first:", summarize([1e3 * a_.elapsed_time(b_) for a_, b_ in fe]), file=sys.stderr)
+        for i in range(40, 42):  # back to a multiple of 6 eager steps past the warm-up
+            step(Wm + i)
+        Wm += 42
     # The timed steps as one captured CUDA graph (gm_decode_graph_create; a
     # multiple of 6 steps, the rest enqueued eagerly): one host call launches
     # them, with every step's own buffers baked in.

@@ -41,6 +41,15 @@
 #ifndef PRE3_COMPACT_MIXED
 #define PRE3_COMPACT_MIXED 0  // light pass: all mixed chunks of a segment copied in one round trip
 #endif
+#ifndef PRE3_MIXED_RED
+#define PRE3_MIXED_RED 0  // light pass: mixed spans blended in L2 (bulk stores + cp.reduce.async.bulk .min.bf16)
+#endif
+#ifndef PRE3_DIAG_NO_MIXED
+#define PRE3_DIAG_NO_MIXED 0  // (diagnostics only, wrong logits) every full span bulk-stored as -inf
+#endif
+#ifndef PRE3_SPAN_READ_ALL
+#define PRE3_SPAN_READ_ALL 0  // (A/B) mixed spans: every chunk not all-allowed is read, not just the mixed ones
+#endif
 #ifndef PRE3_BULK_MASKED
 #define PRE3_BULK_MASKED 1  // fully masked spans as one bulk (TMA) store
 #endif
@@ -1360,7 +1369,7 @@ __device__ __forceinline__ void SpanBytes(uint32_t mword, int lane, uint32_t byt
 // merges them sector by sector and still fetches the rest of each sector
 // from HBM); an all-allowed chunk is skipped.
 __device__ __forceinline__ void MaskSpan(uint16_t* row, int tw, int t1, bool vec_ok, uint32_t mword, int lane,
-                                         unsigned long long* rd, unsigned long long* wr) {
+                                         unsigned* rd, unsigned* wr) {
   uint32_t byte[4];
   SpanBytes(mword, lane, byte);
   if (vec_ok && tw + 1024 <= t1) {
@@ -1443,6 +1452,36 @@ __device__ __forceinline__ void BulkStore(void* gmem, const void* smem, int byte
 }
 __device__ __forceinline__ void BulkCommit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void BulkWaitRead() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void BulkWaitRead1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
+// Bulk (TMA) reduction into global memory, done in L2: dst = min(dst, src)
+// per bf16 element.  min() returns the non-NaN operand, so a NaN source
+// element leaves the destination's value (a NaN destination becomes the
+// canonical NaN) and a -inf source element writes -inf.
+__device__ __forceinline__ void BulkReduceMinBf16(void* gmem, const void* smem, int bytes) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.min.bf16 [%0], [%1], %2;\n" ::"l"(gmem), "r"(sa),
+               "r"(bytes)
+               : "memory");
+}
+// Bits 0, 2, 4, ..., 30 of x packed into bits 0..15.
+__device__ __forceinline__ uint32_t EvenBits(uint32_t x) {
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  return (x | (x >> 8)) & 0x0000FFFFu;
+}
+// Runs of set bits of a 64-sector mask: fn(first sector, sectors).
+template <typename Fn>
+__device__ __forceinline__ void ForRuns(unsigned long long x, Fn fn) {
+  while (x) {
+    const int s = __ffsll(static_cast<long long>(x)) - 1;
+    const unsigned long long above = ~(x >> s);
+    const int len = above ? __ffsll(static_cast<long long>(above)) - 1 : 64 - s;
+    fn(s, len);
+    x &= len >= 64 ? 0ull : ~(((1ull << len) - 1ull) << s);
+  }
+}
 
 // Mixed chunks of a full span -> this lane's slots of a span buffer.
 __device__ __forceinline__ void SpanPrefetch(const uint16_t* row, int tw, uint32_t mword, int lane,
@@ -1451,13 +1490,17 @@ __device__ __forceinline__ void SpanPrefetch(const uint16_t* row, int tw, uint32
   SpanBytes(mword, lane, byte);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
+#if PRE3_SPAN_READ_ALL
+    if (byte[k] != 0xffu) CpAsync16(&buf[k][lane], row + tw + (32 * k + lane) * 8);  // (A/B) whole sectors read
+#else
     if (byte[k] != 0u && byte[k] != 0xffu) CpAsync16(&buf[k][lane], row + tw + (32 * k + lane) * 8);
+#endif
   }
 }
 
 // Stores of a full span whose mixed chunks were prefetched into `buf`.
 __device__ __forceinline__ void SpanStore(uint16_t* row, int tw, uint32_t mword, int lane, const uint4 (*buf)[32],
-                                          unsigned long long* rd, unsigned long long* wr) {
+                                          unsigned* rd, unsigned* wr) {
   uint32_t byte[4];
   SpanBytes(mword, lane, byte);
 #pragma unroll
@@ -1496,7 +1539,7 @@ __device__ __forceinline__ void SpanPrefetchAllowed(const uint16_t* row, int tw,
 // This lane's best allowed (key, token) of a full span prefetched by
 // SpanPrefetchAllowed (0 when none).
 __device__ __forceinline__ unsigned long long ArgmaxBuffered(int tw, uint32_t mword, int lane,
-                                                             const uint4 (*buf)[32], unsigned long long* rd) {
+                                                             const uint4 (*buf)[32], unsigned* rd) {
   uint32_t byte[4];
   SpanBytes(mword, lane, byte);
   unsigned long long mine = 0;
@@ -1518,9 +1561,39 @@ __device__ __forceinline__ unsigned long long ArgmaxBuffered(int tw, uint32_t mw
   return mine;
 }
 
+// ArgmaxBuffered in 32-bit packed form: (16-bit order key << 16) |
+// (0xFFFF - token offset in the segment), 0 when no allowed token — one max
+// per token instead of 64-bit keys (an allowed key-0 token, bf16 0xFFFF, still
+// packs above 0: offsets are < 8192).  Key32 + the offset restore GreedyKey.
+__device__ __forceinline__ uint32_t ArgmaxBufferedPacked(int span_off, uint32_t mword, int lane,
+                                                         const uint4 (*buf)[32], unsigned* rd) {
+  uint32_t byte[4];
+  SpanBytes(mword, lane, byte);
+  uint32_t best = 0u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (!byte[k]) continue;
+    const uint4 v = buf[k][lane];
+    const uint32_t* pv = reinterpret_cast<const uint32_t*>(&v);
+    const uint32_t c0 = 0xFFFFu - static_cast<uint32_t>(span_off + (32 * k + lane) * 8);  // token 0 of the chunk
+    *rd += 16;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t w = pv[j];
+      const uint32_t neg = (w >> 15) & 0x00010001u;
+      const uint32_t key2 = w ^ (0x80008000u | (neg * 0x7FFFu));  // two 16-bit order keys
+      const uint32_t lo = (key2 << 16) | (c0 - 2 * j);
+      const uint32_t hi = (key2 & 0xFFFF0000u) | (c0 - 2 * j - 1);
+      if ((byte[k] >> (2 * j)) & 1u) best = max(best, lo);
+      if ((byte[k] >> (2 * j + 1)) & 1u) best = max(best, hi);
+    }
+  }
+  return best;
+}
+
 // This lane's best allowed (key, token) of the span (0 when none).
 __device__ __forceinline__ unsigned long long ArgmaxSpan(const uint16_t* row, int tw, int t1, bool vec_ok,
-                                                         uint32_t mword, int lane, unsigned long long* rd) {
+                                                         uint32_t mword, int lane, unsigned* rd) {
   uint32_t byte[4];
   SpanBytes(mword, lane, byte);
   unsigned long long mine = 0;
@@ -1591,7 +1664,7 @@ __device__ __forceinline__ int EosBitOf(const AutView& A, const VocabView& Vv, c
 // Logit columns [V, ncols) of a model layout (specials, EOS column): -inf,
 // except the EOS column when EOS is allowed.  Lanes stride the columns.
 __device__ __forceinline__ void TailColumns(const VocabView& Vv, uint16_t* row, int eos_bit, int lane, int nlanes,
-                                            unsigned long long* wr) {
+                                            unsigned* wr) {
   for (int c = Vv.V + lane; c < Vv.ncols; c += nlanes) {
     if (c == Vv.eos_col && eos_bit) continue;
     row[c] = 0xFF80u;
@@ -1715,6 +1788,45 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     __syncwarp();  // the buffer is reused for logits chunks below
   }
 
+  // ---- logits spans by class (MaskSpans): all allowed -> untouched, all
+  // masked -> a bulk store, mixed -> the mixed chunks read, blended, stored.
+  // The first two mixed spans' chunks are requested now, so their round trip
+  // overlaps the bitmask and count stores and the bulk stores below (an EOS
+  // column patched into this item's words waits until its bit is known).
+  uint32_t masked = 0u, mixed = 0u, pend = 0u;
+  const bool spans_early = MODE == kFillMask && F.logits != nullptr && !eos_in_seg;
+  uint16_t* lrow = F.logits != nullptr ? F.logits + static_cast<long long>(b) * F.ld : nullptr;
+  const int nfull = F.vec_ok ? (tl1 - t0) >> 10 : 0;
+  auto classify = [&]() {
+#pragma unroll
+    for (int i = 0; i < kSpans; ++i) {
+      const unsigned nz = __ballot_sync(0xffffffffu, m[i] != 0u);
+      const unsigned nf = __ballot_sync(0xffffffffu, m[i] != 0xffffffffu);
+      if (i < nfull) {
+        if ((!nz || PRE3_DIAG_NO_MIXED) && PRE3_BULK_MASKED && ((PRE3_BULK_SPANS >> i) & 1)) masked |= 1u << i;
+        else if (nf) mixed |= 1u << i;  // (a masked span left to the LSU path: -inf chunk stores)
+      }
+    }
+  };
+  auto prefetch2 = [&]() {  // the first two mixed spans -> the warp's span buffers 0, 1
+    pend = mixed;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (pend) {
+        const int i = __ffs(pend) - 1;
+        pend &= pend - 1;
+        SpanPrefetch(lrow, t0 + 1024 * i, Pick(m, i), lane, span_buf[q]);
+      }
+      CpAsyncCommit();
+    }
+  };
+#if !PRE3_MIXED_RED && !PRE3_COMPACT_MIXED
+  if (spans_early) {
+    classify();
+    prefetch2();
+  }
+#endif
+
   // ---- bitmask words and sampler counts (a pure item's are the slot's).
   const int eos_word = Vv.V >> 5;
   int ca = 0, cs = 0;
@@ -1759,7 +1871,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       eos_bit = __shfl_sync(0xffffffffu, eos_bit, 0);
     }
   }
-  unsigned long long rd = 0, wr = 0;
+  unsigned rd = 0, wr = 0;  // this lane's logit bytes (stats)
   if (MODE == kFillGreedy) {
     // Argmax over the allowed entries: only 16-B chunks holding an allowed
     // token are read, two spans in flight (cp.async into the warp's span
@@ -1902,18 +2014,24 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       CpAsyncCommit();
     }
     int q = 0;
+    uint32_t packed = 0u;  // ArgmaxBufferedPacked over the full spans
 #pragma unroll 1
     for (uint32_t todo = live; todo; todo &= todo - 1, q ^= 1) {
       const int i = __ffs(todo) - 1;
       CpAsyncWait1();
-      const unsigned long long p = ArgmaxBuffered(t0 + 1024 * i, Pick(m, i), lane, buf[q], &rd);
-      mine = p > mine ? p : mine;
+      packed = max(packed, ArgmaxBufferedPacked(1024 * i, Pick(m, i), lane, buf[q], &rd));
       if (pend) {
         const int j = __ffs(pend) - 1;
         pend &= pend - 1;
         SpanPrefetchAllowed(row, t0 + 1024 * j, Pick(m, j), lane, buf[q]);
       }
       CpAsyncCommit();
+    }
+    packed = __reduce_max_sync(0xffffffffu, packed);
+    if (packed != 0u) {
+      const int t = t0 + static_cast<int>(0xFFFFu - (packed & 0xFFFFu));
+      mine = (static_cast<unsigned long long>(Key32(packed >> 16)) << 32) |
+             static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(t));
     }
 #endif
 #pragma unroll 1
@@ -1945,11 +2063,15 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   if (MODE == kFillMask && F.logits != nullptr) {
     uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;
     if (eos_in_seg) {  // the EOS column carries bit V, not its (disabled) id's bit
+      // Branch-free selects (an `if` on i here made ptxas index m[] and move
+      // the whole array to local memory).
       const int wi = (Vv.eos_col - t0) >> 5;
-      const uint32_t bit = 1u << (Vv.eos_col & 31);
+      const uint32_t bit = lane == (wi & 31) ? 1u << (Vv.eos_col & 31) : 0u;
+      const uint32_t set = eos_bit ? bit : 0u, clr = eos_bit ? 0u : bit;
 #pragma unroll
       for (int i = 0; i < kSpans; ++i) {
-        if (i == (wi >> 5) && lane == (wi & 31)) m[i] = eos_bit ? (m[i] | bit) : (m[i] & ~bit);
+        const bool hit = i == (wi >> 5);
+        m[i] = (m[i] & ~(hit ? clr : 0u)) | (hit ? set : 0u);
       }
     }
     // Full spans by class: all allowed -> untouched; all masked -> one bulk
@@ -1957,17 +2079,12 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     // mixed -> 16-B chunks, two spans in flight: the mixed chunks of the next
     // two mixed spans are being copied (cp.async, no registers held) while
     // one is blended and stored.  Then a partial last span, if any.
-    const int nfull = F.vec_ok ? (tl1 - t0) >> 10 : 0;
-    uint32_t masked = 0u, mixed = 0u;
-#pragma unroll
-    for (int i = 0; i < kSpans; ++i) {
-      const unsigned nz = __ballot_sync(0xffffffffu, m[i] != 0u);
-      const unsigned nf = __ballot_sync(0xffffffffu, m[i] != 0xffffffffu);
-      if (i < nfull) {
-        if (!nz && PRE3_BULK_MASKED && ((PRE3_BULK_SPANS >> i) & 1)) masked |= 1u << i;
-        else if (nf) mixed |= 1u << i;  // (a masked span left to the LSU path: -inf chunk stores)
-      }
-    }
+#if PRE3_MIXED_RED || PRE3_COMPACT_MIXED
+    const bool late = true;
+#else
+    const bool late = !spans_early;
+#endif
+    if (late) classify();
     if (masked && lane == 0) {
       const unsigned long long pol = EvictFirstPolicy();
 #if PRE3_BULK_RUN > 1
@@ -1983,9 +2100,10 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       for (uint32_t x = masked; x; x &= x - 1) BulkStore(row + t0 + 1024 * (__ffs(x) - 1), ninf, 2048, pol);
 #endif
       BulkCommit();
-      wr += 2048ull * static_cast<unsigned>(__popc(masked));
+      wr += 2048u * static_cast<unsigned>(__popc(masked));
     }
 #if PRE3_COMPACT_MIXED
+    const unsigned long long t_mx = Bt.trace ? NowNs() : 0ull;
     // Mixed chunks of as many mixed spans as fit the warp's 256-chunk buffer,
     // packed in (span, round, lane) order, are all copied in ONE round trip
     // (cp.async: no registers held), then blended and stored span by span; a
@@ -2054,19 +2172,65 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       todo &= ~batch;
       __syncwarp();  // the buffer is refilled by the next batch
     }
+#elif PRE3_MIXED_RED
+    // Mixed spans blended in L2, nothing read back by the SM: per 32-B sector
+    // (two 16-B chunks), all masked -> bulk store of -inf, all allowed ->
+    // untouched, otherwise -> cp.reduce.async.bulk .min.bf16 from a pattern
+    // (masked token -inf, allowed token NaN, which min() ignores).  Each run
+    // of same-kind sectors is one op, issued by lane 0; two pattern buffers
+    // per warp, reused once the TMA engine has read them.
+    const unsigned long long t_mx = Bt.trace ? NowNs() : 0ull;
+    uint4* pbuf = &span_buf[0][0][0];  // [2][128] chunks of this warp
+    int q = 0;
+#pragma unroll 1
+    for (uint32_t todo = mixed; todo; todo &= todo - 1, q ^= 1) {
+      const int i = __ffs(todo) - 1;
+      uint16_t* span = row + t0 + 1024 * i;
+      uint32_t byte[4];
+      SpanBytes(Pick(m, i), lane, byte);
+      unsigned long long st_sec = 0ull, rd_sec = 0ull;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned msk = __ballot_sync(0xffffffffu, byte[k] == 0u);
+        const unsigned all = __ballot_sync(0xffffffffu, byte[k] == 0xffu);
+        const uint32_t sm = EvenBits(msk & (msk >> 1));  // both chunks masked
+        const uint32_t sa = EvenBits(all & (all >> 1));  // both chunks allowed
+        st_sec |= static_cast<unsigned long long>(sm) << (16 * k);
+        rd_sec |= static_cast<unsigned long long>(~(sm | sa) & 0xffffu) << (16 * k);
+      }
+#if PRE3_MIXED_RED == 2
+      st_sec = 0ull;  // (A/B) the whole span as one reduce op
+      rd_sec = ~0ull;
+#endif
+      if (lane == 0) BulkWaitRead1();  // buffer q's previous op group (maybe an earlier item's) has been read
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t x = byte[k];
+        uint4 o;
+        uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t keep = ((x >> (2 * j)) & 1u ? 0x0000FFFFu : 0u) | ((x >> (2 * j + 1)) & 1u ? 0xFFFF0000u : 0u);
+          po[j] = (0x7FFF7FFFu & keep) | (0xFF80FF80u & ~keep);
+        }
+        pbuf[q * 128 + 32 * k + lane] = o;
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // pattern visible to the bulk copies
+      __syncwarp();
+      if (lane == 0) {
+        const uint4* pat = pbuf + q * 128;
+        ForRuns(st_sec, [&](int s0, int len) { BulkStore(span + 16 * s0, ninf, 32 * len, EvictFirstPolicy()); });
+        ForRuns(rd_sec, [&](int s0, int len) { BulkReduceMinBf16(span + 16 * s0, pat + 2 * s0, 32 * len); });
+        BulkCommit();
+        rd += 32u * static_cast<unsigned>(__popcll(rd_sec));  // read (in L2) and written back
+        wr += 32u * static_cast<unsigned>(__popcll(rd_sec) + __popcll(st_sec));
+      }
+    }
 #else
     const unsigned long long t_mx = Bt.trace ? NowNs() : 0ull;
     uint4(*buf)[4][32] = span_buf;  // [2][4][32] of this warp
-    uint32_t pend = mixed;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (pend) {
-        const int i = __ffs(pend) - 1;
-        pend &= pend - 1;
-        SpanPrefetch(row, t0 + 1024 * i, Pick(m, i), lane, buf[q]);
-      }
-      CpAsyncCommit();
-    }
+    if (late) prefetch2();
     int q = 0;
 #pragma unroll 1
     for (uint32_t todo = mixed; todo; todo &= todo - 1, q ^= 1) {
@@ -2087,7 +2251,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     }
     if (Vv.layout && last_seg) TailColumns(Vv, row, eos_bit, lane, 32, &wr);
     const unsigned long long t_bw = Bt.trace ? NowNs() : 0ull;
-    if (masked && lane == 0) BulkWaitRead();  // the -inf source outlives the reads
+    if ((masked || (PRE3_MIXED_RED && mixed)) && lane == 0) BulkWaitRead();  // the smem sources outlive the reads
     if (Bt.trace && lane == 0) {
       TraceEvent(Bt, 15, b, seg, t_mx, static_cast<unsigned long long>(__popc(mixed)));  // l:mixed spans
       TraceEvent(Bt, 16, b, seg, t_bw, static_cast<unsigned long long>(__popc(masked)));  // l:bulk wait
@@ -2334,7 +2498,7 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
   __syncthreads();
   const int eos_bit = Vv.layout && (last_seg || eos_in_seg) ? sh.eos : 0;
   // Warp w covers words [32w, 32w+32) of the segment = one 1024-token span.
-  unsigned long long rd = 0, wr = 0;
+  unsigned rd = 0, wr = 0;  // this lane's logit bytes (stats)
   const int tw = t0 + warp * 1024;
   if (MODE == kFillGreedy) {
     const uint16_t* row = F.logits + static_cast<long long>(b) * F.ld;

@@ -26,6 +26,7 @@ p.add_argument("--slots", type=int, default=65536)
 p.add_argument("--parent", type=int, default=0)
 p.add_argument("--prewarm", type=int, default=10000)
 p.add_argument("--n", type=int, default=60)
+p.add_argument("--graph-first", type=int, default=0, help="replay a graph of N split steps before the measurements")
 a = p.parse_args()
 
 flat = bench.automaton_bytes(a.grammar)
@@ -103,6 +104,12 @@ def loop(fn, label, k=120):
     print(f"{label:44s} {1e3 * e0.elapsed_time(e1) / k:7.2f} us/step (host-enqueued)")
 
 
+if a.graph_first:
+    gf = batch.capture_steps(a.graph_first, seed=1, logits=[logits[i % R] for i in range(a.graph_first)], bitmask=bm,
+                             seg_counts=[counts] * a.graph_first, tokens_out=[toks] * a.graph_first)
+    gf.launch()
+    torch.cuda.synchronize()
+    bracket(split, "split: fill bracketed (right after the graph)")
 batch.set_stats(True)
 between(split, "split: events between steps")
 print("  stats", batch.fill_stats(), eng.cache_stats())
