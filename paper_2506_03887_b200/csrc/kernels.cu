@@ -2737,6 +2737,9 @@ struct SampleShared {
   unsigned int red[kThreads / 32 + 1];
   unsigned long long red64[kThreads / 32];
   int found;
+  int claim[256];                  // one-pass key counting: high byte -> kcnt row (-1: none yet, -2: being claimed)
+  short row_h[kSampleKeySlots];    // kcnt row -> high byte
+  int nclaim;
 };
 
 enum : int { kPassHi = 0, kPassWeights = 1, kPassLoBin = 2 };
@@ -2784,10 +2787,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   const int nchunks = (V1 + 7) >> 3;
   const uint32_t* mrow = S.bitmask + static_cast<long long>(b) * S.ldw;
   const uint16_t* row = S.logits + static_cast<long long>(b) * S.ld;
-  for (int i = tid; i < 256 * (kThreads / 32); i += kThreads) {
-    sh.u.pw.cnt_hi_w[i >> 8][i & 255] = 0u;
-    sh.u.pw.w_hi_w[i >> 8][i & 255] = 0ull;
-  }
+  for (int i = tid; i < kSampleKeySlots * 256; i += kThreads) sh.u.kcnt[i >> 8][i & 255] = 0u;
   for (int i = tid; i < 256; i += kThreads) {
     sh.cnt_hi[i] = 0u;
     sh.w_hi[i] = 0ull;
@@ -2795,12 +2795,30 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     sh.w_lo[i] = 0ull;
     sh.cnt_lo2[i] = 0u;
     sh.w_lo2[i] = 0ull;
+    sh.claim[i] = -1;
   }
+  if (tid < kSampleKeySlots) sh.row_h[tid] = -1;
+  if (tid == 0) sh.nclaim = 0;
   __syncthreads();
-  // ---- pass 1: high-byte counts, max key, |allowed|.
+  // ---- pass 1 (one-pass key counting): every allowed token's 16-bit key
+  // counted in kcnt, a row per high byte claimed on first sight; max key,
+  // |allowed|.  More high bytes than rows: the two-pass path below.
   unsigned int kmax = 0u, n_allowed = 0u;
   ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
-    atomicAdd(&sh.u.pw.cnt_hi_w[warp][key >> 8], 1u);
+    const int h = static_cast<int>(key >> 8);
+    int r = sh.claim[h];
+    if (r < 0) {
+      // -1 -> -2 (claiming) -> row id; a thread that loses the race waits for
+      // the winner's id (independent thread scheduling: the winner progresses).
+      if (atomicCAS(&sh.claim[h], -1, -2) == -1) {
+        r = atomicAdd(&sh.nclaim, 1);
+        atomicExch(&sh.claim[h], r);
+      } else {
+        while ((r = *reinterpret_cast<volatile int*>(&sh.claim[h])) < 0) {
+        }
+      }
+    }
+    if (r < kSampleKeySlots) atomicAdd(&sh.u.kcnt[r][key & 0xffu], 1u);
     kmax = key > kmax ? key : kmax;
     ++n_allowed;
   });
@@ -2808,11 +2826,33 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   n_allowed = __reduce_add_sync(0xffffffffu, n_allowed);
   if (lane == 0) sh.red[warp] = kmax;
   __syncthreads();
-  for (int i = tid; i < 256; i += kThreads) {
-    unsigned int c = 0u;
+  const bool one_pass = sh.nclaim <= kSampleKeySlots;
+  if (one_pass) {
+    // Row -> high byte, then the high-byte counts from the rows.
+    if (sh.claim[tid] >= 0) sh.row_h[sh.claim[tid]] = static_cast<short>(tid);
+    __syncthreads();
+    for (int r = 0; r < sh.nclaim; ++r) {
+      unsigned int c = sh.u.kcnt[r][tid];
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (lane == 0 && c) atomicAdd(&sh.cnt_hi[sh.row_h[r]], c);
+    }
+  } else {
+    // Two-pass path: per-warp high-byte histograms (a bf16 logit's sign +
+    // exponent byte takes few values: one shared copy would serialize).
+    for (int i = tid; i < 256 * (kThreads / 32); i += kThreads) {
+      sh.u.pw.cnt_hi_w[i >> 8][i & 255] = 0u;
+      sh.u.pw.w_hi_w[i >> 8][i & 255] = 0ull;
+    }
+    __syncthreads();
+    ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads,
+               [&](int, uint32_t key) { atomicAdd(&sh.u.pw.cnt_hi_w[warp][key >> 8], 1u); });
+    __syncthreads();
+    for (int i = tid; i < 256; i += kThreads) {
+      unsigned int c = 0u;
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) c += sh.u.pw.cnt_hi_w[w][i];
-    sh.cnt_hi[i] = c;
+      for (int w = 0; w < kThreads / 32; ++w) c += sh.u.pw.cnt_hi_w[w][i];
+      sh.cnt_hi[i] = c;
+    }
   }
   if (tid == 0) {
     unsigned int m = 0u;
@@ -2850,8 +2890,21 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     }
     // ---- pass 2: weights per high bin above hi_k; counts + weights per low
     // byte inside hi_k.  Key-count mode: dense rows whose high bytes above
-    // hi_k fit kSampleKeySlots rows of kcnt.
-    if (tid == 0) {
+    // hi_k fit kSampleKeySlots rows of kcnt.  After a one-pass count every
+    // key's count is on chip already: no pass over the row.
+    if (one_pass) {
+      if (tid == 0) sh.nslots = sh.nclaim;
+      for (int h = tid; h < 256; h += kThreads) sh.hslot[h] = static_cast<signed char>(sh.claim[h]);
+      for (int r = tid; r < kSampleKeySlots; r += kThreads) sh.slot_h[r] = static_cast<unsigned char>(sh.row_h[r] < 0 ? 0 : sh.row_h[r]);
+      if (hi_k >= 0) {
+        const uint32_t c = sh.u.kcnt[sh.claim[hi_k]][tid];
+        sh.cnt_lo[tid] = c;
+        sh.w_lo[tid] = c ? static_cast<unsigned long long>(c) *
+                               SampleWeight((static_cast<uint32_t>(hi_k) << 8) | tid, vmax, S.temperature)
+                         : 0ull;
+      }
+      __syncthreads();
+    } else if (tid == 0) {
       int n = 0;
       for (int h = 0; h < 256; ++h) {
         const bool act = h > hi_k && sh.cnt_hi[h] > 0u;
@@ -2865,24 +2918,29 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     }
     __syncthreads();
     const int nslots = sh.nslots;
-    if (nslots >= 0) {
-      for (int i = tid; i < kSampleKeySlots * 256; i += kThreads) sh.u.kcnt[i >> 8][i & 255] = 0u;
+    if (!one_pass) {
+      if (nslots >= 0) {
+        for (int i = tid; i < kSampleKeySlots * 256; i += kThreads) sh.u.kcnt[i >> 8][i & 255] = 0u;
+        __syncthreads();
+      }
+      ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+        const int h = static_cast<int>(key >> 8);
+        if (h > hi_k) {
+          if (nslots >= 0) atomicAdd(&sh.u.kcnt[sh.hslot[h]][key & 0xffu], 1u);
+          else atomicAdd(&sh.u.pw.w_hi_w[warp][h], SampleWeight(key, vmax, S.temperature));
+        } else if (h == hi_k) {
+          atomicAdd(&sh.cnt_lo[key & 0xffu], 1u);
+          atomicAdd(&sh.w_lo[key & 0xffu], SampleWeight(key, vmax, S.temperature));
+        }
+      });
       __syncthreads();
     }
-    ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
-      const int h = static_cast<int>(key >> 8);
-      if (h > hi_k) {
-        if (nslots >= 0) atomicAdd(&sh.u.kcnt[sh.hslot[h]][key & 0xffu], 1u);
-        else atomicAdd(&sh.u.pw.w_hi_w[warp][h], SampleWeight(key, vmax, S.temperature));
-      } else if (h == hi_k) {
-        atomicAdd(&sh.cnt_lo[key & 0xffu], 1u);
-        atomicAdd(&sh.w_lo[key & 0xffu], SampleWeight(key, vmax, S.temperature));
-      }
-    });
-    __syncthreads();
     if (nslots >= 0) {
-      // Thread t = low byte t: weigh each (high byte, t) key once.
+      // Thread t = low byte t: weigh each (high byte, t) key once (bins above
+      // hi_k; after a one-pass count every bin has a row — the others' sums
+      // are never read).
       for (int sl = 0; sl < nslots; ++sl) {
+        if (one_pass && (sh.row_h[sl] < 0 || sh.row_h[sl] <= hi_k)) continue;
         const uint32_t c = sh.u.kcnt[sl][tid];
         unsigned long long w =
             c ? static_cast<unsigned long long>(c) * SampleWeight((static_cast<uint32_t>(sh.slot_h[sl]) << 8) | tid,
