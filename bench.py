@@ -90,7 +90,7 @@ def parse(argv=None):
     p.add_argument("--one-launch", action="store_true", help="stream mode: the one-launch fused step")
     p.add_argument("--no-graph", action="store_true",
                    help="enqueue every step from Python instead of replaying a captured CUDA graph")
-    p.add_argument("--fill-samples", type=int, default=24,
+    p.add_argument("--fill-samples", type=int, default=120,
                    help="steps of the roofline sub-loop (the fill kernel bracketed by events every step)")
     p.add_argument("--latency-samples", type=int, default=64,
                    help="steps of the latency sub-loop (events between steps: per-step latency p50/p99)")
@@ -511,20 +511,6 @@ def main(argv=None):
     for i in range(Wm):
         step(i)
     batch.check()
-    if os.environ.get("PRE3_DIAG_FILL_FIRST"):  # diagnostics: the roofline sub-loop before the timed loop too
-        fe = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(40)]
-        for pair in fe:
-            for e_ in pair:
-                e_.record(stream)
-        torch.cuda.synchronize()
-        for i in range(40):
-            batch.time_next_fill(*fe[i])
-            step(Wm + i)
-        torch.cuda.synchronize()
-        print("diag fill-first:", summarize([1e3 * a_.elapsed_time(b_) for a_, b_ in fe]), file=sys.stderr)
-        for i in range(40, 42):  # back to a multiple of 6 eager steps past the warm-up
-            step(Wm + i)
-        Wm += 42
     # The timed steps as one captured CUDA graph (gm_decode_graph_create; a
     # multiple of 6 steps, the rest enqueued eagerly): one host call launches
     # them, with every step's own buffers baked in.
