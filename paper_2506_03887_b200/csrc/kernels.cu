@@ -50,6 +50,9 @@
 #ifndef PRE3_SPAN_READ_ALL
 #define PRE3_SPAN_READ_ALL 0  // (A/B) mixed spans: every chunk not all-allowed is read, not just the mixed ones
 #endif
+#ifndef PRE3_GREEDY_VMAX
+#define PRE3_GREEDY_VMAX 0  // (A/B, measured slower: 42 vs 37 us) greedy light pass: SIMD halfword max per chunk + one chunk re-read for the id
+#endif
 #ifndef PRE3_BULK_MASKED
 #define PRE3_BULK_MASKED 1  // fully masked spans as one bulk (TMA) store
 #endif
@@ -1561,6 +1564,14 @@ __device__ __forceinline__ unsigned long long ArgmaxBuffered(int tw, uint32_t mw
   return mine;
 }
 
+// The two 16-bit order keys of the bf16 pair w (low half = lower token):
+// h ^ 0xFFFF for a negative value, h ^ 0x8000 otherwise (PRMT replicates
+// each half's sign bit over the half).
+__device__ __forceinline__ uint32_t PairOrderKeys(uint32_t w) {
+  const uint32_t sgn = __byte_perm(w, 0u, 0xBB99u);
+  return w ^ (sgn | 0x80008000u);
+}
+
 // ArgmaxBuffered in 32-bit packed form: (16-bit order key << 16) |
 // (0xFFFF - token offset in the segment), 0 when no allowed token — one max
 // per token instead of 64-bit keys (an allowed key-0 token, bf16 0xFFFF, still
@@ -2014,6 +2025,73 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       CpAsyncCommit();
     }
     int q = 0;
+#if PRE3_GREEDY_VMAX
+    // Per chunk: the 8 tokens' 16-bit order keys two at a time (masked -> 0
+    // through a per-CTA keep-mask table), their max by SIMD halfword max, and
+    // the lane's running best key with the chunk where it first appeared.
+    // The lowest id holding the warp's best key is then found by re-reading
+    // that one chunk (in L2).  An item whose allowed tokens are all key 0
+    // (bf16 0xFFFF) takes its lowest allowed id.
+    const uint4* keep_lut = ninf;  // greedy: the CTA's keep-mask table (FillKernel)
+    uint32_t lbest = 0u, lbyte = 0u;
+    int lwhere = -1;
+#pragma unroll 1
+    for (uint32_t todo = live; todo; todo &= todo - 1, q ^= 1) {
+      const int i = __ffs(todo) - 1;
+      CpAsyncWait1();
+      uint32_t byte[4];
+      SpanBytes(Pick(m, i), lane, byte);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!byte[k]) continue;
+        const uint4 v = buf[q][k][lane];
+        const uint4 kp = keep_lut[byte[k]];
+        const uint32_t k0 = PairOrderKeys(v.x) & kp.x, k1 = PairOrderKeys(v.y) & kp.y;
+        const uint32_t k2 = PairOrderKeys(v.z) & kp.z, k3 = PairOrderKeys(v.w) & kp.w;
+        const uint32_t m2 = __vmaxu2(__vmaxu2(k0, k1), __vmaxu2(k2, k3));
+        const uint32_t ck = max(m2 & 0xFFFFu, m2 >> 16);
+        if (ck > lbest) {
+          lbest = ck;
+          lwhere = 4 * i + k;
+          lbyte = byte[k];
+        }
+        rd += 16;
+      }
+      if (pend) {
+        const int j = __ffs(pend) - 1;
+        pend &= pend - 1;
+        SpanPrefetchAllowed(row, t0 + 1024 * j, Pick(m, j), lane, buf[q]);
+      }
+      CpAsyncCommit();
+    }
+    const uint32_t kbest = __reduce_max_sync(0xffffffffu, lbest);
+    if (live) {
+      uint32_t tcand = 0xFFFFFFFFu;
+      if (kbest != 0u) {
+        if (lbest == kbest) {
+          const int i = lwhere >> 2, k = lwhere & 3;
+          const int tb = t0 + 1024 * i + (32 * k + lane) * 8;
+          const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + tb));
+          const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 7; j >= 0; --j) {  // the lowest j holding kbest wins
+            const uint32_t kj = (PairOrderKeys(w4[j >> 1]) >> ((j & 1) * 16)) & 0xFFFFu;
+            if (((lbyte >> j) & 1u) && kj == kbest) tcand = static_cast<uint32_t>(tb + j);
+          }
+        }
+      } else {  // every allowed key is 0: the lowest allowed id of the full spans
+        const int i0 = __ffs(live) - 1;
+        const uint32_t mw = Pick(m, i0);
+        const unsigned nzl = __ballot_sync(0xffffffffu, mw != 0u);
+        const int src = __ffs(nzl) - 1;
+        const uint32_t w = __shfl_sync(0xffffffffu, mw, src);
+        tcand = static_cast<uint32_t>(t0 + 1024 * i0 + 32 * src + __ffs(w) - 1);
+      }
+      const uint32_t tmin = __reduce_min_sync(0xffffffffu, tcand);
+      mine = (static_cast<unsigned long long>(Key32(kbest)) << 32) |
+             static_cast<unsigned long long>(0xFFFFFFFFu - tmin);
+    }
+#else
     uint32_t packed = 0u;  // ArgmaxBufferedPacked over the full spans
 #pragma unroll 1
     for (uint32_t todo = live; todo; todo &= todo - 1, q ^= 1) {
@@ -2033,6 +2111,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       mine = (static_cast<unsigned long long>(Key32(packed >> 16)) << 32) |
              static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(t));
     }
+#endif
 #endif
 #pragma unroll 1
     for (int i = nfull; i < kSpans; ++i) {
@@ -2312,6 +2391,8 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
   __shared__ FillShared sh;
   __shared__ uint4 span_buf[kWarps][2][4][32];  // light pass: per-warp double buffer of mixed chunks (32 KB)
   __shared__ __align__(128) uint4 ninf_buf[128 * PRE3_BULK_RUN];  // bf16 -inf: the bulk-store source
+  // Greedy: chunk mask byte -> the four pairs' halfword keep masks.
+  __shared__ uint4 keep_lut[MODE == kFillGreedy ? 256 : 1];
   extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -2340,6 +2421,15 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
       }
       __syncthreads();
     }
+    if (MODE == kFillGreedy) {
+      for (int x = tid; x < 256; x += kThreads) {
+        uint32_t kp[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) kp[j] = ((x >> (2 * j)) & 1 ? 0x0000FFFFu : 0u) | ((x >> (2 * j + 1)) & 1 ? 0xFFFF0000u : 0u);
+        keep_lut[x & (MODE == kFillGreedy ? 255 : 0)] = make_uint4(kp[0], kp[1], kp[2], kp[3]);
+      }
+      __syncthreads();
+    }
     const int item = (bid - Bt.h_grid) * kWarps + warp;
     const bool in_range = item < Bt.B * Vv.nseg;
     const int b = in_range ? item / Vv.nseg : 0;
@@ -2361,7 +2451,8 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
     // row, the counts are the slot's (and with publish_arrival 2 nobody
     // waits for this sequence's items).
     const bool pure = hmask == 0u && slot >= 0 && slot < Cc.C && Vv.nseg <= 32;
-    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, lane, span_buf[warp], ninf_buf);
+    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, lane, span_buf[warp],
+                          MODE == kFillGreedy ? keep_lut : ninf_buf);
     return;
   }
 

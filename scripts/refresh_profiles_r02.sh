@@ -27,7 +27,7 @@ for c in 2 3 4 5; do
   python scripts/launches.py $Q/c${c}_launches.csv > $P/r02_c${c}_launches_summary.txt
   summ $Q/c${c}_fill.ncu-rep > $P/r02_c${c}_fill_summary.txt
 done
-summ $Q/c2_accept.ncu-rep > $P/r02_c2_accept_summary.txt
+[ -f $Q/c2_accept.ncu-rep ] && summ $Q/c2_accept.ncu-rep > $P/r02_c2_accept_summary.txt
 summ $Q/sample.ncu-rep > $P/r02_sample_summary.txt
 cp $Q/c3_fill.ncu-rep $P/r02_c3_fill.ncu-rep
 python - <<'PY'
@@ -46,7 +46,9 @@ src = "ncu --set full, one steady-state launch (profiles/r02_c%d_fill_summary.tx
 t["json:128255:256:stream:separate"].update(dram_bytes_per_launch=dram(Q + "/c2_fill.ncu-rep"), source=src % 2)
 t["schema:128255:1024:stream:separate"].update(dram_bytes_per_launch=dram(Q + "/c3_fill.ncu-rep"), source=src % 3)
 t["sql:128255:4096:stream:separate"].update(dram_bytes_per_launch=dram(Q + "/c4_fill.ncu-rep"), source=src % 4)
-t["json:128255:512:greedy:fused"].update(dram_bytes_per_launch=dram(Q + "/c5_fill.ncu-rep"), source=src % 5)
+g = t.pop("json:128255:512:greedy:fused", {})
+g.update(dram_bytes_per_launch=dram(Q + "/c5_fill.ncu-rep"), source=src % 5)
+t["json:128255:512:greedy:separate"] = g
 json.dump(t, open("profiles/traffic.json", "w"), indent=1)
 print(t)
 PY
