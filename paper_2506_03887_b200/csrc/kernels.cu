@@ -53,6 +53,20 @@
 #ifndef PRE3_GREEDY_VMAX
 #define PRE3_GREEDY_VMAX 0  // (A/B, measured slower: 42 vs 37 us) greedy light pass: SIMD halfword max per chunk + one chunk re-read for the id
 #endif
+// Register caps (A/B): a fill at 64 registers x 4 CTAs fills the register
+// file, so no accept CTA can be resident beside it until fill CTAs retire.
+#ifndef PRE3_FILL_BOUNDS
+#define PRE3_FILL_BOUNDS __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS)
+#endif
+#ifndef PRE3_ACCEPT_BOUNDS
+#define PRE3_ACCEPT_BOUNDS __launch_bounds__(128)
+#endif
+#ifndef PRE3_LIGHT_PER_CTA
+#define PRE3_LIGHT_PER_CTA 0  // light items per fill CTA (0: chosen per launch, LightPerCta)
+#endif
+#ifndef PRE3_FILL_SMEM_PAD
+#define PRE3_FILL_SMEM_PAD 0  // (A/B) extra dynamic shared memory per fill CTA: fewer fill CTAs per SM
+#endif
 #ifndef PRE3_BULK_MASKED
 #define PRE3_BULK_MASKED 1  // fully masked spans as one bulk (TMA) store
 #endif
@@ -873,17 +887,25 @@ __device__ void HelpSegment(const AutView& A, const VocabView& Vv, const CacheVi
 // the context lookup.
 // ---------------------------------------------------------------------------
 // Synthetic stream; identical rule in oracle/gmask_port.c.
+// Segment s's mask words and counts come from (row, counts) when bit s of
+// `hm` is set, else from (crow, ccounts) — a sequence's context CI row and
+// the slot's counts, equal to what the fill writes for its segments without
+// context-dependent tokens (hm = ~0: everything from row/counts; segments >=
+// 32 always are).
 __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row, const int32_t* counts,
+                                const uint32_t* crow, const int32_t* ccounts, uint32_t hm,
                                 unsigned long long seed, uint32_t draw, int lane) {
   // Round trip 1: the per-segment counts (segments 0..31 stay in registers)
   // and the EOS word.
   int c_all = 0, c_str = 0;
   if (lane < Vv.nseg) {
-    const int2 v = __ldcg(reinterpret_cast<const int2*>(counts) + lane);
+    const int32_t* src = ((hm >> lane) & 1u) ? counts : ccounts;
+    const int2 v = __ldcg(reinterpret_cast<const int2*>(src) + lane);
     c_all = v.x;
     c_str = v.y;
   }
-  const uint32_t eos_word = __ldcg(row + (Vv.V >> 5));
+  const int eos_seg = (Vv.V >> 5) / kSegWords;
+  const uint32_t eos_word = __ldcg((eos_seg >= 32 || ((hm >> eos_seg) & 1u) ? row : crow) + (Vv.V >> 5));
   int na = c_all, ns = c_str;
   for (int s = lane + 32; s < Vv.nseg; s += 32) {
     na += __ldcg(counts + 2 * s);
@@ -923,6 +945,7 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
   // counts finds the lane, which finds the word and bit alone.
   const int w0 = seg * kSegWords;
   const int w1 = min(Vv.W, w0 + kSegWords);
+  const uint32_t* wsrc = (seg >= 32 || ((hm >> seg) & 1u)) ? row : crow;
   uint32_t xs[kSegWords / 32];
   int c = 0;
 #pragma unroll
@@ -930,7 +953,7 @@ __device__ int SampleStreamWarp(const VocabView& Vv, int b, const uint32_t* row,
     const int w = w0 + lane * (kSegWords / 32) + j;
     uint32_t x = 0;
     if (w < w1) {
-      x = __ldcg(row + w);
+      x = __ldcg(wsrc + w);
       if (w == (Vv.V >> 5)) x &= ~(1u << (Vv.V & 31));
       if (use_s) x &= __ldg(Vv.structural + w);
     }
@@ -1697,8 +1720,9 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
     tok = p ? static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(p)) : -1;
     if (lane == 0) F.best[b] = 0ull;
   } else {
-    tok = SampleStreamWarp(Vv, b, F.bitmask + static_cast<long long>(b) * F.ldw,
-                           F.seg_counts + static_cast<long long>(b) * Vv.nseg * 2, F.seed, st.draws, lane);
+    const uint32_t* brow = F.bitmask + static_cast<long long>(b) * F.ldw;
+    const int32_t* bcnt = F.seg_counts + static_cast<long long>(b) * Vv.nseg * 2;
+    tok = SampleStreamWarp(Vv, b, brow, bcnt, brow, bcnt, ~0u, F.seed, st.draws, lane);
     st.draws += 1;
     if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
   }
@@ -1716,7 +1740,8 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
 template <int MODE, int TAIL>
 __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                           const BatchView& Bt, const FillArgs& F, int b, int seg, int slot,
-                                          bool pure, int lane, uint4 (*span_buf)[4][32], const uint4* ninf) {
+                                          bool pure, bool publish, int lane, uint4 (*span_buf)[4][32],
+                                          const uint4* ninf) {
   const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   const int w0 = seg * kSegWords;
   const int nwords = min(Vv.W - w0, kSegWords);
@@ -2132,7 +2157,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   // ---- arrival (fused tail): mask words, counts and argmax partials are
   // made visible first; the bulk logits stores follow.
   bool last = false;
-  if (TAIL != kTailNone || F.publish_arrival == 1 || (F.publish_arrival == 2 && !pure)) {
+  if (TAIL != kTailNone || F.publish_arrival == 1 || (F.publish_arrival == 2 && publish)) {
     __threadfence();
     __syncwarp();
     int l = 0;
@@ -2385,7 +2410,7 @@ struct FillShared {
 // Every CTA first helps drain the build queue of new contexts (empty in the
 // steady state).
 template <int MODE, int TAIL>
-__global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+__global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                           FillArgs F) {
   PdlEnter();
   __shared__ FillShared sh;
@@ -2430,8 +2455,8 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
       }
       __syncthreads();
     }
-    const int item = (bid - Bt.h_grid) * kWarps + warp;
-    const bool in_range = item < Bt.B * Vv.nseg;
+    const int item = (bid - Bt.h_grid) * F.light_per_cta + warp;
+    const bool in_range = warp < F.light_per_cta && item < Bt.B * Vv.nseg;
     const int b = in_range ? item / Vv.nseg : 0;
     const int seg = item - b * Vv.nseg;
     int hi = -1, slot = -2;
@@ -2450,8 +2475,13 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
     // Pure CI: a built shared slot and no heavy segment — the mask is the CI
     // row, the counts are the slot's (and with publish_arrival 2 nobody
     // waits for this sequence's items).
-    const bool pure = hmask == 0u && slot >= 0 && slot < Cc.C && Vv.nseg <= 32;
-    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, lane, span_buf[warp],
+    const bool shared_ok = slot >= 0 && slot < Cc.C && Vv.nseg <= 32;
+    const bool pure = shared_ok && hmask == 0u;
+    // Split step (publish_arrival 2): only the items of a sequence's heavy
+    // segments publish arrivals — its accept takes the other segments from the
+    // slot's CI row (AcceptKernel's ci_shortcut, the same test).
+    const bool publish = !shared_ok || ((hmask >> seg) & 1u);
+    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, publish, lane, span_buf[warp],
                           MODE == kFillGreedy ? keep_lut : ninf_buf);
     return;
   }
@@ -2650,11 +2680,11 @@ __global__ void __launch_bounds__(kThreads, PRE3_FILL_MIN_BLOCKS) FillKernel(Aut
 template <int SAMPLE>
 __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                            const BatchView& Bt, const AcceptArgs& G, int b, SeqState st, int topv,
-                                           const uint32_t* row, const int32_t* counts, int lane,
-                                           unsigned long long t_in);
+                                           const uint32_t* row, const int32_t* counts, const uint32_t* crow,
+                                           const int32_t* ccounts, uint32_t hm, int lane, unsigned long long t_in);
 
 template <int SAMPLE>
-__global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
+__global__ void PRE3_ACCEPT_BOUNDS AcceptKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
                                                     AcceptArgs G) {
   // wait_fill: the preceding fill (launched just before, publishing
   // per-sequence arrivals) may still be running — each warp starts as soon as
@@ -2674,34 +2704,42 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
     const int topv = StackWindow(Bt, b, st.depth, lane);
     const uint32_t* row = G.bitmask + static_cast<long long>(b) * G.ldw;
     const int32_t* counts = G.seg_counts + static_cast<long long>(b) * Vv.nseg * 2;
-    bool pure = false;
+    const uint32_t* crow = row;
+    const int32_t* ccounts = counts;
+    uint32_t hm = ~0u;  // segments read from the fill's outputs (the rest: the context's CI row)
+    int need = Vv.nseg;
     if (G.ci_shortcut) {
-      // Pure CI (the fill's own test, LightItem): its bitmask row is the
-      // slot's CI row and its counts the slot's — sample from those now.
+      // A built shared slot (the fill's own test, FillKernel): the segments
+      // without context-dependent tokens are the slot's CI row and counts —
+      // sample from those now; wait only for the heavy segments' items (the
+      // only ones that publish arrivals).  Pure CI: no wait at all.
       const int slot = SeqSlot(Bt, PrevFill(G.lookup_tag))[b];
-      const uint32_t hm = SeqHmask(Bt, PrevFill(G.lookup_tag))[b];
-      pure = hm == 0u && slot >= 0 && slot < Cc.C && Vv.nseg <= 32;
-      if (pure) {
-        row = Cc.ci + static_cast<long long>(slot) * Vv.W;
-        counts = Cc.ci_cnt + static_cast<long long>(slot) * Vv.nseg * 2;
+      const uint32_t hmask = SeqHmask(Bt, PrevFill(G.lookup_tag))[b];
+      if (slot >= 0 && slot < Cc.C && Vv.nseg <= 32) {
+        const uint32_t all = Vv.nseg >= 32 ? 0xffffffffu : ((1u << Vv.nseg) - 1u);
+        hm = hmask & all;
+        need = __popc(hm);
+        crow = Cc.ci + static_cast<long long>(slot) * Vv.W;
+        ccounts = Cc.ci_cnt + static_cast<long long>(slot) * Vv.nseg * 2;
       }
     }
-    if (G.wait_fill && !pure) {
+    if (G.wait_fill && need > 0) {
       // Bounded (200 ms): a fill that never delivers the items would be an
       // internal error — reported through gm_batch_check, never a hung GPU.
-      if (LoadAcquire(Bt.seq_arrive + b) < Vv.nseg) {
+      if (LoadAcquire(Bt.seq_arrive + b) < need) {
         unsigned long long t_start, t_now;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         do {
           __nanosleep(64);
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
-        } while (LoadAcquire(Bt.seq_arrive + b) < Vv.nseg && t_now - t_start < 200000000ull);
+        } while (LoadAcquire(Bt.seq_arrive + b) < need && t_now - t_start < 200000000ull);
         if (t_now - t_start >= 200000000ull && lane == 0) atomicOr(Bt.err, 2u);
       }
       __syncwarp();
       if (lane == 0) Bt.seq_arrive[b] = 0;
     }
-    AcceptBody<SAMPLE>(A, Vv, Cc, Bt, G, b, st, topv, row, counts, lane, Bt.trace ? NowNs() : 0ull);
+    AcceptBody<SAMPLE>(A, Vv, Cc, Bt, G, b, st, topv, row, counts, crow, ccounts, hm, lane,
+                       Bt.trace ? NowNs() : 0ull);
   }
   if (G.wait_fill) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
@@ -2709,8 +2747,8 @@ __global__ void __launch_bounds__(128) AcceptKernel(AutView A, VocabView Vv, Cac
 template <int SAMPLE>
 __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                            const BatchView& Bt, const AcceptArgs& G, int b, SeqState st, int topv,
-                                           const uint32_t* row, const int32_t* counts, int lane,
-                                           unsigned long long t_in) {
+                                           const uint32_t* row, const int32_t* counts, const uint32_t* crow,
+                                           const int32_t* ccounts, uint32_t hm, int lane, unsigned long long t_in) {
   int tok = -1;
   if (SAMPLE == kSampleGiven) {
     tok = IdToBit(Vv, G.tokens[b]);
@@ -2720,7 +2758,7 @@ __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv
     __syncwarp();
     if (lane == 0) G.best[b] = 0ull;
   } else {
-    tok = SampleStreamWarp(Vv, b, row, counts, G.seed, st.draws, lane);
+    tok = SampleStreamWarp(Vv, b, row, counts, crow, ccounts, hm, G.seed, st.draws, lane);
     st.draws += 1;
     if (lane == 0) atomicAdd(Bt.counters + 1, 1ull);
   }
@@ -3480,6 +3518,15 @@ cudaError_t LaunchDrain(const AutView& a, const VocabView& v, const CacheView& c
   return Launch(DrainKernel, dim3(b.build_grid), dim3(kThreads), dyn, s, a, v, c, b, queue);
 }
 
+// Light items per CTA (<= 8 warps).  Measured: 7 per CTA for config 2's
+// 4,096 items (586 CTAs: every SM holds 4, 28 items each) slows the step
+// 32.6 -> 37.4 us against 8 (512 CTAs): the slots left free host accept CTAs
+// while the fill runs.
+static int LightPerCta(unsigned items) {
+  (void)items;
+  return PRE3_LIGHT_PER_CTA > 0 ? PRE3_LIGHT_PER_CTA : kWarps;
+}
+
 template <int MODE, int TAIL>
 static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c, const BatchView& b,
                         const FillArgs& f, size_t dyn, cudaStream_t s) {
@@ -3491,15 +3538,17 @@ static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c
     opted = dyn;
   }
   const unsigned items = static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
-  const unsigned grid = static_cast<unsigned>(b.h_grid) + (items + kWarps - 1) / kWarps;
-  Launch(FillKernel<MODE, TAIL>, dim3(grid), dim3(kThreads), dyn, s, a, v, c, b, f);
+  FillArgs g = f;
+  g.light_per_cta = LightPerCta(items);
+  const unsigned grid = static_cast<unsigned>(b.h_grid) + (items + g.light_per_cta - 1) / g.light_per_cta;
+  Launch(FillKernel<MODE, TAIL>, dim3(grid), dim3(kThreads), dyn, s, a, v, c, b, g);
 }
 
 cudaError_t LaunchFill(int mode, int tail, const AutView& a, const VocabView& v, const CacheView& c,
                        const BatchView& b, FillArgs f, cudaStream_t s) {
   if (b.B == 0) return cudaSuccess;
   f.vec_ok = f.logits != nullptr && (f.ld % 8) == 0 && (reinterpret_cast<uintptr_t>(f.logits) % 16) == 0;
-  const size_t dyn = static_cast<size_t>(b.cap > kMaxContext ? b.cap : kMaxContext) * sizeof(int32_t);
+  const size_t dyn = static_cast<size_t>(b.cap > kMaxContext ? b.cap : kMaxContext) * sizeof(int32_t) + PRE3_FILL_SMEM_PAD;
   if (mode == kFillGreedy) {
     if (tail == kTailGreedy) {
       LaunchFillT<kFillGreedy, kTailGreedy>(a, v, c, b, f, dyn, s);

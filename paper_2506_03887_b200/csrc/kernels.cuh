@@ -171,9 +171,11 @@ struct FillArgs {
   int fill_no;              // this fill's number (heavy_index tags; the tail tags fill_no + 1)
   int publish_arrival;      // no tail: still count finished items per sequence (seq_arrive) so a
                             // following AcceptKernel with wait_fill can start per sequence;
-                            // 2: only sequences that are not pure CI (seq_hmask != 0; the
-                            // accept's ci_shortcut skips the others)
+                            // 2: only the items of a sequence's heavy segments (the accept's
+                            // ci_shortcut takes the other segments from the slot's CI row)
   int vec_ok;               // set by LaunchFill
+  int light_per_cta;        // light items per CTA (<= kThreads/32; set by LaunchFill so the
+                            // light CTAs fill whole waves of the SMs' CTA slots)
 };
 
 struct AcceptArgs {
