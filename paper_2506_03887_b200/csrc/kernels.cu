@@ -67,6 +67,9 @@
 #ifndef PRE3_FILL_SMEM_PAD
 #define PRE3_FILL_SMEM_PAD 0  // (A/B) extra dynamic shared memory per fill CTA: fewer fill CTAs per SM
 #endif
+#ifndef PRE3_SAMPLE_BATCH
+#define PRE3_SAMPLE_BATCH 2  // sampler pass 1: chunks whose loads are issued together per thread
+#endif
 #ifndef PRE3_BULK_MASKED
 #define PRE3_BULK_MASKED 1  // fully masked spans as one bulk (TMA) store
 #endif
@@ -2899,6 +2902,83 @@ __device__ __forceinline__ void ForAllowed(const uint32_t* mrow, const uint16_t*
   }
 }
 
+// ForAllowed with U chunks' mask bytes, then their logit loads, issued
+// together (one dependent round trip per U chunks instead of per chunk).
+template <int U, typename Fn>
+__device__ __forceinline__ void ForAllowedBatched(const uint32_t* mrow, const uint16_t* row, int V, int eos_col,
+                                                  bool vec_ok, int c_begin, int c_end, int c_step, Fn&& fn) {
+  for (int c0 = c_begin; c0 < c_end; c0 += U * c_step) {
+    uint32_t byte[U];
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u * c_step;
+      byte[u] = c < c_end ? (__ldg(mrow + (c >> 2)) >> ((c & 3) * 8)) & 0xffu : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tb = (c0 + u * c_step) * 8;
+      q[u] = byte[u] && vec_ok && tb + 8 <= V ? __ldcg(reinterpret_cast<const uint4*>(row + tb)) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!byte[u]) continue;
+      const int tb = (c0 + u * c_step) * 8;
+      if (vec_ok && tb + 8 <= V) {
+        const uint32_t w4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if ((byte[u] >> j) & 1u) fn(tb + j, SampleKey((w4[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu));
+        }
+      } else {
+        for (int j = 0; j < 8 && tb + j <= V; ++j) {
+          if ((byte[u] >> j) & 1u) fn(tb + j, SampleKey(row[tb + j == V ? eos_col : tb + j]));
+        }
+      }
+    }
+  }
+}
+
+// The 16-bit keys of the allowed tokens of chunks [c_begin, c_end) equal to
+// `kappa`, in id order: fn(t) per match.  Four chunks' mask bytes, then their
+// logit loads, are issued together (pass 5 walks a contiguous chunk range per
+// thread; one load at a time made it a chain of ~60 dependent round trips).
+template <typename Fn>
+__device__ __forceinline__ void ForKeyMatches(const uint32_t* mrow, const uint16_t* row, int V, int eos_col,
+                                              bool vec_ok, int c_begin, int c_end, uint32_t kappa, Fn&& fn) {
+  constexpr int U = 4;
+  for (int c0 = c_begin; c0 < c_end; c0 += U) {
+    uint32_t byte[U];
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + u;
+      byte[u] = c < c_end ? (__ldg(mrow + (c >> 2)) >> ((c & 3) * 8)) & 0xffu : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tb = (c0 + u) * 8;
+      q[u] = byte[u] && vec_ok && tb + 8 <= V ? __ldcg(reinterpret_cast<const uint4*>(row + tb)) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!byte[u]) continue;
+      const int tb = (c0 + u) * 8;
+      if (vec_ok && tb + 8 <= V) {
+        const uint32_t w4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (((byte[u] >> j) & 1u) && SampleKey((w4[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) == kappa) fn(tb + j);
+        }
+      } else {
+        for (int j = 0; j < 8 && tb + j <= V; ++j) {
+          if (((byte[u] >> j) & 1u) && SampleKey(row[tb + j == V ? eos_col : tb + j]) == kappa) fn(tb + j);
+        }
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ unsigned long long MulHi32(unsigned long long a, uint32_t u) {
   // (a * u) >> 32 for a < 2^63
   return __umul64hi(a, static_cast<unsigned long long>(u) << 32);
@@ -2933,7 +3013,7 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   // counted in kcnt, a row per high byte claimed on first sight; max key,
   // |allowed|.  More high bytes than rows: the two-pass path below.
   unsigned int kmax = 0u, n_allowed = 0u;
-  ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
+  ForAllowedBatched<PRE3_SAMPLE_BATCH>(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
     const int h = static_cast<int>(key >> 8);
     int r = sh.claim[h];
     if (r < 0) {
@@ -3229,8 +3309,15 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     // ranges per thread, counts scanned across the CTA.
     const int per = (nchunks + kThreads - 1) / kThreads;
     const int c0 = tid * per, c1 = min(nchunks, c0 + per);
+    // The first two matches of each thread are kept, so the thread holding
+    // the jth rarely walks its range again.
     unsigned int mine = 0u;
-    ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, c0, c1, 1, [&](int, uint32_t key) { mine += key == kappa; });
+    int first0 = -1, first1 = -1;
+    ForKeyMatches(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, c0, c1, kappa, [&](int t) {
+      if (mine == 0u) first0 = t;
+      else if (mine == 1u) first1 = t;
+      ++mine;
+    });
     int total = 0;
     const int excl = BlockExclusiveScan(static_cast<int>(mine), reinterpret_cast<int*>(sh.red), &total);
     if (tid == 0) sh.found = -1;
@@ -3238,12 +3325,14 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     if (jth >= static_cast<unsigned long long>(excl) && jth < static_cast<unsigned long long>(excl) + mine) {
       unsigned int want = static_cast<unsigned int>(jth) - static_cast<unsigned int>(excl);
       int hit = -1;
-      ForAllowed(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, c0, c1, 1, [&](int t, uint32_t key) {
-        if (key == kappa) {
+      if (want < 2u) {
+        hit = want == 0u ? first0 : first1;
+      } else {
+        ForKeyMatches(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, c0, c1, kappa, [&](int t) {
           if (want == 0u && hit < 0) hit = t;
           --want;
-        }
-      });
+        });
+      }
       sh.found = hit;
     }
     __syncthreads();

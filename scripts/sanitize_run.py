@@ -134,6 +134,35 @@ def overflow(B=8, steps=12):
         batch.check()
 
 
+def refill(B=16, K=2):
+    """Fills without an accept between (past the 6-fill tag period), a sample
+    without accept, then split steps with heavy segments (K = 2 leaves many
+    context-dependent tokens): masks equal to the port's on the same stacks."""
+    eng = pk.DeviceEngine(pk.Automaton.load(FLAT), VOCAB, context_depth=K, context_slots=1024)
+    port = Port(FLAT, VOCAB)
+    batch = eng.batch(B)
+    bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
+    cnt = torch.zeros((B, 2 * batch.nseg), dtype=torch.int32, device=DEV)
+    tk = torch.zeros(B, dtype=torch.int32, device=DEV)
+    for _ in range(5):
+        batch.decode_step_stream_split(3, bitmask=bm, seg_counts=cnt, tokens_out=tk)
+    want = []
+    for b in range(B):
+        c = batch.get(b)
+        cfg = port.config(c.status, c.stack)
+        want.append(port.mask(cfg))
+        port.free(cfg)
+    want = np.stack(want)
+    for _ in range(8):
+        batch.fill(bm, None, cnt)
+        batch.check()
+        assert np.array_equal(bm.cpu().numpy().view(np.uint32), want)
+    batch.sample_stream(bm, cnt, 3, tk)
+    for _ in range(4):
+        batch.decode_step_stream_split(3, bitmask=bm, seg_counts=cnt, tokens_out=tk)
+        batch.check()
+
+
 PARTS = {
     "two_call": lambda: stream("two_call"),
     "split": lambda: stream("split"),
@@ -146,6 +175,7 @@ PARTS = {
     "graph": graph,
     "layout": layout,
     "overflow": overflow,
+    "refill": refill,
 }
 
 if __name__ == "__main__":
