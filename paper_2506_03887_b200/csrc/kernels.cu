@@ -3023,7 +3023,13 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
         r = atomicAdd(&sh.nclaim, 1);
         atomicExch(&sh.claim[h], r);
       } else {
-        while ((r = *reinterpret_cast<volatile int*>(&sh.claim[h])) < 0) {
+        // Bounded: past it (a tool that serializes threads), force the
+        // two-pass path — the counts are then rebuilt from scratch.
+        for (int spin = 0; (r = atomicAdd(&sh.claim[h], 0)) < 0 && spin < 4096; ++spin) {
+        }
+        if (r < 0) {
+          atomicMax(&sh.nclaim, kSampleKeySlots + 1);
+          r = kSampleKeySlots;
         }
       }
     }
