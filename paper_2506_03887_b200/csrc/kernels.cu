@@ -1594,7 +1594,10 @@ __device__ __forceinline__ unsigned long long ArgmaxBuffered(int tw, uint32_t mw
 // h ^ 0xFFFF for a negative value, h ^ 0x8000 otherwise (PRMT replicates
 // each half's sign bit over the half).
 __device__ __forceinline__ uint32_t PairOrderKeys(uint32_t w) {
-  const uint32_t sgn = __byte_perm(w, 0u, 0xBB99u);
+  // prmt's generic mode (a selector nibble with its msb set replicates the
+  // sign of the selected byte); __byte_perm masks that bit off.
+  uint32_t sgn;
+  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(sgn) : "r"(w));
   return w ^ (sgn | 0x80008000u);
 }
 
@@ -2966,6 +2969,16 @@ __device__ __forceinline__ void ForKeyMatches(const uint32_t* mrow, const uint16
       const int tb = (c0 + u) * 8;
       if (vec_ok && tb + 8 <= V) {
         const uint32_t w4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+        // Any of the 8 keys equal to kappa?  Two keys per word: a zero half of
+        // keys ^ (kappa, kappa) (the haszero test), most chunks have none.
+        const uint32_t k2 = kappa | (kappa << 16);
+        uint32_t hit = 0u;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint32_t x = PairOrderKeys(w4[p]) ^ k2;
+          hit |= (x - 0x00010001u) & ~x & 0x80008000u;
+        }
+        if (!hit) continue;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (((byte[u] >> j) & 1u) && SampleKey((w4[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu) == kappa) fn(tb + j);
