@@ -2928,10 +2928,11 @@ __device__ __forceinline__ void ForAllowedBatched(const uint32_t* mrow, const ui
       if (!byte[u]) continue;
       const int tb = (c0 + u * c_step) * 8;
       if (vec_ok && tb + 8 <= V) {
-        const uint32_t w4[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+        const uint32_t k4[4] = {PairOrderKeys(q[u].x), PairOrderKeys(q[u].y), PairOrderKeys(q[u].z),
+                                PairOrderKeys(q[u].w)};  // = SampleKey of each half
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          if ((byte[u] >> j) & 1u) fn(tb + j, SampleKey((w4[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu));
+          if ((byte[u] >> j) & 1u) fn(tb + j, (k4[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu);
         }
       } else {
         for (int j = 0; j < 8 && tb + j <= V; ++j) {
@@ -3026,9 +3027,10 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
   // counted in kcnt, a row per high byte claimed on first sight; max key,
   // |allowed|.  More high bytes than rows: the two-pass path below.
   unsigned int kmax = 0u, n_allowed = 0u;
+  int last_h = -1, last_r = 0;  // the previous token's high byte and row (consecutive tokens often share it)
   ForAllowedBatched<PRE3_SAMPLE_BATCH>(mrow, row, Vv.V, Vv.eos_col, S.vec_ok, tid, nchunks, kThreads, [&](int, uint32_t key) {
     const int h = static_cast<int>(key >> 8);
-    int r = sh.claim[h];
+    int r = h == last_h ? last_r : sh.claim[h];
     if (r < 0) {
       // -1 -> -2 (claiming) -> row id; a thread that loses the race waits for
       // the winner's id (independent thread scheduling: the winner progresses).
@@ -3046,6 +3048,8 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
         }
       }
     }
+    last_h = h;
+    last_r = r;
     if (r < kSampleKeySlots) atomicAdd(&sh.u.kcnt[r][key & 0xffu], 1u);
     kmax = key > kmax ? key : kmax;
     ++n_allowed;
