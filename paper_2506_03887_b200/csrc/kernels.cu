@@ -1619,9 +1619,7 @@ __device__ __forceinline__ uint32_t ArgmaxBufferedPacked(int span_off, uint32_t 
     *rd += 16;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t w = pv[j];
-      const uint32_t neg = (w >> 15) & 0x00010001u;
-      const uint32_t key2 = w ^ (0x80008000u | (neg * 0x7FFFu));  // two 16-bit order keys
+      const uint32_t key2 = PairOrderKeys(pv[j]);  // two 16-bit order keys
       const uint32_t lo = (key2 << 16) | (c0 - 2 * j);
       const uint32_t hi = (key2 & 0xFFFF0000u) | (c0 - 2 * j - 1);
       if ((byte[k] >> (2 * j)) & 1u) best = max(best, lo);
