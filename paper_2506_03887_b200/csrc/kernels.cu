@@ -41,17 +41,8 @@
 #ifndef PRE3_COMPACT_MIXED
 #define PRE3_COMPACT_MIXED 0  // light pass: all mixed chunks of a segment copied in one round trip
 #endif
-#ifndef PRE3_MIXED_RED
-#define PRE3_MIXED_RED 0  // light pass: mixed spans blended in L2 (bulk stores + cp.reduce.async.bulk .min.bf16)
-#endif
 #ifndef PRE3_DIAG_NO_MIXED
 #define PRE3_DIAG_NO_MIXED 0  // (diagnostics only, wrong logits) every full span bulk-stored as -inf
-#endif
-#ifndef PRE3_SPAN_READ_ALL
-#define PRE3_SPAN_READ_ALL 0  // (A/B) mixed spans: every chunk not all-allowed is read, not just the mixed ones
-#endif
-#ifndef PRE3_GREEDY_VMAX
-#define PRE3_GREEDY_VMAX 0  // (A/B, measured slower: 42 vs 37 us) greedy light pass: SIMD halfword max per chunk + one chunk re-read for the id
 #endif
 // Register caps (A/B): a fill at 64 registers x 4 CTAs fills the register
 // file, so no accept CTA can be resident beside it until fill CTAs retire.
@@ -69,6 +60,9 @@
 #endif
 #ifndef PRE3_SAMPLE_BATCH
 #define PRE3_SAMPLE_BATCH 2  // sampler pass 1: chunks whose loads are issued together per thread
+#endif
+#ifndef PRE3_LIGHT_BUILD_UNITS
+#define PRE3_LIGHT_BUILD_UNITS -1  // build units a light fill CTA takes before its items (-1: until none is left)
 #endif
 #ifndef PRE3_BULK_MASKED
 #define PRE3_BULK_MASKED 1  // fully masked spans as one bulk (TMA) store
@@ -838,12 +832,12 @@ __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView
 // Drains build queue q (CTA-cooperative).  Items were appended by earlier
 // launches, so the count is final here.
 __device__ void HelpBuild(const AutView& A, const VocabView& Vv, const CacheView& Cc, const BatchView& Bt, int q,
-                          int32_t* base_s, int* sh_unit) {
+                          int32_t* base_s, int* sh_unit, int max_units = -1) {
   const BuildQueue Q = QueueOf(Bt, q);
   const unsigned int n_items = LoadRelaxed(Q.n_items);
   if (n_items == 0) return;
   const unsigned int units = n_items * kChunksPerSeg;
-  for (;;) {
+  for (int done = 0; max_units < 0 || done < max_units; ++done) {
     if (threadIdx.x == 0) *sh_unit = static_cast<int>(atomicAdd(Q.next_unit, 1u));
     __syncthreads();
     const unsigned int u = static_cast<unsigned int>(*sh_unit);
@@ -1481,37 +1475,6 @@ __device__ __forceinline__ void BulkStore(void* gmem, const void* smem, int byte
 }
 __device__ __forceinline__ void BulkCommit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void BulkWaitRead() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
-__device__ __forceinline__ void BulkWaitRead1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
-// Bulk (TMA) reduction into global memory, done in L2: dst = min(dst, src)
-// per bf16 element.  min() returns the non-NaN operand, so a NaN source
-// element leaves the destination's value (a NaN destination becomes the
-// canonical NaN) and a -inf source element writes -inf.
-__device__ __forceinline__ void BulkReduceMinBf16(void* gmem, const void* smem, int bytes) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.min.bf16 [%0], [%1], %2;\n" ::"l"(gmem), "r"(sa),
-               "r"(bytes)
-               : "memory");
-}
-// Bits 0, 2, 4, ..., 30 of x packed into bits 0..15.
-__device__ __forceinline__ uint32_t EvenBits(uint32_t x) {
-  x &= 0x55555555u;
-  x = (x | (x >> 1)) & 0x33333333u;
-  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
-  x = (x | (x >> 4)) & 0x00FF00FFu;
-  return (x | (x >> 8)) & 0x0000FFFFu;
-}
-// Runs of set bits of a 64-sector mask: fn(first sector, sectors).
-template <typename Fn>
-__device__ __forceinline__ void ForRuns(unsigned long long x, Fn fn) {
-  while (x) {
-    const int s = __ffsll(static_cast<long long>(x)) - 1;
-    const unsigned long long above = ~(x >> s);
-    const int len = above ? __ffsll(static_cast<long long>(above)) - 1 : 64 - s;
-    fn(s, len);
-    x &= len >= 64 ? 0ull : ~(((1ull << len) - 1ull) << s);
-  }
-}
-
 // Mixed chunks of a full span -> this lane's slots of a span buffer.
 __device__ __forceinline__ void SpanPrefetch(const uint16_t* row, int tw, uint32_t mword, int lane,
                                              uint4 (*buf)[32]) {
@@ -1519,11 +1482,7 @@ __device__ __forceinline__ void SpanPrefetch(const uint16_t* row, int tw, uint32
   SpanBytes(mword, lane, byte);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-#if PRE3_SPAN_READ_ALL
-    if (byte[k] != 0xffu) CpAsync16(&buf[k][lane], row + tw + (32 * k + lane) * 8);  // (A/B) whole sectors read
-#else
     if (byte[k] != 0u && byte[k] != 0xffu) CpAsync16(&buf[k][lane], row + tw + (32 * k + lane) * 8);
-#endif
   }
 }
 
@@ -1860,7 +1819,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       CpAsyncCommit();
     }
   };
-#if !PRE3_MIXED_RED && !PRE3_COMPACT_MIXED
+#if !PRE3_COMPACT_MIXED
   if (spans_early) {
     classify();
     prefetch2();
@@ -2054,73 +2013,6 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       CpAsyncCommit();
     }
     int q = 0;
-#if PRE3_GREEDY_VMAX
-    // Per chunk: the 8 tokens' 16-bit order keys two at a time (masked -> 0
-    // through a per-CTA keep-mask table), their max by SIMD halfword max, and
-    // the lane's running best key with the chunk where it first appeared.
-    // The lowest id holding the warp's best key is then found by re-reading
-    // that one chunk (in L2).  An item whose allowed tokens are all key 0
-    // (bf16 0xFFFF) takes its lowest allowed id.
-    const uint4* keep_lut = ninf;  // greedy: the CTA's keep-mask table (FillKernel)
-    uint32_t lbest = 0u, lbyte = 0u;
-    int lwhere = -1;
-#pragma unroll 1
-    for (uint32_t todo = live; todo; todo &= todo - 1, q ^= 1) {
-      const int i = __ffs(todo) - 1;
-      CpAsyncWait1();
-      uint32_t byte[4];
-      SpanBytes(Pick(m, i), lane, byte);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (!byte[k]) continue;
-        const uint4 v = buf[q][k][lane];
-        const uint4 kp = keep_lut[byte[k]];
-        const uint32_t k0 = PairOrderKeys(v.x) & kp.x, k1 = PairOrderKeys(v.y) & kp.y;
-        const uint32_t k2 = PairOrderKeys(v.z) & kp.z, k3 = PairOrderKeys(v.w) & kp.w;
-        const uint32_t m2 = __vmaxu2(__vmaxu2(k0, k1), __vmaxu2(k2, k3));
-        const uint32_t ck = max(m2 & 0xFFFFu, m2 >> 16);
-        if (ck > lbest) {
-          lbest = ck;
-          lwhere = 4 * i + k;
-          lbyte = byte[k];
-        }
-        rd += 16;
-      }
-      if (pend) {
-        const int j = __ffs(pend) - 1;
-        pend &= pend - 1;
-        SpanPrefetchAllowed(row, t0 + 1024 * j, Pick(m, j), lane, buf[q]);
-      }
-      CpAsyncCommit();
-    }
-    const uint32_t kbest = __reduce_max_sync(0xffffffffu, lbest);
-    if (live) {
-      uint32_t tcand = 0xFFFFFFFFu;
-      if (kbest != 0u) {
-        if (lbest == kbest) {
-          const int i = lwhere >> 2, k = lwhere & 3;
-          const int tb = t0 + 1024 * i + (32 * k + lane) * 8;
-          const uint4 v = __ldcg(reinterpret_cast<const uint4*>(row + tb));
-          const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int j = 7; j >= 0; --j) {  // the lowest j holding kbest wins
-            const uint32_t kj = (PairOrderKeys(w4[j >> 1]) >> ((j & 1) * 16)) & 0xFFFFu;
-            if (((lbyte >> j) & 1u) && kj == kbest) tcand = static_cast<uint32_t>(tb + j);
-          }
-        }
-      } else {  // every allowed key is 0: the lowest allowed id of the full spans
-        const int i0 = __ffs(live) - 1;
-        const uint32_t mw = Pick(m, i0);
-        const unsigned nzl = __ballot_sync(0xffffffffu, mw != 0u);
-        const int src = __ffs(nzl) - 1;
-        const uint32_t w = __shfl_sync(0xffffffffu, mw, src);
-        tcand = static_cast<uint32_t>(t0 + 1024 * i0 + 32 * src + __ffs(w) - 1);
-      }
-      const uint32_t tmin = __reduce_min_sync(0xffffffffu, tcand);
-      mine = (static_cast<unsigned long long>(Key32(kbest)) << 32) |
-             static_cast<unsigned long long>(0xFFFFFFFFu - tmin);
-    }
-#else
     uint32_t packed = 0u;  // ArgmaxBufferedPacked over the full spans
 #pragma unroll 1
     for (uint32_t todo = live; todo; todo &= todo - 1, q ^= 1) {
@@ -2140,7 +2032,6 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       mine = (static_cast<unsigned long long>(Key32(packed >> 16)) << 32) |
              static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(t));
     }
-#endif
 #endif
 #pragma unroll 1
     for (int i = nfull; i < kSpans; ++i) {
@@ -2187,7 +2078,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     // mixed -> 16-B chunks, two spans in flight: the mixed chunks of the next
     // two mixed spans are being copied (cp.async, no registers held) while
     // one is blended and stored.  Then a partial last span, if any.
-#if PRE3_MIXED_RED || PRE3_COMPACT_MIXED
+#if PRE3_COMPACT_MIXED
     const bool late = true;
 #else
     const bool late = !spans_early;
@@ -2280,61 +2171,6 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       todo &= ~batch;
       __syncwarp();  // the buffer is refilled by the next batch
     }
-#elif PRE3_MIXED_RED
-    // Mixed spans blended in L2, nothing read back by the SM: per 32-B sector
-    // (two 16-B chunks), all masked -> bulk store of -inf, all allowed ->
-    // untouched, otherwise -> cp.reduce.async.bulk .min.bf16 from a pattern
-    // (masked token -inf, allowed token NaN, which min() ignores).  Each run
-    // of same-kind sectors is one op, issued by lane 0; two pattern buffers
-    // per warp, reused once the TMA engine has read them.
-    const unsigned long long t_mx = Bt.trace ? NowNs() : 0ull;
-    uint4* pbuf = &span_buf[0][0][0];  // [2][128] chunks of this warp
-    int q = 0;
-#pragma unroll 1
-    for (uint32_t todo = mixed; todo; todo &= todo - 1, q ^= 1) {
-      const int i = __ffs(todo) - 1;
-      uint16_t* span = row + t0 + 1024 * i;
-      uint32_t byte[4];
-      SpanBytes(Pick(m, i), lane, byte);
-      unsigned long long st_sec = 0ull, rd_sec = 0ull;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const unsigned msk = __ballot_sync(0xffffffffu, byte[k] == 0u);
-        const unsigned all = __ballot_sync(0xffffffffu, byte[k] == 0xffu);
-        const uint32_t sm = EvenBits(msk & (msk >> 1));  // both chunks masked
-        const uint32_t sa = EvenBits(all & (all >> 1));  // both chunks allowed
-        st_sec |= static_cast<unsigned long long>(sm) << (16 * k);
-        rd_sec |= static_cast<unsigned long long>(~(sm | sa) & 0xffffu) << (16 * k);
-      }
-#if PRE3_MIXED_RED == 2
-      st_sec = 0ull;  // (A/B) the whole span as one reduce op
-      rd_sec = ~0ull;
-#endif
-      if (lane == 0) BulkWaitRead1();  // buffer q's previous op group (maybe an earlier item's) has been read
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t x = byte[k];
-        uint4 o;
-        uint32_t* po = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t keep = ((x >> (2 * j)) & 1u ? 0x0000FFFFu : 0u) | ((x >> (2 * j + 1)) & 1u ? 0xFFFF0000u : 0u);
-          po[j] = (0x7FFF7FFFu & keep) | (0xFF80FF80u & ~keep);
-        }
-        pbuf[q * 128 + 32 * k + lane] = o;
-      }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // pattern visible to the bulk copies
-      __syncwarp();
-      if (lane == 0) {
-        const uint4* pat = pbuf + q * 128;
-        ForRuns(st_sec, [&](int s0, int len) { BulkStore(span + 16 * s0, ninf, 32 * len, EvictFirstPolicy()); });
-        ForRuns(rd_sec, [&](int s0, int len) { BulkReduceMinBf16(span + 16 * s0, pat + 2 * s0, 32 * len); });
-        BulkCommit();
-        rd += 32u * static_cast<unsigned>(__popcll(rd_sec));  // read (in L2) and written back
-        wr += 32u * static_cast<unsigned>(__popcll(rd_sec) + __popcll(st_sec));
-      }
-    }
 #else
     const unsigned long long t_mx = Bt.trace ? NowNs() : 0ull;
     uint4(*buf)[4][32] = span_buf;  // [2][4][32] of this warp
@@ -2359,7 +2195,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     }
     if (Vv.layout && last_seg) TailColumns(Vv, row, eos_bit, lane, 32, &wr);
     const unsigned long long t_bw = Bt.trace ? NowNs() : 0ull;
-    if ((masked || (PRE3_MIXED_RED && mixed)) && lane == 0) BulkWaitRead();  // the smem sources outlive the reads
+    if (masked && lane == 0) BulkWaitRead();  // the -inf source outlives the reads
     if (Bt.trace && lane == 0) {
       TraceEvent(Bt, 15, b, seg, t_mx, static_cast<unsigned long long>(__popc(mixed)));  // l:mixed spans
       TraceEvent(Bt, 16, b, seg, t_bw, static_cast<unsigned long long>(__popc(masked)));  // l:bulk wait
@@ -2420,8 +2256,7 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
   __shared__ FillShared sh;
   __shared__ uint4 span_buf[kWarps][2][4][32];  // light pass: per-warp double buffer of mixed chunks (32 KB)
   __shared__ __align__(128) uint4 ninf_buf[128 * PRE3_BULK_RUN];  // bf16 -inf: the bulk-store source
-  // Greedy: chunk mask byte -> the four pairs' halfword keep masks.
-  __shared__ uint4 keep_lut[MODE == kFillGreedy ? 256 : 1];
+
   extern __shared__ int32_t stack_s[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -2450,15 +2285,6 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
       }
       __syncthreads();
     }
-    if (MODE == kFillGreedy) {
-      for (int x = tid; x < 256; x += kThreads) {
-        uint32_t kp[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) kp[j] = ((x >> (2 * j)) & 1 ? 0x0000FFFFu : 0u) | ((x >> (2 * j + 1)) & 1 ? 0xFFFF0000u : 0u);
-        keep_lut[x & (MODE == kFillGreedy ? 255 : 0)] = make_uint4(kp[0], kp[1], kp[2], kp[3]);
-      }
-      __syncthreads();
-    }
     const int item = (bid - Bt.h_grid) * F.light_per_cta + warp;
     const bool in_range = warp < F.light_per_cta && item < Bt.B * Vv.nseg;
     const int b = in_range ? item / Vv.nseg : 0;
@@ -2470,8 +2296,13 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
       slot = SeqSlot(Bt, F.fill_no)[b];
       hmask = SeqHmask(Bt, F.fill_no)[b];
     }
+    // Light CTAs help build at most PRE3_LIGHT_BUILD_UNITS units first (-1:
+    // until the queue is empty); the heavy CTAs, resident from the start,
+    // always drain it, so every unit is claimed by a running CTA.
     const unsigned int n_items = LoadRelaxed(Qc.n_items);
-    if (n_items != 0u) HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit);  // CTA-uniform
+    if (n_items != 0u && PRE3_LIGHT_BUILD_UNITS != 0) {
+      HelpBuild(A, Vv, Cc, Bt, F.consume, stack_s, &sh.unit, PRE3_LIGHT_BUILD_UNITS);  // CTA-uniform
+    }
     // Owned by the heavy pass: listed for this fill at a position the grid's
     // h_grid heavy CTAs cover (a longer list spills over to the light pass,
     // whose warps take the rare CD/wait paths themselves).
@@ -2485,8 +2316,7 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
     // segments publish arrivals — its accept takes the other segments from the
     // slot's CI row (AcceptKernel's ci_shortcut, the same test).
     const bool publish = !shared_ok || ((hmask >> seg) & 1u);
-    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, publish, lane, span_buf[warp],
-                          MODE == kFillGreedy ? keep_lut : ninf_buf);
+    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, publish, lane, span_buf[warp], ninf_buf);
     return;
   }
 
