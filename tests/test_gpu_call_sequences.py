@@ -5,7 +5,8 @@
   heavy-list tags, so a fill can never read context rows or heavy-list
   entries a lookup wrote for an older fill;
 * a sample without accept, then a fill;
-* a CUDA graph captured right after such fills.
+* a CUDA graph captured right after such fills;
+* two batches of one engine stepping concurrently on two CUDA streams.
 
 Every mask is compared with the C port's on the sequences' current stacks.
 Context depth 2 leaves many context-dependent tokens, so the fills schedule
@@ -104,3 +105,38 @@ def test_graph_captured_after_repeated_fills(setup):
     got_t = np.stack([x.cpu().numpy() for x in tks], 1)
     assert np.array_equal(got_h, hashes)
     assert np.array_equal(got_t, toks)
+
+
+@pytest.mark.parametrize("slots", [2048, 16])
+def test_two_batches_step_concurrently_on_two_streams(slots):
+    """Two batches of one engine decode at the same time on two CUDA streams
+    (they share the context cache: lookups, inserts, builds and parent links
+    race; 16 slots: the table fills and sequences fall back to private rows):
+    every step's mask and token equal the port's decode loop."""
+    vocab = pk.synth_vocab(20000)
+    eng = pk.DeviceEngine(pk.Automaton.load(flat()), vocab, context_depth=6, context_slots=slots, parent_depth=3)
+    port = Port(flat(), vocab)
+    structural = oracle.structural_words(vocab)
+    B, steps = 64, 30
+    seeds = (101, 202)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    batches = [eng.batch(B), eng.batch(B)]
+    bms = [[torch.zeros((B, eng.W), dtype=torch.int32, device=DEV) for _ in range(steps)] for _ in range(2)]
+    cns = [torch.zeros((B, 2 * batches[0].nseg), dtype=torch.int32, device=DEV) for _ in range(2)]
+    tks = [[torch.zeros(B, dtype=torch.int32, device=DEV) for _ in range(steps)] for _ in range(2)]
+    torch.cuda.synchronize()
+    for s in range(steps):  # interleaved launches, no synchronization between the streams
+        for i in range(2):
+            with torch.cuda.stream(streams[i]):
+                batches[i].decode_step_stream_split(seeds[i], bitmask=bms[i][s], seg_counts=cns[i], tokens_out=tks[i][s],
+                                                    stream=streams[i].cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(2):
+        batches[i].check(stream=streams[i].cuda_stream)
+        _, toks, _, hashes = port.decode_run(structural, B, steps, seeds[i], want_tokens=True, want_stacks=True,
+                                             want_mask_hashes=True)
+        got_h = np.stack([oracle.mask_hashes(x.cpu().numpy().view(np.uint32)) for x in bms[i]], 1)
+        got_t = np.stack([x.cpu().numpy() for x in tks[i]], 1)
+        assert np.array_equal(got_h, hashes), f"batch {i}: masks"
+        assert np.array_equal(got_t, toks), f"batch {i}: tokens"
+    assert eng.info()["context_slots_used"] > min(50, slots // 2)
