@@ -815,6 +815,13 @@ __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView
       if (cd) {
         atomicAdd(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg, __popc(cd));
         if (seg < 32) atomicOr(Cc.cd_segmask + slot, 1u << seg);
+        // A context-dependent EOS in a logit layout whose EOS column lies
+        // among the regular ids: that column's segment needs the walked EOS
+        // bit, so it is heavy too (its item is then waited for, EosBitOf).
+        if (w == (Vv.V >> 5) && ((cd >> (Vv.V & 31)) & 1u) && Vv.layout && Vv.eos_col < Vv.V) {
+          const int eseg = (Vv.eos_col >> 5) / kSegWords;
+          if (eseg < 32) atomicOr(Cc.cd_segmask + slot, 1u << eseg);
+        }
       }
     }
   }
@@ -1645,14 +1652,20 @@ __device__ __forceinline__ unsigned long long WarpMax64(unsigned long long v) {
 }
 
 // The EOS bit (mask bit V) of sequence b for an item of another segment
-// (logit layouts whose EOS column lies among the regular ids): a pure-CI
-// sequence's is its slot's CI bit (its stack may already be changing under
-// the overlapped accept); any other sequence's accept waits for this item's
-// arrival, so its stack is stable and EOS (one terminal) is walked on it —
+// (logit layouts whose EOS column lies among the regular ids).  With a
+// settled (built, shared) slot whose EOS is context-independent it is the
+// slot's CI bit — no walk: the sequence's stack may already be changing under
+// the overlapped accept, which waits only for its heavy segments.  Otherwise
+// the accept waits for this item (a waiting or private slot makes every
+// segment heavy; a context-dependent EOS makes the EOS column's segment heavy,
+// BuildUnit), so the stack is stable and EOS (one terminal) is walked on it —
 // Step(kEndMarker) succeeds iff AllowedTerminals reports the end marker.
 __device__ __forceinline__ int EosBitOf(const AutView& A, const VocabView& Vv, const CacheView& Cc,
-                                        const BatchView& Bt, int b, int slot, bool pure) {
-  if (pure) return static_cast<int>((__ldcg(Cc.ci + static_cast<long long>(slot) * Vv.W + (Vv.V >> 5)) >> (Vv.V & 31)) & 1u);
+                                        const BatchView& Bt, int b, int slot, bool settled) {
+  if (settled && slot >= 0 && slot < Cc.C) {
+    const long long w = static_cast<long long>(slot) * Vv.W + (Vv.V >> 5);
+    if (!((__ldcg(Cc.cdb + w) >> (Vv.V & 31)) & 1u)) return static_cast<int>((__ldcg(Cc.ci + w) >> (Vv.V & 31)) & 1u);
+  }
   const SeqState st = Bt.seq[b];
   if (st.status != kAlive) return 0;
   return WalkToken(A, Vv, Vv.V, Bt.stacks + static_cast<long long>(b) * Bt.cap, st.depth, true) == kAccept ? 1 : 0;
@@ -1866,7 +1879,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       const int we = (Vv.V >> 5) - w0;
       eos_bit = static_cast<int>((__shfl_sync(0xffffffffu, Pick(m, we >> 5), we & 31) >> (Vv.V & 31)) & 1u);
     } else {
-      if (lane == 0) eos_bit = slot == -2 ? 0 : EosBitOf(A, Vv, Cc, Bt, b, slot, pure);
+      if (lane == 0) eos_bit = slot == -2 ? 0 : EosBitOf(A, Vv, Cc, Bt, b, slot, !wait);
       eos_bit = __shfl_sync(0xffffffffu, eos_bit, 0);
     }
   }
@@ -2447,7 +2460,7 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
       if (w0 + tid == (Vv.V >> 5)) sh.eos = static_cast<int>((mword >> (Vv.V & 31)) & 1u);
     } else if (tid == 0) {
       const int sl = SeqSlot(Bt, F.fill_no)[b];
-      sh.eos = sl == -2 ? 0 : EosBitOf(A, Vv, Cc, Bt, b, sl & ~kSlotWait, false);
+      sh.eos = sl == -2 ? 0 : EosBitOf(A, Vv, Cc, Bt, b, sl & ~kSlotWait, !(sl & kSlotWait));
     }
   }
   __syncthreads();

@@ -67,12 +67,16 @@ def setup(request):
     return L, eng, port
 
 
-def test_masked_logits_follow_the_layout(setup):
+@pytest.mark.parametrize("K,B", [(8, 24), (2, 64)])
+def test_masked_logits_follow_the_layout(setup, K, B):
     """Fused mask + -inf: regular columns by their bit, the EOS column by bit
     V, every other special column -inf; the bitmask keeps the reference
-    layout and equals the port's."""
-    L, eng, port = setup
-    B = 24
+    layout and equals the port's.  K = 2 makes EOS context-dependent in most
+    contexts (the EOS column's segment is then heavy: its item walks EOS on
+    the stack while the overlapped accept waits for it)."""
+    L, eng8, port = setup
+    eng = eng8 if K == 8 else pk.DeviceEngine(pk.Automaton.load(json_flat()), L["engine_vocab"], context_depth=K,
+                                               num_columns=L["ncols"], eos_column=L["eos"], disabled=L["disabled"])
     batch = eng.batch(B)
     g = torch.Generator(device=DEV).manual_seed(3)
     toks = torch.zeros(B, dtype=torch.int32, device=DEV)
