@@ -413,12 +413,15 @@ def test_tokenizer_json_vocabulary_on_device():
 
 @pytest.mark.parametrize("T,k,p,ties", [(1.0, 0, 1.0, False), (0.7, 50, 1.0, False), (1.3, 0, 0.9, False),
                                         (0.5, 20, 0.8, False), (2.0, 3, 0.5, True), (1.0, 0, 0.95, True),
-                                        (0.05, 0, 1.0, False), (1.0, 1, 1.0, True)])
+                                        (0.05, 0, 1.0, False), (1.0, 1, 1.0, True), (1.0, 0, 1.0, "wide"),
+                                        (40.0, 200, 0.9, "wide")])
 def test_sample_decode_step_matches_port(T, k, p, ties):
     """gm_decode_step_sample (fill + temperature/top-k/top-p sampler + accept,
     one host call, no round trip) == the C port's rule step by step: masks,
     sampled tokens, stacks.  `ties` quantizes the logits to few values so the
-    tie rules (thresholds keep ties, draws walk ties in id order) are hit."""
+    tie rules (thresholds keep ties, draws walk ties in id order) are hit;
+    "wide" spreads them over 2^-40..2^40 (more than 24 sign+exponent bytes:
+    the sampler's two-pass histogram path instead of one-pass key counts)."""
     vocab = pk.synth_vocab(128255)
     f = flat("json")
     eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=12)
@@ -431,7 +434,9 @@ def test_sample_decode_step_matches_port(T, k, p, ties):
     g = torch.Generator(device=DEV).manual_seed(5)
     for s in range(steps):
         lg = torch.randn((B, eng.V + 1), dtype=torch.float32, device=DEV, generator=g)
-        if ties:
+        if ties == "wide":
+            lg = torch.sign(lg) * torch.exp2(torch.rand((B, eng.V + 1), device=DEV, generator=g) * 80 - 40)
+        elif ties:
             lg = torch.round(lg * 2) / 2
         lg = lg.to(torch.bfloat16)
         batch.decode_step_sample(lg, temperature=T, top_k=k, top_p=p, seed=seed, tokens_out=toks, bitmask=bm)
