@@ -516,6 +516,14 @@ int gm_engine_create(const gm_automaton* a, const uint8_t* tok_bytes, const int6
     c.slot_parent = DevAlloc<int32_t>(C, &e->owned);
     Check(cudaMemset(c.slot_parent, 0xff, C * 4), "memset");
     c.R = static_cast<int32_t>(o.parent_depth);
+    c.W = e->W;
+    c.eos_word = num_tokens >> 5;
+    c.eos_bit = 1u << (num_tokens & 31);
+    c.eos_segbit = 0u;
+    if (e->vocab.layout && e->vocab.eos_col < num_tokens) {
+      const int eseg = (e->vocab.eos_col >> 5) / pre3::kSegWords;
+      if (eseg < 32) c.eos_segbit = 1u << eseg;
+    }
     c.cd_segmask = DevAlloc<uint32_t>(C, &e->owned);
     Check(cudaMemset(c.cd_segmask, 0, C * 4), "memset");
     c.ci_cnt = DevAlloc<int32_t>(C * static_cast<size_t>(e->nseg) * 2, &e->owned);

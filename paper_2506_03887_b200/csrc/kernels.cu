@@ -693,13 +693,22 @@ __device__ __forceinline__ int32_t* HeavyIndex(const BatchView& Bt, int fill_no,
   return Bt.heavy_index + static_cast<long long>(fill_no & 1) * Bt.B * nseg;
 }
 
+// A logit layout whose EOS column lies among the regular ids needs the EOS
+// bit in that column's segment: when the built slot's EOS is context-
+// dependent, that segment is heavy too (its item walks EOS on the stack, so
+// the split step's accept must wait for it; EosBitOf).  0 otherwise.
+__device__ __forceinline__ uint32_t EosSegExtra(const CacheView& Cc, int slot) {
+  if (!Cc.eos_segbit) return 0u;
+  return (__ldcg(Cc.cdb + static_cast<long long>(slot) * Cc.W + Cc.eos_word) & Cc.eos_bit) ? Cc.eos_segbit : 0u;
+}
+
 // Segments of sequence b the next fill should schedule first: those with
 // context-dependent tokens (walks) or a pending build (waits).
 __device__ uint32_t HeavyMask(const CacheView& Cc, int flagged, int nseg) {
   if (flagged < 0) return 0u;
   const uint32_t all = nseg >= 32 ? 0xffffffffu : ((1u << nseg) - 1u);
   if ((flagged & kSlotWait) || (flagged & ~kSlotWait) >= Cc.C) return all;
-  return LoadRelaxed(Cc.cd_segmask + (flagged & ~kSlotWait)) & all;
+  return (LoadRelaxed(Cc.cd_segmask + (flagged & ~kSlotWait)) | EosSegExtra(Cc, flagged & ~kSlotWait)) & all;
 }
 
 // Appends b's heavy segments to queue q's heavy list and records, for every
@@ -815,13 +824,6 @@ __device__ void BuildUnit(const AutView& A, const VocabView& Vv, const CacheView
       if (cd) {
         atomicAdd(Cc.cd_cnt + static_cast<long long>(slot) * Vv.nseg + seg, __popc(cd));
         if (seg < 32) atomicOr(Cc.cd_segmask + slot, 1u << seg);
-        // A context-dependent EOS in a logit layout whose EOS column lies
-        // among the regular ids: that column's segment needs the walked EOS
-        // bit, so it is heavy too (its item is then waited for, EosBitOf).
-        if (w == (Vv.V >> 5) && ((cd >> (Vv.V & 31)) & 1u) && Vv.layout && Vv.eos_col < Vv.V) {
-          const int eseg = (Vv.eos_col >> 5) / kSegWords;
-          if (eseg < 32) atomicOr(Cc.cd_segmask + slot, 1u << eseg);
-        }
       }
     }
   }
@@ -1125,7 +1127,7 @@ __device__ uint32_t AssignSlotWarp(const CacheView& Cc, const BatchView& Bt, int
   }
   if (lane == 0) *slot_out = slot | (wait ? kSlotWait : 0);
   const uint32_t all = nseg >= 32 ? 0xffffffffu : ((1u << nseg) - 1u);
-  return (wait || slot >= Cc.C) ? all : (segmask & all);
+  return (wait || slot >= Cc.C) ? all : ((segmask | EosSegExtra(Cc, slot)) & all);
 }
 
 // Engine::Step over the bytes of `tok` (EOS = V) on the device stack
@@ -1658,7 +1660,7 @@ __device__ __forceinline__ unsigned long long WarpMax64(unsigned long long v) {
 // the overlapped accept, which waits only for its heavy segments.  Otherwise
 // the accept waits for this item (a waiting or private slot makes every
 // segment heavy; a context-dependent EOS makes the EOS column's segment heavy,
-// BuildUnit), so the stack is stable and EOS (one terminal) is walked on it —
+// EosSegExtra), so the stack is stable and EOS (one terminal) is walked on it —
 // Step(kEndMarker) succeeds iff AllowedTerminals reports the end marker.
 __device__ __forceinline__ int EosBitOf(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                         const BatchView& Bt, int b, int slot, bool settled) {
@@ -1879,7 +1881,11 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
       const int we = (Vv.V >> 5) - w0;
       eos_bit = static_cast<int>((__shfl_sync(0xffffffffu, Pick(m, we >> 5), we & 31) >> (Vv.V & 31)) & 1u);
     } else {
-      if (lane == 0) eos_bit = slot == -2 ? 0 : EosBitOf(A, Vv, Cc, Bt, b, slot, !wait);
+      if (lane == 0) {
+        // (the raw slot again, rather than keeping `wait` live across the item)
+        const bool settled = !(SeqSlot(Bt, F.fill_no)[b] & kSlotWait);
+        eos_bit = slot == -2 ? 0 : EosBitOf(A, Vv, Cc, Bt, b, slot, settled);
+      }
       eos_bit = __shfl_sync(0xffffffffu, eos_bit, 0);
     }
   }

@@ -106,6 +106,11 @@ struct CacheView {
   int32_t IC;                     // index positions (power of two, 2C)
   int32_t K;
   int32_t R;                      // parent key depth (0: no parents)
+  int32_t W;                      // mask words per row
+  int32_t eos_word;               // V >> 5 (the EOS bit's word)
+  uint32_t eos_bit;               // 1 << (V & 31)
+  uint32_t eos_segbit;            // logit layout with the EOS column among the regular ids: bit of that
+                                  //    column's segment (EosSegExtra), else 0
 };
 
 // Build work queue: items {slot, seg, seq, 0}; units = items * kChunksPerSeg.
