@@ -94,6 +94,30 @@ class DeviceEngine {
     return b;
   }
 
+  // Context cache (no reference counterpart: the reference recomputes every
+  // mask).  Prewarm populates it with synthetic decode steps; a snapshot
+  // ("P3GMCTX1") of the built table loads into a fresh engine of the same
+  // automaton / vocabulary / options instead (gm_engine_snapshot_*).
+  void Prewarm(int32_t batch, int32_t steps, uint64_t seed) const {
+    Check(gm_engine_prewarm(engine_, batch, steps, seed, 0, nullptr));
+  }
+  std::vector<uint8_t> SaveContexts() const {
+    uint64_t n = 0;
+    Check(gm_engine_snapshot_save(engine_, nullptr, 0, &n));
+    std::vector<uint8_t> buf(static_cast<size_t>(n));
+    Check(gm_engine_snapshot_save(engine_, buf.data(), n, &n));
+    buf.resize(static_cast<size_t>(n));
+    return buf;
+  }
+  void LoadContexts(const std::vector<uint8_t>& snapshot) const {
+    Check(gm_engine_snapshot_load(engine_, snapshot.data(), snapshot.size()));
+  }
+  int64_t ContextsUsed() const {
+    int64_t info[8];
+    Check(gm_engine_info(engine_, info));
+    return info[3];
+  }
+
 #ifdef PRE3_DEVICE_ENGINE_SINGLE
   // Engine::ComputeMask (runtime.cpp:280-287) for one configuration: V+1
   // bits in 32-bit words (bit t of word t/32; bit V = EOS), the reference's

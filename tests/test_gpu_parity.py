@@ -625,8 +625,11 @@ def test_cpp_device_engine_known_answers(vectors, tmp_path):
     lines = [" ".join(str(vocab.index(c)) for c in p) for p in prefixes]
     path = tmp_path / "paren.p3dpda"
     path.write_bytes(flat("paren"))
+    env = dict(os.environ, PRE3_CLI_SNAPSHOT="1")
     out = subprocess.run([str(exe), str(path)] + vocab, input="\n".join(lines) + "\n", capture_output=True,
-                         text=True, check=True).stdout.splitlines()
+                         text=True, check=True, env=env).stdout.splitlines()
+    assert out[-1].startswith("snapshot ok") and int(out[-1].split()[2]) > 0, out[-1]
+    out = out[:-1]
     assert len(out) == len(prefixes)
     port = Port(flat("paren"), [t.encode() for t in vocab])
     for p, row in zip(prefixes, out):
