@@ -125,6 +125,36 @@ def layout(B=8, steps=6):
         batch.check()
 
 
+def layout_eos_inside(B=16, steps=8):
+    """Llama-2-like layout: the EOS column (id 2) among the regular ids,
+    K = 2 so EOS is mostly context-dependent (its segment goes heavy)."""
+    vocab = [b"", b"", b""] + VOCAB[3:]
+    V = len(vocab)
+    eng = pk.DeviceEngine(pk.Automaton.load(FLAT), vocab, context_depth=2, num_columns=V, eos_column=2,
+                          disabled=[0, 1, 2])
+    batch = eng.batch(B)
+    tk = torch.zeros(B, dtype=torch.int32, device=DEV)
+    for _ in range(steps):
+        lg = torch.randn((B, V), device=DEV).to(torch.bfloat16)
+        batch.decode_step_stream_split(4, logits=lg, tokens_out=tk)
+        batch.check()
+
+
+def two_streams(B=16, steps=8):
+    """Two batches of one engine stepping concurrently on two streams."""
+    eng = pk.DeviceEngine(pk.Automaton.load(FLAT), VOCAB, context_depth=6, context_slots=64, parent_depth=3)
+    ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+    bs = [eng.batch(B), eng.batch(B)]
+    tks = [torch.zeros(B, dtype=torch.int32, device=DEV) for _ in range(2)]
+    for _ in range(steps):
+        for i in range(2):
+            with torch.cuda.stream(ss[i]):
+                bs[i].decode_step_stream_split(11 + i, tokens_out=tks[i], stream=ss[i].cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(2):
+        bs[i].check(stream=ss[i].cuda_stream)
+
+
 def overflow(B=8, steps=12):
     eng = pk.DeviceEngine(pk.Automaton.load(FLAT), VOCAB, context_depth=4)
     batch = eng.batch(B, stack_capacity=8)
@@ -176,6 +206,8 @@ PARTS = {
     "layout": layout,
     "overflow": overflow,
     "refill": refill,
+    "layout_eos_inside": layout_eos_inside,
+    "two_streams": two_streams,
 }
 
 if __name__ == "__main__":
