@@ -2840,6 +2840,51 @@ __device__ __forceinline__ void ForKeyMatches(const uint32_t* mrow, const uint16
   }
 }
 
+// Warp-parallel descending scan of arr[hi], arr[hi-1], ..., arr[lo]
+// (smem, at most 256 entries) starting from c0: the first index i whose
+// inclusive running sum reaches `target`, with the running sum before it in
+// *excl (-1 when none: *excl = c0 + the whole range).  Lane l takes entries
+// hi-8l .. hi-8l-7; every lane returns the same result (each warp of the CTA
+// can run it redundantly — no barrier).
+template <typename T>
+__device__ __forceinline__ int ScanDescWarp(const T* arr, int hi, int lo, T c0, T target, T* excl) {
+  const int lane = threadIdx.x & 31;
+  T v[8];
+  T mine = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int i = hi - 8 * lane - j;
+    v[j] = i >= lo ? arr[i] : T(0);
+    mine += v[j];
+  }
+  T inc = mine;  // inclusive warp scan (exact integers)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const T before = c0 + inc - mine;  // the running sum before this lane's entries
+  const unsigned hit = __ballot_sync(0xffffffffu, c0 + inc >= target && hi - 8 * lane >= lo);
+  if (!hit) {
+    *excl = c0 + __shfl_sync(0xffffffffu, inc, 31);
+    return -1;
+  }
+  const int src = __ffs(hit) - 1;
+  int idx = -1;
+  T cum = before;
+  if (lane == src) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (idx < 0) {
+        if (cum + v[j] >= target) idx = hi - 8 * lane - j;
+        else cum += v[j];
+      }
+    }
+  }
+  *excl = __shfl_sync(0xffffffffu, cum, src);
+  return __shfl_sync(0xffffffffu, idx, src);
+}
+
 __device__ __forceinline__ unsigned long long MulHi32(unsigned long long a, uint32_t u) {
   // (a * u) >> 32 for a < 2^63
   return __umul64hi(a, static_cast<unsigned long long>(u) << 32);
@@ -2958,14 +3003,8 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     unsigned int need_k = 0u;
     if (k > 0u && k < total_allowed) {
       unsigned int cum = 0u;
-      for (int h = 255; h >= 0; --h) {
-        if (cum + sh.cnt_hi[h] >= k) {
-          hi_k = h;
-          need_k = k - cum;
-          break;
-        }
-        cum += sh.cnt_hi[h];
-      }
+      hi_k = ScanDescWarp<unsigned int>(sh.cnt_hi, 255, 0, 0u, k, &cum);
+      need_k = k - cum;
     }
     // ---- pass 2: weights per high bin above hi_k; counts + weights per low
     // byte inside hi_k.  Key-count mode: dense rows whose high bytes above
@@ -3041,19 +3080,12 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
     int lo_k = 0;
     if (hi_k >= 0) {
       unsigned int cum = 0u;
-      for (int l = 255; l >= 0; --l) {
-        cum += sh.cnt_lo[l];
-        if (cum >= need_k) {
-          lo_k = l;
-          break;
-        }
-      }
+      const int l = ScanDescWarp<unsigned int>(sh.cnt_lo, 255, 0, 0u, need_k, &cum);
+      lo_k = l < 0 ? 0 : l;
     }
     unsigned long long s_k = 0ull;
-    for (int h = 255; h > hi_k; --h) s_k += sh.w_hi[h];
-    if (hi_k >= 0) {
-      for (int l = 255; l >= lo_k; --l) s_k += sh.w_lo[l];
-    }
+    ScanDescWarp<unsigned long long>(sh.w_hi, 255, hi_k + 1, 0ull, ~0ull, &s_k);  // (a sum: no index reaches ~0)
+    if (hi_k >= 0) ScanDescWarp<unsigned long long>(sh.w_lo, 255, lo_k, s_k, ~0ull, &s_k);
     // Threshold tau_p as (bin, low byte); lo_p < 0 = resolve with pass 3.
     int hi_p = hi_k, lo_p = lo_k;
     unsigned long long s_p = s_k;
@@ -3063,25 +3095,20 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
       // target = ceil(s_k * P24 / 2^24): high part via umul64hi of the product shifted by 40 (2^64 / 2^24)
       unsigned long long cum = 0ull;
       bool done = false;
-      for (int h = 255; h > hi_k && !done; --h) {
-        if (cum + sh.w_hi[h] >= target) {
-          hi_p = h;
-          lo_p = -1;
-          s_p = cum;  // plus the bin's part, after pass 3
-          done = true;
-        } else {
-          cum += sh.w_hi[h];
-        }
+      const int h = ScanDescWarp<unsigned long long>(sh.w_hi, 255, hi_k + 1, 0ull, target, &cum);
+      if (h >= 0) {
+        hi_p = h;
+        lo_p = -1;
+        s_p = cum;  // plus the bin's part, after pass 3
+        done = true;
       }
       if (!done && hi_k >= 0) {
-        for (int l = 255; l >= lo_k; --l) {
-          cum += sh.w_lo[l];
-          if (cum >= target) {
-            lo_p = l;
-            s_p = cum;
-            done = true;
-            break;
-          }
+        unsigned long long before = 0ull;
+        const int l = ScanDescWarp<unsigned long long>(sh.w_lo, 255, lo_k, cum, target, &before);
+        if (l >= 0) {
+          lo_p = l;
+          s_p = before + sh.w_lo[l];
+          done = true;
         }
       }
       if (lo_p < 0) {
@@ -3102,14 +3129,11 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
           });
         }
         __syncthreads();
-        unsigned long long c2 = cum;
-        for (int l = 255; l >= 0; --l) {
-          c2 += sh.w_lo2[l];
-          if (c2 >= target) {
-            lo_p = l;
-            s_p = c2;
-            break;
-          }
+        unsigned long long before = 0ull;
+        const int l = ScanDescWarp<unsigned long long>(sh.w_lo2, 255, 0, cum, target, &before);
+        if (l >= 0) {
+          lo_p = l;
+          s_p = before + sh.w_lo2[l];
         }
       }
     }
@@ -3125,15 +3149,8 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
       // are whole; the threshold bin counts low bytes >= lo_p.
       const int hb = hi_p;  // threshold bin (hi_p == hi_k when top-p is off)
       unsigned long long cum = 0ull;
-      int h_sel = -1;
-      for (int h = 255; h > hb; --h) {
-        const unsigned long long w = (hb == hi_k || h > hi_k) ? sh.w_hi[h] : 0ull;
-        if (r < cum + w) {
-          h_sel = h;
-          break;
-        }
-        cum += w;
-      }
+      // (every bin above hb >= hi_k is whole: r < cum + w  <=>  cum + w >= r + 1)
+      int h_sel = ScanDescWarp<unsigned long long>(sh.w_hi, 255, hb + 1, 0ull, r + 1ull, &cum);
       const unsigned long long* wl;
       int lmin = 0;
       if (h_sel < 0) {
@@ -3166,13 +3183,13 @@ __global__ void __launch_bounds__(kThreads) SampleKernel(AutView A, VocabView Vv
         __syncthreads();
         wl = sh.w_lo2;
       }
-      for (int l = 255; l >= lmin; --l) {
-        if (r < cum + wl[l]) {
+      {
+        unsigned long long before = 0ull;
+        const int l = ScanDescWarp<unsigned long long>(wl, 255, lmin, cum, r + 1ull, &before);
+        if (l >= 0) {
           kappa = (static_cast<uint32_t>(h_sel) << 8) | static_cast<uint32_t>(l);
-          jth = (r - cum) / SampleWeight(kappa, vmax, S.temperature);
-          break;
+          jth = (r - before) / SampleWeight(kappa, vmax, S.temperature);
         }
-        cum += wl[l];
       }
     }
     // ---- pass 5: the jth token (id order) with key kappa: contiguous chunk
