@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <string_view>
 #include <vector>
@@ -1176,7 +1177,7 @@ namespace {
 
 constexpr char kSnapMagic[8] = {'P', '3', 'G', 'M', 'C', 'T', 'X', '1'};
 constexpr uint32_t kSnapHeader = 96;
-constexpr uint32_t kSnapVersion = 2;
+constexpr uint32_t kSnapVersion = 3;  // 3: chunked payload checksum (SnapChecksum)
 
 struct SnapHeader {
   char magic[8];
@@ -1188,6 +1189,32 @@ struct SnapHeader {
 static_assert(sizeof(SnapHeader) == kSnapHeader, "snapshot header layout");
 
 constexpr int kSnapChunk = 1024;  // rows per gather/scatter launch
+
+// Payload checksum: Hash64 of every 16 MiB chunk (hashed on up to 16 host
+// threads), then Hash64 of those chunk hashes seeded with the length — the
+// load of a multi-GB table is not held up by one core hashing it.
+uint64_t SnapChecksum(const uint8_t* p, uint64_t n) {
+  constexpr uint64_t kChunk = 16ull << 20;
+  const size_t chunks = static_cast<size_t>((n + kChunk - 1) / kChunk);
+  std::vector<uint64_t> hs(chunks);
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned nt = static_cast<unsigned>(std::min<size_t>(hw, chunks));
+  auto work = [&](unsigned t) {
+    for (size_t c = t; c < chunks; c += nt) {
+      const uint64_t off = c * kChunk;
+      hs[c] = Hash64(p + off, static_cast<size_t>(std::min(kChunk, n - off)), 0x243F6A8885A308D3ull ^ c);
+    }
+  };
+  if (nt <= 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+  }
+  return Hash64(hs.data(), hs.size() * 8, 0x13198A2E03707344ull ^ n);
+}
 
 struct RowTables {
   std::vector<int32_t> meta, built, parent;
@@ -1292,7 +1319,7 @@ int gm_engine_snapshot_save(gm_engine* e, void* buf, uint64_t cap, uint64_t* siz
     h.n = static_cast<int32_t>(n);
     h.max_context = pre3::kMaxContext;
     h.payload_bytes = payload;
-    h.checksum = Hash64(out + kSnapHeader, payload);
+    h.checksum = SnapChecksum(out + kSnapHeader, payload);
     std::memcpy(out, &h, sizeof h);
     return GM_OK;
   });
@@ -1310,7 +1337,9 @@ int gm_engine_snapshot_load(gm_engine* e, const void* buf, uint64_t bytes) {
     }
     const uint8_t* in = static_cast<const uint8_t*>(buf);
     if (h.payload_bytes != bytes - kSnapHeader) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: size mismatch");
-    if (Hash64(in + kSnapHeader, h.payload_bytes) != h.checksum) return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: checksum");
+    if (SnapChecksum(in + kSnapHeader, h.payload_bytes) != h.checksum) {
+      return Fail(GM_ERR_CORRUPT_INPUT, "snapshot: checksum");
+    }
     if (h.grammar_hash != e->grammar_hash || h.layout_hash != e->layout_hash) {
       return Fail(GM_ERR_SNAPSHOT_MISMATCH, "snapshot: taken for another automaton");
     }
