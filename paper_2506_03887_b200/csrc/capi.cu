@@ -1242,27 +1242,70 @@ size_t SnapBlockWords(const gm_engine* e) {
 // Gathers (scatter = false: device -> host blocks) or scatters the rows'
 // blocks, kSnapChunk rows per launch through a device staging buffer.
 void SnapshotRows(gm_engine* e, const std::vector<int32_t>& ids, uint8_t* host, bool scatter) {
+  // Rows move in chunks of kSnapChunk through two pinned staging buffers:
+  // the host copy of one chunk overlaps the transfer and gather/scatter
+  // kernel of the other (the caller's buffer may be a pageable memory map).
   const size_t n = ids.size(), blk = SnapBlockWords(e);
   if (!n) return;
+  const size_t cbytes = static_cast<size_t>(kSnapChunk) * blk * 4;
   std::vector<void*> tmp;
-  try {
-    int32_t* d_ids = DevAlloc<int32_t>(kSnapChunk, &tmp);
-    uint32_t* d_blk = DevAlloc<uint32_t>(kSnapChunk * blk, &tmp);
-    for (size_t k0 = 0; k0 < n; k0 += kSnapChunk) {
-      const int m = static_cast<int>(std::min<size_t>(kSnapChunk, n - k0));
-      const size_t bytes = static_cast<size_t>(m) * blk * 4;
-      Check(cudaMemcpy(d_ids, ids.data() + k0, static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice), "snapshot");
-      if (scatter) Check(cudaMemcpy(d_blk, host, bytes, cudaMemcpyHostToDevice), "snapshot");
-      Check(pre3::LaunchSnapshotRows(e->cache, e->W, e->nseg, d_ids, m, d_blk, scatter, nullptr), "snapshot rows");
-      if (!scatter) Check(cudaMemcpy(host, d_blk, bytes, cudaMemcpyDeviceToHost), "snapshot");
-      Check(cudaDeviceSynchronize(), "snapshot rows");
-      host += bytes;
-    }
-  } catch (...) {
+  void* pinned[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  auto release = [&]() {
+    if (st) cudaStreamSynchronize(st);
     for (void* q : tmp) cudaFree(q);
+    for (void* q : pinned)
+      if (q) cudaFreeHost(q);
+    for (cudaEvent_t x : ev)
+      if (x) cudaEventDestroy(x);
+    if (st) cudaStreamDestroy(st);
+  };
+  try {
+    int32_t* d_ids[2] = {DevAlloc<int32_t>(kSnapChunk, &tmp), DevAlloc<int32_t>(kSnapChunk, &tmp)};
+    uint32_t* d_blk[2] = {DevAlloc<uint32_t>(kSnapChunk * blk, &tmp), DevAlloc<uint32_t>(kSnapChunk * blk, &tmp)};
+    for (int q = 0; q < 2; ++q) {
+      Check(cudaHostAlloc(&pinned[q], cbytes, cudaHostAllocDefault), "snapshot staging");
+      Check(cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming), "snapshot event");
+    }
+    Check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "snapshot stream");
+    const size_t chunks = (n + kSnapChunk - 1) / kSnapChunk;
+    auto rows = [&](size_t k) { return static_cast<int>(std::min<size_t>(kSnapChunk, n - k * kSnapChunk)); };
+    auto launch = [&](size_t k) {  // chunk k on the stream (staging buffer k % 2)
+      const int q = static_cast<int>(k & 1), m = rows(k);
+      const size_t bytes = static_cast<size_t>(m) * blk * 4;
+      Check(cudaMemcpyAsync(d_ids[q], ids.data() + k * kSnapChunk, static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice,
+                            st), "snapshot");
+      if (scatter) Check(cudaMemcpyAsync(d_blk[q], pinned[q], bytes, cudaMemcpyHostToDevice, st), "snapshot");
+      Check(pre3::LaunchSnapshotRows(e->cache, e->W, e->nseg, d_ids[q], m, d_blk[q], scatter, st), "snapshot rows");
+      if (!scatter) Check(cudaMemcpyAsync(pinned[q], d_blk[q], bytes, cudaMemcpyDeviceToHost, st), "snapshot");
+      Check(cudaEventRecord(ev[q], st), "snapshot event");
+    };
+    if (scatter) {
+      for (size_t k = 0; k < chunks; ++k) {
+        const int q = static_cast<int>(k & 1);
+        if (k >= 2) Check(cudaEventSynchronize(ev[q]), "snapshot");  // chunk k-2 has left this buffer
+        std::memcpy(pinned[q], host + k * cbytes, static_cast<size_t>(rows(k)) * blk * 4);
+        launch(k);
+      }
+    } else {
+      for (size_t k = 0; k < chunks; ++k) {
+        launch(k);  // (its buffer's previous chunk, k-2, was copied out last iteration)
+        if (k >= 1) {  // chunk k-1 is back in its buffer while chunk k runs
+          Check(cudaEventSynchronize(ev[(k - 1) & 1]), "snapshot");
+          std::memcpy(host + (k - 1) * cbytes, pinned[(k - 1) & 1], static_cast<size_t>(rows(k - 1)) * blk * 4);
+        }
+      }
+      const size_t k = chunks - 1;
+      Check(cudaEventSynchronize(ev[k & 1]), "snapshot");
+      std::memcpy(host + k * cbytes, pinned[k & 1], static_cast<size_t>(rows(k)) * blk * 4);
+    }
+    Check(cudaStreamSynchronize(st), "snapshot rows");
+  } catch (...) {
+    release();
     throw;
   }
-  for (void* q : tmp) cudaFree(q);
+  release();
 }
 
 }  // namespace
