@@ -194,7 +194,9 @@ int gm_batch_download(gm_batch* b, int32_t seq, int32_t* state, int32_t* status,
 int gm_batch_upload(gm_batch* b, int32_t seq, int32_t status, const int32_t* stack,
                     int32_t depth);
 /* Synchronizes `stream` and reports device-side errors (GM_ERR_STACK_OVERFLOW
- * if a mask walk overflowed its overlay); clears them. */
+ * if a mask walk overflowed its overlay; GM_ERR_CUDA if an accept's bounded
+ * wait for its fill's per-sequence items expired — an internal error, never
+ * raised by a sequence of calls this header allows); clears them. */
 int gm_batch_check(gm_batch* b, void* stream);
 /* counters[0..3] = restarts, total draws, mask fills, accepts */
 int gm_batch_counters(gm_batch* b, int64_t counters[4]);
