@@ -64,6 +64,9 @@
 #ifndef PRE3_LIGHT_BUILD_UNITS
 #define PRE3_LIGHT_BUILD_UNITS -1  // build units a light fill CTA takes before its items (-1: until none is left)
 #endif
+#ifndef PRE3_ARRIVE_FENCE
+#define PRE3_ARRIVE_FENCE 0  // (A/B) item arrivals behind a full __threadfence() instead of a release add
+#endif
 #ifndef PRE3_BULK_MASKED
 #define PRE3_BULK_MASKED 1  // fully masked spans as one bulk (TMA) store
 #endif
@@ -153,6 +156,19 @@ __device__ __forceinline__ T LoadAcquire(const T* p) {
 template <typename T>
 __device__ __forceinline__ void StoreRelease(T* p, T v) {
   cuda::atomic_ref<T, cuda::thread_scope_device>(*p).store(v, cuda::memory_order_release);
+}
+
+// Publishes an item's arrival: the group's (warp's / CTA's) stores were
+// ordered before the calling thread by the barrier that precedes this call,
+// and the release makes them visible with the count (MEMBAR.ALL, no L1
+// invalidate — a full __threadfence() is MEMBAR.SC + CCTL.IVALL).
+__device__ __forceinline__ int ArriveRelease(int* p) {
+#if PRE3_ARRIVE_FENCE
+  __threadfence();
+  return atomicAdd(p, 1);
+#else
+  return cuda::atomic_ref<int, cuda::thread_scope_device>(*p).fetch_add(1, cuda::memory_order_release);
+#endif
 }
 
 // Queue q of the batch, selected without indexing the by-value parameter
@@ -2072,10 +2088,9 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   // made visible first; the bulk logits stores follow.
   bool last = false;
   if (TAIL != kTailNone || F.publish_arrival == 1 || (F.publish_arrival == 2 && publish)) {
-    __threadfence();
     __syncwarp();
     int l = 0;
-    if (lane == 0) l = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
+    if (lane == 0) l = ArriveRelease(Bt.seq_arrive + b) == Vv.nseg - 1;
     last = __shfl_sync(0xffffffffu, l, 0) != 0;
   }
   if (MODE == kFillMask && F.logits != nullptr) {
@@ -2497,9 +2512,8 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
   // precedes the (bulk) logits stores below.
   bool last = false;
   if (TAIL != kTailNone || F.publish_arrival) {
-    __threadfence();
     __syncthreads();
-    if (tid == 0) sh.last = atomicAdd(Bt.seq_arrive + b, 1) == Vv.nseg - 1;
+    if (tid == 0) sh.last = ArriveRelease(Bt.seq_arrive + b) == Vv.nseg - 1;
     __syncthreads();
     last = sh.last;
   }
