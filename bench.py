@@ -722,9 +722,13 @@ def main(argv=None):
                                                       "sample": f"4 sequences x {max(2, steps_cpu // 4)} steps"}}
 
     info = eng.info()
+    split_launches = batch.split_step_launches
     kname = ("FillKernel<greedy> (mask + argmax over allowed logits; accept runs in AcceptKernel)" if greedy else
              "FillKernel (one-launch step: fill + -inf logits + sample/accept tail)" if args.one_launch else
+             "FillKernel (split step in one grid: fill + -inf logits, the sample/accept CTAs interleaved with "
+             "the light CTAs)" if split_launches == 1 else
              "FillKernel (fill + -inf logits; accept runs in AcceptKernel)")
+    launches_per_step = 2 if greedy else 1 if args.one_launch else split_launches
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wm,
         "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
@@ -738,11 +742,12 @@ def main(argv=None):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": kname,
                      "samples": nf, "alg_bytes_per_seq_step": alg_bytes_seq, "alg_bytes_rule": alg_rule,
+                     "timed_loop_frac": B * alg_bytes_seq / (elapsed_ms / K / 1e3) / 1e9 / peak,
                      "device_counted_logit_bytes_per_seq_step": {"read": logit_rd, "written": logit_wr}},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "check": check,
-        "gpu_launches": K * (1 if args.one_launch else 2),  # split / greedy: fill + accept per step
+        "gpu_launches": K * launches_per_step,  # greedy: fill + accept per step; split: gm_split_step_launches()
         "launch": (f"CUDA graph of {Kg} steps (one gm_graph_launch)" + (f" + {K - Kg} eager steps" if K > Kg else "")
                    if Kg else "eager, one ABI call per step"),
         "clocks": clocks.summary(),

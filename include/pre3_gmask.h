@@ -223,8 +223,8 @@ int gm_fill_and_mask_logits(gm_batch* b, uint32_t* bitmask, int64_t ld_words, ui
 int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
                           int64_t ld, uint64_t seed, int32_t* tokens_out, void* stream);
 
-/* The same step as two kernels: the fill, then the sample/accept/lookup
- * kernel, which overlaps it — a sequence whose mask is exactly its context's
+/* The same step with the sample/accept/lookup overlapping the fill — a
+ * sequence whose mask is exactly its context's
  * cached CI row (no context-dependent tokens) samples from that
  * row at once; the others start as soon as their own fill items are in.
  * Same results as gm_decode_step_stream.  seg_counts may be NULL (internal
@@ -233,6 +233,12 @@ int gm_decode_step_stream(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint
 int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words, uint16_t* logits_bf16,
                                 int64_t ld, int32_t* seg_counts, uint64_t seed, int32_t* tokens_out,
                                 void* stream);
+/* Kernel launches of one gm_decode_step_stream_split of this batch in the
+ * steady state: 1 when the accepts run as CTAs of the fill's grid
+ * (interleaved with its light CTAs; batches of at most ~16 light CTAs per SM,
+ * B x segments <= 128 x SMs), else 2 (the fill + a programmatically dependent
+ * accept kernel); -GM_ERR_USAGE for a NULL batch. */
+int gm_batch_split_step_launches(gm_batch* b);
 
 /* Engine::AllowedTerminals (runtime.cpp:188-208) for every sequence: the
  * exact next-byte set plus $ — terminal t is allowed iff an edge of the

@@ -129,6 +129,7 @@ def lib() -> ctypes.CDLL:
             "gm_batch_download": ([P, I32, P, P, P, I32, P], ctypes.c_int),
             "gm_batch_upload": ([P, I32, I32, P, I32], ctypes.c_int),
             "gm_batch_check": ([P, P], ctypes.c_int),
+            "gm_batch_split_step_launches": ([P], ctypes.c_int),
             "gm_batch_counters": ([P, P], ctypes.c_int),
             "gm_batch_fill_stats": ([P, P], ctypes.c_int),
             "gm_batch_set_stats": ([P, I32], ctypes.c_int),
@@ -663,6 +664,12 @@ class Batch:
 
     def check(self, stream=None):
         _check(lib().gm_batch_check(self._h, _stream(stream)))
+
+    @property
+    def split_step_launches(self) -> int:
+        """Kernels one decode_step_stream_split launches (1: the accepts run
+        as CTAs of the fill's grid; 2: fill + accept kernel)."""
+        return int(lib().gm_batch_split_step_launches(self._h))
 
     def counters(self) -> dict:
         out = np.zeros(4, np.int64)

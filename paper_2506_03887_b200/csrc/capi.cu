@@ -186,6 +186,18 @@ struct gm_batch {
     slots_valid = true;
     return prod;
   }
+  int sms = 148;  // the device's SM count
+  // Split step in one grid (the accepts as CTAs among the fill's light CTAs)
+  // when the light CTAs (8 items each) are at most 16 per SM, about four
+  // waves: measured +9-11% steps/s at 256 and 1,024 sequences (the PDL accept
+  // grid only starts with the fill's last wave); at 4,096 sequences (14
+  // waves) the accept kernel after the fill is 1% faster — it starts late
+  // relative to a long fill, and merged accepts of context-dependent
+  // sequences would hold CTA slots while their items are walked.
+  bool OneGridSplit() const {
+    return PRE3_SPLIT_ONE_GRID &&
+           static_cast<int64_t>(view.B) * engine->nseg <= static_cast<int64_t>(8) * 16 * sms;
+  }
   cudaStream_t capture_stream = nullptr;  // graph capture (the legacy stream cannot capture)
   std::vector<void*> owned;
   ~gm_batch() {
@@ -628,6 +640,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
     v.build_grid = sms * 4;
     v.h_grid = std::min(v.h_cap, PRE3_HEAVY_PER_SM * sms);
+    b->sms = sms;
     b->seg_counts = DevAlloc<int32_t>(bn * 2, &b->owned);
     b->scratch_mask = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     b->best = DevAlloc<unsigned long long>(static_cast<size_t>(batch), &b->owned);
@@ -855,12 +868,15 @@ int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words
     f.publish_arrival = 2;
     b->ClearArrivals(s);
     b->BeginFill(&f);
-    b->FillStart(s);
-    Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s),
-          "fill launch");
-    b->FillEnd(s);
+    const bool one_grid = b->OneGridSplit();
+    if (!one_grid) {
+      b->FillStart(s);
+      Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s),
+            "fill launch");
+      b->FillEnd(s);
+    }
     b->EndFill(false);
-    pre3::AcceptArgs g{};
+    pre3::AcceptArgs& g = f.acc;
     g.restart = 1;
     g.bitmask = f.bitmask;
     g.ldw = f.ldw;
@@ -872,9 +888,23 @@ int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words
     g.lookup_tag = b->fill_seq;
     g.wait_fill = 1;
     g.ci_shortcut = 1;
-    Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, g, s), "accept launch");
+    if (one_grid) {
+      // One grid: the accept CTAs run among the light CTAs (FillArgs::accept_ctas).
+      f.accept_ctas = 1;
+      b->FillStart(s);
+      Check(pre3::LaunchFill(pre3::kFillMask, pre3::kTailNone, e->aut, e->vocab, e->cache, b->view, f, s),
+            "fill launch");
+      b->FillEnd(s);
+    } else {
+      Check(pre3::LaunchAccept(pre3::kSampleStream, e->aut, e->vocab, e->cache, b->view, g, s), "accept launch");
+    }
     return GM_OK;
   });
+}
+
+int gm_batch_split_step_launches(gm_batch* b) {
+  if (!b) return -Fail(GM_ERR_USAGE, "null batch");
+  return b->OneGridSplit() ? 1 : 2;
 }
 
 int gm_allowed_terminals(gm_batch* b, uint32_t* out, void* stream) {

@@ -19,6 +19,7 @@
 //
 // Integer/bit work only: no tensor cores (nothing here is a contraction).
 #include <cuda/atomic>
+#include <algorithm>
 #include <utility>
 
 #include "kernels.cuh"
@@ -63,6 +64,9 @@
 #endif
 #ifndef PRE3_LIGHT_BUILD_UNITS
 #define PRE3_LIGHT_BUILD_UNITS -1  // build units a light fill CTA takes before its items (-1: until none is left)
+#endif
+#ifndef PRE3_ACCEPT_SPREAD
+#define PRE3_ACCEPT_SPREAD 5  // merged split step: accept CTAs interleaved over this many eighths of the light CTAs
 #endif
 #ifndef PRE3_ARRIVE_FENCE
 #define PRE3_ARRIVE_FENCE 0  // (A/B) item arrivals behind a full __threadfence() instead of a release add
@@ -1361,6 +1365,11 @@ __global__ void __launch_bounds__(kThreads) DrainKernel(AutView A, VocabView Vv,
 }
 
 // ---------------------------------------------------------------------------
+// Defined with AcceptKernel below; the split step's fill runs it too.
+template <int SAMPLE>
+__device__ __forceinline__ void AcceptSeq(const AutView& A, const VocabView& Vv, const CacheView& Cc,
+                                          const BatchView& Bt, const AcceptArgs& G, int b, int lane);
+
 namespace {
 
 constexpr int kWarps = kThreads / 32;     // light items per fill CTA
@@ -1731,10 +1740,23 @@ __device__ __forceinline__ void SequenceTail(const AutView& A, const VocabView& 
 // ready context slot, few or no context-dependent tokens).  Lane j owns mask
 // words j, 32+j, ..., 224+j of the segment (registers m[]); span i = words
 // [32i, 32i+32) = tokens t0 + [1024i, 1024i+1024).  No CTA barriers.
+// Split step in one grid (FillArgs::accept_ctas): the arrivals sequence b's
+// accept needs — its heavy segments of a built shared slot, else every
+// segment (AcceptSeq's ci_shortcut test; the fill's `publish`).  None: an
+// accept CTA runs it; otherwise the item completing them does, so nothing
+// in the grid ever waits for another CTA's items.
+__device__ __forceinline__ int ArrivalsNeeded(const CacheView& Cc, const VocabView& Vv, int slot, uint32_t hmask) {
+  if (slot >= 0 && slot < Cc.C && Vv.nseg <= 32) {
+    const uint32_t all = Vv.nseg >= 32 ? 0xffffffffu : ((1u << Vv.nseg) - 1u);
+    return __popc(hmask & all);
+  }
+  return Vv.nseg;
+}
+
 template <int MODE, int TAIL>
 __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv, const CacheView& Cc,
                                           const BatchView& Bt, const FillArgs& F, int b, int seg, int slot,
-                                          bool pure, bool publish, int lane, uint4 (*span_buf)[4][32],
+                                          bool pure, bool publish, int need, int lane, uint4 (*span_buf)[4][32],
                                           const uint4* ninf) {
   const unsigned long long t_in = Bt.trace ? NowNs() : 0ull;
   const int w0 = seg * kSegWords;
@@ -2090,7 +2112,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   if (TAIL != kTailNone || F.publish_arrival == 1 || (F.publish_arrival == 2 && publish)) {
     __syncwarp();
     int l = 0;
-    if (lane == 0) l = ArriveRelease(Bt.seq_arrive + b) == Vv.nseg - 1;
+    if (lane == 0) l = ArriveRelease(Bt.seq_arrive + b) == need - 1;
     last = __shfl_sync(0xffffffffu, l, 0) != 0;
   }
   if (MODE == kFillMask && F.logits != nullptr) {
@@ -2262,6 +2284,9 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
     }
   }
   if (TAIL != kTailNone && last) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
+  if constexpr (PRE3_SPLIT_ONE_GRID && MODE == kFillMask && TAIL == kTailNone) {
+    if (F.accept_ctas > 0 && last) AcceptSeq<kSampleStream>(A, Vv, Cc, Bt, F.acc, b, lane);
+  }
 }
 
 }  // namespace
@@ -2309,6 +2334,23 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
   const int32_t* hidx = HeavyIndex(Bt, F.fill_no, Vv.nseg);
 
   if (bid >= Bt.h_grid) {
+    int r = bid - Bt.h_grid;
+    if constexpr (PRE3_SPLIT_ONE_GRID && MODE == kFillMask && TAIL == kTailNone) {
+      // ---- split step in one grid: accept CTA i sits after light CTA
+      // (i + 1) * accept_period - 1, so the accepts run while the light pass
+      // streams (a separate accept grid only starts with the fill's last wave).
+      const int P = F.accept_period, q = r / (P + 1);
+      if (F.accept_ctas > 0 && q < F.accept_ctas && r - q * (P + 1) == P) {
+        const int b = q * kWarps + warp;
+        // Sequences whose mask is their slot's CI row (no arrivals needed);
+        // the others are accepted by the item completing their arrivals.
+        if (b < Bt.B && ArrivalsNeeded(Cc, Vv, SeqSlot(Bt, F.fill_no)[b], SeqHmask(Bt, F.fill_no)[b]) == 0) {
+          AcceptSeq<kSampleStream>(A, Vv, Cc, Bt, F.acc, b, lane);
+        }
+        return;
+      }
+      if (F.accept_ctas > 0) r -= min(q, F.accept_ctas);
+    }
     // ---- light pass.  Loads that only depend on (b, seg) are issued together.
     if (MODE == kFillMask && F.logits != nullptr) {
       for (int i = tid; i < 128 * PRE3_BULK_RUN; i += kThreads) {
@@ -2319,7 +2361,7 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
       }
       __syncthreads();
     }
-    const int item = (bid - Bt.h_grid) * F.light_per_cta + warp;
+    const int item = r * F.light_per_cta + warp;
     const bool in_range = warp < F.light_per_cta && item < Bt.B * Vv.nseg;
     const int b = in_range ? item / Vv.nseg : 0;
     const int seg = item - b * Vv.nseg;
@@ -2350,7 +2392,10 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
     // segments publish arrivals — its accept takes the other segments from the
     // slot's CI row (AcceptKernel's ci_shortcut, the same test).
     const bool publish = !shared_ok || ((hmask >> seg) & 1u);
-    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, publish, lane, span_buf[warp], ninf_buf);
+    // Arrivals that complete the sequence: its accept's (split step in one
+    // grid), else every segment (the fused tail's).
+    const int need = F.accept_ctas > 0 ? ArrivalsNeeded(Cc, Vv, slot, hmask) : Vv.nseg;
+    LightItem<MODE, TAIL>(A, Vv, Cc, Bt, F, b, seg, slot, pure, publish, need, lane, span_buf[warp], ninf_buf);
     return;
   }
 
@@ -2513,7 +2558,12 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
   bool last = false;
   if (TAIL != kTailNone || F.publish_arrival) {
     __syncthreads();
-    if (tid == 0) sh.last = ArriveRelease(Bt.seq_arrive + b) == Vv.nseg - 1;
+    if (tid == 0) {
+      const int need = F.accept_ctas > 0
+                           ? ArrivalsNeeded(Cc, Vv, SeqSlot(Bt, F.fill_no)[b], SeqHmask(Bt, F.fill_no)[b])
+                           : Vv.nseg;
+      sh.last = ArriveRelease(Bt.seq_arrive + b) == need - 1;
+    }
     __syncthreads();
     last = sh.last;
   }
@@ -2540,6 +2590,9 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
   if (tid == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
   if (tid == 0) TraceEvent(Bt, kTraceHeavy, b, seg, t_in, n_walks);
   if (TAIL != kTailNone && last && warp == 0) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
+  if constexpr (PRE3_SPLIT_ONE_GRID && MODE == kFillMask && TAIL == kTailNone) {
+    if (F.accept_ctas > 0 && last && warp == 0) AcceptSeq<kSampleStream>(A, Vv, Cc, Bt, F.acc, b, lane);
+  }
 }
 // ---------------------------------------------------------------------------
 // AcceptKernel: one warp per sequence (standalone accept / sample).
@@ -2549,6 +2602,57 @@ __device__ __forceinline__ void AcceptBody(const AutView& A, const VocabView& Vv
                                            const BatchView& Bt, const AcceptArgs& G, int b, SeqState st, int topv,
                                            const uint32_t* row, const int32_t* counts, const uint32_t* crow,
                                            const int32_t* ccounts, uint32_t hm, int lane, unsigned long long t_in);
+
+// One sequence's sample + accept (+ the next fill's lookup), one warp: the
+// body of AcceptKernel, and of the accept CTAs a split-step fill carries
+// (FillArgs::accept_ctas).  wait_fill: the fill producing this step's items
+// is still running — wait only for this sequence's (heavy) items.
+template <int SAMPLE>
+__device__ __forceinline__ void AcceptSeq(const AutView& A, const VocabView& Vv, const CacheView& Cc,
+                                          const BatchView& Bt, const AcceptArgs& G, int b, int lane) {
+  // The sequence's state and stack window are not written by the fill:
+  // their loads overlap the wait for its items.
+  const SeqState st = Bt.seq[b];
+  const int topv = StackWindow(Bt, b, st.depth, lane);
+  const uint32_t* row = G.bitmask + static_cast<long long>(b) * G.ldw;
+  const int32_t* counts = G.seg_counts + static_cast<long long>(b) * Vv.nseg * 2;
+  const uint32_t* crow = row;
+  const int32_t* ccounts = counts;
+  uint32_t hm = ~0u;  // segments read from the fill's outputs (the rest: the context's CI row)
+  int need = Vv.nseg;
+  if (G.ci_shortcut) {
+    // A built shared slot (the fill's own test, FillKernel): the segments
+    // without context-dependent tokens are the slot's CI row and counts —
+    // sample from those now; wait only for the heavy segments' items (the
+    // only ones that publish arrivals).  Pure CI: no wait at all.
+    const int slot = SeqSlot(Bt, PrevFill(G.lookup_tag))[b];
+    const uint32_t hmask = SeqHmask(Bt, PrevFill(G.lookup_tag))[b];
+    if (slot >= 0 && slot < Cc.C && Vv.nseg <= 32) {
+      const uint32_t all = Vv.nseg >= 32 ? 0xffffffffu : ((1u << Vv.nseg) - 1u);
+      hm = hmask & all;
+      need = __popc(hm);
+      crow = Cc.ci + static_cast<long long>(slot) * Vv.W;
+      ccounts = Cc.ci_cnt + static_cast<long long>(slot) * Vv.nseg * 2;
+    }
+  }
+  if (G.wait_fill && need > 0) {
+    // Bounded (200 ms): a fill that never delivers the items would be an
+    // internal error — reported through gm_batch_check, never a hung GPU.
+    if (LoadAcquire(Bt.seq_arrive + b) < need) {
+      unsigned long long t_start, t_now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+      do {
+        __nanosleep(64);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+      } while (LoadAcquire(Bt.seq_arrive + b) < need && t_now - t_start < 200000000ull);
+      if (t_now - t_start >= 200000000ull && lane == 0) atomicOr(Bt.err, 2u);
+    }
+    __syncwarp();
+    if (lane == 0) Bt.seq_arrive[b] = 0;
+  }
+  AcceptBody<SAMPLE>(A, Vv, Cc, Bt, G, b, st, topv, row, counts, crow, ccounts, hm, lane,
+                     Bt.trace ? NowNs() : 0ull);
+}
 
 template <int SAMPLE>
 __global__ void PRE3_ACCEPT_BOUNDS AcceptKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
@@ -2564,50 +2668,7 @@ __global__ void PRE3_ACCEPT_BOUNDS AcceptKernel(AutView A, VocabView Vv, CacheVi
   }
   const int lane = threadIdx.x & 31;
   const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (b < Bt.B) {
-    // The sequence's state and stack window are not written by the fill:
-    // their loads overlap the wait for its items.
-    const SeqState st = Bt.seq[b];
-    const int topv = StackWindow(Bt, b, st.depth, lane);
-    const uint32_t* row = G.bitmask + static_cast<long long>(b) * G.ldw;
-    const int32_t* counts = G.seg_counts + static_cast<long long>(b) * Vv.nseg * 2;
-    const uint32_t* crow = row;
-    const int32_t* ccounts = counts;
-    uint32_t hm = ~0u;  // segments read from the fill's outputs (the rest: the context's CI row)
-    int need = Vv.nseg;
-    if (G.ci_shortcut) {
-      // A built shared slot (the fill's own test, FillKernel): the segments
-      // without context-dependent tokens are the slot's CI row and counts —
-      // sample from those now; wait only for the heavy segments' items (the
-      // only ones that publish arrivals).  Pure CI: no wait at all.
-      const int slot = SeqSlot(Bt, PrevFill(G.lookup_tag))[b];
-      const uint32_t hmask = SeqHmask(Bt, PrevFill(G.lookup_tag))[b];
-      if (slot >= 0 && slot < Cc.C && Vv.nseg <= 32) {
-        const uint32_t all = Vv.nseg >= 32 ? 0xffffffffu : ((1u << Vv.nseg) - 1u);
-        hm = hmask & all;
-        need = __popc(hm);
-        crow = Cc.ci + static_cast<long long>(slot) * Vv.W;
-        ccounts = Cc.ci_cnt + static_cast<long long>(slot) * Vv.nseg * 2;
-      }
-    }
-    if (G.wait_fill && need > 0) {
-      // Bounded (200 ms): a fill that never delivers the items would be an
-      // internal error — reported through gm_batch_check, never a hung GPU.
-      if (LoadAcquire(Bt.seq_arrive + b) < need) {
-        unsigned long long t_start, t_now;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-        do {
-          __nanosleep(64);
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
-        } while (LoadAcquire(Bt.seq_arrive + b) < need && t_now - t_start < 200000000ull);
-        if (t_now - t_start >= 200000000ull && lane == 0) atomicOr(Bt.err, 2u);
-      }
-      __syncwarp();
-      if (lane == 0) Bt.seq_arrive[b] = 0;
-    }
-    AcceptBody<SAMPLE>(A, Vv, Cc, Bt, G, b, st, topv, row, counts, crow, ccounts, hm, lane,
-                       Bt.trace ? NowNs() : 0ull);
-  }
+  if (b < Bt.B) AcceptSeq<SAMPLE>(A, Vv, Cc, Bt, G, b, lane);
   if (G.wait_fill) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
@@ -3530,7 +3591,16 @@ static void LaunchFillT(const AutView& a, const VocabView& v, const CacheView& c
   const unsigned items = static_cast<unsigned>(v.nseg) * static_cast<unsigned>(b.B);
   FillArgs g = f;
   g.light_per_cta = LightPerCta(items);
-  const unsigned grid = static_cast<unsigned>(b.h_grid) + (items + g.light_per_cta - 1) / g.light_per_cta;
+  const unsigned light = (items + g.light_per_cta - 1) / g.light_per_cta;
+  unsigned grid = static_cast<unsigned>(b.h_grid) + light;
+  if (g.accept_ctas > 0) {
+    // Accept CTAs spread over the first PRE3_ACCEPT_SPREAD/8 of the light
+    // CTAs: every accept is done well before the light pass ends.
+    g.accept_ctas = (b.B + kWarps - 1) / kWarps;
+    const unsigned span = std::max(1u, light * PRE3_ACCEPT_SPREAD / 8u);
+    g.accept_period = static_cast<int>(std::max(1u, span / static_cast<unsigned>(g.accept_ctas)));
+    grid += static_cast<unsigned>(g.accept_ctas);
+  }
   Launch(FillKernel<MODE, TAIL>, dim3(grid), dim3(kThreads), dyn, s, a, v, c, b, g);
 }
 

@@ -157,9 +157,31 @@ struct BatchView {
 
 enum TraceKind { kTraceLight = 1, kTraceHeavy = 2, kTraceTail = 3, kTraceAccept = 4 };
 
+#ifndef PRE3_SPLIT_ONE_GRID
+#define PRE3_SPLIT_ONE_GRID 1  // split step: the accepts as CTAs of the fill's grid (0: a PDL accept kernel)
+#endif
+
 enum FillMode { kFillMask = 0, kFillGreedy = 1 };
 enum FillTail { kTailNone = 0, kTailStream = 1, kTailGreedy = 2 };
 enum SampleMode { kSampleGiven = 0, kSampleStream = 1, kSampleGreedy = 2 };
+
+struct AcceptArgs {
+  const int32_t* tokens;
+  int32_t* status_out;
+  int restart;
+  const uint32_t* bitmask;
+  long long ldw;
+  const int32_t* seg_counts;
+  unsigned long long seed;
+  unsigned long long* best;
+  int32_t* tokens_out;
+  int do_accept;     // 0: sample only
+  int lookup_queue;  // >= 0: assign next-fill context slots into this queue
+  int lookup_tag;    // number of the fill that consumes it
+  int wait_fill;     // overlap the preceding fill (publish_arrival): per-sequence start
+  int ci_shortcut;   // with wait_fill, bitmask/seg_counts from that fill, unmodified: a pure-CI
+                     // sequence samples from its slot's CI row and counts without waiting
+};
 
 struct FillArgs {
   uint32_t* bitmask;        // [B][ldw] (never null with a tail)
@@ -181,25 +203,13 @@ struct FillArgs {
   int vec_ok;               // set by LaunchFill
   int light_per_cta;        // light items per CTA (<= kThreads/32; set by LaunchFill so the
                             // light CTAs fill whole waves of the SMs' CTA slots)
+  int accept_ctas;          // split step in one grid: this many CTAs (kThreads/32 sequences
+                            // each) run AcceptSeq with `acc`, one after every accept_period
+                            // light CTAs (set by LaunchFill; 0: none)
+  int accept_period;
+  AcceptArgs acc;
 };
 
-struct AcceptArgs {
-  const int32_t* tokens;
-  int32_t* status_out;
-  int restart;
-  const uint32_t* bitmask;
-  long long ldw;
-  const int32_t* seg_counts;
-  unsigned long long seed;
-  unsigned long long* best;
-  int32_t* tokens_out;
-  int do_accept;     // 0: sample only
-  int lookup_queue;  // >= 0: assign next-fill context slots into this queue
-  int lookup_tag;    // number of the fill that consumes it
-  int wait_fill;     // overlap the preceding fill (publish_arrival): per-sequence start
-  int ci_shortcut;   // with wait_fill, bitmask/seg_counts from that fill, unmodified: a pure-CI
-                     // sequence samples from its slot's CI row and counts without waiting
-};
 
 struct SampleArgs {
   const uint32_t* bitmask;   // [B][ldw], from a preceding fill

@@ -121,6 +121,26 @@ if a.chain:
         print(f"  fill {k}: light start {lo:7.1f}..{hi:7.1f}  light end max {lend[sel].max():7.1f}  "
               f"accepts ended by then: {int((acc_end <= lo).sum())}")
     print("  accept end times (sorted, every 256th):", " ".join(f"{x:.1f}" for x in acc_end[::256]))
+    # Per step: accept records come B per step; a fill's items start after
+    # the previous step's accepts ended (its grid waits for them).
+    acc = rec[kind == 4]
+    acc = acc[np.argsort(acc[:, 2])]
+    ends = [(acc[(k + 1) * B - 1, 2] - t0) / 1e3 for k in range(len(acc) // B)]
+    prev = -1e9
+    print("  step: heavy start / light start..end / accept start..end (us); gap = this fill's first item - previous accept end")
+    for k, e in enumerate(ends):
+        def sel(kd):
+            r = rec[kind == kd]
+            st = (r[:, 1] - t0) / 1e3
+            m = (st > prev) & (st <= e)
+            return r[m], st[m]
+        hr, hs = sel(2)
+        lr, ls = sel(1)
+        a_r = acc[k * B:(k + 1) * B]
+        first = min(hs.min() if len(hs) else 1e9, ls.min() if len(ls) else 1e9)
+        print(f"  {k}: heavy {hs.min() if len(hs) else float('nan'):7.1f} light {ls.min():7.1f}..{((lr[:, 2] - t0) / 1e3).max():7.1f}"
+              f"  accept {((a_r[:, 1] - t0) / 1e3).min():7.1f}..{e:7.1f}  gap {first - prev if prev > 0 else float('nan'):5.1f}")
+        prev = e
 
 if a.per_sm:
     # Per-SM view of the last traced step's light items (extra = walks |

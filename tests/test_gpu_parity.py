@@ -477,12 +477,13 @@ def test_allowed_terminals_matches_port(vectors, name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("grammar,flavor,K", [("json", 0, 16), ("schema", 0, 16)])
-def test_split_step_large_batch(grammar, flavor, K):
+@pytest.mark.parametrize("grammar,flavor,K,B", [("json", 0, 16, 1024), ("schema", 0, 16, 1024), ("json", 0, 16, 1536)])
+def test_split_step_large_batch(grammar, flavor, K, B):
     """gm_decode_step_stream_split at a batch that fills several waves (the
-    accept kernel overlaps the fill and pure-CI sequences sample from the
-    context cache): tokens, masks and stacks equal the two-call loop's, and
-    the first 48 sequences' tokens equal the C port's."""
+    accepts overlap the fill and pure-CI sequences sample from the context
+    cache; 1,024 sequences: accept CTAs inside the fill's grid, 1,536: the
+    separate accept kernel): tokens, masks and stacks equal the two-call
+    loop's, and the first 48 sequences' tokens equal the C port's."""
     if grammar == "json":
         f = flat("json")
     else:
@@ -491,7 +492,9 @@ def test_split_step_large_batch(grammar, flavor, K):
     vocab = pk.synth_vocab(128255, flavor)
     eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
     eng.prewarm(512, 200, seed=0xC0FFEE)
-    B, steps, seed = 1024, 8, 13
+    steps, seed = 8, 13
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert eng.batch(B).split_step_launches == (1 if B * eng.info()["num_segments"] <= 128 * sms else 2)
     b1, m1, t1 = run_stream(eng, B, steps, seed, fused="split", check_logits=True)
     b2, m2, t2 = run_stream(eng, B, steps, seed)
     assert np.array_equal(t1, t2)
