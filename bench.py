@@ -683,7 +683,19 @@ def main(argv=None):
     else:
         alg_bytes_seq = 2 * V1 + 8 * W  # write-only -inf formulation
         alg_rule = "2(V+1) (-inf row write) + 8W (bitmask write + CI read); mixed-chunk reads not counted"
-    achieved = B * alg_bytes_seq / (fill_ms / 1e3) / 1e9
+    # The roofline kernel's launch duration: when it is the step's only
+    # kernel (the one-grid split step, the one-launch step) the timed loop's
+    # time per launch (consecutive launches pipelined by PDL, as in a decode
+    # loop); otherwise the isolated launches of the sub-loop above (the accept
+    # kernel cannot overlap them).  Both are reported.
+    split_launches = batch.split_step_launches
+    launches_per_step = 2 if greedy else 1 if args.one_launch else split_launches
+    kernel_ms = elapsed_ms / K if launches_per_step == 1 else fill_ms
+    duration_src = ("timed loop: elapsed / launches (the step is one launch of this kernel)"
+                    if launches_per_step == 1 else
+                    "isolated launches (events around each fill in a sub-loop; mean)")
+    achieved = B * alg_bytes_seq / (kernel_ms / 1e3) / 1e9
+    isolated_frac = B * alg_bytes_seq / (fill_ms / 1e3) / 1e9 / peak
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -722,13 +734,11 @@ def main(argv=None):
                                                       "sample": f"4 sequences x {max(2, steps_cpu // 4)} steps"}}
 
     info = eng.info()
-    split_launches = batch.split_step_launches
     kname = ("FillKernel<greedy> (mask + argmax over allowed logits; accept runs in AcceptKernel)" if greedy else
              "FillKernel (one-launch step: fill + -inf logits + sample/accept tail)" if args.one_launch else
              "FillKernel (split step in one grid: fill + -inf logits, the sample/accept CTAs interleaved with "
              "the light CTAs)" if split_launches == 1 else
              "FillKernel (fill + -inf logits; accept runs in AcceptKernel)")
-    launches_per_step = 2 if greedy else 1 if args.one_launch else split_launches
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wm,
         "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
@@ -742,6 +752,8 @@ def main(argv=None):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": kname,
                      "samples": nf, "alg_bytes_per_seq_step": alg_bytes_seq, "alg_bytes_rule": alg_rule,
+                     "duration_us": 1e3 * kernel_ms, "duration_source": duration_src,
+                     "isolated_launch_frac": isolated_frac,
                      "timed_loop_frac": B * alg_bytes_seq / (elapsed_ms / K / 1e3) / 1e9 / peak,
                      "device_counted_logit_bytes_per_seq_step": {"read": logit_rd, "written": logit_wr}},
         "cpu_baseline": cpu,

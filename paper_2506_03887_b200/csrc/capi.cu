@@ -196,7 +196,7 @@ struct gm_batch {
   // sequences would hold CTA slots while their items are walked.
   bool OneGridSplit() const {
     return PRE3_SPLIT_ONE_GRID &&
-           static_cast<int64_t>(view.B) * engine->nseg <= static_cast<int64_t>(8) * 16 * sms;
+           static_cast<int64_t>(view.B) * engine->nseg <= static_cast<int64_t>(8) * PRE3_ONE_GRID_CTAS_PER_SM * sms;
   }
   cudaStream_t capture_stream = nullptr;  // graph capture (the legacy stream cannot capture)
   std::vector<void*> owned;

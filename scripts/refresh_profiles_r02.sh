@@ -27,7 +27,7 @@ for c in 2 3 4 5; do
   python scripts/launches.py $Q/c${c}_launches.csv > $P/r02_c${c}_launches_summary.txt
   summ $Q/c${c}_fill.ncu-rep > $P/r02_c${c}_fill_summary.txt
 done
-[ -f $Q/c2_accept.ncu-rep ] && summ $Q/c2_accept.ncu-rep > $P/r02_c2_accept_summary.txt
+[ -f $Q/c4_accept.ncu-rep ] && summ $Q/c4_accept.ncu-rep > $P/r02_c4_accept_summary.txt && rm -f $P/r02_c2_accept_summary.txt
 summ $Q/sample.ncu-rep > $P/r02_sample_summary.txt
 cp $Q/c3_fill.ncu-rep $P/r02_c3_fill.ncu-rep
 python - <<'PY'
