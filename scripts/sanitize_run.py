@@ -36,6 +36,8 @@ def check_stacks(batch, stk, B):
 def stream(kind, slots=1024, parent=0, K=8, B=24, steps=10, seed=5):
     eng = pk.DeviceEngine(pk.Automaton.load(FLAT), VOCAB, context_depth=K, context_slots=slots, parent_depth=parent)
     batch = eng.batch(B)
+    if kind == "split":
+        print(f"split step: {batch.split_step_launches} launch(es) at B = {B}")
     bm = torch.zeros((B, eng.W), dtype=torch.int32, device=DEV)
     cnt = torch.zeros((B, 2 * batch.nseg), dtype=torch.int32, device=DEV)
     lg = torch.randn((B, eng.V + 1), dtype=torch.bfloat16, device=DEV)
@@ -196,6 +198,7 @@ def refill(B=16, K=2):
 PARTS = {
     "two_call": lambda: stream("two_call"),
     "split": lambda: stream("split"),
+    "split_two_grid": lambda: stream("split", B=6400, steps=2),  # past the one-grid limit (B x 3 segments > 128 x SMs)
     "one_launch": lambda: stream("one_launch"),
     "tiny_table": lambda: stream("split", slots=4),
     "parents": lambda: stream("split", parent=3, K=12),
