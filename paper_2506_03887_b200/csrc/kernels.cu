@@ -2109,7 +2109,7 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
   // ---- arrival (fused tail): mask words, counts and argmax partials are
   // made visible first; the bulk logits stores follow.
   bool last = false;
-  if (TAIL != kTailNone || F.publish_arrival == 1 || (F.publish_arrival == 2 && publish)) {
+  if (FusedTail(TAIL) || F.publish_arrival == 1 || (F.publish_arrival == 2 && publish)) {
     __syncwarp();
     int l = 0;
     if (lane == 0) l = ArriveRelease(Bt.seq_arrive + b) == need - 1;
@@ -2283,8 +2283,10 @@ __device__ __forceinline__ void LightItem(const AutView& A, const VocabView& Vv,
                      (static_cast<unsigned long long>(bytes) << 40));
     }
   }
-  if (TAIL != kTailNone && last) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
-  if constexpr (PRE3_SPLIT_ONE_GRID && MODE == kFillMask && TAIL == kTailNone) {
+  if constexpr (FusedTail(TAIL)) {
+    if (last) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
+  }
+  if constexpr (TAIL == kTailSplit) {
     if (F.accept_ctas > 0 && last) AcceptSeq<kSampleStream>(A, Vv, Cc, Bt, F.acc, b, lane);
   }
 }
@@ -2309,8 +2311,9 @@ struct FillShared {
 // Every CTA first helps drain the build queue of new contexts (empty in the
 // steady state).
 template <int MODE, int TAIL>
-__global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView Cc, BatchView Bt,
-                                                          FillArgs F) {
+__global__ void PRE3_FILL_BOUNDS FillKernel(const __grid_constant__ AutView A, const __grid_constant__ VocabView Vv,
+                                            const __grid_constant__ CacheView Cc, const __grid_constant__ BatchView Bt,
+                                            const __grid_constant__ FillArgs F) {
   PdlEnter();
   __shared__ FillShared sh;
   __shared__ uint4 span_buf[kWarps][2][4][32];  // light pass: per-warp double buffer of mixed chunks (32 KB)
@@ -2335,7 +2338,7 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
 
   if (bid >= Bt.h_grid) {
     int r = bid - Bt.h_grid;
-    if constexpr (PRE3_SPLIT_ONE_GRID && MODE == kFillMask && TAIL == kTailNone) {
+    if constexpr (TAIL == kTailSplit) {
       // ---- split step in one grid: accept CTA i sits after light CTA
       // (i + 1) * accept_period - 1, so the accepts run while the light pass
       // streams (a separate accept grid only starts with the fill's last wave).
@@ -2556,7 +2559,7 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
   // words, counts and argmax partials must be visible to it, so the fence
   // precedes the (bulk) logits stores below.
   bool last = false;
-  if (TAIL != kTailNone || F.publish_arrival) {
+  if (FusedTail(TAIL) || F.publish_arrival) {
     __syncthreads();
     if (tid == 0) {
       const int need = F.accept_ctas > 0
@@ -2589,8 +2592,10 @@ __global__ void PRE3_FILL_BOUNDS FillKernel(AutView A, VocabView Vv, CacheView C
   }
   if (tid == 0 && seg == 0) atomicAdd(Bt.counters + 2, 1ull);
   if (tid == 0) TraceEvent(Bt, kTraceHeavy, b, seg, t_in, n_walks);
-  if (TAIL != kTailNone && last && warp == 0) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
-  if constexpr (PRE3_SPLIT_ONE_GRID && MODE == kFillMask && TAIL == kTailNone) {
+  if constexpr (FusedTail(TAIL)) {
+    if (last && warp == 0) SequenceTail<TAIL>(A, Vv, Cc, Bt, F, b, lane);
+  }
+  if constexpr (TAIL == kTailSplit) {
     if (F.accept_ctas > 0 && last && warp == 0) AcceptSeq<kSampleStream>(A, Vv, Cc, Bt, F.acc, b, lane);
   }
 }
@@ -3617,6 +3622,10 @@ cudaError_t LaunchFill(int mode, int tail, const AutView& a, const VocabView& v,
     }
   } else if (tail == kTailStream) {
     LaunchFillT<kFillMask, kTailStream>(a, v, c, b, f, dyn, s);
+  } else if (f.accept_ctas > 0) {
+    // The one-grid split step: its own instantiation, so the accept code
+    // (and its register pressure) stays out of the plain fill.
+    LaunchFillT<kFillMask, kTailSplit>(a, v, c, b, f, dyn, s);
   } else {
     LaunchFillT<kFillMask, kTailNone>(a, v, c, b, f, dyn, s);
   }

@@ -165,7 +165,9 @@ enum TraceKind { kTraceLight = 1, kTraceHeavy = 2, kTraceTail = 3, kTraceAccept 
 #endif
 
 enum FillMode { kFillMask = 0, kFillGreedy = 1 };
-enum FillTail { kTailNone = 0, kTailStream = 1, kTailGreedy = 2 };
+enum FillTail { kTailNone = 0, kTailStream = 1, kTailGreedy = 2, kTailSplit = 3 };  // kTailSplit: the one-grid split step
+// The fill's last item of a sequence runs sample + accept (the one-launch steps).
+__host__ __device__ constexpr bool FusedTail(int tail) { return tail == kTailStream || tail == kTailGreedy; }
 enum SampleMode { kSampleGiven = 0, kSampleStream = 1, kSampleGreedy = 2 };
 
 struct AcceptArgs {

@@ -7,7 +7,7 @@ cd "$(dirname "$0")/.."
 NAME=$1; shift
 D=build/var_$NAME; mkdir -p $D
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -lineinfo -Xcompiler -fPIC -Iinclude -Ipaper_2506_03887_b200/csrc $*"
-$NV -Xptxas -v -c paper_2506_03887_b200/csrc/kernels.cu -o $D/kernels.o 2> $D/ptxas.txt &
+$NV -Xptxas -v -c ${KSRC:-paper_2506_03887_b200/csrc/kernels.cu} -o $D/kernels.o 2> $D/ptxas.txt &
 $NV -c paper_2506_03887_b200/csrc/capi.cu -o $D/capi.o &
 $NV -c paper_2506_03887_b200/csrc/workload_dev.cu -o $D/workload_dev.o &
 wait
