@@ -316,7 +316,8 @@ int gm_graph_destroy(gm_graph* g);
 /* Measurement hook (diagnostics): the next fill kernel launched for this
  * batch, by any call, is bracketed by cudaEventRecord(start_event) and
  * cudaEventRecord(end_event) on its stream (cudaEvent_t handles; one-shot).
- * In an overlapped step the following kernel then cannot start under it. */
+ * In an overlapped step the following kernel then cannot start under it; a
+ * one-grid split step's fill kernel includes its sample/accept CTAs. */
 int gm_batch_time_next_fill(gm_batch* b, void* start_event, void* end_event);
 
 /* Statistics accumulated while enabled (gm_batch_set_stats), reset on read:
