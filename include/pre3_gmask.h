@@ -235,9 +235,10 @@ int gm_decode_step_stream_split(gm_batch* b, uint32_t* bitmask, int64_t ld_words
                                 void* stream);
 /* Kernel launches of one gm_decode_step_stream_split of this batch in the
  * steady state: 1 when the accepts run as CTAs of the fill's grid
- * (interleaved with its light CTAs; batches of at most ~16 light CTAs per SM,
- * B x segments <= 128 x SMs), else 2 (the fill + a programmatically dependent
- * accept kernel); -GM_ERR_USAGE for a NULL batch. */
+ * (interleaved with its light CTAs; the default), 2 for the fill + a
+ * programmatically dependent accept kernel (environment
+ * PRE3_SPLIT_TWO_KERNELS=1 when the batch was created); -GM_ERR_USAGE for a
+ * NULL batch. */
 int gm_batch_split_step_launches(gm_batch* b);
 
 /* Engine::AllowedTerminals (runtime.cpp:188-208) for every sequence: the

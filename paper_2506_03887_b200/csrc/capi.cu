@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <cstdlib>
 #include <thread>
 #include <unordered_set>
 #include <string_view>
@@ -187,15 +188,14 @@ struct gm_batch {
     return prod;
   }
   int sms = 148;  // the device's SM count
-  // Split step in one grid (the accepts as CTAs among the fill's light CTAs)
-  // when the light CTAs (8 items each) are at most 16 per SM, about four
-  // waves: measured +9-11% steps/s at 256 and 1,024 sequences (the PDL accept
-  // grid only starts with the fill's last wave); at 4,096 sequences (14
-  // waves) the accept kernel after the fill is 1% faster — it starts late
-  // relative to a long fill, and merged accepts of context-dependent
-  // sequences would hold CTA slots while their items are walked.
+  bool split_two_kernels = false;  // PRE3_SPLIT_TWO_KERNELS=1 at batch creation (tests, A/B)
+  // Split step in one grid (the accepts as CTAs among the fill's light
+  // CTAs): measured faster at 256, 1,024 and 4,096 sequences (+9 %, +11 %,
+  // +3 %; the PDL accept grid only starts with the fill's last wave).  The
+  // fill + accept kernel form stays for PRE3_SPLIT_TWO_KERNELS and batches
+  // past PRE3_ONE_GRID_CTAS_PER_SM light CTAs per SM (default: no limit).
   bool OneGridSplit() const {
-    return PRE3_SPLIT_ONE_GRID &&
+    return PRE3_SPLIT_ONE_GRID && !split_two_kernels &&
            static_cast<int64_t>(view.B) * engine->nseg <= static_cast<int64_t>(8) * PRE3_ONE_GRID_CTAS_PER_SM * sms;
   }
   cudaStream_t capture_stream = nullptr;  // graph capture (the legacy stream cannot capture)
@@ -641,6 +641,7 @@ int gm_batch_create(gm_engine* e, int32_t batch, int32_t stack_capacity, gm_batc
     v.build_grid = sms * 4;
     v.h_grid = std::min(v.h_cap, PRE3_HEAVY_PER_SM * sms);
     b->sms = sms;
+    if (const char* two = std::getenv("PRE3_SPLIT_TWO_KERNELS")) b->split_two_kernels = std::atoi(two) != 0;
     b->seg_counts = DevAlloc<int32_t>(bn * 2, &b->owned);
     b->scratch_mask = DevAlloc<uint32_t>(static_cast<size_t>(batch) * static_cast<size_t>(e->W), &b->owned);
     b->best = DevAlloc<unsigned long long>(static_cast<size_t>(batch), &b->owned);

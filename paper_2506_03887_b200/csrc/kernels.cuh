@@ -158,7 +158,7 @@ struct BatchView {
 enum TraceKind { kTraceLight = 1, kTraceHeavy = 2, kTraceTail = 3, kTraceAccept = 4 };
 
 #ifndef PRE3_ONE_GRID_CTAS_PER_SM
-#define PRE3_ONE_GRID_CTAS_PER_SM 16  // one-grid split step up to this many light CTAs per SM
+#define PRE3_ONE_GRID_CTAS_PER_SM (1 << 20)  // one-grid split step up to this many light CTAs per SM (no limit)
 #endif
 #ifndef PRE3_SPLIT_ONE_GRID
 #define PRE3_SPLIT_ONE_GRID 1  // split step: the accepts as CTAs of the fill's grid (0: a PDL accept kernel)

@@ -195,10 +195,19 @@ def refill(B=16, K=2):
         batch.check()
 
 
+def split_two_grid(B=64, steps=6):
+    """The split step as fill + accept kernel (PRE3_SPLIT_TWO_KERNELS)."""
+    os.environ["PRE3_SPLIT_TWO_KERNELS"] = "1"
+    try:
+        stream("split", B=B, steps=steps)
+    finally:
+        del os.environ["PRE3_SPLIT_TWO_KERNELS"]
+
+
 PARTS = {
     "two_call": lambda: stream("two_call"),
     "split": lambda: stream("split"),
-    "split_two_grid": lambda: stream("split", B=6400, steps=2),  # past the one-grid limit (B x 3 segments > 128 x SMs)
+    "split_two_grid": split_two_grid,
     "one_launch": lambda: stream("one_launch"),
     "tiny_table": lambda: stream("split", slots=4),
     "parents": lambda: stream("split", parent=3, K=12),

@@ -477,13 +477,16 @@ def test_allowed_terminals_matches_port(vectors, name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("grammar,flavor,K,B", [("json", 0, 16, 1024), ("schema", 0, 16, 1024), ("json", 0, 16, 1536)])
-def test_split_step_large_batch(grammar, flavor, K, B):
+@pytest.mark.parametrize("grammar,flavor,K,B,two", [("json", 0, 16, 1024, False), ("schema", 0, 16, 1024, False),
+                                                   ("json", 0, 16, 1536, False), ("json", 0, 16, 1536, True)])
+def test_split_step_large_batch(grammar, flavor, K, B, two, monkeypatch):
     """gm_decode_step_stream_split at a batch that fills several waves (the
     accepts overlap the fill and pure-CI sequences sample from the context
-    cache; 1,024 sequences: accept CTAs inside the fill's grid, 1,536: the
-    separate accept kernel): tokens, masks and stacks equal the two-call
+    cache; accept CTAs inside the fill's grid, or — PRE3_SPLIT_TWO_KERNELS —
+    the separate accept kernel): tokens, masks and stacks equal the two-call
     loop's, and the first 48 sequences' tokens equal the C port's."""
+    if two:
+        monkeypatch.setenv("PRE3_SPLIT_TWO_KERNELS", "1")
     if grammar == "json":
         f = flat("json")
     else:
@@ -493,8 +496,7 @@ def test_split_step_large_batch(grammar, flavor, K, B):
     eng = pk.DeviceEngine(pk.Automaton.load(f), vocab, context_depth=K)
     eng.prewarm(512, 200, seed=0xC0FFEE)
     steps, seed = 8, 13
-    sms = torch.cuda.get_device_properties(0).multi_processor_count
-    assert eng.batch(B).split_step_launches == (1 if B * eng.info()["num_segments"] <= 128 * sms else 2)
+    assert eng.batch(B).split_step_launches == (2 if two else 1)
     b1, m1, t1 = run_stream(eng, B, steps, seed, fused="split", check_logits=True)
     b2, m2, t2 = run_stream(eng, B, steps, seed)
     assert np.array_equal(t1, t2)
