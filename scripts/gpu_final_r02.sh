@@ -12,8 +12,8 @@ for c in 3 2 4 5; do timeout 900 python bench.py --config $c > $F/bench_c$c.json
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $F/bench_ref_c3.json 2> $F/bench_ref_c3.err; echo "ref rc=$?"
 bash scripts/gpu_prof_r02.sh "3 2 5 4" > $F/prof.log 2>&1; echo "prof rc=$?"
 P=gpurun_out/prof
-# The separate accept kernel runs at config 4 (configs 2/3 carry the accepts in the fill's grid).
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:AcceptKernel -s 45 -c 1 -o $P/c4_accept -f \
+# The separate accept kernel: the split step's two-kernel form at config 4 (the default carries the accepts in the fill's grid).
+PRE3_SPLIT_TWO_KERNELS=1 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:AcceptKernel -s 45 -c 1 -o $P/c4_accept -f \
   python bench.py --config 4 --prewarm-steps 2000 --prewarm-batch 1024 --no-e2e --no-cpu-baseline --cold-steps 0 --no-graph \
   --latency-samples 10 --fill-samples 10 --steps 10 --warmup 40 > $P/c4_accept.log 2>&1; echo "accept rc=$?"
 bash scripts/gpu_prof_sample.sh > /dev/null 2>&1; echo "sample prof rc=$?"
